@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the world step (BASELINE.json metric: agent-steps/s and grid cell-updates/s
+per world step, % of the B200 HBM roofline) on the paper-scale world (configs[1]).
+
+One bench "step" is one world step: regrowth, observation, per-agent LSTM + argmax,
+movement/consumption/physiology, death/reproduction/mutation (all of SURVEY.md §8(a)).
+
+Our arm (default):
+  * creates the configs[1] world (200x400, 8192 slots, 1000 agents, 7x7x2 obs, Hd 32,
+    seed 1; under torchrun rank r runs an independent replica with seed 1 + r, weak
+    scaling, no data-path collective), runs W warm-up steps, then times EXACTLY K steps
+    through sim_step (one CUDA graph per step), each bracketed by CUDA events on the
+    library's stream, with a 256 MiB memset flushing L2 between timed steps;
+  * replays the same K steps from a snapshot through sim_step_timed (events around every
+    kernel) for the per-kernel breakdown and the roofline of the dominant kernel;
+  * e2e: the same K steps through the public API from pinned HOST buffers: sim_set_state
+    (H2D of the whole state) + per step sim_step + sim_get_step_log (D2H of the step's
+    record), wall clock;
+  * cpu_baseline: the oracle (oracle/, single thread) on a bounded sample of the same
+    workload from the same start state.
+--impl reference: the oracle as the reference arm (no GPU code on that path).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "agent-steps/s (paper-scale world step)"
+UNIT = "agent-steps/s"
+FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "tiny", "large_world", "ensemble"))
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--ref-budget-s", type=float, default=120.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+def workload(name: str, rank: int) -> workloads.WorldConfig:
+    if name == "paper_scale":
+        wc = workloads.paper_scale()
+        return wc.replace(seeds=(wc.seeds[0] + rank,))
+    if name == "tiny":
+        return workloads.tiny().replace(seeds=(rank,))
+    if name == "large_world":
+        return workloads.large_world().replace(seeds=(3 + rank,))
+    return workloads.ensemble()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(self.REASONS, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- bytes model
+def policy_bytes(wc, agents: int, nnz: int) -> int:
+    """Algorithmic bytes of the policy kernel: the W_ih
+    columns of active inputs, W_hh, b, W_out, b_out, h and c read+written, 32 B of SoA
+    fields and claims per agent."""
+    Hd = wc.hidden
+    per_agent_fixed = 4 * (4 * Hd * Hd + 4 * Hd + 5 * Hd + 5) + 16 * Hd + 32
+    return 4 * 4 * Hd * nnz + agents * per_agent_fixed
+
+
+def step_bytes(wc, agents: int, nnz: int, births: int) -> int:
+    """Whole-step algorithmic bytes: policy bytes + the R and O bit planes read and written
+    (H*W/2 B) + 8P per birth (parent read, child written)."""
+    return policy_bytes(wc, agents, nnz) + wc.rows * wc.cols // 2 + births * 8 * wc.n_params
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(args, rank, world_size, local_rank):
+    import torch
+    from paper_2302_09334_b200 import sim
+
+    dist = None
+    if world_size > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    wc = workload(args.config, rank)
+    K, W = args.steps, args.warmup
+    stream = torch.cuda.Stream(device=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def allmax(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    with torch.cuda.stream(stream):
+        world = sim.World(wc, device=local_rank, stream=stream, log_capacity=max(4096, W + K + 8))
+        flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+        world.step(W)
+        world.synchronize()
+        need_snap = not (args.no_replay and args.no_e2e and args.no_cpu_baseline)
+        snap = world.get_state() if need_snap else None
+        t0 = world.t
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        clocks = ClockSampler(local_rank)
+        clocks.start()
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush.zero_()
+            evs[k][0].record(stream)
+            world.step(1)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks.stop()
+        world.synchronize()
+        step_ms = np.array([a.elapsed_time(b) for a, b in evs], np.float64)
+        total_ms = float(step_ms.sum())
+        log = world.step_log(t0, K)
+        agents = int(log["agents_at_start"].sum())
+        nnz = int(log["obs_nnz"].sum())
+        births = int(log["births"].sum())
+        max_ms = allmax(total_ms)
+        all_agents = allsum(agents)
+        value = all_agents / (max_ms / 1e3)
+        cells = K * wc.rows * wc.cols * wc.n_worlds
+
+        # -- replay of the same K steps with per-kernel events
+        kern = None
+        if not args.no_replay:
+            world.set_state(snap)
+            ksum = np.zeros(sim.NUM_KERNELS)
+            ssum = 0.0
+            for k in range(K):
+                flush.zero_()
+                tm = world.step_timed()
+                ksum += np.array([tm[n] for n in sim.KERNEL_NAMES])
+                ssum += tm["step_ms"]
+            log2 = world.step_log(t0, K)
+            replay_identical = bool(np.array_equal(log2, log))
+            kern = {"kernel_ms_total": dict(zip(sim.KERNEL_NAMES, ksum.tolist())), "step_ms_total": ssum,
+                    "replay_identical": replay_identical}
+
+        # -- e2e through the public API from pinned host buffers
+        e2e = None
+        if not args.no_e2e:
+            pinned = {}
+            h2d = 0
+            for k_, v in snap.items():
+                if isinstance(v, np.ndarray):
+                    tt = torch.empty(v.shape, dtype=getattr(torch, str(v.dtype)), pin_memory=True)
+                    tt.numpy()[...] = v
+                    pinned[k_] = tt.numpy()
+                    h2d += v.nbytes
+                else:
+                    pinned[k_] = v
+            rec_bytes = sim.RECORD_DTYPE.itemsize * wc.n_worlds
+            torch.cuda.synchronize()
+            barrier()
+            te = time.perf_counter()
+            world.set_state(pinned)
+            for k in range(K):
+                world.step(1)
+                world.step_log(t0 + k, 1)
+            world.synchronize()
+            e_s = time.perf_counter() - te
+            e_s = allmax(e_s)
+            e2e = {"value": all_agents / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
+                   "d2h_bytes_per_step": rec_bytes, "seconds": e_s}
+        world.destroy()
+
+    result = None
+    if rank == 0:
+        peak, peak_src = peaks()
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": K, "warmup": W,
+            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{wc.name} (BASELINE.json configs[1])" if args.config == "paper_scale" else wc.name,
+                       "grid": f"{wc.rows}x{wc.cols}", "slots": wc.slots, "n_initial": wc.n_initial,
+                       "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x2", "hidden": wc.hidden,
+                       "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + K],
+                       "l2": "flushed between timed steps (256 MiB memset on the library stream)",
+                       "parallelism": "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
+                       else "single GPU", "global_batch": wc.slots * world_size},
+            "cell_updates_per_s": cells * world_size / (max_ms / 1e3),
+            "agents_mean": agents / K,
+            "gpu_launches": sim.NUM_KERNELS * K,
+            "clocks": clk,
+        }
+        if kern is not None:
+            ks = kern["kernel_ms_total"]
+            pb = policy_bytes(wc, agents, nnz)
+            pol_s = ks["policy"] / 1e3
+            achieved = pb / pol_s / 1e9
+            sb = step_bytes(wc, agents, nnz, births)
+            result["roofline"] = {
+                "kernel": "k_policy (observe + LSTM + argmax + move claim)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "bytes_per_launch": pb / K, "launch_ms": ks["policy"] / K, "peak_source": peak_src,
+                "share_of_step": ks["policy"] / kern["step_ms_total"],
+            }
+            result["step_roofline"] = {"bytes_per_step": sb / K, "achieved_GBps": sb / (max_ms / 1e3) / 1e9,
+                                       "frac": sb / (max_ms / 1e3) / 1e9 / peak,
+                                       "dense_equiv_GBps": step_bytes(wc, agents, agents * wc.n_inputs, births)
+                                       / (max_ms / 1e3) / 1e9}
+            result["kernel_ms_per_step"] = {k: v / K for k, v in ks.items()}
+            result["replay_identical"] = kern["replay_identical"]
+        if e2e is not None:
+            result["e2e"] = e2e
+    return result, snap, wc
+
+
+# -------------------------------------------------------------- oracle (CPU) legs
+def oracle_rate(wc, start_state, budget_s, max_steps):
+    import oracle
+    w = oracle.OracleWorld(wc, state=start_state)
+    agents = 0
+    steps = 0
+    a0 = int(w.st["alive"].sum())
+    t0 = time.perf_counter()
+    while steps < max_steps and time.perf_counter() - t0 < budget_s:
+        agents += int(w.st["alive"].sum())
+        w.step()
+        steps += 1
+    el = time.perf_counter() - t0
+    return agents / el, steps, el, a0, int(w.st["alive"].sum()), w.t
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    import oracle
+    wc = workload(args.config, 0)
+    w = oracle.OracleWorld(wc)
+    for _ in range(args.warmup):
+        w.step()
+    rate, steps, el, a0, a1, t1 = oracle_rate(wc, w.state(), args.ref_budget_s, args.steps)
+    sample = (f"oracle world steps t={args.warmup}..{t1} ({steps} of the {args.steps} requested steps, "
+              f"bounded to {args.ref_budget_s:.0f} s; agents {a0}->{a1}); rate metric, so comparable")
+    return {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": el / max(steps, 1) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{wc.name} (BASELINE.json configs[1])", "grid": f"{wc.rows}x{wc.cols}",
+                   "slots": wc.slots, "n_initial": wc.n_initial, "seed": int(wc.seeds[0])},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank)
+        if res is not None:
+            line = json.dumps(res)
+            print(line, flush=True)
+            if args.out:
+                open(args.out, "w").write(line + "\n")
+        return
+    res, snap, wc = run_ours(args, rank, world_size, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline and world_size == 1 and snap is not None:
+            w0 = {k: (v[0] if isinstance(v, np.ndarray) else v) for k, v in snap.items()}
+            rate, steps, el, a0, a1, t1 = oracle_rate(wc.replace(seeds=(wc.seeds[0],)), w0, args.cpu_budget_s,
+                                                      args.steps)
+            res["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{steps} oracle world steps from the timed region's start state (t={w0['t']}..{t1}, "
+                          f"agents {a0}->{a1}), {el:.1f} s on one host core",
+            }
+        line = json.dumps(res)
+        print(line, flush=True)
+        if args.out:
+            open(args.out, "w").write(line + "\n")
+    if world_size > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * include/sim.h — C ABI of the B200 world-step library (libsim.so), version 1.
+ *
+ * The library runs the per-timestep world step of the non-episodic neuroevolution
+ * simulator of arXiv 2302.09334 (Hamon, Nisioti, Moulin-Frier), App. B
+ * (PAPER.md:248-350), under the BASELINE.json configs, entirely in hand-written
+ * sm_100a CUDA kernels:
+ *   (a) resource regrowth  p(x,y) = p_I(x,y)*c(x) + c
+ *   (b) egocentric observation of every live agent
+ *   (c) per-agent LSTM policy + linear head, argmax action
+ *   (d) movement, consumption, energy/age physiology
+ *   (e) death and minimal-criterion reproduction with mutation
+ * Readings of silent/garbled passages (R1-R30) are listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Every function returns sim_status; none throws or aborts.  sim_last_error()
+ *    returns a thread-local message for the most recent failure on the calling thread.
+ *  - Ownership: the handle owns all device memory.  Caller buffers are read or written
+ *    during the call only and never retained.  `seeds` is copied at create.  The CUDA
+ *    stream in sim_config is borrowed and must outlive the handle.
+ *  - Any CUDA failure poisons the handle; later calls return SIM_E_STATE.
+ *  - sim_step is asynchronous on the handle's stream; sim_get_* synchronise.
+ *  - A non-finite LSTM value found on the device is reported as SIM_E_NONFINITE by the
+ *    next synchronising call (or the next sim_step).  Extinction is not an error.
+ *  - A handle is not thread-safe.  Distinct handles share nothing.
+ *  - There is no CPU fallback: without a usable CUDA device sim_create fails with
+ *    SIM_E_CUDA.  sim_validate / sim_param_count / sim_state_sizes are host-only.
+ */
+#ifndef ECO_SIM_H
+#define ECO_SIM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIM_ABI_VERSION 1u
+
+#if defined(__GNUC__)
+#define SIM_API __attribute__((visibility("default")))
+#else
+#define SIM_API
+#endif
+
+typedef struct sim_ctx *sim_handle; /* opaque */
+
+typedef enum {
+    SIM_OK = 0,
+    SIM_E_INVALID = -1,   /* a config field or argument is invalid; message names it   */
+    SIM_E_CUDA = -2,      /* CUDA runtime failure (handle poisoned)                      */
+    SIM_E_OOM = -3,       /* device allocation failed                                    */
+    SIM_E_NCCL = -4,      /* reserved for the banded multi-GPU mode                      */
+    SIM_E_NONFINITE = -5, /* a non-finite h', c' or logit was produced */
+    SIM_E_STATE = -6      /* the handle is poisoned by an earlier failure                */
+} sim_status;
+
+/* World parameters.  Field meanings follow PAPER.md App. B.4 (lines 311-338) under the
+ * BASELINE.json constants.  Energies are int32 milli-units (R16). */
+typedef struct {
+    uint32_t abi_version;   /* = SIM_ABI_VERSION                                       */
+    uint32_t struct_size;   /* = sizeof(sim_config)                                     */
+    int32_t rows, cols;     /* H (latitude axis, row 0 = top), W; W % 4 == 0             */
+    int32_t n_worlds;       /* >= 1 independent worlds batched on the device             */
+    int32_t device;         /* CUDA device ordinal                                       */
+    const uint64_t *seeds;  /* [n_worlds] Philox keys; copied at create                  */
+    double init_resource_p; /* Bernoulli rho of the initial resources                   */
+    int32_t regrow_r2;      /* squared Euclidean radius of the count disc, 1..8 (4 = 12 cells) */
+    int32_t f_class_min_k[4]; /* class c iff k >= f_class_min_k[c]; [0] = 0, ascending */
+    double f_value[4];      /* f(class): {0, .01, .05, .1}                               */
+    double lat_top, lat_bottom; /* climate lat(0), lat(H-1), linear in y/(H-1)         */
+    double spontaneous;     /* constant spontaneous growth probability c                */
+    int32_t slots, n_initial; /* S agent slots (population cap), N0 initial agents       */
+    int32_t obs_radius;     /* r: window (2r+1)^2, 0..3                                   */
+    int32_t hidden;         /* LSTM hidden size Hd in {4, 8, 16, 32}                      */
+    int32_t n_actions;      /* must be 5 (stay, N, S, E, W)                               */
+    int32_t log_capacity;   /* step records kept per world (ring); 0 -> 4096              */
+    double init_weight_std, mutation_std; /* standard deviations (R23)                   */
+    int32_t e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max; /* milli-units;
+                                                e_max = INT32_MAX means no clip          */
+    int32_t repr_steps, max_age;
+    void *cuda_stream;      /* borrowed cudaStream_t; NULL -> library-owned stream       */
+} sim_config;
+
+/* Canonical state, host buffers owned by the caller, layouts with the world index
+ * outermost.  For sim_get_state a NULL field is skipped; for sim_set_state a NULL field
+ * keeps the device value.  Dead slots: only `alive` is meaningful.
+ *   weights: per slot P floats in canonical order W_ih[4Hd][I] (gate blocks i,f,g,o,
+ *   row-major), W_hh[4Hd][Hd], b[4Hd], W_out[5][Hd], b_out[5];
+ *   P = 4Hd*I + 4Hd*Hd + 4Hd + 5Hd + 5 with I = 2(2r+1)^2. */
+typedef struct {
+    int64_t t;             /* steps taken; all worlds share t                              */
+    uint8_t *resources;    /* [n_worlds][H][W] 0/1                                         */
+    uint8_t *alive;        /* [n_worlds][S]                                                */
+    int32_t *cell;         /* [n_worlds][S] y*W + x                                        */
+    int32_t *energy;       /* [n_worlds][S] milli-units                                    */
+    int32_t *age;          /* [n_worlds][S]                                                */
+    int32_t *repr;         /* [n_worlds][S] consecutive steps with energy > e_repr_gt      */
+    uint8_t *last_action;  /* [n_worlds][S] 0 stay, 1 N, 2 S, 3 E, 4 W                     */
+    uint8_t *ate;          /* [n_worlds][S]                                                */
+    float *h;              /* [n_worlds][S][Hd]                                            */
+    float *c;              /* [n_worlds][S][Hd]                                            */
+    float *weights;        /* [n_worlds][S][P]                                             */
+    float *logits;         /* [n_worlds][S][5] of the last step                            */
+} sim_state;
+
+/* Per world, per step counters (integer, exact). */
+typedef struct {
+    int64_t t;                 /* step index described                                    */
+    int64_t agents_at_start;   /* live agents at step start (= agent-steps of this step)  */
+    int64_t grown, eaten, births;
+    int64_t deaths_energy, deaths_age;
+    int64_t deferred_no_cell;  /* eligible parent without an empty adjacent cell          */
+    int64_t deferred_claim;    /* lost the claim on its candidate cell                    */
+    int64_t deferred_capacity; /* won the cell but no free slot                           */
+    int64_t population;        /* after the step                                          */
+    int64_t resources;         /* after the step                                          */
+    int64_t near_ties;         /* live agents with top-1 minus top-2 logit margin < 1e-4  */
+    int64_t obs_nnz;           /* sum over live agents of active (= 1) observation inputs:
+                                  the W_ih columns the policy kernel must read            */
+} sim_step_record;
+
+/* Cumulative counters since create (or the last set_state), summed over worlds. */
+typedef struct {
+    int64_t steps;
+    int64_t agent_steps;
+    int64_t cell_updates;
+    int64_t births, deaths, eaten, grown;
+} sim_totals;
+
+/* Sizes a caller needs to allocate sim_state buffers (elements, per world). */
+typedef struct {
+    int64_t cells;   /* H*W                */
+    int64_t slots;   /* S                  */
+    int32_t hidden;  /* Hd                 */
+    int32_t inputs;  /* I                  */
+    int32_t params;  /* P                  */
+    int32_t n_actions;
+    int64_t device_bytes; /* device memory the handle will allocate */
+} sim_state_sizes_t;
+
+/* Per-kernel timing of one instrumented step (milliseconds, CUDA events). */
+#define SIM_NUM_KERNELS 6
+typedef struct {
+    float step_ms;                     /* first event to last event of the step */
+    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_rank, mutate */
+} sim_step_timing;
+
+/* --- lifecycle ------------------------------------------------------------------- */
+/* Validate cfg, allocate device state and initialise every world (C.2: Bernoulli
+ * resources, N0 agents on the N0 smallest (draw, cell) empty cells, N(0, std^2)
+ * weights).  n_initial > number of empty cells -> SIM_E_INVALID. */
+SIM_API sim_status sim_create(const sim_config *cfg, sim_handle *out);
+/* Enqueue n >= 0 world steps on the stream (one CUDA graph launch per step). */
+SIM_API sim_status sim_step(sim_handle h, int64_t n);
+/* Synchronise, convert to the canonical layout and copy into caller buffers. */
+SIM_API sim_status sim_get_state(sim_handle h, sim_state *out);
+/* Replace state (resume / inject): host buffers -> device; rebuilds occupancy and lists.
+ * Rejects out-of-range cells and non-exclusive occupancy (SIM_E_INVALID). */
+SIM_API sim_status sim_set_state(sim_handle h, const sim_state *in);
+/* NULL-safe; frees everything. */
+SIM_API sim_status sim_destroy(sim_handle h);
+SIM_API const char *sim_last_error(void);
+
+/* --- host-only helpers (no device needed) ------------------------------------------ */
+SIM_API sim_status sim_validate(const sim_config *cfg);
+SIM_API sim_status sim_state_sizes(const sim_config *cfg, sim_state_sizes_t *out);
+
+/* --- test and measurement hooks ------------------------------------------------------ */
+/* act: [n_worlds][S], 255 = use the policy; NULL clears.  The policy still runs (h, c,
+ * logits update); only the move uses the forced action.  Applies to every later step. */
+SIM_API sim_status sim_set_forced_actions(sim_handle h, const uint8_t *act);
+/* Records of steps [first, first+n) for all worlds, out[n][n_worlds]; the steps must be
+ * among the last log_capacity steps taken. */
+SIM_API sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_record *out);
+SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
+/* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
+SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
+/* Synchronise the handle's stream (reports deferred errors). */
+SIM_API sim_status sim_synchronize(sim_handle h);
+/* Number of kernel launches one step performs (for the bench's launch count). */
+SIM_API int32_t sim_kernels_per_step(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

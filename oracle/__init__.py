@@ -116,7 +116,7 @@ def lib():
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]
             L.orc_init.argtypes = [cp, ctypes.POINTER(State)]
-            L.orc_step.argtypes = [cp, ctypes.POINTER(State), ctypes.c_void_p, ctypes.POINTER(Record)]
+            L.orc_step.argtypes = [cp, ctypes.POINTER(State), ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Record)]
             _lib = L
     return _lib
 
@@ -271,17 +271,23 @@ class OracleWorld:
     def t(self) -> int:
         return int(self.st["t"])
 
-    def step(self, forced: np.ndarray | None = None) -> dict:
+    def step(self, forced: np.ndarray | None = None, return_actions: bool = False) -> dict:
+        """One oracle step.  With return_actions, d["actions"] holds the action every slot
+        alive at step start used (255 elsewhere)."""
         rec = Record()
         ref = self._bind()
         fp = None
         if forced is not None:
             forced = np.ascontiguousarray(forced, np.uint8)
             fp = _ptr(forced)
-        rc = lib().orc_step(ctypes.byref(self.cfg), ref, fp, ctypes.byref(rec))
+        acts = np.full(self.wc.slots, 255, np.uint8) if return_actions else None
+        rc = lib().orc_step(ctypes.byref(self.cfg), ref, fp, _ptr(acts) if return_actions else None,
+                            ctypes.byref(rec))
         self.st["t"] = int(self._cst.t)
         d = rec.as_dict()
         d["status"] = int(rc)
+        if return_actions:
+            d["actions"] = acts
         return d
 
     def state(self) -> dict:

@@ -333,7 +333,8 @@ int orc_init(const orc_config *cfg, orc_state *st) {
 static const int32_t DY[5] = {0, -1, 1, 0, 0};
 static const int32_t DX[5] = {0, 0, 0, 1, -1};
 
-int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, orc_record *rec) {
+int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_t *actions_out,
+             orc_record *rec) {
     int32_t H = cfg->rows, W = cfg->cols, S = cfg->slots, Hd = cfg->hidden;
     int32_t P = orc_param_count(cfg), I = orc_input_count(cfg), A = cfg->n_actions;
     int64_t HW = (int64_t)H * W;
@@ -377,6 +378,8 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, orc_re
         action[i] = a;
         st->last_action[i] = (uint8_t)a;
     }
+    if (actions_out)
+        for (int32_t i = 0; i < S; ++i) actions_out[i] = st->alive[i] ? (uint8_t)action[i] : 255;
 
     /* 4. MOVE: exclusive occupancy, claim by max key (R14), blocked at the edge (R15) */
     for (int32_t i = 0; i < S; ++i) {

@@ -118,8 +118,12 @@ int orc_policy(const orc_config *cfg, const float *w, const double *x, const flo
 
 /* initial world (C.2) */
 int orc_init(const orc_config *cfg, orc_state *st);
-/* one full world step (C.3); forced: [S] action per slot, 255 = policy; NULL = none */
-int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, orc_record *rec);
+/* one full world step (C.3); forced: [S] action per slot, 255 = policy; NULL = none.
+ * actions_out (test hook, may be NULL): [S] the action each slot alive at step start
+ * used this step (255 for slots not alive at step start) — recorded before births can
+ * reuse a slot freed by a death in the same step. */
+int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_t *actions_out,
+             orc_record *rec);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,653 @@
+// api.cu — the C ABI of include/sim.h: validation, device allocation, initialisation,
+// the per-step CUDA graph, state import/export and the test/measurement hooks.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sim_internal.cuh"
+
+using eco::DevParams;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sim_status fail(sim_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+// host copy of the validated configuration plus derived sizes
+struct Derived {
+    int H, W, WW, S, Hd, I, P, Pd, n_worlds, log_cap;
+    int off_hh, off_b, off_out, off_bout;
+    size_t pw;  // words per plane per world
+};
+
+sim_status validate_cfg(const sim_config *cfg, Derived *d) {
+    if (!cfg) return fail(SIM_E_INVALID, "invalid field: cfg (NULL)");
+    if (cfg->abi_version != SIM_ABI_VERSION) return fail(SIM_E_INVALID, "invalid field: abi_version");
+    if (cfg->struct_size != sizeof(sim_config)) return fail(SIM_E_INVALID, "invalid field: struct_size");
+    if (cfg->rows < 2) return fail(SIM_E_INVALID, "invalid field: rows (need >= 2)");
+    if (cfg->cols < 4 || cfg->cols % 4 != 0) return fail(SIM_E_INVALID, "invalid field: cols (need >= 4, multiple of 4)");
+    if ((int64_t)cfg->rows * cfg->cols >= (int64_t)1 << 31) return fail(SIM_E_INVALID, "invalid field: rows*cols");
+    if (cfg->n_worlds < 1) return fail(SIM_E_INVALID, "invalid field: n_worlds");
+    if (!cfg->seeds) return fail(SIM_E_INVALID, "invalid field: seeds (NULL)");
+    auto prob = [](double v) { return v >= 0.0 && v <= 1.0; };
+    if (!prob(cfg->init_resource_p)) return fail(SIM_E_INVALID, "invalid field: init_resource_p");
+    if (cfg->regrow_r2 < 1 || cfg->regrow_r2 > 8) return fail(SIM_E_INVALID, "invalid field: regrow_r2 (1..8)");
+    if (cfg->f_class_min_k[0] != 0) return fail(SIM_E_INVALID, "invalid field: f_class_min_k");
+    for (int c = 1; c < 4; ++c)
+        if (cfg->f_class_min_k[c] < cfg->f_class_min_k[c - 1]) return fail(SIM_E_INVALID, "invalid field: f_class_min_k");
+    for (int c = 0; c < 4; ++c)
+        if (!prob(cfg->f_value[c])) return fail(SIM_E_INVALID, "invalid field: f_value");
+    if (!prob(cfg->lat_top) || !prob(cfg->lat_bottom)) return fail(SIM_E_INVALID, "invalid field: lat");
+    if (!prob(cfg->spontaneous)) return fail(SIM_E_INVALID, "invalid field: spontaneous");
+    if (cfg->slots < 0) return fail(SIM_E_INVALID, "invalid field: slots");
+    if (cfg->n_initial < 0 || cfg->n_initial > cfg->slots) return fail(SIM_E_INVALID, "invalid field: n_initial");
+    if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return fail(SIM_E_INVALID, "invalid field: obs_radius (0..3)");
+    if (!(cfg->hidden == 4 || cfg->hidden == 8 || cfg->hidden == 16 || cfg->hidden == 32))
+        return fail(SIM_E_INVALID, "invalid field: hidden (4, 8, 16 or 32)");
+    if (cfg->n_actions != 5) return fail(SIM_E_INVALID, "invalid field: n_actions (must be 5)");
+    if (!(cfg->init_weight_std >= 0.0) || !std::isfinite(cfg->init_weight_std))
+        return fail(SIM_E_INVALID, "invalid field: init_weight_std");
+    if (!(cfg->mutation_std >= 0.0) || !std::isfinite(cfg->mutation_std))
+        return fail(SIM_E_INVALID, "invalid field: mutation_std");
+    if (cfg->repr_steps < 1) return fail(SIM_E_INVALID, "invalid field: repr_steps");
+    if (cfg->max_age < 0) return fail(SIM_E_INVALID, "invalid field: max_age");
+    if (cfg->log_capacity < 0 || cfg->log_capacity == 1) return fail(SIM_E_INVALID, "invalid field: log_capacity");
+    if (d) {
+        d->H = cfg->rows;
+        d->W = cfg->cols;
+        d->WW = (((cfg->cols + 31) / 32) + 3) / 4 * 4;
+        d->S = cfg->slots;
+        d->Hd = cfg->hidden;
+        const int wd = 2 * cfg->obs_radius + 1;
+        d->I = 2 * wd * wd;
+        d->P = 4 * d->Hd * d->I + 4 * d->Hd * d->Hd + 4 * d->Hd + 5 * d->Hd + 5;
+        d->off_hh = d->I * d->Hd * 4;
+        d->off_b = d->off_hh + d->Hd * d->Hd * 4;
+        d->off_out = d->off_b + d->Hd * 4;
+        d->off_bout = d->off_out + 5 * d->Hd;
+        d->Pd = (d->off_bout + 5 + 31) / 32 * 32;
+        d->n_worlds = cfg->n_worlds;
+        d->log_cap = cfg->log_capacity ? cfg->log_capacity : 4096;
+        d->pw = (size_t)d->H * d->WW;
+    }
+    return SIM_OK;
+}
+
+// Bernoulli thresholds T[y][c] = min(floor((lat(y) f_c + c_spont) 2^32), 2^32-1) with the
+// linear climate lat(y) = lat_top + (lat_bottom - lat_top) * (y / (H-1)) (R3, R8).
+void threshold_table(const sim_config *cfg, std::vector<uint32_t> &T) {
+    T.assign((size_t)cfg->rows * 4, 0u);
+    for (int y = 0; y < cfg->rows; ++y) {
+        const double frac = (double)y / (double)(cfg->rows - 1);
+        const double lat = cfg->lat_top + (cfg->lat_bottom - cfg->lat_top) * frac;
+        for (int c = 0; c < 4; ++c) {
+            const double pr = lat * cfg->f_value[c] + cfg->spontaneous;
+            const double s = std::floor(pr * 4294967296.0);
+            T[(size_t)y * 4 + c] = s >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)s;
+        }
+    }
+}
+
+size_t device_bytes(const Derived &d) {
+    const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
+    size_t b = 0;
+    b += nw * d.pw * 4 * 4;                 // plane0, plane1, occ, bbits
+    b += nw * d.pw * 4;                     // bprefix
+    b += nw * HW * 8 * 2;                   // claim, bclaim
+    b += nw * S * (1 * 4 + 4 * 4);          // u8 x4, i32 x4
+    b += nw * S * (size_t)d.Hd * 4 * 2;     // h, c
+    b += nw * S * eco::LOGIT_STRIDE * 4;    // logits
+    b += nw * S * (size_t)d.Pd * 4;         // weights
+    b += nw * S * (4 + 8 + 4 + 8);          // target, mkey, bcand, bkey
+    b += nw * S * 4 * 5;                    // alive, cand, free, birth lists
+    b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
+    return b;
+}
+
+}  // namespace
+
+struct sim_ctx {
+    Derived d{};
+    sim_config cfg{};
+    std::vector<uint64_t> seeds;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    DevParams p{};
+    eco::LaunchCfg lc{};
+    bool poisoned = false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    int64_t t = 0;
+    int32_t *nonfinite_host = nullptr;
+    int32_t *forced_on_dev = nullptr;
+    uint8_t *forced_dev = nullptr;
+    std::vector<void *> allocs;
+    cudaEvent_t ev[SIM_NUM_KERNELS + 1] = {};
+};
+
+namespace {
+
+sim_status cuda_fail(sim_ctx *h, cudaError_t e, const char *what) {
+    if (h) h->poisoned = true;
+    if (e == cudaErrorMemoryAllocation) return fail(SIM_E_OOM, "%s: %s", what, cudaGetErrorString(e));
+    return fail(SIM_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(h, expr, what)                                    \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(sim_ctx *h, T **ptr, size_t count) {
+    *ptr = nullptr;
+    if (count == 0) count = 1;
+    void *v = nullptr;
+    cudaError_t e = cudaMalloc(&v, count * sizeof(T));
+    if (e != cudaSuccess) return e;
+    h->allocs.push_back(v);
+    *ptr = static_cast<T *>(v);
+    return cudaMemsetAsync(v, 0, count * sizeof(T), h->stream);
+}
+
+sim_status check_handle(sim_ctx *h) {
+    if (!h) return fail(SIM_E_INVALID, "invalid argument: NULL handle");
+    if (h->poisoned) return fail(SIM_E_STATE, "handle poisoned by an earlier failure");
+    return SIM_OK;
+}
+
+sim_status check_nonfinite(sim_ctx *h) {
+    if (h->nonfinite_host && *reinterpret_cast<volatile int32_t *>(h->nonfinite_host)) {
+        *reinterpret_cast<volatile int32_t *>(h->nonfinite_host) = 0;
+        return fail(SIM_E_NONFINITE, "non-finite LSTM state or logit produced on the device");
+    }
+    return SIM_OK;
+}
+
+cudaError_t enqueue_step(sim_ctx *h) {
+    cudaError_t e;
+    if ((e = eco::launch_regrow(h->p, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_policy(h->p, h->lc, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_move(h->p, h->lc, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_birth_claim(h->p, h->lc, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_birth_rank(h->p, h->stream)) != cudaSuccess) return e;
+    return eco::launch_mutate(h->p, h->lc, h->stream);
+}
+
+sim_status sync(sim_ctx *h) {
+    CK(h, cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    return check_nonfinite(h);
+}
+
+void destroy_all(sim_ctx *h) {
+    if (!h) return;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    for (auto &e : h->ev)
+        if (e) cudaEventDestroy(e);
+    for (void *v : h->allocs) cudaFree(v);
+    if (h->nonfinite_host) cudaFreeHost(h->nonfinite_host);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sim_last_error(void) { return g_last_error.c_str(); }
+
+int32_t sim_kernels_per_step(void) { return SIM_NUM_KERNELS; }
+
+sim_status sim_validate(const sim_config *cfg) { return validate_cfg(cfg, nullptr); }
+
+sim_status sim_state_sizes(const sim_config *cfg, sim_state_sizes_t *out) {
+    Derived d;
+    sim_status st = validate_cfg(cfg, &d);
+    if (st != SIM_OK) return st;
+    if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    out->cells = (int64_t)d.H * d.W;
+    out->slots = d.S;
+    out->hidden = d.Hd;
+    out->inputs = d.I;
+    out->params = d.P;
+    out->n_actions = 5;
+    out->device_bytes = (int64_t)device_bytes(d);
+    return SIM_OK;
+}
+
+sim_status sim_create(const sim_config *cfg, sim_handle *out) {
+    if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    *out = nullptr;
+    Derived d;
+    sim_status st = validate_cfg(cfg, &d);
+    if (st != SIM_OK) return st;
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+        return fail(SIM_E_CUDA, "no CUDA device available (the library has no CPU fallback)");
+    if (cfg->device < 0 || cfg->device >= n_dev) return fail(SIM_E_INVALID, "invalid field: device");
+    sim_ctx *h = new sim_ctx();
+    h->d = d;
+    h->cfg = *cfg;
+    h->seeds.assign(cfg->seeds, cfg->seeds + cfg->n_worlds);
+    h->cfg.seeds = nullptr;
+    h->device = cfg->device;
+    auto bail = [&](sim_status s) {
+        destroy_all(h);
+        return s;
+    };
+#define CKC(expr, what)                                              \
+    do {                                                             \
+        cudaError_t _e = (expr);                                     \
+        if (_e != cudaSuccess) return bail(cuda_fail(h, _e, what));  \
+    } while (0)
+    CKC(cudaSetDevice(h->device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    CKC(cudaGetDeviceProperties(&prop, h->device), "cudaGetDeviceProperties");
+    if (prop.major < 10) return bail(fail(SIM_E_CUDA, "device %s is sm_%d%d; libsim.so is built for sm_100a only", prop.name, prop.major, prop.minor));
+    if (cfg->cuda_stream) {
+        h->stream = static_cast<cudaStream_t>(cfg->cuda_stream);
+    } else {
+        CKC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        h->own_stream = true;
+    }
+    for (auto &e : h->ev) CKC(cudaEventCreate(&e), "cudaEventCreate");
+    CKC(cudaHostAlloc(reinterpret_cast<void **>(&h->nonfinite_host), sizeof(int32_t), cudaHostAllocMapped),
+        "cudaHostAlloc");
+    *h->nonfinite_host = 0;
+
+    DevParams &p = h->p;
+    p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
+    p.n_worlds = d.n_worlds; p.r = cfg->obs_radius; p.log_cap = d.log_cap;
+    p.repr_steps = cfg->repr_steps; p.max_age = cfg->max_age;
+    p.e_init = cfg->e_init; p.e_decay = cfg->e_decay; p.e_gain = cfg->e_gain;
+    p.e_repr_gt = cfg->e_repr_gt; p.e_death_le = cfg->e_death_le; p.e_max = cfg->e_max;
+    p.cls_k1 = cfg->f_class_min_k[1]; p.cls_k2 = cfg->f_class_min_k[2]; p.cls_k3 = cfg->f_class_min_k[3];
+    p.n_off = 0;
+    for (int dy = -2; dy <= 2; ++dy)
+        for (int dx = -2; dx <= 2; ++dx)
+            if ((dy || dx) && dy * dy + dx * dx <= cfg->regrow_r2) {
+                p.off_dy[p.n_off] = dy;
+                p.off_dx[p.n_off] = dx;
+                ++p.n_off;
+            }
+    p.off_hh = d.off_hh; p.off_b = d.off_b; p.off_out = d.off_out; p.off_bout = d.off_bout;
+    p.mutation_std = cfg->mutation_std; p.init_weight_std = cfg->init_weight_std;
+    {
+        const double s = std::floor(cfg->init_resource_p * 4294967296.0);
+        p.init_res_thr = s >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)s;
+    }
+    const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
+    uint64_t *seeds_d;
+    uint32_t *T_d;
+    CKC(dalloc(h, &seeds_d, nw), "alloc");
+    CKC(dalloc(h, &p.t, nw), "alloc");
+    CKC(dalloc(h, &p.plane0, nw * d.pw), "alloc");
+    CKC(dalloc(h, &p.plane1, nw * d.pw), "alloc");
+    CKC(dalloc(h, &p.occ, nw * d.pw), "alloc");
+    CKC(dalloc(h, &p.bbits, nw * d.pw), "alloc");
+    CKC(dalloc(h, &p.bprefix, nw * d.pw), "alloc");
+    CKC(dalloc(h, &T_d, (size_t)d.H * 4), "alloc");
+    CKC(dalloc(h, &p.claim, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.bclaim, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.alive, nw * S), "alloc");
+    CKC(dalloc(h, &p.last_action, nw * S), "alloc");
+    CKC(dalloc(h, &p.ate, nw * S), "alloc");
+    CKC(dalloc(h, &p.bwin, nw * S), "alloc");
+    CKC(dalloc(h, &p.cell, nw * S), "alloc");
+    CKC(dalloc(h, &p.energy, nw * S), "alloc");
+    CKC(dalloc(h, &p.age, nw * S), "alloc");
+    CKC(dalloc(h, &p.repr, nw * S), "alloc");
+    CKC(dalloc(h, &p.h, nw * S * d.Hd), "alloc");
+    CKC(dalloc(h, &p.c, nw * S * d.Hd), "alloc");
+    CKC(dalloc(h, &p.logits, nw * S * eco::LOGIT_STRIDE), "alloc");
+    CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
+    CKC(dalloc(h, &p.target, nw * S), "alloc");
+    CKC(dalloc(h, &p.mkey, nw * S), "alloc");
+    CKC(dalloc(h, &p.bcand, nw * S), "alloc");
+    CKC(dalloc(h, &p.bkey, nw * S), "alloc");
+    CKC(dalloc(h, &p.alive_list, nw * S), "alloc");
+    CKC(dalloc(h, &p.n_alive, nw), "alloc");
+    CKC(dalloc(h, &p.cand_list, nw * S), "alloc");
+    CKC(dalloc(h, &p.n_cand, nw), "alloc");
+    CKC(dalloc(h, &p.free_list, nw * S), "alloc");
+    CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
+    CKC(dalloc(h, &p.birth_parent, nw * S), "alloc");
+    CKC(dalloc(h, &p.n_births, nw), "alloc");
+    CKC(dalloc(h, &p.res_count, nw), "alloc");
+    CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");
+    CKC(dalloc(h, &p.totals, 8), "alloc");
+    CKC(dalloc(h, &h->forced_dev, nw * S), "alloc");
+    CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
+    p.seeds = seeds_d;
+    p.T = T_d;
+    p.forced = h->forced_dev;
+    p.forced_on = h->forced_on_dev;
+    int32_t *nf_dev = nullptr;
+    CKC(cudaHostGetDevicePointer(reinterpret_cast<void **>(&nf_dev), h->nonfinite_host, 0), "cudaHostGetDevicePointer");
+    p.nonfinite = nf_dev;
+    std::vector<uint32_t> T;
+    threshold_table(cfg, T);
+    CKC(cudaMemcpyAsync(T_d, T.data(), T.size() * 4, cudaMemcpyHostToDevice, h->stream), "upload T");
+    CKC(cudaMemcpyAsync(seeds_d, h->seeds.data(), nw * 8, cudaMemcpyHostToDevice, h->stream), "upload seeds");
+    if (S) CKC(cudaMemsetAsync(p.target, 0xff, nw * S * 4, h->stream), "memset");
+
+    // launch configuration: persistent-style grids sized to the 148 SMs
+    int bps = 0;
+    CKC(eco::policy_occupancy(d.Hd, 256, &bps), "occupancy");
+    if (bps < 1) bps = 1;
+    h->lc.policy_threads = 256;
+    h->lc.policy_blocks = prop.multiProcessorCount * bps;
+    h->lc.agent_threads = 256;
+    {
+        const long need = ((long)nw * S + 255) / 256;
+        const long cap = (long)prop.multiProcessorCount * 8;
+        h->lc.agent_blocks = (int)(need < 1 ? 1 : need < cap ? need : cap);
+    }
+    h->lc.mutate_blocks_y = 32;
+
+    // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
+    CKC(eco::launch_init_resources(p, h->stream), "init resources");
+    CKC(eco::launch_rebuild(p, h->stream), "rebuild");
+    std::vector<int64_t> res(nw);
+    CKC(cudaMemcpyAsync(res.data(), p.res_count, nw * 8, cudaMemcpyDeviceToHost, h->stream), "download");
+    CKC(cudaStreamSynchronize(h->stream), "sync");
+    for (size_t w = 0; w < nw; ++w)
+        if ((int64_t)HW - res[w] < cfg->n_initial)
+            return bail(fail(SIM_E_INVALID, "invalid field: n_initial (%d > %lld empty cells in world %zu)",
+                             cfg->n_initial, (long long)((int64_t)HW - res[w]), w));
+    if (S) {
+        const size_t sb = eco::init_agents_scratch_bytes(p);
+        void *scratch = nullptr;
+        CKC(cudaMalloc(&scratch, sb), "alloc scratch");
+        cudaError_t e = eco::launch_init_agents(p, cfg->n_initial, h->stream, scratch, sb);
+        cudaError_t e2 = cudaStreamSynchronize(h->stream);
+        cudaFree(scratch);
+        CKC(e, "init agents");
+        CKC(e2, "init agents sync");
+    }
+    CKC(eco::launch_rebuild(p, h->stream), "rebuild");
+    CKC(cudaStreamSynchronize(h->stream), "sync");
+#undef CKC
+    *out = h;
+    return SIM_OK;
+}
+
+sim_status sim_destroy(sim_handle h) {
+    if (!h) return SIM_OK;
+    cudaSetDevice(h->device);
+    destroy_all(h);
+    return SIM_OK;
+}
+
+sim_status sim_step(sim_handle h, int64_t n) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (n < 0) return fail(SIM_E_INVALID, "invalid argument: n < 0");
+    if ((st = check_nonfinite(h)) != SIM_OK) return st;
+    if (n == 0) return SIM_OK;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (!h->graph_exec) {
+        CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        cudaError_t e = enqueue_step(h);
+        cudaGraph_t g = nullptr;
+        cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
+        CK(h, e, "capture step");
+        CK(h, e2, "end capture");
+        h->graph = g;
+        CK(h, cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
+    }
+    for (int64_t i = 0; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
+    h->t += n;
+    return SIM_OK;
+}
+
+sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
+    CK(h, eco::launch_regrow(h->p, h->stream), "regrow");
+    CK(h, cudaEventRecord(h->ev[1], h->stream), "event");
+    CK(h, eco::launch_policy(h->p, h->lc, h->stream), "policy");
+    CK(h, cudaEventRecord(h->ev[2], h->stream), "event");
+    CK(h, eco::launch_move(h->p, h->lc, h->stream), "move");
+    CK(h, cudaEventRecord(h->ev[3], h->stream), "event");
+    CK(h, eco::launch_birth_claim(h->p, h->lc, h->stream), "birth claim");
+    CK(h, cudaEventRecord(h->ev[4], h->stream), "event");
+    CK(h, eco::launch_birth_rank(h->p, h->stream), "birth rank");
+    CK(h, cudaEventRecord(h->ev[5], h->stream), "event");
+    CK(h, eco::launch_mutate(h->p, h->lc, h->stream), "mutate");
+    CK(h, cudaEventRecord(h->ev[6], h->stream), "event");
+    CK(h, cudaEventSynchronize(h->ev[6]), "event sync");
+    h->t += 1;
+    for (int k = 0; k < SIM_NUM_KERNELS; ++k)
+        CK(h, cudaEventElapsedTime(&out->kernel_ms[k], h->ev[k], h->ev[k + 1]), "elapsed");
+    CK(h, cudaEventElapsedTime(&out->step_ms, h->ev[0], h->ev[SIM_NUM_KERNELS]), "elapsed");
+    return check_nonfinite(h);
+}
+
+sim_status sim_synchronize(sim_handle h) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    return sync(h);
+}
+
+sim_status sim_get_state(sim_handle h, sim_state *out) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    const Derived &d = h->d;
+    const DevParams &p = h->p;
+    const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
+    cudaStream_t s = h->stream;
+    out->t = h->t;
+    if (out->resources) {
+        uint8_t *tmp;
+        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), nw * HW, s), "alloc");
+        cudaError_t e = eco::launch_unpack_resources(p, tmp, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out->resources, tmp, nw * HW, cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(tmp, s);
+        CK(h, e, "resources");
+    }
+    auto get = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
+        if (!dst || !bytes) return cudaSuccess;
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+    };
+    CK(h, get(out->alive, p.alive, nw * S), "alive");
+    CK(h, get(out->cell, p.cell, nw * S * 4), "cell");
+    CK(h, get(out->energy, p.energy, nw * S * 4), "energy");
+    CK(h, get(out->age, p.age, nw * S * 4), "age");
+    CK(h, get(out->repr, p.repr, nw * S * 4), "repr");
+    CK(h, get(out->last_action, p.last_action, nw * S), "last_action");
+    CK(h, get(out->ate, p.ate, nw * S), "ate");
+    CK(h, get(out->h, p.h, nw * S * d.Hd * 4), "h");
+    CK(h, get(out->c, p.c, nw * S * d.Hd * 4), "c");
+    if (out->logits && S)
+        CK(h, cudaMemcpy2DAsync(out->logits, 5 * 4, p.logits, eco::LOGIT_STRIDE * 4, 5 * 4, nw * S,
+                                cudaMemcpyDeviceToHost, s), "logits");
+    if (out->weights && S) {
+        const size_t total_agents = nw * S;
+        const size_t chunk = ((size_t)1 << 26) / (size_t)d.P > 0 ? ((size_t)1 << 26) / (size_t)d.P : 1;
+        float *tmp;
+        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), chunk * d.P * 4, s), "alloc");
+        cudaError_t e = cudaSuccess;
+        for (size_t a0 = 0; a0 < total_agents && e == cudaSuccess; a0 += chunk) {
+            const size_t n = (total_agents - a0) < chunk ? total_agents - a0 : chunk;
+            e = eco::launch_weights_to_canon(p, tmp, a0, n, s);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(out->weights + a0 * d.P, tmp, n * d.P * 4, cudaMemcpyDeviceToHost, s);
+        }
+        cudaFreeAsync(tmp, s);
+        CK(h, e, "weights");
+    }
+    return sync(h);
+}
+
+sim_status sim_set_state(sim_handle h, const sim_state *in) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!in) return fail(SIM_E_INVALID, "invalid argument: in (NULL)");
+    if (in->t < 0 || in->t >= ((int64_t)1 << 32)) return fail(SIM_E_INVALID, "invalid field: t");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    const Derived &d = h->d;
+    DevParams &p = h->p;
+    const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
+    cudaStream_t s = h->stream;
+    // host-side validation on the merged view (device values where a field is NULL)
+    if (S) {
+        std::vector<uint8_t> alive(nw * S);
+        std::vector<int32_t> cell(nw * S);
+        if (in->alive) memcpy(alive.data(), in->alive, nw * S);
+        else CK(h, cudaMemcpy(alive.data(), p.alive, nw * S, cudaMemcpyDeviceToHost), "download");
+        if (in->cell) memcpy(cell.data(), in->cell, nw * S * 4);
+        else CK(h, cudaMemcpy(cell.data(), p.cell, nw * S * 4, cudaMemcpyDeviceToHost), "download");
+        std::vector<uint8_t> seen(HW);
+        for (size_t w = 0; w < nw; ++w) {
+            std::fill(seen.begin(), seen.end(), 0);
+            for (size_t i = 0; i < S; ++i) {
+                if (!alive[w * S + i]) continue;
+                const int32_t c = cell[w * S + i];
+                if (c < 0 || (size_t)c >= HW) return fail(SIM_E_INVALID, "invalid field: cell (out of range, world %zu slot %zu)", w, i);
+                if (seen[c]) return fail(SIM_E_INVALID, "invalid field: cell (two agents on cell %d, world %zu)", c, w);
+                seen[c] = 1;
+            }
+        }
+        if (in->weights) {
+            const size_t n = nw * S * (size_t)d.P;
+            for (size_t k = 0; k < n; ++k)
+                if (!std::isfinite(in->weights[k])) return fail(SIM_E_INVALID, "invalid field: weights (non-finite)");
+        }
+    }
+    if (!in->resources && ((in->t ^ h->t) & 1)) {
+        // the current resource plane is selected by step parity: carry it over
+        uint32_t *from = (h->t & 1) ? p.plane1 : p.plane0;
+        uint32_t *to = (in->t & 1) ? p.plane1 : p.plane0;
+        CK(h, cudaMemcpyAsync(to, from, nw * d.pw * 4, cudaMemcpyDeviceToDevice, s), "plane");
+    }
+    std::vector<int64_t> tv(nw, in->t);
+    CK(h, cudaMemcpyAsync(p.t, tv.data(), nw * 8, cudaMemcpyHostToDevice, s), "t");
+    h->t = in->t;
+    if (in->resources) {
+        uint8_t *tmp;
+        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), nw * HW, s), "alloc");
+        cudaError_t e = cudaMemcpyAsync(tmp, in->resources, nw * HW, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = eco::launch_pack_resources(p, tmp, s);
+        cudaFreeAsync(tmp, s);
+        CK(h, e, "resources");
+    }
+    auto put = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
+        if (!src || !bytes) return cudaSuccess;
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    };
+    CK(h, put(p.alive, in->alive, nw * S), "alive");
+    CK(h, put(p.cell, in->cell, nw * S * 4), "cell");
+    CK(h, put(p.energy, in->energy, nw * S * 4), "energy");
+    CK(h, put(p.age, in->age, nw * S * 4), "age");
+    CK(h, put(p.repr, in->repr, nw * S * 4), "repr");
+    CK(h, put(p.last_action, in->last_action, nw * S), "last_action");
+    CK(h, put(p.ate, in->ate, nw * S), "ate");
+    CK(h, put(p.h, in->h, nw * S * d.Hd * 4), "h");
+    CK(h, put(p.c, in->c, nw * S * d.Hd * 4), "c");
+    if (in->logits && S)
+        CK(h, cudaMemcpy2DAsync(p.logits, eco::LOGIT_STRIDE * 4, in->logits, 5 * 4, 5 * 4, nw * S,
+                                cudaMemcpyHostToDevice, s), "logits");
+    if (in->weights && S) {
+        const size_t total_agents = nw * S;
+        const size_t chunk = ((size_t)1 << 26) / (size_t)d.P > 0 ? ((size_t)1 << 26) / (size_t)d.P : 1;
+        float *tmp;
+        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), chunk * d.P * 4, s), "alloc");
+        cudaError_t e = cudaSuccess;
+        for (size_t a0 = 0; a0 < total_agents && e == cudaSuccess; a0 += chunk) {
+            const size_t n = (total_agents - a0) < chunk ? total_agents - a0 : chunk;
+            e = cudaMemcpyAsync(tmp, in->weights + a0 * d.P, n * d.P * 4, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = eco::launch_weights_to_device(p, tmp, a0, n, s);
+        }
+        cudaFreeAsync(tmp, s);
+        CK(h, e, "weights");
+    }
+    // scratch and derived structures
+    if (S) {
+        CK(h, cudaMemsetAsync(p.claim, 0, nw * HW * 8, s), "memset");
+        CK(h, cudaMemsetAsync(p.bclaim, 0, nw * HW * 8, s), "memset");
+    }
+    CK(h, cudaMemsetAsync(p.bbits, 0, nw * d.pw * 4, s), "memset");
+    CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
+    CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
+    CK(h, eco::launch_rebuild(p, s), "rebuild");
+    return sync(h);
+}
+
+sim_status sim_set_forced_actions(sim_handle h, const uint8_t *act) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    const size_t n = (size_t)h->d.n_worlds * h->d.S;
+    int32_t on = act ? 1 : 0;
+    if (act) {
+        for (size_t i = 0; i < n; ++i)
+            if (act[i] > 4 && act[i] != 255) return fail(SIM_E_INVALID, "invalid argument: act (values 0..4 or 255)");
+        if (n) CK(h, cudaMemcpyAsync(h->forced_dev, act, n, cudaMemcpyHostToDevice, h->stream), "forced");
+    }
+    CK(h, cudaMemcpyAsync(h->forced_on_dev, &on, 4, cudaMemcpyHostToDevice, h->stream), "forced flag");
+    CK(h, cudaStreamSynchronize(h->stream), "sync");
+    return SIM_OK;
+}
+
+sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_record *out) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (n < 0 || (n > 0 && !out)) return fail(SIM_E_INVALID, "invalid argument: n/out");
+    if (first < 0 || first + n > h->t || first < h->t - (h->d.log_cap - 1))
+        return fail(SIM_E_INVALID, "invalid argument: steps [%lld, %lld) not in the log (t = %lld, capacity %d)",
+                    (long long)first, (long long)(first + n), (long long)h->t, h->d.log_cap);
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    const size_t nw = h->d.n_worlds;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t step = first + i;
+        CK(h, cudaMemcpyAsync(out + i * nw, h->p.log + (size_t)(step % h->d.log_cap) * nw, nw * sizeof(sim_step_record),
+                              cudaMemcpyDeviceToHost, h->stream), "log");
+    }
+    return sync(h);
+}
+
+sim_status sim_get_totals(sim_handle h, sim_totals *out) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    unsigned long long v[8];
+    CK(h, cudaMemcpyAsync(v, h->p.totals, sizeof v, cudaMemcpyDeviceToHost, h->stream), "totals");
+    if ((st = sync(h)) != SIM_OK) return st;
+    out->steps = (int64_t)v[0];
+    out->agent_steps = (int64_t)v[1];
+    out->cell_updates = (int64_t)v[2];
+    out->births = (int64_t)v[3];
+    out->deaths = (int64_t)v[4];
+    out->eaten = (int64_t)v[5];
+    out->grown = (int64_t)v[6];
+    return SIM_OK;
+}
+
+}  // extern "C"

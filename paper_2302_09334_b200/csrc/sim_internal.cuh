@@ -1,0 +1,189 @@
+// sim_internal.cuh — device-side layout and helpers of libsim.so (sm_100a).
+//
+// Device layout:
+//  * resource plane R and occupancy plane O: one bit per cell, rows padded to WW 32-bit
+//    words (WW = ceil(W/32) rounded up to a multiple of 4 words = 16 B); bit b of word
+//    (y, wx) is column 32*wx + b; padding bits are always 0.  R is double-buffered by
+//    step parity: plane[t&1] = R_t, plane[(t+1)&1] = R' (post-regrowth) which becomes
+//    R_{t+1} after consumption.
+//  * agents: structure of arrays [world][slot]; weights [world][slot][Pd] in the
+//    GEMV-friendly order W_ih^T[I][Hd][4], W_hh^T[Hd][Hd][4], b[Hd][4], W_out[5][Hd],
+//    b_out[5], padded to Pd (multiple of 32 floats = 128 B).  Lane k of an agent's lane
+//    group reads its unit's four gate weights (i,f,g,o) with one 16-B load.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sim.h"
+
+namespace eco {
+
+constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
+                   PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7;
+constexpr int MAX_OFFSETS = 24;
+constexpr int LOGIT_STRIDE = 8;
+
+// Everything a kernel needs, passed by value (fixed for the handle's lifetime, so one
+// captured CUDA graph serves every step; the step index lives in device memory).
+struct DevParams {
+    int H, W, WW, S, Hd, I, P, Pd, n_worlds, r, log_cap;
+    int repr_steps, max_age;
+    int e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max;
+    int cls_k1, cls_k2, cls_k3;  // class thresholds f_class_min_k[1..3]
+    int n_off;
+    int off_dy[MAX_OFFSETS], off_dx[MAX_OFFSETS];
+    int off_hh, off_b, off_out, off_bout;  // offsets inside one agent's device weights
+    double mutation_std, init_weight_std;
+    uint32_t init_res_thr;
+    const uint64_t *seeds;    // [n_worlds]
+    int64_t *t;               // [n_worlds] step index (all equal)
+    uint32_t *plane0, *plane1;// R double buffer [n_worlds][H][WW]
+    uint32_t *occ;            // O [n_worlds][H][WW]
+    uint32_t *bbits;          // birth bitmap [n_worlds][H][WW]
+    uint32_t *bprefix;        // exclusive prefix counts of bbits words [n_worlds][H*WW]
+    const uint32_t *T;        // [H][4] Bernoulli thresholds
+    unsigned long long *claim;   // [n_worlds][H*W] move claims (0 = none)
+    unsigned long long *bclaim;  // [n_worlds][H*W] birth claims
+    uint8_t *alive, *last_action, *ate, *bwin;
+    int32_t *cell, *energy, *age, *repr;
+    float *h, *c, *logits, *weights;
+    int32_t *target;             // [n_worlds][S] move target of this step or -1
+    unsigned long long *mkey;    // [n_worlds][S]
+    int32_t *bcand;              // [n_worlds][S] birth candidate cell or -1
+    unsigned long long *bkey;    // [n_worlds][S]
+    int32_t *alive_list, *n_alive;   // [n_worlds][S], [n_worlds]
+    int32_t *cand_list, *n_cand;     // eligible parents with a candidate cell
+    int32_t *free_list;              // [n_worlds][S] scratch
+    int32_t *birth_child, *birth_parent, *n_births;
+    int64_t *res_count;              // [n_worlds] resources at step start
+    sim_step_record *log;            // [log_cap][n_worlds]
+    unsigned long long *totals;      // [7] sim_totals order
+    const uint8_t *forced;           // [n_worlds][S]
+    const int32_t *forced_on;        // device flag
+    int32_t *nonfinite;              // host-mapped flag
+};
+
+// ------------------------------------------------------------------ Philox4x32-10
+// Salmon et al. SC'11.  Counter (c0 = sub, c1 = entity, c2 = step, c3 = purpose),
+// key (seed lo, seed hi) — the RNG contract of DESIGN.md §3 (C.1).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint4 draw4(uint64_t seed, uint32_t purpose, uint32_t step, uint32_t entity,
+                                       uint32_t sub) {
+    return philox4x32_10(make_uint4(sub, entity, step, purpose), (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+__device__ __forceinline__ uint32_t word_of(uint4 v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// fp64 Box-Muller of one word pair; products explicitly rounded (no contraction).
+__device__ __forceinline__ void box_muller(uint32_t wa, uint32_t wb, double &za, double &zb) {
+    const double two_m32 = 2.3283064365386963e-10;
+    const double u1 = __dmul_rn(__dadd_rn((double)wa, 1.0), two_m32);
+    const double u2 = __dmul_rn((double)wb, two_m32);
+    const double rad = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+    const double th = __dmul_rn(6.283185307179586, u2);
+    za = __dmul_rn(rad, cos(th));
+    zb = __dmul_rn(rad, sin(th));
+}
+
+// canonical weight index j -> device index (see the layout note above)
+__device__ __forceinline__ int canon_to_dev(int j, int I, int Hd, int off_hh, int off_b, int off_out,
+                                            int off_bout) {
+    const int G = 4 * Hd;
+    if (j < G * I) {
+        const int r = j / I, col = j - r * I;
+        const int g = r / Hd, k = r - g * Hd;
+        return (col * Hd + k) * 4 + g;
+    }
+    j -= G * I;
+    if (j < G * Hd) {
+        const int r = j / Hd, col = j - r * Hd;
+        const int g = r / Hd, k = r - g * Hd;
+        return off_hh + (col * Hd + k) * 4 + g;
+    }
+    j -= G * Hd;
+    if (j < G) {
+        const int g = j / Hd, k = j - g * Hd;
+        return off_b + k * 4 + g;
+    }
+    j -= G;
+    if (j < 5 * Hd) return off_out + j;
+    j -= 5 * Hd;
+    return off_bout + j;
+}
+
+// ------------------------------------------------------------------- bit planes
+__device__ __forceinline__ size_t plane_words(const DevParams &p) { return (size_t)p.H * p.WW; }
+
+__device__ __forceinline__ uint32_t get_bit(const uint32_t *plane, const DevParams &p, int cell) {
+    const int y = cell / p.W, x = cell - y * p.W;
+    return (plane[(size_t)y * p.WW + (x >> 5)] >> (x & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t *word_ptr(uint32_t *plane, const DevParams &p, int cell, uint32_t &bit) {
+    const int y = cell / p.W, x = cell - y * p.W;
+    bit = 1u << (x & 31);
+    return plane + (size_t)y * p.WW + (x >> 5);
+}
+
+// n (<= 31) bits of row `row` starting at column x0 (may be negative / past the row);
+// out-of-row bits read 0.
+__device__ __forceinline__ uint32_t row_bits(const uint32_t *row, int WW, int x0, int n) {
+    const int w0 = x0 >> 5;  // arithmetic shift: floor division
+    const int b0 = x0 & 31;
+    const uint32_t lo = (w0 >= 0 && w0 < WW) ? __ldg(row + w0) : 0u;
+    const uint32_t hi = (w0 + 1 >= 0 && w0 + 1 < WW) ? __ldg(row + w0 + 1) : 0u;
+    return __funnelshift_r(lo, hi, b0) & ((1u << n) - 1u);
+}
+
+__device__ __forceinline__ uint32_t *plane_cur(const DevParams &p, int64_t t) {
+    return (t & 1) ? p.plane1 : p.plane0;
+}
+__device__ __forceinline__ uint32_t *plane_next(const DevParams &p, int64_t t) {
+    return (t & 1) ? p.plane0 : p.plane1;
+}
+
+__device__ __forceinline__ sim_step_record *record_of(const DevParams &p, int64_t t, int w) {
+    return p.log + (size_t)(t % p.log_cap) * p.n_worlds + w;
+}
+
+// ----------------------------------------------------------------- host launchers
+struct LaunchCfg {
+    int policy_blocks, policy_threads;
+    int agent_blocks, agent_threads;
+    int mutate_blocks_y;
+};
+
+cudaError_t launch_init_resources(const DevParams &p, cudaStream_t s);
+size_t init_agents_scratch_bytes(const DevParams &p);
+cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
+cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
+cudaError_t launch_regrow(const DevParams &p, cudaStream_t s);
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);
+cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
+
+// state conversion (canonical <-> device)
+cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);
+cudaError_t launch_unpack_resources(const DevParams &p, uint8_t *bytes, cudaStream_t s);
+cudaError_t launch_weights_to_device(const DevParams &p, const float *canon, size_t first_agent, size_t n_agents,
+                                     cudaStream_t s);
+cudaError_t launch_weights_to_canon(const DevParams &p, float *canon, size_t first_agent, size_t n_agents,
+                                    cudaStream_t s);
+
+}  // namespace eco

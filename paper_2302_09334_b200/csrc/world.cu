@@ -1,0 +1,351 @@
+// world.cu — grid-side kernels: K1 regrowth (step row a1), world initialisation, the
+// occupancy/list rebuild used by create and set_state, and resource-plane conversion.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "block_scan.cuh"
+#include "sim_internal.cuh"
+
+namespace eco {
+
+// --------------------------------------------------------------------------- K1 regrow
+// each empty cell grows with p = lat(y)*f(k) + c, k = resources in the
+// Euclidean radius-r disc (centre excluded) of the START-of-step grid (synchronous),
+// drawn as philox(REGROW, t, cell>>2)[cell&3] < T[y][class(k)].  Full cells stay full.
+//
+// One thread per 32-cell word.  The 12 (generally n_off <= 24) neighbour bit-vectors are
+// funnel-shifted words of rows y-2..y+2; k is accumulated bit-sliced (5 planes), so the
+// stencil costs ~10 LOP3/IADD per neighbour per 32 cells.  Philox runs only for 4-cell
+// groups holding an empty cell (exact: draws are keyed by cell, not by sequence).
+__device__ __forceinline__ uint32_t shifted_word(uint32_t prv, uint32_t cur, uint32_t nxt, int dx) {
+    // bit b of the result = bit (b + dx) of the row around word `cur`
+    if (dx > 0) return __funnelshift_r(cur, nxt, dx);
+    if (dx < 0) return __funnelshift_l(prv, cur, -dx);
+    return cur;
+}
+
+__device__ __forceinline__ uint32_t ge_const(const uint32_t c[5], int m) {
+    if (m <= 0) return 0xffffffffu;
+    if (m >= 32) return 0u;
+    uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+    for (int i = 4; i >= 0; --i) {
+        if ((m >> i) & 1) {
+            eq &= c[i];
+        } else {
+            gt |= eq & c[i];
+            eq &= ~c[i];
+        }
+    }
+    return gt | eq;
+}
+
+__global__ void __launch_bounds__(256) k_regrow(DevParams p) {
+    const int wx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int w = blockIdx.z;
+    const int real_words = (p.W + 31) >> 5;
+    const int64_t t = p.t[w];
+    uint32_t grow = 0u;
+    if (wx < real_words && y < p.H) {
+        const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
+        uint32_t *dst = plane_next(p, t) + (size_t)w * plane_words(p);
+        // 5 rows x 3 words around (y, wx)
+        uint32_t win[5][3];
+#pragma unroll
+        for (int dy = -2; dy <= 2; ++dy) {
+            const int yy = y + dy;
+#pragma unroll
+            for (int dw = -1; dw <= 1; ++dw) {
+                const int ww = wx + dw;
+                win[dy + 2][dw + 1] =
+                    (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? __ldg(src + (size_t)yy * p.WW + ww) : 0u;
+            }
+        }
+        const uint32_t cur = win[2][1];
+        uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
+        for (int o = 0; o < p.n_off; ++o) {
+            const int dy = p.off_dy[o], dx = p.off_dx[o];
+            uint32_t prv, cen, nxt;
+            // dy in [-2, 2] (validated r2 <= 8)
+            switch (dy) {
+                case -2: prv = win[0][0]; cen = win[0][1]; nxt = win[0][2]; break;
+                case -1: prv = win[1][0]; cen = win[1][1]; nxt = win[1][2]; break;
+                case 0: prv = win[2][0]; cen = win[2][1]; nxt = win[2][2]; break;
+                case 1: prv = win[3][0]; cen = win[3][1]; nxt = win[3][2]; break;
+                default: prv = win[4][0]; cen = win[4][1]; nxt = win[4][2]; break;
+            }
+            uint32_t cy = shifted_word(prv, cen, nxt, dx), tt;
+            tt = c[0] & cy; c[0] ^= cy; cy = tt;
+            tt = c[1] & cy; c[1] ^= cy; cy = tt;
+            tt = c[2] & cy; c[2] ^= cy; cy = tt;
+            tt = c[3] & cy; c[3] ^= cy; cy = tt;
+            c[4] ^= cy;
+        }
+        const uint32_t ge1 = ge_const(c, p.cls_k1), ge2 = ge_const(c, p.cls_k2), ge3 = ge_const(c, p.cls_k3);
+        const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
+        const uint64_t seed = p.seeds[w];
+        const int x_base = wx << 5;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const int x0 = x_base + 4 * g;
+            if (x0 >= p.W) break;
+            if (((cur >> (4 * g)) & 0xFu) == 0xFu) continue;  // all four cells full: no draw needed
+            const uint32_t entity = (uint32_t)(((int64_t)y * p.W + x0) >> 2);
+            const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)t, entity, 0u);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int b = 4 * g + m;
+                if ((cur >> b) & 1u) continue;
+                const int cls = (int)((ge1 >> b) & 1u) + (int)((ge2 >> b) & 1u) + (int)((ge3 >> b) & 1u);
+                const uint32_t thr = cls == 0 ? Trow.x : cls == 1 ? Trow.y : cls == 2 ? Trow.z : Trow.w;
+                if (word_of(d, m) < thr) grow |= 1u << b;
+            }
+        }
+        dst[(size_t)y * p.WW + wx] = cur | grow;
+    }
+    // grown count: warp reduce then one atomic per warp
+    unsigned cnt = __popc(grow);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        sim_step_record *rec = record_of(p, p.t[w], w);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&rec->grown), (unsigned long long)cnt);
+    }
+}
+
+cudaError_t launch_regrow(const DevParams &p, cudaStream_t s) {
+    const int real_words = (p.W + 31) >> 5;
+    dim3 block(real_words >= 32 ? 32 : 16, real_words >= 32 ? 8 : 16);
+    dim3 grid((real_words + block.x - 1) / block.x, (p.H + block.y - 1) / block.y, p.n_worlds);
+    k_regrow<<<grid, block, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K0 initialisation
+// R[cell] = philox(INIT_RES, 0, cell>>2)[cell&3] < floor(rho * 2^32)
+__global__ void k_init_resources(DevParams p) {
+    const int wx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int w = blockIdx.z;
+    if (wx >= p.WW) return;
+    uint32_t bits = 0u;
+    const int x_base = wx << 5;
+    for (int g = 0; g < 8; ++g) {
+        const int x0 = x_base + 4 * g;
+        if (x0 >= p.W) break;
+        const uint4 d = draw4(p.seeds[w], PURPOSE_INIT_RES, 0u, (uint32_t)(((int64_t)y * p.W + x0) >> 2), 0u);
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            if (word_of(d, m) < p.init_res_thr) bits |= 1u << (4 * g + m);
+    }
+    p.plane0[(size_t)w * plane_words(p) + (size_t)y * p.WW + wx] = bits;
+}
+
+// placement keys: (draw(INIT_PLACE, 0, cell) << 32 | cell) for empty cells, ~0 for full
+__global__ void k_place_keys(DevParams p, int w, unsigned long long *keys) {
+    const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t HW = (int64_t)p.H * p.W;
+    if (cell >= HW) return;
+    const uint32_t *R = p.plane0 + (size_t)w * plane_words(p);
+    unsigned long long k = ~0ull;
+    if (!get_bit(R, p, (int)cell)) {
+        const uint4 d = draw4(p.seeds[w], PURPOSE_INIT_PLACE, 0u, (uint32_t)(cell >> 2), 0u);
+        k = ((unsigned long long)word_of(d, (int)(cell & 3)) << 32) | (unsigned long long)(uint32_t)cell;
+    }
+    keys[cell] = k;
+}
+
+// slot i < N0 takes the i-th smallest key; everything else is dead
+__global__ void k_init_agents(DevParams p, int w, int n_initial, const unsigned long long *sorted) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.S) return;
+    const size_t gs = (size_t)w * p.S + i;
+    const bool live = i < n_initial;
+    p.alive[gs] = live ? 1 : 0;
+    p.cell[gs] = live ? (int32_t)(uint32_t)(sorted[i] & 0xffffffffull) : 0;
+    p.energy[gs] = live ? p.e_init : 0;
+    p.age[gs] = 0;
+    p.repr[gs] = 0;
+    p.last_action[gs] = 0;
+    p.ate[gs] = 0;
+    p.target[gs] = -1;
+    p.bcand[gs] = -1;
+}
+
+// initial weights w_j = (float)(std * z_j), z from INIT_W keyed by the initial cell
+__global__ void k_init_weights(DevParams p, int w, int n_initial) {
+    const int groups = (p.P + 3) >> 2;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = blockIdx.y; i < n_initial; i += gridDim.y) {
+        if (q >= groups) continue;
+        const size_t gs = (size_t)w * p.S + i;
+        const uint4 d = draw4(p.seeds[w], PURPOSE_INIT_W, 0u, (uint32_t)p.cell[gs], (uint32_t)q);
+        double z[4];
+        box_muller(d.x, d.y, z[0], z[1]);
+        box_muller(d.z, d.w, z[2], z[3]);
+        float *wd = p.weights + gs * (size_t)p.Pd;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int j = 4 * q + m;
+            if (j >= p.P) break;
+            wd[canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout)] =
+                __double2float_rn(__dmul_rn(p.init_weight_std, z[m]));
+        }
+    }
+}
+
+cudaError_t launch_init_resources(const DevParams &p, cudaStream_t s) {
+    dim3 g1((p.WW + 127) / 128, p.H, p.n_worlds);
+    k_init_resources<<<g1, 128, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+size_t init_agents_scratch_bytes(const DevParams &p) {
+    const int64_t HW = (int64_t)p.H * p.W;
+    size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                   (int)HW, 0, 64);
+    return 2 * sizeof(unsigned long long) * (size_t)HW + need + 256;
+}
+
+cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch,
+                               size_t scratch_bytes) {
+    if (p.S == 0) return cudaSuccess;
+    const int64_t HW = (int64_t)p.H * p.W;
+    unsigned long long *keys_in = static_cast<unsigned long long *>(scratch);
+    unsigned long long *keys_out = keys_in + HW;
+    void *tmp = keys_out + HW;
+    const size_t tmp_bytes = scratch_bytes - 2 * sizeof(unsigned long long) * (size_t)HW;
+    cudaError_t e;
+    for (int w = 0; w < p.n_worlds; ++w) {
+        k_place_keys<<<(unsigned)((HW + 255) / 256), 256, 0, s>>>(p, w, keys_in);
+        size_t need = 0;
+        e = cub::DeviceRadixSort::SortKeys(nullptr, need, keys_in, keys_out, (int)HW, 0, 64, s);
+        if (e != cudaSuccess) return e;
+        if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+        e = cub::DeviceRadixSort::SortKeys(tmp, need, keys_in, keys_out, (int)HW, 0, 64, s);
+        if (e != cudaSuccess) return e;
+        k_init_agents<<<(p.S + 255) / 256, 256, 0, s>>>(p, w, n_initial, keys_out);
+        if (n_initial > 0) {
+            const int groups = (p.P + 3) >> 2;
+            dim3 g((groups + 127) / 128, n_initial < 4096 ? n_initial : 4096);
+            k_init_weights<<<g, 128, 0, s>>>(p, w, n_initial);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// ------------------------------------------------------- rebuild (create / set_state)
+// One CTA per world: O from (alive, cell); ascending alive list; resource count.
+__global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
+    __shared__ uint32_t scratch[33];
+    __shared__ unsigned long long res_acc;
+    const int w = blockIdx.x;
+    uint32_t *O = p.occ + (size_t)w * plane_words(p);
+    const uint32_t *R = plane_cur(p, p.t[w]) + (size_t)w * plane_words(p);
+    if (threadIdx.x == 0) res_acc = 0ull;
+    unsigned long long local = 0ull;
+    for (size_t i = threadIdx.x; i < plane_words(p); i += blockDim.x) {
+        O[i] = 0u;
+        local += __popc(R[i]);
+    }
+    atomicAdd(&res_acc, local);
+    __syncthreads();
+    uint32_t base = 0u;
+    for (int i0 = 0; i0 < p.S; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const size_t gs = (size_t)w * p.S + i;
+        const uint32_t a = (i < p.S && p.alive[gs]) ? 1u : 0u;
+        if (a) {
+            uint32_t bit;
+            uint32_t *wp = word_ptr(O, p, p.cell[gs], bit);
+            atomicOr(wp, bit);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan<1024>(a, scratch, tot);
+        if (a) p.alive_list[(size_t)w * p.S + base + ex] = i;
+        if (i < p.S) {
+            p.target[gs] = -1;
+            p.bcand[gs] = -1;
+        }
+        base += tot;
+    }
+    if (threadIdx.x == 0) {
+        p.n_alive[w] = (int32_t)base;
+        p.n_cand[w] = 0;
+        p.n_births[w] = 0;
+        p.res_count[w] = (int64_t)res_acc;
+    }
+}
+
+cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s) {
+    k_rebuild<<<p.n_worlds, 1024, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- plane <-> bytes
+__global__ void k_pack_resources(DevParams p, const uint8_t *bytes) {
+    const int wx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y, w = blockIdx.z;
+    if (wx >= p.WW) return;
+    uint32_t bits = 0u;
+    for (int b = 0; b < 32; ++b) {
+        const int x = (wx << 5) + b;
+        if (x < p.W && bytes[((size_t)w * p.H + y) * p.W + x]) bits |= 1u << b;
+    }
+    uint32_t *R = plane_cur(p, p.t[w]) + (size_t)w * plane_words(p);
+    R[(size_t)y * p.WW + wx] = bits;
+}
+
+__global__ void k_unpack_resources(DevParams p, uint8_t *bytes) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y, w = blockIdx.z;
+    if (x >= p.W) return;
+    const uint32_t *R = plane_cur(p, p.t[w]) + (size_t)w * plane_words(p);
+    bytes[((size_t)w * p.H + y) * p.W + x] = (R[(size_t)y * p.WW + (x >> 5)] >> (x & 31)) & 1u;
+}
+
+cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s) {
+    k_pack_resources<<<dim3((p.WW + 127) / 128, p.H, p.n_worlds), 128, 0, s>>>(p, bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_resources(const DevParams &p, uint8_t *bytes, cudaStream_t s) {
+    k_unpack_resources<<<dim3((p.W + 255) / 256, p.H, p.n_worlds), 256, 0, s>>>(p, bytes);
+    return cudaGetLastError();
+}
+
+// --------------------------------------------------- weights canonical <-> device
+__global__ void k_weights_to_device(DevParams p, const float *canon, size_t first, size_t n) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * (size_t)p.P) return;
+    const size_t a = idx / p.P;
+    const int j = (int)(idx - a * p.P);
+    p.weights[(first + a) * p.Pd + canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout)] = canon[idx];
+}
+
+__global__ void k_weights_to_canon(DevParams p, float *canon, size_t first, size_t n) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * (size_t)p.P) return;
+    const size_t a = idx / p.P;
+    const int j = (int)(idx - a * p.P);
+    canon[idx] = p.weights[(first + a) * p.Pd + canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout)];
+}
+
+cudaError_t launch_weights_to_device(const DevParams &p, const float *canon, size_t first, size_t n, cudaStream_t s) {
+    const size_t tot = n * (size_t)p.P;
+    if (!tot) return cudaSuccess;
+    k_weights_to_device<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(p, canon, first, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_weights_to_canon(const DevParams &p, float *canon, size_t first, size_t n, cudaStream_t s) {
+    const size_t tot = n * (size_t)p.P;
+    if (!tot) return cudaSuccess;
+    k_weights_to_canon<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(p, canon, first, n);
+    return cudaGetLastError();
+}
+
+}  // namespace eco

@@ -1,0 +1,292 @@
+"""Thin ctypes binding of libsim.so (include/sim.h).  Argument marshalling only: every
+step of the world step runs in the library's CUDA kernels.  There is no CPU fallback —
+if the extension cannot be loaded or no CUDA device is present, calls raise.
+
+Names follow the C ABI: create / step / get_state / set_state / destroy, plus the test
+and measurement hooks (forced actions, step log, totals, per-kernel timed step).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import build as _build
+
+_lock = threading.Lock()
+_lib = None
+
+SIM_OK, SIM_E_INVALID, SIM_E_CUDA, SIM_E_OOM, SIM_E_NCCL, SIM_E_NONFINITE, SIM_E_STATE = 0, -1, -2, -3, -4, -5, -6
+ABI_VERSION = 1
+INT32_MAX = 2**31 - 1
+NUM_KERNELS = 6
+KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate")
+
+EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
+            "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
+            "sim_step_timed", "sim_synchronize", "sim_kernels_per_step")
+
+
+class SimError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libsim status {status}: {msg}")
+        self.status = status
+
+
+class SimConfig(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_uint32), ("struct_size", ctypes.c_uint32),
+        ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+        ("n_worlds", ctypes.c_int32), ("device", ctypes.c_int32),
+        ("seeds", ctypes.POINTER(ctypes.c_uint64)),
+        ("init_resource_p", ctypes.c_double),
+        ("regrow_r2", ctypes.c_int32),
+        ("f_class_min_k", ctypes.c_int32 * 4),
+        ("f_value", ctypes.c_double * 4),
+        ("lat_top", ctypes.c_double), ("lat_bottom", ctypes.c_double),
+        ("spontaneous", ctypes.c_double),
+        ("slots", ctypes.c_int32), ("n_initial", ctypes.c_int32),
+        ("obs_radius", ctypes.c_int32), ("hidden", ctypes.c_int32),
+        ("n_actions", ctypes.c_int32), ("log_capacity", ctypes.c_int32),
+        ("init_weight_std", ctypes.c_double), ("mutation_std", ctypes.c_double),
+        ("e_init", ctypes.c_int32), ("e_decay", ctypes.c_int32), ("e_gain", ctypes.c_int32),
+        ("e_repr_gt", ctypes.c_int32), ("e_death_le", ctypes.c_int32), ("e_max", ctypes.c_int32),
+        ("repr_steps", ctypes.c_int32), ("max_age", ctypes.c_int32),
+        ("cuda_stream", ctypes.c_void_p),
+    ]
+
+
+class SimState(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64)] + [(f, ctypes.c_void_p) for f in (
+        "resources", "alive", "cell", "energy", "age", "repr", "last_action", "ate", "h", "c", "weights",
+        "logits")]
+
+
+RECORD_FIELDS = ("t", "agents_at_start", "grown", "eaten", "births", "deaths_energy", "deaths_age",
+                 "deferred_no_cell", "deferred_claim", "deferred_capacity", "population", "resources",
+                 "near_ties", "obs_nnz")
+RECORD_DTYPE = np.dtype([(f, np.int64) for f in RECORD_FIELDS])
+TOTALS_FIELDS = ("steps", "agent_steps", "cell_updates", "births", "deaths", "eaten", "grown")
+
+
+class SimTotals(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in TOTALS_FIELDS]
+
+
+class SimStateSizes(ctypes.Structure):
+    _fields_ = [("cells", ctypes.c_int64), ("slots", ctypes.c_int64), ("hidden", ctypes.c_int32),
+                ("inputs", ctypes.c_int32), ("params", ctypes.c_int32), ("n_actions", ctypes.c_int32),
+                ("device_bytes", ctypes.c_int64)]
+
+
+class SimStepTiming(ctypes.Structure):
+    _fields_ = [("step_ms", ctypes.c_float), ("kernel_ms", ctypes.c_float * NUM_KERNELS)]
+
+
+def lib():
+    """Load (building first if stale) the in-tree libsim.so.  Raises if it cannot."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build.LIB
+            if not os.path.exists(path) or _build._stale():
+                _build.build()
+            L = ctypes.CDLL(path)
+            H = ctypes.c_void_p
+            L.sim_create.argtypes = [ctypes.POINTER(SimConfig), ctypes.POINTER(H)]
+            L.sim_step.argtypes = [H, ctypes.c_int64]
+            L.sim_get_state.argtypes = [H, ctypes.POINTER(SimState)]
+            L.sim_set_state.argtypes = [H, ctypes.POINTER(SimState)]
+            L.sim_destroy.argtypes = [H]
+            L.sim_last_error.restype = ctypes.c_char_p
+            L.sim_validate.argtypes = [ctypes.POINTER(SimConfig)]
+            L.sim_state_sizes.argtypes = [ctypes.POINTER(SimConfig), ctypes.POINTER(SimStateSizes)]
+            L.sim_set_forced_actions.argtypes = [H, ctypes.c_void_p]
+            L.sim_get_step_log.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+            L.sim_get_totals.argtypes = [H, ctypes.POINTER(SimTotals)]
+            L.sim_step_timed.argtypes = [H, ctypes.POINTER(SimStepTiming)]
+            L.sim_synchronize.argtypes = [H]
+            L.sim_kernels_per_step.restype = ctypes.c_int32
+            for f in EXPORTED:
+                if f not in ("sim_last_error", "sim_kernels_per_step"):
+                    getattr(L, f).restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != SIM_OK:
+        raise SimError(rc, lib().sim_last_error().decode())
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        return 0
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)  # torch.cuda.Stream
+
+
+def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0):
+    """SimConfig from a workloads.WorldConfig (or any object with the same fields).
+    Returns (config, seeds array) — keep the array alive while the config is used."""
+    seeds = np.ascontiguousarray(np.array([int(s) & 0xFFFFFFFFFFFFFFFF for s in wc.seeds], dtype=np.uint64))
+    c = SimConfig()
+    c.abi_version, c.struct_size = ABI_VERSION, ctypes.sizeof(SimConfig)
+    c.rows, c.cols, c.n_worlds, c.device = wc.rows, wc.cols, len(seeds), device
+    c.seeds = seeds.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    c.init_resource_p, c.regrow_r2 = wc.init_resource_p, wc.regrow_r2
+    for i in range(4):
+        c.f_class_min_k[i] = int(wc.f_class_min_k[i])
+        c.f_value[i] = float(wc.f_value[i])
+    c.lat_top, c.lat_bottom, c.spontaneous = wc.lat_top, wc.lat_bottom, wc.spontaneous
+    c.slots, c.n_initial = wc.slots, wc.n_initial
+    c.obs_radius, c.hidden, c.n_actions = wc.obs_radius, wc.hidden, wc.n_actions
+    c.log_capacity = log_capacity
+    c.init_weight_std, c.mutation_std = wc.init_weight_std, wc.mutation_std
+    c.e_init, c.e_decay, c.e_gain = wc.e_init, wc.e_decay, wc.e_gain
+    c.e_repr_gt, c.e_death_le, c.e_max = wc.e_repr_gt, wc.e_death_le, wc.e_max
+    c.repr_steps, c.max_age = wc.repr_steps, wc.max_age
+    c.cuda_stream = _stream_handle(stream)
+    return c, seeds
+
+
+def validate(wc) -> None:
+    c, _seeds = make_config(wc)
+    _check(lib().sim_validate(ctypes.byref(c)))
+
+
+def state_sizes(wc) -> dict:
+    c, _seeds = make_config(wc)
+    s = SimStateSizes()
+    _check(lib().sim_state_sizes(ctypes.byref(c), ctypes.byref(s)))
+    return {f: int(getattr(s, f)) for f, _ in SimStateSizes._fields_}
+
+
+STATE_FIELDS = ("resources", "alive", "cell", "energy", "age", "repr", "last_action", "ate", "h", "c",
+                "weights", "logits")
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class World:
+    """One handle of libsim.so: n_worlds independent worlds batched on one GPU."""
+
+    def __init__(self, wc, device: int = 0, stream=None, log_capacity: int = 0):
+        self.wc = wc
+        self.n_worlds = len(wc.seeds)
+        self._cfg, self._seeds = make_config(wc, device, stream, log_capacity)
+        self.log_capacity = log_capacity or 4096
+        h = ctypes.c_void_p()
+        _check(lib().sim_create(ctypes.byref(self._cfg), ctypes.byref(h)))
+        self._h = h
+        self._t = 0
+
+    # -- lifecycle ------------------------------------------------------------------
+    def destroy(self):
+        if getattr(self, "_h", None):
+            lib().sim_destroy(self._h)
+            self._h = None
+
+    close = destroy
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def t(self) -> int:
+        return self._t
+
+    def step(self, n: int = 1):
+        _check(lib().sim_step(self._h, int(n)))
+        self._t += int(n)
+
+    def step_timed(self) -> dict:
+        tm = SimStepTiming()
+        _check(lib().sim_step_timed(self._h, ctypes.byref(tm)))
+        self._t += 1
+        return {"step_ms": float(tm.step_ms), **{k: float(tm.kernel_ms[i]) for i, k in enumerate(KERNEL_NAMES)}}
+
+    def synchronize(self):
+        _check(lib().sim_synchronize(self._h))
+
+    # -- state ----------------------------------------------------------------------
+    def empty_state(self, fields=STATE_FIELDS) -> dict:
+        wc, nw = self.wc, self.n_worlds
+        S, Hd, P = wc.slots, wc.hidden, wc.n_params
+        shapes = {
+            "resources": ((nw, wc.rows, wc.cols), np.uint8), "alive": ((nw, S), np.uint8),
+            "cell": ((nw, S), np.int32), "energy": ((nw, S), np.int32), "age": ((nw, S), np.int32),
+            "repr": ((nw, S), np.int32), "last_action": ((nw, S), np.uint8), "ate": ((nw, S), np.uint8),
+            "h": ((nw, S, Hd), np.float32), "c": ((nw, S, Hd), np.float32),
+            "weights": ((nw, S, P), np.float32), "logits": ((nw, S, 5), np.float32),
+        }
+        return {f: np.zeros(*shapes[f]) for f in fields}
+
+    def get_state(self, fields=STATE_FIELDS) -> dict:
+        """Canonical state (include/sim.h sim_state) as numpy arrays with a leading world axis."""
+        out = self.empty_state(fields)
+        st = SimState()
+        for f in fields:
+            setattr(st, f, _ptr(out[f]))
+        _check(lib().sim_get_state(self._h, ctypes.byref(st)))
+        out["t"] = int(st.t)
+        self._t = int(st.t)
+        return out
+
+    def set_state(self, state: dict):
+        """Inject canonical state (fields missing from `state` keep their device values).
+        Per-field arrays may omit the world axis when n_worlds == 1."""
+        st = SimState()
+        keep = []
+        ref = self.empty_state([f for f in STATE_FIELDS if f in state])
+        for f in STATE_FIELDS:
+            if f not in state:
+                continue
+            a = np.ascontiguousarray(np.asarray(state[f]).reshape(ref[f].shape), dtype=ref[f].dtype)
+            keep.append(a)
+            setattr(st, f, _ptr(a))
+        st.t = int(state.get("t", self._t))
+        _check(lib().sim_set_state(self._h, ctypes.byref(st)))
+        self._t = int(st.t)
+
+    def set_forced_actions(self, actions):
+        """actions: [n_worlds][S] (or [S]) uint8, 255 = policy; None clears."""
+        if actions is None:
+            _check(lib().sim_set_forced_actions(self._h, None))
+            return
+        a = np.ascontiguousarray(np.asarray(actions, dtype=np.uint8).reshape(self.n_worlds, self.wc.slots))
+        _check(lib().sim_set_forced_actions(self._h, _ptr(a)))
+
+    def step_log(self, first: int, n: int) -> np.ndarray:
+        """Records of steps [first, first+n): structured array of shape [n, n_worlds]."""
+        out = np.zeros((n, self.n_worlds), RECORD_DTYPE)
+        _check(lib().sim_get_step_log(self._h, int(first), int(n), _ptr(out)))
+        return out
+
+    def totals(self) -> dict:
+        tt = SimTotals()
+        _check(lib().sim_get_totals(self._h, ctypes.byref(tt)))
+        return {f: int(getattr(tt, f)) for f in TOTALS_FIELDS}
+
+
+def world_view(state: dict, w: int) -> dict:
+    """One world's slice of a batched state dict."""
+    return {k: (v[w] if isinstance(v, np.ndarray) else v) for k, v in state.items()}

@@ -1,0 +1,340 @@
+"""GPU parity: the CUDA library (through its C ABI) against the oracle on seeded inputs.
+
+Integer state, step records and slot layout bit-exact; LSTM state within R27; weights
+bit-exact up to counted 1-ulp differences (R29); argmax disagreements only at flagged
+near-ties (R28).  Sizes span several tiles and ragged tails; BASELINE sizes are covered
+by sampled one-step checks in test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from harness import (compare_floats, compare_ints, compare_record, compare_weights, gpu_world_state, lockstep)
+from scenario import E, N, STAY, W, build_state, forced, small_config
+
+pytestmark = pytest.mark.gpu
+
+sim = pytest.importorskip("paper_2302_09334_b200.sim")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+
+
+def gpu_state(world, w=0, weights=True):
+    fields = sim.STATE_FIELDS if weights else tuple(f for f in sim.STATE_FIELDS if f != "weights")
+    return gpu_world_state(world.get_state(fields), w)
+
+
+# ----------------------------------------------------------------------------- init
+@pytest.mark.parametrize("cfg", ["tiny", "paper", "odd"])
+def test_init_matches_oracle(cfg):
+    wc = {"tiny": workloads.tiny(), "paper": workloads.paper_scale(),
+          "odd": workloads.tiny().replace(rows=37, cols=68, slots=100, n_initial=77, seeds=(12345678901,),
+                                          hidden=16, obs_radius=3)}[cfg]
+    with sim.World(wc) as world:
+        g = gpu_state(world)
+        o = oracle.OracleWorld(wc).state()
+        compare_ints(g, o, "init")
+        assert np.array_equal(g["last_action"], o["last_action"])
+        live = o["alive"] == 1
+        compare_weights(g["weights"], o["weights"], live, where="init")
+        assert np.all(g["weights"][~live] == 0)
+        assert np.all(g["h"] == 0) and np.all(g["c"] == 0)
+
+
+def test_init_invalid_too_many_agents():
+    wc = workloads.tiny().replace(init_resource_p=0.99, slots=900, n_initial=800)
+    with pytest.raises(sim.SimError) as ei:
+        sim.World(wc)
+    assert ei.value.status == sim.SIM_E_INVALID and "n_initial" in str(ei.value)
+
+
+# ------------------------------------------------------------------- regrowth-only
+@pytest.mark.parametrize("rows,cols,steps,every", [(200, 400, 1000, 1), (37, 68, 300, 1), (2, 36, 200, 1),
+                                                   (2048, 4096, 100, 10)])
+def test_regrowth_only_bit_exact(rows, cols, steps, every):
+    wc = workloads.regrowth_micro(rows, cols)
+    world = sim.World(wc)
+    R = oracle.OracleWorld(wc).st["resources"].copy()
+    g = world.get_state(("resources",))["resources"][0]
+    assert np.array_equal(g, R)
+    for t in range(steps):
+        R, grown = oracle.regrow(wc, t, R)
+        world.step(1)
+        rec = world.step_log(t, 1)[0, 0]
+        assert rec["grown"] == grown and rec["resources"] == int(R.sum()), t
+        if (t + 1) % every == 0 or t + 1 == steps:
+            g = world.get_state(("resources",))["resources"][0]
+            assert np.array_equal(g, R), f"step {t}"
+    world.destroy()
+
+
+@pytest.mark.parametrize("r2", [1, 2, 5, 8])
+def test_regrowth_other_radii(r2):
+    wc = workloads.regrowth_micro(45, 100).replace(regrow_r2=r2, f_class_min_k=(0, 1, 2, 4),
+                                                  f_value=(0.0, 0.2, 0.4, 0.9))
+    world = sim.World(wc)
+    R = oracle.OracleWorld(wc).st["resources"].copy()
+    for t in range(40):
+        R, _ = oracle.regrow(wc, t, R)
+    world.step(40)
+    assert np.array_equal(world.get_state(("resources",))["resources"][0], R)
+
+
+# --------------------------------------------------------------- full trajectories
+def test_tiny_free_running_100_steps_bit_exact():
+    """M1: the tiny config's 100 steps, free running on both sides."""
+    wc = workloads.tiny()
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    near = 0
+    for t in range(100):
+        orec = orc.step()
+        world.step(1)
+        g = gpu_state(world, weights=False)
+        o = orc.state()
+        where = f"tiny step {t}"
+        compare_ints(g, o, where)
+        assert np.array_equal(g["last_action"][o["alive"] == 1], o["last_action"][o["alive"] == 1]), where
+        compare_record(world.step_log(t, 1)[0, 0], orec, where)
+        near += orec["near_ties"]
+        live = np.flatnonzero(o["alive"] == 1)
+        compare_floats(g, o, live, where)
+    gw = world.get_state(("weights",))["weights"][0]
+    compare_weights(gw, orc.st["weights"], orc.st["alive"] == 1, where="tiny end")
+    print(f"tiny: {near} near-tie agent-steps flagged, trajectory bit-exact")
+
+
+def test_tiny_lockstep_m2_m3():
+    wc = workloads.tiny()
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    flips, n, nulp = lockstep(world, orc, 100, check_weights_every=25)
+    assert n > 1000
+
+
+def test_paper_scale_lockstep_200_steps():
+    """C1 (configs[1]) first 200 steps: M2 + M3 every step."""
+    wc = workloads.paper_scale()
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    flips, n, nulp = lockstep(world, orc, 200, check_weights_every=100)
+    print(f"paper-scale: {n} agent-steps compared, {flips} near-tie disagreements, {nulp} one-ulp weights")
+    assert n > 200000
+
+
+@pytest.mark.parametrize("hidden,r", [(4, 1), (16, 2), (32, 0), (8, 3)])
+def test_other_shapes_lockstep(hidden, r):
+    wc = workloads.tiny().replace(rows=30, cols=72, slots=200, n_initial=90, hidden=hidden, obs_radius=r,
+                                  repr_steps=5, e_repr_gt=10200, seeds=(77,))
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    flips, n, _ = lockstep(world, orc, 60, check_weights_every=30)
+    assert n > 1000
+
+
+# --------------------------------------------------------------- injected states (M3)
+@pytest.mark.parametrize("cfg,seed", [("tiny", 1), ("tiny", 2), ("paper", 3), ("crowd", 4)])
+def test_random_state_one_step(cfg, seed):
+    if cfg == "paper":
+        wc = workloads.paper_scale().replace(slots=2048)
+        st = workloads.random_state(wc, seed, n_alive=1500, density=0.5)
+    elif cfg == "crowd":
+        # a crowded small world: many claims, births, deaths and capacity deferrals
+        wc = workloads.tiny().replace(rows=16, cols=32, slots=300, mutation_std=0.05)
+        st = workloads.random_state(wc, seed, n_alive=250, density=0.3)
+    else:
+        wc = workloads.tiny()
+        st = workloads.random_state(wc, seed, n_alive=20, density=0.4)
+    st["t"] = 1234 + seed
+    for rep in range(3):
+        world = sim.World(wc)
+        world.set_state(st)
+        orc = oracle.OracleWorld(wc, state=st)
+        orec = orc.step()
+        world.step(1)
+        g = gpu_state(world)
+        o = orc.state()
+        compare_ints(g, o, f"{cfg} rep {rep}")
+        compare_record(world.step_log(st["t"], 1)[0, 0], orec, cfg)
+        live = np.flatnonzero((o["alive"] == 1) & (o["age"] > 0))
+        compare_floats(g, o, live, cfg)
+        compare_weights(g["weights"], o["weights"], o["alive"] == 1, where=cfg)
+        world.destroy()
+        st = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in o.items()}
+
+
+# --------------------------------------------------------------------- scenarios
+def run_both(wc, st, f):
+    world = sim.World(wc)
+    world.set_state(st)
+    world.set_forced_actions(f)
+    world.step(1)
+    g = gpu_state(world)
+    orc = oracle.OracleWorld(wc, state=st)
+    orec = orc.step(f)
+    compare_ints(g, orc.state(), "scenario")
+    compare_record(world.step_log(st["t"], 1)[0, 0], orec, "scenario")
+    return g, orec
+
+
+def test_scenarios_s1_to_s13_match_oracle():
+    wc = small_config()
+    cases = [
+        ([dict(slot=0, y=2, x=2), dict(slot=1, y=2, x=3)], None, {0: E, 1: W}),              # S1
+        ([dict(slot=0, y=2, x=2), dict(slot=1, y=2, x=3)], None, {0: E, 1: E}),              # S2
+        ([dict(slot=0, y=2, x=1), dict(slot=1, y=2, x=3)], None, {0: E, 1: W}),              # S3
+        ([dict(slot=0, y=0, x=3)], None, {0: N}),                                            # S4
+        ([dict(slot=0, y=3, x=3)], [(3, 4), (0, 0)], {0: E}),                                # S6
+        ([dict(slot=0, y=3, x=3, energy=100)], None, {}),                                    # S11
+        ([dict(slot=0, y=3, x=3, energy=50000, age=1000)], None, {}),                        # S12
+        ([dict(slot=0, y=3, x=3, energy=11100, repr=7)], [(3, 3)], {}),                      # S13
+        ([dict(slot=0, y=2, x=1, energy=20000, repr=19), dict(slot=1, y=2, x=3, energy=20000, repr=19)],
+         [(1, 1), (3, 1), (2, 0), (1, 3), (3, 3), (2, 4)], {}),                              # S7
+        ([dict(slot=0, y=0, x=0, energy=20000, repr=19), dict(slot=1, y=0, x=1), dict(slot=2, y=1, x=0)],
+         None, {}),                                                                          # S8
+    ]
+    for t in range(0, 40, 7):
+        for agents, res, acts in cases:
+            st = build_state(wc, agents, resources=res, t=t)
+            run_both(wc, st, forced(wc, acts))
+    # S9 capacity and S10 slot reuse
+    wc3 = small_config(rows=6, cols=8, slots=3)
+    st = build_state(wc3, [dict(slot=i, y=1 + 2 * i, x=2 + 2 * i, energy=20000, repr=25) for i in range(3)])
+    g, rec = run_both(wc3, st, forced(wc3, {}))
+    assert rec["deferred_capacity"] == 3
+    st = build_state(wc3, [dict(slot=0, y=1, x=1, energy=20000, repr=25), dict(slot=1, y=4, x=6, energy=100),
+                           dict(slot=2, y=4, x=2, energy=20000)])
+    g, rec = run_both(wc3, st, forced(wc3, {}))
+    assert rec["births"] == 1 and g["alive"][1] == 1
+    # S5 regrowth fills the cell under a staying agent
+    wc5 = small_config(regrowth=True).replace(f_value=(0.0, 0.0, 0.0, 0.0), spontaneous=1.0)
+    g, rec = run_both(wc5, build_state(wc5, [dict(slot=0, y=3, x=3)]), forced(wc5, {0: STAY}))
+    assert g["ate"][0] == 1 and rec["eaten"] == 1
+
+
+def test_scripted_walk_births_21_41_61_81_on_gpu():
+    wc = small_config(rows=5, cols=120, slots=8)
+    st = build_state(wc, [dict(slot=0, y=2, x=0)], resources=[(2, x) for x in range(1, 120)])
+    world = sim.World(wc)
+    world.set_state(st)
+    world.set_forced_actions(forced(wc, {0: E}))
+    world.step(100)
+    log = world.step_log(0, 100)[:, 0]
+    assert list(np.flatnonzero(log["births"])) == [21, 41, 61, 81]
+    # walk (i): a never-eating agent dies at 0-based step 99
+    world.set_state(build_state(wc, [dict(slot=0, y=2, x=0)]))
+    world.set_forced_actions(forced(wc, {}))
+    world.step(100)
+    log = world.step_log(0, 100)[:, 0]
+    assert list(np.flatnonzero(log["deaths_energy"])) == [99]
+
+
+# ----------------------------------------------------------------------- ensemble
+def test_ensemble_batch_equals_single_worlds_and_oracle():
+    seeds = (100, 131, 163)
+    wc = workloads.ensemble(seeds).replace(slots=4096)
+    batched = sim.World(wc)
+    batched.step(60)
+    gb = batched.get_state()
+    for wi, s in enumerate(seeds):
+        single = sim.World(wc.replace(seeds=(s,)))
+        single.step(60)
+        g1 = single.get_state()
+        for k in sim.STATE_FIELDS:
+            assert np.array_equal(gb[k][wi], g1[k][0]), (s, k)
+        single.destroy()
+    log = batched.step_log(0, 60)
+    assert log.shape == (60, 3)
+    # worlds 100 and 163 against the oracle (lockstep, 40 steps each)
+    for s in (100, 163):
+        w1 = sim.World(wc.replace(seeds=(s,)))
+        orc = oracle.OracleWorld(wc.replace(seeds=(s,)))
+        lockstep(w1, orc, 40)
+        w1.destroy()
+
+
+# --------------------------------------------------------------------- edge cases
+def test_edge_empty_and_degenerate_worlds():
+    # no agents at all, agents but zero initial, single-row-pair grid, W not a multiple of 32
+    for wc in (workloads.tiny().replace(slots=0, n_initial=0),
+               workloads.tiny().replace(n_initial=0),
+               workloads.tiny().replace(rows=2, cols=36, slots=10, n_initial=6),
+               workloads.tiny().replace(rows=9, cols=100, slots=64, n_initial=64)):
+        world = sim.World(wc)
+        orc = oracle.OracleWorld(wc)
+        for t in range(30):
+            orec = orc.step()
+            world.step(1)
+            compare_ints(gpu_state(world, weights=False), orc.state(), f"edge {wc.rows}x{wc.cols} step {t}")
+            compare_record(world.step_log(t, 1)[0, 0], orec)
+        world.destroy()
+
+
+def test_extinction_and_step_zero():
+    wc = workloads.no_regrowth(workloads.tiny()).replace(init_resource_p=0.0)
+    world = sim.World(wc)
+    world.step(0)
+    world.step(101)
+    log = world.step_log(0, 101)[:, 0]
+    assert log["population"][-1] == 0 and world.totals()["steps"] == 101
+
+
+def test_determinism_and_resume():
+    wc = workloads.tiny().replace(rows=40, cols=80, slots=128, n_initial=60, seeds=(9,))
+    a = sim.World(wc)
+    a.step(150)
+    sa = a.get_state()
+    b = sim.World(wc)
+    b.step(70)
+    snap = b.get_state()
+    c = sim.World(wc)
+    c.set_state(snap)
+    c.step(80)
+    sc = c.get_state()
+    b.step(80)
+    sb = b.get_state()
+    for k in sim.STATE_FIELDS:
+        assert np.array_equal(sa[k], sb[k]), k
+        assert np.array_equal(sa[k], sc[k]), k
+    assert sa["t"] == sc["t"] == 150
+
+
+def test_set_state_rejects_bad_occupancy_and_nonfinite():
+    wc = workloads.tiny()
+    world = sim.World(wc)
+    st = world.get_state()
+    st2 = dict(st)
+    st2["cell"] = st["cell"].copy()
+    live = np.flatnonzero(st["alive"][0])
+    st2["cell"][0, live[1]] = st["cell"][0, live[0]]
+    with pytest.raises(sim.SimError):
+        world.set_state(st2)
+    st3 = dict(st)
+    st3["weights"] = st["weights"].copy()
+    st3["weights"][0, live[0], 3] = np.nan
+    with pytest.raises(sim.SimError):
+        world.set_state(st3)
+
+
+def test_nonfinite_state_reported():
+    wc = workloads.tiny()
+    world = sim.World(wc)
+    st = world.get_state()
+    live = np.flatnonzero(st["alive"][0])[0]
+    G = 4 * wc.hidden
+    boff = G * wc.n_inputs + G * wc.hidden
+    # bias 50 on every gate: i = f = o = 1, g = 1, so h' ~ tanh(2); W_out = 3e38 overflows the logits
+    st["weights"][0, live, boff:boff + G] = 50.0
+    st["weights"][0, live, boff + G:boff + G + 5 * wc.hidden] = 3.0e38
+    st["c"][0, live, :] = 1.0
+    world.set_state(st)
+    with pytest.raises(sim.SimError) as ei:
+        world.step(1)
+        world.synchronize()
+    assert ei.value.status == sim.SIM_E_NONFINITE
