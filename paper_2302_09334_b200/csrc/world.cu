@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_regrow(DevParams p) {
     unsigned cnt = __popc(grow);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0 && cnt) {
+    if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0 && cnt) {
         sim_step_record *rec = record_of(p, p.t[w], w);
         atomicAdd(reinterpret_cast<unsigned long long *>(&rec->grown), (unsigned long long)cnt);
     }
