@@ -1,0 +1,24 @@
+#!/bin/bash
+# One GPU job: build, smoke, GPU tests, bench, ncu launch list + one full capture of k_policy.
+# Usage (under gpurun): bash tools/gpu_round.sh [tag]
+TAG=${1:-r1}
+OUT=gpurun_out
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1; echo build=$? > $OUT/status.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo smoke=$? >> $OUT/status.txt
+if [ "${SKIP_TESTS:-0}" != "1" ]; then
+  timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -rf > $OUT/gpu_tests.log 2>&1; echo tests=$? >> $OUT/status.txt
+fi
+timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo bench=$? >> $OUT/status.txt
+if [ "${SKIP_NCU:-0}" != "1" ]; then
+  CMD="python bench.py --steps 30 --warmup 300 --no-e2e --no-cpu-baseline --no-replay"
+  timeout 300 $CMD > $OUT/plain_$TAG.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(regrow|policy|move|birth|mutate)" \
+      -s 1806 -c 120 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
+  echo ncu_launch=$? >> $OUT/status.txt
+  timeout 300 $CMD > $OUT/plain2_$TAG.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_policy -s 300 -c 2 \
+      -o $OUT/prof_policy_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1
+  echo ncu_full=$? >> $OUT/status.txt
+fi
+cat $OUT/status.txt
