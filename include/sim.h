@@ -139,10 +139,10 @@ typedef struct {
 } sim_state_sizes_t;
 
 /* Per-kernel timing of one instrumented step (milliseconds, CUDA events). */
-#define SIM_NUM_KERNELS 6
+#define SIM_NUM_KERNELS 7
 typedef struct {
     float step_ms;                     /* first event to last event of the step */
-    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_rank, mutate */
+    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_win, birth_rank, mutate */
 } sim_step_timing;
 
 /* --- lifecycle ------------------------------------------------------------------- */

@@ -48,17 +48,34 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
     const long per_round = (long)gridDim.x * warps_per_block * AG;
     const size_t HW = (size_t)p.H * p.W;
 
+    // housekeeping for the later phases of this step: the survivor list of step t+1 and
+    // the winner counters start at 0; the birth bitmap of parity t+1 (used by step t-1)
+    // is cleared for step t+1.
+    {
+        const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const size_t gthreads = (size_t)gridDim.x * blockDim.x;
+        const size_t pw = plane_words(p);
+        for (size_t k = gtid; k < (size_t)p.n_worlds * pw; k += gthreads) {
+            const int w = (int)(k / pw);
+            bbits_of(p, p.t[w] + 1, w)[k - (size_t)w * pw] = 0u;
+        }
+        for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
+            *count_of(p, p.t[w] + 1, (int)w) = 0;
+            p.n_win[w] = 0;
+        }
+    }
+
     for (long base = 0; base < total; base += per_round) {
         // consecutive agents go to different CTAs so a small population spreads over all SMs
         const long v = base + (long)(wib * AG + grp) * gridDim.x + blockIdx.x;
         const bool in_range = v < total;
         const int w = in_range ? (int)(v / p.S) : 0;
         const int i = in_range ? (int)(v - (long)w * p.S) : 0;
-        const bool active = in_range && i < p.n_alive[w];
-        if (!__any_sync(FULL, active)) continue;
-        const int slot = active ? p.alive_list[(size_t)w * p.S + i] : 0;
-        const size_t gs = (size_t)w * p.S + slot;
         const int64_t t = p.t[w];
+        const bool active = in_range && i < *count_of(p, t, w);
+        if (!__any_sync(FULL, active)) continue;
+        const int slot = active ? list_of(p, t, w)[i] : 0;
+        const size_t gs = (size_t)w * p.S + slot;
 
         // ---- a2: observation bitmask (channel 0 = R' after regrowth, 1 = O_t incl. self)
         uint64_t m_lo = 0ull, m_hi = 0ull;
@@ -234,26 +251,40 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 // live agent eats the resource under its final cell; fixed-point energy
 // e += gain*ate - decay, age += 1, repr = e > thr ? repr+1 : 0 (R16, R17, R19); death
 // iff e <= 0 (cause energy) or age > max_age (cause age) (R18).  O is updated in place
-// (moves, deaths) with bit atomics; distinct agents touch distinct bits.
+// (moves, deaths) with bit atomics; distinct agents touch distinct bits.  Survivors are
+// appended to the step-(t+1) list (order is irrelevant to every result).
 __device__ __forceinline__ void warp_count_add(unsigned long long *dst, bool flag) {
     const unsigned m = __ballot_sync(0xffffffffu, flag);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(dst, (unsigned long long)__popc(m));
+}
+
+// iteration helper: virtual index v over [0, n_worlds*S) -> (world, list position)
+struct AgentIter {
+    int w, i;
+    bool in_range;
+};
+__device__ __forceinline__ AgentIter agent_at(const DevParams &p, long v) {
+    AgentIter a;
+    a.in_range = v < (long)p.n_worlds * p.S;
+    a.w = a.in_range ? (int)(v / p.S) : 0;
+    a.i = a.in_range ? (int)(v - (long)a.w * p.S) : 0;
+    return a;
 }
 
 __global__ void __launch_bounds__(256) k_move(DevParams p) {
     const long total = (long)p.n_worlds * p.S;
     const long stride = (long)gridDim.x * blockDim.x;
     const size_t HW = (size_t)p.H * p.W;
+    const unsigned lane = threadIdx.x & 31;
     for (long base = (long)blockIdx.x * blockDim.x; base < total; base += stride) {
-        const long v = base + threadIdx.x;
-        const bool in_range = v < total;
-        const int w = in_range ? (int)(v / p.S) : 0;
-        const int i = in_range ? (int)(v - (long)w * p.S) : 0;
-        const bool active = in_range && i < p.n_alive[w];
-        bool ate = false, died_e = false, died_a = false;
+        const AgentIter it = agent_at(p, base + threadIdx.x);
+        const int w = it.w;
         const int64_t t = p.t[w];
+        const bool active = it.in_range && it.i < *count_of(p, t, w);
+        bool ate = false, died_e = false, died_a = false, survive = false;
+        int slot = 0;
         if (active) {
-            const int slot = p.alive_list[(size_t)w * p.S + i];
+            slot = list_of(p, t, w)[it.i];
             const size_t gs = (size_t)w * p.S + slot;
             uint32_t *O = p.occ + (size_t)w * plane_words(p);
             uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
@@ -284,21 +315,28 @@ __global__ void __launch_bounds__(256) k_move(DevParams p) {
             if (died_e || died_a) {
                 p.alive[gs] = 0;
                 atomicAnd(word_ptr(O, p, cellv, bit), ~bit);
+                atomicAnd(p.alive_bits + (size_t)w * p.SW + (slot >> 5), ~(1u << (slot & 31)));
+            } else {
+                survive = true;
             }
         }
-        // counters (all lanes of a warp share the world only if S is a multiple of 32,
-        // so fall back to per-lane atomics when a warp straddles worlds)
         const int w0 = __shfl_sync(0xffffffffu, w, 0);
         if (__all_sync(0xffffffffu, w == w0)) {
             sim_step_record *rec = record_of(p, p.t[w0], w0);
             warp_count_add(reinterpret_cast<unsigned long long *>(&rec->eaten), ate);
             warp_count_add(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), died_e);
             warp_count_add(reinterpret_cast<unsigned long long *>(&rec->deaths_age), died_a);
+            const unsigned m = __ballot_sync(0xffffffffu, survive);
+            int pos0 = 0;
+            if (lane == 0 && m) pos0 = atomicAdd(count_of(p, p.t[w0] + 1, w0), __popc(m));
+            pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+            if (survive) list_of(p, t + 1, w)[pos0 + __popc(m & ((1u << lane) - 1u))] = slot;
         } else {
             sim_step_record *rec = record_of(p, t, w);
             if (ate) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), 1ull);
             if (died_e) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), 1ull);
             if (died_a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), 1ull);
+            if (survive) list_of(p, t + 1, w)[atomicAdd(count_of(p, t + 1, w), 1)] = slot;
         }
     }
 }
@@ -314,64 +352,123 @@ cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s)
 // because K3 has finished reading them).  Then every live parent with repr >= T_repr
 // picks the first cell of a Philox-rotated (N, S, E, W) order that is
 // in-grid, agent-free after moves/deaths (O'') and resource-free after consumption (R'')
-// (R21), and posts (BIRTH w1 << 32 | ~cell) with atomicMax on bclaim[candidate].
+// (R21), and records the direction on its own cell (bdir; NO_DIR when it has none).
 __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
     const long total = (long)p.n_worlds * p.S;
     const long stride = (long)gridDim.x * blockDim.x;
     const size_t HW = (size_t)p.H * p.W;
-    const int BDY[4] = {-1, 1, 0, 0};
-    const int BDX[4] = {0, 0, 1, -1};
     for (long base = (long)blockIdx.x * blockDim.x; base < total; base += stride) {
-        const long v = base + threadIdx.x;
-        const bool in_range = v < total;
-        const int w = in_range ? (int)(v / p.S) : 0;
-        const int i = in_range ? (int)(v - (long)w * p.S) : 0;
-        const bool active = in_range && i < p.n_alive[w];
+        const AgentIter it = agent_at(p, base + threadIdx.x);
+        const int w = it.w;
+        const int64_t t = p.t[w];
+        const bool active = it.in_range && it.i < *count_of(p, t, w);
         bool no_cell = false;
         if (active) {
-            const int slot = p.alive_list[(size_t)w * p.S + i];
+            const int slot = list_of(p, t, w)[it.i];
             const size_t gs = (size_t)w * p.S + slot;
-            const int64_t t = p.t[w];
             const int tg = p.target[gs];
             if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;
-            int cand = -1;
-            if (p.alive[gs] && p.repr[gs] >= p.repr_steps) {
-                const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-                const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
+            if (p.alive[gs]) {
                 const int cellv = p.cell[gs];
-                const int y = cellv / p.W, x = cellv - y * p.W;
-                const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
-                const int s0 = (int)(d.x & 3u);
-                for (int kk = 0; kk < 4; ++kk) {
-                    const int dir = (s0 + kk) & 3;
-                    const int cy = y + BDY[dir], cx = x + BDX[dir];
-                    if (cy < 0 || cy >= p.H || cx < 0 || cx >= p.W) continue;
-                    const int c = cy * p.W + cx;
-                    if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
-                    cand = c;
-                    break;
+                uint8_t dir = NO_DIR;
+                if (p.repr[gs] >= p.repr_steps) {
+                    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+                    const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
+                    const int y = cellv / p.W, x = cellv - y * p.W;
+                    const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+                    const int s0 = (int)(d.x & 3u);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int dd = (s0 + kk) & 3;
+                        const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
+                        if (cy < 0 || cy >= p.H || cx < 0 || cx >= p.W) continue;
+                        const int c = cy * p.W + cx;
+                        if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
+                        dir = (uint8_t)dd;
+                        break;
+                    }
+                    no_cell = dir == NO_DIR;
                 }
-                if (cand < 0) {
-                    no_cell = true;
-                } else {
-                    const unsigned long long key =
-                        ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
-                    atomicMax(p.bclaim + (size_t)w * HW + cand, key);
-                    p.bkey[gs] = key;
-                    const int idx = atomicAdd(p.n_cand + w, 1);
-                    p.cand_list[(size_t)w * p.S + idx] = slot;
-                }
+                p.bdir[(size_t)w * HW + cellv] = dir;
             }
-            p.bcand[gs] = cand;
         }
         if (no_cell)
-            atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, p.t[w], w)->deferred_no_cell), 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_no_cell), 1ull);
     }
 }
 
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
     k_birth_claim<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------- K3c birth win
+// Claim resolution without atomics: the parent on cell p whose candidate is c wins iff
+// its key (BIRTH w1 << 32 | ~p) exceeds the key of every other live parent adjacent to c
+// that chose c (read from bdir of c's other neighbours, valid where O'' is set).  The
+// winner marks c in the birth bitmap and records itself as c's parent.
+__device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t, int cellv) {
+    const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+    return ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
+}
+
+__global__ void __launch_bounds__(256) k_birth_win(DevParams p) {
+    const long total = (long)p.n_worlds * p.S;
+    const long stride = (long)gridDim.x * blockDim.x;
+    const size_t HW = (size_t)p.H * p.W;
+    for (long base = (long)blockIdx.x * blockDim.x; base < total; base += stride) {
+        const AgentIter it = agent_at(p, base + threadIdx.x);
+        const int w = it.w;
+        const int64_t t = p.t[w];
+        const bool active = it.in_range && it.i < *count_of(p, t, w);
+        bool win = false, lost = false;
+        if (active) {
+            const int slot = list_of(p, t, w)[it.i];
+            const size_t gs = (size_t)w * p.S + slot;
+            if (p.alive[gs]) {
+                const int pc = p.cell[gs];
+                const uint8_t *bd = p.bdir + (size_t)w * HW;
+                const int d = bd[pc];
+                if (d != NO_DIR) {
+                    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+                    const int py = pc / p.W, px = pc - py * p.W;
+                    const int cy = py + dir_dy(d), cx = px + dir_dx(d);
+                    const int c = cy * p.W + cx;
+                    const uint64_t seed = p.seeds[w];
+                    const unsigned long long kp = birth_key(seed, t, pc);
+                    win = true;
+                    for (int dq = 0; dq < 4 && win; ++dq) {
+                        const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
+                        if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
+                        const int q = qy * p.W + qx;
+                        if (q == pc || !get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
+                        if (birth_key(seed, t, q) > kp) win = false;
+                    }
+                    if (win) {
+                        uint32_t bit;
+                        atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
+                        p.bparent[(size_t)w * HW + c] = slot;
+                    } else {
+                        lost = true;
+                    }
+                }
+            }
+        }
+        const int w0 = __shfl_sync(0xffffffffu, w, 0);
+        if (__all_sync(0xffffffffu, w == w0)) {
+            const unsigned m = __ballot_sync(0xffffffffu, win);
+            if ((threadIdx.x & 31) == 0 && m) atomicAdd(p.n_win + w0, __popc(m));
+            warp_count_add(reinterpret_cast<unsigned long long *>(&record_of(p, p.t[w0], w0)->deferred_claim), lost);
+        } else {
+            if (win) atomicAdd(p.n_win + w, 1);
+            if (lost) atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_claim), 1ull);
+        }
+    }
+}
+
+cudaError_t launch_birth_win(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
+    if (p.S == 0) return cudaSuccess;
+    k_birth_win<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

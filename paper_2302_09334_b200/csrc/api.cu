@@ -27,7 +27,7 @@ sim_status fail(sim_status st, const char *fmt, ...) {
 
 // host copy of the validated configuration plus derived sizes
 struct Derived {
-    int H, W, WW, S, Hd, I, P, Pd, n_worlds, log_cap;
+    int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, log_cap;
     int off_hh, off_b, off_out, off_bout;
     size_t pw;  // words per plane per world
 };
@@ -69,6 +69,7 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
         d->W = cfg->cols;
         d->WW = (((cfg->cols + 31) / 32) + 3) / 4 * 4;
         d->S = cfg->slots;
+        d->SW = (cfg->slots + 31) / 32;
         d->Hd = cfg->hidden;
         const int wd = 2 * cfg->obs_radius + 1;
         d->I = 2 * wd * wd;
@@ -103,15 +104,15 @@ void threshold_table(const sim_config *cfg, std::vector<uint32_t> &T) {
 size_t device_bytes(const Derived &d) {
     const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
     size_t b = 0;
-    b += nw * d.pw * 4 * 4;                 // plane0, plane1, occ, bbits
-    b += nw * d.pw * 4;                     // bprefix
-    b += nw * HW * 8 * 2;                   // claim, bclaim
-    b += nw * S * (1 * 4 + 4 * 4);          // u8 x4, i32 x4
+    b += nw * d.pw * 4 * 5;                 // plane0, plane1, occ, bbits[2]
+    b += nw * HW * (8 + 1 + 4);             // claim, bdir, bparent
+    b += nw * ((S + 31) / 32) * 4;          // alive bits
+    b += nw * S * (1 * 3 + 4 * 4);          // u8 x3, i32 x4
     b += nw * S * (size_t)d.Hd * 4 * 2;     // h, c
     b += nw * S * eco::LOGIT_STRIDE * 4;    // logits
     b += nw * S * (size_t)d.Pd * 4;         // weights
-    b += nw * S * (4 + 8 + 4 + 8);          // target, mkey, bcand, bkey
-    b += nw * S * 4 * 5;                    // alive, cand, free, birth lists
+    b += nw * S * (4 + 8);                  // target, mkey
+    b += nw * S * 4 * 5;                    // alive lists [2], free, birth lists
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
 }
@@ -178,12 +179,27 @@ sim_status check_nonfinite(sim_ctx *h) {
     return SIM_OK;
 }
 
+// the step's kernels in order (K1 regrow, K2 policy, K3 move, K3b birth claim,
+// K3c birth win, K4 birth rank, K5 mutate)
+cudaError_t launch_phase(sim_ctx *h, int k) {
+    switch (k) {
+        case 0: return eco::launch_regrow(h->p, h->stream);
+        case 1: return eco::launch_policy(h->p, h->lc, h->stream);
+        case 2: return eco::launch_move(h->p, h->lc, h->stream);
+        case 3: return eco::launch_birth_claim(h->p, h->lc, h->stream);
+        case 4: return eco::launch_birth_win(h->p, h->lc, h->stream);
+        case 5: return eco::launch_birth_rank(h->p, h->stream);
+        default: return eco::launch_mutate(h->p, h->lc, h->stream);
+    }
+}
+
 cudaError_t enqueue_step(sim_ctx *h) {
     cudaError_t e;
     if ((e = eco::launch_regrow(h->p, h->stream)) != cudaSuccess) return e;
     if ((e = eco::launch_policy(h->p, h->lc, h->stream)) != cudaSuccess) return e;
     if ((e = eco::launch_move(h->p, h->lc, h->stream)) != cudaSuccess) return e;
     if ((e = eco::launch_birth_claim(h->p, h->lc, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_birth_win(h->p, h->lc, h->stream)) != cudaSuccess) return e;
     if ((e = eco::launch_birth_rank(h->p, h->stream)) != cudaSuccess) return e;
     return eco::launch_mutate(h->p, h->lc, h->stream);
 }
@@ -272,7 +288,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     *h->nonfinite_host = 0;
 
     DevParams &p = h->p;
-    p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
+    p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
     p.n_worlds = d.n_worlds; p.r = cfg->obs_radius; p.log_cap = d.log_cap;
     p.repr_steps = cfg->repr_steps; p.max_age = cfg->max_age;
     p.e_init = cfg->e_init; p.e_decay = cfg->e_decay; p.e_gain = cfg->e_gain;
@@ -300,15 +316,15 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.plane0, nw * d.pw), "alloc");
     CKC(dalloc(h, &p.plane1, nw * d.pw), "alloc");
     CKC(dalloc(h, &p.occ, nw * d.pw), "alloc");
-    CKC(dalloc(h, &p.bbits, nw * d.pw), "alloc");
-    CKC(dalloc(h, &p.bprefix, nw * d.pw), "alloc");
+    CKC(dalloc(h, &p.bbits, 2 * nw * d.pw), "alloc");
     CKC(dalloc(h, &T_d, (size_t)d.H * 4), "alloc");
     CKC(dalloc(h, &p.claim, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.bclaim, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.bdir, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.bparent, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.alive_bits, nw * (size_t)d.SW), "alloc");
     CKC(dalloc(h, &p.alive, nw * S), "alloc");
     CKC(dalloc(h, &p.last_action, nw * S), "alloc");
     CKC(dalloc(h, &p.ate, nw * S), "alloc");
-    CKC(dalloc(h, &p.bwin, nw * S), "alloc");
     CKC(dalloc(h, &p.cell, nw * S), "alloc");
     CKC(dalloc(h, &p.energy, nw * S), "alloc");
     CKC(dalloc(h, &p.age, nw * S), "alloc");
@@ -319,12 +335,9 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
     CKC(dalloc(h, &p.target, nw * S), "alloc");
     CKC(dalloc(h, &p.mkey, nw * S), "alloc");
-    CKC(dalloc(h, &p.bcand, nw * S), "alloc");
-    CKC(dalloc(h, &p.bkey, nw * S), "alloc");
-    CKC(dalloc(h, &p.alive_list, nw * S), "alloc");
-    CKC(dalloc(h, &p.n_alive, nw), "alloc");
-    CKC(dalloc(h, &p.cand_list, nw * S), "alloc");
-    CKC(dalloc(h, &p.n_cand, nw), "alloc");
+    CKC(dalloc(h, &p.alive_list, 2 * nw * S), "alloc");
+    CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
+    CKC(dalloc(h, &p.n_win, nw), "alloc");
     CKC(dalloc(h, &p.free_list, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_parent, nw * S), "alloc");
@@ -423,19 +436,11 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
-    CK(h, eco::launch_regrow(h->p, h->stream), "regrow");
-    CK(h, cudaEventRecord(h->ev[1], h->stream), "event");
-    CK(h, eco::launch_policy(h->p, h->lc, h->stream), "policy");
-    CK(h, cudaEventRecord(h->ev[2], h->stream), "event");
-    CK(h, eco::launch_move(h->p, h->lc, h->stream), "move");
-    CK(h, cudaEventRecord(h->ev[3], h->stream), "event");
-    CK(h, eco::launch_birth_claim(h->p, h->lc, h->stream), "birth claim");
-    CK(h, cudaEventRecord(h->ev[4], h->stream), "event");
-    CK(h, eco::launch_birth_rank(h->p, h->stream), "birth rank");
-    CK(h, cudaEventRecord(h->ev[5], h->stream), "event");
-    CK(h, eco::launch_mutate(h->p, h->lc, h->stream), "mutate");
-    CK(h, cudaEventRecord(h->ev[6], h->stream), "event");
-    CK(h, cudaEventSynchronize(h->ev[6]), "event sync");
+    for (int k = 0; k < SIM_NUM_KERNELS; ++k) {
+        CK(h, launch_phase(h, k), "step kernel");
+        CK(h, cudaEventRecord(h->ev[k + 1], h->stream), "event");
+    }
+    CK(h, cudaEventSynchronize(h->ev[SIM_NUM_KERNELS]), "event sync");
     h->t += 1;
     for (int k = 0; k < SIM_NUM_KERNELS; ++k)
         CK(h, cudaEventElapsedTime(&out->kernel_ms[k], h->ev[k], h->ev[k + 1]), "elapsed");
@@ -589,9 +594,9 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     // scratch and derived structures
     if (S) {
         CK(h, cudaMemsetAsync(p.claim, 0, nw * HW * 8, s), "memset");
-        CK(h, cudaMemsetAsync(p.bclaim, 0, nw * HW * 8, s), "memset");
+        CK(h, cudaMemsetAsync(p.bdir, 0xff, nw * HW, s), "memset");
     }
-    CK(h, cudaMemsetAsync(p.bbits, 0, nw * d.pw * 4, s), "memset");
+    CK(h, cudaMemsetAsync(p.bbits, 0, 2 * nw * d.pw * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");

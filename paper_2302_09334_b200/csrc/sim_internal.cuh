@@ -10,6 +10,10 @@
 //    GEMV-friendly order W_ih^T[I][Hd][4], W_hh^T[Hd][Hd][4], b[Hd][4], W_out[5][Hd],
 //    b_out[5], padded to Pd (multiple of 32 floats = 128 B).  Lane k of an agent's lane
 //    group reads its unit's four gate weights (i,f,g,o) with one 16-B load.
+//  * alive slots: a u8 flag per slot plus a bitmap [world][SW]; the live agents of step t
+//    are listed (any order: no result depends on it) in alive_list[t&1].
+//  * reproduction: per-cell birth direction bdir (0..3 = N,S,E,W, 0xFF none), per-cell
+//    winning parent bparent, and a birth bitmap bbits[t&1] over cells (plane layout).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -22,11 +26,12 @@ constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W 
                    PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7;
 constexpr int MAX_OFFSETS = 24;
 constexpr int LOGIT_STRIDE = 8;
+constexpr uint8_t NO_DIR = 0xFF;
 
 // Everything a kernel needs, passed by value (fixed for the handle's lifetime, so one
 // captured CUDA graph serves every step; the step index lives in device memory).
 struct DevParams {
-    int H, W, WW, S, Hd, I, P, Pd, n_worlds, r, log_cap;
+    int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, r, log_cap;
     int repr_steps, max_age;
     int e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max;
     int cls_k1, cls_k2, cls_k3;  // class thresholds f_class_min_k[1..3]
@@ -39,28 +44,28 @@ struct DevParams {
     int64_t *t;               // [n_worlds] step index (all equal)
     uint32_t *plane0, *plane1;// R double buffer [n_worlds][H][WW]
     uint32_t *occ;            // O [n_worlds][H][WW]
-    uint32_t *bbits;          // birth bitmap [n_worlds][H][WW]
-    uint32_t *bprefix;        // exclusive prefix counts of bbits words [n_worlds][H*WW]
+    uint32_t *bbits;          // birth bitmaps [2][n_worlds][H][WW] (by step parity)
     const uint32_t *T;        // [H][4] Bernoulli thresholds
     unsigned long long *claim;   // [n_worlds][H*W] move claims (0 = none)
-    unsigned long long *bclaim;  // [n_worlds][H*W] birth claims
-    uint8_t *alive, *last_action, *ate, *bwin;
+    uint8_t *bdir;               // [n_worlds][H*W] birth direction of the agent on the cell
+    int32_t *bparent;            // [n_worlds][H*W] winning parent slot of a child cell
+    uint8_t *alive, *last_action, *ate;
+    uint32_t *alive_bits;        // [n_worlds][SW]
     int32_t *cell, *energy, *age, *repr;
     float *h, *c, *logits, *weights;
     int32_t *target;             // [n_worlds][S] move target of this step or -1
     unsigned long long *mkey;    // [n_worlds][S]
-    int32_t *bcand;              // [n_worlds][S] birth candidate cell or -1
-    unsigned long long *bkey;    // [n_worlds][S]
-    int32_t *alive_list, *n_alive;   // [n_worlds][S], [n_worlds]
-    int32_t *cand_list, *n_cand;     // eligible parents with a candidate cell
-    int32_t *free_list;              // [n_worlds][S] scratch
+    int32_t *alive_list;         // [2][n_worlds][S]
+    int32_t *n_alive;            // [2][n_worlds]
+    int32_t *n_win;              // [n_worlds] birth-claim winners this step
+    int32_t *free_list;          // [n_worlds][S] scratch (first n_place entries used)
     int32_t *birth_child, *birth_parent, *n_births;
-    int64_t *res_count;              // [n_worlds] resources at step start
-    sim_step_record *log;            // [log_cap][n_worlds]
-    unsigned long long *totals;      // [7] sim_totals order
-    const uint8_t *forced;           // [n_worlds][S]
-    const int32_t *forced_on;        // device flag
-    int32_t *nonfinite;              // host-mapped flag
+    int64_t *res_count;          // [n_worlds] resources at step start
+    sim_step_record *log;        // [log_cap][n_worlds]
+    unsigned long long *totals;  // [7] sim_totals order
+    const uint8_t *forced;       // [n_worlds][S]
+    const int32_t *forced_on;    // device flag
+    int32_t *nonfinite;          // host-mapped flag
 };
 
 // ------------------------------------------------------------------ Philox4x32-10
@@ -154,10 +159,23 @@ __device__ __forceinline__ uint32_t *plane_cur(const DevParams &p, int64_t t) {
 __device__ __forceinline__ uint32_t *plane_next(const DevParams &p, int64_t t) {
     return (t & 1) ? p.plane0 : p.plane1;
 }
+__device__ __forceinline__ uint32_t *bbits_of(const DevParams &p, int64_t t, int w) {
+    return p.bbits + ((size_t)(t & 1) * p.n_worlds + w) * plane_words(p);
+}
+__device__ __forceinline__ int32_t *list_of(const DevParams &p, int64_t t, int w) {
+    return p.alive_list + ((size_t)(t & 1) * p.n_worlds + w) * p.S;
+}
+__device__ __forceinline__ int32_t *count_of(const DevParams &p, int64_t t, int w) {
+    return p.n_alive + (size_t)(t & 1) * p.n_worlds + w;
+}
 
 __device__ __forceinline__ sim_step_record *record_of(const DevParams &p, int64_t t, int w) {
     return p.log + (size_t)(t % p.log_cap) * p.n_worlds + w;
 }
+
+// N, S, E, W (R13 order for moves is stay, N, S, E, W; births use N, S, E, W = 0..3)
+__device__ __forceinline__ int dir_dy(int d) { return d == 0 ? -1 : d == 1 ? 1 : 0; }
+__device__ __forceinline__ int dir_dx(int d) { return d == 2 ? 1 : d == 3 ? -1 : 0; }
 
 // ----------------------------------------------------------------- host launchers
 struct LaunchCfg {
@@ -174,6 +192,7 @@ cudaError_t launch_regrow(const DevParams &p, cudaStream_t s);
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_birth_win(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);

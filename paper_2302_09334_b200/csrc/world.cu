@@ -169,7 +169,7 @@ __global__ void k_init_agents(DevParams p, int w, int n_initial, const unsigned 
     p.last_action[gs] = 0;
     p.ate[gs] = 0;
     p.target[gs] = -1;
-    p.bcand[gs] = -1;
+
 }
 
 // initial weights w_j = (float)(std * z_j), z from INIT_W keyed by the initial cell
@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
     atomicAdd(&res_acc, local);
     __syncthreads();
     uint32_t base = 0u;
+    const int64_t t = p.t[w];
+    int32_t *list = list_of(p, t, w);
     for (int i0 = 0; i0 < p.S; i0 += blockDim.x) {
         const int i = i0 + threadIdx.x;
         const size_t gs = (size_t)w * p.S + i;
@@ -263,18 +265,18 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
             uint32_t *wp = word_ptr(O, p, p.cell[gs], bit);
             atomicOr(wp, bit);
         }
+        const uint32_t word = __ballot_sync(0xffffffffu, a != 0u);
+        if ((threadIdx.x & 31) == 0 && i < p.S) p.alive_bits[(size_t)w * p.SW + (i >> 5)] = word;
         uint32_t tot;
         const uint32_t ex = block_exclusive_scan<1024>(a, scratch, tot);
-        if (a) p.alive_list[(size_t)w * p.S + base + ex] = i;
-        if (i < p.S) {
-            p.target[gs] = -1;
-            p.bcand[gs] = -1;
-        }
+        if (a) list[base + ex] = i;
+        if (i < p.S) p.target[gs] = -1;
         base += tot;
     }
     if (threadIdx.x == 0) {
-        p.n_alive[w] = (int32_t)base;
-        p.n_cand[w] = 0;
+        *count_of(p, t, w) = (int32_t)base;
+        *count_of(p, t + 1, w) = 0;
+        p.n_win[w] = 0;
         p.n_births[w] = 0;
         p.res_count[w] = (int64_t)res_acc;
     }
