@@ -6,8 +6,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsim.so")
-SOURCES = ["api.cu", "world.cu", "agents.cu", "births.cu"]
-HEADERS = ["sim_internal.cuh", "block_scan.cuh"]
+SOURCES = ["api.cu", "world.cu", "step.cu"]
+HEADERS = ["sim_internal.cuh", "block_scan.cuh", "phases.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

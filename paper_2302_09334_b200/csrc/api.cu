@@ -129,8 +129,12 @@ struct sim_ctx {
     DevParams p{};
     eco::LaunchCfg lc{};
     bool poisoned = false;
+    // graph mode: [k_policy, k_post] per step; the first step after create/set_state is
+    // preceded by a standalone regrowth (afterwards each k_post regrows the next step).
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    bool regrown_ahead = false;
+    unsigned int *bar = nullptr;  // grid-barrier words of k_post
     int64_t t = 0;
     int32_t *nonfinite_host = nullptr;
     int32_t *forced_on_dev = nullptr;
@@ -179,11 +183,15 @@ sim_status check_nonfinite(sim_ctx *h) {
     return SIM_OK;
 }
 
-// the step's kernels in order (K1 regrow, K2 policy, K3 move, K3b birth claim,
-// K3c birth win, K4 birth rank, K5 mutate)
+// Instrumented mode: the phases of k_post as separate kernels, in k_post's order, so that
+// every kernel can be bracketed by events.  Index order of sim_step_timing.kernel_ms:
+// 0 regrow (of step t+1, as inside k_post), 1 policy, 2 move, 3 birth_claim, 4 birth_win,
+// 5 birth_rank, 6 mutate.  Launch order: policy, move, regrow, claim, win, rank, mutate.
+constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5, 6};
+
 cudaError_t launch_phase(sim_ctx *h, int k) {
     switch (k) {
-        case 0: return eco::launch_regrow(h->p, h->stream);
+        case 0: return eco::launch_regrow(h->p, 1, h->stream);
         case 1: return eco::launch_policy(h->p, h->lc, h->stream);
         case 2: return eco::launch_move(h->p, h->lc, h->stream);
         case 3: return eco::launch_birth_claim(h->p, h->lc, h->stream);
@@ -193,15 +201,19 @@ cudaError_t launch_phase(sim_ctx *h, int k) {
     }
 }
 
+// graph-mode step: the policy kernel, then the cooperative post-policy kernel
 cudaError_t enqueue_step(sim_ctx *h) {
     cudaError_t e;
-    if ((e = eco::launch_regrow(h->p, h->stream)) != cudaSuccess) return e;
     if ((e = eco::launch_policy(h->p, h->lc, h->stream)) != cudaSuccess) return e;
-    if ((e = eco::launch_move(h->p, h->lc, h->stream)) != cudaSuccess) return e;
-    if ((e = eco::launch_birth_claim(h->p, h->lc, h->stream)) != cudaSuccess) return e;
-    if ((e = eco::launch_birth_win(h->p, h->lc, h->stream)) != cudaSuccess) return e;
-    if ((e = eco::launch_birth_rank(h->p, h->stream)) != cudaSuccess) return e;
-    return eco::launch_mutate(h->p, h->lc, h->stream);
+    return eco::launch_post(h->p, h->lc, h->bar, h->stream);
+}
+
+// the regrowth of the current step, needed once after create/set_state
+cudaError_t ensure_regrown(sim_ctx *h) {
+    if (h->regrown_ahead) return cudaSuccess;
+    cudaError_t e = eco::launch_regrow(h->p, 0, h->stream);
+    if (e == cudaSuccess) h->regrown_ahead = true;
+    return e;
 }
 
 sim_status sync(sim_ctx *h) {
@@ -372,7 +384,17 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         const long cap = (long)prop.multiProcessorCount * 8;
         h->lc.agent_blocks = (int)(need < 1 ? 1 : need < cap ? need : cap);
     }
-    h->lc.mutate_blocks_y = 32;
+    {
+        int coop = 0;
+        CKC(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device), "attribute");
+        if (!coop) return bail(fail(SIM_E_CUDA, "device does not support cooperative launches"));
+        int pbs = 0;
+        CKC(eco::post_occupancy(&pbs), "occupancy");
+        if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
+        if (pbs > 4) pbs = 4;
+        h->lc.post_blocks = prop.multiProcessorCount * pbs;
+    }
+    CKC(dalloc(h, &h->bar, 2), "alloc");
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");
@@ -425,6 +447,7 @@ sim_status sim_step(sim_handle h, int64_t n) {
         h->graph = g;
         CK(h, cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
     }
+    CK(h, ensure_regrown(h), "regrow");
     for (int64_t i = 0; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
     h->t += n;
     return SIM_OK;
@@ -435,15 +458,16 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, ensure_regrown(h), "regrow");
     CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
-    for (int k = 0; k < SIM_NUM_KERNELS; ++k) {
-        CK(h, launch_phase(h, k), "step kernel");
-        CK(h, cudaEventRecord(h->ev[k + 1], h->stream), "event");
+    for (int i = 0; i < SIM_NUM_KERNELS; ++i) {
+        CK(h, launch_phase(h, kTimedOrder[i]), "step kernel");
+        CK(h, cudaEventRecord(h->ev[i + 1], h->stream), "event");
     }
     CK(h, cudaEventSynchronize(h->ev[SIM_NUM_KERNELS]), "event sync");
     h->t += 1;
-    for (int k = 0; k < SIM_NUM_KERNELS; ++k)
-        CK(h, cudaEventElapsedTime(&out->kernel_ms[k], h->ev[k], h->ev[k + 1]), "elapsed");
+    for (int i = 0; i < SIM_NUM_KERNELS; ++i)
+        CK(h, cudaEventElapsedTime(&out->kernel_ms[kTimedOrder[i]], h->ev[i], h->ev[i + 1]), "elapsed");
     CK(h, cudaEventElapsedTime(&out->step_ms, h->ev[0], h->ev[SIM_NUM_KERNELS]), "elapsed");
     return check_nonfinite(h);
 }
@@ -600,6 +624,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
+    h->regrown_ahead = false;
     return sync(h);
 }
 

@@ -1,0 +1,501 @@
+// phases.cuh — the phases of one world step as device functions, shared by the
+// standalone kernels (instrumented mode) and the fused cooperative k_post (graph mode).
+//
+//   regrow_word        a1  one 32-cell word of the grid (step index given explicitly)
+//   move_agent         a4  claim resolution, movement, consumption, physiology, death
+//   birth_claim_agent  a5  lazy move-claim reset, birth candidate direction
+//   birth_win_agent    a5  declarative birth-claim resolution, birth bitmap
+//   birth_rank_world   a5  (one block) free slots, winner ranks, placement, counters, t += 1
+//   mutate_item        a5  one canonical weight group of one child
+//
+// Data written by one phase and read by a later phase of the same kernel is read with
+// plain (coherent) loads, never through the read-only path.
+#pragma once
+#include "block_scan.cuh"
+#include "sim_internal.cuh"
+
+namespace eco {
+
+// ------------------------------------------------------------------ grid barrier
+// Generation barrier over all blocks of a cooperatively launched grid (co-residency is
+// guaranteed by the cooperative launch).  bar[0] = arrivals, bar[1] = generation.
+__device__ __forceinline__ void grid_sync(unsigned int *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int *vgen = bar + 1;
+        const unsigned int gen = *vgen;
+        __threadfence();
+        const unsigned int nblocks = gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*vgen == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t ld_plain(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
+
+// ----------------------------------------------------------------------- a1 regrow
+// each empty cell grows with p = lat(y)*f(k) + c, k = resources in the
+// Euclidean radius-r disc (centre excluded) of the START-of-step grid (synchronous),
+// drawn as philox(REGROW, t, cell>>2)[cell&3] < T[y][class(k)].  Full cells stay full.
+// The 12 (generally n_off <= 24) neighbour bit-vectors are funnel-shifted words of rows
+// y-2..y+2; k is accumulated bit-sliced (5 planes), ~10 logic ops per neighbour per 32
+// cells.  Philox runs only for 4-cell groups holding an empty cell (exact: draws are keyed
+// by cell, not by sequence).
+__device__ __forceinline__ uint32_t shifted_word(uint32_t prv, uint32_t cur, uint32_t nxt, int dx) {
+    if (dx > 0) return __funnelshift_r(cur, nxt, dx);
+    if (dx < 0) return __funnelshift_l(prv, cur, -dx);
+    return cur;
+}
+
+__device__ __forceinline__ uint32_t ge_const(const uint32_t c[5], int m) {
+    if (m <= 0) return 0xffffffffu;
+    if (m >= 32) return 0u;
+    uint32_t gt = 0u, eq = 0xffffffffu;
+#pragma unroll
+    for (int i = 4; i >= 0; --i) {
+        if ((m >> i) & 1) {
+            eq &= c[i];
+        } else {
+            gt |= eq & c[i];
+            eq &= ~c[i];
+        }
+    }
+    return gt | eq;
+}
+
+// Regrow word (y, wx) of world w for step `t`: src = plane_cur(t), dst = plane_next(t).
+// Returns the number of cells grown.
+__device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int wx, int64_t t) {
+    const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
+    uint32_t *dst = plane_next(p, t) + (size_t)w * plane_words(p);
+    uint32_t win[5][3];
+#pragma unroll
+    for (int dy = -2; dy <= 2; ++dy) {
+        const int yy = y + dy;
+#pragma unroll
+        for (int dw = -1; dw <= 1; ++dw) {
+            const int ww = wx + dw;
+            win[dy + 2][dw + 1] =
+                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
+        }
+    }
+    const uint32_t cur = win[2][1];
+    uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
+    for (int o = 0; o < p.n_off; ++o) {
+        const int dy = p.off_dy[o], dx = p.off_dx[o];
+        uint32_t prv, cen, nxt;
+        switch (dy) {  // dy in [-2, 2] (validated r2 <= 8)
+            case -2: prv = win[0][0]; cen = win[0][1]; nxt = win[0][2]; break;
+            case -1: prv = win[1][0]; cen = win[1][1]; nxt = win[1][2]; break;
+            case 0: prv = win[2][0]; cen = win[2][1]; nxt = win[2][2]; break;
+            case 1: prv = win[3][0]; cen = win[3][1]; nxt = win[3][2]; break;
+            default: prv = win[4][0]; cen = win[4][1]; nxt = win[4][2]; break;
+        }
+        uint32_t cy = shifted_word(prv, cen, nxt, dx), tt;
+        tt = c[0] & cy; c[0] ^= cy; cy = tt;
+        tt = c[1] & cy; c[1] ^= cy; cy = tt;
+        tt = c[2] & cy; c[2] ^= cy; cy = tt;
+        tt = c[3] & cy; c[3] ^= cy; cy = tt;
+        c[4] ^= cy;
+    }
+    const uint32_t ge1 = ge_const(c, p.cls_k1), ge2 = ge_const(c, p.cls_k2), ge3 = ge_const(c, p.cls_k3);
+    const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
+    const uint64_t seed = p.seeds[w];
+    const int x_base = wx << 5;
+    uint32_t grow = 0u;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const int x0 = x_base + 4 * g;
+        if (x0 >= p.W) break;
+        if (((cur >> (4 * g)) & 0xFu) == 0xFu) continue;  // all four cells full: no draw needed
+        const uint32_t entity = (uint32_t)(((int64_t)y * p.W + x0) >> 2);
+        const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)t, entity, 0u);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int b = 4 * g + m;
+            if ((cur >> b) & 1u) continue;
+            const int cls = (int)((ge1 >> b) & 1u) + (int)((ge2 >> b) & 1u) + (int)((ge3 >> b) & 1u);
+            const uint32_t thr = cls == 0 ? Trow.x : cls == 1 ? Trow.y : cls == 2 ? Trow.z : Trow.w;
+            if (word_of(d, m) < thr) grow |= 1u << b;
+        }
+    }
+    dst[(size_t)y * p.WW + wx] = cur | grow;
+    return __popc(grow);
+}
+
+// Grid-stride regrowth of every world for step t_of(w) = p.t[w] + ahead; one atomic per
+// warp on the world's record (warp-uniform world check).
+__device__ __forceinline__ void regrow_phase(const DevParams &p, int ahead, size_t gtid, size_t gthreads) {
+    const int real_words = (p.W + 31) >> 5;
+    const size_t per_world = (size_t)p.H * real_words;
+    const size_t total = per_world * p.n_worlds;
+    for (size_t base = gtid - (gtid & 31); base < total; base += gthreads) {
+        const size_t k = base + (gtid & 31);
+        int w = 0, cnt = 0;
+        int64_t t = 0;
+        if (k < total) {
+            w = (int)(k / per_world);
+            const size_t r = k - (size_t)w * per_world;
+            const int y = (int)(r / real_words), wx = (int)(r - (size_t)y * real_words);
+            t = p.t[w] + ahead;
+            cnt = regrow_word(p, w, y, wx, t);
+        }
+        const int w0 = __shfl_sync(0xffffffffu, w, 0);
+        if (__all_sync(0xffffffffu, w == w0)) {
+            unsigned s = (unsigned)cnt;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if ((gtid & 31) == 0 && s)
+                atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, p.t[w0] + ahead, w0)->grown),
+                          (unsigned long long)s);
+        } else if (cnt) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->grown), (unsigned long long)cnt);
+        }
+    }
+}
+
+// ------------------------------------------------------------------- agent iteration
+struct AgentIter {
+    int w, i;
+    bool in_range;
+};
+__device__ __forceinline__ AgentIter agent_at(const DevParams &p, long v) {
+    AgentIter a;
+    a.in_range = v < (long)p.n_worlds * p.S;
+    a.w = a.in_range ? (int)(v / p.S) : 0;
+    a.i = a.in_range ? (int)(v - (long)a.w * p.S) : 0;
+    return a;
+}
+
+__device__ __forceinline__ void warp_count_add(unsigned long long *dst, bool flag) {
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(dst, (unsigned long long)__popc(m));
+}
+
+// ----------------------------------------------------------------------- a4 move
+// An agent moves iff it holds the max key on its target (R14); every live agent eats the
+// resource under its final cell; fixed-point energy e += gain*ate - decay,
+// age += 1, repr = e > thr ? repr+1 : 0 (R16, R17, R19); death iff e <= 0 (cause energy)
+// or age > max_age (cause age) (R18).  O is updated in place with bit atomics; distinct
+// agents touch distinct bits.  Survivors are appended to the step-(t+1) list (order is
+// irrelevant to every result).  Must be called by all 32 lanes of a warp.
+__device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size_t gthreads) {
+    const long total = (long)p.n_worlds * p.S;
+    const size_t HW = (size_t)p.H * p.W;
+    const unsigned lane = gtid & 31;
+    for (long base = (long)(gtid - lane); base < total; base += (long)gthreads) {
+        const AgentIter it = agent_at(p, base + lane);
+        const int w = it.w;
+        const int64_t t = p.t[w];
+        const bool active = it.in_range && it.i < *count_of(p, t, w);
+        bool ate = false, died_e = false, died_a = false, survive = false;
+        int slot = 0;
+        if (active) {
+            slot = list_of(p, t, w)[it.i];
+            const size_t gs = (size_t)w * p.S + slot;
+            uint32_t *O = p.occ + (size_t)w * plane_words(p);
+            uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
+            int cellv = p.cell[gs];
+            const int tg = p.target[gs];
+            uint32_t bit;
+            if (tg >= 0 && p.claim[(size_t)w * HW + tg] == p.mkey[gs]) {
+                atomicAnd(word_ptr(O, p, cellv, bit), ~bit);
+                atomicOr(word_ptr(O, p, tg, bit), bit);
+                cellv = tg;
+                p.cell[gs] = tg;
+            }
+            uint32_t *rw = word_ptr(Rn, p, cellv, bit);
+            if (ld_plain(rw) & bit) {
+                atomicAnd(rw, ~bit);
+                ate = true;
+            }
+            p.ate[gs] = ate ? 1 : 0;
+            long long e = (long long)p.energy[gs] + (ate ? (long long)p.e_gain : 0ll) - (long long)p.e_decay;
+            if (p.e_max != 0x7fffffff && e > p.e_max) e = p.e_max;
+            const int en = (int)e;
+            const int ag = p.age[gs] + 1;
+            p.energy[gs] = en;
+            p.age[gs] = ag;
+            p.repr[gs] = en > p.e_repr_gt ? p.repr[gs] + 1 : 0;
+            if (en <= p.e_death_le) died_e = true;
+            else if (ag > p.max_age) died_a = true;
+            if (died_e || died_a) {
+                p.alive[gs] = 0;
+                atomicAnd(word_ptr(O, p, cellv, bit), ~bit);
+                atomicAnd(p.alive_bits + (size_t)w * p.SW + (slot >> 5), ~(1u << (slot & 31)));
+            } else {
+                survive = true;
+            }
+        }
+        const int w0 = __shfl_sync(0xffffffffu, w, 0);
+        if (__all_sync(0xffffffffu, w == w0)) {
+            const int64_t t0 = p.t[w0];
+            sim_step_record *rec = record_of(p, t0, w0);
+            warp_count_add(reinterpret_cast<unsigned long long *>(&rec->eaten), ate);
+            warp_count_add(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), died_e);
+            warp_count_add(reinterpret_cast<unsigned long long *>(&rec->deaths_age), died_a);
+            const unsigned m = __ballot_sync(0xffffffffu, survive);
+            int pos0 = 0;
+            if (lane == 0 && m) pos0 = atomicAdd(count_of(p, t0 + 1, w0), __popc(m));
+            pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+            if (survive) list_of(p, t + 1, w)[pos0 + __popc(m & ((1u << lane) - 1u))] = slot;
+        } else {
+            sim_step_record *rec = record_of(p, t, w);
+            if (ate) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), 1ull);
+            if (died_e) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), 1ull);
+            if (died_a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), 1ull);
+            if (survive) list_of(p, t + 1, w)[atomicAdd(count_of(p, t + 1, w), 1)] = slot;
+        }
+    }
+}
+
+// ----------------------------------------------------------------- a5 birth claim
+// Lazy reset of this step's move claims (every claimant clears its own target; safe
+// because the move phase has finished reading them).  Then every live parent with repr >=
+// T_repr picks the first cell of a Philox-rotated (N, S, E, W) order that is
+// in-grid, agent-free after moves/deaths (O'') and resource-free after consumption (R'')
+// (R21), and records the direction on its own cell (bdir; NO_DIR when it has none).
+__device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads) {
+    const long total = (long)p.n_worlds * p.S;
+    const size_t HW = (size_t)p.H * p.W;
+    for (long v = (long)gtid; v < total; v += (long)gthreads) {
+        const AgentIter it = agent_at(p, v);
+        const int w = it.w;
+        const int64_t t = p.t[w];
+        if (it.i >= *count_of(p, t, w)) continue;
+        const int slot = list_of(p, t, w)[it.i];
+        const size_t gs = (size_t)w * p.S + slot;
+        const int tg = p.target[gs];
+        if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;
+        if (!p.alive[gs]) continue;
+        const int cellv = p.cell[gs];
+        uint8_t dir = NO_DIR;
+        if (p.repr[gs] >= p.repr_steps) {
+            const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+            const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
+            const int y = cellv / p.W, x = cellv - y * p.W;
+            const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+            const int s0 = (int)(d.x & 3u);
+            for (int kk = 0; kk < 4; ++kk) {
+                const int dd = (s0 + kk) & 3;
+                const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
+                if (cy < 0 || cy >= p.H || cx < 0 || cx >= p.W) continue;
+                const int c = cy * p.W + cx;
+                if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
+                dir = (uint8_t)dd;
+                break;
+            }
+            if (dir == NO_DIR)
+                atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_no_cell), 1ull);
+        }
+        p.bdir[(size_t)w * HW + cellv] = dir;
+    }
+}
+
+// ------------------------------------------------------------------- a5 birth win
+// Claim resolution without atomics: the parent on cell p whose candidate is c wins iff its
+// key (BIRTH w1 << 32 | ~p) exceeds the key of every other live parent adjacent to c that
+// chose c (read from bdir of c's other neighbours, valid where O'' is set).  The winner
+// marks c in the birth bitmap and records itself as c's parent.
+__device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t, int cellv) {
+    const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+    return ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
+}
+
+__device__ __forceinline__ void birth_win_phase(const DevParams &p, size_t gtid, size_t gthreads) {
+    const long total = (long)p.n_worlds * p.S;
+    const size_t HW = (size_t)p.H * p.W;
+    for (long v = (long)gtid; v < total; v += (long)gthreads) {
+        const AgentIter it = agent_at(p, v);
+        const int w = it.w;
+        const int64_t t = p.t[w];
+        if (it.i >= *count_of(p, t, w)) continue;
+        const int slot = list_of(p, t, w)[it.i];
+        const size_t gs = (size_t)w * p.S + slot;
+        if (!p.alive[gs]) continue;
+        const int pc = p.cell[gs];
+        const uint8_t *bd = p.bdir + (size_t)w * HW;
+        const int d = bd[pc];
+        if (d == NO_DIR) continue;
+        const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+        const int py = pc / p.W, px = pc - py * p.W;
+        const int cy = py + dir_dy(d), cx = px + dir_dx(d);
+        const int c = cy * p.W + cx;
+        const uint64_t seed = p.seeds[w];
+        const unsigned long long kp = birth_key(seed, t, pc);
+        bool win = true;
+        for (int dq = 0; dq < 4 && win; ++dq) {
+            const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
+            if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
+            const int q = qy * p.W + qx;
+            if (q == pc || !get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
+            if (birth_key(seed, t, q) > kp) win = false;
+        }
+        if (win) {
+            uint32_t bit;
+            atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
+            p.bparent[(size_t)w * HW + c] = slot;
+            atomicAdd(p.n_win + w, 1);
+        } else {
+            atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_claim), 1ull);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ a5 birth rank
+// One block per world: the first n_place = min(winners, free slots) free slots in
+// ascending order (prefix scan of the alive bitmap) and the first n_place winning child
+// cells in row-major order (prefix scan of the birth bitmap); both scans stop once
+// n_place entries are found.  Rank r gets free slot F[r] (R22); later winners are deferred
+// for capacity.  Then the step's counters, the next alive count and t += 1.
+template <int NT>
+__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch) {
+    const int tid = threadIdx.x;
+    const int64_t t = p.t[w];
+    const size_t HW = (size_t)p.H * p.W;
+    const size_t pw = plane_words(p);
+    const int n_start = *count_of(p, t, w);
+    const int n_surv = *reinterpret_cast<volatile int32_t *>(count_of(p, t + 1, w));
+    const int n_win = *reinterpret_cast<volatile int32_t *>(p.n_win + w);
+    const int n_free = p.S - n_surv;
+    const int n_place = n_win < n_free ? n_win : n_free;
+    uint32_t *O = p.occ + (size_t)w * pw;
+    int32_t *next_list = list_of(p, t + 1, w);
+
+    if (n_place > 0) {
+        uint32_t running = 0u;
+        for (int w0 = 0; w0 < p.SW; w0 += NT) {
+            const int wi = w0 + tid;
+            uint32_t fr = 0u;
+            if (wi < p.SW) {
+                const int nbits = p.S - wi * 32;
+                const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
+                fr = ~ld_plain(p.alive_bits + (size_t)w * p.SW + wi) & valid;
+            }
+            uint32_t tot;
+            const uint32_t ex = block_exclusive_scan<NT>((uint32_t)__popc(fr), scratch, tot);
+            uint32_t r = running + ex;
+            while (fr && r < (uint32_t)n_place) {
+                const int b = __ffs(fr) - 1;
+                fr &= fr - 1u;
+                p.free_list[(size_t)w * p.S + r] = wi * 32 + b;
+                ++r;
+            }
+            running += tot;
+            if (running >= (uint32_t)n_place) break;
+        }
+        __syncthreads();
+        const uint32_t *bb = bbits_of(p, t, w);
+        running = 0u;
+        for (size_t w0 = 0; w0 < pw; w0 += NT) {
+            const size_t wi = w0 + tid;
+            uint32_t word = wi < pw ? ld_plain(bb + wi) : 0u;
+            uint32_t tot;
+            const uint32_t ex = block_exclusive_scan<NT>((uint32_t)__popc(word), scratch, tot);
+            uint32_t r = running + ex;
+            while (word && r < (uint32_t)n_place) {
+                const int b = __ffs(word) - 1;
+                word &= word - 1u;
+                const int y = (int)(wi / p.WW), x = (int)(wi - (size_t)y * p.WW) * 32 + b;
+                const int c = y * p.W + x;
+                const int parent = *reinterpret_cast<volatile int32_t *>(p.bparent + (size_t)w * HW + c);
+                const int child = *reinterpret_cast<volatile int32_t *>(p.free_list + (size_t)w * p.S + r);
+                const size_t cs = (size_t)w * p.S + child;
+                p.alive[cs] = 1;
+                atomicOr(p.alive_bits + (size_t)w * p.SW + (child >> 5), 1u << (child & 31));
+                p.cell[cs] = c;
+                p.energy[cs] = p.e_init;
+                p.age[cs] = 0;
+                p.repr[cs] = 0;
+                p.last_action[cs] = 0;
+                p.ate[cs] = 0;
+                for (int k = 0; k < p.Hd; ++k) {
+                    p.h[cs * p.Hd + k] = 0.f;
+                    p.c[cs * p.Hd + k] = 0.f;
+                }
+                for (int a = 0; a < LOGIT_STRIDE; ++a) p.logits[cs * LOGIT_STRIDE + a] = 0.f;
+                p.target[cs] = -1;
+                uint32_t bit;
+                atomicOr(word_ptr(O, p, c, bit), bit);
+                p.repr[(size_t)w * p.S + parent] = 0;
+                p.birth_child[(size_t)w * p.S + r] = child;
+                p.birth_parent[(size_t)w * p.S + r] = parent;
+                next_list[n_surv + r] = child;
+                ++r;
+            }
+            running += tot;
+            if (running >= (uint32_t)n_place) break;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        volatile sim_step_record *rec = record_of(p, t, w);
+        const int64_t deaths = rec->deaths_energy + rec->deaths_age;
+        const int64_t grown = rec->grown, eaten = rec->eaten;
+        p.res_count[w] += grown - eaten;
+        rec->t = t;
+        rec->agents_at_start = n_start;
+        rec->births = n_place;
+        rec->deferred_capacity = n_win - n_place;
+        rec->population = n_surv + n_place;
+        rec->resources = p.res_count[w];
+        *count_of(p, t + 1, w) = n_surv + n_place;
+        p.n_births[w] = n_place;
+        unsigned long long *tot = p.totals;
+        if (w == 0) atomicAdd(tot + 0, 1ull);
+        atomicAdd(tot + 1, (unsigned long long)n_start);
+        atomicAdd(tot + 2, (unsigned long long)HW);
+        atomicAdd(tot + 3, (unsigned long long)n_place);
+        atomicAdd(tot + 4, (unsigned long long)deaths);
+        atomicAdd(tot + 5, (unsigned long long)eaten);
+        atomicAdd(tot + 6, (unsigned long long)grown);
+        p.t[w] = t + 1;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------- a5 mutation
+// "an agent's weights are mutated by adding noise sampled from N(0, sigma)",
+// sigma = 0.02 a standard deviation (R23).  One item = one canonical group q = j >> 2 of
+// one child: one Philox call, two fp64 Box-Muller pairs, four weights.  Runs after the
+// rank phase advanced t, so the step of the birth is p.t[w] - 1.
+__device__ __forceinline__ void mutate_item(const DevParams &p, int w, int b, int q) {
+    const int64_t t = p.t[w] - 1;
+    const int child = p.birth_child[(size_t)w * p.S + b];
+    const int parent = p.birth_parent[(size_t)w * p.S + b];
+    const size_t cs = (size_t)w * p.S + child, ps = (size_t)w * p.S + parent;
+    const uint4 d = draw4(p.seeds[w], PURPOSE_MUTATE, (uint32_t)t, (uint32_t)p.cell[cs], (uint32_t)q);
+    double z[4];
+    box_muller(d.x, d.y, z[0], z[1]);
+    box_muller(d.z, d.w, z[2], z[3]);
+    const float *wp = p.weights + ps * (size_t)p.Pd;
+    float *wc = p.weights + cs * (size_t)p.Pd;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int j = 4 * q + m;
+        if (j >= p.P) break;
+        const int dd = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
+        wc[dd] = __fadd_rn(wp[dd], __double2float_rn(__dmul_rn(p.mutation_std, z[m])));
+    }
+}
+
+// All mutation items of all worlds: grid-stride over (birth, group) items world by world.
+__device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
+    const int groups = (p.P + 3) >> 2;
+    for (int w = 0; w < p.n_worlds; ++w) {
+        const size_t n = (size_t)(*reinterpret_cast<volatile int32_t *>(p.n_births + w)) * groups;
+        for (size_t k = gtid; k < n; k += gthreads) {
+            const int b = (int)(k / groups), q = (int)(k - (size_t)b * groups);
+            mutate_item(p, w, b, q);
+        }
+    }
+}
+
+}  // namespace eco

@@ -181,14 +181,14 @@ __device__ __forceinline__ int dir_dx(int d) { return d == 2 ? 1 : d == 3 ? -1 :
 struct LaunchCfg {
     int policy_blocks, policy_threads;
     int agent_blocks, agent_threads;
-    int mutate_blocks_y;
+    int post_blocks;  // co-resident blocks of the cooperative k_post
 };
 
 cudaError_t launch_init_resources(const DevParams &p, cudaStream_t s);
 size_t init_agents_scratch_bytes(const DevParams &p);
 cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
-cudaError_t launch_regrow(const DevParams &p, cudaStream_t s);
+cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
@@ -196,6 +196,8 @@ cudaError_t launch_birth_win(const DevParams &p, const LaunchCfg &lc, cudaStream
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
+cudaError_t post_occupancy(int *blocks_per_sm);
+cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned int *bar, cudaStream_t s);
 
 // state conversion (canonical <-> device)
 cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);

@@ -1,125 +1,11 @@
-// world.cu — grid-side kernels: K1 regrowth (step row a1), world initialisation, the
-// occupancy/list rebuild used by create and set_state, and resource-plane conversion.
+// world.cu — world initialisation (K0), the occupancy/list rebuild used by create and
+// set_state, and the canonical <-> device state conversions.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "block_scan.cuh"
 #include "sim_internal.cuh"
 
 namespace eco {
-
-// --------------------------------------------------------------------------- K1 regrow
-// each empty cell grows with p = lat(y)*f(k) + c, k = resources in the
-// Euclidean radius-r disc (centre excluded) of the START-of-step grid (synchronous),
-// drawn as philox(REGROW, t, cell>>2)[cell&3] < T[y][class(k)].  Full cells stay full.
-//
-// One thread per 32-cell word.  The 12 (generally n_off <= 24) neighbour bit-vectors are
-// funnel-shifted words of rows y-2..y+2; k is accumulated bit-sliced (5 planes), so the
-// stencil costs ~10 LOP3/IADD per neighbour per 32 cells.  Philox runs only for 4-cell
-// groups holding an empty cell (exact: draws are keyed by cell, not by sequence).
-__device__ __forceinline__ uint32_t shifted_word(uint32_t prv, uint32_t cur, uint32_t nxt, int dx) {
-    // bit b of the result = bit (b + dx) of the row around word `cur`
-    if (dx > 0) return __funnelshift_r(cur, nxt, dx);
-    if (dx < 0) return __funnelshift_l(prv, cur, -dx);
-    return cur;
-}
-
-__device__ __forceinline__ uint32_t ge_const(const uint32_t c[5], int m) {
-    if (m <= 0) return 0xffffffffu;
-    if (m >= 32) return 0u;
-    uint32_t gt = 0u, eq = 0xffffffffu;
-#pragma unroll
-    for (int i = 4; i >= 0; --i) {
-        if ((m >> i) & 1) {
-            eq &= c[i];
-        } else {
-            gt |= eq & c[i];
-            eq &= ~c[i];
-        }
-    }
-    return gt | eq;
-}
-
-__global__ void __launch_bounds__(256) k_regrow(DevParams p) {
-    const int wx = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    const int w = blockIdx.z;
-    const int real_words = (p.W + 31) >> 5;
-    const int64_t t = p.t[w];
-    uint32_t grow = 0u;
-    if (wx < real_words && y < p.H) {
-        const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
-        uint32_t *dst = plane_next(p, t) + (size_t)w * plane_words(p);
-        // 5 rows x 3 words around (y, wx)
-        uint32_t win[5][3];
-#pragma unroll
-        for (int dy = -2; dy <= 2; ++dy) {
-            const int yy = y + dy;
-#pragma unroll
-            for (int dw = -1; dw <= 1; ++dw) {
-                const int ww = wx + dw;
-                win[dy + 2][dw + 1] =
-                    (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? __ldg(src + (size_t)yy * p.WW + ww) : 0u;
-            }
-        }
-        const uint32_t cur = win[2][1];
-        uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
-        for (int o = 0; o < p.n_off; ++o) {
-            const int dy = p.off_dy[o], dx = p.off_dx[o];
-            uint32_t prv, cen, nxt;
-            // dy in [-2, 2] (validated r2 <= 8)
-            switch (dy) {
-                case -2: prv = win[0][0]; cen = win[0][1]; nxt = win[0][2]; break;
-                case -1: prv = win[1][0]; cen = win[1][1]; nxt = win[1][2]; break;
-                case 0: prv = win[2][0]; cen = win[2][1]; nxt = win[2][2]; break;
-                case 1: prv = win[3][0]; cen = win[3][1]; nxt = win[3][2]; break;
-                default: prv = win[4][0]; cen = win[4][1]; nxt = win[4][2]; break;
-            }
-            uint32_t cy = shifted_word(prv, cen, nxt, dx), tt;
-            tt = c[0] & cy; c[0] ^= cy; cy = tt;
-            tt = c[1] & cy; c[1] ^= cy; cy = tt;
-            tt = c[2] & cy; c[2] ^= cy; cy = tt;
-            tt = c[3] & cy; c[3] ^= cy; cy = tt;
-            c[4] ^= cy;
-        }
-        const uint32_t ge1 = ge_const(c, p.cls_k1), ge2 = ge_const(c, p.cls_k2), ge3 = ge_const(c, p.cls_k3);
-        const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
-        const uint64_t seed = p.seeds[w];
-        const int x_base = wx << 5;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            const int x0 = x_base + 4 * g;
-            if (x0 >= p.W) break;
-            if (((cur >> (4 * g)) & 0xFu) == 0xFu) continue;  // all four cells full: no draw needed
-            const uint32_t entity = (uint32_t)(((int64_t)y * p.W + x0) >> 2);
-            const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)t, entity, 0u);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int b = 4 * g + m;
-                if ((cur >> b) & 1u) continue;
-                const int cls = (int)((ge1 >> b) & 1u) + (int)((ge2 >> b) & 1u) + (int)((ge3 >> b) & 1u);
-                const uint32_t thr = cls == 0 ? Trow.x : cls == 1 ? Trow.y : cls == 2 ? Trow.z : Trow.w;
-                if (word_of(d, m) < thr) grow |= 1u << b;
-            }
-        }
-        dst[(size_t)y * p.WW + wx] = cur | grow;
-    }
-    // grown count: warp reduce then one atomic per warp
-    unsigned cnt = __popc(grow);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0 && cnt) {
-        sim_step_record *rec = record_of(p, p.t[w], w);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&rec->grown), (unsigned long long)cnt);
-    }
-}
-
-cudaError_t launch_regrow(const DevParams &p, cudaStream_t s) {
-    const int real_words = (p.W + 31) >> 5;
-    dim3 block(real_words >= 32 ? 32 : 16, real_words >= 32 ? 8 : 16);
-    dim3 grid((real_words + block.x - 1) / block.x, (p.H + block.y - 1) / block.y, p.n_worlds);
-    k_regrow<<<grid, block, 0, s>>>(p);
-    return cudaGetLastError();
-}
 
 // ---------------------------------------------------------------- K0 initialisation
 // R[cell] = philox(INIT_RES, 0, cell>>2)[cell&3] < floor(rho * 2^32)
