@@ -208,6 +208,7 @@ def run_ours(args, rank, world_size, local_rank):
         barrier()
         clk = clocks.stop()
         world.synchronize()
+        post_phases = {k_: v / K / 1e3 for k_, v in world.phase_ns().items()}
         step_ms = np.array([a.elapsed_time(b) for a, b in evs], np.float64)
         total_ms = float(step_ms.sum())
         log = world.step_log(t0, K)
@@ -279,7 +280,8 @@ def run_ours(args, rank, world_size, local_rank):
                        else "single GPU", "global_batch": wc.slots * world_size},
             "cell_updates_per_s": cells * world_size / (max_ms / 1e3),
             "agents_mean": agents / K,
-            "gpu_launches": sim.NUM_KERNELS * K,
+            "gpu_launches": 2 * K,
+            "post_phase_us_per_step": post_phases,
             "clocks": clk,
         }
         if kern is not None:

@@ -357,6 +357,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.res_count, nw), "alloc");
     CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");
     CKC(dalloc(h, &p.totals, 8), "alloc");
+    CKC(dalloc(h, &p.phase_ns, SIM_NUM_POST_PHASES), "alloc");
     CKC(dalloc(h, &h->forced_dev, nw * S), "alloc");
     CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
     p.seeds = seeds_d;
@@ -659,6 +660,17 @@ sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_rec
         CK(h, cudaMemcpyAsync(out + i * nw, h->p.log + (size_t)(step % h->d.log_cap) * nw, nw * sizeof(sim_step_record),
                               cudaMemcpyDeviceToHost, h->stream), "log");
     }
+    return sync(h);
+}
+
+sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (out)
+        CK(h, cudaMemcpyAsync(out, h->p.phase_ns, SIM_NUM_POST_PHASES * 8, cudaMemcpyDeviceToHost, h->stream),
+           "phase clock");
+    if (reset) CK(h, cudaMemsetAsync(h->p.phase_ns, 0, SIM_NUM_POST_PHASES * 8, h->stream), "phase clock");
     return sync(h);
 }
 

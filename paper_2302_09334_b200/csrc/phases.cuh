@@ -40,6 +40,12 @@ __device__ __forceinline__ void grid_sync(unsigned int *bar) {
 
 __device__ __forceinline__ uint32_t ld_plain(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ----------------------------------------------------------------------- a1 regrow
 // each empty cell grows with p = lat(y)*f(k) + c, k = resources in the
 // Euclidean radius-r disc (centre excluded) of the START-of-step grid (synchronous),

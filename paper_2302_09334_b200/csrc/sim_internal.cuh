@@ -63,6 +63,7 @@ struct DevParams {
     int64_t *res_count;          // [n_worlds] resources at step start
     sim_step_record *log;        // [log_cap][n_worlds]
     unsigned long long *totals;  // [7] sim_totals order
+    unsigned long long *phase_ns;  // [SIM_NUM_POST_PHASES] k_post phase clock (block 0)
     const uint8_t *forced;       // [n_worlds][S]
     const int32_t *forced_on;    // device flag
     int32_t *nonfinite;          // host-mapped flag

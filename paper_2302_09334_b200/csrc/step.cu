@@ -288,16 +288,24 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned int
     __shared__ uint32_t scratch[POST_THREADS / 32 + 1];
     const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
+    // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
+    const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
+    uint64_t t0 = clk ? globaltimer_ns() : 0ull, t1;
     move_phase(p, gtid, gthreads);
     grid_sync(bar);
+    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 0, t1 - t0); t0 = t1; }
     regrow_phase(p, 1, gtid, gthreads);  // step t+1's regrowth, off the critical path
     birth_claim_phase(p, gtid, gthreads);
     grid_sync(bar);
+    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 1, t1 - t0); t0 = t1; }
     birth_win_phase(p, gtid, gthreads);
     grid_sync(bar);
+    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 2, t1 - t0); t0 = t1; }
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<POST_THREADS>(p, w, scratch);
     grid_sync(bar);
+    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 3, t1 - t0); t0 = t1; }
     mutate_phase(p, gtid, gthreads);
+    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 4, t1 - t0); }
 }
 
 // --------------------------------------------------------------------------- launchers
@@ -335,7 +343,7 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
 
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
-    k_mutate<<<lc.agent_blocks, 256, 0, s>>>(p);
+    k_mutate<<<lc.post_blocks, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 

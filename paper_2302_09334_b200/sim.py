@@ -26,7 +26,8 @@ KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_win", "birth_r
 
 EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
-            "sim_step_timed", "sim_synchronize", "sim_kernels_per_step")
+            "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns")
+POST_PHASES = ("move", "regrow_next+birth_claim", "birth_win", "birth_rank", "mutate")
 
 
 class SimError(RuntimeError):
@@ -109,6 +110,7 @@ def lib():
             L.sim_step_timed.argtypes = [H, ctypes.POINTER(SimStepTiming)]
             L.sim_synchronize.argtypes = [H]
             L.sim_kernels_per_step.restype = ctypes.c_int32
+            L.sim_get_phase_ns.argtypes = [H, ctypes.c_void_p, ctypes.c_int32]
             for f in EXPORTED:
                 if f not in ("sim_last_error", "sim_kernels_per_step"):
                     getattr(L, f).restype = ctypes.c_int
@@ -280,6 +282,12 @@ class World:
         out = np.zeros((n, self.n_worlds), RECORD_DTYPE)
         _check(lib().sim_get_step_log(self._h, int(first), int(n), _ptr(out)))
         return out
+
+    def phase_ns(self, reset: bool = False) -> dict:
+        """Summed k_post phase durations (ns, block-0 view) since the last reset."""
+        out = np.zeros(len(POST_PHASES), np.int64)
+        _check(lib().sim_get_phase_ns(self._h, _ptr(out), int(reset)))
+        return dict(zip(POST_PHASES, out.tolist()))
 
     def totals(self) -> dict:
         tt = SimTotals()

@@ -13,12 +13,12 @@ timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo 
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   CMD="python bench.py --steps 30 --warmup 300 --no-e2e --no-cpu-baseline --no-replay"
   timeout 300 $CMD > $OUT/plain_$TAG.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(regrow|policy|move|birth|mutate)" \
-      -s 1806 -c 120 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(regrow|policy|post|move|birth|mutate)" \
+      -s ${NCU_SKIP:-602} -c 60 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
   echo ncu_launch=$? >> $OUT/status.txt
   timeout 300 $CMD > $OUT/plain2_$TAG.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_policy -s 300 -c 2 \
-      -o $OUT/prof_policy_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_policy} -s 300 -c 2 \
+      -o $OUT/prof_${NCU_KERNEL:-k_policy}_$TAG $CMD > $OUT/ncu_full_$TAG.log 2>&1
   echo ncu_full=$? >> $OUT/status.txt
 fi
 cat $OUT/status.txt
