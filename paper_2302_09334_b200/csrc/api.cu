@@ -111,7 +111,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * (size_t)d.Hd * 4 * 2;     // h, c
     b += nw * S * eco::LOGIT_STRIDE * 4;    // logits
     b += nw * S * (size_t)d.Pd * 4;         // weights
-    b += nw * S * (4 + 8);                  // target, mkey
+    b += nw * S * 16 + 2 * nw * d.H * 4;    // move records, row winner counts
     b += nw * S * 4 * 5;                    // alive lists [2], free, birth lists
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
@@ -345,8 +345,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.c, nw * S * d.Hd), "alloc");
     CKC(dalloc(h, &p.logits, nw * S * eco::LOGIT_STRIDE), "alloc");
     CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
-    CKC(dalloc(h, &p.target, nw * S), "alloc");
-    CKC(dalloc(h, &p.mkey, nw * S), "alloc");
+    CKC(dalloc(h, &p.mrec, nw * S), "alloc");
+    CKC(dalloc(h, &p.row_wins, 2 * nw * (size_t)d.H), "alloc");
     CKC(dalloc(h, &p.alive_list, 2 * nw * S), "alloc");
     CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
     CKC(dalloc(h, &p.n_win, nw), "alloc");
@@ -371,7 +371,6 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     threshold_table(cfg, T);
     CKC(cudaMemcpyAsync(T_d, T.data(), T.size() * 4, cudaMemcpyHostToDevice, h->stream), "upload T");
     CKC(cudaMemcpyAsync(seeds_d, h->seeds.data(), nw * 8, cudaMemcpyHostToDevice, h->stream), "upload seeds");
-    if (S) CKC(cudaMemsetAsync(p.target, 0xff, nw * S * 4, h->stream), "memset");
 
     // launch configuration: persistent-style grids sized to the 148 SMs
     int bps = 0;
@@ -392,8 +391,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         int pbs = 0;
         CKC(eco::post_occupancy(&pbs), "occupancy");
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
-        if (pbs > 4) pbs = 4;
-        h->lc.post_blocks = prop.multiProcessorCount * pbs;
+        h->lc.post_blocks = prop.multiProcessorCount;  // one 512-thread block per SM
     }
     CKC(dalloc(h, &h->bar, 2), "alloc");
 
@@ -622,6 +620,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
         CK(h, cudaMemsetAsync(p.bdir, 0xff, nw * HW, s), "memset");
     }
     CK(h, cudaMemsetAsync(p.bbits, 0, 2 * nw * d.pw * 4, s), "memset");
+    CK(h, cudaMemsetAsync(p.row_wins, 0, 2 * nw * (size_t)d.H * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");

@@ -204,14 +204,18 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
         bool ate = false, died_e = false, died_a = false, survive = false;
         int slot = 0;
         if (active) {
-            slot = list_of(p, t, w)[it.i];
+            // the policy kernel's move record of list position i: (slot, cell, target, key hi)
+            const int4 mr = p.mrec[(size_t)w * p.S + it.i];
+            slot = mr.x;
             const size_t gs = (size_t)w * p.S + slot;
             uint32_t *O = p.occ + (size_t)w * plane_words(p);
             uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
-            int cellv = p.cell[gs];
-            const int tg = p.target[gs];
+            int cellv = mr.y;
+            const int tg = mr.z;
+            const unsigned long long key =
+                ((unsigned long long)(uint32_t)mr.w << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
             uint32_t bit;
-            if (tg >= 0 && p.claim[(size_t)w * HW + tg] == p.mkey[gs]) {
+            if (tg >= 0 && p.claim[(size_t)w * HW + tg] == key) {
                 atomicAnd(word_ptr(O, p, cellv, bit), ~bit);
                 atomicOr(word_ptr(O, p, tg, bit), bit);
                 cellv = tg;
@@ -276,9 +280,10 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
         const int w = it.w;
         const int64_t t = p.t[w];
         if (it.i >= *count_of(p, t, w)) continue;
-        const int slot = list_of(p, t, w)[it.i];
+        const int4 mr = p.mrec[(size_t)w * p.S + it.i];
+        const int slot = mr.x;
         const size_t gs = (size_t)w * p.S + slot;
-        const int tg = p.target[gs];
+        const int tg = mr.z;
         if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;
         if (!p.alive[gs]) continue;
         const int cellv = p.cell[gs];
@@ -349,6 +354,7 @@ __device__ __forceinline__ void birth_win_phase(const DevParams &p, size_t gtid,
             atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
             p.bparent[(size_t)w * HW + c] = slot;
             atomicAdd(p.n_win + w, 1);
+            atomicAdd(rows_of(p, t, w) + cy, 1);
         } else {
             atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_claim), 1ull);
         }
@@ -356,26 +362,53 @@ __device__ __forceinline__ void birth_win_phase(const DevParams &p, size_t gtid,
 }
 
 // ------------------------------------------------------------------ a5 birth rank
-// One block per world: the first n_place = min(winners, free slots) free slots in
-// ascending order (prefix scan of the alive bitmap) and the first n_place winning child
-// cells in row-major order (prefix scan of the birth bitmap); both scans stop once
-// n_place entries are found.  Rank r gets free slot F[r] (R22); later winners are deferred
-// for capacity.  Then the step's counters, the next alive count and t += 1.
+// One block per world.  n_place = min(winners, free slots).  (1) The first n_place free
+// slots in ascending order (prefix scan of the alive bitmap).  (2) The first n_place
+// winning child cells in row-major order: a prefix scan of the per-row winner counts
+// finds the rows holding them, then one warp per such row ranks its cells with a warp
+// scan of the row's bitmap words.  Rank r takes free slot F[r] (R22); every later winner
+// is deferred for capacity.  Both scans stop once n_place entries are covered.  Then the
+// step's counters, the next alive count and t += 1.
+__device__ __forceinline__ void place_birth(const DevParams &p, int w, int c, int r, int n_surv) {
+    const size_t HW = (size_t)p.H * p.W;
+    const int parent = *reinterpret_cast<volatile int32_t *>(p.bparent + (size_t)w * HW + c);
+    const int child = *reinterpret_cast<volatile int32_t *>(p.free_list + (size_t)w * p.S + r);
+    const size_t cs = (size_t)w * p.S + child;
+    p.alive[cs] = 1;
+    atomicOr(p.alive_bits + (size_t)w * p.SW + (child >> 5), 1u << (child & 31));
+    p.cell[cs] = c;
+    p.energy[cs] = p.e_init;
+    p.age[cs] = 0;
+    p.repr[cs] = 0;
+    p.last_action[cs] = 0;
+    p.ate[cs] = 0;
+    for (int k = 0; k < p.Hd; ++k) {
+        p.h[cs * p.Hd + k] = 0.f;
+        p.c[cs * p.Hd + k] = 0.f;
+    }
+    for (int a = 0; a < LOGIT_STRIDE; ++a) p.logits[cs * LOGIT_STRIDE + a] = 0.f;
+    uint32_t bit;
+    atomicOr(word_ptr(p.occ + (size_t)w * plane_words(p), p, c, bit), bit);
+    p.repr[(size_t)w * p.S + parent] = 0;
+    p.birth_child[(size_t)w * p.S + r] = child;
+    p.birth_parent[(size_t)w * p.S + r] = parent;
+    list_of(p, p.t[w] + 1, w)[n_surv + r] = child;
+}
+
 template <int NT>
-__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch) {
-    const int tid = threadIdx.x;
+__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int2 *rowq) {
+    constexpr int NWARP = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = p.t[w];
     const size_t HW = (size_t)p.H * p.W;
-    const size_t pw = plane_words(p);
     const int n_start = *count_of(p, t, w);
     const int n_surv = *reinterpret_cast<volatile int32_t *>(count_of(p, t + 1, w));
     const int n_win = *reinterpret_cast<volatile int32_t *>(p.n_win + w);
     const int n_free = p.S - n_surv;
     const int n_place = n_win < n_free ? n_win : n_free;
-    uint32_t *O = p.occ + (size_t)w * pw;
-    int32_t *next_list = list_of(p, t + 1, w);
 
     if (n_place > 0) {
+        // (1) free slots
         uint32_t running = 0u;
         for (int w0 = 0; w0 < p.SW; w0 += NT) {
             const int wi = w0 + tid;
@@ -398,45 +431,46 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch) {
             if (running >= (uint32_t)n_place) break;
         }
         __syncthreads();
+        // (2) rows holding the first n_place winners, then warp-per-row ranking
         const uint32_t *bb = bbits_of(p, t, w);
+        const int32_t *rows = rows_of(p, t, w);
         running = 0u;
-        for (size_t w0 = 0; w0 < pw; w0 += NT) {
-            const size_t wi = w0 + tid;
-            uint32_t word = wi < pw ? ld_plain(bb + wi) : 0u;
+        for (int y0 = 0; y0 < p.H; y0 += NT) {
+            const int y = y0 + tid;
+            const uint32_t cnt = y < p.H ? (uint32_t)*reinterpret_cast<const volatile int32_t *>(rows + y) : 0u;
             uint32_t tot;
-            const uint32_t ex = block_exclusive_scan<NT>((uint32_t)__popc(word), scratch, tot);
-            uint32_t r = running + ex;
-            while (word && r < (uint32_t)n_place) {
-                const int b = __ffs(word) - 1;
-                word &= word - 1u;
-                const int y = (int)(wi / p.WW), x = (int)(wi - (size_t)y * p.WW) * 32 + b;
-                const int c = y * p.W + x;
-                const int parent = *reinterpret_cast<volatile int32_t *>(p.bparent + (size_t)w * HW + c);
-                const int child = *reinterpret_cast<volatile int32_t *>(p.free_list + (size_t)w * p.S + r);
-                const size_t cs = (size_t)w * p.S + child;
-                p.alive[cs] = 1;
-                atomicOr(p.alive_bits + (size_t)w * p.SW + (child >> 5), 1u << (child & 31));
-                p.cell[cs] = c;
-                p.energy[cs] = p.e_init;
-                p.age[cs] = 0;
-                p.repr[cs] = 0;
-                p.last_action[cs] = 0;
-                p.ate[cs] = 0;
-                for (int k = 0; k < p.Hd; ++k) {
-                    p.h[cs * p.Hd + k] = 0.f;
-                    p.c[cs * p.Hd + k] = 0.f;
+            const uint32_t ex = block_exclusive_scan<NT>(cnt, scratch, tot);
+            // compact the qualifying rows of this chunk into rowq (block scan keeps order)
+            const uint32_t q = (cnt && running + ex < (uint32_t)n_place) ? 1u : 0u;
+            uint32_t nq;
+            const uint32_t qi = block_exclusive_scan<NT>(q, scratch, nq);
+            if (q) rowq[qi] = make_int2(y, (int)(running + ex));
+            __syncthreads();
+            for (uint32_t k = warp; k < nq; k += NWARP) {
+                const int yy = rowq[k].x;
+                uint32_t base = (uint32_t)rowq[k].y;
+                for (int s0 = 0; s0 < p.WW && base < (uint32_t)n_place; s0 += 32) {
+                    const int wx = s0 + lane;
+                    uint32_t word = wx < p.WW ? ld_plain(bb + (size_t)yy * p.WW + wx) : 0u;
+                    const uint32_t pc = (uint32_t)__popc(word);
+                    uint32_t inc = pc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t n = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += n;
+                    }
+                    uint32_t r = base + inc - pc;
+                    while (word && r < (uint32_t)n_place) {
+                        const int b = __ffs(word) - 1;
+                        word &= word - 1u;
+                        place_birth(p, w, yy * p.W + wx * 32 + b, (int)r, n_surv);
+                        ++r;
+                    }
+                    base += __shfl_sync(0xffffffffu, inc, 31);
                 }
-                for (int a = 0; a < LOGIT_STRIDE; ++a) p.logits[cs * LOGIT_STRIDE + a] = 0.f;
-                p.target[cs] = -1;
-                uint32_t bit;
-                atomicOr(word_ptr(O, p, c, bit), bit);
-                p.repr[(size_t)w * p.S + parent] = 0;
-                p.birth_child[(size_t)w * p.S + r] = child;
-                p.birth_parent[(size_t)w * p.S + r] = parent;
-                next_list[n_surv + r] = child;
-                ++r;
             }
             running += tot;
+            __syncthreads();
             if (running >= (uint32_t)n_place) break;
         }
     }

@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
             const int w = (int)(k / pw);
             bbits_of(p, p.t[w] + 1, w)[k - (size_t)w * pw] = 0u;
         }
+        for (size_t k = gtid; k < (size_t)p.n_worlds * p.H; k += gthreads) {
+            const int w = (int)(k / p.H);
+            rows_of(p, p.t[w] + 1, w)[k - (size_t)w * p.H] = 0;
+        }
         for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
             const int64_t tw = p.t[w];
             *count_of(p, tw + 1, (int)w) = 0;
@@ -226,8 +230,7 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
                         }
                     }
                 }
-                p.target[gs] = tg;
-                p.mkey[gs] = key;
+                p.mrec[(size_t)w * p.S + i] = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
             }
             if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
         }
@@ -275,7 +278,8 @@ __global__ void __launch_bounds__(256) k_birth_win(DevParams p) {
 constexpr int RANK_THREADS = 1024;
 __global__ void __launch_bounds__(RANK_THREADS) k_birth_rank(DevParams p) {
     __shared__ uint32_t scratch[RANK_THREADS / 32 + 1];
-    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<RANK_THREADS>(p, w, scratch);
+    __shared__ int2 rowq[RANK_THREADS];
+    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<RANK_THREADS>(p, w, scratch, rowq);
 }
 
 __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
@@ -283,9 +287,10 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 }
 
 // ------------------------------------------------------------------------ k_post
-constexpr int POST_THREADS = 256;
+constexpr int POST_THREADS = 512;
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned int *bar) {
     __shared__ uint32_t scratch[POST_THREADS / 32 + 1];
+    __shared__ int2 rowq[POST_THREADS];
     const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
     // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned int
     birth_win_phase(p, gtid, gthreads);
     grid_sync(bar);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 2, t1 - t0); t0 = t1; }
-    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<POST_THREADS>(p, w, scratch);
+    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<POST_THREADS>(p, w, scratch, rowq);
     grid_sync(bar);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 3, t1 - t0); t0 = t1; }
     mutate_phase(p, gtid, gthreads);

@@ -54,8 +54,6 @@ __global__ void k_init_agents(DevParams p, int w, int n_initial, const unsigned 
     p.repr[gs] = 0;
     p.last_action[gs] = 0;
     p.ate[gs] = 0;
-    p.target[gs] = -1;
-
 }
 
 // initial weights w_j = (float)(std * z_j), z from INIT_W keyed by the initial cell
@@ -156,7 +154,6 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
         uint32_t tot;
         const uint32_t ex = block_exclusive_scan<1024>(a, scratch, tot);
         if (a) list[base + ex] = i;
-        if (i < p.S) p.target[gs] = -1;
         base += tot;
     }
     if (threadIdx.x == 0) {
