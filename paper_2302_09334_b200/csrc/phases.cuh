@@ -31,7 +31,8 @@ __device__ __forceinline__ void grid_sync(unsigned int *bar) {
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*vgen == gen) __nanosleep(32);
+            while (*vgen == gen) {
+            }
         }
         __threadfence();
     }
@@ -39,6 +40,12 @@ __device__ __forceinline__ void grid_sync(unsigned int *bar) {
 }
 
 __device__ __forceinline__ uint32_t ld_plain(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
+
+// Warp-interleaved global thread index (a permutation of [0, gridDim*blockDim)): warp k of
+// the work goes to block k % gridDim, so short phases spread over every SM.
+__device__ __forceinline__ size_t interleaved_gtid() {
+    return ((size_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31);
+}
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;

@@ -260,19 +260,19 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 
 // ----------------------------------------------------------- standalone phase kernels
 __global__ void __launch_bounds__(256) k_regrow(DevParams p, int ahead) {
-    regrow_phase(p, ahead, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+    regrow_phase(p, ahead, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 __global__ void __launch_bounds__(256) k_move(DevParams p) {
-    move_phase(p, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+    move_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
-    birth_claim_phase(p, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+    birth_claim_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 __global__ void __launch_bounds__(256) k_birth_win(DevParams p) {
-    birth_win_phase(p, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+    birth_win_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 constexpr int RANK_THREADS = 1024;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_birth_rank(DevParams p) {
 }
 
 __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
-    mutate_phase(p, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+    mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 // ------------------------------------------------------------------------ k_post
@@ -291,7 +291,9 @@ constexpr int POST_THREADS = 512;
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned int *bar) {
     __shared__ uint32_t scratch[POST_THREADS / 32 + 1];
     __shared__ int2 rowq[POST_THREADS];
-    const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // warp-interleaved global index: consecutive warps of work land on different blocks
+    // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
+    const size_t gtid = interleaved_gtid();
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
     // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
     const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
