@@ -353,6 +353,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.free_list, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_parent, nw * S), "alloc");
+    CKC(dalloc(h, &p.birth_cell, nw * S), "alloc");
     CKC(dalloc(h, &p.n_births, nw), "alloc");
     CKC(dalloc(h, &p.res_count, nw), "alloc");
     CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");

@@ -273,47 +273,68 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
     }
 }
 
+// Warp-aggregated "+1 per flagged lane" on a per-world counter (one atomic per warp when
+// the warp's lanes share a world, which holds whenever S is a multiple of 32).
+template <typename T, typename AddrOf>
+__device__ __forceinline__ void warp_flag_add(bool flag, int w, AddrOf addr_of) {
+    const unsigned lane = threadIdx.x & 31;
+    const int w0 = __shfl_sync(0xffffffffu, w, 0);
+    if (__all_sync(0xffffffffu, w == w0)) {
+        const unsigned m = __ballot_sync(0xffffffffu, flag);
+        if (lane == 0 && m) atomicAdd(addr_of(w0), (T)__popc(m));
+    } else if (flag) {
+        atomicAdd(addr_of(w), (T)1);
+    }
+}
+
 // ----------------------------------------------------------------- a5 birth claim
 // Lazy reset of this step's move claims (every claimant clears its own target; safe
 // because the move phase has finished reading them).  Then every live parent with repr >=
 // T_repr picks the first cell of a Philox-rotated (N, S, E, W) order that is
 // in-grid, agent-free after moves/deaths (O'') and resource-free after consumption (R'')
 // (R21), and records the direction on its own cell (bdir; NO_DIR when it has none).
+// Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
-    for (long v = (long)gtid; v < total; v += (long)gthreads) {
-        const AgentIter it = agent_at(p, v);
+    const unsigned lane = gtid & 31;
+    for (long base = (long)(gtid - lane); base < total; base += (long)gthreads) {
+        const AgentIter it = agent_at(p, base + lane);
         const int w = it.w;
         const int64_t t = p.t[w];
-        if (it.i >= *count_of(p, t, w)) continue;
-        const int4 mr = p.mrec[(size_t)w * p.S + it.i];
-        const int slot = mr.x;
-        const size_t gs = (size_t)w * p.S + slot;
-        const int tg = mr.z;
-        if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;
-        if (!p.alive[gs]) continue;
-        const int cellv = p.cell[gs];
-        uint8_t dir = NO_DIR;
-        if (p.repr[gs] >= p.repr_steps) {
-            const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-            const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
-            const int y = cellv / p.W, x = cellv - y * p.W;
-            const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
-            const int s0 = (int)(d.x & 3u);
-            for (int kk = 0; kk < 4; ++kk) {
-                const int dd = (s0 + kk) & 3;
-                const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
-                if (cy < 0 || cy >= p.H || cx < 0 || cx >= p.W) continue;
-                const int c = cy * p.W + cx;
-                if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
-                dir = (uint8_t)dd;
-                break;
+        bool no_cell = false;
+        if (it.in_range && it.i < *count_of(p, t, w)) {
+            const int4 mr = p.mrec[(size_t)w * p.S + it.i];
+            const int slot = mr.x;
+            const size_t gs = (size_t)w * p.S + slot;
+            const int tg = mr.z;
+            if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;
+            if (p.alive[gs]) {
+                const int cellv = p.cell[gs];
+                uint8_t dir = NO_DIR;
+                if (p.repr[gs] >= p.repr_steps) {
+                    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+                    const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
+                    const int y = cellv / p.W, x = cellv - y * p.W;
+                    const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+                    const int s0 = (int)(d.x & 3u);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int dd = (s0 + kk) & 3;
+                        const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
+                        if (cy < 0 || cy >= p.H || cx < 0 || cx >= p.W) continue;
+                        const int c = cy * p.W + cx;
+                        if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
+                        dir = (uint8_t)dd;
+                        break;
+                    }
+                    no_cell = dir == NO_DIR;
+                }
+                p.bdir[(size_t)w * HW + cellv] = dir;
             }
-            if (dir == NO_DIR)
-                atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_no_cell), 1ull);
         }
-        p.bdir[(size_t)w * HW + cellv] = dir;
+        warp_flag_add<unsigned long long>(no_cell, w, [&](int ww) {
+            return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww], ww)->deferred_no_cell);
+        });
     }
 }
 
@@ -321,7 +342,8 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
 // Claim resolution without atomics: the parent on cell p whose candidate is c wins iff its
 // key (BIRTH w1 << 32 | ~p) exceeds the key of every other live parent adjacent to c that
 // chose c (read from bdir of c's other neighbours, valid where O'' is set).  The winner
-// marks c in the birth bitmap and records itself as c's parent.
+// marks c in the birth bitmap, counts it in its row and records itself as c's parent.
+// Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t, int cellv) {
     const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
     return ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
@@ -330,41 +352,47 @@ __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t
 __device__ __forceinline__ void birth_win_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
-    for (long v = (long)gtid; v < total; v += (long)gthreads) {
-        const AgentIter it = agent_at(p, v);
+    const unsigned lane = gtid & 31;
+    for (long base = (long)(gtid - lane); base < total; base += (long)gthreads) {
+        const AgentIter it = agent_at(p, base + lane);
         const int w = it.w;
         const int64_t t = p.t[w];
-        if (it.i >= *count_of(p, t, w)) continue;
-        const int slot = list_of(p, t, w)[it.i];
-        const size_t gs = (size_t)w * p.S + slot;
-        if (!p.alive[gs]) continue;
-        const int pc = p.cell[gs];
-        const uint8_t *bd = p.bdir + (size_t)w * HW;
-        const int d = bd[pc];
-        if (d == NO_DIR) continue;
-        const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-        const int py = pc / p.W, px = pc - py * p.W;
-        const int cy = py + dir_dy(d), cx = px + dir_dx(d);
-        const int c = cy * p.W + cx;
-        const uint64_t seed = p.seeds[w];
-        const unsigned long long kp = birth_key(seed, t, pc);
-        bool win = true;
-        for (int dq = 0; dq < 4 && win; ++dq) {
-            const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
-            if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
-            const int q = qy * p.W + qx;
-            if (q == pc || !get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
-            if (birth_key(seed, t, q) > kp) win = false;
+        bool win = false, lost = false;
+        if (it.in_range && it.i < *count_of(p, t, w)) {
+            const int slot = p.mrec[(size_t)w * p.S + it.i].x;
+            const size_t gs = (size_t)w * p.S + slot;
+            const int pc = p.cell[gs];
+            const uint8_t *bd = p.bdir + (size_t)w * HW;
+            const int d = p.alive[gs] ? bd[pc] : NO_DIR;
+            if (d != NO_DIR) {
+                const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+                const int py = pc / p.W, px = pc - py * p.W;
+                const int cy = py + dir_dy(d), cx = px + dir_dx(d);
+                const int c = cy * p.W + cx;
+                const uint64_t seed = p.seeds[w];
+                const unsigned long long kp = birth_key(seed, t, pc);
+                win = true;
+                for (int dq = 0; dq < 4 && win; ++dq) {
+                    const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
+                    if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
+                    const int q = qy * p.W + qx;
+                    if (q == pc || !get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
+                    if (birth_key(seed, t, q) > kp) win = false;
+                }
+                if (win) {
+                    uint32_t bit;
+                    atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
+                    p.bparent[(size_t)w * HW + c] = slot;
+                    atomicAdd(rows_of(p, t, w) + cy, 1);
+                } else {
+                    lost = true;
+                }
+            }
         }
-        if (win) {
-            uint32_t bit;
-            atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
-            p.bparent[(size_t)w * HW + c] = slot;
-            atomicAdd(p.n_win + w, 1);
-            atomicAdd(rows_of(p, t, w) + cy, 1);
-        } else {
-            atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->deferred_claim), 1ull);
-        }
+        warp_flag_add<int>(win, w, [&](int ww) { return p.n_win + ww; });
+        warp_flag_add<unsigned long long>(lost, w, [&](int ww) {
+            return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww], ww)->deferred_claim);
+        });
     }
 }
 
@@ -470,7 +498,7 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
                     while (word && r < (uint32_t)n_place) {
                         const int b = __ffs(word) - 1;
                         word &= word - 1u;
-                        place_birth(p, w, yy * p.W + wx * 32 + b, (int)r, n_surv);
+                        p.birth_cell[(size_t)w * p.S + r] = yy * p.W + wx * 32 + b;
                         ++r;
                     }
                     base += __shfl_sync(0xffffffffu, inc, 31);
@@ -480,6 +508,9 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
             __syncthreads();
             if (running >= (uint32_t)n_place) break;
         }
+        // (3) placement, one birth per thread (independent dependency chains)
+        for (int r = tid; r < n_place; r += NT)
+            place_birth(p, w, *reinterpret_cast<volatile int32_t *>(p.birth_cell + (size_t)w * p.S + r), r, n_surv);
     }
     __syncthreads();
     if (tid == 0) {
@@ -513,34 +544,57 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
 // sigma = 0.02 a standard deviation (R23).  One item = one canonical group q = j >> 2 of
 // one child: one Philox call, two fp64 Box-Muller pairs, four weights.  Runs after the
 // rank phase advanced t, so the step of the birth is p.t[w] - 1.
-__device__ __forceinline__ void mutate_item(const DevParams &p, int w, int b, int q) {
-    const int64_t t = p.t[w] - 1;
-    const int child = p.birth_child[(size_t)w * p.S + b];
-    const int parent = p.birth_parent[(size_t)w * p.S + b];
-    const size_t cs = (size_t)w * p.S + child, ps = (size_t)w * p.S + parent;
-    const uint4 d = draw4(p.seeds[w], PURPOSE_MUTATE, (uint32_t)t, (uint32_t)p.cell[cs], (uint32_t)q);
+struct MutItem {
+    const float *wp;
+    float *wc;
+    int q;
     double z[4];
-    box_muller(d.x, d.y, z[0], z[1]);
-    box_muller(d.z, d.w, z[2], z[3]);
-    const float *wp = p.weights + ps * (size_t)p.Pd;
-    float *wc = p.weights + cs * (size_t)p.Pd;
+};
+
+// load the item's birth, draw its Philox block and transform it (no dependent loads
+// other than the birth record, so two items per thread overlap their fp64 chains)
+__device__ __forceinline__ MutItem mutate_prepare(const DevParams &p, int w, int64_t t, size_t k, int groups) {
+    MutItem it;
+    const int b = (int)(k / groups);
+    it.q = (int)(k - (size_t)b * groups);
+    const size_t bs = (size_t)w * p.S + b;
+    const int child = p.birth_child[bs], parent = p.birth_parent[bs], cellc = p.birth_cell[bs];
+    it.wp = p.weights + ((size_t)w * p.S + parent) * (size_t)p.Pd;
+    it.wc = p.weights + ((size_t)w * p.S + child) * (size_t)p.Pd;
+    const uint4 d = draw4(p.seeds[w], PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)it.q);
+    box_muller(d.x, d.y, it.z[0], it.z[1]);
+    box_muller(d.z, d.w, it.z[2], it.z[3]);
+    return it;
+}
+
+__device__ __forceinline__ void mutate_write(const DevParams &p, const MutItem &it) {
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const int j = 4 * q + m;
+        const int j = 4 * it.q + m;
         if (j >= p.P) break;
         const int dd = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
-        wc[dd] = __fadd_rn(wp[dd], __double2float_rn(__dmul_rn(p.mutation_std, z[m])));
+        it.wc[dd] = __fadd_rn(it.wp[dd], __double2float_rn(__dmul_rn(p.mutation_std, it.z[m])));
     }
 }
 
-// All mutation items of all worlds: grid-stride over (birth, group) items world by world.
+// All mutation items of all worlds: grid-stride over (birth, group) items world by world,
+// two items per thread per iteration.
 __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const int groups = (p.P + 3) >> 2;
     for (int w = 0; w < p.n_worlds; ++w) {
         const size_t n = (size_t)(*reinterpret_cast<volatile int32_t *>(p.n_births + w)) * groups;
-        for (size_t k = gtid; k < n; k += gthreads) {
-            const int b = (int)(k / groups), q = (int)(k - (size_t)b * groups);
-            mutate_item(p, w, b, q);
+        if (n == 0) continue;
+        const int64_t t = p.t[w] - 1;  // the rank phase already advanced t
+        for (size_t k = gtid; k < n; k += 2 * gthreads) {
+            const size_t k2 = k + gthreads;
+            const MutItem a = mutate_prepare(p, w, t, k, groups);
+            if (k2 < n) {
+                const MutItem b = mutate_prepare(p, w, t, k2, groups);
+                mutate_write(p, a);
+                mutate_write(p, b);
+            } else {
+                mutate_write(p, a);
+            }
         }
     }
 }

@@ -27,6 +27,14 @@ __device__ __forceinline__ float4 ld_weights4(const float *ptr) {
 
 __device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
 
+__device__ __forceinline__ void flush_counters(const DevParams &p, int w, unsigned long long nnz,
+                                               unsigned long long ties) {
+    if (w < 0) return;
+    sim_step_record *rec = record_of(p, p.t[w], w);
+    if (nnz) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->obs_nnz), nnz);
+    if (ties) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->near_ties), ties);
+}
+
 // ------------------------------------------------------------------------- K2 policy
 // Lane group of HD lanes per live agent (warp per agent at Hd = 32); lane k owns hidden
 // unit k and its four gate rows (i, f, g, o).
@@ -79,6 +87,8 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
         }
     }
 
+    int acc_w = -1;
+    unsigned long long acc_nnz = 0ull, acc_ties = 0ull;
     for (long base = 0; base < total; base += per_round) {
         // consecutive agents go to different CTAs so a small population spreads over all SMs
         const long v = base + (long)(wib * AG + grp) * gridDim.x + blockIdx.x;
@@ -204,11 +214,13 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
                     bad = bad || !isfinite(lg[a]);
                     p.logits[gs * LOGIT_STRIDE + a] = lg[a];
                 }
-                sim_step_record *rec = record_of(p, t, w);
-                if ((double)bestv - second < 1e-4)
-                    atomicAdd(reinterpret_cast<unsigned long long *>(&rec->near_ties), 1ull);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&rec->obs_nnz),
-                          (unsigned long long)(__popcll(m_lo) + __popcll(m_hi)));
+                // per-lane accumulation of the world's counters, flushed on world change
+                if (w != acc_w) {
+                    flush_counters(p, acc_w, acc_nnz, acc_ties);
+                    acc_w = w;
+                }
+                acc_ties += ((double)bestv - second < 1e-4) ? 1ull : 0ull;
+                acc_nnz += (unsigned long long)(__popcll(m_lo) + __popcll(m_hi));
                 int act = best;
                 if (*p.forced_on) {
                     const uint8_t f = p.forced[gs];
@@ -235,6 +247,7 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
             if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
         }
     }
+    flush_counters(p, acc_w, acc_nnz, acc_ties);
 }
 
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
