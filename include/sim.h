@@ -139,10 +139,10 @@ typedef struct {
 } sim_state_sizes_t;
 
 /* Per-kernel timing of one instrumented step (milliseconds, CUDA events). */
-#define SIM_NUM_KERNELS 7
+#define SIM_NUM_KERNELS 6
 typedef struct {
     float step_ms;                     /* first event to last event of the step */
-    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_win, birth_rank, mutate */
+    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_rank, mutate */
 } sim_step_timing;
 
 /* --- lifecycle ------------------------------------------------------------------- */
@@ -176,10 +176,11 @@ SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
 /* Graph mode runs everything after the policy kernel as one cooperative kernel whose
- * phases are separated by grid barriers: move, regrow(t+1)+birth candidates, birth
- * winners, birth rank, mutation.  out[i] = summed duration (ns, device global timer, as
- * seen by block 0) of phase i over the steps since the last reset; reset != 0 zeroes. */
-#define SIM_NUM_POST_PHASES 5
+ * phases are separated by grid barriers: move, regrow(t+1)+birth candidates, birth rank
+ * (the children's weights are written by the next policy kernel).  out[i] = summed
+ * duration (ns, device global timer, as seen by block 0) of phase i over the steps since
+ * the last reset; reset != 0 zeroes. */
+#define SIM_NUM_POST_PHASES 3
 SIM_API sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset);
 /* Synchronise the handle's stream (reports deferred errors). */
 SIM_API sim_status sim_synchronize(sim_handle h);

@@ -105,14 +105,14 @@ size_t device_bytes(const Derived &d) {
     const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
     size_t b = 0;
     b += nw * d.pw * 4 * 5;                 // plane0, plane1, occ, bbits[2]
-    b += nw * HW * (8 + 1 + 4);             // claim, bdir, bparent
+    b += nw * HW * (8 + 1 + 4);             // claim, bdir, bslot
     b += nw * ((S + 31) / 32) * 4;          // alive bits
     b += nw * S * (1 * 3 + 4 * 4);          // u8 x3, i32 x4
     b += nw * S * (size_t)d.Hd * 4 * 2;     // h, c
     b += nw * S * eco::LOGIT_STRIDE * 4;    // logits
     b += nw * S * (size_t)d.Pd * 4;         // weights
     b += nw * S * 16 + 2 * nw * d.H * 4;    // move records, row winner counts
-    b += nw * S * 4 * 5;                    // alive lists [2], free, birth lists
+    b += nw * S * 4 * 7;                    // alive lists [2], free, birth lists, mutation counters
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
 }
@@ -134,7 +134,8 @@ struct sim_ctx {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     bool regrown_ahead = false;
-    unsigned int *bar = nullptr;  // grid-barrier words of k_post
+    bool mutation_pending = false;       // the last graph step's children lack weights
+    unsigned long long *bar = nullptr;   // grid-barrier words of k_post
     int64_t t = 0;
     int32_t *nonfinite_host = nullptr;
     int32_t *forced_on_dev = nullptr;
@@ -183,29 +184,38 @@ sim_status check_nonfinite(sim_ctx *h) {
     return SIM_OK;
 }
 
-// Instrumented mode: the phases of k_post as separate kernels, in k_post's order, so that
-// every kernel can be bracketed by events.  Index order of sim_step_timing.kernel_ms:
-// 0 regrow (of step t+1, as inside k_post), 1 policy, 2 move, 3 birth_claim, 4 birth_win,
-// 5 birth_rank, 6 mutate.  Launch order: policy, move, regrow, claim, win, rank, mutate.
-constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5, 6};
+// Instrumented mode: the phases as separate kernels, in graph mode's order, so that every
+// kernel can be bracketed by events.  Index order of sim_step_timing.kernel_ms:
+// 0 regrow (of step t+1, as inside k_post), 1 policy, 2 move, 3 birth_claim, 4 birth_rank,
+// 5 mutate.  Launch order: policy, move, regrow, claim, rank, mutate.
+constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5};
 
 cudaError_t launch_phase(sim_ctx *h, int k) {
     switch (k) {
         case 0: return eco::launch_regrow(h->p, 1, h->stream);
-        case 1: return eco::launch_policy(h->p, h->lc, h->stream);
+        case 1: return eco::launch_policy(h->p, h->lc, 0, h->stream);
         case 2: return eco::launch_move(h->p, h->lc, h->stream);
         case 3: return eco::launch_birth_claim(h->p, h->lc, h->stream);
-        case 4: return eco::launch_birth_win(h->p, h->lc, h->stream);
-        case 5: return eco::launch_birth_rank(h->p, h->stream);
+        case 4: return eco::launch_birth_rank(h->p, h->stream);
         default: return eco::launch_mutate(h->p, h->lc, h->stream);
     }
 }
 
-// graph-mode step: the policy kernel, then the cooperative post-policy kernel
+// graph-mode step: the policy kernel (with the previous step's mutation as prologue), then
+// the cooperative post-policy kernel
 cudaError_t enqueue_step(sim_ctx *h) {
     cudaError_t e;
-    if ((e = eco::launch_policy(h->p, h->lc, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_policy(h->p, h->lc, 1, h->stream)) != cudaSuccess) return e;
     return eco::launch_post(h->p, h->lc, h->bar, h->stream);
+}
+
+// children placed by the last graph step get their weights in the next k_policy; before
+// any state export, import or instrumented step, write them now
+cudaError_t flush_mutation(sim_ctx *h) {
+    if (!h->mutation_pending) return cudaSuccess;
+    cudaError_t e = eco::launch_mutate(h->p, h->lc, h->stream);
+    if (e == cudaSuccess) h->mutation_pending = false;
+    return e;
 }
 
 // the regrowth of the current step, needed once after create/set_state
@@ -332,7 +342,10 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &T_d, (size_t)d.H * 4), "alloc");
     CKC(dalloc(h, &p.claim, S ? nw * HW : 1), "alloc");
     CKC(dalloc(h, &p.bdir, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.bparent, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.bslot, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.mut_done, nw * S), "alloc");
+    CKC(dalloc(h, &p.mut_pending, nw), "alloc");
+    CKC(dalloc(h, &p.newborn_base, nw), "alloc");
     CKC(dalloc(h, &p.alive_bits, nw * (size_t)d.SW), "alloc");
     CKC(dalloc(h, &p.alive, nw * S), "alloc");
     CKC(dalloc(h, &p.last_action, nw * S), "alloc");
@@ -450,6 +463,7 @@ sim_status sim_step(sim_handle h, int64_t n) {
     CK(h, ensure_regrown(h), "regrow");
     for (int64_t i = 0; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
     h->t += n;
+    h->mutation_pending = true;
     return SIM_OK;
 }
 
@@ -458,6 +472,7 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, flush_mutation(h), "mutation");
     CK(h, ensure_regrown(h), "regrow");
     CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
     for (int i = 0; i < SIM_NUM_KERNELS; ++i) {
@@ -484,6 +499,7 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, flush_mutation(h), "mutation");
     if ((st = sync(h)) != SIM_OK) return st;
     const Derived &d = h->d;
     const DevParams &p = h->p;
@@ -538,6 +554,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     if (!in) return fail(SIM_E_INVALID, "invalid argument: in (NULL)");
     if (in->t < 0 || in->t >= ((int64_t)1 << 32)) return fail(SIM_E_INVALID, "invalid field: t");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, flush_mutation(h), "mutation");
     if ((st = sync(h)) != SIM_OK) return st;
     const Derived &d = h->d;
     DevParams &p = h->p;
@@ -624,6 +641,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemsetAsync(p.row_wins, 0, 2 * nw * (size_t)d.H * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
+    CK(h, cudaMemsetAsync(p.mut_pending, 0, nw * 4, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     h->regrown_ahead = false;
     return sync(h);

@@ -1,12 +1,13 @@
-// phases.cuh — the phases of one world step as device functions, shared by the
-// standalone kernels (instrumented mode) and the fused cooperative k_post (graph mode).
+// phases.cuh — the phases of one world step as device functions, shared by the standalone
+// kernels (instrumented mode) and the fused kernels of graph mode.
 //
-//   regrow_word        a1  one 32-cell word of the grid (step index given explicitly)
-//   move_agent         a4  claim resolution, movement, consumption, physiology, death
-//   birth_claim_agent  a5  lazy move-claim reset, birth candidate direction
-//   birth_win_agent    a5  declarative birth-claim resolution, birth bitmap
-//   birth_rank_world   a5  (one block) free slots, winner ranks, placement, counters, t += 1
-//   mutate_item        a5  one canonical weight group of one child
+//   regrow_phase       a1  grid regrowth for step t (+ahead), one 32-cell word per item
+//   move_phase         a4  claim resolution, movement, consumption, physiology, death
+//   birth_claim_phase  a5  lazy move-claim reset, birth candidate, claimed-cell dedup
+//   birth_rank_world   a5  (one block per world) free slots, claimed cells in row-major
+//                          order, claim winners, placement, counters, t += 1
+//   mutate_phase       a5  children's weights (run by the NEXT step's policy kernel in
+//                          graph mode, or standalone)
 //
 // Data written by one phase and read by a later phase of the same kernel is read with
 // plain (coherent) loads, never through the read-only path.
@@ -17,27 +18,29 @@
 namespace eco {
 
 // ------------------------------------------------------------------ grid barrier
-// Generation barrier over all blocks of a cooperatively launched grid (co-residency is
-// guaranteed by the cooperative launch).  bar[0] = arrivals, bar[1] = generation.
-__device__ __forceinline__ void grid_sync(unsigned int *bar) {
+// Release/acquire barrier over all blocks of a cooperatively launched grid (co-residency
+// guaranteed by the cooperative launch).  bar[0] counts arrivals monotonically across
+// launches; bar[1] counts completed launches of the kernel.  `target` starts at
+// bar[1] * nblocks * barriers_per_launch (read by every block before its first arrival).
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long long &target) {
     __syncthreads();
+    target += gridDim.x;
     if (threadIdx.x == 0) {
-        volatile unsigned int *vgen = bar + 1;
-        const unsigned int gen = *vgen;
-        __threadfence();
-        const unsigned int nblocks = gridDim.x * gridDim.y * gridDim.z;
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            bar[0] = 0u;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*vgen == gen) {
-            }
-        }
-        __threadfence();
+        unsigned long long cur;
+        asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(cur) : "l"(bar) : "memory");
+        cur += 1;
+        while (cur < target) asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
     }
     __syncthreads();
 }
+
+__device__ __forceinline__ unsigned long long grid_sync_base(unsigned long long *bar, int barriers_per_launch) {
+    const unsigned long long launches = *reinterpret_cast<volatile unsigned long long *>(bar + 1);
+    return launches * (unsigned long long)gridDim.x * (unsigned long long)barriers_per_launch;
+}
+
+// called once per launch after its last barrier by one thread of block 0
+__device__ __forceinline__ void grid_sync_done(unsigned long long *bar) { atomicAdd(bar + 1, 1ull); }
 
 __device__ __forceinline__ uint32_t ld_plain(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
@@ -51,6 +54,22 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// Warp-aggregated "+v per lane" on a per-world counter (one atomic per warp when the
+// warp's lanes share a world, which holds whenever S is a multiple of 32).
+template <typename T, typename AddrOf>
+__device__ __forceinline__ void warp_world_add(T v, int w, AddrOf addr_of) {
+    const unsigned lane = threadIdx.x & 31;
+    const int w0 = __shfl_sync(0xffffffffu, w, 0);
+    if (__all_sync(0xffffffffu, w == w0)) {
+        T s = v;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0 && s) atomicAdd(addr_of(w0), s);
+    } else if (v) {
+        atomicAdd(addr_of(w), v);
+    }
 }
 
 // ----------------------------------------------------------------------- a1 regrow
@@ -143,34 +162,25 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
     return __popc(grow);
 }
 
-// Grid-stride regrowth of every world for step t_of(w) = p.t[w] + ahead; one atomic per
-// warp on the world's record (warp-uniform world check).
+// Grid-stride regrowth of every world for step p.t[w] + ahead; one atomic per warp on the
+// world's record.  Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ void regrow_phase(const DevParams &p, int ahead, size_t gtid, size_t gthreads) {
     const int real_words = (p.W + 31) >> 5;
     const size_t per_world = (size_t)p.H * real_words;
     const size_t total = per_world * p.n_worlds;
     for (size_t base = gtid - (gtid & 31); base < total; base += gthreads) {
         const size_t k = base + (gtid & 31);
-        int w = 0, cnt = 0;
-        int64_t t = 0;
+        int w = 0;
+        unsigned long long cnt = 0;
         if (k < total) {
             w = (int)(k / per_world);
             const size_t r = k - (size_t)w * per_world;
             const int y = (int)(r / real_words), wx = (int)(r - (size_t)y * real_words);
-            t = p.t[w] + ahead;
-            cnt = regrow_word(p, w, y, wx, t);
+            cnt = (unsigned long long)regrow_word(p, w, y, wx, p.t[w] + ahead);
         }
-        const int w0 = __shfl_sync(0xffffffffu, w, 0);
-        if (__all_sync(0xffffffffu, w == w0)) {
-            unsigned s = (unsigned)cnt;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if ((gtid & 31) == 0 && s)
-                atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, p.t[w0] + ahead, w0)->grown),
-                          (unsigned long long)s);
-        } else if (cnt) {
-            atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, t, w)->grown), (unsigned long long)cnt);
-        }
+        warp_world_add<unsigned long long>(cnt, w, [&](int ww) {
+            return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww] + ahead, ww)->grown);
+        });
     }
 }
 
@@ -185,11 +195,6 @@ __device__ __forceinline__ AgentIter agent_at(const DevParams &p, long v) {
     a.w = a.in_range ? (int)(v / p.S) : 0;
     a.i = a.in_range ? (int)(v - (long)a.w * p.S) : 0;
     return a;
-}
-
-__device__ __forceinline__ void warp_count_add(unsigned long long *dst, bool flag) {
-    const unsigned m = __ballot_sync(0xffffffffu, flag);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(dst, (unsigned long long)__popc(m));
 }
 
 // ----------------------------------------------------------------------- a4 move
@@ -221,6 +226,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             const int tg = mr.z;
             const unsigned long long key =
                 ((unsigned long long)(uint32_t)mr.w << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
+            int en0 = p.energy[gs], ag0 = p.age[gs], rp0 = p.repr[gs];  // issued early, independent
             uint32_t bit;
             if (tg >= 0 && p.claim[(size_t)w * HW + tg] == key) {
                 atomicAnd(word_ptr(O, p, cellv, bit), ~bit);
@@ -234,13 +240,13 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 ate = true;
             }
             p.ate[gs] = ate ? 1 : 0;
-            long long e = (long long)p.energy[gs] + (ate ? (long long)p.e_gain : 0ll) - (long long)p.e_decay;
+            long long e = (long long)en0 + (ate ? (long long)p.e_gain : 0ll) - (long long)p.e_decay;
             if (p.e_max != 0x7fffffff && e > p.e_max) e = p.e_max;
             const int en = (int)e;
-            const int ag = p.age[gs] + 1;
+            const int ag = ag0 + 1;
             p.energy[gs] = en;
             p.age[gs] = ag;
-            p.repr[gs] = en > p.e_repr_gt ? p.repr[gs] + 1 : 0;
+            p.repr[gs] = en > p.e_repr_gt ? rp0 + 1 : 0;
             if (en <= p.e_death_le) died_e = true;
             else if (ag > p.max_age) died_a = true;
             if (died_e || died_a) {
@@ -255,12 +261,15 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
         if (__all_sync(0xffffffffu, w == w0)) {
             const int64_t t0 = p.t[w0];
             sim_step_record *rec = record_of(p, t0, w0);
-            warp_count_add(reinterpret_cast<unsigned long long *>(&rec->eaten), ate);
-            warp_count_add(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), died_e);
-            warp_count_add(reinterpret_cast<unsigned long long *>(&rec->deaths_age), died_a);
-            const unsigned m = __ballot_sync(0xffffffffu, survive);
+            const unsigned me = __ballot_sync(0xffffffffu, ate), md = __ballot_sync(0xffffffffu, died_e),
+                           ma = __ballot_sync(0xffffffffu, died_a), m = __ballot_sync(0xffffffffu, survive);
             int pos0 = 0;
-            if (lane == 0 && m) pos0 = atomicAdd(count_of(p, t0 + 1, w0), __popc(m));
+            if (lane == 0) {
+                if (me) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), (unsigned long long)__popc(me));
+                if (md) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), (unsigned long long)__popc(md));
+                if (ma) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), (unsigned long long)__popc(ma));
+                if (m) pos0 = atomicAdd(count_of(p, t0 + 1, w0), __popc(m));
+            }
             pos0 = __shfl_sync(0xffffffffu, pos0, 0);
             if (survive) list_of(p, t + 1, w)[pos0 + __popc(m & ((1u << lane) - 1u))] = slot;
         } else {
@@ -273,27 +282,15 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
     }
 }
 
-// Warp-aggregated "+1 per flagged lane" on a per-world counter (one atomic per warp when
-// the warp's lanes share a world, which holds whenever S is a multiple of 32).
-template <typename T, typename AddrOf>
-__device__ __forceinline__ void warp_flag_add(bool flag, int w, AddrOf addr_of) {
-    const unsigned lane = threadIdx.x & 31;
-    const int w0 = __shfl_sync(0xffffffffu, w, 0);
-    if (__all_sync(0xffffffffu, w == w0)) {
-        const unsigned m = __ballot_sync(0xffffffffu, flag);
-        if (lane == 0 && m) atomicAdd(addr_of(w0), (T)__popc(m));
-    } else if (flag) {
-        atomicAdd(addr_of(w), (T)1);
-    }
-}
-
 // ----------------------------------------------------------------- a5 birth claim
 // Lazy reset of this step's move claims (every claimant clears its own target; safe
 // because the move phase has finished reading them).  Then every live parent with repr >=
 // T_repr picks the first cell of a Philox-rotated (N, S, E, W) order that is
 // in-grid, agent-free after moves/deaths (O'') and resource-free after consumption (R'')
-// (R21), and records the direction on its own cell (bdir; NO_DIR when it has none).
-// Must be called by all 32 lanes of a warp.
+// (R21), records (direction, slot) on its own cell, and marks the candidate cell in the
+// step's claimed-cell bitmap.  Distinct claimed cells are counted (each has exactly one
+// winner, resolved later by max key) per world and per row.  Deferred-claim losers are
+// (candidates - claimed cells), also settled later.  Must be called by all 32 lanes.
 __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
@@ -302,7 +299,8 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
         const AgentIter it = agent_at(p, base + lane);
         const int w = it.w;
         const int64_t t = p.t[w];
-        bool no_cell = false;
+        unsigned long long no_cell = 0, cand = 0;
+        int new_cell = 0;
         if (it.in_range && it.i < *count_of(p, t, w)) {
             const int4 mr = p.mrec[(size_t)w * p.S + it.i];
             const int slot = mr.x;
@@ -325,88 +323,68 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
                         const int c = cy * p.W + cx;
                         if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
                         dir = (uint8_t)dd;
+                        uint32_t bit;
+                        const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
+                        if (!(old & bit)) {
+                            new_cell = 1;
+                            atomicAdd(rows_of(p, t, w) + cy, 1);
+                        }
                         break;
                     }
-                    no_cell = dir == NO_DIR;
+                    if (dir == NO_DIR) no_cell = 1;
+                    else cand = 1;
                 }
                 p.bdir[(size_t)w * HW + cellv] = dir;
+                p.bslot[(size_t)w * HW + cellv] = slot;
             }
         }
-        warp_flag_add<unsigned long long>(no_cell, w, [&](int ww) {
+        warp_world_add<unsigned long long>(no_cell, w, [&](int ww) {
             return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww], ww)->deferred_no_cell);
         });
+        // deferred_claim accumulates the candidates here; the rank phase subtracts the winners
+        warp_world_add<unsigned long long>(cand, w, [&](int ww) {
+            return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww], ww)->deferred_claim);
+        });
+        warp_world_add<int>(new_cell, w, [&](int ww) { return p.n_win + ww; });
     }
 }
 
-// ------------------------------------------------------------------- a5 birth win
-// Claim resolution without atomics: the parent on cell p whose candidate is c wins iff its
-// key (BIRTH w1 << 32 | ~p) exceeds the key of every other live parent adjacent to c that
-// chose c (read from bdir of c's other neighbours, valid where O'' is set).  The winner
-// marks c in the birth bitmap, counts it in its row and records itself as c's parent.
-// Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t, int cellv) {
     const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
     return ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
 }
 
-__device__ __forceinline__ void birth_win_phase(const DevParams &p, size_t gtid, size_t gthreads) {
-    const long total = (long)p.n_worlds * p.S;
-    const size_t HW = (size_t)p.H * p.W;
-    const unsigned lane = gtid & 31;
-    for (long base = (long)(gtid - lane); base < total; base += (long)gthreads) {
-        const AgentIter it = agent_at(p, base + lane);
-        const int w = it.w;
-        const int64_t t = p.t[w];
-        bool win = false, lost = false;
-        if (it.in_range && it.i < *count_of(p, t, w)) {
-            const int slot = p.mrec[(size_t)w * p.S + it.i].x;
-            const size_t gs = (size_t)w * p.S + slot;
-            const int pc = p.cell[gs];
-            const uint8_t *bd = p.bdir + (size_t)w * HW;
-            const int d = p.alive[gs] ? bd[pc] : NO_DIR;
-            if (d != NO_DIR) {
-                const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-                const int py = pc / p.W, px = pc - py * p.W;
-                const int cy = py + dir_dy(d), cx = px + dir_dx(d);
-                const int c = cy * p.W + cx;
-                const uint64_t seed = p.seeds[w];
-                const unsigned long long kp = birth_key(seed, t, pc);
-                win = true;
-                for (int dq = 0; dq < 4 && win; ++dq) {
-                    const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
-                    if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
-                    const int q = qy * p.W + qx;
-                    if (q == pc || !get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
-                    if (birth_key(seed, t, q) > kp) win = false;
-                }
-                if (win) {
-                    uint32_t bit;
-                    atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
-                    p.bparent[(size_t)w * HW + c] = slot;
-                    atomicAdd(rows_of(p, t, w) + cy, 1);
-                } else {
-                    lost = true;
-                }
-            }
-        }
-        warp_flag_add<int>(win, w, [&](int ww) { return p.n_win + ww; });
-        warp_flag_add<unsigned long long>(lost, w, [&](int ww) {
-            return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww], ww)->deferred_claim);
-        });
-    }
-}
-
 // ------------------------------------------------------------------ a5 birth rank
-// One block per world.  n_place = min(winners, free slots).  (1) The first n_place free
-// slots in ascending order (prefix scan of the alive bitmap).  (2) The first n_place
-// winning child cells in row-major order: a prefix scan of the per-row winner counts
-// finds the rows holding them, then one warp per such row ranks its cells with a warp
-// scan of the row's bitmap words.  Rank r takes free slot F[r] (R22); every later winner
-// is deferred for capacity.  Both scans stop once n_place entries are covered.  Then the
-// step's counters, the next alive count and t += 1.
-__device__ __forceinline__ void place_birth(const DevParams &p, int w, int c, int r, int n_surv) {
+// One block per world.  Each claimed cell c has exactly one winner: the live parent q
+// adjacent to c that chose c with the largest key (BIRTH w1 << 32 | ~q).  n_place =
+// min(claimed cells, free slots).  (1) The first n_place free slots in ascending order
+// (prefix scan of the alive bitmap).  (2) The first n_place claimed cells in row-major
+// order: a prefix scan of the per-row counts finds the rows, one warp per row ranks its
+// cells with a warp scan of the row's bitmap words.  (3) One thread per rank r resolves the
+// winner of cell c_r and places the child in free slot F[r] (R22); every later claimed cell
+// is deferred for capacity.  Then the step's counters, the next alive count and t += 1.
+// The children's weights are written by mutate_phase (they are marked pending here).
+__device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t, int c, int r, int n_surv) {
     const size_t HW = (size_t)p.H * p.W;
-    const int parent = *reinterpret_cast<volatile int32_t *>(p.bparent + (size_t)w * HW + c);
+    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+    const uint8_t *bd = p.bdir + (size_t)w * HW;
+    const uint64_t seed = p.seeds[w];
+    const int cy = c / p.W, cx = c - cy * p.W;
+    // winner among the claimants of c (at least one exists)
+    int qbest = -1;
+    unsigned long long kbest = 0ull;
+    for (int dq = 0; dq < 4; ++dq) {
+        const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
+        if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
+        const int q = qy * p.W + qx;
+        if (!get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
+        const unsigned long long kq = birth_key(seed, t, q);
+        if (qbest < 0 || kq > kbest) {
+            kbest = kq;
+            qbest = q;
+        }
+    }
+    const int parent = p.bslot[(size_t)w * HW + qbest];
     const int child = *reinterpret_cast<volatile int32_t *>(p.free_list + (size_t)w * p.S + r);
     const size_t cs = (size_t)w * p.S + child;
     p.alive[cs] = 1;
@@ -427,7 +405,8 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int c, in
     p.repr[(size_t)w * p.S + parent] = 0;
     p.birth_child[(size_t)w * p.S + r] = child;
     p.birth_parent[(size_t)w * p.S + r] = parent;
-    list_of(p, p.t[w] + 1, w)[n_surv + r] = child;
+    p.mut_done[(size_t)w * p.S + r] = 0;
+    list_of(p, t + 1, w)[n_surv + r] = child;
 }
 
 template <int NT>
@@ -465,8 +444,7 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
             running += tot;
             if (running >= (uint32_t)n_place) break;
         }
-        __syncthreads();
-        // (2) rows holding the first n_place winners, then warp-per-row ranking
+        // (2) rows holding the first n_place claimed cells, then warp-per-row ranking
         const uint32_t *bb = bbits_of(p, t, w);
         const int32_t *rows = rows_of(p, t, w);
         running = 0u;
@@ -475,7 +453,6 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
             const uint32_t cnt = y < p.H ? (uint32_t)*reinterpret_cast<const volatile int32_t *>(rows + y) : 0u;
             uint32_t tot;
             const uint32_t ex = block_exclusive_scan<NT>(cnt, scratch, tot);
-            // compact the qualifying rows of this chunk into rowq (block scan keeps order)
             const uint32_t q = (cnt && running + ex < (uint32_t)n_place) ? 1u : 0u;
             uint32_t nq;
             const uint32_t qi = block_exclusive_scan<NT>(q, scratch, nq);
@@ -508,9 +485,9 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
             __syncthreads();
             if (running >= (uint32_t)n_place) break;
         }
-        // (3) placement, one birth per thread (independent dependency chains)
+        // (3) winners and placement, one birth per thread (independent dependency chains)
         for (int r = tid; r < n_place; r += NT)
-            place_birth(p, w, *reinterpret_cast<volatile int32_t *>(p.birth_cell + (size_t)w * p.S + r), r, n_surv);
+            place_birth(p, w, t, *reinterpret_cast<volatile int32_t *>(p.birth_cell + (size_t)w * p.S + r), r, n_surv);
     }
     __syncthreads();
     if (tid == 0) {
@@ -521,11 +498,14 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
         rec->t = t;
         rec->agents_at_start = n_start;
         rec->births = n_place;
+        rec->deferred_claim = rec->deferred_claim - n_win;  // candidates - claimed cells
         rec->deferred_capacity = n_win - n_place;
         rec->population = n_surv + n_place;
         rec->resources = p.res_count[w];
         *count_of(p, t + 1, w) = n_surv + n_place;
         p.n_births[w] = n_place;
+        p.newborn_base[w] = n_surv;
+        p.mut_pending[w] = n_place > 0 ? 1 : 0;
         unsigned long long *tot = p.totals;
         if (w == 0) atomicAdd(tot + 0, 1ull);
         atomicAdd(tot + 1, (unsigned long long)n_start);
@@ -542,22 +522,22 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
 // ------------------------------------------------------------------- a5 mutation
 // "an agent's weights are mutated by adding noise sampled from N(0, sigma)",
 // sigma = 0.02 a standard deviation (R23).  One item = one canonical group q = j >> 2 of
-// one child: one Philox call, two fp64 Box-Muller pairs, four weights.  Runs after the
-// rank phase advanced t, so the step of the birth is p.t[w] - 1.
+// one child: one Philox call (MUTATE, birth step, child cell, q), two fp64 Box-Muller
+// pairs, four weights.  Runs after the rank phase advanced t: the birth step is t - 1.
+// Each child's item count is published in mut_done (release) so that the policy kernel
+// can wait for exactly its newborn's weights.
 struct MutItem {
     const float *wp;
     float *wc;
-    int q;
+    int q, b;
     double z[4];
 };
 
-// load the item's birth, draw its Philox block and transform it (no dependent loads
-// other than the birth record, so two items per thread overlap their fp64 chains)
 __device__ __forceinline__ MutItem mutate_prepare(const DevParams &p, int w, int64_t t, size_t k, int groups) {
     MutItem it;
-    const int b = (int)(k / groups);
-    it.q = (int)(k - (size_t)b * groups);
-    const size_t bs = (size_t)w * p.S + b;
+    it.b = (int)(k / groups);
+    it.q = (int)(k - (size_t)it.b * groups);
+    const size_t bs = (size_t)w * p.S + it.b;
     const int child = p.birth_child[bs], parent = p.birth_parent[bs], cellc = p.birth_cell[bs];
     it.wp = p.weights + ((size_t)w * p.S + parent) * (size_t)p.Pd;
     it.wc = p.weights + ((size_t)w * p.S + child) * (size_t)p.Pd;
@@ -577,26 +557,52 @@ __device__ __forceinline__ void mutate_write(const DevParams &p, const MutItem &
     }
 }
 
-// All mutation items of all worlds: grid-stride over (birth, group) items world by world,
-// two items per thread per iteration.
+// publish one completed item of birth b (release: the item's writes happen-before)
+__device__ __forceinline__ void mutate_publish(const DevParams &p, int w, int b, int valid) {
+    // lanes of a warp usually share b: aggregate with a match
+    const unsigned act = __activemask();
+    const int key = valid ? b : -1;
+    const unsigned peers = __match_any_sync(act, key);
+    const int leader = __ffs(peers) - 1;
+    if (valid && (int)(threadIdx.x & 31) == leader) {
+        int *ctr = p.mut_done + (size_t)w * p.S + b;
+        const int n = __popc(peers);
+        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(n) : "memory");
+    }
+}
+
+// All mutation items of the pending worlds: grid-stride over (birth, group) items world by
+// world, two items per thread per iteration.  Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const int groups = (p.P + 3) >> 2;
     for (int w = 0; w < p.n_worlds; ++w) {
+        if (!*reinterpret_cast<volatile int32_t *>(p.mut_pending + w)) continue;
         const size_t n = (size_t)(*reinterpret_cast<volatile int32_t *>(p.n_births + w)) * groups;
-        if (n == 0) continue;
-        const int64_t t = p.t[w] - 1;  // the rank phase already advanced t
-        for (size_t k = gtid; k < n; k += 2 * gthreads) {
-            const size_t k2 = k + gthreads;
-            const MutItem a = mutate_prepare(p, w, t, k, groups);
-            if (k2 < n) {
-                const MutItem b = mutate_prepare(p, w, t, k2, groups);
-                mutate_write(p, a);
-                mutate_write(p, b);
-            } else {
-                mutate_write(p, a);
-            }
+        const int64_t t = p.t[w] - 1;
+        const size_t lane = gtid & 31;
+        for (size_t base = gtid - lane; base < n; base += 2 * gthreads) {
+            const size_t k = base + lane, k2 = k + gthreads;
+            const bool ok1 = k < n, ok2 = k2 < n;
+            MutItem a, b;
+            if (ok1) a = mutate_prepare(p, w, t, k, groups);
+            if (ok2) b = mutate_prepare(p, w, t, k2, groups);
+            if (ok1) mutate_write(p, a);
+            if (ok2) mutate_write(p, b);
+            __syncwarp();
+            mutate_publish(p, w, ok1 ? a.b : 0, ok1);
+            mutate_publish(p, w, ok2 ? b.b : 0, ok2);
         }
     }
+}
+
+// Wait (one lane) until birth b of world w has all its items written (acquire).
+__device__ __forceinline__ void mutate_wait(const DevParams &p, int w, int b) {
+    const int groups = (p.P + 3) >> 2;
+    const int *ctr = p.mut_done + (size_t)w * p.S + b;
+    int v;
+    do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < groups);
 }
 
 }  // namespace eco

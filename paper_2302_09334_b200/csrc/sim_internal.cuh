@@ -13,7 +13,7 @@
 //  * alive slots: a u8 flag per slot plus a bitmap [world][SW]; the live agents of step t
 //    are listed (any order: no result depends on it) in alive_list[t&1].
 //  * reproduction: per-cell birth direction bdir (0..3 = N,S,E,W, 0xFF none), per-cell
-//    winning parent bparent, and a birth bitmap bbits[t&1] over cells (plane layout).
+//    parent slot bslot, and a claimed-cell bitmap bbits[t&1] over cells (plane layout).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -48,7 +48,10 @@ struct DevParams {
     const uint32_t *T;        // [H][4] Bernoulli thresholds
     unsigned long long *claim;   // [n_worlds][H*W] move claims (0 = none)
     uint8_t *bdir;               // [n_worlds][H*W] birth direction of the agent on the cell
-    int32_t *bparent;            // [n_worlds][H*W] winning parent slot of a child cell
+    int32_t *bslot;              // [n_worlds][H*W] slot of the parent standing on the cell
+    int32_t *mut_done;           // [n_worlds][S] by birth rank: mutation items completed
+    int32_t *mut_pending;        // [n_worlds] children of the last step still need weights
+    int32_t *newborn_base;       // [n_worlds] list position of the last step's first child
     uint8_t *alive, *last_action, *ate;
     uint32_t *alive_bits;        // [n_worlds][SW]
     int32_t *cell, *energy, *age, *repr;
@@ -193,15 +196,17 @@ size_t init_agents_scratch_bytes(const DevParams &p);
 cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
-cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+// policy kernel; with_mutation = 1 runs the pending children's mutation as a prologue
+// (cooperative launch: newborn warps wait for their weights)
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, int with_mutation, cudaStream_t s);
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
-cudaError_t launch_birth_win(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);
+// standalone mutation of the pending children, then clears mut_pending
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
 cudaError_t post_occupancy(int *blocks_per_sm);
-cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned int *bar, cudaStream_t s);
+cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s);
 
 // state conversion (canonical <-> device)
 cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);

@@ -1,12 +1,12 @@
 // step.cu — the kernels of one world step (sm_100a).
 //
-// Graph mode (sim_step): two launches per step,
-//   k_policy  a2 observation + a3 per-agent LSTM/head/argmax + the claim half of a4
-//   k_post    cooperative persistent kernel: a4 move/consume/physiology/death | grid sync |
-//             a1 regrowth of step t+1 (it needs only R'' of step t) + a5 birth candidates |
-//             sync | birth winners | sync | birth rank/placement per world, t += 1 | sync |
-//             mutation of the children
-// (the first step after create/set_state is preceded by a standalone k_regrow).
+// Graph mode (sim_step): two cooperative launches per step,
+//   k_policy  [mutation of the previous step's children] + a2 observation + a3 per-agent
+//             LSTM/head/argmax + the claim half of a4
+//   k_post    a4 move/consume/physiology/death | grid barrier | a1 regrowth of step t+1 +
+//             a5 birth candidates | grid barrier | a5 rank/winners/placement, t += 1
+// (the first step after create/set_state is preceded by a standalone k_regrow; state
+// export first completes any pending mutation with the standalone k_mutate).
 // Instrumented mode (sim_step_timed): the same phases as separate kernels, timed one by one.
 #include "phases.cuh"
 
@@ -17,11 +17,24 @@ __device__ __constant__ int kDX[5] = {0, 0, 0, 1, -1};
 
 // streaming 16-B load of per-agent weights: read once per step, no reuse inside the
 // step, so keep them out of L1 (L2 still serves re-reads across steps when they fit).
-__device__ __forceinline__ float4 ld_weights4(const float *ptr) {
+// `fresh` weights (a child written earlier in the same kernel) take the coherent L2 path.
+__device__ __forceinline__ float4 ld_weights4(const float *ptr, bool fresh) {
     float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(ptr));
+    if (fresh)
+        asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "l"(ptr));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "l"(ptr));
+    return v;
+}
+
+__device__ __forceinline__ float ld_weight(const float *ptr, bool fresh) {
+    float v;
+    if (fresh) asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
+    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
     return v;
 }
 
@@ -45,8 +58,13 @@ __device__ __forceinline__ void flush_counters(const DevParams &p, int w, unsign
 //   a    = argmax, lowest index on ties; margin < 1e-4 counted as a near-tie (R28)
 // then the move claim of a4: a valid non-stay move posts (MOVE draw << 32 | ~cell) with
 // atomicMax on claim[target] (R14).
+//
+// with_mutation: the children placed by the previous step's rank phase get their weights
+// here first (every warp runs its share of the mutation items before any agent); a warp
+// whose agent is such a child waits for that child's items (mut_done) before reading its
+// weights, through the coherent L2 path.  Requires a cooperative launch (co-residency).
 template <int HD>
-__global__ void __launch_bounds__(256) k_policy(DevParams p) {
+__global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutation) {
     constexpr int G = HD;
     constexpr int AG = 32 / HD;  // agents per warp
     constexpr int U = 8;         // sparse columns in flight per lane
@@ -86,6 +104,7 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
             nxt->t = tw + 1;
         }
     }
+    if (with_mutation) mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 
     int acc_w = -1;
     unsigned long long acc_nnz = 0ull, acc_ties = 0ull;
@@ -100,6 +119,16 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
         if (!__any_sync(FULL, active)) continue;
         const int slot = active ? list_of(p, t, w)[i] : 0;
         const size_t gs = (size_t)w * p.S + slot;
+        // a child of the previous step whose weights are being written in this kernel
+        bool fresh = false;
+        if (with_mutation && active && p.mut_pending[w]) {
+            const int b = i - p.newborn_base[w];
+            if (b >= 0 && b < p.n_births[w]) {
+                fresh = true;
+                if (k == 0) mutate_wait(p, w, b);
+            }
+        }
+        __syncwarp();
 
         // ---- a2: observation bitmask (channel 0 = R' after regrowth, 1 = O_t incl. self)
         uint64_t m_lo = 0ull, m_hi = 0ull;
@@ -144,7 +173,7 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
                     idx = 64 + __ffsll((long long)r_hi) - 1;
                     r_hi &= r_hi - 1;
                 }
-                vv[u] = idx >= 0 ? ld_weights4(Wa + ((size_t)idx * HD + k) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                vv[u] = idx >= 0 ? ld_weights4(Wa + ((size_t)idx * HD + k) * 4, fresh) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -162,7 +191,7 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
             float4 vv[UH];
 #pragma unroll
             for (int u = 0; u < UH; ++u)
-                vv[u] = active ? ld_weights4(Whh + ((j0 + u) * HD + k) * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                vv[u] = active ? ld_weights4(Whh + ((j0 + u) * HD + k) * 4, fresh) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < UH; ++u) {
                 const float hj = __shfl_sync(FULL, hk, j0 + u, G);
@@ -172,7 +201,7 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
                 acc.w = fmaf(hj, vv[u].w, acc.w);
             }
         }
-        const float4 bb = active ? ld_weights4(Wa + p.off_b + k * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 bb = active ? ld_weights4(Wa + p.off_b + k * 4, fresh) : make_float4(0.f, 0.f, 0.f, 0.f);
         acc.x += bb.x;
         acc.y += bb.y;
         acc.z += bb.z;
@@ -188,10 +217,10 @@ __global__ void __launch_bounds__(256) k_policy(DevParams p) {
         float lg[5];
 #pragma unroll
         for (int a = 0; a < 5; ++a) {
-            float s = active ? __ldg(Wa + p.off_out + a * HD + k) * hn : 0.f;
+            float s = active ? ld_weight(Wa + p.off_out + a * HD + k, fresh) * hn : 0.f;
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
-            lg[a] = s + (active ? __ldg(Wa + p.off_bout + a) : 0.f);
+            lg[a] = s + (active ? ld_weight(Wa + p.off_bout + a, fresh) : 0.f);
         }
 
         if (active) {
@@ -260,15 +289,29 @@ cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
     }
 }
 
-cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
+template <typename Kernel, typename... Args>
+cudaError_t launch_coop(Kernel kernel, int blocks, int threads, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, int with_mutation, cudaStream_t s) {
     switch (p.Hd) {
-        case 4: k_policy<4><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
-        case 8: k_policy<8><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
-        case 16: k_policy<16><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
-        case 32: k_policy<32><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
+        case 4: return launch_coop(k_policy<4>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
+        case 8: return launch_coop(k_policy<8>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
+        case 16: return launch_coop(k_policy<16>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
+        case 32: return launch_coop(k_policy<32>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 // ----------------------------------------------------------- standalone phase kernels
@@ -284,10 +327,6 @@ __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
     birth_claim_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
-__global__ void __launch_bounds__(256) k_birth_win(DevParams p) {
-    birth_win_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
-}
-
 constexpr int RANK_THREADS = 1024;
 __global__ void __launch_bounds__(RANK_THREADS) k_birth_rank(DevParams p) {
     __shared__ uint32_t scratch[RANK_THREADS / 32 + 1];
@@ -299,33 +338,40 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
     mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
+__global__ void k_clear_pending(DevParams p) {
+    for (int w = threadIdx.x; w < p.n_worlds; w += blockDim.x) p.mut_pending[w] = 0;
+}
+
 // ------------------------------------------------------------------------ k_post
+// a4 move/consume/physiology/death | barrier | a1 regrowth of step t+1 (needs only R'' of
+// step t) + a5 birth candidates and claimed cells | barrier | a5 rank, winners, placement,
+// counters, t += 1.  (The children's weights are written by the next k_policy.)
 constexpr int POST_THREADS = 512;
-__global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned int *bar) {
+constexpr int POST_BARRIERS = 2;
+__global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned long long *bar) {
     __shared__ uint32_t scratch[POST_THREADS / 32 + 1];
     __shared__ int2 rowq[POST_THREADS];
     // warp-interleaved global index: consecutive warps of work land on different blocks
     // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
     const size_t gtid = interleaved_gtid();
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
+    unsigned long long target = grid_sync_base(bar, POST_BARRIERS);
     // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
     const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
     uint64_t t0 = clk ? globaltimer_ns() : 0ull, t1;
     move_phase(p, gtid, gthreads);
-    grid_sync(bar);
+    grid_sync(bar, target);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 0, t1 - t0); t0 = t1; }
-    regrow_phase(p, 1, gtid, gthreads);  // step t+1's regrowth, off the critical path
+    regrow_phase(p, 1, gtid, gthreads);
     birth_claim_phase(p, gtid, gthreads);
-    grid_sync(bar);
+    grid_sync(bar, target);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 1, t1 - t0); t0 = t1; }
-    birth_win_phase(p, gtid, gthreads);
-    grid_sync(bar);
-    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 2, t1 - t0); t0 = t1; }
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<POST_THREADS>(p, w, scratch, rowq);
-    grid_sync(bar);
-    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 3, t1 - t0); t0 = t1; }
-    mutate_phase(p, gtid, gthreads);
-    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 4, t1 - t0); }
+    if (clk) {
+        t1 = globaltimer_ns();
+        atomicAdd(p.phase_ns + 2, t1 - t0);
+        grid_sync_done(bar);
+    }
 }
 
 // --------------------------------------------------------------------------- launchers
@@ -350,12 +396,6 @@ cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_birth_win(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
-    if (p.S == 0) return cudaSuccess;
-    k_birth_win<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
     return cudaGetLastError();
@@ -364,6 +404,9 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
     k_mutate<<<lc.post_blocks, 256, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_clear_pending<<<1, 64, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -371,18 +414,8 @@ cudaError_t post_occupancy(int *blocks_per_sm) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post, POST_THREADS, 0);
 }
 
-cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned int *bar, cudaStream_t s) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(lc.post_blocks);
-    cfg.blockDim = dim3(POST_THREADS);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_post, p, bar);
+cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
+    return launch_coop(k_post, lc.post_blocks, POST_THREADS, s, p, bar);
 }
 
 }  // namespace eco
