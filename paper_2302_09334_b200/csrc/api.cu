@@ -134,7 +134,6 @@ struct sim_ctx {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     bool regrown_ahead = false;
-    bool mutation_pending = false;       // the last graph step's children lack weights
     unsigned long long *bar = nullptr;   // grid-barrier words of k_post
     int64_t t = 0;
     int32_t *nonfinite_host = nullptr;
@@ -193,7 +192,7 @@ constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5};
 cudaError_t launch_phase(sim_ctx *h, int k) {
     switch (k) {
         case 0: return eco::launch_regrow(h->p, 1, h->stream);
-        case 1: return eco::launch_policy(h->p, h->lc, 0, h->stream);
+        case 1: return eco::launch_policy(h->p, h->lc, h->stream);
         case 2: return eco::launch_move(h->p, h->lc, h->stream);
         case 3: return eco::launch_birth_claim(h->p, h->lc, h->stream);
         case 4: return eco::launch_birth_rank(h->p, h->stream);
@@ -201,21 +200,11 @@ cudaError_t launch_phase(sim_ctx *h, int k) {
     }
 }
 
-// graph-mode step: the policy kernel (with the previous step's mutation as prologue), then
-// the cooperative post-policy kernel
+// graph-mode step: the policy kernel, then the cooperative post-policy kernel
 cudaError_t enqueue_step(sim_ctx *h) {
     cudaError_t e;
-    if ((e = eco::launch_policy(h->p, h->lc, 1, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_policy(h->p, h->lc, h->stream)) != cudaSuccess) return e;
     return eco::launch_post(h->p, h->lc, h->bar, h->stream);
-}
-
-// children placed by the last graph step get their weights in the next k_policy; before
-// any state export, import or instrumented step, write them now
-cudaError_t flush_mutation(sim_ctx *h) {
-    if (!h->mutation_pending) return cudaSuccess;
-    cudaError_t e = eco::launch_mutate(h->p, h->lc, h->stream);
-    if (e == cudaSuccess) h->mutation_pending = false;
-    return e;
 }
 
 // the regrowth of the current step, needed once after create/set_state
@@ -343,9 +332,6 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.claim, S ? nw * HW : 1), "alloc");
     CKC(dalloc(h, &p.bdir, S ? nw * HW : 1), "alloc");
     CKC(dalloc(h, &p.bslot, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.mut_done, nw * S), "alloc");
-    CKC(dalloc(h, &p.mut_pending, nw), "alloc");
-    CKC(dalloc(h, &p.newborn_base, nw), "alloc");
     CKC(dalloc(h, &p.alive_bits, nw * (size_t)d.SW), "alloc");
     CKC(dalloc(h, &p.alive, nw * S), "alloc");
     CKC(dalloc(h, &p.last_action, nw * S), "alloc");
@@ -389,9 +375,11 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     // launch configuration: persistent-style grids sized to the 148 SMs
     int bps = 0;
     CKC(eco::policy_occupancy(d.Hd, 256, &bps), "occupancy");
+    CKC(eco::policy_prepare(), "kernel attributes");
     if (bps < 1) bps = 1;
     h->lc.policy_threads = 256;
     h->lc.policy_blocks = prop.multiProcessorCount * bps;
+    h->lc.sms = prop.multiProcessorCount;
     h->lc.agent_threads = 256;
     {
         const long need = ((long)nw * S + 255) / 256;
@@ -463,7 +451,6 @@ sim_status sim_step(sim_handle h, int64_t n) {
     CK(h, ensure_regrown(h), "regrow");
     for (int64_t i = 0; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
     h->t += n;
-    h->mutation_pending = true;
     return SIM_OK;
 }
 
@@ -472,7 +459,6 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
-    CK(h, flush_mutation(h), "mutation");
     CK(h, ensure_regrown(h), "regrow");
     CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
     for (int i = 0; i < SIM_NUM_KERNELS; ++i) {
@@ -499,7 +485,6 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
-    CK(h, flush_mutation(h), "mutation");
     if ((st = sync(h)) != SIM_OK) return st;
     const Derived &d = h->d;
     const DevParams &p = h->p;
@@ -554,7 +539,6 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     if (!in) return fail(SIM_E_INVALID, "invalid argument: in (NULL)");
     if (in->t < 0 || in->t >= ((int64_t)1 << 32)) return fail(SIM_E_INVALID, "invalid field: t");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
-    CK(h, flush_mutation(h), "mutation");
     if ((st = sync(h)) != SIM_OK) return st;
     const Derived &d = h->d;
     DevParams &p = h->p;
@@ -641,7 +625,6 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemsetAsync(p.row_wins, 0, 2 * nw * (size_t)d.H * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
-    CK(h, cudaMemsetAsync(p.mut_pending, 0, nw * 4, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     h->regrown_ahead = false;
     return sync(h);

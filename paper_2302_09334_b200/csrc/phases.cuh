@@ -6,8 +6,7 @@
 //   birth_claim_phase  a5  lazy move-claim reset, birth candidate, claimed-cell dedup
 //   birth_rank_world   a5  (one block per world) free slots, claimed cells in row-major
 //                          order, claim winners, placement, counters, t += 1
-//   mutate_phase       a5  children's weights (run by the NEXT step's policy kernel in
-//                          graph mode, or standalone)
+//   mutate_phase       a5  children's weights (coalesced, one device weight per item)
 //
 // Data written by one phase and read by a later phase of the same kernel is read with
 // plain (coherent) loads, never through the read-only path.
@@ -363,7 +362,6 @@ __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t
 // cells with a warp scan of the row's bitmap words.  (3) One thread per rank r resolves the
 // winner of cell c_r and places the child in free slot F[r] (R22); every later claimed cell
 // is deferred for capacity.  Then the step's counters, the next alive count and t += 1.
-// The children's weights are written by mutate_phase (they are marked pending here).
 __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t, int c, int r, int n_surv) {
     const size_t HW = (size_t)p.H * p.W;
     const uint32_t *O = p.occ + (size_t)w * plane_words(p);
@@ -405,7 +403,6 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
     p.repr[(size_t)w * p.S + parent] = 0;
     p.birth_child[(size_t)w * p.S + r] = child;
     p.birth_parent[(size_t)w * p.S + r] = parent;
-    p.mut_done[(size_t)w * p.S + r] = 0;
     list_of(p, t + 1, w)[n_surv + r] = child;
 }
 
@@ -504,8 +501,6 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
         rec->resources = p.res_count[w];
         *count_of(p, t + 1, w) = n_surv + n_place;
         p.n_births[w] = n_place;
-        p.newborn_base[w] = n_surv;
-        p.mut_pending[w] = n_place > 0 ? 1 : 0;
         unsigned long long *tot = p.totals;
         if (w == 0) atomicAdd(tot + 0, 1ull);
         atomicAdd(tot + 1, (unsigned long long)n_start);
@@ -521,88 +516,63 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
 
 // ------------------------------------------------------------------- a5 mutation
 // "an agent's weights are mutated by adding noise sampled from N(0, sigma)",
-// sigma = 0.02 a standard deviation (R23).  One item = one canonical group q = j >> 2 of
-// one child: one Philox call (MUTATE, birth step, child cell, q), two fp64 Box-Muller
-// pairs, four weights.  Runs after the rank phase advanced t: the birth step is t - 1.
-// Each child's item count is published in mut_done (release) so that the policy kernel
-// can wait for exactly its newborn's weights.
-struct MutItem {
-    const float *wp;
-    float *wc;
-    int q, b;
-    double z[4];
-};
+// sigma = 0.02 a standard deviation (R23).  The noise of canonical weight j comes from the
+// Philox block (MUTATE, birth step, child cell, q = j >> 2): words (w0,w1) give z[4q],
+// z[4q+1], (w2,w3) give z[4q+2], z[4q+3] via fp64 Box-Muller.  One item = one DEVICE
+// weight position of one child (consecutive threads write consecutive addresses); it
+// recomputes the Philox block and the half of the Box-Muller pair it needs.  Runs after
+// the rank phase advanced t, so the birth step is p.t[w] - 1.
 
-__device__ __forceinline__ MutItem mutate_prepare(const DevParams &p, int w, int64_t t, size_t k, int groups) {
-    MutItem it;
-    it.b = (int)(k / groups);
-    it.q = (int)(k - (size_t)it.b * groups);
-    const size_t bs = (size_t)w * p.S + it.b;
-    const int child = p.birth_child[bs], parent = p.birth_parent[bs], cellc = p.birth_cell[bs];
-    it.wp = p.weights + ((size_t)w * p.S + parent) * (size_t)p.Pd;
-    it.wc = p.weights + ((size_t)w * p.S + child) * (size_t)p.Pd;
-    const uint4 d = draw4(p.seeds[w], PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)it.q);
-    box_muller(d.x, d.y, it.z[0], it.z[1]);
-    box_muller(d.z, d.w, it.z[2], it.z[3]);
-    return it;
-}
-
-__device__ __forceinline__ void mutate_write(const DevParams &p, const MutItem &it) {
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const int j = 4 * it.q + m;
-        if (j >= p.P) break;
-        const int dd = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
-        it.wc[dd] = __fadd_rn(it.wp[dd], __double2float_rn(__dmul_rn(p.mutation_std, it.z[m])));
+// device weight index d -> canonical index j (-1 for padding)
+__device__ __forceinline__ int dev_to_canon(int d, const DevParams &p) {
+    const int Hd = p.Hd, G = 4 * Hd, HD4 = Hd * 4;
+    if (d < p.off_hh) {
+        const int col = d / HD4, rem = d - col * HD4;
+        return ((rem & 3) * Hd + (rem >> 2)) * p.I + col;
     }
-}
-
-// publish one completed item of birth b (release: the item's writes happen-before)
-__device__ __forceinline__ void mutate_publish(const DevParams &p, int w, int b, int valid) {
-    // lanes of a warp usually share b: aggregate with a match
-    const unsigned act = __activemask();
-    const int key = valid ? b : -1;
-    const unsigned peers = __match_any_sync(act, key);
-    const int leader = __ffs(peers) - 1;
-    if (valid && (int)(threadIdx.x & 31) == leader) {
-        int *ctr = p.mut_done + (size_t)w * p.S + b;
-        const int n = __popc(peers);
-        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ctr), "r"(n) : "memory");
+    if (d < p.off_b) {
+        const int dd = d - p.off_hh, col = dd / HD4, rem = dd - col * HD4;
+        return G * p.I + ((rem & 3) * Hd + (rem >> 2)) * Hd + col;
     }
+    if (d < p.off_out) {
+        const int rem = d - p.off_b;
+        return G * p.I + G * Hd + (rem & 3) * Hd + (rem >> 2);
+    }
+    if (d < p.off_bout + 5) return G * p.I + G * Hd + G + (d - p.off_out);
+    return -1;
 }
 
-// All mutation items of the pending worlds: grid-stride over (birth, group) items world by
-// world, two items per thread per iteration.  Must be called by all 32 lanes of a warp.
+// z of canonical j for (step t, child cell): bit-identical to box_muller()'s za / zb
+__device__ __forceinline__ double gauss_of(uint64_t seed, int64_t t, int cellc, int j) {
+    const uint4 d = draw4(seed, PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)(j >> 2));
+    const int m = j & 3;
+    const uint32_t wa = m < 2 ? d.x : d.z, wb = m < 2 ? d.y : d.w;
+    const double two_m32 = 2.3283064365386963e-10;
+    const double u1 = __dmul_rn(__dadd_rn((double)wa, 1.0), two_m32);
+    const double u2 = __dmul_rn((double)wb, two_m32);
+    const double rad = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+    const double th = __dmul_rn(6.283185307179586, u2);
+    return __dmul_rn(rad, (m & 1) ? sin(th) : cos(th));
+}
+
 __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
-    const int groups = (p.P + 3) >> 2;
     for (int w = 0; w < p.n_worlds; ++w) {
-        if (!*reinterpret_cast<volatile int32_t *>(p.mut_pending + w)) continue;
-        const size_t n = (size_t)(*reinterpret_cast<volatile int32_t *>(p.n_births + w)) * groups;
+        const int nb = *reinterpret_cast<volatile int32_t *>(p.n_births + w);
+        if (nb == 0) continue;
+        const size_t n = (size_t)nb * p.Pd;
         const int64_t t = p.t[w] - 1;
-        const size_t lane = gtid & 31;
-        for (size_t base = gtid - lane; base < n; base += 2 * gthreads) {
-            const size_t k = base + lane, k2 = k + gthreads;
-            const bool ok1 = k < n, ok2 = k2 < n;
-            MutItem a, b;
-            if (ok1) a = mutate_prepare(p, w, t, k, groups);
-            if (ok2) b = mutate_prepare(p, w, t, k2, groups);
-            if (ok1) mutate_write(p, a);
-            if (ok2) mutate_write(p, b);
-            __syncwarp();
-            mutate_publish(p, w, ok1 ? a.b : 0, ok1);
-            mutate_publish(p, w, ok2 ? b.b : 0, ok2);
+        const uint64_t seed = p.seeds[w];
+        for (size_t k = gtid; k < n; k += gthreads) {
+            const int b = (int)(k / p.Pd), d = (int)(k - (size_t)b * p.Pd);
+            const int j = dev_to_canon(d, p);
+            if (j < 0) continue;
+            const size_t bs = (size_t)w * p.S + b;
+            const int child = p.birth_child[bs], parent = p.birth_parent[bs], cellc = p.birth_cell[bs];
+            const float wp = p.weights[((size_t)w * p.S + parent) * p.Pd + d];
+            const double z = gauss_of(seed, t, cellc, j);
+            p.weights[((size_t)w * p.S + child) * p.Pd + d] = __fadd_rn(wp, __double2float_rn(__dmul_rn(p.mutation_std, z)));
         }
     }
-}
-
-// Wait (one lane) until birth b of world w has all its items written (acquire).
-__device__ __forceinline__ void mutate_wait(const DevParams &p, int w, int b) {
-    const int groups = (p.P + 3) >> 2;
-    const int *ctr = p.mut_done + (size_t)w * p.S + b;
-    int v;
-    do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    } while (v < groups);
 }
 
 }  // namespace eco

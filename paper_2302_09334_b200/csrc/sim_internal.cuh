@@ -49,9 +49,6 @@ struct DevParams {
     unsigned long long *claim;   // [n_worlds][H*W] move claims (0 = none)
     uint8_t *bdir;               // [n_worlds][H*W] birth direction of the agent on the cell
     int32_t *bslot;              // [n_worlds][H*W] slot of the parent standing on the cell
-    int32_t *mut_done;           // [n_worlds][S] by birth rank: mutation items completed
-    int32_t *mut_pending;        // [n_worlds] children of the last step still need weights
-    int32_t *newborn_base;       // [n_worlds] list position of the last step's first child
     uint8_t *alive, *last_action, *ate;
     uint32_t *alive_bits;        // [n_worlds][SW]
     int32_t *cell, *energy, *age, *repr;
@@ -189,6 +186,7 @@ struct LaunchCfg {
     int policy_blocks, policy_threads;
     int agent_blocks, agent_threads;
     int post_blocks;  // co-resident blocks of the cooperative k_post
+    int sms;          // multiprocessors (one k_policy_tma CTA each)
 };
 
 cudaError_t launch_init_resources(const DevParams &p, cudaStream_t s);
@@ -196,13 +194,11 @@ size_t init_agents_scratch_bytes(const DevParams &p);
 cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
-// policy kernel; with_mutation = 1 runs the pending children's mutation as a prologue
-// (cooperative launch: newborn warps wait for their weights)
-cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, int with_mutation, cudaStream_t s);
+cudaError_t policy_prepare();  // kernel attributes (dynamic shared memory of k_policy_tma)
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);
-// standalone mutation of the pending children, then clears mut_pending
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
 cudaError_t post_occupancy(int *blocks_per_sm);

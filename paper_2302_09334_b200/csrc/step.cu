@@ -1,12 +1,14 @@
 // step.cu — the kernels of one world step (sm_100a).
 //
-// Graph mode (sim_step): two cooperative launches per step,
-//   k_policy  [mutation of the previous step's children] + a2 observation + a3 per-agent
-//             LSTM/head/argmax + the claim half of a4
-//   k_post    a4 move/consume/physiology/death | grid barrier | a1 regrowth of step t+1 +
-//             a5 birth candidates | grid barrier | a5 rank/winners/placement, t += 1
-// (the first step after create/set_state is preceded by a standalone k_regrow; state
-// export first completes any pending mutation with the standalone k_mutate).
+// Graph mode (sim_step): two launches per step,
+//   k_policy_tma  (Hd = 32)  a2 observation + a3 per-agent LSTM/head/argmax + the claim
+//                 half of a4; each warp streams its agents' weights with 1-D TMA bulk
+//                 copies (cp.async.bulk) through a 3-stage shared-memory pipeline
+//   k_policy_reg  (Hd = 4, 8, 16) the same step with register loads, lane groups of Hd
+//   k_post        cooperative: a4 move/consume/physiology/death | grid barrier | a1
+//                 regrowth of step t+1 + a5 birth candidates | barrier | a5 rank, winners,
+//                 placement, t += 1 | barrier | a5 mutation of the children
+// (the first step after create/set_state is preceded by a standalone k_regrow).
 // Instrumented mode (sim_step_timed): the same phases as separate kernels, timed one by one.
 #include "phases.cuh"
 
@@ -14,29 +16,6 @@ namespace eco {
 
 __device__ __constant__ int kDY[5] = {0, -1, 1, 0, 0};  // stay, N, S, E, W (R13)
 __device__ __constant__ int kDX[5] = {0, 0, 0, 1, -1};
-
-// streaming 16-B load of per-agent weights: read once per step, no reuse inside the
-// step, so keep them out of L1 (L2 still serves re-reads across steps when they fit).
-// `fresh` weights (a child written earlier in the same kernel) take the coherent L2 path.
-__device__ __forceinline__ float4 ld_weights4(const float *ptr, bool fresh) {
-    float4 v;
-    if (fresh)
-        asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                     : "l"(ptr));
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                     : "l"(ptr));
-    return v;
-}
-
-__device__ __forceinline__ float ld_weight(const float *ptr, bool fresh) {
-    float v;
-    if (fresh) asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
-    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
-    return v;
-}
 
 __device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
 
@@ -48,68 +27,383 @@ __device__ __forceinline__ void flush_counters(const DevParams &p, int w, unsign
     if (ties) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->near_ties), ties);
 }
 
-// ------------------------------------------------------------------------- K2 policy
-// Lane group of HD lanes per live agent (warp per agent at Hd = 32); lane k owns hidden
-// unit k and its four gate rows (i, f, g, o).
-//   x    : the (2r+1)^2 x 2 window of (R', O_t) as a bitmask in registers
-//   z    = sum over ACTIVE inputs j of W_ih^T[j][k][:]  +  sum_j h_j W_hh^T[j][k][:]  + b[k][:]
-//          (x is binary, so only the columns with x_j = 1 are read: the algorithmic bytes)
-//   c'   = f*c + i*g,  h' = o*tanh(c'),  logits = W_out h' + b_out
-//   a    = argmax, lowest index on ties; margin < 1e-4 counted as a near-tie (R28)
-// then the move claim of a4: a valid non-stay move posts (MOVE draw << 32 | ~cell) with
-// atomicMax on claim[target] (R14).
+// Per-lane accumulation of the policy counters of a world (flushed on world change/end).
+struct PolicyCounters {
+    int w = -1;
+    unsigned long long nnz = 0ull, ties = 0ull;
+    __device__ __forceinline__ void add(const DevParams &p, int ww, unsigned long long n, bool tie) {
+        if (ww != w) {
+            flush_counters(p, w, nnz, ties);
+            w = ww;
+            nnz = ties = 0ull;
+        }
+        nnz += n;
+        ties += tie ? 1ull : 0ull;
+    }
+    __device__ __forceinline__ void flush(const DevParams &p) { flush_counters(p, w, nnz, ties); }
+};
+
+// ------------------------------------------------------------- a2 observation mask
+// The (2r+1)^2 x 2 window of (R' after regrowth, O_t incl. self) around (y, x) as a
+// bitmask: input index ch*(2r+1)^2 + row*(2r+1) + col (R10, R11).
+// Lane l < 2(2r+1) fetches one row of one channel; the rows are OR-reduced over the
+// warp (or the lane group `gmask`), so every lane of the group ends with the full mask.
+__device__ __forceinline__ void obs_mask(const DevParams &p, int w, int64_t t, int y, int x, int l, int stride,
+                                         unsigned gmask, uint64_t &m_lo, uint64_t &m_hi) {
+    const int wd = 2 * p.r + 1;
+    uint64_t lo = 0ull, hi = 0ull;
+    for (int q = l; q < 2 * wd; q += stride) {
+        const int ch = q / wd, row = q - ch * wd;
+        const int yy = y - p.r + row;
+        if (yy < 0 || yy >= p.H) continue;
+        const uint32_t *pl = ch ? p.occ + (size_t)w * plane_words(p) : plane_next(p, t) + (size_t)w * plane_words(p);
+        const uint64_t bits = row_bits(pl + (size_t)yy * p.WW, p.WW, x - p.r, wd);
+        const int pos = ch * wd * wd + row * wd;
+        if (pos < 64) {
+            lo |= bits << pos;
+            if (pos + wd > 64) hi |= bits >> (64 - pos);
+        } else {
+            hi |= bits << (pos - 64);
+        }
+    }
+    const uint32_t a0 = __reduce_or_sync(gmask, (uint32_t)lo), a1 = __reduce_or_sync(gmask, (uint32_t)(lo >> 32));
+    const uint32_t a2 = __reduce_or_sync(gmask, (uint32_t)hi), a3 = __reduce_or_sync(gmask, (uint32_t)(hi >> 32));
+    m_lo = ((uint64_t)a1 << 32) | a0;
+    m_hi = ((uint64_t)a3 << 32) | a2;
+}
+
+// ------------------------------------------------------------ agent epilogue (a3, a4)
+// argmax (lowest index on exact ties), near-tie flag (margin < 1e-4, R28), forced action,
+// stored logits/action, and the move claim of a4: a valid non-stay move posts
+// (MOVE w0 << 32 | ~cell) with atomicMax on claim[target] (R14).  Called by the agent's
+// group leader only.
+__device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i, int slot, size_t gs, int64_t t,
+                                               int cellv, const float lg[5], unsigned nnz, PolicyCounters &ctr,
+                                               bool &bad) {
+    int best = 0;
+    float bestv = lg[0];
+#pragma unroll
+    for (int a = 1; a < 5; ++a)
+        if (lg[a] > bestv) {
+            bestv = lg[a];
+            best = a;
+        }
+    double second = -INFINITY;
+#pragma unroll
+    for (int a = 0; a < 5; ++a) {
+        if (a != best && (double)lg[a] > second) second = (double)lg[a];
+        bad = bad || !isfinite(lg[a]);
+        p.logits[gs * LOGIT_STRIDE + a] = lg[a];
+    }
+    ctr.add(p, w, nnz, (double)bestv - second < 1e-4);
+    int act = best;
+    if (*p.forced_on) {
+        const uint8_t f = p.forced[gs];
+        if (f != 255) act = f;
+    }
+    p.last_action[gs] = (uint8_t)act;
+    int tg = -1;
+    unsigned long long key = 0ull;
+    if (act != 0) {
+        const int y = cellv / p.W, x = cellv - y * p.W;
+        const int ty = y + kDY[act], tx = x + kDX[act];
+        if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
+            const int tc = ty * p.W + tx;
+            const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+            if (!get_bit(O, p, tc)) {
+                const uint4 d = draw4(p.seeds[w], PURPOSE_MOVE, (uint32_t)t, (uint32_t)cellv, 0u);
+                key = ((unsigned long long)d.x << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
+                atomicMax(p.claim + (size_t)w * p.H * p.W + tc, key);
+                tg = tc;
+            }
+        }
+    }
+    p.mrec[(size_t)w * p.S + i] = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
+}
+
+// housekeeping for the later phases of this step (any policy kernel runs it): the survivor
+// list of step t+1, the winner counters and the record of step t+1 (whose regrowth runs
+// early, inside this step's k_post) start at 0; the claimed-cell bitmap and row counts of
+// parity t+1 (used by step t-1) are cleared for step t+1.
+__device__ __forceinline__ void step_housekeeping(const DevParams &p) {
+    const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t gthreads = (size_t)gridDim.x * blockDim.x;
+    const size_t pw = plane_words(p);
+    for (size_t k = gtid; k < (size_t)p.n_worlds * pw; k += gthreads) {
+        const int w = (int)(k / pw);
+        bbits_of(p, p.t[w] + 1, w)[k - (size_t)w * pw] = 0u;
+    }
+    for (size_t k = gtid; k < (size_t)p.n_worlds * p.H; k += gthreads) {
+        const int w = (int)(k / p.H);
+        rows_of(p, p.t[w] + 1, w)[k - (size_t)w * p.H] = 0;
+    }
+    for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
+        const int64_t tw = p.t[w];
+        *count_of(p, tw + 1, (int)w) = 0;
+        p.n_win[w] = 0;
+        sim_step_record *nxt = record_of(p, tw + 1, (int)w);
+        *nxt = sim_step_record{};
+        nxt->t = tw + 1;
+    }
+}
+
+// ============================================================ k_policy_tma (Hd = 32)
+// Per live agent:
+//   z  = sum over ACTIVE inputs j of W_ih^T[j][k][:] + sum_j h_j W_hh^T[j][k][:] + b[k][:]
+//        (x is binary: only the nnz columns with x_j = 1 are read — the algorithmic bytes)
+//   c' = f*c + i*g,  h' = o*tanh(c'),  logits = W_out h' + b_out,  a = argmax   (R12, R28)
+// Lane k of the agent's warp owns hidden unit k and its gate rows (i, f, g, o).
 //
-// with_mutation: the children placed by the previous step's rank phase get their weights
-// here first (every warp runs its share of the mutation items before any agent); a warp
-// whose agent is such a child waits for that child's items (mut_done) before reading its
-// weights, through the coherent L2 path.  Requires a cooperative launch (co-residency).
+// Data movement: each warp owns STAGES shared-memory stages and one mbarrier per stage.
+// An agent is 1 + ceil(nnz/32) units: unit 0 = the contiguous [W_hh | b | W_out | b_out]
+// block (17,568 B, one bulk copy), then up to 32 active W_ih columns per unit (512 B each,
+// one bulk copy per column, issued by 32 lanes in parallel).  The warp keeps two units in
+// flight ahead of the one it computes; weights are streamed with an L2 evict-first policy
+// so the planes and claim buffers stay L2-resident.
+constexpr int TMA_WARPS = 4;
+constexpr int TMA_STAGES = 3;
+constexpr int TMA_STAGE_BYTES = 17664;  // >= max(17,568, 32 x 512), multiple of 128
+constexpr int TMA_SMEM = TMA_WARPS * TMA_STAGES * TMA_STAGE_BYTES;
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
+struct TmaAgent {
+    int w, i, slot, cellv, nunits;
+    size_t gs;
+    int64_t t;
+    uint64_t m_lo, m_hi;
+    unsigned nnz;
+    float hk, ck;
+};
+
+__global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[TMA_WARPS][TMA_STAGES];
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    step_housekeeping(p);
+    if (lane == 0)
+        for (int s = 0; s < TMA_STAGES; ++s) mbar_init(&bars[wib][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    uint8_t *stage_base = smem + (size_t)wib * TMA_STAGES * TMA_STAGE_BYTES;
+
+    // static interleaved agent assignment: agent index v = gw + m * nwarps (worlds flattened
+    // over their live-agent lists)
+    const int nwarps = gridDim.x * TMA_WARPS;
+    const int gw = wib * gridDim.x + blockIdx.x;  // consecutive agents on different SMs
+    const long total = (long)p.n_worlds * p.S;
+    long v_next = gw;  // next virtual index to examine
+    PolicyCounters ctr;
+
+    // fetch the next active agent (skipping empty virtual indices); returns false at end
+    auto next_agent = [&](TmaAgent &a) -> bool {
+        while (v_next < total) {
+            const long v = v_next;
+            v_next += nwarps;
+            const int w = (int)(v / p.S), i = (int)(v - (long)w * p.S);
+            const int64_t t = p.t[w];
+            if (i >= *count_of(p, t, w)) {
+                // lists are dense: skip the rest of this world
+                const long world_end = (long)(w + 1) * p.S;
+                while (v_next < world_end) v_next += nwarps;
+                continue;
+            }
+            a.w = w;
+            a.i = i;
+            a.t = t;
+            a.slot = list_of(p, t, w)[i];
+            a.gs = (size_t)w * p.S + a.slot;
+            a.cellv = p.cell[a.gs];
+            a.hk = p.h[a.gs * 32 + lane];
+            a.ck = p.c[a.gs * 32 + lane];
+            const int y = a.cellv / p.W, x = a.cellv - y * p.W;
+            obs_mask(p, w, t, y, x, lane, 32, FULL, a.m_lo, a.m_hi);
+            a.nnz = (unsigned)(__popcll(a.m_lo) + __popcll(a.m_hi));
+            a.nunits = 1 + (int)((a.nnz + 31) / 32);
+            return true;
+        }
+        return false;
+    };
+
+    // issue unit u of agent a into stage s (all lanes participate)
+    auto issue = [&](const TmaAgent &a, int u, int s) {
+        uint8_t *dst = stage_base + (size_t)s * TMA_STAGE_BYTES;
+        uint64_t *bar = &bars[wib][s];
+        const float *Wa = p.weights + a.gs * (size_t)p.Pd;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (u == 0) {
+            const uint32_t bytes = (uint32_t)(p.Pd - p.off_hh) * 4u;  // W_hh | b | W_out | b_out (+pad)
+            if (lane == 0) {
+                mbar_expect_tx(bar, bytes);
+                bulk_g2s(dst, Wa + p.off_hh, bytes, bar, policy);
+            }
+        } else {
+            const unsigned r0 = (unsigned)(u - 1) * 32u;
+            const unsigned ncols = min(32u, a.nnz - r0);
+            if (lane == 0) mbar_expect_tx(bar, ncols * 512u);
+            __syncwarp();
+            // lane l looks at input columns l, l+32, l+64, l+96; rank = # active before it
+            for (int q = 0; q < 4; ++q) {
+                const int col = lane + 32 * q;
+                if (col >= p.I) break;
+                const uint64_t word = col < 64 ? a.m_lo : a.m_hi;
+                const int b = col & 63;
+                if (!((word >> b) & 1ull)) continue;
+                const uint64_t below = b ? (word & ((1ull << b) - 1ull)) : 0ull;
+                const unsigned rank = (unsigned)__popcll(below) + (col >= 64 ? (unsigned)__popcll(a.m_lo) : 0u);
+                if (rank >= r0 && rank < r0 + 32u)
+                    bulk_g2s(dst + (size_t)(rank - r0) * 512, Wa + (size_t)col * 128, 512u, bar, policy);
+            }
+        }
+    };
+
+    // the warp's unit sequence: units of agent A (current), then of agent B (lookahead)
+    TmaAgent A, B;
+    bool haveA = next_agent(A), haveB = haveA && next_agent(B);
+    int ua = 0;        // next unit of A to consume
+    int ia = 0, ib = 0;  // units issued of A / of B
+    uint32_t use[TMA_STAGES] = {0u, 0u, 0u};
+    int s_issue = 0, s_cons = 0, in_flight = 0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float wout[5], bout[5];  // head weights of A, taken from its unit 0
+
+    while (haveA) {
+        // keep two units in flight beyond the one being consumed
+        while (in_flight < TMA_STAGES) {
+            if (ia < A.nunits) {
+                issue(A, ia++, s_issue);
+            } else if (haveB && ib < B.nunits) {
+                issue(B, ib++, s_issue);
+            } else {
+                break;
+            }
+            s_issue = (s_issue + 1) % TMA_STAGES;
+            ++in_flight;
+        }
+        // consume unit ua of A
+        mbar_wait(&bars[wib][s_cons], use[s_cons] & 1u);
+        ++use[s_cons];
+        const uint8_t *src = stage_base + (size_t)s_cons * TMA_STAGE_BYTES;
+        if (ua == 0) {
+            const float4 *whh = reinterpret_cast<const float4 *>(src);
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) {
+                const float hj = __shfl_sync(FULL, A.hk, j);
+                const float4 v = whh[j * 32 + lane];
+                acc.x = fmaf(hj, v.x, acc.x);
+                acc.y = fmaf(hj, v.y, acc.y);
+                acc.z = fmaf(hj, v.z, acc.z);
+                acc.w = fmaf(hj, v.w, acc.w);
+            }
+            const float4 bb = whh[32 * 32 + lane];
+            acc.x += bb.x;
+            acc.y += bb.y;
+            acc.z += bb.z;
+            acc.w += bb.w;
+            const float *tail = reinterpret_cast<const float *>(src) + (p.off_out - p.off_hh);
+#pragma unroll
+            for (int a = 0; a < 5; ++a) {
+                wout[a] = tail[a * 32 + lane];
+                bout[a] = tail[5 * 32 + a];
+            }
+        } else {
+            const unsigned ncols = min(32u, A.nnz - (unsigned)(ua - 1) * 32u);
+            const float4 *cols = reinterpret_cast<const float4 *>(src);
+            for (unsigned c = 0; c < ncols; ++c) {
+                const float4 v = cols[c * 32 + lane];
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+        }
+        ++ua;
+        --in_flight;
+        const bool last = ua == A.nunits;
+        if (last) {
+            // gates and head
+            const float ig = sigmoidf_acc(acc.x);
+            const float fg = sigmoidf_acc(acc.y);
+            const float gg = tanhf(acc.z);
+            const float og = sigmoidf_acc(acc.w);
+            const float cn = fg * A.ck + ig * gg;
+            const float hn = og * tanhf(cn);
+            float lg[5];
+#pragma unroll
+            for (int a = 0; a < 5; ++a) {
+                float s = wout[a] * hn;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+                lg[a] = s + bout[a];
+            }
+            p.h[A.gs * 32 + lane] = hn;
+            p.c[A.gs * 32 + lane] = cn;
+            bool bad = !isfinite(hn) || !isfinite(cn);
+            if (lane == 0) agent_epilogue(p, A.w, A.i, A.slot, A.gs, A.t, A.cellv, lg, A.nnz, ctr, bad);
+            if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
+            acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            // advance: B becomes A
+            A = B;
+            haveA = haveB;
+            ia = ib;
+            ua = 0;
+            ib = 0;
+            haveB = haveA && next_agent(B);
+        }
+        s_cons = (s_cons + 1) % TMA_STAGES;
+        __syncwarp();
+    }
+    if (lane == 0) ctr.flush(p);
+}
+
+// ============================================================ k_policy_reg (Hd < 32)
+// The same step with register loads; a lane group of HD lanes per agent.
 template <int HD>
-__global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutation) {
+__global__ void __launch_bounds__(256) k_policy_reg(DevParams p) {
     constexpr int G = HD;
-    constexpr int AG = 32 / HD;  // agents per warp
-    constexpr int U = 8;         // sparse columns in flight per lane
+    constexpr int AG = 32 / HD;
+    constexpr int U = 8;
     constexpr int UH = HD < 8 ? HD : 8;
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int k = lane & (G - 1);
     const int grp = lane / G;
+    const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (grp * G));
     const int wib = threadIdx.x >> 5;
     const int warps_per_block = blockDim.x >> 5;
     const long total = (long)p.n_worlds * p.S;
     const long per_round = (long)gridDim.x * warps_per_block * AG;
-    const size_t HW = (size_t)p.H * p.W;
-
-    // housekeeping for the later phases of this step: the survivor list of step t+1, the
-    // winner counters and the record of step t+1 (whose regrowth runs early, inside this
-    // step's k_post) start at 0; the birth bitmap of parity t+1 (used by step t-1) is
-    // cleared for step t+1.
-    {
-        const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-        const size_t gthreads = (size_t)gridDim.x * blockDim.x;
-        const size_t pw = plane_words(p);
-        for (size_t k = gtid; k < (size_t)p.n_worlds * pw; k += gthreads) {
-            const int w = (int)(k / pw);
-            bbits_of(p, p.t[w] + 1, w)[k - (size_t)w * pw] = 0u;
-        }
-        for (size_t k = gtid; k < (size_t)p.n_worlds * p.H; k += gthreads) {
-            const int w = (int)(k / p.H);
-            rows_of(p, p.t[w] + 1, w)[k - (size_t)w * p.H] = 0;
-        }
-        for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
-            const int64_t tw = p.t[w];
-            *count_of(p, tw + 1, (int)w) = 0;
-            p.n_win[w] = 0;
-            sim_step_record *nxt = record_of(p, tw + 1, (int)w);
-            *nxt = sim_step_record{};
-            nxt->t = tw + 1;
-        }
-    }
-    if (with_mutation) mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
-
-    int acc_w = -1;
-    unsigned long long acc_nnz = 0ull, acc_ties = 0ull;
+    step_housekeeping(p);
+    PolicyCounters ctr;
     for (long base = 0; base < total; base += per_round) {
-        // consecutive agents go to different CTAs so a small population spreads over all SMs
         const long v = base + (long)(wib * AG + grp) * gridDim.x + blockIdx.x;
         const bool in_range = v < total;
         const int w = in_range ? (int)(v / p.S) : 0;
@@ -119,45 +413,18 @@ __global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutatio
         if (!__any_sync(FULL, active)) continue;
         const int slot = active ? list_of(p, t, w)[i] : 0;
         const size_t gs = (size_t)w * p.S + slot;
-        // a child of the previous step whose weights are being written in this kernel
-        bool fresh = false;
-        if (with_mutation && active && p.mut_pending[w]) {
-            const int b = i - p.newborn_base[w];
-            if (b >= 0 && b < p.n_births[w]) {
-                fresh = true;
-                if (k == 0) mutate_wait(p, w, b);
-            }
-        }
-        __syncwarp();
-
-        // ---- a2: observation bitmask (channel 0 = R' after regrowth, 1 = O_t incl. self)
         uint64_t m_lo = 0ull, m_hi = 0ull;
-        int cellv = 0, y = 0, x = 0;
-        if (active) {
-            cellv = p.cell[gs];
-            y = cellv / p.W;
-            x = cellv - y * p.W;
-            const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
-            const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-            const int wd = 2 * p.r + 1;
-            for (int ch = 0; ch < 2; ++ch) {
-                const uint32_t *pl = ch ? O : Rn;
-                for (int row = 0; row < wd; ++row) {
-                    const int yy = y - p.r + row;
-                    if (yy < 0 || yy >= p.H) continue;
-                    const uint64_t bits = row_bits(pl + (size_t)yy * p.WW, p.WW, x - p.r, wd);
-                    const int pos = ch * wd * wd + row * wd;
-                    if (pos < 64) {
-                        m_lo |= bits << pos;
-                        if (pos + wd > 64) m_hi |= bits >> (64 - pos);
-                    } else {
-                        m_hi |= bits << (pos - 64);
-                    }
-                }
+        int cellv = 0;
+        if (active) cellv = p.cell[gs];
+        {
+            const int y = cellv / p.W, x = cellv - (cellv / p.W) * p.W;
+            uint64_t lo, hi;
+            obs_mask(p, w, t, y, x, active ? k : 1 << 20, G, gmask, lo, hi);
+            if (active) {
+                m_lo = lo;
+                m_hi = hi;
             }
         }
-
-        // ---- a3: LSTM
         const float *Wa = p.weights + gs * (size_t)p.Pd;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         uint64_t r_lo = m_lo, r_hi = m_hi;
@@ -173,7 +440,8 @@ __global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutatio
                     idx = 64 + __ffsll((long long)r_hi) - 1;
                     r_hi &= r_hi - 1;
                 }
-                vv[u] = idx >= 0 ? ld_weights4(Wa + ((size_t)idx * HD + k) * 4, fresh) : make_float4(0.f, 0.f, 0.f, 0.f);
+                vv[u] = idx >= 0 ? __ldg(reinterpret_cast<const float4 *>(Wa + ((size_t)idx * HD + k) * 4))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -191,7 +459,8 @@ __global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutatio
             float4 vv[UH];
 #pragma unroll
             for (int u = 0; u < UH; ++u)
-                vv[u] = active ? ld_weights4(Whh + ((j0 + u) * HD + k) * 4, fresh) : make_float4(0.f, 0.f, 0.f, 0.f);
+                vv[u] = active ? __ldg(reinterpret_cast<const float4 *>(Whh + ((j0 + u) * HD + k) * 4))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < UH; ++u) {
                 const float hj = __shfl_sync(FULL, hk, j0 + u, G);
@@ -201,7 +470,8 @@ __global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutatio
                 acc.w = fmaf(hj, vv[u].w, acc.w);
             }
         }
-        const float4 bb = active ? ld_weights4(Wa + p.off_b + k * 4, fresh) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 bb = active ? __ldg(reinterpret_cast<const float4 *>(Wa + p.off_b + k * 4))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         acc.x += bb.x;
         acc.y += bb.y;
         acc.z += bb.z;
@@ -212,106 +482,49 @@ __global__ void __launch_bounds__(256, 3) k_policy(DevParams p, int with_mutatio
         const float og = sigmoidf_acc(acc.w);
         const float cn = fg * ck + ig * gg;
         const float hn = og * tanhf(cn);
-
-        // linear head: 5 group reductions
         float lg[5];
 #pragma unroll
         for (int a = 0; a < 5; ++a) {
-            float s = active ? ld_weight(Wa + p.off_out + a * HD + k, fresh) * hn : 0.f;
+            float s = active ? __ldg(Wa + p.off_out + a * HD + k) * hn : 0.f;
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, G);
-            lg[a] = s + (active ? ld_weight(Wa + p.off_bout + a, fresh) : 0.f);
+            lg[a] = s + (active ? __ldg(Wa + p.off_bout + a) : 0.f);
         }
-
         if (active) {
             p.h[gs * HD + k] = hn;
             p.c[gs * HD + k] = cn;
             bool bad = !isfinite(hn) || !isfinite(cn);
-            if (k == 0) {
-                int best = 0;
-                float bestv = lg[0];
-#pragma unroll
-                for (int a = 1; a < 5; ++a)
-                    if (lg[a] > bestv) {
-                        bestv = lg[a];
-                        best = a;
-                    }
-                double second = -INFINITY;
-#pragma unroll
-                for (int a = 0; a < 5; ++a) {
-                    if (a != best && (double)lg[a] > second) second = (double)lg[a];
-                    bad = bad || !isfinite(lg[a]);
-                    p.logits[gs * LOGIT_STRIDE + a] = lg[a];
-                }
-                // per-lane accumulation of the world's counters, flushed on world change
-                if (w != acc_w) {
-                    flush_counters(p, acc_w, acc_nnz, acc_ties);
-                    acc_w = w;
-                }
-                acc_ties += ((double)bestv - second < 1e-4) ? 1ull : 0ull;
-                acc_nnz += (unsigned long long)(__popcll(m_lo) + __popcll(m_hi));
-                int act = best;
-                if (*p.forced_on) {
-                    const uint8_t f = p.forced[gs];
-                    if (f != 255) act = f;
-                }
-                p.last_action[gs] = (uint8_t)act;
-                int tg = -1;
-                unsigned long long key = 0ull;
-                if (act != 0) {
-                    const int ty = y + kDY[act], tx = x + kDX[act];
-                    if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
-                        const int tc = ty * p.W + tx;
-                        const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-                        if (!get_bit(O, p, tc)) {
-                            const uint4 d = draw4(p.seeds[w], PURPOSE_MOVE, (uint32_t)t, (uint32_t)cellv, 0u);
-                            key = ((unsigned long long)d.x << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
-                            atomicMax(p.claim + (size_t)w * HW + tc, key);
-                            tg = tc;
-                        }
-                    }
-                }
-                p.mrec[(size_t)w * p.S + i] = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
-            }
+            if (k == 0)
+                agent_epilogue(p, w, i, slot, gs, t, cellv, lg, (unsigned)(__popcll(m_lo) + __popcll(m_hi)), ctr, bad);
             if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
         }
     }
-    flush_counters(p, acc_w, acc_nnz, acc_ties);
+    if (k == 0) ctr.flush(p);
 }
 
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
     switch (hidden) {
-        case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy<4>, threads, 0);
-        case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy<8>, threads, 0);
-        case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy<16>, threads, 0);
-        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy<32>, threads, 0);
+        case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<4>, threads, 0);
+        case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<8>, threads, 0);
+        case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<16>, threads, 0);
+        case 32: *blocks_per_sm = 1; return cudaSuccess;
         default: return cudaErrorInvalidValue;
     }
 }
 
-template <typename Kernel, typename... Args>
-cudaError_t launch_coop(Kernel kernel, int blocks, int threads, cudaStream_t s, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, args...);
+cudaError_t policy_prepare() {
+    return cudaFuncSetAttribute(k_policy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM);
 }
 
-cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, int with_mutation, cudaStream_t s) {
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     switch (p.Hd) {
-        case 4: return launch_coop(k_policy<4>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
-        case 8: return launch_coop(k_policy<8>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
-        case 16: return launch_coop(k_policy<16>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
-        case 32: return launch_coop(k_policy<32>, lc.policy_blocks, lc.policy_threads, s, p, with_mutation);
+        case 4: k_policy_reg<4><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
+        case 8: k_policy_reg<8><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
+        case 16: k_policy_reg<16><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
+        case 32: k_policy_tma<<<lc.sms, TMA_WARPS * 32, TMA_SMEM, s>>>(p); break;
         default: return cudaErrorInvalidValue;
     }
+    return cudaGetLastError();
 }
 
 // ----------------------------------------------------------- standalone phase kernels
@@ -338,16 +551,12 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
     mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
-__global__ void k_clear_pending(DevParams p) {
-    for (int w = threadIdx.x; w < p.n_worlds; w += blockDim.x) p.mut_pending[w] = 0;
-}
-
 // ------------------------------------------------------------------------ k_post
 // a4 move/consume/physiology/death | barrier | a1 regrowth of step t+1 (needs only R'' of
 // step t) + a5 birth candidates and claimed cells | barrier | a5 rank, winners, placement,
-// counters, t += 1.  (The children's weights are written by the next k_policy.)
+// counters, t += 1 | barrier | a5 mutation of the children.
 constexpr int POST_THREADS = 512;
-constexpr int POST_BARRIERS = 2;
+constexpr int POST_BARRIERS = 3;
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned long long *bar) {
     __shared__ uint32_t scratch[POST_THREADS / 32 + 1];
     __shared__ int2 rowq[POST_THREADS];
@@ -367,9 +576,12 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
     grid_sync(bar, target);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 1, t1 - t0); t0 = t1; }
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) birth_rank_world<POST_THREADS>(p, w, scratch, rowq);
+    grid_sync(bar, target);
+    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 2, t1 - t0); t0 = t1; }
+    mutate_phase(p, gtid, gthreads);
     if (clk) {
         t1 = globaltimer_ns();
-        atomicAdd(p.phase_ns + 2, t1 - t0);
+        atomicAdd(p.phase_ns + 3, t1 - t0);
         grid_sync_done(bar);
     }
 }
@@ -403,10 +615,7 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
 
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
-    k_mutate<<<lc.post_blocks, 256, 0, s>>>(p);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    k_clear_pending<<<1, 64, 0, s>>>(p);
+    k_mutate<<<lc.sms * 8, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -415,7 +624,17 @@ cudaError_t post_occupancy(int *blocks_per_sm) {
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
-    return launch_coop(k_post, lc.post_blocks, POST_THREADS, s, p, bar);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(lc.post_blocks);
+    cfg.blockDim = dim3(POST_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_post, p, bar);
 }
 
 }  // namespace eco
