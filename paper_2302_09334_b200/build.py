@@ -15,6 +15,9 @@ FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "-shared", "-cudart", "shared",
+    # plain loads are cached in L2 only: the cooperative kernel's phases read state written
+    # by other blocks earlier in the same launch, which a stale L1 line would hide
+    "-Xptxas", "-dlcm=cg",
 ]
 
 

@@ -78,8 +78,9 @@ __device__ __forceinline__ void obs_mask(const DevParams &p, int w, int64_t t, i
 // (MOVE w0 << 32 | ~cell) with atomicMax on claim[target] (R14).  Called by the agent's
 // group leader only.
 __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i, int slot, size_t gs, int64_t t,
-                                               int cellv, const float lg[5], unsigned nnz, PolicyCounters &ctr,
-                                               bool &bad) {
+                                               int cellv, const float lg[5], uint64_t m_lo, uint64_t m_hi,
+                                               int forced_on, PolicyCounters &ctr, bool &bad) {
+    const unsigned nnz = (unsigned)(__popcll(m_lo) + __popcll(m_hi));
     int best = 0;
     float bestv = lg[0];
 #pragma unroll
@@ -97,7 +98,7 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
     }
     ctr.add(p, w, nnz, (double)bestv - second < 1e-4);
     int act = best;
-    if (*p.forced_on) {
+    if (forced_on) {
         const uint8_t f = p.forced[gs];
         if (f != 255) act = f;
     }
@@ -109,8 +110,16 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
         const int ty = y + kDY[act], tx = x + kDX[act];
         if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
             const int tc = ty * p.W + tx;
-            const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-            if (!get_bit(O, p, tc)) {
+            // O_t of the target: the agent channel of the window already holds it (r >= 1)
+            bool occupied;
+            if (p.r >= 1) {
+                const int wd = 2 * p.r + 1;
+                const int bi = wd * wd + (p.r + kDY[act]) * wd + (p.r + kDX[act]);
+                occupied = ((bi < 64 ? (m_lo >> bi) : (m_hi >> (bi - 64))) & 1ull) != 0ull;
+            } else {
+                occupied = get_bit(p.occ + (size_t)w * plane_words(p), p, tc) != 0u;
+            }
+            if (!occupied) {
                 const uint4 d = draw4(p.seeds[w], PURPOSE_MOVE, (uint32_t)t, (uint32_t)cellv, 0u);
                 key = ((unsigned long long)d.x << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
                 atomicMax(p.claim + (size_t)w * p.H * p.W + tc, key);
@@ -154,24 +163,34 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
 //   c' = f*c + i*g,  h' = o*tanh(c'),  logits = W_out h' + b_out,  a = argmax   (R12, R28)
 // Lane k of the agent's warp owns hidden unit k and its gate rows (i, f, g, o).
 //
-// Data movement: each warp owns STAGES shared-memory stages and one mbarrier per stage.
-// An agent is 1 + ceil(nnz/32) units: unit 0 = the contiguous [W_hh | b | W_out | b_out]
-// block (17,568 B, one bulk copy), then up to 32 active W_ih columns per unit (512 B each,
-// one bulk copy per column, issued by 32 lanes in parallel).  The warp keeps two units in
-// flight ahead of the one it computes; weights are streamed with an L2 evict-first policy
-// so the planes and claim buffers stay L2-resident.
+// Data movement: each warp owns TMA_STAGES shared-memory stages with one mbarrier each and
+// streams a sequence of units through them, keeping up to TMA_STAGES units in flight:
+//   unit 0 of an agent  = the contiguous [W_hh | b | W_out | b_out] block (17,664 B) plus
+//                         its h and c (128 B each): three 1-D TMA bulk copies
+//                         (cp.async.bulk ... complete_tx), expect_tx by lane 0;
+//   units 1.. (<= 32 each) = the agent's active W_ih columns, 512 B each: one cp.async
+//                         (16 B per lane, LDGSTS) warp instruction per column, completion
+//                         counted by cp.async.mbarrier.arrive.noinc of all 32 lanes.
+// Every stage's mbarrier expects 32 arrivals.  Weights stream with an L2 evict-first
+// policy so planes, lists and claims stay L2-resident.  Observation masks are computed
+// 32 agents at a time (one per lane) into a per-warp ring, so no agent waits on its
+// window gather.
 constexpr int TMA_WARPS = 4;
 constexpr int TMA_STAGES = 3;
-constexpr int TMA_STAGE_BYTES = 17664;  // >= max(17,568, 32 x 512), multiple of 128
+constexpr int TMA_STAGE_BYTES = 17920;  // 17,664 (W_hh|b|W_out|b_out|pad) + 128 (h) + 128 (c)
+constexpr int TMA_RING = 64;
 constexpr int TMA_SMEM = TMA_WARPS * TMA_STAGES * TMA_STAGE_BYTES;
 
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ uint32_t smem_addr(const void *ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
 }
@@ -191,132 +210,180 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 
-struct TmaAgent {
-    int w, i, slot, cellv, nunits;
-    size_t gs;
-    int64_t t;
-    uint64_t m_lo, m_hi;
-    unsigned nnz;
-    float hk, ck;
+struct __align__(16) AgentRec {
+    uint64_t lo, hi;   // observation mask
+    int w, i, slot, cell;
 };
+
+// lane-local observation mask (all 2(2r+1) rows by one lane)
+__device__ __forceinline__ void obs_mask_lane(const DevParams &p, int w, int64_t t, int y, int x, uint64_t &m_lo,
+                                              uint64_t &m_hi) {
+    const int wd = 2 * p.r + 1;
+    const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
+    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+    uint64_t lo = 0ull, hi = 0ull;
+#pragma unroll 2
+    for (int q = 0; q < 2 * wd; ++q) {
+        const int ch = q / wd, row = q - ch * wd;
+        const int yy = y - p.r + row;
+        if (yy < 0 || yy >= p.H) continue;
+        const uint64_t bits = row_bits((ch ? O : Rn) + (size_t)yy * p.WW, p.WW, x - p.r, wd);
+        const int pos = ch * wd * wd + row * wd;
+        if (pos < 64) {
+            lo |= bits << pos;
+            if (pos + wd > 64) hi |= bits >> (64 - pos);
+        } else {
+            hi |= bits << (pos - 64);
+        }
+    }
+    m_lo = lo;
+    m_hi = hi;
+}
 
 __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bars[TMA_WARPS][TMA_STAGES];
+    __shared__ AgentRec ring_all[TMA_WARPS][TMA_RING];
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     step_housekeeping(p);
     if (lane == 0)
-        for (int s = 0; s < TMA_STAGES; ++s) mbar_init(&bars[wib][s], 1);
+        for (int s = 0; s < TMA_STAGES; ++s) mbar_init(&bars[wib][s], 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
+    const int forced_on = *p.forced_on;
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     uint8_t *stage_base = smem + (size_t)wib * TMA_STAGES * TMA_STAGE_BYTES;
+    AgentRec *ring = ring_all[wib];
+    const uint32_t u0_bytes = (uint32_t)(p.Pd - p.off_hh) * 4u;  // 17,664 at Hd=32, I=98
 
-    // static interleaved agent assignment: agent index v = gw + m * nwarps (worlds flattened
-    // over their live-agent lists)
+    // static interleaved assignment over the flattened (world, list position) space
     const int nwarps = gridDim.x * TMA_WARPS;
-    const int gw = wib * gridDim.x + blockIdx.x;  // consecutive agents on different SMs
     const long total = (long)p.n_worlds * p.S;
-    long v_next = gw;  // next virtual index to examine
-    PolicyCounters ctr;
+    long v_next = wib * gridDim.x + blockIdx.x;  // consecutive agents on different SMs
+    int filled = 0;                              // ring entries written (monotonic)
 
-    // fetch the next active agent (skipping empty virtual indices); returns false at end
-    auto next_agent = [&](TmaAgent &a) -> bool {
+    // fill the ring with the next <= 32 live agents (one per lane); false at the end
+    auto refill = [&]() -> bool {
         while (v_next < total) {
-            const long v = v_next;
-            v_next += nwarps;
-            const int w = (int)(v / p.S), i = (int)(v - (long)w * p.S);
-            const int64_t t = p.t[w];
-            if (i >= *count_of(p, t, w)) {
-                // lists are dense: skip the rest of this world
-                const long world_end = (long)(w + 1) * p.S;
-                while (v_next < world_end) v_next += nwarps;
-                continue;
+            const long v = v_next + (long)lane * nwarps;
+            v_next += 32L * nwarps;
+            AgentRec rec;
+            bool act = false;
+            if (v < total) {
+                rec.w = (int)(v / p.S);
+                rec.i = (int)(v - (long)rec.w * p.S);
+                const int64_t t = p.t[rec.w];
+                if (rec.i < *count_of(p, t, rec.w)) {
+                    act = true;
+                    rec.slot = list_of(p, t, rec.w)[rec.i];
+                    rec.cell = p.cell[(size_t)rec.w * p.S + rec.slot];
+                    const int y = rec.cell / p.W;
+                    obs_mask_lane(p, rec.w, t, y, rec.cell - y * p.W, rec.lo, rec.hi);
+                }
             }
-            a.w = w;
-            a.i = i;
-            a.t = t;
-            a.slot = list_of(p, t, w)[i];
-            a.gs = (size_t)w * p.S + a.slot;
-            a.cellv = p.cell[a.gs];
-            a.hk = p.h[a.gs * 32 + lane];
-            a.ck = p.c[a.gs * 32 + lane];
-            const int y = a.cellv / p.W, x = a.cellv - y * p.W;
-            obs_mask(p, w, t, y, x, lane, 32, FULL, a.m_lo, a.m_hi);
-            a.nnz = (unsigned)(__popcll(a.m_lo) + __popcll(a.m_hi));
-            a.nunits = 1 + (int)((a.nnz + 31) / 32);
-            return true;
+            const unsigned m = __ballot_sync(FULL, act);
+            if (act) ring[(filled + __popc(m & ((1u << lane) - 1u))) % TMA_RING] = rec;
+            filled += __popc(m);
+            __syncwarp();
+            if (m) return true;
         }
         return false;
     };
+    auto nunits = [](const AgentRec &r) -> int {
+        return 1 + (int)(((unsigned)(__popcll(r.lo) + __popcll(r.hi)) + 31u) / 32u);
+    };
 
-    // issue unit u of agent a into stage s (all lanes participate)
-    auto issue = [&](const TmaAgent &a, int u, int s) {
+    // issue unit u of agent rec into stage s (all lanes)
+    auto issue = [&](const AgentRec &rec, int u, int s) {
         uint8_t *dst = stage_base + (size_t)s * TMA_STAGE_BYTES;
         uint64_t *bar = &bars[wib][s];
-        const float *Wa = p.weights + a.gs * (size_t)p.Pd;
+        const size_t gs = (size_t)rec.w * p.S + rec.slot;
+        const float *Wa = p.weights + gs * (size_t)p.Pd;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (u == 0) {
-            const uint32_t bytes = (uint32_t)(p.Pd - p.off_hh) * 4u;  // W_hh | b | W_out | b_out (+pad)
             if (lane == 0) {
-                mbar_expect_tx(bar, bytes);
-                bulk_g2s(dst, Wa + p.off_hh, bytes, bar, policy);
+                mbar_arrive_expect_tx(bar, u0_bytes + 256u);
+                bulk_g2s(dst, Wa + p.off_hh, u0_bytes, bar, policy);
+                bulk_g2s(dst + u0_bytes, p.h + gs * 32, 128u, bar, policy);
+                bulk_g2s(dst + u0_bytes + 128, p.c + gs * 32, 128u, bar, policy);
+            } else {
+                mbar_arrive(bar);
             }
         } else {
             const unsigned r0 = (unsigned)(u - 1) * 32u;
-            const unsigned ncols = min(32u, a.nnz - r0);
-            if (lane == 0) mbar_expect_tx(bar, ncols * 512u);
-            __syncwarp();
-            // lane l looks at input columns l, l+32, l+64, l+96; rank = # active before it
-            for (int q = 0; q < 4; ++q) {
-                const int col = lane + 32 * q;
-                if (col >= p.I) break;
-                const uint64_t word = col < 64 ? a.m_lo : a.m_hi;
-                const int b = col & 63;
-                if (!((word >> b) & 1ull)) continue;
-                const uint64_t below = b ? (word & ((1ull << b) - 1ull)) : 0ull;
-                const unsigned rank = (unsigned)__popcll(below) + (col >= 64 ? (unsigned)__popcll(a.m_lo) : 0u);
-                if (rank >= r0 && rank < r0 + 32u)
-                    bulk_g2s(dst + (size_t)(rank - r0) * 512, Wa + (size_t)col * 128, 512u, bar, policy);
+            uint64_t lo = rec.lo, hi = rec.hi;
+            unsigned rank = 0;
+            while (lo | hi) {  // warp-uniform walk over the active columns in order
+                int col;
+                if (lo) {
+                    col = __ffsll((long long)lo) - 1;
+                    lo &= lo - 1ull;
+                } else {
+                    col = 64 + __ffsll((long long)hi) - 1;
+                    hi &= hi - 1ull;
+                }
+                if (rank >= r0 + 32u) break;
+                if (rank >= r0) cp_async16(dst + (size_t)(rank - r0) * 512 + lane * 16, Wa + (size_t)col * 128 + lane * 4,
+                                           policy);
+                ++rank;
             }
+            cp_async_arrive(bar);
         }
     };
 
-    // the warp's unit sequence: units of agent A (current), then of agent B (lookahead)
-    TmaAgent A, B;
-    bool haveA = next_agent(A), haveB = haveA && next_agent(B);
-    int ua = 0;        // next unit of A to consume
-    int ia = 0, ib = 0;  // units issued of A / of B
-    uint32_t use[TMA_STAGES] = {0u, 0u, 0u};
+    PolicyCounters ctr;
+    uint32_t use[TMA_STAGES];
+#pragma unroll
+    for (int s = 0; s < TMA_STAGES; ++s) use[s] = 0u;
+    int pi = 0, ui = 0;  // issue cursor: ring position, unit
+    int pc = 0, uc = 0;  // consume cursor
     int s_issue = 0, s_cons = 0, in_flight = 0;
+    bool more = true;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float wout[5], bout[5];  // head weights of A, taken from its unit 0
+    float hk = 0.f, ck = 0.f;
+    float wout[5], bout[5];
 
-    while (haveA) {
-        // keep two units in flight beyond the one being consumed
+    while (true) {
         while (in_flight < TMA_STAGES) {
-            if (ia < A.nunits) {
-                issue(A, ia++, s_issue);
-            } else if (haveB && ib < B.nunits) {
-                issue(B, ib++, s_issue);
-            } else {
-                break;
+            if (pi == filled) {
+                if (!more || !(more = refill())) break;
             }
-            s_issue = (s_issue + 1) % TMA_STAGES;
+            const AgentRec rec = ring[pi % TMA_RING];
+            issue(rec, ui, s_issue);
+            s_issue = s_issue + 1 == TMA_STAGES ? 0 : s_issue + 1;
             ++in_flight;
+            if (++ui == nunits(rec)) {
+                ui = 0;
+                ++pi;
+            }
         }
-        // consume unit ua of A
-        mbar_wait(&bars[wib][s_cons], use[s_cons] & 1u);
-        ++use[s_cons];
+        if (in_flight == 0) break;
+        const AgentRec rec = ring[pc % TMA_RING];
+        uint32_t par = 0u;
+#pragma unroll
+        for (int s = 0; s < TMA_STAGES; ++s)
+            if (s == s_cons) par = use[s]++ & 1u;
+        mbar_wait(&bars[wib][s_cons], par);
         const uint8_t *src = stage_base + (size_t)s_cons * TMA_STAGE_BYTES;
-        if (ua == 0) {
+        if (uc == 0) {
+            const float *tail = reinterpret_cast<const float *>(src);
+            hk = tail[u0_bytes / 4 + lane];
+            ck = tail[u0_bytes / 4 + 32 + lane];
             const float4 *whh = reinterpret_cast<const float4 *>(src);
 #pragma unroll 8
             for (int j = 0; j < 32; ++j) {
-                const float hj = __shfl_sync(FULL, A.hk, j);
+                const float hj = __shfl_sync(FULL, hk, j);
                 const float4 v = whh[j * 32 + lane];
                 acc.x = fmaf(hj, v.x, acc.x);
                 acc.y = fmaf(hj, v.y, acc.y);
@@ -328,14 +395,14 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
             acc.y += bb.y;
             acc.z += bb.z;
             acc.w += bb.w;
-            const float *tail = reinterpret_cast<const float *>(src) + (p.off_out - p.off_hh);
 #pragma unroll
             for (int a = 0; a < 5; ++a) {
-                wout[a] = tail[a * 32 + lane];
-                bout[a] = tail[5 * 32 + a];
+                wout[a] = tail[(p.off_out - p.off_hh) + a * 32 + lane];
+                bout[a] = tail[(p.off_bout - p.off_hh) + a];
             }
         } else {
-            const unsigned ncols = min(32u, A.nnz - (unsigned)(ua - 1) * 32u);
+            const unsigned nnz = (unsigned)(__popcll(rec.lo) + __popcll(rec.hi));
+            const unsigned ncols = min(32u, nnz - (unsigned)(uc - 1) * 32u);
             const float4 *cols = reinterpret_cast<const float4 *>(src);
             for (unsigned c = 0; c < ncols; ++c) {
                 const float4 v = cols[c * 32 + lane];
@@ -345,16 +412,14 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
                 acc.w += v.w;
             }
         }
-        ++ua;
         --in_flight;
-        const bool last = ua == A.nunits;
-        if (last) {
-            // gates and head
+        s_cons = s_cons + 1 == TMA_STAGES ? 0 : s_cons + 1;
+        if (++uc == nunits(rec)) {
             const float ig = sigmoidf_acc(acc.x);
             const float fg = sigmoidf_acc(acc.y);
             const float gg = tanhf(acc.z);
             const float og = sigmoidf_acc(acc.w);
-            const float cn = fg * A.ck + ig * gg;
+            const float cn = fg * ck + ig * gg;
             const float hn = og * tanhf(cn);
             float lg[5];
 #pragma unroll
@@ -364,21 +429,18 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
                 for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
                 lg[a] = s + bout[a];
             }
-            p.h[A.gs * 32 + lane] = hn;
-            p.c[A.gs * 32 + lane] = cn;
+            const size_t gs = (size_t)rec.w * p.S + rec.slot;
+            p.h[gs * 32 + lane] = hn;
+            p.c[gs * 32 + lane] = cn;
             bool bad = !isfinite(hn) || !isfinite(cn);
-            if (lane == 0) agent_epilogue(p, A.w, A.i, A.slot, A.gs, A.t, A.cellv, lg, A.nnz, ctr, bad);
+            if (lane == 0)
+                agent_epilogue(p, rec.w, rec.i, rec.slot, gs, p.t[rec.w], rec.cell, lg, rec.lo, rec.hi, forced_on, ctr,
+                               bad);
             if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
             acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            // advance: B becomes A
-            A = B;
-            haveA = haveB;
-            ia = ib;
-            ua = 0;
-            ib = 0;
-            haveB = haveA && next_agent(B);
+            uc = 0;
+            ++pc;
         }
-        s_cons = (s_cons + 1) % TMA_STAGES;
         __syncwarp();
     }
     if (lane == 0) ctr.flush(p);
@@ -494,8 +556,7 @@ __global__ void __launch_bounds__(256) k_policy_reg(DevParams p) {
             p.h[gs * HD + k] = hn;
             p.c[gs * HD + k] = cn;
             bool bad = !isfinite(hn) || !isfinite(cn);
-            if (k == 0)
-                agent_epilogue(p, w, i, slot, gs, t, cellv, lg, (unsigned)(__popcll(m_lo) + __popcll(m_hi)), ctr, bad);
+            if (k == 0) agent_epilogue(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, ctr, bad);
             if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
         }
     }
