@@ -12,6 +12,15 @@
 // Instrumented mode (sim_step_timed): the same phases as separate kernels, timed one by one.
 #include "phases.cuh"
 
+// cp.async with an .L2::cache_hint operand raised "illegal instruction" on the B200 pool
+// (driver 580.159), so the per-lane column copies use the default L2 policy.
+#ifndef ECO_CPASYNC_HINT
+#define ECO_CPASYNC_HINT 0
+#endif
+#ifndef ECO_SPARSE_BULK
+#define ECO_SPARSE_BULK 0
+#endif
+
 namespace eco {
 
 __device__ __constant__ int kDY[5] = {0, -1, 1, 0, 0};  // stay, N, S, E, W (R13)
@@ -188,11 +197,17 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+    uint64_t state;
+    asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(state) : "r"(smem_addr(bar)) : "memory");
+    (void)state;
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+    uint64_t state;
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 %0, [%1], %2;"
+                 : "=l"(state)
+                 : "r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
+    (void)state;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
@@ -211,12 +226,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t policy) {
+#if ECO_CPASYNC_HINT
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                  "l"(policy)
                  : "memory");
+#else
+    (void)policy;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 struct __align__(16) AgentRec {
@@ -324,6 +344,11 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
             const unsigned r0 = (unsigned)(u - 1) * 32u;
             uint64_t lo = rec.lo, hi = rec.hi;
             unsigned rank = 0;
+#if ECO_SPARSE_BULK
+            if (lane == 0)
+                mbar_arrive_expect_tx(bar, min(32u, (unsigned)(__popcll(lo) + __popcll(hi)) - r0) * 512u);
+            __syncwarp();
+#endif
             while (lo | hi) {  // warp-uniform walk over the active columns in order
                 int col;
                 if (lo) {
@@ -334,11 +359,20 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
                     hi &= hi - 1ull;
                 }
                 if (rank >= r0 + 32u) break;
+#if ECO_SPARSE_BULK
+                if (rank >= r0 && lane == 0) bulk_g2s(dst + (size_t)(rank - r0) * 512, Wa + (size_t)col * 128, 512u, bar, policy);
+                ++rank;
+                continue;
+#endif
                 if (rank >= r0) cp_async16(dst + (size_t)(rank - r0) * 512 + lane * 16, Wa + (size_t)col * 128 + lane * 4,
                                            policy);
                 ++rank;
             }
+#if ECO_SPARSE_BULK
+            if (lane != 0) mbar_arrive(bar);
+#else
             cp_async_arrive(bar);
+#endif
         }
     };
 

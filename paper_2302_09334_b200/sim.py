@@ -91,8 +91,8 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            path = _build.LIB
-            if not os.path.exists(path) or _build._stale():
+            path = os.environ.get("ECO_LIBSIM_OVERRIDE") or _build.LIB  # diagnostics: alternative build
+            if path == _build.LIB and (not os.path.exists(path) or _build._stale()):
                 _build.build()
             L = ctypes.CDLL(path)
             H = ctypes.c_void_p
