@@ -176,11 +176,10 @@ SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
 /* Graph mode runs everything after the policy kernel as one cooperative kernel whose
- * phases are separated by grid barriers: move, regrow(t+1)+birth candidates, birth rank
- * (the children's weights are written by the next policy kernel).  out[i] = summed
- * duration (ns, device global timer, as seen by block 0) of phase i over the steps since
- * the last reset; reset != 0 zeroes. */
-#define SIM_NUM_POST_PHASES 3
+ * phases are separated by grid barriers: move, regrow(t+1)+birth candidates, birth rank,
+ * mutation.  out[i] = summed duration (ns, device global timer, as seen by block 0) of
+ * phase i over the steps since the last reset; reset != 0 zeroes. */
+#define SIM_NUM_POST_PHASES 4
 SIM_API sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset);
 /* Synchronise the handle's stream (reports deferred errors). */
 SIM_API sim_status sim_synchronize(sim_handle h);

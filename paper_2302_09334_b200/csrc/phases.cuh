@@ -313,22 +313,31 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
                     const uint32_t *O = p.occ + (size_t)w * plane_words(p);
                     const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
                     const int y = cellv / p.W, x = cellv - y * p.W;
+                    // the four neighbours' O'' and R'' bits, loaded together (no dependent chain)
+                    bool freec[4];
+#pragma unroll
+                    for (int dd = 0; dd < 4; ++dd) {
+                        const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
+                        const bool in = cy >= 0 && cy < p.H && cx >= 0 && cx < p.W;
+                        const int c = in ? cy * p.W + cx : cellv;
+                        const uint32_t ob = get_bit(O, p, c), rb = get_bit(Rn, p, c);
+                        freec[dd] = in && !ob && !rb;
+                    }
                     const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
                     const int s0 = (int)(d.x & 3u);
+#pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const int dd = (s0 + kk) & 3;
-                        const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
-                        if (cy < 0 || cy >= p.H || cx < 0 || cx >= p.W) continue;
-                        const int c = cy * p.W + cx;
-                        if (get_bit(O, p, c) || get_bit(Rn, p, c)) continue;
-                        dir = (uint8_t)dd;
+                        if (dir == NO_DIR && freec[dd]) dir = (uint8_t)dd;
+                    }
+                    if (dir != NO_DIR) {
+                        const int cy = y + dir_dy(dir), c = cy * p.W + x + dir_dx(dir);
                         uint32_t bit;
                         const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
                         if (!(old & bit)) {
                             new_cell = 1;
                             atomicAdd(rows_of(p, t, w) + cy, 1);
                         }
-                        break;
                     }
                     if (dir == NO_DIR) no_cell = 1;
                     else cand = 1;
@@ -362,7 +371,10 @@ __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t
 // cells with a warp scan of the row's bitmap words.  (3) One thread per rank r resolves the
 // winner of cell c_r and places the child in free slot F[r] (R22); every later claimed cell
 // is deferred for capacity.  Then the step's counters, the next alive count and t += 1.
-__device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t, int c, int r, int n_surv) {
+constexpr int RANK_SMEM_CAP = 1024;  // births ranked in shared memory (more spill to global)
+
+__device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t, int c, int r, int n_surv,
+                                            int child) {
     const size_t HW = (size_t)p.H * p.W;
     const uint32_t *O = p.occ + (size_t)w * plane_words(p);
     const uint8_t *bd = p.bdir + (size_t)w * HW;
@@ -383,7 +395,6 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
         }
     }
     const int parent = p.bslot[(size_t)w * HW + qbest];
-    const int child = *reinterpret_cast<volatile int32_t *>(p.free_list + (size_t)w * p.S + r);
     const size_t cs = (size_t)w * p.S + child;
     p.alive[cs] = 1;
     atomicOr(p.alive_bits + (size_t)w * p.SW + (child >> 5), 1u << (child & 31));
@@ -407,7 +418,8 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
 }
 
 template <int NT>
-__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int2 *rowq) {
+__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int2 *rowq, int *s_free,
+                                 int *s_bcell) {
     constexpr int NWARP = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = p.t[w];
@@ -417,43 +429,41 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
     const int n_win = *reinterpret_cast<volatile int32_t *>(p.n_win + w);
     const int n_free = p.S - n_surv;
     const int n_place = n_win < n_free ? n_win : n_free;
+    int32_t *g_free = p.free_list + (size_t)w * p.S, *g_bcell = p.birth_cell + (size_t)w * p.S;
 
     if (n_place > 0) {
-        // (1) free slots
-        uint32_t running = 0u;
-        for (int w0 = 0; w0 < p.SW; w0 += NT) {
-            const int wi = w0 + tid;
-            uint32_t fr = 0u;
-            if (wi < p.SW) {
-                const int nbits = p.S - wi * 32;
+        // (1)+(2) in lock-step chunks: the first n_place free slots (alive bitmap) and the
+        // rows holding the first n_place claimed cells (per-row counts), then one warp per
+        // such row ranks its cells with a warp scan of the row's bitmap words
+        const uint32_t *bb = bbits_of(p, t, w);
+        const int32_t *rows = rows_of(p, t, w);
+        uint32_t run_f = 0u, run_r = 0u;
+        const int span = p.SW > p.H ? p.SW : p.H;
+        for (int k0 = 0; k0 < span; k0 += NT) {
+            const bool need_f = run_f < (uint32_t)n_place, need_r = run_r < (uint32_t)n_place;  // block-uniform
+            if (!need_f && !need_r) break;
+            const int i = k0 + tid;
+            uint32_t fr = 0u, cnt = 0u;
+            if (need_f && i < p.SW) {
+                const int nbits = p.S - i * 32;
                 const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
-                fr = ~ld_plain(p.alive_bits + (size_t)w * p.SW + wi) & valid;
+                fr = ~ld_plain(p.alive_bits + (size_t)w * p.SW + i) & valid;
             }
-            uint32_t tot;
-            const uint32_t ex = block_exclusive_scan<NT>((uint32_t)__popc(fr), scratch, tot);
-            uint32_t r = running + ex;
+            if (need_r && i < p.H) cnt = (uint32_t)*reinterpret_cast<const volatile int32_t *>(rows + i);
+            uint32_t tot_f, tot_r, nq;
+            const uint32_t ex_f = block_exclusive_scan<NT>((uint32_t)__popc(fr), scratch, tot_f);
+            const uint32_t ex_r = block_exclusive_scan<NT>(cnt, scratch, tot_r);
+            uint32_t r = run_f + ex_f;
             while (fr && r < (uint32_t)n_place) {
                 const int b = __ffs(fr) - 1;
                 fr &= fr - 1u;
-                p.free_list[(size_t)w * p.S + r] = wi * 32 + b;
+                if (r < RANK_SMEM_CAP) s_free[r] = i * 32 + b;
+                else g_free[r] = i * 32 + b;
                 ++r;
             }
-            running += tot;
-            if (running >= (uint32_t)n_place) break;
-        }
-        // (2) rows holding the first n_place claimed cells, then warp-per-row ranking
-        const uint32_t *bb = bbits_of(p, t, w);
-        const int32_t *rows = rows_of(p, t, w);
-        running = 0u;
-        for (int y0 = 0; y0 < p.H; y0 += NT) {
-            const int y = y0 + tid;
-            const uint32_t cnt = y < p.H ? (uint32_t)*reinterpret_cast<const volatile int32_t *>(rows + y) : 0u;
-            uint32_t tot;
-            const uint32_t ex = block_exclusive_scan<NT>(cnt, scratch, tot);
-            const uint32_t q = (cnt && running + ex < (uint32_t)n_place) ? 1u : 0u;
-            uint32_t nq;
+            const uint32_t q = (cnt && run_r + ex_r < (uint32_t)n_place) ? 1u : 0u;
             const uint32_t qi = block_exclusive_scan<NT>(q, scratch, nq);
-            if (q) rowq[qi] = make_int2(y, (int)(running + ex));
+            if (q) rowq[qi] = make_int2(i, (int)(run_r + ex_r));
             __syncthreads();
             for (uint32_t k = warp; k < nq; k += NWARP) {
                 const int yy = rowq[k].x;
@@ -468,37 +478,44 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
                         const uint32_t n = __shfl_up_sync(0xffffffffu, inc, o);
                         if (lane >= o) inc += n;
                     }
-                    uint32_t r = base + inc - pc;
-                    while (word && r < (uint32_t)n_place) {
+                    uint32_t rr = base + inc - pc;
+                    while (word && rr < (uint32_t)n_place) {
                         const int b = __ffs(word) - 1;
                         word &= word - 1u;
-                        p.birth_cell[(size_t)w * p.S + r] = yy * p.W + wx * 32 + b;
-                        ++r;
+                        const int c = yy * p.W + wx * 32 + b;
+                        if (rr < RANK_SMEM_CAP) s_bcell[rr] = c;
+                        else g_bcell[rr] = c;
+                        ++rr;
                     }
                     base += __shfl_sync(0xffffffffu, inc, 31);
                 }
             }
-            running += tot;
+            run_f += tot_f;
+            run_r += tot_r;
             __syncthreads();
-            if (running >= (uint32_t)n_place) break;
         }
         // (3) winners and placement, one birth per thread (independent dependency chains)
-        for (int r = tid; r < n_place; r += NT)
-            place_birth(p, w, t, *reinterpret_cast<volatile int32_t *>(p.birth_cell + (size_t)w * p.S + r), r, n_surv);
+        for (int r = tid; r < n_place; r += NT) {
+            const int c = r < RANK_SMEM_CAP ? s_bcell[r] : *reinterpret_cast<volatile int32_t *>(g_bcell + r);
+            const int child = r < RANK_SMEM_CAP ? s_free[r] : *reinterpret_cast<volatile int32_t *>(g_free + r);
+            g_bcell[r] = c;  // the mutation phase reads the birth lists from global memory
+            place_birth(p, w, t, c, r, n_surv, child);
+        }
     }
     __syncthreads();
     if (tid == 0) {
         volatile sim_step_record *rec = record_of(p, t, w);
-        const int64_t deaths = rec->deaths_energy + rec->deaths_age;
-        const int64_t grown = rec->grown, eaten = rec->eaten;
-        p.res_count[w] += grown - eaten;
+        const int64_t de = rec->deaths_energy, da = rec->deaths_age, grown = rec->grown, eaten = rec->eaten,
+                      dc = rec->deferred_claim;
+        const int64_t res = p.res_count[w] + grown - eaten;
+        p.res_count[w] = res;
         rec->t = t;
         rec->agents_at_start = n_start;
         rec->births = n_place;
-        rec->deferred_claim = rec->deferred_claim - n_win;  // candidates - claimed cells
+        rec->deferred_claim = dc - n_win;  // candidates - claimed cells
         rec->deferred_capacity = n_win - n_place;
         rec->population = n_surv + n_place;
-        rec->resources = p.res_count[w];
+        rec->resources = res;
         *count_of(p, t + 1, w) = n_surv + n_place;
         p.n_births[w] = n_place;
         unsigned long long *tot = p.totals;
@@ -506,7 +523,7 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
         atomicAdd(tot + 1, (unsigned long long)n_start);
         atomicAdd(tot + 2, (unsigned long long)HW);
         atomicAdd(tot + 3, (unsigned long long)n_place);
-        atomicAdd(tot + 4, (unsigned long long)deaths);
+        atomicAdd(tot + 4, (unsigned long long)(de + da));
         atomicAdd(tot + 5, (unsigned long long)eaten);
         atomicAdd(tot + 6, (unsigned long long)grown);
         p.t[w] = t + 1;

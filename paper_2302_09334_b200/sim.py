@@ -27,7 +27,7 @@ KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate
 EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns")
-POST_PHASES = ("move", "regrow_next+birth_claim", "birth_rank")
+POST_PHASES = ("move", "regrow_next+birth_claim", "birth_rank", "mutate")
 
 
 class SimError(RuntimeError):
