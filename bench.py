@@ -55,6 +55,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--no-flush", action="store_true",
+                    help="diagnostic: do not flush L2 between timed steps (the line says so in config.l2)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -200,7 +202,8 @@ def run_ours(args, rank, world_size, local_rank):
         barrier()
         torch.cuda.synchronize()
         for k in range(K):
-            flush.zero_()
+            if not args.no_flush:
+                flush.zero_()
             evs[k][0].record(stream)
             world.step(1)
             evs[k][1].record(stream)
@@ -209,6 +212,9 @@ def run_ours(args, rank, world_size, local_rank):
         clk = clocks.stop()
         world.synchronize()
         post_phases = {k_: v / K / 1e3 for k_, v in world.phase_ns().items()}
+        # k_post runs 512 threads per block: block 0 has 16 claim warps and 8 regrowth warps
+        for k_, nw in (("claim.warp_sum_b0", 16), ("regrow.warp_sum_b0", 8)):
+            post_phases[k_.replace(".warp_sum_b0", ".warp_mean")] = post_phases.pop(k_) / nw
         step_ms = np.array([a.elapsed_time(b) for a, b in evs], np.float64)
         total_ms = float(step_ms.sum())
         log = world.step_log(t0, K)
@@ -227,7 +233,8 @@ def run_ours(args, rank, world_size, local_rank):
             ksum = np.zeros(sim.NUM_KERNELS)
             ssum = 0.0
             for k in range(K):
-                flush.zero_()
+                if not args.no_flush:
+                    flush.zero_()
                 tm = world.step_timed()
                 ksum += np.array([tm[n] for n in sim.KERNEL_NAMES])
                 ssum += tm["step_ms"]
@@ -275,11 +282,13 @@ def run_ours(args, rank, world_size, local_rank):
                        "grid": f"{wc.rows}x{wc.cols}", "slots": wc.slots, "n_initial": wc.n_initial,
                        "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x2", "hidden": wc.hidden,
                        "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + K],
-                       "l2": "flushed between timed steps (256 MiB memset on the library stream)",
+                       "l2": "NOT flushed (diagnostic run)" if args.no_flush
+                       else "flushed between timed steps (256 MiB memset on the library stream)",
                        "parallelism": "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
                        else "single GPU", "global_batch": wc.slots * world_size},
             "cell_updates_per_s": cells * world_size / (max_ms / 1e3),
             "agents_mean": agents / K,
+            "births_mean": births / K,
             "gpu_launches": 2 * K,
             "post_phase_us_per_step": post_phases,
             "clocks": clk,

@@ -31,17 +31,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *(os.path.join(CSRC, s) for s in SOURCES), "-o", tmp]
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Build LIB (or, for diagnostic variants with extra -D defines, `out`)."""
+    lib = out or LIB
+    if not force and not defines and not _stale():
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *(f"-D{d}" for d in defines), *(os.path.join(CSRC, s) for s in SOURCES), "-o", tmp]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd, cwd=CSRC)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -111,7 +111,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * (size_t)d.Hd * 4 * 2;     // h, c
     b += nw * S * eco::LOGIT_STRIDE * 4;    // logits
     b += nw * S * (size_t)d.Pd * 4;         // weights
-    b += nw * S * 16 + 2 * nw * d.H * 4;    // move records, row winner counts
+    b += nw * S * 16;                       // move records
     b += nw * S * 4 * 7;                    // alive lists [2], free, birth lists, mutation counters
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
@@ -345,7 +345,6 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.logits, nw * S * eco::LOGIT_STRIDE), "alloc");
     CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
     CKC(dalloc(h, &p.mrec, nw * S), "alloc");
-    CKC(dalloc(h, &p.row_wins, 2 * nw * (size_t)d.H), "alloc");
     CKC(dalloc(h, &p.alive_list, 2 * nw * S), "alloc");
     CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
     CKC(dalloc(h, &p.n_win, nw), "alloc");
@@ -357,7 +356,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.res_count, nw), "alloc");
     CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");
     CKC(dalloc(h, &p.totals, 8), "alloc");
-    CKC(dalloc(h, &p.phase_ns, SIM_NUM_POST_PHASES), "alloc");
+    CKC(dalloc(h, &p.phase_ns, 16 + 4 * 2 * 1024), "alloc");  // + per-block clocks of diagnostic builds
     CKC(dalloc(h, &h->forced_dev, nw * S), "alloc");
     CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
     p.seeds = seeds_d;
@@ -622,7 +621,6 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
         CK(h, cudaMemsetAsync(p.bdir, 0xff, nw * HW, s), "memset");
     }
     CK(h, cudaMemsetAsync(p.bbits, 0, 2 * nw * d.pw * 4, s), "memset");
-    CK(h, cudaMemsetAsync(p.row_wins, 0, 2 * nw * (size_t)d.H * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
@@ -669,9 +667,10 @@ sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset) {
     if (st != SIM_OK) return st;
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     if (out)
-        CK(h, cudaMemcpyAsync(out, h->p.phase_ns, SIM_NUM_POST_PHASES * 8, cudaMemcpyDeviceToHost, h->stream),
+        CK(h, cudaMemcpyAsync(out, h->p.phase_ns, (reset < 0 ? 16 + 4 * 2 * 1024 : SIM_NUM_POST_PHASES) * 8,
+                              cudaMemcpyDeviceToHost, h->stream),
            "phase clock");
-    if (reset) CK(h, cudaMemsetAsync(h->p.phase_ns, 0, SIM_NUM_POST_PHASES * 8, h->stream), "phase clock");
+    if (reset > 0) CK(h, cudaMemsetAsync(h->p.phase_ns, 0, (16 + 4 * 2 * 1024) * 8, h->stream), "phase clock");
     return sync(h);
 }
 

@@ -38,4 +38,53 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
     return res;
 }
 
+// Two independent exclusive scans (a and b) sharing the block barriers.  `warp_tot` holds
+// 2 * (NT/32 + 1) words.
+template <int NT>
+__device__ __forceinline__ uint2 block_exclusive_scan2(uint2 v, uint32_t *warp_tot, uint2 &total) {
+    static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t ia = v.x, ib = v.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t na = __shfl_up_sync(0xffffffffu, ia, o), nb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) {
+            ia += na;
+            ib += nb;
+        }
+    }
+    uint32_t *ta = warp_tot, *tb = warp_tot + NW + 1;
+    if (lane == 31) {
+        ta[wid] = ia;
+        tb[wid] = ib;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t wa = lane < NW ? ta[lane] : 0u, wb = lane < NW ? tb[lane] : 0u;
+        uint32_t xa = wa, xb = wb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t na = __shfl_up_sync(0xffffffffu, xa, o), nb = __shfl_up_sync(0xffffffffu, xb, o);
+            if (lane >= o) {
+                xa += na;
+                xb += nb;
+            }
+        }
+        if (lane < NW) {
+            ta[lane] = xa - wa;
+            tb[lane] = xb - wb;
+        }
+        if (lane == NW - 1) {
+            ta[NW] = xa;
+            tb[NW] = xb;
+        }
+    }
+    __syncthreads();
+    const uint2 res = make_uint2(ta[wid] + ia - v.x, tb[wid] + ib - v.y);
+    total = make_uint2(ta[NW], tb[NW]);
+    __syncthreads();
+    return res;
+}
+
 }  // namespace eco

@@ -14,6 +14,13 @@
 #include "block_scan.cuh"
 #include "sim_internal.cuh"
 
+#ifndef ECO_DIAG_SKIP
+// diagnostic builds only (results are wrong): 1 skips the birth claims, 2 the regrowth in
+// k_post, 4 the mutation maths, 8 the regrowth's counter atomics, 16 its plane stores,
+// 32 its atomics replaced by plain stores, 64 its loads made non-volatile
+#define ECO_DIAG_SKIP 0
+#endif
+
 namespace eco {
 
 // ------------------------------------------------------------------ grid barrier
@@ -114,7 +121,9 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
         for (int dw = -1; dw <= 1; ++dw) {
             const int ww = wx + dw;
             win[dy + 2][dw + 1] =
-                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
+                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW)
+                    ? ((ECO_DIAG_SKIP & 64) ? __ldcg(src + (size_t)yy * p.WW + ww) : ld_plain(src + (size_t)yy * p.WW + ww))
+                    : 0u;
         }
     }
     const uint32_t cur = win[2][1];
@@ -157,7 +166,7 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
             if (word_of(d, m) < thr) grow |= 1u << b;
         }
     }
-    dst[(size_t)y * p.WW + wx] = cur | grow;
+    if (!(ECO_DIAG_SKIP & 16)) dst[(size_t)y * p.WW + wx] = cur | grow;
     return __popc(grow);
 }
 
@@ -176,6 +185,11 @@ __device__ __forceinline__ void regrow_phase(const DevParams &p, int ahead, size
             const size_t r = k - (size_t)w * per_world;
             const int y = (int)(r / real_words), wx = (int)(r - (size_t)y * real_words);
             cnt = (unsigned long long)regrow_word(p, w, y, wx, p.t[w] + ahead);
+            if (ECO_DIAG_SKIP & 8) cnt = 0;
+        }
+        if (ECO_DIAG_SKIP & 32) {
+            if (cnt) p.phase_ns[16 + 4096 + (gtid & 1023)] = cnt;
+            continue;
         }
         warp_world_add<unsigned long long>(cnt, w, [&](int ww) {
             return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww] + ahead, ww)->grown);
@@ -288,7 +302,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
 // in-grid, agent-free after moves/deaths (O'') and resource-free after consumption (R'')
 // (R21), records (direction, slot) on its own cell, and marks the candidate cell in the
 // step's claimed-cell bitmap.  Distinct claimed cells are counted (each has exactly one
-// winner, resolved later by max key) per world and per row.  Deferred-claim losers are
+// winner, resolved later by max key) per world.  Deferred-claim losers are
 // (candidates - claimed cells), also settled later.  Must be called by all 32 lanes.
 __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
@@ -334,10 +348,7 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
                         const int cy = y + dir_dy(dir), c = cy * p.W + x + dir_dx(dir);
                         uint32_t bit;
                         const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
-                        if (!(old & bit)) {
-                            new_cell = 1;
-                            atomicAdd(rows_of(p, t, w) + cy, 1);
-                        }
+                        if (!(old & bit)) new_cell = 1;
                     }
                     if (dir == NO_DIR) no_cell = 1;
                     else cand = 1;
@@ -366,12 +377,14 @@ __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t
 // One block per world.  Each claimed cell c has exactly one winner: the live parent q
 // adjacent to c that chose c with the largest key (BIRTH w1 << 32 | ~q).  n_place =
 // min(claimed cells, free slots).  (1) The first n_place free slots in ascending order
-// (prefix scan of the alive bitmap).  (2) The first n_place claimed cells in row-major
-// order: a prefix scan of the per-row counts finds the rows, one warp per row ranks its
-// cells with a warp scan of the row's bitmap words.  (3) One thread per rank r resolves the
-// winner of cell c_r and places the child in free slot F[r] (R22); every later claimed cell
-// is deferred for capacity.  Then the step's counters, the next alive count and t += 1.
+// (prefix scan of the alive bitmap) and (2) the first n_place claimed cells in row-major
+// order (prefix scan of the claimed-cell bitmap) are found together, in chunks of NT alive
+// words and NT*RANK_K bitmap words loaded at once (one memory round trip per chunk; the
+// 200x400 world is one chunk).  (3) One thread per rank r resolves the winner of cell c_r
+// and places the child in free slot F[r] (R22); every later claimed cell is deferred for
+// capacity.  Then the step's counters, the next alive count and t += 1.
 constexpr int RANK_SMEM_CAP = 1024;  // births ranked in shared memory (more spill to global)
+constexpr int RANK_K = 8;            // claimed-cell bitmap words per thread per chunk
 
 __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t, int c, int r, int n_surv,
                                             int child) {
@@ -380,18 +393,26 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
     const uint8_t *bd = p.bdir + (size_t)w * HW;
     const uint64_t seed = p.seeds[w];
     const int cy = c / p.W, cx = c - cy * p.W;
-    // winner among the claimants of c (at least one exists)
-    int qbest = -1;
-    unsigned long long kbest = 0ull;
+    // winner among the claimants of c (at least one exists): the four neighbours' occupancy
+    // bits and recorded directions are loaded together, their keys computed independently
+    int qn[4];
+    bool claims[4];
+#pragma unroll
     for (int dq = 0; dq < 4; ++dq) {
         const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
-        if (qy < 0 || qy >= p.H || qx < 0 || qx >= p.W) continue;
-        const int q = qy * p.W + qx;
-        if (!get_bit(O, p, q) || bd[q] != (uint8_t)(dq ^ 1)) continue;
-        const unsigned long long kq = birth_key(seed, t, q);
-        if (qbest < 0 || kq > kbest) {
+        const bool in = qy >= 0 && qy < p.H && qx >= 0 && qx < p.W;
+        qn[dq] = in ? qy * p.W + qx : c;
+        const bool occ = get_bit(O, p, qn[dq]) != 0u;
+        claims[dq] = in && occ && bd[qn[dq]] == (uint8_t)(dq ^ 1);
+    }
+    int qbest = -1;
+    unsigned long long kbest = 0ull;
+#pragma unroll
+    for (int dq = 0; dq < 4; ++dq) {
+        const unsigned long long kq = birth_key(seed, t, qn[dq]);
+        if (claims[dq] && (qbest < 0 || kq > kbest)) {
             kbest = kq;
-            qbest = q;
+            qbest = qn[dq];
         }
     }
     const int parent = p.bslot[(size_t)w * HW + qbest];
@@ -404,11 +425,13 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
     p.repr[cs] = 0;
     p.last_action[cs] = 0;
     p.ate[cs] = 0;
-    for (int k = 0; k < p.Hd; ++k) {
-        p.h[cs * p.Hd + k] = 0.f;
-        p.c[cs * p.Hd + k] = 0.f;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);  // Hd in {4, 8, 16, 32}: rows are float4-aligned
+    for (int k = 0; k < p.Hd; k += 4) {
+        *reinterpret_cast<float4 *>(p.h + cs * p.Hd + k) = z4;
+        *reinterpret_cast<float4 *>(p.c + cs * p.Hd + k) = z4;
     }
-    for (int a = 0; a < LOGIT_STRIDE; ++a) p.logits[cs * LOGIT_STRIDE + a] = 0.f;
+#pragma unroll
+    for (int a = 0; a < LOGIT_STRIDE; a += 4) *reinterpret_cast<float4 *>(p.logits + cs * LOGIT_STRIDE + a) = z4;
     uint32_t bit;
     atomicOr(word_ptr(p.occ + (size_t)w * plane_words(p), p, c, bit), bit);
     p.repr[(size_t)w * p.S + parent] = 0;
@@ -417,11 +440,20 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
     list_of(p, t + 1, w)[n_surv + r] = child;
 }
 
+// `scratch` holds 2 * (NT/32 + 1) words
 template <int NT>
-__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int2 *rowq, int *s_free,
-                                 int *s_bcell) {
-    constexpr int NWARP = NT / 32;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int *s_free, int *s_bcell) {
+    const int tid = threadIdx.x;
+    // sub-phase clock of world 0's rank (phase_ns[4..7]: setup, scans, placement, counters)
+    const bool clk = w == 0 && tid == 0;
+    uint64_t c0 = clk ? globaltimer_ns() : 0ull;
+    auto tick = [&](int k) {
+        if (clk) {
+            const uint64_t c1 = globaltimer_ns();
+            atomicAdd(p.phase_ns + 4 + k, c1 - c0);
+            c0 = c1;
+        }
+    };
     const int64_t t = p.t[w];
     const size_t HW = (size_t)p.H * p.W;
     const int n_start = *count_of(p, t, w);
@@ -430,70 +462,67 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
     const int n_free = p.S - n_surv;
     const int n_place = n_win < n_free ? n_win : n_free;
     int32_t *g_free = p.free_list + (size_t)w * p.S, *g_bcell = p.birth_cell + (size_t)w * p.S;
+    if (clk && n_place >= 0) tick(0);
 
     if (n_place > 0) {
-        // (1)+(2) in lock-step chunks: the first n_place free slots (alive bitmap) and the
-        // rows holding the first n_place claimed cells (per-row counts), then one warp per
-        // such row ranks its cells with a warp scan of the row's bitmap words
+        const uint32_t *ab = p.alive_bits + (size_t)w * p.SW;
         const uint32_t *bb = bbits_of(p, t, w);
-        const int32_t *rows = rows_of(p, t, w);
-        uint32_t run_f = 0u, run_r = 0u;
-        const int span = p.SW > p.H ? p.SW : p.H;
-        for (int k0 = 0; k0 < span; k0 += NT) {
-            const bool need_f = run_f < (uint32_t)n_place, need_r = run_r < (uint32_t)n_place;  // block-uniform
-            if (!need_f && !need_r) break;
-            const int i = k0 + tid;
-            uint32_t fr = 0u, cnt = 0u;
-            if (need_f && i < p.SW) {
-                const int nbits = p.S - i * 32;
+        const size_t nbw = (size_t)p.H * p.WW;
+        uint32_t run_f = 0u, run_c = 0u;
+        for (size_t j = 0;; ++j) {
+            const bool need_f = run_f < (uint32_t)n_place, need_c = run_c < (uint32_t)n_place;  // block-uniform
+            if (!need_f && !need_c) break;
+            // all loads of the chunk first (independent), then one dual scan
+            const size_t fi = j * NT + tid;
+            uint32_t fr = 0u;
+            if (need_f && fi < (size_t)p.SW) {
+                const int nbits = p.S - (int)fi * 32;
                 const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
-                fr = ~ld_plain(p.alive_bits + (size_t)w * p.SW + i) & valid;
+                fr = ~ld_plain(ab + fi) & valid;
             }
-            if (need_r && i < p.H) cnt = (uint32_t)*reinterpret_cast<const volatile int32_t *>(rows + i);
-            uint32_t tot_f, tot_r, nq;
-            const uint32_t ex_f = block_exclusive_scan<NT>((uint32_t)__popc(fr), scratch, tot_f);
-            const uint32_t ex_r = block_exclusive_scan<NT>(cnt, scratch, tot_r);
-            uint32_t r = run_f + ex_f;
+            const size_t bi0 = (j * NT + tid) * RANK_K;
+            uint32_t wd[RANK_K];
+#pragma unroll
+            for (int u = 0; u < RANK_K; ++u) wd[u] = (need_c && bi0 + u < nbw) ? ld_plain(bb + bi0 + u) : 0u;
+            uint32_t cc = 0u;
+#pragma unroll
+            for (int u = 0; u < RANK_K; ++u) cc += (uint32_t)__popc(wd[u]);
+            uint2 tot;
+            const uint2 ex = block_exclusive_scan2<NT>(make_uint2((uint32_t)__popc(fr), cc), scratch, tot);
+            uint32_t r = run_f + ex.x;
             while (fr && r < (uint32_t)n_place) {
                 const int b = __ffs(fr) - 1;
                 fr &= fr - 1u;
-                if (r < RANK_SMEM_CAP) s_free[r] = i * 32 + b;
-                else g_free[r] = i * 32 + b;
+                const int slot = (int)fi * 32 + b;
+                if (r < RANK_SMEM_CAP) s_free[r] = slot;
+                else g_free[r] = slot;
                 ++r;
             }
-            const uint32_t q = (cnt && run_r + ex_r < (uint32_t)n_place) ? 1u : 0u;
-            const uint32_t qi = block_exclusive_scan<NT>(q, scratch, nq);
-            if (q) rowq[qi] = make_int2(i, (int)(run_r + ex_r));
-            __syncthreads();
-            for (uint32_t k = warp; k < nq; k += NWARP) {
-                const int yy = rowq[k].x;
-                uint32_t base = (uint32_t)rowq[k].y;
-                for (int s0 = 0; s0 < p.WW && base < (uint32_t)n_place; s0 += 32) {
-                    const int wx = s0 + lane;
-                    uint32_t word = wx < p.WW ? ld_plain(bb + (size_t)yy * p.WW + wx) : 0u;
-                    const uint32_t pc = (uint32_t)__popc(word);
-                    uint32_t inc = pc;
+            uint32_t rc = run_c + ex.y;
+            if (cc && rc < (uint32_t)n_place) {
+                int y = (int)(bi0 / (size_t)p.WW), wx = (int)(bi0 - (size_t)y * p.WW);
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t n = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += n;
-                    }
-                    uint32_t rr = base + inc - pc;
-                    while (word && rr < (uint32_t)n_place) {
+                for (int u = 0; u < RANK_K; ++u) {
+                    uint32_t word = wd[u];
+                    while (word && rc < (uint32_t)n_place) {
                         const int b = __ffs(word) - 1;
                         word &= word - 1u;
-                        const int c = yy * p.W + wx * 32 + b;
-                        if (rr < RANK_SMEM_CAP) s_bcell[rr] = c;
-                        else g_bcell[rr] = c;
-                        ++rr;
+                        const int c = y * p.W + wx * 32 + b;
+                        if (rc < RANK_SMEM_CAP) s_bcell[rc] = c;
+                        else g_bcell[rc] = c;
+                        ++rc;
                     }
-                    base += __shfl_sync(0xffffffffu, inc, 31);
+                    if (++wx == p.WW) {
+                        wx = 0;
+                        ++y;
+                    }
                 }
             }
-            run_f += tot_f;
-            run_r += tot_r;
-            __syncthreads();
+            run_f += tot.x;
+            run_c += tot.y;
         }
+        __syncthreads();
+        tick(1);
         // (3) winners and placement, one birth per thread (independent dependency chains)
         for (int r = tid; r < n_place; r += NT) {
             const int c = r < RANK_SMEM_CAP ? s_bcell[r] : *reinterpret_cast<volatile int32_t *>(g_bcell + r);
@@ -503,6 +532,7 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
         }
     }
     __syncthreads();
+    tick(2);
     if (tid == 0) {
         volatile sim_step_record *rec = record_of(p, t, w);
         const int64_t de = rec->deaths_energy, da = rec->deaths_age, grown = rec->grown, eaten = rec->eaten,
@@ -529,66 +559,121 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
         p.t[w] = t + 1;
     }
     __syncthreads();
+    tick(3);
 }
 
 // ------------------------------------------------------------------- a5 mutation
 // "an agent's weights are mutated by adding noise sampled from N(0, sigma)",
 // sigma = 0.02 a standard deviation (R23).  The noise of canonical weight j comes from the
 // Philox block (MUTATE, birth step, child cell, q = j >> 2): words (w0,w1) give z[4q],
-// z[4q+1], (w2,w3) give z[4q+2], z[4q+3] via fp64 Box-Muller.  One item = one DEVICE
-// weight position of one child (consecutive threads write consecutive addresses); it
-// recomputes the Philox block and the half of the Box-Muller pair it needs.  Runs after
-// the rank phase advanced t, so the birth step is p.t[w] - 1.
+// z[4q+1], (w2,w3) give z[4q+2], z[4q+3] via fp64 Box-Muller.  One item = one Box-Muller
+// PAIR (canonical j even, j+1) of one child: one log, one sqrt and one sincos for two
+// weights.  In the device layout the partner of j sits HD4 floats later (W_ih^T, W_hh^T:
+// next column), 4 floats later (b: next unit of the same gate) or 1 float later (W_out,
+// b_out), so consecutive items still touch consecutive addresses.  Runs after the rank
+// phase advanced t, so the birth step is p.t[w] - 1.
 
-// device weight index d -> canonical index j (-1 for padding)
-__device__ __forceinline__ int dev_to_canon(int d, const DevParams &p) {
-    const int Hd = p.Hd, G = 4 * Hd, HD4 = Hd * 4;
-    if (d < p.off_hh) {
-        const int col = d / HD4, rem = d - col * HD4;
-        return ((rem & 3) * Hd + (rem >> 2)) * p.I + col;
-    }
-    if (d < p.off_b) {
-        const int dd = d - p.off_hh, col = dd / HD4, rem = dd - col * HD4;
-        return G * p.I + ((rem & 3) * Hd + (rem >> 2)) * Hd + col;
-    }
-    if (d < p.off_out) {
-        const int rem = d - p.off_b;
-        return G * p.I + G * Hd + (rem & 3) * Hd + (rem >> 2);
-    }
-    if (d < p.off_bout + 5) return G * p.I + G * Hd + G + (d - p.off_out);
-    return -1;
+// pair items per child: (I + Hd)/2 column pairs x HD4 rows, 2Hd bias pairs, ceil((5Hd+5)/2)
+__device__ __forceinline__ int mutate_items_per_child(const DevParams &p) {
+    return ((p.I + p.Hd) >> 1) * (p.Hd * 4) + 2 * p.Hd + (5 * p.Hd + 6) / 2;
 }
 
-// z of canonical j for (step t, child cell): bit-identical to box_muller()'s za / zb
-__device__ __forceinline__ double gauss_of(uint64_t seed, int64_t t, int cellc, int j) {
-    const uint4 d = draw4(seed, PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)(j >> 2));
-    const int m = j & 3;
-    const uint32_t wa = m < 2 ? d.x : d.z, wb = m < 2 ? d.y : d.w;
+// pair item -> device index d0 of its first weight, device stride of the partner (0 when
+// the pair is a singleton: the last b_out entry), canonical index j0 (even)
+__device__ __forceinline__ void mutate_item(const DevParams &p, int it, int &d0, int &dstep, int &j0) {
+    const int Hd = p.Hd, G = 4 * Hd, HD4 = Hd * 4;
+    const int nA = ((p.I + Hd) >> 1) * HD4;
+    if (it < nA) {
+        const int pc = it / HD4, rem = it - pc * HD4, col = 2 * pc;
+        const int row = (rem & 3) * Hd + (rem >> 2);
+        d0 = col * HD4 + rem;  // W_hh^T follows W_ih^T contiguously (off_hh = I * HD4)
+        dstep = HD4;
+        j0 = col < p.I ? row * p.I + col : G * p.I + row * Hd + (col - p.I);
+        return;
+    }
+    it -= nA;
+    if (it < 2 * Hd) {  // b: it = kp*4 + gate, units 2kp and 2kp+1
+        const int kp = it >> 2, gate = it & 3;
+        d0 = p.off_b + (2 * kp) * 4 + gate;
+        dstep = 4;
+        j0 = G * p.I + G * Hd + gate * Hd + 2 * kp;
+        return;
+    }
+    it -= 2 * Hd;  // W_out[5][Hd] then b_out[5], identical order in both layouts
+    const int e = 2 * it, n_tail = 5 * Hd + 5;
+    d0 = p.off_out + e;
+    dstep = e + 1 < n_tail ? 1 : 0;
+    j0 = G * p.I + G * Hd + G + e;
+}
+
+// (z[j0], z[j0+1]) for (step t, child cell): bit-identical to box_muller()'s (za, zb)
+__device__ __forceinline__ void gauss_pair(uint64_t seed, int64_t t, int cellc, int j0, double &za, double &zb) {
+    const uint4 d = draw4(seed, PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)(j0 >> 2));
+    const bool lo = (j0 & 3) == 0;
+    const uint32_t wa = lo ? d.x : d.z, wb = lo ? d.y : d.w;
     const double two_m32 = 2.3283064365386963e-10;
     const double u1 = __dmul_rn(__dadd_rn((double)wa, 1.0), two_m32);
     const double u2 = __dmul_rn((double)wb, two_m32);
     const double rad = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
     const double th = __dmul_rn(6.283185307179586, u2);
-    return __dmul_rn(rad, (m & 1) ? sin(th) : cos(th));
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    za = __dmul_rn(rad, cs);
+    zb = __dmul_rn(rad, sn);
+}
+
+// U independent items per thread: all loads, then all Philox/log/sincos chains, then all
+// stores (stores last, so no child store can alias an input the compiler must re-order)
+template <int U>
+__device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t t, uint64_t seed, int Q, size_t k0,
+                                             size_t stride, size_t n) {
+    float pa[U], pb[U];
+    int cellc[U], d0[U], dstep[U], j0[U];
+    float *dst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const size_t k = k0 + u * stride;
+        dst[u] = nullptr;
+        if (k >= n) continue;
+        const int b = (int)(k / (size_t)Q), it = (int)(k - (size_t)b * Q);
+        mutate_item(p, it, d0[u], dstep[u], j0[u]);
+        const size_t bs = (size_t)w * p.S + b;
+        const int child = p.birth_child[bs], parent = p.birth_parent[bs];
+        cellc[u] = p.birth_cell[bs];
+        const float *wp = p.weights + ((size_t)w * p.S + parent) * p.Pd + d0[u];
+        pa[u] = wp[0];
+        pb[u] = dstep[u] ? wp[dstep[u]] : 0.f;
+        dst[u] = p.weights + ((size_t)w * p.S + child) * p.Pd + d0[u];
+    }
+    double za[U], zb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (dst[u]) {
+#if ECO_DIAG_SKIP & 4
+            za[u] = (double)cellc[u];
+            zb[u] = (double)j0[u];
+#else
+            gauss_pair(seed, t, cellc[u], j0[u], za[u], zb[u]);
+#endif
+        }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (!dst[u]) continue;
+        dst[u][0] = __fadd_rn(pa[u], __double2float_rn(__dmul_rn(p.mutation_std, za[u])));
+        if (dstep[u]) dst[u][dstep[u]] = __fadd_rn(pb[u], __double2float_rn(__dmul_rn(p.mutation_std, zb[u])));
+    }
 }
 
 __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
+    constexpr int U = 2;
+    const int Q = mutate_items_per_child(p);
     for (int w = 0; w < p.n_worlds; ++w) {
         const int nb = *reinterpret_cast<volatile int32_t *>(p.n_births + w);
         if (nb == 0) continue;
-        const size_t n = (size_t)nb * p.Pd;
+        const size_t n = (size_t)nb * Q;
         const int64_t t = p.t[w] - 1;
         const uint64_t seed = p.seeds[w];
-        for (size_t k = gtid; k < n; k += gthreads) {
-            const int b = (int)(k / p.Pd), d = (int)(k - (size_t)b * p.Pd);
-            const int j = dev_to_canon(d, p);
-            if (j < 0) continue;
-            const size_t bs = (size_t)w * p.S + b;
-            const int child = p.birth_child[bs], parent = p.birth_parent[bs], cellc = p.birth_cell[bs];
-            const float wp = p.weights[((size_t)w * p.S + parent) * p.Pd + d];
-            const double z = gauss_of(seed, t, cellc, j);
-            p.weights[((size_t)w * p.S + child) * p.Pd + d] = __fadd_rn(wp, __double2float_rn(__dmul_rn(p.mutation_std, z)));
-        }
+        for (size_t k = gtid; k < n; k += U * gthreads) mutate_batch<U>(p, w, t, seed, Q, k, gthreads, n);
     }
 }
 

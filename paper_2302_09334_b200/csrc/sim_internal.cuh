@@ -54,7 +54,6 @@ struct DevParams {
     int32_t *cell, *energy, *age, *repr;
     float *h, *c, *logits, *weights;
     int4 *mrec;                  // [n_worlds][S] per list position: (slot, cell, target or -1, MOVE w0)
-    int32_t *row_wins;           // [2][n_worlds][H] birth-claim winners per row (by step parity)
     int32_t *alive_list;         // [2][n_worlds][S]
     int32_t *n_alive;            // [2][n_worlds]
     int32_t *n_win;              // [n_worlds] birth-claim winners this step
@@ -162,9 +161,6 @@ __device__ __forceinline__ uint32_t *plane_next(const DevParams &p, int64_t t) {
 }
 __device__ __forceinline__ uint32_t *bbits_of(const DevParams &p, int64_t t, int w) {
     return p.bbits + ((size_t)(t & 1) * p.n_worlds + w) * plane_words(p);
-}
-__device__ __forceinline__ int32_t *rows_of(const DevParams &p, int64_t t, int w) {
-    return p.row_wins + ((size_t)(t & 1) * p.n_worlds + w) * p.H;
 }
 __device__ __forceinline__ int32_t *list_of(const DevParams &p, int64_t t, int w) {
     return p.alive_list + ((size_t)(t & 1) * p.n_worlds + w) * p.S;

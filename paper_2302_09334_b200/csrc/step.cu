@@ -5,9 +5,9 @@
 //                 half of a4; each warp streams its agents' weights with 1-D TMA bulk
 //                 copies (cp.async.bulk) through a 3-stage shared-memory pipeline
 //   k_policy_reg  (Hd = 4, 8, 16) the same step with register loads, lane groups of Hd
-//   k_post        cooperative: a4 move/consume/physiology/death | grid barrier | a1
-//                 regrowth of step t+1 + a5 birth candidates | barrier | a5 rank, winners,
-//                 placement, t += 1 | barrier | a5 mutation of the children
+//   k_post        cooperative: a4 move/consume/physiology/death | grid barrier | a5 birth
+//                 candidates | barrier | a5 rank, winners, placement, t += 1 | barrier |
+//                 a1 regrowth of step t+1 beside a5 mutation of the children
 // (the first step after create/set_state is preceded by a standalone k_regrow).
 // Instrumented mode (sim_step_timed): the same phases as separate kernels, timed one by one.
 #include "phases.cuh"
@@ -146,8 +146,8 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
 
 // housekeeping for the later phases of this step (any policy kernel runs it): the survivor
 // list of step t+1, the winner counters and the record of step t+1 (whose regrowth runs
-// early, inside this step's k_post) start at 0; the claimed-cell bitmap and row counts of
-// parity t+1 (used by step t-1) are cleared for step t+1.
+// early, inside this step's k_post) start at 0; the claimed-cell bitmap of parity t+1
+// (used by step t-1) is cleared for step t+1.
 __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
     const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
@@ -155,10 +155,6 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
     for (size_t k = gtid; k < (size_t)p.n_worlds * pw; k += gthreads) {
         const int w = (int)(k / pw);
         bbits_of(p, p.t[w] + 1, w)[k - (size_t)w * pw] = 0u;
-    }
-    for (size_t k = gtid; k < (size_t)p.n_worlds * p.H; k += gthreads) {
-        const int w = (int)(k / p.H);
-        rows_of(p, p.t[w] + 1, w)[k - (size_t)w * p.H] = 0;
     }
     for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
         const int64_t tw = p.t[w];
@@ -650,11 +646,10 @@ __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
 
 constexpr int RANK_THREADS = 1024;
 __global__ void __launch_bounds__(RANK_THREADS) k_birth_rank(DevParams p) {
-    __shared__ uint32_t scratch[RANK_THREADS / 32 + 1];
-    __shared__ int2 rowq[RANK_THREADS];
+    __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP];
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
-        birth_rank_world<RANK_THREADS>(p, w, scratch, rowq, s_free, s_bcell);
+        birth_rank_world<RANK_THREADS>(p, w, scratch, s_free, s_bcell);
 }
 
 __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
@@ -662,14 +657,44 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 }
 
 // ------------------------------------------------------------------------ k_post
-// a4 move/consume/physiology/death | barrier | a1 regrowth of step t+1 (needs only R'' of
-// step t) + a5 birth candidates and claimed cells | barrier | a5 rank, winners, placement,
-// counters, t += 1 | barrier | a5 mutation of the children.
+// a4 move/consume/physiology/death | barrier | a5 birth candidates and claimed cells |
+// barrier | a5 rank, winners, placement, counters, t += 1 | barrier | a1 regrowth of step
+// t+1 (needs only R'' of step t) beside a5 mutation of the children.  A phase that ends in
+// a barrier pays for its writes in the barrier's release fence; the regrowth's plane writes
+// (measured: +3..6 us of fence when they preceded a barrier) go last, where only the
+// kernel's end waits for them.
 constexpr int POST_THREADS = 512;
 constexpr int POST_BARRIERS = 3;
+#ifdef ECO_BLOCK_CLOCK
+// diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
+// phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
+// fence.acq_rel.gpu before the arrival, timed alone)
+constexpr int ECO_BLOCK_CLOCK_BASE = 16;
+#define POST_SYNC(k)                                                                              \
+    do {                                                                                          \
+        __syncthreads();                                                                          \
+        const uint64_t a_ = globaltimer_ns();                                                     \
+        uint64_t f_ = a_;                                                                         \
+        if (threadIdx.x == 0) {                                                                   \
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");                                     \
+            f_ = globaltimer_ns();                                                                \
+        }                                                                                         \
+        grid_sync(bar, target);                                                                   \
+        const uint64_t e_ = globaltimer_ns();                                                     \
+        if (threadIdx.x == 0) {                                                                   \
+            unsigned long long *q_ = p.phase_ns + ECO_BLOCK_CLOCK_BASE + ((k) * gridDim.x + blockIdx.x) * 3; \
+            q_[0] += a_ - bt_;                                                                    \
+            q_[1] += e_ - a_;                                                                     \
+            q_[2] += f_ - a_;                                                                     \
+        }                                                                                         \
+        bt_ = e_;                                                                                 \
+    } while (0)
+#else
+#define POST_SYNC(k) grid_sync(bar, target)
+#endif
+
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned long long *bar) {
-    __shared__ uint32_t scratch[POST_THREADS / 32 + 1];
-    __shared__ int2 rowq[POST_THREADS];
+    __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP];
     // warp-interleaved global index: consecutive warps of work land on different blocks
     // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
@@ -679,21 +704,37 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
     // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
     const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
     uint64_t t0 = clk ? globaltimer_ns() : 0ull, t1;
+#ifdef ECO_BLOCK_CLOCK
+    uint64_t bt_ = globaltimer_ns();
+#endif
     move_phase(p, gtid, gthreads);
-    grid_sync(bar, target);
+    POST_SYNC(0);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 0, t1 - t0); t0 = t1; }
-    // birth candidates on the first half of the (warp-interleaved) threads, the regrowth of
-    // step t+1 on the second half, concurrently
-    const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
-    if (gtid < half) birth_claim_phase(p, gtid, half);
-    else regrow_phase(p, 1, gtid - half, gthreads - half);
-    grid_sync(bar, target);
+    // birth candidates on every thread
+    const uint64_t h0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
+    if (!(ECO_DIAG_SKIP & 1)) birth_claim_phase(p, gtid, gthreads);
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)  // summed warp durations of block 0
+        atomicAdd(p.phase_ns + 8, globaltimer_ns() - h0);
+    POST_SYNC(1);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 1, t1 - t0); t0 = t1; }
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
-        birth_rank_world<POST_THREADS>(p, w, scratch, rowq, s_free, s_bcell);
-    grid_sync(bar, target);
+        birth_rank_world<POST_THREADS>(p, w, scratch, s_free, s_bcell);
+    POST_SYNC(2);
     if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 2, t1 - t0); t0 = t1; }
+    // the regrowth of step t+1 (t has advanced: ahead = 0) on the second half of the threads,
+    // then the children's weights on all of them.  Nothing in this launch reads the plane
+    // the regrowth writes, so no barrier (and no release fence) follows it.
+    const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
+    if (gtid >= half && !(ECO_DIAG_SKIP & 2)) {
+        const uint64_t r0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
+        regrow_phase(p, 0, gtid - half, gthreads - half);
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
+    }
     mutate_phase(p, gtid, gthreads);
+#ifdef ECO_BLOCK_CLOCK
+    __syncthreads();
+    if (threadIdx.x == 0) p.phase_ns[ECO_BLOCK_CLOCK_BASE + (3 * gridDim.x + blockIdx.x) * 3] += globaltimer_ns() - bt_;
+#endif
     if (clk) {
         t1 = globaltimer_ns();
         atomicAdd(p.phase_ns + 3, t1 - t0);
