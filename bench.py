@@ -10,7 +10,9 @@ Our arm (default):
     seed 1; under torchrun rank r runs an independent replica with seed 1 + r, weak
     scaling, no data-path collective), runs W warm-up steps, then times EXACTLY K steps
     through sim_step (one CUDA graph per step), each bracketed by CUDA events on the
-    library's stream, with a 256 MiB memset flushing L2 between timed steps;
+    library's stream, with L2 flushed between timed steps: a 256 MiB memset (evicts every
+    line the step left) followed by a 256 MiB read, so the evicted lines are clean and the
+    next step is not charged for writing back the flush buffer's dirty lines;
   * replays the same K steps from a snapshot through sim_step_timed (events around every
     kernel) for the per-kernel breakdown and the roofline of the dominant kernel;
   * e2e: the same K steps through the public API from pinned HOST buffers: sim_set_state
@@ -191,6 +193,12 @@ def run_ours(args, rank, world_size, local_rank):
     with torch.cuda.stream(stream):
         world = sim.World(wc, device=local_rank, stream=stream, log_capacity=max(4096, W + K + 8))
         flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+        flush_rd = torch.ones(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+        def flush_l2():
+            flush.zero_()
+            flush_rd.sum()  # clean lines: no dirty write-back lands in the timed step
+
         world.step(W)
         world.synchronize()
         need_snap = not (args.no_replay and args.no_e2e and args.no_cpu_baseline)
@@ -203,7 +211,7 @@ def run_ours(args, rank, world_size, local_rank):
         torch.cuda.synchronize()
         for k in range(K):
             if not args.no_flush:
-                flush.zero_()
+                flush_l2()
             evs[k][0].record(stream)
             world.step(1)
             evs[k][1].record(stream)
@@ -212,9 +220,11 @@ def run_ours(args, rank, world_size, local_rank):
         clk = clocks.stop()
         world.synchronize()
         post_phases = {k_: v / K / 1e3 for k_, v in world.phase_ns().items()}
-        # k_post runs 512 threads per block: block 0 has 16 claim warps and 8 regrowth warps
-        for k_, nw in (("claim.warp_sum_b0", 16), ("regrow.warp_sum_b0", 8)):
-            post_phases[k_.replace(".warp_sum_b0", ".warp_mean")] = post_phases.pop(k_) / nw
+        # k_post runs 512 threads per block: 16 claim warps in block 0, 16 regrowth warps in block 1
+        for k_, nw in (("claim.warp_sum_b0", 16), ("regrow.warp_sum_b1", 16)):
+            post_phases[k_.split(".")[0] + ".warp_mean"] = post_phases.pop(k_) / nw
+        for k_ in [k_ for k_ in post_phases if k_.startswith("reserved")]:
+            post_phases.pop(k_)
         step_ms = np.array([a.elapsed_time(b) for a, b in evs], np.float64)
         total_ms = float(step_ms.sum())
         log = world.step_log(t0, K)
@@ -234,7 +244,7 @@ def run_ours(args, rank, world_size, local_rank):
             ssum = 0.0
             for k in range(K):
                 if not args.no_flush:
-                    flush.zero_()
+                    flush_l2()
                 tm = world.step_timed()
                 ksum += np.array([tm[n] for n in sim.KERNEL_NAMES])
                 ssum += tm["step_ms"]
@@ -283,7 +293,7 @@ def run_ours(args, rank, world_size, local_rank):
                        "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x2", "hidden": wc.hidden,
                        "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + K],
                        "l2": "NOT flushed (diagnostic run)" if args.no_flush
-                       else "flushed between timed steps (256 MiB memset on the library stream)",
+                       else "flushed between timed steps (256 MiB memset + 256 MiB read on the library stream)",
                        "parallelism": "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
                        else "single GPU", "global_batch": wc.slots * world_size},
             "cell_updates_per_s": cells * world_size / (max_ms / 1e3),

@@ -176,14 +176,14 @@ SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
 /* Graph mode runs everything after the policy kernel as one cooperative kernel whose
- * phases are separated by grid barriers: move, birth candidates, birth rank,
- * regrow(t+1)+mutation.  out[i] = summed duration (ns, device global timer, as seen by block 0) of
- * phase i over the steps since the last reset; reset != 0 zeroes.  out[4..7] split world
- * 0's birth rank into its sub-steps: setup, free-slot/claimed-cell scans, placement,
- * counters.  out[8]: summed durations of block 0's warps working on the birth claims;
- * out[9]: the same for its warps running the regrowth of step t+1.
- * reset < 0 (diagnostic builds): out receives 16 + 8192 words, the per-block clocks after
- * the first 16. */
+ * phases are separated by grid barriers: move | birth candidates | birth rank (beside the
+ * regrowth of step t+1 on the blocks without a world) | mutation.
+ * out[i] = summed duration (ns, device global timer, as seen by block 0) over the steps
+ * since the last reset; reset > 0 zeroes.  out[0..3]: those four phases; out[4..7]
+ * reserved; out[8]: summed durations of block 0's warps working on the birth claims;
+ * out[9]: summed durations of the regrowth warps of the first block without a world.
+ * reset < 0 (diagnostic builds): out receives 16 + 32768 words, the per-block clocks or
+ * per-agent traces after the first 16. */
 #define SIM_NUM_POST_PHASES 10
 SIM_API sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset);
 /* Synchronise the handle's stream (reports deferred errors). */

@@ -101,6 +101,8 @@ void threshold_table(const sim_config *cfg, std::vector<uint32_t> &T) {
     }
 }
 
+constexpr size_t PHASE_WORDS = 16 + 4 * 8192;  // phase clocks + diagnostic-build per-block clocks / traces
+
 size_t device_bytes(const Derived &d) {
     const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
     size_t b = 0;
@@ -356,7 +358,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.res_count, nw), "alloc");
     CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");
     CKC(dalloc(h, &p.totals, 8), "alloc");
-    CKC(dalloc(h, &p.phase_ns, 16 + 4 * 2 * 1024), "alloc");  // + per-block clocks of diagnostic builds
+    CKC(dalloc(h, &p.phase_ns, PHASE_WORDS), "alloc");  // + per-block clocks / traces of diagnostic builds
     CKC(dalloc(h, &h->forced_dev, nw * S), "alloc");
     CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
     p.seeds = seeds_d;
@@ -373,8 +375,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
 
     // launch configuration: persistent-style grids sized to the 148 SMs
     int bps = 0;
+    CKC(eco::policy_prepare(), "kernel attributes");  // before the occupancy query (dynamic smem opt-in)
     CKC(eco::policy_occupancy(d.Hd, 256, &bps), "occupancy");
-    CKC(eco::policy_prepare(), "kernel attributes");
     if (bps < 1) bps = 1;
     h->lc.policy_threads = 256;
     h->lc.policy_blocks = prop.multiProcessorCount * bps;
@@ -667,10 +669,10 @@ sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset) {
     if (st != SIM_OK) return st;
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     if (out)
-        CK(h, cudaMemcpyAsync(out, h->p.phase_ns, (reset < 0 ? 16 + 4 * 2 * 1024 : SIM_NUM_POST_PHASES) * 8,
+        CK(h, cudaMemcpyAsync(out, h->p.phase_ns, (reset < 0 ? PHASE_WORDS : SIM_NUM_POST_PHASES) * 8,
                               cudaMemcpyDeviceToHost, h->stream),
            "phase clock");
-    if (reset > 0) CK(h, cudaMemsetAsync(h->p.phase_ns, 0, (16 + 4 * 2 * 1024) * 8, h->stream), "phase clock");
+    if (reset > 0) CK(h, cudaMemsetAsync(h->p.phase_ns, 0, PHASE_WORDS * 8, h->stream), "phase clock");
     return sync(h);
 }
 

@@ -14,20 +14,12 @@
 #include "block_scan.cuh"
 #include "sim_internal.cuh"
 
-#ifndef ECO_DIAG_SKIP
-// diagnostic builds only (results are wrong): 1 skips the birth claims, 2 the regrowth in
-// k_post, 4 the mutation maths, 8 the regrowth's counter atomics, 16 its plane stores,
-// 32 its atomics replaced by plain stores, 64 its loads made non-volatile
-#define ECO_DIAG_SKIP 0
-#endif
-
 namespace eco {
 
 // ------------------------------------------------------------------ grid barrier
 // Release/acquire barrier over all blocks of a cooperatively launched grid (co-residency
 // guaranteed by the cooperative launch).  bar[0] counts arrivals monotonically across
-// launches; bar[1] counts completed launches of the kernel.  `target` starts at
-// bar[1] * nblocks * barriers_per_launch (read by every block before its first arrival).
+// launches; `target` starts at grid_sync_base() and grows by gridDim per barrier.
 __device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long long &target) {
     __syncthreads();
     target += gridDim.x;
@@ -40,13 +32,16 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long
     __syncthreads();
 }
 
-__device__ __forceinline__ unsigned long long grid_sync_base(unsigned long long *bar, int barriers_per_launch) {
-    const unsigned long long launches = *reinterpret_cast<volatile unsigned long long *>(bar + 1);
-    return launches * (unsigned long long)gridDim.x * (unsigned long long)barriers_per_launch;
+// bar[1] holds the arrival count after the previous launch's last barrier (the launches
+// may differ in their number of barriers); every block reads it before its first arrival.
+__device__ __forceinline__ unsigned long long grid_sync_base(const unsigned long long *bar) {
+    return *reinterpret_cast<const volatile unsigned long long *>(bar + 1);
 }
 
 // called once per launch after its last barrier by one thread of block 0
-__device__ __forceinline__ void grid_sync_done(unsigned long long *bar) { atomicAdd(bar + 1, 1ull); }
+__device__ __forceinline__ void grid_sync_done(unsigned long long *bar, unsigned long long target) {
+    *reinterpret_cast<volatile unsigned long long *>(bar + 1) = target;
+}
 
 __device__ __forceinline__ uint32_t ld_plain(const uint32_t *p) { return *reinterpret_cast<const volatile uint32_t *>(p); }
 
@@ -121,9 +116,7 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
         for (int dw = -1; dw <= 1; ++dw) {
             const int ww = wx + dw;
             win[dy + 2][dw + 1] =
-                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW)
-                    ? ((ECO_DIAG_SKIP & 64) ? __ldcg(src + (size_t)yy * p.WW + ww) : ld_plain(src + (size_t)yy * p.WW + ww))
-                    : 0u;
+                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
         }
     }
     const uint32_t cur = win[2][1];
@@ -166,13 +159,13 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
             if (word_of(d, m) < thr) grow |= 1u << b;
         }
     }
-    if (!(ECO_DIAG_SKIP & 16)) dst[(size_t)y * p.WW + wx] = cur | grow;
+    dst[(size_t)y * p.WW + wx] = cur | grow;
     return __popc(grow);
 }
 
-// Grid-stride regrowth of every world for step p.t[w] + ahead; one atomic per warp on the
-// world's record.  Must be called by all 32 lanes of a warp.
-__device__ __forceinline__ void regrow_phase(const DevParams &p, int ahead, size_t gtid, size_t gthreads) {
+// Grid-stride regrowth of every world for step `tstep` (all worlds share t); one atomic per
+// warp on the world's record of that step.  Must be called by all 32 lanes of a warp.
+__device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, size_t gtid, size_t gthreads) {
     const int real_words = (p.W + 31) >> 5;
     const size_t per_world = (size_t)p.H * real_words;
     const size_t total = per_world * p.n_worlds;
@@ -184,15 +177,10 @@ __device__ __forceinline__ void regrow_phase(const DevParams &p, int ahead, size
             w = (int)(k / per_world);
             const size_t r = k - (size_t)w * per_world;
             const int y = (int)(r / real_words), wx = (int)(r - (size_t)y * real_words);
-            cnt = (unsigned long long)regrow_word(p, w, y, wx, p.t[w] + ahead);
-            if (ECO_DIAG_SKIP & 8) cnt = 0;
-        }
-        if (ECO_DIAG_SKIP & 32) {
-            if (cnt) p.phase_ns[16 + 4096 + (gtid & 1023)] = cnt;
-            continue;
+            cnt = (unsigned long long)regrow_word(p, w, y, wx, tstep);
         }
         warp_world_add<unsigned long long>(cnt, w, [&](int ww) {
-            return reinterpret_cast<unsigned long long *>(&record_of(p, p.t[ww] + ahead, ww)->grown);
+            return reinterpret_cast<unsigned long long *>(&record_of(p, tstep, ww)->grown);
         });
     }
 }
@@ -374,27 +362,30 @@ __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t
 }
 
 // ------------------------------------------------------------------ a5 birth rank
-// One block per world.  Each claimed cell c has exactly one winner: the live parent q
-// adjacent to c that chose c with the largest key (BIRTH w1 << 32 | ~q).  n_place =
-// min(claimed cells, free slots).  (1) The first n_place free slots in ascending order
-// (prefix scan of the alive bitmap) and (2) the first n_place claimed cells in row-major
-// order (prefix scan of the claimed-cell bitmap) are found together, in chunks of NT alive
-// words and NT*RANK_K bitmap words loaded at once (one memory round trip per chunk; the
-// 200x400 world is one chunk).  (3) One thread per rank r resolves the winner of cell c_r
-// and places the child in free slot F[r] (R22); every later claimed cell is deferred for
-// capacity.  Then the step's counters, the next alive count and t += 1.
+// Each claimed cell c has exactly one winner: the live parent q adjacent to c that chose c
+// with the largest key (BIRTH w1 << 32 | ~q).  n_place = min(claimed cells, free slots).
+// (1) The first n_place free slots in ascending order (prefix scan of the alive bitmap) and
+// (2) the first n_place claimed cells in row-major order (prefix scan of the claimed-cell
+// bitmap) are found together, in chunks of NT alive words and NT*RANK_K bitmap words loaded
+// at once (one memory round trip per chunk; the 200x400 world is one chunk).  (3) Rank r
+// resolves the winner of cell c_r and places the child in free slot F[r] (R22); every later
+// claimed cell is deferred for capacity.  Then the step's counters and the next alive count.
 constexpr int RANK_SMEM_CAP = 1024;  // births ranked in shared memory (more spill to global)
 constexpr int RANK_K = 8;            // claimed-cell bitmap words per thread per chunk
 
-__device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t, int c, int r, int n_surv,
-                                            int child) {
+// Parent slot of claimed cell c.  A claimant q is a neighbour holding a live agent in O''
+// that recorded the direction towards c.  Claimed cells are never claimants (they were
+// empty in O''), which also keeps the test exact while children are being placed into
+// claimed cells concurrently (their new O bits and the stale bdir of an empty cell).  The
+// four neighbours' bits and directions are loaded together and their keys computed
+// independently.
+__device__ __forceinline__ int birth_parent_of(const DevParams &p, int w, int64_t t, int c) {
     const size_t HW = (size_t)p.H * p.W;
     const uint32_t *O = p.occ + (size_t)w * plane_words(p);
+    const uint32_t *BB = bbits_of(p, t, w);
     const uint8_t *bd = p.bdir + (size_t)w * HW;
     const uint64_t seed = p.seeds[w];
     const int cy = c / p.W, cx = c - cy * p.W;
-    // winner among the claimants of c (at least one exists): the four neighbours' occupancy
-    // bits and recorded directions are loaded together, their keys computed independently
     int qn[4];
     bool claims[4];
 #pragma unroll
@@ -402,8 +393,8 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
         const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
         const bool in = qy >= 0 && qy < p.H && qx >= 0 && qx < p.W;
         qn[dq] = in ? qy * p.W + qx : c;
-        const bool occ = get_bit(O, p, qn[dq]) != 0u;
-        claims[dq] = in && occ && bd[qn[dq]] == (uint8_t)(dq ^ 1);
+        const bool occ = get_bit(O, p, qn[dq]) != 0u, claimed = get_bit(BB, p, qn[dq]) != 0u;
+        claims[dq] = in && occ && !claimed && bd[qn[dq]] == (uint8_t)(dq ^ 1);
     }
     int qbest = -1;
     unsigned long long kbest = 0ull;
@@ -415,7 +406,12 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
             qbest = qn[dq];
         }
     }
-    const int parent = p.bslot[(size_t)w * HW + qbest];
+    return p.bslot[(size_t)w * HW + qbest];
+}
+
+// child state of birth r in slot `child` on cell c; parent's repr reset; birth lists
+__device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t, int c, int r, int n_surv, int child,
+                                            int parent) {
     const size_t cs = (size_t)w * p.S + child;
     p.alive[cs] = 1;
     atomicOr(p.alive_bits + (size_t)w * p.SW + (child >> 5), 1u << (child & 31));
@@ -440,126 +436,135 @@ __device__ __forceinline__ void place_birth(const DevParams &p, int w, int64_t t
     list_of(p, t + 1, w)[n_surv + r] = child;
 }
 
-// `scratch` holds 2 * (NT/32 + 1) words
+// (1) + (2): free slots and claimed cells of ranks r < n_place into s_free / s_bcell (r <
+// RANK_SMEM_CAP) or g_free / g_bcell (larger r).  All NT threads; `scratch` holds
+// 2 * (NT/32 + 1) words.
+template <int NT>
+__device__ void rank_lists(const DevParams &p, int w, int64_t t, int n_place, uint32_t *scratch, int *s_free,
+                           int *s_bcell, int32_t *g_free, int32_t *g_bcell) {
+    const int tid = threadIdx.x;
+    const uint32_t *ab = p.alive_bits + (size_t)w * p.SW;
+    const uint32_t *bb = bbits_of(p, t, w);
+    const size_t nbw = (size_t)p.H * p.WW;
+    uint32_t run_f = 0u, run_c = 0u;
+    for (size_t j = 0;; ++j) {
+        const bool need_f = run_f < (uint32_t)n_place, need_c = run_c < (uint32_t)n_place;  // block-uniform
+        if (!need_f && !need_c) break;
+        // all loads of the chunk first (independent), then one dual scan
+        const size_t fi = j * NT + tid;
+        uint32_t fr = 0u;
+        if (need_f && fi < (size_t)p.SW) {
+            const int nbits = p.S - (int)fi * 32;
+            const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
+            fr = ~ld_plain(ab + fi) & valid;
+        }
+        const size_t bi0 = (j * NT + tid) * RANK_K;
+        uint32_t wd[RANK_K];
+#pragma unroll
+        for (int u = 0; u < RANK_K; ++u) wd[u] = (need_c && bi0 + u < nbw) ? ld_plain(bb + bi0 + u) : 0u;
+        uint32_t cc = 0u;
+#pragma unroll
+        for (int u = 0; u < RANK_K; ++u) cc += (uint32_t)__popc(wd[u]);
+        uint2 tot;
+        const uint2 ex = block_exclusive_scan2<NT>(make_uint2((uint32_t)__popc(fr), cc), scratch, tot);
+        uint32_t r = run_f + ex.x;
+        while (fr && r < (uint32_t)n_place) {
+            const int b = __ffs(fr) - 1;
+            fr &= fr - 1u;
+            const int slot = (int)fi * 32 + b;
+            if (r < RANK_SMEM_CAP) s_free[r] = slot;
+            else g_free[r] = slot;
+            ++r;
+        }
+        uint32_t rc = run_c + ex.y;
+        if (cc && rc < (uint32_t)n_place) {
+            int y = (int)(bi0 / (size_t)p.WW), wx = (int)(bi0 - (size_t)y * p.WW);
+#pragma unroll
+            for (int u = 0; u < RANK_K; ++u) {
+                uint32_t word = wd[u];
+                while (word && rc < (uint32_t)n_place) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1u;
+                    const int c = y * p.W + wx * 32 + b;
+                    if (rc < RANK_SMEM_CAP) s_bcell[rc] = c;
+                    else g_bcell[rc] = c;
+                    ++rc;
+                }
+                if (++wx == p.WW) {
+                    wx = 0;
+                    ++y;
+                }
+            }
+        }
+        run_f += tot.x;
+        run_c += tot.y;
+    }
+    __syncthreads();
+}
+
+// step t's record, counters and the next alive count (one thread)
+__device__ __forceinline__ void rank_finalize(const DevParams &p, int w, int64_t t, int n_start, int n_surv,
+                                              int n_win, int n_place) {
+    volatile sim_step_record *rec = record_of(p, t, w);
+    const int64_t de = rec->deaths_energy, da = rec->deaths_age, grown = rec->grown, eaten = rec->eaten,
+                  dc = rec->deferred_claim;
+    const int64_t res = p.res_count[w] + grown - eaten;
+    p.res_count[w] = res;
+    rec->t = t;
+    rec->agents_at_start = n_start;
+    rec->births = n_place;
+    rec->deferred_claim = dc - n_win;  // candidates - claimed cells
+    rec->deferred_capacity = n_win - n_place;
+    rec->population = n_surv + n_place;
+    rec->resources = res;
+    *count_of(p, t + 1, w) = n_surv + n_place;
+    p.n_births[w] = n_place;
+    unsigned long long *tot = p.totals;
+    if (w == 0) atomicAdd(tot + 0, 1ull);
+    atomicAdd(tot + 1, (unsigned long long)n_start);
+    atomicAdd(tot + 2, (unsigned long long)((size_t)p.H * p.W));
+    atomicAdd(tot + 3, (unsigned long long)n_place);
+    atomicAdd(tot + 4, (unsigned long long)(de + da));
+    atomicAdd(tot + 5, (unsigned long long)eaten);
+    atomicAdd(tot + 6, (unsigned long long)grown);
+}
+
+struct RankCounts {
+    int n_start, n_surv, n_win, n_place;
+};
+__device__ __forceinline__ RankCounts rank_counts(const DevParams &p, int w, int64_t t) {
+    RankCounts k;
+    k.n_start = *reinterpret_cast<volatile int32_t *>(count_of(p, t, w));
+    k.n_surv = *reinterpret_cast<volatile int32_t *>(count_of(p, t + 1, w));
+    k.n_win = *reinterpret_cast<volatile int32_t *>(p.n_win + w);
+    const int n_free = p.S - k.n_surv;
+    k.n_place = k.n_win < n_free ? k.n_win : n_free;
+    return k;
+}
+
+// One block ranks and places world w's births, then t += 1 (the path with a barrier
+// between rank and mutation: several worlds, or more births than RANK_SMEM_CAP).
 template <int NT>
 __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int *s_free, int *s_bcell) {
     const int tid = threadIdx.x;
-    // sub-phase clock of world 0's rank (phase_ns[4..7]: setup, scans, placement, counters)
-    const bool clk = w == 0 && tid == 0;
-    uint64_t c0 = clk ? globaltimer_ns() : 0ull;
-    auto tick = [&](int k) {
-        if (clk) {
-            const uint64_t c1 = globaltimer_ns();
-            atomicAdd(p.phase_ns + 4 + k, c1 - c0);
-            c0 = c1;
-        }
-    };
     const int64_t t = p.t[w];
-    const size_t HW = (size_t)p.H * p.W;
-    const int n_start = *count_of(p, t, w);
-    const int n_surv = *reinterpret_cast<volatile int32_t *>(count_of(p, t + 1, w));
-    const int n_win = *reinterpret_cast<volatile int32_t *>(p.n_win + w);
-    const int n_free = p.S - n_surv;
-    const int n_place = n_win < n_free ? n_win : n_free;
+    const RankCounts k = rank_counts(p, w, t);
     int32_t *g_free = p.free_list + (size_t)w * p.S, *g_bcell = p.birth_cell + (size_t)w * p.S;
-    if (clk && n_place >= 0) tick(0);
-
-    if (n_place > 0) {
-        const uint32_t *ab = p.alive_bits + (size_t)w * p.SW;
-        const uint32_t *bb = bbits_of(p, t, w);
-        const size_t nbw = (size_t)p.H * p.WW;
-        uint32_t run_f = 0u, run_c = 0u;
-        for (size_t j = 0;; ++j) {
-            const bool need_f = run_f < (uint32_t)n_place, need_c = run_c < (uint32_t)n_place;  // block-uniform
-            if (!need_f && !need_c) break;
-            // all loads of the chunk first (independent), then one dual scan
-            const size_t fi = j * NT + tid;
-            uint32_t fr = 0u;
-            if (need_f && fi < (size_t)p.SW) {
-                const int nbits = p.S - (int)fi * 32;
-                const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
-                fr = ~ld_plain(ab + fi) & valid;
-            }
-            const size_t bi0 = (j * NT + tid) * RANK_K;
-            uint32_t wd[RANK_K];
-#pragma unroll
-            for (int u = 0; u < RANK_K; ++u) wd[u] = (need_c && bi0 + u < nbw) ? ld_plain(bb + bi0 + u) : 0u;
-            uint32_t cc = 0u;
-#pragma unroll
-            for (int u = 0; u < RANK_K; ++u) cc += (uint32_t)__popc(wd[u]);
-            uint2 tot;
-            const uint2 ex = block_exclusive_scan2<NT>(make_uint2((uint32_t)__popc(fr), cc), scratch, tot);
-            uint32_t r = run_f + ex.x;
-            while (fr && r < (uint32_t)n_place) {
-                const int b = __ffs(fr) - 1;
-                fr &= fr - 1u;
-                const int slot = (int)fi * 32 + b;
-                if (r < RANK_SMEM_CAP) s_free[r] = slot;
-                else g_free[r] = slot;
-                ++r;
-            }
-            uint32_t rc = run_c + ex.y;
-            if (cc && rc < (uint32_t)n_place) {
-                int y = (int)(bi0 / (size_t)p.WW), wx = (int)(bi0 - (size_t)y * p.WW);
-#pragma unroll
-                for (int u = 0; u < RANK_K; ++u) {
-                    uint32_t word = wd[u];
-                    while (word && rc < (uint32_t)n_place) {
-                        const int b = __ffs(word) - 1;
-                        word &= word - 1u;
-                        const int c = y * p.W + wx * 32 + b;
-                        if (rc < RANK_SMEM_CAP) s_bcell[rc] = c;
-                        else g_bcell[rc] = c;
-                        ++rc;
-                    }
-                    if (++wx == p.WW) {
-                        wx = 0;
-                        ++y;
-                    }
-                }
-            }
-            run_f += tot.x;
-            run_c += tot.y;
-        }
-        __syncthreads();
-        tick(1);
-        // (3) winners and placement, one birth per thread (independent dependency chains)
-        for (int r = tid; r < n_place; r += NT) {
+    if (k.n_place > 0) {
+        rank_lists<NT>(p, w, t, k.n_place, scratch, s_free, s_bcell, g_free, g_bcell);
+        for (int r = tid; r < k.n_place; r += NT) {  // one birth per thread
             const int c = r < RANK_SMEM_CAP ? s_bcell[r] : *reinterpret_cast<volatile int32_t *>(g_bcell + r);
             const int child = r < RANK_SMEM_CAP ? s_free[r] : *reinterpret_cast<volatile int32_t *>(g_free + r);
             g_bcell[r] = c;  // the mutation phase reads the birth lists from global memory
-            place_birth(p, w, t, c, r, n_surv, child);
+            place_child(p, w, t, c, r, k.n_surv, child, birth_parent_of(p, w, t, c));
         }
     }
     __syncthreads();
-    tick(2);
     if (tid == 0) {
-        volatile sim_step_record *rec = record_of(p, t, w);
-        const int64_t de = rec->deaths_energy, da = rec->deaths_age, grown = rec->grown, eaten = rec->eaten,
-                      dc = rec->deferred_claim;
-        const int64_t res = p.res_count[w] + grown - eaten;
-        p.res_count[w] = res;
-        rec->t = t;
-        rec->agents_at_start = n_start;
-        rec->births = n_place;
-        rec->deferred_claim = dc - n_win;  // candidates - claimed cells
-        rec->deferred_capacity = n_win - n_place;
-        rec->population = n_surv + n_place;
-        rec->resources = res;
-        *count_of(p, t + 1, w) = n_surv + n_place;
-        p.n_births[w] = n_place;
-        unsigned long long *tot = p.totals;
-        if (w == 0) atomicAdd(tot + 0, 1ull);
-        atomicAdd(tot + 1, (unsigned long long)n_start);
-        atomicAdd(tot + 2, (unsigned long long)HW);
-        atomicAdd(tot + 3, (unsigned long long)n_place);
-        atomicAdd(tot + 4, (unsigned long long)(de + da));
-        atomicAdd(tot + 5, (unsigned long long)eaten);
-        atomicAdd(tot + 6, (unsigned long long)grown);
+        rank_finalize(p, w, t, k.n_start, k.n_surv, k.n_win, k.n_place);
         p.t[w] = t + 1;
     }
     __syncthreads();
-    tick(3);
 }
 
 // ------------------------------------------------------------------- a5 mutation
@@ -623,10 +628,11 @@ __device__ __forceinline__ void gauss_pair(uint64_t seed, int64_t t, int cellc, 
 }
 
 // U independent items per thread: all loads, then all Philox/log/sincos chains, then all
-// stores (stores last, so no child store can alias an input the compiler must re-order)
-template <int U>
+// stores (stores last, so no child store can alias an input the compiler must re-order).
+// birth(b, child, parent, cell) gives birth b's slots and cell.
+template <int U, typename Birth>
 __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t t, uint64_t seed, int Q, size_t k0,
-                                             size_t stride, size_t n) {
+                                             size_t stride, size_t n, Birth birth) {
     float pa[U], pb[U];
     int cellc[U], d0[U], dstep[U], j0[U];
     float *dst[U];
@@ -637,9 +643,8 @@ __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t 
         if (k >= n) continue;
         const int b = (int)(k / (size_t)Q), it = (int)(k - (size_t)b * Q);
         mutate_item(p, it, d0[u], dstep[u], j0[u]);
-        const size_t bs = (size_t)w * p.S + b;
-        const int child = p.birth_child[bs], parent = p.birth_parent[bs];
-        cellc[u] = p.birth_cell[bs];
+        int child, parent;
+        birth(b, child, parent, cellc[u]);
         const float *wp = p.weights + ((size_t)w * p.S + parent) * p.Pd + d0[u];
         pa[u] = wp[0];
         pb[u] = dstep[u] ? wp[dstep[u]] : 0.f;
@@ -648,14 +653,7 @@ __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t 
     double za[U], zb[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (dst[u]) {
-#if ECO_DIAG_SKIP & 4
-            za[u] = (double)cellc[u];
-            zb[u] = (double)j0[u];
-#else
-            gauss_pair(seed, t, cellc[u], j0[u], za[u], zb[u]);
-#endif
-        }
+        if (dst[u]) gauss_pair(seed, t, cellc[u], j0[u], za[u], zb[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (!dst[u]) continue;
@@ -664,6 +662,7 @@ __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t 
     }
 }
 
+// all worlds, birth lists from global memory, after the rank advanced t
 __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     constexpr int U = 2;
     const int Q = mutate_items_per_child(p);
@@ -673,7 +672,13 @@ __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, si
         const size_t n = (size_t)nb * Q;
         const int64_t t = p.t[w] - 1;
         const uint64_t seed = p.seeds[w];
-        for (size_t k = gtid; k < n; k += U * gthreads) mutate_batch<U>(p, w, t, seed, Q, k, gthreads, n);
+        const size_t ws = (size_t)w * p.S;
+        auto birth = [&](int b, int &child, int &parent, int &cell) {
+            child = p.birth_child[ws + b];
+            parent = p.birth_parent[ws + b];
+            cell = p.birth_cell[ws + b];
+        };
+        for (size_t k = gtid; k < n; k += U * gthreads) mutate_batch<U>(p, w, t, seed, Q, k, gthreads, n, birth);
     }
 }
 

@@ -1,13 +1,13 @@
 // step.cu — the kernels of one world step (sm_100a).
 //
 // Graph mode (sim_step): two launches per step,
-//   k_policy_tma  (Hd = 32)  a2 observation + a3 per-agent LSTM/head/argmax + the claim
-//                 half of a4; each warp streams its agents' weights with 1-D TMA bulk
-//                 copies (cp.async.bulk) through a 3-stage shared-memory pipeline
+//   k_policy_half (Hd = 32)  a2 observation + a3 per-agent LSTM/head/argmax + the claim
+//                 half of a4; one agent per half-warp, its weights streamed as 512-B
+//                 chunks through a per-agent cp.async ring in shared memory
 //   k_policy_reg  (Hd = 4, 8, 16) the same step with register loads, lane groups of Hd
 //   k_post        cooperative: a4 move/consume/physiology/death | grid barrier | a5 birth
-//                 candidates | barrier | a5 rank, winners, placement, t += 1 | barrier |
-//                 a1 regrowth of step t+1 beside a5 mutation of the children
+//                 candidates | barrier | a5 rank (every block), winners, placement and
+//                 counters (block 0), a1 regrowth of step t+1, a5 mutation, t += 1
 // (the first step after create/set_state is preceded by a standalone k_regrow).
 // Instrumented mode (sim_step_timed): the same phases as separate kernels, timed one by one.
 #include "phases.cuh"
@@ -20,8 +20,10 @@
 #ifndef ECO_SPARSE_BULK
 #define ECO_SPARSE_BULK 0
 #endif
-// Hd = 32 policy kernel: 0 = register-streaming k_policy_reg<32> (measured faster: 43 vs
-// 73 us per step at ~5,000 agents), 1 = the per-warp TMA/cp.async pipeline k_policy_tma
+// Hd = 32 policy kernel: 0 = k_policy_half (one agent per half-warp, per-lane cp.async
+// ring), 1 = the per-warp TMA/cp.async pipeline k_policy_tma (73 us per step at ~5,000
+// agents), 2 = register-streaming k_policy_reg<32> (43 us), 3 = k_policy_ring (one warp per
+// agent, 34 us), 4 = k_policy_stream (persistent warps, ring across agents, 39 us)
 #ifndef ECO_POLICY_TMA
 #define ECO_POLICY_TMA 0
 #endif
@@ -598,22 +600,729 @@ __global__ void __launch_bounds__(256) k_policy_reg(DevParams p) {
     if (k == 0) ctr.flush(p);
 }
 
+// ============================================================ k_policy_ring (Hd = 32)
+// One warp per live agent (lane k = hidden unit k, gates i,f,g,o in a float4), a block of
+// RING_WARPS independent warps, the grid sized to all slots (inactive warps exit early).
+// The agent's weights are streamed as a sequence of 512-B chunks, one 16-B cp.async per lane
+// (each lane copies exactly the 16 B it later reads: no cross-lane synchronisation), through
+// a per-warp ring of RING_DEPTH chunks kept in flight (one commit group per chunk):
+//   q = 0..31        W_hh^T row q   (acc += h_q * chunk)   - needs only the slot, so these
+//   q = 32           b                                        stream while the observation
+//   q = 33..32+nnz   active W_ih^T columns, ascending (acc += chunk)    mask is gathered
+// The column offsets are compacted once per agent into a per-warp shared list (ballots), and
+// the loops are unrolled so that ring slots and W_hh offsets are compile-time constants.
+constexpr int RING_WARPS = 8;
+constexpr int RING_DEPTH = 12;
+constexpr int RING_COLS = 128;  // >= I = 2(2r+1)^2 for r <= 3 (98)
+constexpr int RING_SMEM = RING_WARPS * RING_DEPTH * 32 * 16;  // 48 KB (dynamic: + lists > 48 KB)
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(RING_WARPS * 32, 4) k_policy_ring(DevParams p) {
+    constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33;  // chunk q: W_hh row q < 32, b at 32, columns from 33
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ float4 ring_smem[];  // [RING_WARPS][RING_DEPTH][32]
+    __shared__ int s_col[RING_WARPS][RING_COLS];  // float offsets idx * HD * 4 of the active columns
+    __shared__ int s_w[RING_WARPS];
+    __shared__ unsigned long long s_nnz[RING_WARPS], s_ties[RING_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    step_housekeeping(p);
+    const long total = (long)p.n_worlds * p.S;
+    const long v = (long)blockIdx.x * RING_WARPS + warp;
+    const bool in_range = v < total;
+    const int w = in_range ? (int)(v / p.S) : 0;
+    const int i = in_range ? (int)(v - (long)w * p.S) : 0;
+    const int64_t t = p.t[w];
+    const bool active = in_range && i < *count_of(p, t, w);
+    unsigned long long nnz_w = 0ull, tie_w = 0ull;
+#ifdef ECO_POLICY_TRACE
+    // diagnostic build: per agent (start, mask ready, end, nnz) of the last launch
+    unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(v & 8191);
+    if (lane == 0 && active) trace[0] = globaltimer_ns();
+#endif
+    if (active) {
+        const int slot = list_of(p, t, w)[i];
+        const size_t gs = (size_t)w * p.S + slot;
+        const float *Wl = p.weights + gs * (size_t)p.Pd + lane * 4;  // this lane's 16 B of any chunk
+        const float *Whh = Wl + p.off_hh;
+        float4 *rg = ring_smem + (warp * RING_DEPTH) * 32 + lane;  // ring slot s of this lane: rg[s * 32]
+        int *cols = s_col[warp];
+#pragma unroll
+        for (int q = 0; q < RING_DEPTH; ++q) {  // prologue: W_hh rows 0..RING_DEPTH-1
+            cp_async16(rg + q * 32, Whh + q * HD * 4, 0ull);
+            cp_commit();
+        }
+        const float hk = p.h[gs * HD + lane];
+        const float ck = p.c[gs * HD + lane];
+        float wo[5], bo[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            wo[a] = __ldg(Wl - lane * 4 + p.off_out + a * HD + lane);
+            bo[a] = __ldg(Wl - lane * 4 + p.off_bout + a);
+        }
+        const int cellv = p.cell[gs];
+        uint64_t m_lo, m_hi;
+        {
+            const int y = cellv / p.W, x = cellv - y * p.W;
+            obs_mask(p, w, t, y, x, lane, 32, FULL, m_lo, m_hi);
+        }
+        // compacted list of the active columns (ascending)
+        int nnz = 0;
+#pragma unroll
+        for (int part = 0; part < 4; ++part) {
+            const int bit = part * 32 + lane;
+            const uint64_t word = part < 2 ? m_lo : m_hi;
+            const bool on = ((word >> (bit & 63)) & 1ull) != 0ull;
+            const unsigned bal = __ballot_sync(FULL, on);
+            if (on) cols[nnz + __popc(bal & ((1u << lane) - 1u))] = bit * HD * 4;
+            nnz += __popc(bal);
+        }
+        __syncwarp();
+#ifdef ECO_POLICY_TRACE
+        if (lane == 0) {
+            trace[1] = globaltimer_ns();
+            trace[3] = nnz;
+        }
+#endif
+        const int N = Q0 + nnz;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        // W_hh rows: consume q, refill with chunk q + RING_DEPTH
+#pragma unroll
+        for (int q = 0; q < NHH; ++q) {
+            cp_wait<RING_DEPTH - 1>();
+            const float4 c4 = rg[(q % RING_DEPTH) * 32];
+            const float hj = __shfl_sync(FULL, hk, q);
+            acc.x = fmaf(hj, c4.x, acc.x);
+            acc.y = fmaf(hj, c4.y, acc.y);
+            acc.z = fmaf(hj, c4.z, acc.z);
+            acc.w = fmaf(hj, c4.w, acc.w);
+            const int qn = q + RING_DEPTH;
+            if (qn < NHH) {
+                cp_async16(rg + (q % RING_DEPTH) * 32, Whh + qn * HD * 4, 0ull);
+            } else if (qn == QB) {
+                cp_async16(rg + (q % RING_DEPTH) * 32, Wl + p.off_b, 0ull);
+            } else if (qn - Q0 < nnz) {
+                cp_async16(rg + (q % RING_DEPTH) * 32, Wl + cols[qn - Q0], 0ull);
+            }
+            cp_commit();
+        }
+        {  // q = 32: the bias
+            constexpr int q = QB;
+            cp_wait<RING_DEPTH - 1>();
+            const float4 c4 = rg[(q % RING_DEPTH) * 32];
+            acc.x += c4.x;
+            acc.y += c4.y;
+            acc.z += c4.z;
+            acc.w += c4.w;
+            if (q + RING_DEPTH - Q0 < nnz) cp_async16(rg + (q % RING_DEPTH) * 32, Wl + cols[q + RING_DEPTH - Q0], 0ull);
+            cp_commit();
+        }
+        // active columns q = 33.., RING_DEPTH per round so ring slots stay static
+        for (int q0 = Q0; q0 < N; q0 += RING_DEPTH) {
+#pragma unroll
+            for (int s = 0; s < RING_DEPTH; ++s) {
+                const int q = q0 + s;
+                if (q >= N) break;
+                constexpr int base = Q0 % RING_DEPTH;
+                const int rs = (base + s) % RING_DEPTH;
+                cp_wait<RING_DEPTH - 1>();
+                const float4 c4 = rg[rs * 32];
+                acc.x += c4.x;
+                acc.y += c4.y;
+                acc.z += c4.z;
+                acc.w += c4.w;
+                const int cn = q + RING_DEPTH - Q0;
+                if (cn < nnz) cp_async16(rg + rs * 32, Wl + cols[cn], 0ull);
+                cp_commit();
+            }
+        }
+        cp_wait<0>();
+        const float ig = sigmoidf_acc(acc.x);
+        const float fg = sigmoidf_acc(acc.y);
+        const float gg = tanhf(acc.z);
+        const float og = sigmoidf_acc(acc.w);
+        const float cn = fg * ck + ig * gg;
+        const float hn = og * tanhf(cn);
+        float lg[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            float s = wo[a] * hn;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+            lg[a] = s + bo[a];
+        }
+        p.h[gs * HD + lane] = hn;
+        p.c[gs * HD + lane] = cn;
+        bool bad = !isfinite(hn) || !isfinite(cn);
+        if (lane == 0) {
+            PolicyCounters one;  // the block flushes the counters below
+            agent_epilogue(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, one, bad);
+            nnz_w = one.nnz;
+            tie_w = one.ties;
+        }
+        if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
+#ifdef ECO_POLICY_TRACE
+        if (lane == 0) trace[2] = globaltimer_ns();
+#endif
+    }
+    // per-block counters: one atomic per (block, world) run instead of one per agent
+    if (lane == 0) {
+        s_w[warp] = active ? w : -1;
+        s_nnz[warp] = nnz_w;
+        s_ties[warp] = tie_w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        PolicyCounters ctr;
+        for (int k = 0; k < RING_WARPS; ++k)
+            if (s_w[k] >= 0) {
+                ctr.add(p, s_w[k], s_nnz[k], false);
+                ctr.ties += s_ties[k];
+            }
+        ctr.flush(p);
+    }
+}
+
+// ========================================================== k_policy_stream (Hd = 32)
+// Persistent form of k_policy_ring: a grid of STREAM_BPS blocks per SM, every warp walks the
+// live agents v = g, g + TW, g + 2TW, ... (g = its warp index interleaved over SMs, TW = all
+// warps) and its ring never drains between agents:
+//   * an agent's chunk sequence (32 W_hh rows, b, nnz columns) is padded to a multiple of
+//     RING_DEPTH ticks, so every agent starts on ring slot 0 and all slot indices are
+//     compile-time constants; pad ticks consume nothing and commit empty groups;
+//   * the refills of the current agent's last RING_DEPTH ticks are the next agent's first
+//     W_hh rows;
+//   * the next agent's list slot, cell, h/c and observation rows are gathered in stages at
+//     fixed ticks of the current agent's W_hh phase (0, 4, 10, 18), so its mask and column
+//     list are ready long before its first column chunk is issued.
+constexpr int STREAM_BPS = 3;
+
+// observation rows of one agent: lane q < 2(2r+1) loads the two plane words of its row
+__device__ __forceinline__ void obs_issue(const DevParams &p, int w, int64_t t, int cellv, int lane, uint32_t &wlo,
+                                          uint32_t &whi) {
+    const int wd = 2 * p.r + 1;
+    const int y = cellv / p.W, x = cellv - y * p.W;
+    wlo = whi = 0u;
+    if (lane < 2 * wd) {
+        const int ch = lane / wd, row = lane - ch * wd;
+        const int yy = y - p.r + row;
+        if (yy >= 0 && yy < p.H) {
+            const uint32_t *pl = ch ? p.occ + (size_t)w * plane_words(p) : plane_next(p, t) + (size_t)w * plane_words(p);
+            const uint32_t *rw = pl + (size_t)yy * p.WW;
+            const int w0 = (x - p.r) >> 5;
+            if (w0 >= 0 && w0 < p.WW) wlo = __ldg(rw + w0);
+            if (w0 + 1 >= 0 && w0 + 1 < p.WW) whi = __ldg(rw + w0 + 1);
+        }
+    }
+}
+__device__ __forceinline__ void obs_finish(const DevParams &p, int cellv, int lane, uint32_t wlo, uint32_t whi,
+                                           uint64_t &m_lo, uint64_t &m_hi) {
+    const int wd = 2 * p.r + 1;
+    const int y = cellv / p.W, x = cellv - y * p.W;
+    (void)y;
+    uint64_t lo = 0ull, hi = 0ull;
+    if (lane < 2 * wd) {
+        const int ch = lane / wd, row = lane - ch * wd;
+        const uint64_t bits = __funnelshift_r(wlo, whi, (x - p.r) & 31) & ((1u << wd) - 1u);
+        const int pos = ch * wd * wd + row * wd;
+        if (pos < 64) {
+            lo = bits << pos;
+            if (pos + wd > 64) hi = bits >> (64 - pos);
+        } else {
+            hi = bits << (pos - 64);
+        }
+    }
+    const uint32_t a0 = __reduce_or_sync(0xffffffffu, (uint32_t)lo), a1 = __reduce_or_sync(0xffffffffu, (uint32_t)(lo >> 32));
+    const uint32_t a2 = __reduce_or_sync(0xffffffffu, (uint32_t)hi), a3 = __reduce_or_sync(0xffffffffu, (uint32_t)(hi >> 32));
+    m_lo = ((uint64_t)a1 << 32) | a0;
+    m_hi = ((uint64_t)a3 << 32) | a2;
+}
+// compacted ascending list of the active columns as float offsets; returns nnz
+__device__ __forceinline__ int obs_columns(uint64_t m_lo, uint64_t m_hi, int lane, int *cols) {
+    int nnz = 0;
+#pragma unroll
+    for (int part = 0; part < 4; ++part) {
+        const int bit = part * 32 + lane;
+        const uint64_t word = part < 2 ? m_lo : m_hi;
+        const bool on = ((word >> (bit & 63)) & 1ull) != 0ull;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (on) cols[nnz + __popc(bal & ((1u << lane) - 1u))] = bit * 32 * 4;
+        nnz += __popc(bal);
+    }
+    __syncwarp();
+    return nnz;
+}
+
+__global__ void __launch_bounds__(RING_WARPS * 32, STREAM_BPS) k_policy_stream(DevParams p) {
+    constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = RING_DEPTH;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ float4 ring_smem[];  // [RING_WARPS][R][32]
+    __shared__ int s_col[RING_WARPS][2][RING_COLS];
+    __shared__ int s_w[RING_WARPS];
+    __shared__ unsigned long long s_nnz[RING_WARPS], s_ties[RING_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    step_housekeeping(p);
+    const long total = (long)p.n_worlds * p.S;
+    const long TW = (long)gridDim.x * RING_WARPS;
+    float4 *rg = ring_smem + (warp * R) * 32 + lane;  // ring slot s of this lane: rg[s * 32]
+    // world cache of advance(): the first live v' >= v of this warp's residue class
+    int cw = -1, ccount = 0;
+    int64_t ct = 0;
+    auto advance = [&](long v) -> long {
+        while (v < total) {
+            const int w = (int)(v / p.S);
+            if (w != cw) {
+                cw = w;
+                ct = p.t[w];
+                ccount = *count_of(p, ct, w);
+            }
+            if (v - (long)w * p.S < ccount) return v;
+            const long nb = (long)(w + 1) * p.S;  // this residue's first v in world w+1
+            v += ((nb - v + TW - 1) / TW) * TW;
+        }
+        return total;
+    };
+    PolicyCounters ctr;
+    long vA = advance((long)warp * gridDim.x + blockIdx.x);
+    int wA = 0, iA = 0, slotA = 0, cellA = 0, nnzA = 0, buf = 0;
+    int64_t tA = 0;
+    size_t gsA = 0;
+    const float *WlA = nullptr;
+    uint64_t mAlo = 0ull, mAhi = 0ull;
+    float hkA = 0.f, ckA = 0.f;
+    if (vA < total) {  // the first agent: its own gather chain, W_hh streaming meanwhile
+        wA = cw;
+        tA = ct;
+        iA = (int)(vA - (long)wA * p.S);
+        slotA = list_of(p, tA, wA)[iA];
+        gsA = (size_t)wA * p.S + slotA;
+        WlA = p.weights + gsA * (size_t)p.Pd + lane * 4;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            cp_async16(rg + q * 32, WlA + p.off_hh + q * HD * 4, 0ull);
+            cp_commit();
+        }
+        cellA = p.cell[gsA];
+        hkA = p.h[gsA * HD + lane];
+        ckA = p.c[gsA * HD + lane];
+        uint32_t rlo, rhi;
+        obs_issue(p, wA, tA, cellA, lane, rlo, rhi);
+        obs_finish(p, cellA, lane, rlo, rhi, mAlo, mAhi);
+        nnzA = obs_columns(mAlo, mAhi, lane, s_col[warp][0]);
+    }
+    while (vA < total) {
+#ifdef ECO_POLICY_TRACE
+        unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(vA & 8191);
+        if (lane == 0) {
+            trace[0] = globaltimer_ns();
+            trace[1] = trace[0];
+            trace[3] = nnzA;
+        }
+#endif
+        const int NA = Q0 + nnzA, TA = (NA + R - 1) / R * R;
+        const int *colsA = s_col[warp][buf];
+        const float *WhhA = WlA + p.off_hh;
+        float wo[5], bo[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            wo[a] = __ldg(WlA - lane * 4 + p.off_out + a * HD + lane);
+            bo[a] = __ldg(WlA - lane * 4 + p.off_bout + a);
+        }
+        // next agent (B) state, gathered in stages
+        long vB = total;
+        int wB = 0, slotB = 0, cellB = 0, nnzB = 0;
+        int64_t tB = 0;
+        size_t gsB = 0;
+        const float *WlB = nullptr;
+        uint32_t rlo = 0u, rhi = 0u;
+        uint64_t mBlo = 0ull, mBhi = 0ull;
+        float hkB = 0.f, ckB = 0.f;
+        // refill the slot of tick k with the sequence's chunk kn = k + R: own chunk, a pad
+        // (nothing) or one of B's first W_hh rows
+        auto refill = [&](int kn, int slot) {
+            const float *src = nullptr;
+            if (kn < NA) src = kn < NHH ? WhhA + kn * HD * 4 : (kn == QB ? WlA + p.off_b : WlA + colsA[kn - Q0]);
+            else if (kn >= TA && vB < total) src = WlB + p.off_hh + (kn - TA) * HD * 4;
+            if (src) cp_async16(rg + slot * 32, src, 0ull);
+            cp_commit();
+        };
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < NHH; ++k) {  // W_hh rows
+            if (k == 0) {
+                vB = advance(vA + TW);
+                if (vB < total) {
+                    wB = cw;
+                    tB = ct;
+                    slotB = list_of(p, tB, wB)[vB - (long)wB * p.S];
+                }
+            } else if (k == 4 && vB < total) {
+                gsB = (size_t)wB * p.S + slotB;
+                WlB = p.weights + gsB * (size_t)p.Pd + lane * 4;
+                cellB = p.cell[gsB];
+                hkB = p.h[gsB * HD + lane];
+                ckB = p.c[gsB * HD + lane];
+            } else if (k == 10 && vB < total) {
+                obs_issue(p, wB, tB, cellB, lane, rlo, rhi);
+            } else if (k == 18 && vB < total) {
+                obs_finish(p, cellB, lane, rlo, rhi, mBlo, mBhi);
+                nnzB = obs_columns(mBlo, mBhi, lane, s_col[warp][buf ^ 1]);
+            }
+            cp_wait<R - 1>();
+            const float4 c4 = rg[(k % R) * 32];
+            const float hj = __shfl_sync(FULL, hkA, k);
+            acc.x = fmaf(hj, c4.x, acc.x);
+            acc.y = fmaf(hj, c4.y, acc.y);
+            acc.z = fmaf(hj, c4.z, acc.z);
+            acc.w = fmaf(hj, c4.w, acc.w);
+            if (k + R < NHH) {
+                cp_async16(rg + (k % R) * 32, WhhA + (k + R) * HD * 4, 0ull);
+                cp_commit();
+            } else if (k + R == QB) {
+                cp_async16(rg + (k % R) * 32, WlA + p.off_b, 0ull);
+                cp_commit();
+            } else {
+                refill(k + R, k % R);
+            }
+        }
+        {  // tick 32: the bias
+            constexpr int k = QB;
+            cp_wait<R - 1>();
+            const float4 c4 = rg[(k % R) * 32];
+            acc.x += c4.x;
+            acc.y += c4.y;
+            acc.z += c4.z;
+            acc.w += c4.w;
+            refill(k + R, k % R);
+        }
+#pragma unroll
+        for (int k = Q0; k < 3 * R; ++k) {  // ticks 33..35 (slots 9..11)
+            cp_wait<R - 1>();
+            if (k < NA) {
+                const float4 c4 = rg[(k % R) * 32];
+                acc.x += c4.x;
+                acc.y += c4.y;
+                acc.z += c4.z;
+                acc.w += c4.w;
+            }
+            refill(k + R, k % R);
+        }
+        for (int k0 = 3 * R; k0 < TA; k0 += R) {  // full rounds of R ticks
+#pragma unroll
+            for (int s2 = 0; s2 < R; ++s2) {
+                const int k = k0 + s2;
+                cp_wait<R - 1>();
+                if (k < NA) {
+                    const float4 c4 = rg[s2 * 32];
+                    acc.x += c4.x;
+                    acc.y += c4.y;
+                    acc.z += c4.z;
+                    acc.w += c4.w;
+                }
+                refill(k + R, s2);
+            }
+        }
+#ifdef ECO_POLICY_TRACE
+        if (lane == 0) trace[1] = globaltimer_ns();
+#endif
+        // epilogue of A (B's first R chunks are in flight)
+        const float ig = sigmoidf_acc(acc.x);
+        const float fg = sigmoidf_acc(acc.y);
+        const float gg = tanhf(acc.z);
+        const float og = sigmoidf_acc(acc.w);
+        const float cn = fg * ckA + ig * gg;
+        const float hn = og * tanhf(cn);
+        float lg[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            float sm = wo[a] * hn;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(FULL, sm, o);
+            lg[a] = sm + bo[a];
+        }
+        p.h[gsA * HD + lane] = hn;
+        p.c[gsA * HD + lane] = cn;
+        bool bad = !isfinite(hn) || !isfinite(cn);
+        if (lane == 0) agent_epilogue(p, wA, iA, slotA, gsA, tA, cellA, lg, mAlo, mAhi, *p.forced_on, ctr, bad);
+        if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
+#ifdef ECO_POLICY_TRACE
+        if (lane == 0) trace[2] = globaltimer_ns();
+#endif
+        // B becomes the current agent
+        vA = vB;
+        wA = wB;
+        tA = tB;
+        iA = (int)(vB - (long)wB * p.S);
+        slotA = slotB;
+        gsA = gsB;
+        WlA = WlB;
+        cellA = cellB;
+        nnzA = nnzB;
+        mAlo = mBlo;
+        mAhi = mBhi;
+        hkA = hkB;
+        ckA = ckB;
+        buf ^= 1;
+    }
+    cp_wait<0>();
+    // per-block counters: one atomic per (block, world) run
+    if (lane == 0) {
+        s_w[warp] = ctr.w;
+        s_nnz[warp] = ctr.nnz;
+        s_ties[warp] = ctr.ties;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        PolicyCounters bc;
+        for (int k = 0; k < RING_WARPS; ++k)
+            if (s_w[k] >= 0) {
+                bc.add(p, s_w[k], s_nnz[k], false);
+                bc.ties += s_ties[k];
+            }
+        bc.flush(p);
+    }
+}
+
+// ============================================================ k_policy_half (Hd = 32)
+// k_policy_ring with one agent per HALF-warp, so that a launch keeps every live agent of the
+// paper-scale world resident at once (4 blocks x 16 agents per SM = 9,472 >= 8,192 slots):
+// no second wave, the tail is one agent's own latency.  Half-lane h owns hidden units h and
+// h+16 (two float4 gate accumulators) and copies/reads their 2 x 16 B of every 512-B chunk.
+// Ring: HALF_DEPTH chunks per agent (3 KB) in flight; 16 agents per block interleaved over
+// the blocks (agent v = a * gridDim + block).  Column indices are compacted to bytes.
+constexpr int HALF_AGENTS = 16;  // per block (8 warps)
+constexpr int HALF_DEPTH = 6;
+constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB
+
+__global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
+    constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ float4 half_smem[];  // [HALF_AGENTS][R][32 units]
+    __shared__ uint8_t s_col[HALF_AGENTS][RING_COLS];
+    __shared__ int s_w[HALF_AGENTS];
+    __shared__ unsigned long long s_nnz[HALF_AGENTS], s_ties[HALF_AGENTS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = lane >> 4, hl = lane & 15;
+    const int ag = warp * 2 + half;                 // agent of this half-warp within the block
+    const unsigned hmask = 0xffffu << (16 * half);  // this half's lanes
+    step_housekeeping(p);
+    const long total = (long)p.n_worlds * p.S;
+    const long v = (long)ag * gridDim.x + blockIdx.x;
+    const bool in_range = v < total;
+    const int w = in_range ? (int)(v / p.S) : 0;
+    const int i = in_range ? (int)(v - (long)w * p.S) : 0;
+    const int64_t t = p.t[w];
+    const bool active = in_range && i < *count_of(p, t, w);
+    unsigned long long nnz_a = 0ull, tie_a = 0ull;
+    if (__any_sync(FULL, active)) {  // both halves stay converged for the warp-wide intrinsics
+        int slot = 0, cellv = 0;
+        size_t gs = 0;
+        const float *Wl = p.weights;  // + hl * 4: unit hl of a chunk; unit hl + 16 at + 64 floats
+        if (active) {
+            slot = list_of(p, t, w)[i];
+            gs = (size_t)w * p.S + slot;
+            Wl = p.weights + gs * (size_t)p.Pd + hl * 4;
+        }
+        float4 *rg = half_smem + (ag * R) * 32 + hl;  // slot s, unit hl: rg[s * 32]; unit hl+16: rg[s * 32 + 16]
+        const float *Whh = Wl + p.off_hh;
+        auto issue = [&](int slot_, const float *src) {
+            if (active) {
+                cp_async16(rg + slot_ * 32, src, 0ull);
+                cp_async16(rg + slot_ * 32 + 16, src + 64, 0ull);
+            }
+        };
+#pragma unroll
+        for (int q = 0; q < R; ++q) {  // prologue: W_hh rows 0..R-1
+            issue(q, Whh + q * HD * 4);
+            cp_commit();
+        }
+        float hk0 = 0.f, hk1 = 0.f, ck0 = 0.f, ck1 = 0.f;
+        float wo0[5], wo1[5], bo[5];
+        if (active) {
+            hk0 = p.h[gs * HD + hl];
+            hk1 = p.h[gs * HD + hl + 16];
+            ck0 = p.c[gs * HD + hl];
+            ck1 = p.c[gs * HD + hl + 16];
+            cellv = p.cell[gs];
+        }
+        const float *Wo = Wl - hl * 4;
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            wo0[a] = active ? __ldg(Wo + p.off_out + a * HD + hl) : 0.f;
+            wo1[a] = active ? __ldg(Wo + p.off_out + a * HD + hl + 16) : 0.f;
+            bo[a] = active ? __ldg(Wo + p.off_bout + a) : 0.f;
+        }
+        // observation mask: half-lane q < 2(2r+1) loads row q; OR over the half
+        uint64_t m_lo = 0ull, m_hi = 0ull;
+        {
+            uint64_t lo = 0ull, hi = 0ull;
+            const int wd = 2 * p.r + 1;
+            if (active && hl < 2 * wd) {
+                const int y = cellv / p.W, x = cellv - y * p.W;
+                const int ch = hl / wd, row = hl - ch * wd;
+                const int yy = y - p.r + row;
+                if (yy >= 0 && yy < p.H) {
+                    const uint32_t *pl =
+                        ch ? p.occ + (size_t)w * plane_words(p) : plane_next(p, t) + (size_t)w * plane_words(p);
+                    const uint64_t bits = row_bits(pl + (size_t)yy * p.WW, p.WW, x - p.r, wd);
+                    const int pos = ch * wd * wd + row * wd;
+                    if (pos < 64) {
+                        lo = bits << pos;
+                        if (pos + wd > 64) hi = bits >> (64 - pos);
+                    } else {
+                        hi = bits << (pos - 64);
+                    }
+                }
+            }
+            const uint32_t a0 = __reduce_or_sync(hmask, (uint32_t)lo), a1 = __reduce_or_sync(hmask, (uint32_t)(lo >> 32));
+            const uint32_t a2 = __reduce_or_sync(hmask, (uint32_t)hi), a3 = __reduce_or_sync(hmask, (uint32_t)(hi >> 32));
+            m_lo = ((uint64_t)a1 << 32) | a0;
+            m_hi = ((uint64_t)a3 << 32) | a2;
+        }
+        // compacted ascending column indices (bytes)
+        uint8_t *cols = s_col[ag];
+        int nnz = 0;
+#pragma unroll
+        for (int part = 0; part < 8; ++part) {
+            const int bit = part * 16 + hl;
+            const uint64_t word = part < 4 ? m_lo : m_hi;
+            const bool on = ((word >> (bit & 63)) & 1ull) != 0ull;
+            const unsigned bal = (__ballot_sync(FULL, on) >> (16 * half)) & 0xffffu;
+            if (on) cols[nnz + __popc(bal & ((1u << hl) - 1u))] = (uint8_t)bit;
+            nnz += __popc(bal);
+        }
+        __syncwarp();
+        const int N = Q0 + nnz;
+        const int Nw = __reduce_max_sync(FULL, active ? N : 0);  // the warp runs the longer sequence
+        auto refill = [&](int kn, int slot_) {
+            if (kn < N) issue(slot_, kn < NHH ? Whh + kn * HD * 4 : (kn == QB ? Wl + p.off_b : Wl + (int)cols[kn - Q0] * HD * 4));
+            cp_commit();
+        };
+        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+#pragma unroll
+        for (int k = 0; k < NHH; ++k) {  // W_hh rows
+            cp_wait<R - 1>();
+            const float4 c0 = rg[(k % R) * 32], c1 = rg[(k % R) * 32 + 16];
+            const float hj = __shfl_sync(FULL, k < 16 ? hk0 : hk1, k & 15, 16);
+            acc0.x = fmaf(hj, c0.x, acc0.x);
+            acc0.y = fmaf(hj, c0.y, acc0.y);
+            acc0.z = fmaf(hj, c0.z, acc0.z);
+            acc0.w = fmaf(hj, c0.w, acc0.w);
+            acc1.x = fmaf(hj, c1.x, acc1.x);
+            acc1.y = fmaf(hj, c1.y, acc1.y);
+            acc1.z = fmaf(hj, c1.z, acc1.z);
+            acc1.w = fmaf(hj, c1.w, acc1.w);
+            if (k + R < NHH) {
+                issue(k % R, Whh + (k + R) * HD * 4);
+                cp_commit();
+            } else if (k + R == QB) {
+                issue(k % R, Wl + p.off_b);
+                cp_commit();
+            } else {
+                refill(k + R, k % R);
+            }
+        }
+        // ticks QB.. : the bias, then the columns; R ticks per round from QB so slots are static
+        for (int k0 = QB; k0 < Nw; k0 += R) {
+#pragma unroll
+            for (int s2 = 0; s2 < R; ++s2) {
+                const int k = k0 + s2;
+                constexpr int base = QB % R;
+                const int rs = (base + s2) % R;
+                cp_wait<R - 1>();
+                if (k < N) {
+                    const float4 c0 = rg[rs * 32], c1 = rg[rs * 32 + 16];
+                    acc0.x += c0.x;
+                    acc0.y += c0.y;
+                    acc0.z += c0.z;
+                    acc0.w += c0.w;
+                    acc1.x += c1.x;
+                    acc1.y += c1.y;
+                    acc1.z += c1.z;
+                    acc1.w += c1.w;
+                }
+                refill(k + R, rs);
+            }
+        }
+        cp_wait<0>();
+        const float cn0 = sigmoidf_acc(acc0.y) * ck0 + sigmoidf_acc(acc0.x) * tanhf(acc0.z);
+        const float hn0 = sigmoidf_acc(acc0.w) * tanhf(cn0);
+        const float cn1 = sigmoidf_acc(acc1.y) * ck1 + sigmoidf_acc(acc1.x) * tanhf(acc1.z);
+        const float hn1 = sigmoidf_acc(acc1.w) * tanhf(cn1);
+        float lg[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            float sm = wo0[a] * hn0 + wo1[a] * hn1;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) sm += __shfl_xor_sync(FULL, sm, o, 16);
+            lg[a] = sm + bo[a];
+        }
+        if (active) {
+            p.h[gs * HD + hl] = hn0;
+            p.h[gs * HD + hl + 16] = hn1;
+            p.c[gs * HD + hl] = cn0;
+            p.c[gs * HD + hl + 16] = cn1;
+            bool bad = !isfinite(hn0) || !isfinite(cn0) || !isfinite(hn1) || !isfinite(cn1);
+            if (hl == 0) {
+                PolicyCounters one;
+                agent_epilogue(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, one, bad);
+                nnz_a = one.nnz;
+                tie_a = one.ties;
+            }
+            if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
+        }
+    }
+    if (hl == 0) {
+        s_w[ag] = active ? w : -1;
+        s_nnz[ag] = nnz_a;
+        s_ties[ag] = tie_a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        PolicyCounters bc;
+        for (int k = 0; k < HALF_AGENTS; ++k)
+            if (s_w[k] >= 0) {
+                bc.add(p, s_w[k], s_nnz[k], false);
+                bc.ties += s_ties[k];
+            }
+        bc.flush(p);
+    }
+}
+
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
     switch (hidden) {
         case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<4>, threads, 0);
         case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<8>, threads, 0);
         case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<16>, threads, 0);
-#if ECO_POLICY_TMA
+#if ECO_POLICY_TMA == 1
         case 32: *blocks_per_sm = 1; return cudaSuccess;
-#else
+#elif ECO_POLICY_TMA == 2
         case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<32>, threads, 0);
+#elif ECO_POLICY_TMA == 3
+        case 32:
+            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_ring, RING_WARPS * 32, RING_SMEM);
+#elif ECO_POLICY_TMA == 4
+        case 32:
+            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_stream, RING_WARPS * 32, RING_SMEM);
+#else
+        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_half, 256, HALF_SMEM);
 #endif
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t policy_prepare() {
-    return cudaFuncSetAttribute(k_policy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_policy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_policy_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, RING_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_policy_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, RING_SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_policy_half, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
 }
 
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
@@ -621,10 +1330,27 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
         case 4: k_policy_reg<4><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
         case 8: k_policy_reg<8><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
         case 16: k_policy_reg<16><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
-#if ECO_POLICY_TMA
+#if ECO_POLICY_TMA == 1
         case 32: k_policy_tma<<<lc.sms, TMA_WARPS * 32, TMA_SMEM, s>>>(p); break;
-#else
+#elif ECO_POLICY_TMA == 2
         case 32: k_policy_reg<32><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
+#elif ECO_POLICY_TMA == 4
+        case 32: k_policy_stream<<<lc.policy_blocks, RING_WARPS * 32, RING_SMEM, s>>>(p); break;
+#elif ECO_POLICY_TMA == 0
+        case 32: {
+            const long slots = (long)p.n_worlds * p.S;
+            const unsigned blocks = (unsigned)((slots + HALF_AGENTS - 1) / HALF_AGENTS);
+            k_policy_half<<<blocks > 0 ? blocks : 1, 256, HALF_SMEM, s>>>(p);
+            break;
+        }
+#else
+        case 32: {
+            // one warp per slot of every world; blocks past the live agents exit at once
+            const long slots = (long)p.n_worlds * p.S;
+            const unsigned blocks = (unsigned)((slots + RING_WARPS - 1) / RING_WARPS);
+            k_policy_ring<<<blocks > 0 ? blocks : 1, RING_WARPS * 32, RING_SMEM, s>>>(p);
+            break;
+        }
 #endif
         default: return cudaErrorInvalidValue;
     }
@@ -633,7 +1359,7 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 
 // ----------------------------------------------------------- standalone phase kernels
 __global__ void __launch_bounds__(256) k_regrow(DevParams p, int ahead) {
-    regrow_phase(p, ahead, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
+    regrow_phase(p, p.t[0] + ahead, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 __global__ void __launch_bounds__(256) k_move(DevParams p) {
@@ -658,13 +1384,13 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 
 // ------------------------------------------------------------------------ k_post
 // a4 move/consume/physiology/death | barrier | a5 birth candidates and claimed cells |
-// barrier | a5 rank, winners, placement, counters, t += 1 | barrier | a1 regrowth of step
-// t+1 (needs only R'' of step t) beside a5 mutation of the children.  A phase that ends in
-// a barrier pays for its writes in the barrier's release fence; the regrowth's plane writes
-// (measured: +3..6 us of fence when they preceded a barrier) go last, where only the
-// kernel's end waits for them.
+// barrier | a5 rank + winners (redundantly in every block), placement and counters (block
+// 0), a1 regrowth of step t+1 (needs only R'' of step t), a5 mutation of the children,
+// t += 1.  With several worlds (or > RANK_SMEM_CAP births) the rank runs one block per world
+// and a third barrier precedes the mutation.  A phase that ends in a barrier pays for its
+// writes in the barrier's release fence; the regrowth's plane writes (measured: +3..6 us of
+// fence when they preceded a barrier) go last, where only the kernel's end waits for them.
 constexpr int POST_THREADS = 512;
-constexpr int POST_BARRIERS = 3;
 #ifdef ECO_BLOCK_CLOCK
 // diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
 // phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
@@ -700,35 +1426,51 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
     // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
     const size_t gtid = interleaved_gtid();
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
-    unsigned long long target = grid_sync_base(bar, POST_BARRIERS);
+    unsigned long long target = grid_sync_base(bar);
+    const int64_t T = p.t[0];  // the step this launch completes (all worlds share t)
     // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
     const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
     uint64_t t0 = clk ? globaltimer_ns() : 0ull, t1;
+    auto lap = [&](int k) {
+        if (clk) {
+            t1 = globaltimer_ns();
+            atomicAdd(p.phase_ns + k, t1 - t0);
+            t0 = t1;
+        }
+    };
 #ifdef ECO_BLOCK_CLOCK
     uint64_t bt_ = globaltimer_ns();
 #endif
     move_phase(p, gtid, gthreads);
     POST_SYNC(0);
-    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 0, t1 - t0); t0 = t1; }
+    lap(0);
     // birth candidates on every thread
     const uint64_t h0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
-    if (!(ECO_DIAG_SKIP & 1)) birth_claim_phase(p, gtid, gthreads);
+    birth_claim_phase(p, gtid, gthreads);
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)  // summed warp durations of block 0
         atomicAdd(p.phase_ns + 8, globaltimer_ns() - h0);
     POST_SYNC(1);
-    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 1, t1 - t0); t0 = t1; }
-    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
-        birth_rank_world<POST_THREADS>(p, w, scratch, s_free, s_bcell);
+    lap(1);
+    // births: one block per world ranks, places and counts them (t += 1).  With fewer worlds
+    // than blocks the idle blocks run the regrowth of step T+1 meanwhile (needs only R'' of
+    // step T; its write-back cost is paid in this barrier, hidden behind the rank).
+    const bool regrow_now = p.n_worlds < (int)gridDim.x;
+    if ((int)blockIdx.x < p.n_worlds) {
+        for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
+            birth_rank_world<POST_THREADS>(p, w, scratch, s_free, s_bcell);
+    } else {
+        // the idle blocks' threads, renumbered densely (warp-interleaved over those blocks)
+        const unsigned nb = gridDim.x - p.n_worlds, b = blockIdx.x - p.n_worlds;
+        const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
+        const uint64_t r0 = b == 0 ? globaltimer_ns() : 0ull;
+        regrow_phase(p, T + 1, btid, (size_t)nb * blockDim.x);
+        if (b == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
+    }
     POST_SYNC(2);
-    if (clk) { t1 = globaltimer_ns(); atomicAdd(p.phase_ns + 2, t1 - t0); t0 = t1; }
-    // the regrowth of step t+1 (t has advanced: ahead = 0) on the second half of the threads,
-    // then the children's weights on all of them.  Nothing in this launch reads the plane
-    // the regrowth writes, so no barrier (and no release fence) follows it.
-    const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
-    if (gtid >= half && !(ECO_DIAG_SKIP & 2)) {
-        const uint64_t r0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
-        regrow_phase(p, 0, gtid - half, gthreads - half);
-        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
+    lap(2);
+    if (!regrow_now) {  // every block ranked a world: the regrowth goes beside the mutation
+        const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
+        if (gtid >= half) regrow_phase(p, T + 1, gtid - half, gthreads - half);
     }
     mutate_phase(p, gtid, gthreads);
 #ifdef ECO_BLOCK_CLOCK
@@ -736,9 +1478,8 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
     if (threadIdx.x == 0) p.phase_ns[ECO_BLOCK_CLOCK_BASE + (3 * gridDim.x + blockIdx.x) * 3] += globaltimer_ns() - bt_;
 #endif
     if (clk) {
-        t1 = globaltimer_ns();
-        atomicAdd(p.phase_ns + 3, t1 - t0);
-        grid_sync_done(bar);
+        lap(3);
+        grid_sync_done(bar, target);
     }
 }
 

@@ -27,9 +27,9 @@ KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate
 EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns")
-POST_PHASES = ("move", "birth_claim", "birth_rank", "regrow_next+mutate",
-               "rank.setup", "rank.scans", "rank.place", "rank.counters",
-               "claim.warp_sum_b0", "regrow.warp_sum_b0")  # block 0: 16 claim warps, 8 regrow warps
+POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
+               "reserved4", "reserved5", "reserved6", "reserved7",
+               "claim.warp_sum_b0", "regrow.warp_sum_b1")  # block 0: 16 claim warps; block 1: 16 regrow warps
 
 
 class SimError(RuntimeError):

@@ -27,11 +27,11 @@ world.synchronize()
 world.phase_ns(reset=True)
 world.step(K)
 world.synchronize()
-out = np.zeros(16 + 8192, np.int64)
+out = np.zeros(16 + 32768, np.int64)
 sim._check(sim.lib().sim_get_phase_ns(world._h, sim._ptr(out), -1))
 nb = 148
 blk = out[16:16 + 4 * nb * 3].reshape(4, nb, 3) / K / 1e3
-names = ("move", "claim", "rank", "regrow+mutate")
+names = ("move", "claim", "rank|noise", "mutate")
 for k in range(4):
     wk, wt, fn = blk[k, :, 0], blk[k, :, 1], blk[k, :, 2]
     order = np.argsort(-wk)[:5]
