@@ -309,9 +309,11 @@ def run_ours(args, rank, world_size, local_rank):
             pol_s = ks["policy"] / 1e3
             achieved = pb / pol_s / 1e9
             sb = step_bytes(wc, agents, nnz, births)
+            ratio, ratio_src = traffic_ratio()
             result["roofline"] = {
-                "kernel": "k_policy (observe + LSTM + argmax + move claim)", "bound": "hbm",
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "kernel": "k_policy_half (observe + LSTM + argmax + move claim)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ratio * pb / K if ratio else None, "traffic_source": ratio_src,
                 "bytes_per_launch": pb / K, "launch_ms": ks["policy"] / K, "peak_source": peak_src,
                 "share_of_step": ks["policy"] / kern["step_ms_total"],
             }
@@ -324,6 +326,24 @@ def run_ours(args, rank, world_size, local_rank):
         if e2e is not None:
             result["e2e"] = e2e
     return result, snap, wc
+
+
+def traffic_ratio():
+    """DRAM bytes (read + write) over algorithmic bytes of the policy launch in the newest
+    committed ncu --set full summary (profiles/*_ncu_summary.json, tools/ncu_summary.py);
+    the roofline's `traffic` is this ratio times the bench's algorithmic bytes per launch
+    (the captured launch is one step of the same workload, not the bench's own launches)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+            for rec in d["launches"]:
+                if "policy" in rec["kernel"] and "traffic_over_algorithmic" in rec:
+                    return float(rec["traffic_over_algorithmic"]), os.path.relpath(f, ROOT)
+        except Exception:
+            continue
+    return None, None
 
 
 # -------------------------------------------------------------- oracle (CPU) legs
