@@ -63,7 +63,10 @@ def parse_args():
     return ap.parse_args()
 
 
-def workload(name: str, rank: int) -> workloads.WorldConfig:
+def workload(name: str, rank: int, world_size: int = 1) -> workloads.WorldConfig:
+    """The rank's share of the workload: one independent replica per rank (seed + rank) for
+    the single-world configs, a contiguous slice of the ensemble's worlds for `ensemble`
+    (weak scaling for the former, the ensemble's worlds split for the latter)."""
     if name == "paper_scale":
         wc = workloads.paper_scale()
         return wc.replace(seeds=(wc.seeds[0] + rank,))
@@ -71,7 +74,33 @@ def workload(name: str, rank: int) -> workloads.WorldConfig:
         return workloads.tiny().replace(seeds=(rank,))
     if name == "large_world":
         return workloads.large_world().replace(seeds=(3 + rank,))
-    return workloads.ensemble()
+    return workloads.ensemble().replace(seeds=tuple(workloads.ensemble_shard(world_size, rank)))
+
+
+class Reducer:
+    """Cross-rank reductions of the bench (max of the timed region, sums of work units);
+    identity without torch.distributed.  `device` is where the gloo/nccl tensors live."""
+
+    def __init__(self, dist=None, device="cpu"):
+        self.dist, self.device = dist, device
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def _all(self, v: float, op) -> float:
+        if self.dist is None:
+            return float(v)
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    def max(self, v: float) -> float:
+        return self._all(v, None if self.dist is None else self.dist.ReduceOp.MAX)
+
+    def sum(self, v: float) -> float:
+        return self._all(v, None if self.dist is None else self.dist.ReduceOp.SUM)
 
 
 def peaks():
@@ -168,27 +197,11 @@ def run_ours(args, rank, world_size, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    wc = workload(args.config, rank)
+    wc = workload(args.config, rank, world_size)
     K, W = args.steps, args.warmup
     stream = torch.cuda.Stream(device=dev)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
-    def allmax(v: float) -> float:
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def allsum(v: float) -> float:
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    red = Reducer(dist, dev)
+    barrier, allmax, allsum = red.barrier, red.max, red.sum
 
     with torch.cuda.stream(stream):
         world = sim.World(wc, device=local_rank, stream=stream, log_capacity=max(4096, W + K + 8))

@@ -1,0 +1,94 @@
+"""The N > 1 path on CPU: world-size-2 gloo process groups (127.0.0.1 rendezvous).
+
+bench.py under torchrun gives each rank an independent share of the work (SURVEY.md §8e:
+replicas of the single-world configs, a contiguous slice of the ensemble's worlds) with no
+data-path collective; only the timed region's max and the work sums are reduced.  These
+tests run that host logic with two gloo ranks, each stepping its shard of a small ensemble
+with the oracle, and check that the reduced statistics equal one process stepping every
+world (worlds are independent), and that the timing reduction is a max.
+"""
+import os
+import socket
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import workloads  # noqa: E402
+
+SEEDS = (21, 22, 23, 24, 25)
+STEPS = 15
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _shard_stats(seeds):
+    """Per-world oracle runs of the tiny config; returns (agent-steps, births, deaths, final pop)."""
+    import oracle
+    out = np.zeros(4, np.float64)
+    for sd in seeds:
+        wc = workloads.tiny().replace(seeds=(sd,))
+        ow = oracle.OracleWorld(wc, 0)
+        for _ in range(STEPS):
+            r = ow.step()
+            out[0] += r["population"] + r["deaths_energy"] + r["deaths_age"] - r["births"]  # agents at step start
+            out[1] += r["births"]
+            out[2] += r["deaths_energy"] + r["deaths_age"]
+        out[3] += int(ow.state()["alive"].sum())
+    return out
+
+
+def _worker(rank, world_size, port, path):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        red = bench.Reducer(dist, "cpu")
+        mine = workloads.ensemble_shard(world_size, rank, SEEDS)
+        stats = _shard_stats(mine)
+        red.barrier()
+        tot = [red.sum(v) for v in stats]
+        tmax = red.max(1.0 + rank)  # stands in for each rank's timed region
+        n_worlds = red.sum(len(mine))
+        if rank == 0:
+            np.save(path, np.array(tot + [tmax, n_worlds]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ensemble_shards_partition_the_worlds():
+    for n in range(1, 9):
+        parts = [workloads.ensemble_shard(n, r) for r in range(n)]
+        flat = [s for p in parts for s in p]
+        assert flat == list(range(100, 164))  # contiguous, disjoint, complete, in order
+        sizes = [len(p) for p in parts]
+        assert max(sizes) - min(sizes) <= 1
+    # bench hands each rank its slice; the single-world configs get one replica per rank
+    assert bench.workload("ensemble", 1, 2).seeds == tuple(range(132, 164))
+    assert bench.workload("paper_scale", 3, 8).seeds == (4,)
+
+
+def test_reducer_without_dist_is_identity():
+    red = bench.Reducer()
+    red.barrier()
+    assert red.max(2.5) == 2.5 and red.sum(3.0) == 3.0
+
+
+def test_two_gloo_ranks_reduce_to_the_single_process_result():
+    import torch.multiprocessing as mp
+    path = os.path.join(tempfile.mkdtemp(), "reduced.npy")
+    mp.spawn(_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    got = np.load(path)
+    want = _shard_stats(SEEDS)
+    assert np.array_equal(got[:4], want), (got, want)
+    assert got[4] == 2.0  # max over ranks, not the sum
+    assert got[5] == len(SEEDS)
