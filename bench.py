@@ -233,9 +233,6 @@ def run_ours(args, rank, world_size, local_rank):
         clk = clocks.stop()
         world.synchronize()
         post_phases = {k_: v / K / 1e3 for k_, v in world.phase_ns().items()}
-        # k_post runs 512 threads per block: 16 claim warps in block 0, 16 regrowth warps in block 1
-        for k_, nw in (("claim.warp_sum_b0", 16), ("regrow.warp_sum_b1", 16)):
-            post_phases[k_.split(".")[0] + ".warp_mean"] = post_phases.pop(k_) / nw
         for k_ in [k_ for k_ in post_phases if k_.startswith("reserved")]:
             post_phases.pop(k_)
         step_ms = np.array([a.elapsed_time(b) for a, b in evs], np.float64)

@@ -73,7 +73,7 @@ typedef struct {
     int32_t obs_radius;     /* r: window (2r+1)^2, 0..3                                   */
     int32_t hidden;         /* LSTM hidden size Hd in {4, 8, 16, 32}                      */
     int32_t n_actions;      /* must be 5 (stay, N, S, E, W)                               */
-    int32_t log_capacity;   /* step records kept per world (ring); 0 -> 4096              */
+    int32_t log_capacity;   /* step records kept per world (ring, rounded up to a power of 2); 0 -> 4096 */
     double init_weight_std, mutation_std; /* standard deviations (R23)                   */
     int32_t e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max; /* milli-units;
                                                 e_max = INT32_MAX means no clip          */

@@ -80,7 +80,12 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
         d->off_bout = d->off_out + 5 * d->Hd;
         d->Pd = (d->off_bout + 5 + 31) / 32 * 32;
         d->n_worlds = cfg->n_worlds;
-        d->log_cap = cfg->log_capacity ? cfg->log_capacity : 4096;
+        {  // the ring holds at least log_capacity steps: rounded up to a power of two (a mask)
+            const int want = cfg->log_capacity ? cfg->log_capacity : 4096;
+            int cap = 2;
+            while (cap < want) cap <<= 1;
+            d->log_cap = cap;
+        }
         d->pw = (size_t)d->H * d->WW;
     }
     return SIM_OK;
@@ -302,19 +307,20 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
 
     DevParams &p = h->p;
     p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
+    p.hd_shift = 0;
+    while ((1 << p.hd_shift) < d.Hd) ++p.hd_shift;  // Hd is a power of two (validated)
     p.n_worlds = d.n_worlds; p.r = cfg->obs_radius; p.log_cap = d.log_cap;
+    p.invW = 1.0 / (double)d.W;
     p.repr_steps = cfg->repr_steps; p.max_age = cfg->max_age;
     p.e_init = cfg->e_init; p.e_decay = cfg->e_decay; p.e_gain = cfg->e_gain;
     p.e_repr_gt = cfg->e_repr_gt; p.e_death_le = cfg->e_death_le; p.e_max = cfg->e_max;
     p.cls_k1 = cfg->f_class_min_k[1]; p.cls_k2 = cfg->f_class_min_k[2]; p.cls_k3 = cfg->f_class_min_k[3];
-    p.n_off = 0;
-    for (int dy = -2; dy <= 2; ++dy)
-        for (int dx = -2; dx <= 2; ++dx)
-            if ((dy || dx) && dy * dy + dx * dx <= cfg->regrow_r2) {
-                p.off_dy[p.n_off] = dy;
-                p.off_dx[p.n_off] = dx;
-                ++p.n_off;
-            }
+    for (int dy = -2; dy <= 2; ++dy) {  // the disc dy^2 + dx^2 <= r2 row by row (r2 <= 8: |dx| <= 2)
+        int m = -1;
+        for (int dx = 0; dx <= 2; ++dx)
+            if (dy * dy + dx * dx <= cfg->regrow_r2) m = dx;
+        p.row_dx[dy + 2] = m;
+    }
     p.off_hh = d.off_hh; p.off_b = d.off_b; p.off_out = d.off_out; p.off_bout = d.off_bout;
     p.mutation_std = cfg->mutation_std; p.init_weight_std = cfg->init_weight_std;
     {
@@ -394,9 +400,9 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         int pbs = 0;
         CKC(eco::post_occupancy(&pbs), "occupancy");
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
-        h->lc.post_blocks = prop.multiProcessorCount;  // one 512-thread block per SM
+        h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    CKC(dalloc(h, &h->bar, 2), "alloc");
+    CKC(dalloc(h, &h->bar, 4), "alloc");  // [0] arrivals, [1] next launch's base, [2] births flag
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");

@@ -1,7 +1,7 @@
 // phases.cuh — the phases of one world step as device functions, shared by the standalone
 // kernels (instrumented mode) and the fused kernels of graph mode.
 //
-//   regrow_phase       a1  grid regrowth for step t (+ahead), one 32-cell word per item
+//   regrow_phase       a1  grid regrowth of a step, 1..8 lanes per 32-cell word
 //   move_phase         a4  claim resolution, movement, consumption, physiology, death
 //   birth_claim_phase  a5  lazy move-claim reset, birth candidate, claimed-cell dedup
 //   birth_rank_world   a5  (one block per world) free slots, claimed cells in row-major
@@ -77,9 +77,8 @@ __device__ __forceinline__ void warp_world_add(T v, int w, AddrOf addr_of) {
 // each empty cell grows with p = lat(y)*f(k) + c, k = resources in the
 // Euclidean radius-r disc (centre excluded) of the START-of-step grid (synchronous),
 // drawn as philox(REGROW, t, cell>>2)[cell&3] < T[y][class(k)].  Full cells stay full.
-// The 12 (generally n_off <= 24) neighbour bit-vectors are funnel-shifted words of rows
-// y-2..y+2; k is accumulated bit-sliced (5 planes), ~10 logic ops per neighbour per 32
-// cells.  Philox runs only for 4-cell groups holding an empty cell (exact: draws are keyed
+// The 12 (generally <= 24) neighbour bit-vectors are funnel-shifted words of rows y-2..y+2;
+// k is accumulated bit-sliced (5 planes), ~10 logic ops per neighbour per 32 cells.  Philox runs only for 4-cell groups holding an empty cell (exact: draws are keyed
 // by cell, not by sequence).
 __device__ __forceinline__ uint32_t shifted_word(uint32_t prv, uint32_t cur, uint32_t nxt, int dx) {
     if (dx > 0) return __funnelshift_r(cur, nxt, dx);
@@ -103,11 +102,12 @@ __device__ __forceinline__ uint32_t ge_const(const uint32_t c[5], int m) {
     return gt | eq;
 }
 
-// Regrow word (y, wx) of world w for step `t`: src = plane_cur(t), dst = plane_next(t).
-// Returns the number of cells grown.
-__device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int wx, int64_t t) {
+// Regrow groups [g0, g0 + ng) (4 cells each) of word (y, wx) of world w for step `t`:
+// src = plane_cur(t).  Returns the grown bits (the caller ORs the lanes of the word and
+// stores cur | grow into plane_next(t)); `cur` gets the word's current bits.
+__device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int y, int wx, int64_t t, int g0, int ng,
+                                                  uint32_t &cur) {
     const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
-    uint32_t *dst = plane_next(p, t) + (size_t)w * plane_words(p);
     uint32_t win[5][3];
 #pragma unroll
     for (int dy = -2; dy <= 2; ++dy) {
@@ -119,32 +119,30 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
                 (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
         }
     }
-    const uint32_t cur = win[2][1];
+    cur = win[2][1];
     uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
-    for (int o = 0; o < p.n_off; ++o) {
-        const int dy = p.off_dy[o], dx = p.off_dx[o];
-        uint32_t prv, cen, nxt;
-        switch (dy) {  // dy in [-2, 2] (validated r2 <= 8)
-            case -2: prv = win[0][0]; cen = win[0][1]; nxt = win[0][2]; break;
-            case -1: prv = win[1][0]; cen = win[1][1]; nxt = win[1][2]; break;
-            case 0: prv = win[2][0]; cen = win[2][1]; nxt = win[2][2]; break;
-            case 1: prv = win[3][0]; cen = win[3][1]; nxt = win[3][2]; break;
-            default: prv = win[4][0]; cen = win[4][1]; nxt = win[4][2]; break;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {  // disc row dy = r - 2: offsets dx = -m..m (compact loop)
+        const int m = p.row_dx[r];
+        const uint32_t prv = win[r][0], cen = win[r][1], nxt = win[r][2];
+#pragma unroll 1
+        for (int dx = -m; dx <= m; ++dx) {
+            if (r == 2 && dx == 0) continue;
+            uint32_t cy = shifted_word(prv, cen, nxt, dx), tt;
+            tt = c[0] & cy; c[0] ^= cy; cy = tt;
+            tt = c[1] & cy; c[1] ^= cy; cy = tt;
+            tt = c[2] & cy; c[2] ^= cy; cy = tt;
+            tt = c[3] & cy; c[3] ^= cy; cy = tt;
+            c[4] ^= cy;
         }
-        uint32_t cy = shifted_word(prv, cen, nxt, dx), tt;
-        tt = c[0] & cy; c[0] ^= cy; cy = tt;
-        tt = c[1] & cy; c[1] ^= cy; cy = tt;
-        tt = c[2] & cy; c[2] ^= cy; cy = tt;
-        tt = c[3] & cy; c[3] ^= cy; cy = tt;
-        c[4] ^= cy;
     }
     const uint32_t ge1 = ge_const(c, p.cls_k1), ge2 = ge_const(c, p.cls_k2), ge3 = ge_const(c, p.cls_k3);
     const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
     const uint64_t seed = p.seeds[w];
     const int x_base = wx << 5;
     uint32_t grow = 0u;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
+#pragma unroll 1
+    for (int g = g0; g < g0 + ng; ++g) {
         const int x0 = x_base + 4 * g;
         if (x0 >= p.W) break;
         if (((cur >> (4 * g)) & 0xFu) == 0xFu) continue;  // all four cells full: no draw needed
@@ -159,25 +157,41 @@ __device__ __forceinline__ int regrow_word(const DevParams &p, int w, int y, int
             if (word_of(d, m) < thr) grow |= 1u << b;
         }
     }
-    dst[(size_t)y * p.WW + wx] = cur | grow;
-    return __popc(grow);
+    return grow;
 }
 
-// Grid-stride regrowth of every world for step `tstep` (all worlds share t); one atomic per
-// warp on the world's record of that step.  Must be called by all 32 lanes of a warp.
+// Grid-stride regrowth of every world for step `tstep` (all worlds share t).  A word's 8
+// four-cell groups are split over L = 1..8 consecutive lanes (as many as the threads allow:
+// a small grid gets 8 short chains per word instead of one long one); the lanes of a word
+// OR their grown bits and the first stores the word.  One atomic per warp on the world's
+// record of that step.  Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, size_t gtid, size_t gthreads) {
     const int real_words = (p.W + 31) >> 5;
     const size_t per_world = (size_t)p.H * real_words;
     const size_t total = per_world * p.n_worlds;
-    for (size_t base = gtid - (gtid & 31); base < total; base += gthreads) {
-        const size_t k = base + (gtid & 31);
-        int w = 0;
-        unsigned long long cnt = 0;
-        if (k < total) {
+    int lsh = 0;  // L = 1 << lsh lanes per word
+    while (lsh < 3 && (total << (lsh + 1)) <= gthreads) ++lsh;
+    const int L = 1 << lsh, ng = 8 >> lsh;
+    const size_t items = total << lsh;
+    const unsigned lane = gtid & 31;
+    for (size_t base = gtid - lane; base < items; base += gthreads) {
+        const size_t it = base + lane;
+        const size_t k = it >> lsh;
+        const int sub = (int)(it & (L - 1));
+        int w = 0, y = 0, wx = 0;
+        uint32_t grow = 0u, cur = 0u;
+        if (it < items) {
             w = (int)(k / per_world);
             const size_t r = k - (size_t)w * per_world;
-            const int y = (int)(r / real_words), wx = (int)(r - (size_t)y * real_words);
-            cnt = (unsigned long long)regrow_word(p, w, y, wx, tstep);
+            y = (int)(r / real_words);
+            wx = (int)(r - (size_t)y * real_words);
+            grow = regrow_groups(p, w, y, wx, tstep, sub * ng, ng, cur);
+        }
+        for (int o = 1; o < L; o <<= 1) grow |= __shfl_xor_sync(0xffffffffu, grow, o);
+        unsigned long long cnt = 0;
+        if (it < items && sub == 0) {
+            plane_next(p, tstep)[(size_t)w * plane_words(p) + (size_t)y * p.WW + wx] = cur | grow;
+            cnt = (unsigned long long)__popc(grow);
         }
         warp_world_add<unsigned long long>(cnt, w, [&](int ww) {
             return reinterpret_cast<unsigned long long *>(&record_of(p, tstep, ww)->grown);
@@ -314,24 +328,22 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
                 if (p.repr[gs] >= p.repr_steps) {
                     const uint32_t *O = p.occ + (size_t)w * plane_words(p);
                     const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
-                    const int y = cellv / p.W, x = cellv - y * p.W;
+                    const int y = row_of(p, cellv), x = cellv - y * p.W;
                     // the four neighbours' O'' and R'' bits, loaded together (no dependent chain)
-                    bool freec[4];
+                    uint32_t freem = 0u;  // bit dd: neighbour dd is a candidate
 #pragma unroll
                     for (int dd = 0; dd < 4; ++dd) {
                         const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
                         const bool in = cy >= 0 && cy < p.H && cx >= 0 && cx < p.W;
                         const int c = in ? cy * p.W + cx : cellv;
                         const uint32_t ob = get_bit(O, p, c), rb = get_bit(Rn, p, c);
-                        freec[dd] = in && !ob && !rb;
+                        if (in && !ob && !rb) freem |= 1u << dd;
                     }
                     const uint4 d = draw4(p.seeds[w], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
                     const int s0 = (int)(d.x & 3u);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const int dd = (s0 + kk) & 3;
-                        if (dir == NO_DIR && freec[dd]) dir = (uint8_t)dd;
-                    }
+                    // first candidate of the order s0, s0+1, s0+2, s0+3 (mod 4)
+                    const uint32_t rot = ((freem >> s0) | (freem << (4 - s0))) & 0xFu;
+                    if (rot) dir = (uint8_t)((s0 + __ffs(rot) - 1) & 3);
                     if (dir != NO_DIR) {
                         const int cy = y + dir_dy(dir), c = cy * p.W + x + dir_dx(dir);
                         uint32_t bit;
@@ -385,7 +397,7 @@ __device__ __forceinline__ int birth_parent_of(const DevParams &p, int w, int64_
     const uint32_t *BB = bbits_of(p, t, w);
     const uint8_t *bd = p.bdir + (size_t)w * HW;
     const uint64_t seed = p.seeds[w];
-    const int cy = c / p.W, cx = c - cy * p.W;
+    const int cy = row_of(p, c), cx = c - cy * p.W;
     int qn[4];
     bool claims[4];
 #pragma unroll
@@ -431,8 +443,6 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
     uint32_t bit;
     atomicOr(word_ptr(p.occ + (size_t)w * plane_words(p), p, c, bit), bit);
     p.repr[(size_t)w * p.S + parent] = 0;
-    p.birth_child[(size_t)w * p.S + r] = child;
-    p.birth_parent[(size_t)w * p.S + r] = parent;
     list_of(p, t + 1, w)[n_surv + r] = child;
 }
 
@@ -542,29 +552,58 @@ __device__ __forceinline__ RankCounts rank_counts(const DevParams &p, int w, int
     return k;
 }
 
-// One block ranks and places world w's births, then t += 1 (the path with a barrier
-// between rank and mutation: several worlds, or more births than RANK_SMEM_CAP).
+// Rank world w's births and resolve their winners: the birth lists (child slot, parent
+// slot, cell) of ranks r < n_place go to global memory (all r) and shared memory (r <
+// RANK_SMEM_CAP), n_births[w] = n_place.  All NT threads; ends with a block barrier.
 template <int NT>
-__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int *s_free, int *s_bcell) {
-    const int tid = threadIdx.x;
-    const int64_t t = p.t[w];
-    const RankCounts k = rank_counts(p, w, t);
+__device__ void rank_publish(const DevParams &p, int w, int64_t t, const RankCounts &k, uint32_t *scratch,
+                             int *s_free, int *s_bcell, int *s_par) {
     int32_t *g_free = p.free_list + (size_t)w * p.S, *g_bcell = p.birth_cell + (size_t)w * p.S;
     if (k.n_place > 0) {
         rank_lists<NT>(p, w, t, k.n_place, scratch, s_free, s_bcell, g_free, g_bcell);
-        for (int r = tid; r < k.n_place; r += NT) {  // one birth per thread
+        for (int r = threadIdx.x; r < k.n_place; r += NT) {  // one birth per thread
             const int c = r < RANK_SMEM_CAP ? s_bcell[r] : *reinterpret_cast<volatile int32_t *>(g_bcell + r);
             const int child = r < RANK_SMEM_CAP ? s_free[r] : *reinterpret_cast<volatile int32_t *>(g_free + r);
-            g_bcell[r] = c;  // the mutation phase reads the birth lists from global memory
-            place_child(p, w, t, c, r, k.n_surv, child, birth_parent_of(p, w, t, c));
+            const int par = birth_parent_of(p, w, t, c);
+            if (r < RANK_SMEM_CAP) s_par[r] = par;
+            p.birth_child[(size_t)w * p.S + r] = child;
+            p.birth_parent[(size_t)w * p.S + r] = par;
+            g_bcell[r] = c;
         }
     }
+    if (threadIdx.x == 0) p.n_births[w] = k.n_place;
     __syncthreads();
-    if (tid == 0) {
+}
+
+// Place the published births (children's state, occupancy, lists), then the step's
+// counters and t += 1.  All NT threads of the block that ran rank_publish.
+template <int NT>
+__device__ void rank_place(const DevParams &p, int w, int64_t t, const RankCounts &k, const int *s_free,
+                           const int *s_bcell, const int *s_par) {
+    const size_t ws = (size_t)w * p.S;
+    for (int r = threadIdx.x; r < k.n_place; r += NT) {
+        const bool sm = r < RANK_SMEM_CAP;
+        const int c = sm ? s_bcell[r] : p.birth_cell[ws + r];
+        const int child = sm ? s_free[r] : p.birth_child[ws + r];
+        const int par = sm ? s_par[r] : p.birth_parent[ws + r];
+        place_child(p, w, t, c, r, k.n_surv, child, par);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         rank_finalize(p, w, t, k.n_start, k.n_surv, k.n_win, k.n_place);
         p.t[w] = t + 1;
     }
     __syncthreads();
+}
+
+// One block ranks and places world w's births, then t += 1.
+template <int NT>
+__device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, int *s_free, int *s_bcell,
+                                 int *s_par) {
+    const int64_t t = p.t[w];
+    const RankCounts k = rank_counts(p, w, t);
+    rank_publish<NT>(p, w, t, k, scratch, s_free, s_bcell, s_par);
+    rank_place<NT>(p, w, t, k, s_free, s_bcell, s_par);
 }
 
 // ------------------------------------------------------------------- a5 mutation
@@ -589,9 +628,10 @@ __device__ __forceinline__ void mutate_item(const DevParams &p, int it, int &d0,
     const int Hd = p.Hd, G = 4 * Hd, HD4 = Hd * 4;
     const int nA = ((p.I + Hd) >> 1) * HD4;
     if (it < nA) {
-        const int pc = it / HD4, rem = it - pc * HD4, col = 2 * pc;
-        const int row = (rem & 3) * Hd + (rem >> 2);
-        d0 = col * HD4 + rem;  // W_hh^T follows W_ih^T contiguously (off_hh = I * HD4)
+        const int s4 = p.hd_shift + 2;  // HD4 = 1 << s4
+        const int pc = it >> s4, rem = it & (HD4 - 1), col = 2 * pc;
+        const int row = ((rem & 3) << p.hd_shift) + (rem >> 2);
+        d0 = (col << s4) + rem;  // W_hh^T follows W_ih^T contiguously (off_hh = I * HD4)
         dstep = HD4;
         j0 = col < p.I ? row * p.I + col : G * p.I + row * Hd + (col - p.I);
         return;
@@ -611,8 +651,17 @@ __device__ __forceinline__ void mutate_item(const DevParams &p, int it, int &d0,
     j0 = G * p.I + G * Hd + G + e;
 }
 
-// (z[j0], z[j0+1]) for (step t, child cell): bit-identical to box_muller()'s (za, zb)
+// (z[j0], z[j0+1]) for (step t, child cell): bit-identical to box_muller()'s (za, zb).
+// Not inlined: one copy of the Philox + log + sincos code serves every call site (the
+// one-shot phases of k_post are bound by instruction fetch, not by call overhead).
+__device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0);
 __device__ __forceinline__ void gauss_pair(uint64_t seed, int64_t t, int cellc, int j0, double &za, double &zb) {
+    const double2 z = gauss_pair_nl(seed, t, cellc, j0);
+    za = z.x;
+    zb = z.y;
+}
+__device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0) {
+    double za, zb;
     const uint4 d = draw4(seed, PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)(j0 >> 2));
     const bool lo = (j0 & 3) == 0;
     const uint32_t wa = lo ? d.x : d.z, wb = lo ? d.y : d.w;
@@ -625,26 +674,26 @@ __device__ __forceinline__ void gauss_pair(uint64_t seed, int64_t t, int cellc, 
     sincos(th, &sn, &cs);
     za = __dmul_rn(rad, cs);
     zb = __dmul_rn(rad, sn);
+    return make_double2(za, zb);
 }
 
 // U independent items per thread: all loads, then all Philox/log/sincos chains, then all
 // stores (stores last, so no child store can alias an input the compiler must re-order).
-// birth(b, child, parent, cell) gives birth b's slots and cell.
+// Item u is pair `iu[u]` of birth `bu[u]` (skipped unless ok[u]); birth(b, child, parent,
+// cell) gives birth b's slots and cell.
 template <int U, typename Birth>
-__device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t t, uint64_t seed, int Q, size_t k0,
-                                             size_t stride, size_t n, Birth birth) {
+__device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t t, uint64_t seed,
+                                             const uint32_t *bu, const uint32_t *iu, const bool *ok, Birth birth) {
     float pa[U], pb[U];
     int cellc[U], d0[U], dstep[U], j0[U];
     float *dst[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const size_t k = k0 + u * stride;
         dst[u] = nullptr;
-        if (k >= n) continue;
-        const int b = (int)(k / (size_t)Q), it = (int)(k - (size_t)b * Q);
-        mutate_item(p, it, d0[u], dstep[u], j0[u]);
+        if (!ok[u]) continue;
+        mutate_item(p, (int)iu[u], d0[u], dstep[u], j0[u]);
         int child, parent;
-        birth(b, child, parent, cellc[u]);
+        birth((int)bu[u], child, parent, cellc[u]);
         const float *wp = p.weights + ((size_t)w * p.S + parent) * p.Pd + d0[u];
         pa[u] = wp[0];
         pb[u] = dstep[u] ? wp[dstep[u]] : 0.f;
@@ -662,23 +711,54 @@ __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t 
     }
 }
 
-// all worlds, birth lists from global memory, after the rank advanced t
+#ifndef ECO_MUTATE_U
+#define ECO_MUTATE_U 2
+#endif
+// the nb children of world w born at step t, from the global birth lists.  Items k = gtid,
+// gtid + gthreads, ... of nb * Q pairs; (birth, pair) = divmod(k, Q) is advanced
+// incrementally (one division per thread).
+__device__ __forceinline__ void mutate_world(const DevParams &p, int w, int64_t t, int nb, size_t gtid,
+                                             size_t gthreads) {
+    constexpr int U = ECO_MUTATE_U;  // independent items in flight per thread
+    const uint32_t Q = (uint32_t)mutate_items_per_child(p);
+    const size_t n = (size_t)nb * Q;
+    if (gtid >= n) return;
+    const uint64_t seed = p.seeds[w];
+    const size_t ws = (size_t)w * p.S;
+    auto birth = [&](int b, int &child, int &parent, int &cell) {
+        child = p.birth_child[ws + b];
+        parent = p.birth_parent[ws + b];
+        cell = p.birth_cell[ws + b];
+    };
+    const uint32_t sb = (uint32_t)(gthreads / Q), si = (uint32_t)(gthreads % Q);
+    auto adv = [&](uint32_t &b, uint32_t &i) {
+        i += si;
+        b += sb;
+        if (i >= Q) {
+            i -= Q;
+            ++b;
+        }
+    };
+    uint32_t b = (uint32_t)(gtid / Q), it = (uint32_t)(gtid % Q);
+    for (size_t k = gtid; k < n; k += U * gthreads) {
+        uint32_t bu[U], iu[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bu[u] = b;
+            iu[u] = it;
+            ok[u] = k + u * gthreads < n;
+            adv(b, it);
+        }
+        mutate_batch<U>(p, w, t, seed, bu, iu, ok, birth);
+    }
+}
+
+// all worlds, after the rank advanced t
 __device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
-    constexpr int U = 2;
-    const int Q = mutate_items_per_child(p);
     for (int w = 0; w < p.n_worlds; ++w) {
         const int nb = *reinterpret_cast<volatile int32_t *>(p.n_births + w);
-        if (nb == 0) continue;
-        const size_t n = (size_t)nb * Q;
-        const int64_t t = p.t[w] - 1;
-        const uint64_t seed = p.seeds[w];
-        const size_t ws = (size_t)w * p.S;
-        auto birth = [&](int b, int &child, int &parent, int &cell) {
-            child = p.birth_child[ws + b];
-            parent = p.birth_parent[ws + b];
-            cell = p.birth_cell[ws + b];
-        };
-        for (size_t k = gtid; k < n; k += U * gthreads) mutate_batch<U>(p, w, t, seed, Q, k, gthreads, n, birth);
+        if (nb > 0) mutate_world(p, w, p.t[w] - 1, nb, gtid, gthreads);
     }
 }
 

@@ -24,7 +24,6 @@ namespace eco {
 
 constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
                    PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7;
-constexpr int MAX_OFFSETS = 24;
 constexpr int LOGIT_STRIDE = 8;
 constexpr uint8_t NO_DIR = 0xFF;
 
@@ -32,11 +31,12 @@ constexpr uint8_t NO_DIR = 0xFF;
 // captured CUDA graph serves every step; the step index lives in device memory).
 struct DevParams {
     int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, r, log_cap;
+    int hd_shift;  // Hd = 1 << hd_shift
+    double invW;   // 1 / W (cell -> row without an integer division)
     int repr_steps, max_age;
     int e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max;
     int cls_k1, cls_k2, cls_k3;  // class thresholds f_class_min_k[1..3]
-    int n_off;
-    int off_dy[MAX_OFFSETS], off_dx[MAX_OFFSETS];
+    int row_dx[5];  // regrowth disc: offsets (dy, dx) with |dx| <= row_dx[dy + 2], centre excluded
     int off_hh, off_b, off_out, off_bout;  // offsets inside one agent's device weights
     double mutation_std, init_weight_std;
     uint32_t init_res_thr;
@@ -71,8 +71,15 @@ struct DevParams {
 // ------------------------------------------------------------------ Philox4x32-10
 // Salmon et al. SC'11.  Counter (c0 = sub, c1 = entity, c2 = step, c3 = purpose),
 // key (seed lo, seed hi) — the RNG contract of DESIGN.md §3 (C.1).
+// Rounds are a loop, not unrolled: the one-shot phases of k_post are bound by instruction
+// fetch (a cold straight-line path costs ~70 cycles per 128-B line; measured), so compact
+// code beats the ILP of an unrolled chain there.
+#ifndef ECO_PHILOX_UNROLL
+#define ECO_PHILOX_UNROLL 1
+#endif
+constexpr int kPhiloxUnroll = ECO_PHILOX_UNROLL;
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
+#pragma unroll kPhiloxUnroll
     for (int round = 0; round < 10; ++round) {
         const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
         const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
@@ -132,13 +139,21 @@ __device__ __forceinline__ int canon_to_dev(int j, int I, int Hd, int off_hh, in
 // ------------------------------------------------------------------- bit planes
 __device__ __forceinline__ size_t plane_words(const DevParams &p) { return (size_t)p.H * p.WW; }
 
+// row of a cell (cell / W) without an integer division: a double multiply (relative error
+// < 2^-52, so the truncation is at most one below for cells < 2^31) plus one correction
+__device__ __forceinline__ int row_of(const DevParams &p, int cell) {
+    int y = __double2int_rz((double)cell * p.invW);
+    y += (cell - y * p.W >= p.W) ? 1 : 0;
+    return y;
+}
+
 __device__ __forceinline__ uint32_t get_bit(const uint32_t *plane, const DevParams &p, int cell) {
-    const int y = cell / p.W, x = cell - y * p.W;
+    const int y = row_of(p, cell), x = cell - y * p.W;
     return (plane[(size_t)y * p.WW + (x >> 5)] >> (x & 31)) & 1u;
 }
 
 __device__ __forceinline__ uint32_t *word_ptr(uint32_t *plane, const DevParams &p, int cell, uint32_t &bit) {
-    const int y = cell / p.W, x = cell - y * p.W;
+    const int y = row_of(p, cell), x = cell - y * p.W;
     bit = 1u << (x & 31);
     return plane + (size_t)y * p.WW + (x >> 5);
 }
@@ -170,7 +185,7 @@ __device__ __forceinline__ int32_t *count_of(const DevParams &p, int64_t t, int 
 }
 
 __device__ __forceinline__ sim_step_record *record_of(const DevParams &p, int64_t t, int w) {
-    return p.log + (size_t)(t % p.log_cap) * p.n_worlds + w;
+    return p.log + (size_t)(t & (p.log_cap - 1)) * p.n_worlds + w;  // log_cap: a power of two
 }
 
 // N, S, E, W (R13 order for moves is stay, N, S, E, W; births use N, S, E, W = 0..3)

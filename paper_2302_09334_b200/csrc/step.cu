@@ -122,7 +122,7 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
     int tg = -1;
     unsigned long long key = 0ull;
     if (act != 0) {
-        const int y = cellv / p.W, x = cellv - y * p.W;
+        const int y = row_of(p, cellv), x = cellv - y * p.W;
         const int ty = y + kDY[act], tx = x + kDX[act];
         if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
             const int tc = ty * p.W + tx;
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
                     act = true;
                     rec.slot = list_of(p, t, rec.w)[rec.i];
                     rec.cell = p.cell[(size_t)rec.w * p.S + rec.slot];
-                    const int y = rec.cell / p.W;
+                    const int y = row_of(p, rec.cell);
                     obs_mask_lane(p, rec.w, t, y, rec.cell - y * p.W, rec.lo, rec.hi);
                 }
             }
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(256) k_policy_reg(DevParams p) {
         int cellv = 0;
         if (active) cellv = p.cell[gs];
         {
-            const int y = cellv / p.W, x = cellv - (cellv / p.W) * p.W;
+            const int y = row_of(p, cellv), x = cellv - y * p.W;
             uint64_t lo, hi;
             obs_mask(p, w, t, y, x, active ? k : 1 << 20, G, gmask, lo, hi);
             if (active) {
@@ -667,7 +667,7 @@ __global__ void __launch_bounds__(RING_WARPS * 32, 4) k_policy_ring(DevParams p)
         const int cellv = p.cell[gs];
         uint64_t m_lo, m_hi;
         {
-            const int y = cellv / p.W, x = cellv - y * p.W;
+            const int y = row_of(p, cellv), x = cellv - y * p.W;
             obs_mask(p, w, t, y, x, lane, 32, FULL, m_lo, m_hi);
         }
         // compacted list of the active columns (ascending)
@@ -805,7 +805,7 @@ constexpr int STREAM_BPS = 3;
 __device__ __forceinline__ void obs_issue(const DevParams &p, int w, int64_t t, int cellv, int lane, uint32_t &wlo,
                                           uint32_t &whi) {
     const int wd = 2 * p.r + 1;
-    const int y = cellv / p.W, x = cellv - y * p.W;
+    const int y = row_of(p, cellv), x = cellv - y * p.W;
     wlo = whi = 0u;
     if (lane < 2 * wd) {
         const int ch = lane / wd, row = lane - ch * wd;
@@ -822,7 +822,7 @@ __device__ __forceinline__ void obs_issue(const DevParams &p, int w, int64_t t, 
 __device__ __forceinline__ void obs_finish(const DevParams &p, int cellv, int lane, uint32_t wlo, uint32_t whi,
                                            uint64_t &m_lo, uint64_t &m_hi) {
     const int wd = 2 * p.r + 1;
-    const int y = cellv / p.W, x = cellv - y * p.W;
+    const int y = row_of(p, cellv), x = cellv - y * p.W;
     (void)y;
     uint64_t lo = 0ull, hi = 0ull;
     if (lane < 2 * wd) {
@@ -1118,6 +1118,11 @@ __global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
     const int64_t t = p.t[w];
     const bool active = in_range && i < *count_of(p, t, w);
     unsigned long long nnz_a = 0ull, tie_a = 0ull;
+#ifdef ECO_POLICY_TRACE
+    // diagnostic build: per agent (kernel entry, mask ready, end, nnz) of the last launch
+    unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(v & 8191);
+    const uint64_t t_entry = globaltimer_ns();
+#endif
     if (__any_sync(FULL, active)) {  // both halves stay converged for the warp-wide intrinsics
         int slot = 0, cellv = 0;
         size_t gs = 0;
@@ -1162,7 +1167,7 @@ __global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
             uint64_t lo = 0ull, hi = 0ull;
             const int wd = 2 * p.r + 1;
             if (active && hl < 2 * wd) {
-                const int y = cellv / p.W, x = cellv - y * p.W;
+                const int y = row_of(p, cellv), x = cellv - y * p.W;
                 const int ch = hl / wd, row = hl - ch * wd;
                 const int yy = y - p.r + row;
                 if (yy >= 0 && yy < p.H) {
@@ -1196,6 +1201,13 @@ __global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
             nnz += __popc(bal);
         }
         __syncwarp();
+#ifdef ECO_POLICY_TRACE
+        if (active && hl == 0) {
+            trace[0] = t_entry;
+            trace[1] = globaltimer_ns();
+            trace[3] = nnz;
+        }
+#endif
         const int N = Q0 + nnz;
         const int Nw = __reduce_max_sync(FULL, active ? N : 0);  // the warp runs the longer sequence
         auto refill = [&](int kn, int slot_) {
@@ -1274,6 +1286,9 @@ __global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
                 tie_a = one.ties;
             }
             if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
+#ifdef ECO_POLICY_TRACE
+            if (hl == 0) trace[2] = globaltimer_ns();
+#endif
         }
     }
     if (hl == 0) {
@@ -1373,9 +1388,9 @@ __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
 constexpr int RANK_THREADS = 1024;
 __global__ void __launch_bounds__(RANK_THREADS) k_birth_rank(DevParams p) {
     __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
-    __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP];
+    __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
-        birth_rank_world<RANK_THREADS>(p, w, scratch, s_free, s_bcell);
+        birth_rank_world<RANK_THREADS>(p, w, scratch, s_free, s_bcell, s_par);
 }
 
 __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
@@ -1390,7 +1405,10 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 // and a third barrier precedes the mutation.  A phase that ends in a barrier pays for its
 // writes in the barrier's release fence; the regrowth's plane writes (measured: +3..6 us of
 // fence when they preceded a barrier) go last, where only the kernel's end waits for them.
-constexpr int POST_THREADS = 512;
+#ifndef ECO_POST_THREADS
+#define ECO_POST_THREADS 1024
+#endif
+constexpr int POST_THREADS = ECO_POST_THREADS;  // one block per SM (64 registers per thread at 1024)
 #ifdef ECO_BLOCK_CLOCK
 // diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
 // phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
@@ -1421,7 +1439,7 @@ constexpr int ECO_BLOCK_CLOCK_BASE = 16;
 
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned long long *bar) {
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
-    __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP];
+    __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     // warp-interleaved global index: consecutive warps of work land on different blocks
     // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
     const size_t gtid = interleaved_gtid();
@@ -1451,28 +1469,86 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
         atomicAdd(p.phase_ns + 8, globaltimer_ns() - h0);
     POST_SYNC(1);
     lap(1);
-    // births: one block per world ranks, places and counts them (t += 1).  With fewer worlds
-    // than blocks the idle blocks run the regrowth of step T+1 meanwhile (needs only R'' of
-    // step T; its write-back cost is paid in this barrier, hidden behind the rank).
-    const bool regrow_now = p.n_worlds < (int)gridDim.x;
-    if ((int)blockIdx.x < p.n_worlds) {
-        for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
-            birth_rank_world<POST_THREADS>(p, w, scratch, s_free, s_bcell);
+    if (p.n_worlds == 1) {
+        // one world: block 0 ranks the births and resolves their winners, publishes the
+        // birth lists with a release flag, then places the children and writes the counters
+        // (t += 1).  The other blocks regrow the grid of step T+1 meanwhile (it needs only R''
+        // of step T), wait for the flag and mutate the children's weights: no grid barrier
+        // between the rank and the mutation, and the placement overlaps the mutation.
+        unsigned long long *flag = bar + 2;
+        if (blockIdx.x == 0) {
+            const RankCounts k = rank_counts(p, 0, T);
+            rank_publish<POST_THREADS>(p, 0, T, k, scratch, s_free, s_bcell, s_par);
+            if (threadIdx.x == 0) {
+                const unsigned long long v = target + 1;  // unique per launch (monotonic)
+                asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
+            }
+            lap(2);
+            rank_place<POST_THREADS>(p, 0, T, k, s_free, s_bcell, s_par);
+            if (gridDim.x == 1) mutate_world(p, 0, T, k.n_place, threadIdx.x, blockDim.x);  // no other block
+        } else {
+            const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
+            const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
+            const size_t bthr = (size_t)nb * blockDim.x;
+            const uint64_t r0 = b == 0 ? globaltimer_ns() : 0ull;
+#ifdef ECO_BLOCK_CLOCK
+            const long long c0_ = clock64();
+            const uint64_t g0_ = globaltimer_ns();
+#endif
+            regrow_phase(p, T + 1, btid, bthr);
+            if (b == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
+#ifdef ECO_BLOCK_CLOCK
+            if (btid < 2600 && (threadIdx.x & 31) == 0) {  // warps with regrowth items: cycles and ns
+                atomicAdd(p.phase_ns + 10, (unsigned long long)(clock64() - c0_));
+                atomicAdd(p.phase_ns + 11, globaltimer_ns() - g0_);
+                atomicAdd(p.phase_ns + 12, 1ull);
+            }
+#endif
+#ifdef ECO_BLOCK_CLOCK
+            __syncthreads();
+            const uint64_t m0_ = globaltimer_ns();
+#endif
+            if (threadIdx.x == 0) {
+                unsigned long long cur;
+                do {
+                    asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(flag) : "memory");
+                } while (cur < target + 1);
+            }
+            __syncthreads();
+#ifdef ECO_BLOCK_CLOCK
+            const uint64_t m1_ = globaltimer_ns();
+#endif
+            const int n_b = *reinterpret_cast<volatile int32_t *>(p.n_births);
+            if (n_b > 0) mutate_world(p, 0, T, n_b, btid, bthr);
+#ifdef ECO_BLOCK_CLOCK
+            __syncthreads();
+            if (threadIdx.x == 0) {  // per-block marks of the single-world tail in the k = 2 slots
+                unsigned long long *q_ = p.phase_ns + ECO_BLOCK_CLOCK_BASE + (2 * gridDim.x + blockIdx.x) * 3;
+                q_[0] += m0_ - bt_;
+                q_[1] += m1_ - bt_;
+                q_[2] += globaltimer_ns() - bt_;
+            }
+#endif
+        }
     } else {
-        // the idle blocks' threads, renumbered densely (warp-interleaved over those blocks)
-        const unsigned nb = gridDim.x - p.n_worlds, b = blockIdx.x - p.n_worlds;
-        const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
-        const uint64_t r0 = b == 0 ? globaltimer_ns() : 0ull;
-        regrow_phase(p, T + 1, btid, (size_t)nb * blockDim.x);
-        if (b == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
+        // several worlds: one block per world ranks, places and counts them (t += 1); the
+        // blocks without a world regrow step T+1; a barrier; then the mutation
+        if ((int)blockIdx.x < p.n_worlds) {
+            for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
+                birth_rank_world<POST_THREADS>(p, w, scratch, s_free, s_bcell, s_par);
+        } else {
+            const unsigned nb = gridDim.x - p.n_worlds, b = blockIdx.x - p.n_worlds;
+            const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
+            regrow_phase(p, T + 1, btid, (size_t)nb * blockDim.x);
+        }
+        POST_SYNC(2);
+        lap(2);
+        if (p.n_worlds >= (int)gridDim.x) {  // no block was free: the regrowth goes beside the mutation
+            const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
+            if (gtid >= half) regrow_phase(p, T + 1, gtid - half, gthreads - half);
+        }
+        mutate_phase(p, gtid, gthreads);
     }
-    POST_SYNC(2);
-    lap(2);
-    if (!regrow_now) {  // every block ranked a world: the regrowth goes beside the mutation
-        const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
-        if (gtid >= half) regrow_phase(p, T + 1, gtid - half, gthreads - half);
-    }
-    mutate_phase(p, gtid, gthreads);
 #ifdef ECO_BLOCK_CLOCK
     __syncthreads();
     if (threadIdx.x == 0) p.phase_ns[ECO_BLOCK_CLOCK_BASE + (3 * gridDim.x + blockIdx.x) * 3] += globaltimer_ns() - bt_;

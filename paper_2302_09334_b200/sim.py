@@ -29,7 +29,7 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns")
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
-               "claim.warp_sum_b0", "regrow.warp_sum_b1")  # block 0: 16 claim warps; block 1: 16 regrow warps
+               "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
 
 
 class SimError(RuntimeError):

@@ -31,11 +31,12 @@ out = np.zeros(16 + 32768, np.int64)
 sim._check(sim.lib().sim_get_phase_ns(world._h, sim._ptr(out), -1))
 nb = 148
 blk = out[16:16 + 4 * nb * 3].reshape(4, nb, 3) / K / 1e3
-names = ("move", "claim", "rank|noise", "mutate")
+names = ("move", "claim", "1w:regrow|flag|end", "tail")
 for k in range(4):
     wk, wt, fn = blk[k, :, 0], blk[k, :, 1], blk[k, :, 2]
     order = np.argsort(-wk)[:5]
     print(f"{names[k]:14s} work: min {wk.min():6.2f} med {np.median(wk):6.2f} max {wk.max():6.2f} (blocks {order.tolist()})"
           f"  wait: min {wt.min():6.2f} med {np.median(wt):6.2f} max {wt.max():6.2f}"
           f"  fence: min {fn.min():6.2f} med {np.median(fn):6.2f} max {fn.max():6.2f}")
+print("regrow warps: cycles/warp", out[10] / max(out[12], 1) / K * K, "ns/warp", out[11] / max(out[12], 1), "warps/step", out[12] / K)
 print("block0 phases", {k: v / K / 1e3 for k, v in zip(sim.POST_PHASES, out[:len(sim.POST_PHASES)])})

@@ -36,7 +36,7 @@ for rep in range(3):
     q = lambda a, f: float(np.quantile(a, f))
     print(f"step {world.t}: agents {n}, nnz mean {nnz.mean():.1f} max {nnz.max()}")
     print(f"  start  q50 {q(st, .5):6.2f} q90 {q(st, .9):6.2f} q99 {q(st, .99):6.2f} max {st.max():6.2f} us")
-    print(f"  mask   (rel start) q50 {q(mk - st, .5):6.2f} q90 {q(mk - st, .9):6.2f} max {(mk - st).max():6.2f}")
+    print(f"  mask   q50 {q(mk, .5):6.2f} q90 {q(mk, .9):6.2f} max {mk.max():6.2f} (rel start q50 {q(mk - st, .5):6.2f})")
     print(f"  agent  (end - start) q50 {q(en - st, .5):6.2f} q90 {q(en - st, .9):6.2f} max {(en - st).max():6.2f}")
     print(f"  end    q50 {q(en, .5):6.2f} q90 {q(en, .9):6.2f} q99 {q(en, .99):6.2f} max {en.max():6.2f} us")
     late = st > q(st, .9)
