@@ -112,7 +112,7 @@ size_t device_bytes(const Derived &d) {
     const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
     size_t b = 0;
     b += nw * d.pw * 4 * 5;                 // plane0, plane1, occ, bbits[2]
-    b += nw * HW * (8 + 1 + 4);             // claim, bdir, bslot
+    b += nw * HW * (8 + 8 + 4);             // move claim, birth key, birth slot
     b += nw * ((S + 31) / 32) * 4;          // alive bits
     b += nw * S * (1 * 3 + 4 * 4);          // u8 x3, i32 x4
     b += nw * S * (size_t)d.Hd * 4 * 2;     // h, c
@@ -338,7 +338,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.bbits, 2 * nw * d.pw), "alloc");
     CKC(dalloc(h, &T_d, (size_t)d.H * 4), "alloc");
     CKC(dalloc(h, &p.claim, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.bdir, S ? nw * HW : 1), "alloc");
+    CKC(dalloc(h, &p.bkey, S ? nw * HW : 1), "alloc");
     CKC(dalloc(h, &p.bslot, S ? nw * HW : 1), "alloc");
     CKC(dalloc(h, &p.alive_bits, nw * (size_t)d.SW), "alloc");
     CKC(dalloc(h, &p.alive, nw * S), "alloc");
@@ -626,7 +626,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     // scratch and derived structures
     if (S) {
         CK(h, cudaMemsetAsync(p.claim, 0, nw * HW * 8, s), "memset");
-        CK(h, cudaMemsetAsync(p.bdir, 0xff, nw * HW, s), "memset");
+        CK(h, cudaMemsetAsync(p.bkey, 0, nw * HW * 8, s), "memset");
     }
     CK(h, cudaMemsetAsync(p.bbits, 0, 2 * nw * d.pw * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");

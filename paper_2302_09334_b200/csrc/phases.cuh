@@ -302,10 +302,10 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
 // because the move phase has finished reading them).  Then every live parent with repr >=
 // T_repr picks the first cell of a Philox-rotated (N, S, E, W) order that is
 // in-grid, agent-free after moves/deaths (O'') and resource-free after consumption (R'')
-// (R21), records (direction, slot) on its own cell, and marks the candidate cell in the
-// step's claimed-cell bitmap.  Distinct claimed cells are counted (each has exactly one
-// winner, resolved later by max key) per world.  Deferred-claim losers are
-// (candidates - claimed cells), also settled later.  Must be called by all 32 lanes.
+// (R21), records its slot on its own cell, posts its claim key (BIRTH w1 << 32 | ~cell) on
+// the candidate cell by atomicMax (the max is the winner) and marks the cell in the step's
+// claimed-cell bitmap.  Distinct claimed cells are counted per world; deferred-claim losers
+// are (candidates - claimed cells).  Must be called by all 32 lanes.
 __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
@@ -349,12 +349,14 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
                         uint32_t bit;
                         const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, w), p, c, bit), bit);
                         if (!(old & bit)) new_cell = 1;
+                        // the claim key (BIRTH w1, -parent cell): the cell's winner is the max
+                        atomicMax(p.bkey + (size_t)w * HW + c,
+                                  ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv));
+                        p.bslot[(size_t)w * HW + cellv] = slot;
                     }
                     if (dir == NO_DIR) no_cell = 1;
                     else cand = 1;
                 }
-                p.bdir[(size_t)w * HW + cellv] = dir;
-                p.bslot[(size_t)w * HW + cellv] = slot;
             }
         }
         warp_world_add<unsigned long long>(no_cell, w, [&](int ww) {
@@ -368,10 +370,6 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
     }
 }
 
-__device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t, int cellv) {
-    const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
-    return ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
-}
 
 // ------------------------------------------------------------------ a5 birth rank
 // Each claimed cell c has exactly one winner: the live parent q adjacent to c that chose c
@@ -385,40 +383,14 @@ __device__ __forceinline__ unsigned long long birth_key(uint64_t seed, int64_t t
 constexpr int RANK_SMEM_CAP = 1024;  // births ranked in shared memory (more spill to global)
 constexpr int RANK_K = 8;            // claimed-cell bitmap words per thread per chunk
 
-// Parent slot of claimed cell c.  A claimant q is a neighbour holding a live agent in O''
-// that recorded the direction towards c.  Claimed cells are never claimants (they were
-// empty in O''), which also keeps the test exact while children are being placed into
-// claimed cells concurrently (their new O bits and the stale bdir of an empty cell).  The
-// four neighbours' bits and directions are loaded together and their keys computed
-// independently.
+// Parent slot of claimed cell c: the claimant with the max key (BIRTH w1 << 32 | ~cell),
+// posted by atomicMax during the claims (R21), then the slot recorded on its cell.
 __device__ __forceinline__ int birth_parent_of(const DevParams &p, int w, int64_t t, int c) {
+    (void)t;
     const size_t HW = (size_t)p.H * p.W;
-    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-    const uint32_t *BB = bbits_of(p, t, w);
-    const uint8_t *bd = p.bdir + (size_t)w * HW;
-    const uint64_t seed = p.seeds[w];
-    const int cy = row_of(p, c), cx = c - cy * p.W;
-    int qn[4];
-    bool claims[4];
-#pragma unroll
-    for (int dq = 0; dq < 4; ++dq) {
-        const int qy = cy + dir_dy(dq), qx = cx + dir_dx(dq);
-        const bool in = qy >= 0 && qy < p.H && qx >= 0 && qx < p.W;
-        qn[dq] = in ? qy * p.W + qx : c;
-        const bool occ = get_bit(O, p, qn[dq]) != 0u, claimed = get_bit(BB, p, qn[dq]) != 0u;
-        claims[dq] = in && occ && !claimed && bd[qn[dq]] == (uint8_t)(dq ^ 1);
-    }
-    int qbest = -1;
-    unsigned long long kbest = 0ull;
-#pragma unroll
-    for (int dq = 0; dq < 4; ++dq) {
-        const unsigned long long kq = birth_key(seed, t, qn[dq]);
-        if (claims[dq] && (qbest < 0 || kq > kbest)) {
-            kbest = kq;
-            qbest = qn[dq];
-        }
-    }
-    return p.bslot[(size_t)w * HW + qbest];
+    const unsigned long long k = *reinterpret_cast<const volatile unsigned long long *>(p.bkey + (size_t)w * HW + c);
+    const int q = (int)(0xFFFFFFFFu - (uint32_t)k);
+    return *reinterpret_cast<const volatile int32_t *>(p.bslot + (size_t)w * HW + q);
 }
 
 // child state of birth r in slot `child` on cell c; parent's repr reset; birth lists

@@ -12,8 +12,9 @@
 //    group reads its unit's four gate weights (i,f,g,o) with one 16-B load.
 //  * alive slots: a u8 flag per slot plus a bitmap [world][SW]; the live agents of step t
 //    are listed (any order: no result depends on it) in alive_list[t&1].
-//  * reproduction: per-cell birth direction bdir (0..3 = N,S,E,W, 0xFF none), per-cell
-//    parent slot bslot, and a claimed-cell bitmap bbits[t&1] over cells (plane layout).
+//  * reproduction: per claimed cell the max birth-claim key bkey (BIRTH w1 << 32 | ~parent
+//    cell, 0 = none), per parent cell its slot bslot, and a claimed-cell bitmap bbits[t&1]
+//    over cells (plane layout).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -47,7 +48,7 @@ struct DevParams {
     uint32_t *bbits;          // birth bitmaps [2][n_worlds][H][WW] (by step parity)
     const uint32_t *T;        // [H][4] Bernoulli thresholds
     unsigned long long *claim;   // [n_worlds][H*W] move claims (0 = none)
-    uint8_t *bdir;               // [n_worlds][H*W] birth direction of the agent on the cell
+    unsigned long long *bkey;    // [n_worlds][H*W] max birth-claim key on a claimed cell (0 = none)
     int32_t *bslot;              // [n_worlds][H*W] slot of the parent standing on the cell
     uint8_t *alive, *last_action, *ate;
     uint32_t *alive_bits;        // [n_worlds][SW]

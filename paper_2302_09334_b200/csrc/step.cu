@@ -27,6 +27,11 @@
 #ifndef ECO_POLICY_TMA
 #define ECO_POLICY_TMA 0
 #endif
+// k_policy_half: bulk L2 prefetch of each agent's W_hh|b|W_out block and active columns
+// (1), of the block only (2), none (0: measured fastest, 34 vs 43 us with 1)
+#ifndef ECO_POLICY_PREFETCH
+#define ECO_POLICY_PREFETCH 0
+#endif
 
 namespace eco {
 
@@ -156,7 +161,17 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
     const size_t pw = plane_words(p);
     for (size_t k = gtid; k < (size_t)p.n_worlds * pw; k += gthreads) {
         const int w = (int)(k / pw);
-        bbits_of(p, p.t[w] + 1, w)[k - (size_t)w * pw] = 0u;
+        uint32_t *wp = bbits_of(p, p.t[w] + 1, w) + (k - (size_t)w * pw);
+        uint32_t v = *wp;
+        if (v) {  // the claimed cells of step t-1: clear their birth keys too
+            *wp = 0u;
+            const int kk = (int)(k - (size_t)w * pw), y = kk / p.WW, wx = kk - y * p.WW;
+            while (v) {
+                const int b = __ffs(v) - 1;
+                v &= v - 1u;
+                p.bkey[(size_t)w * p.H * p.W + (size_t)y * p.W + wx * 32 + b] = 0ull;
+            }
+        }
     }
     for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
         const int64_t tw = p.t[w];
@@ -1095,10 +1110,14 @@ __global__ void __launch_bounds__(RING_WARPS * 32, STREAM_BPS) k_policy_stream(D
 // Ring: HALF_DEPTH chunks per agent (3 KB) in flight; 16 agents per block interleaved over
 // the blocks (agent v = a * gridDim + block).  Column indices are compacted to bytes.
 constexpr int HALF_AGENTS = 16;  // per block (8 warps)
-constexpr int HALF_DEPTH = 6;
-constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB
+#ifndef ECO_HALF_DEPTH
+#define ECO_HALF_DEPTH 6
+#endif
+constexpr int HALF_DEPTH = ECO_HALF_DEPTH;
+constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6
+constexpr int HALF_BPS = HALF_DEPTH <= 6 ? 4 : HALF_DEPTH <= 8 ? 3 : 2;  // blocks per SM the smem allows
 
-__global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
+__global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ float4 half_smem[];  // [HALF_AGENTS][R][32 units]
@@ -1132,6 +1151,15 @@ __global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
             gs = (size_t)w * p.S + slot;
             Wl = p.weights + gs * (size_t)p.Pd + hl * 4;
         }
+#if ECO_POLICY_PREFETCH
+        // the agent's contiguous W_hh | b | W_out | b_out block (17.7 KB at Hd = 32) streams into
+        // L2 as one bulk prefetch: DRAM serves it sequentially, the ring then hits L2
+        if (active && hl == 0) {
+            const float *blk = p.weights + gs * (size_t)p.Pd + p.off_hh;
+            const uint32_t bytes = (uint32_t)(p.Pd - p.off_hh) * 4u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blk), "r"(bytes) : "memory");
+        }
+#endif
         float4 *rg = half_smem + (ag * R) * 32 + hl;  // slot s, unit hl: rg[s * 32]; unit hl+16: rg[s * 32 + 16]
         const float *Whh = Wl + p.off_hh;
         auto issue = [&](int slot_, const float *src) {
@@ -1201,6 +1229,14 @@ __global__ void __launch_bounds__(256, 4) k_policy_half(DevParams p) {
             nnz += __popc(bal);
         }
         __syncwarp();
+#if ECO_POLICY_PREFETCH == 1
+        if (active)  // every active column (512 B) requested at once
+            for (int q = hl; q < nnz; q += 16)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.weights + gs * (size_t)p.Pd +
+                                                                                  (size_t)cols[q] * HD * 4),
+                             "r"(HD * 16)
+                             : "memory");
+#endif
 #ifdef ECO_POLICY_TRACE
         if (active && hl == 0) {
             trace[0] = t_entry;
