@@ -40,6 +40,8 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
     if (cfg->cols < 4 || cfg->cols % 4 != 0) return fail(SIM_E_INVALID, "invalid field: cols (need >= 4, multiple of 4)");
     if ((int64_t)cfg->rows * cfg->cols >= (int64_t)1 << 31) return fail(SIM_E_INVALID, "invalid field: rows*cols");
     if (cfg->n_worlds < 1) return fail(SIM_E_INVALID, "invalid field: n_worlds");
+    if ((int64_t)cfg->n_worlds * cfg->rows * ((cfg->cols + 31) / 32) >= (int64_t)1 << 31)
+        return fail(SIM_E_INVALID, "invalid field: n_worlds (n_worlds * rows * ceil(cols/32) must be < 2^31)");
     if (!cfg->seeds) return fail(SIM_E_INVALID, "invalid field: seeds (NULL)");
     auto prob = [](double v) { return v >= 0.0 && v <= 1.0; };
     if (!prob(cfg->init_resource_p)) return fail(SIM_E_INVALID, "invalid field: init_resource_p");

@@ -108,6 +108,13 @@ __device__ __forceinline__ uint32_t ge_const(const uint32_t c[5], int m) {
 __device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int y, int wx, int64_t t, int g0, int ng,
                                                   uint32_t &cur) {
     const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
+    // a word whose cells are all full cannot grow: no window, no count, no draw
+    cur = ld_plain(src + (size_t)y * p.WW + wx);
+    {
+        const int nv = p.W - (wx << 5);  // valid cells in the word
+        const uint32_t pad = nv >= 32 ? 0u : ~((1u << nv) - 1u);
+        if ((cur | pad) == 0xFFFFFFFFu) return 0u;
+    }
     uint32_t win[5][3];
 #pragma unroll
     for (int dy = -2; dy <= 2; ++dy) {
@@ -119,7 +126,6 @@ __device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int
                 (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
         }
     }
-    cur = win[2][1];
     uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
 #pragma unroll
     for (int r = 0; r < 5; ++r) {  // disc row dy = r - 2: offsets dx = -m..m (compact loop)
@@ -180,11 +186,12 @@ __device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, 
         const int sub = (int)(it & (L - 1));
         int w = 0, y = 0, wx = 0;
         uint32_t grow = 0u, cur = 0u;
-        if (it < items) {
-            w = (int)(k / per_world);
-            const size_t r = k - (size_t)w * per_world;
-            y = (int)(r / real_words);
-            wx = (int)(r - (size_t)y * real_words);
+        if (it < items) {  // 32-bit index arithmetic (validated: H * words * worlds < 2^32)
+            const uint32_t k32 = (uint32_t)k, pw32 = (uint32_t)per_world;
+            w = (int)(k32 / pw32);
+            const uint32_t r = k32 - (uint32_t)w * pw32;
+            y = (int)(r / (uint32_t)real_words);
+            wx = (int)(r - (uint32_t)y * (uint32_t)real_words);
             grow = regrow_groups(p, w, y, wx, tstep, sub * ng, ng, cur);
         }
         for (int o = 1; o < L; o <<= 1) grow |= __shfl_xor_sync(0xffffffffu, grow, o);

@@ -1389,9 +1389,14 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
         case 32: k_policy_stream<<<lc.policy_blocks, RING_WARPS * 32, RING_SMEM, s>>>(p); break;
 #elif ECO_POLICY_TMA == 0
         case 32: {
+            // one half-warp per slot; at least enough blocks for the housekeeping's clear of
+            // the claimed-cell bitmap (a large grid with few slots)
             const long slots = (long)p.n_worlds * p.S;
-            const unsigned blocks = (unsigned)((slots + HALF_AGENTS - 1) / HALF_AGENTS);
-            k_policy_half<<<blocks > 0 ? blocks : 1, 256, HALF_SMEM, s>>>(p);
+            long blocks = (slots + HALF_AGENTS - 1) / HALF_AGENTS;
+            const long hk = ((long)p.n_worlds * plane_words(p) + 255) / 256;
+            const long hk_cap = (long)lc.sms * 4;
+            if (blocks < (hk < hk_cap ? hk : hk_cap)) blocks = hk < hk_cap ? hk : hk_cap;
+            k_policy_half<<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
             break;
         }
 #else

@@ -63,6 +63,12 @@ def test_host_validation_and_sizes():
         with pytest.raises(sim.SimError) as ei:
             sim.validate(workloads.tiny().replace(**kw))
         assert ei.value.status == sim.SIM_E_INVALID and field in str(ei.value)
+    # device index arithmetic is 32-bit: the bit-plane words of all worlds must stay < 2^31
+    big = workloads.regrowth_micro(8192, 16384)
+    sim.validate(big.replace(seeds=tuple(range(127))))
+    with pytest.raises(sim.SimError) as ei:
+        sim.validate(big.replace(seeds=tuple(range(512))))
+    assert ei.value.status == sim.SIM_E_INVALID and "n_worlds" in str(ei.value)
 
 
 def test_no_cpu_fallback():
