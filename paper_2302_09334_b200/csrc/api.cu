@@ -122,6 +122,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * (size_t)d.Pd * 4;         // weights
     b += nw * S * 16;                       // move records
     b += nw * S * 4 * 7;                    // alive lists [2], free, birth lists, mutation counters
+    b += nw * S * 8;                        // birth candidates
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
 }
@@ -359,6 +360,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
     CKC(dalloc(h, &p.n_win, nw), "alloc");
     CKC(dalloc(h, &p.free_list, nw * S), "alloc");
+    CKC(dalloc(h, &p.cand, nw * S), "alloc");
+    CKC(dalloc(h, &p.n_cand, nw), "alloc");
     CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_parent, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_cell, nw * S), "alloc");

@@ -235,7 +235,8 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
         const int w = it.w;
         const int64_t t = p.t[w];
         const bool active = it.in_range && it.i < *count_of(p, t, w);
-        bool ate = false, died_e = false, died_a = false, survive = false;
+        bool ate = false, died_e = false, died_a = false, survive = false, cand = false;
+        int cand_cell = 0;
         int slot = 0;
         if (active) {
             // the policy kernel's move record of list position i: (slot, cell, target, key hi)
@@ -277,7 +278,16 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 atomicAnd(p.alive_bits + (size_t)w * p.SW + (slot >> 5), ~(1u << (slot & 31)));
             } else {
                 survive = true;
+                cand = p.n_worlds == 1 && p.repr[gs] >= p.repr_steps;
+                cand_cell = cellv;
             }
+        }
+        if (p.n_worlds == 1) {  // eligible parents (R19) for the single-world claims in k_post
+            const unsigned mc = __ballot_sync(0xffffffffu, cand);
+            int c0 = 0;
+            if (lane == 0 && mc) c0 = atomicAdd(p.n_cand, __popc(mc));
+            c0 = __shfl_sync(0xffffffffu, c0, 0);
+            if (cand) p.cand[c0 + __popc(mc & ((1u << lane) - 1u))] = make_int2(slot, cand_cell);
         }
         const int w0 = __shfl_sync(0xffffffffu, w, 0);
         if (__all_sync(0xffffffffu, w == w0)) {
@@ -377,6 +387,67 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
     }
 }
 
+
+// Single world: the claims of the eligible parents the move phase listed, by one block
+// (NT threads): the same decision as birth_claim_phase (first Philox-rotated (N, S, E, W)
+// neighbour that is in-grid, agent-free in O'' and resource-free in R''; slot on the own
+// cell; atomicMax of the claim key on the candidate cell; the claimed-cell bitmap), so the
+// rank can follow after a block barrier instead of a grid barrier.
+template <int NT>
+__device__ void birth_claims_block(const DevParams &p, int64_t t) {
+    const size_t HW = (size_t)p.H * p.W;
+    const int nc = *reinterpret_cast<volatile int32_t *>(p.n_cand);
+    const uint32_t *O = p.occ;
+    const uint32_t *Rn = plane_next(p, t);
+    const uint64_t seed = p.seeds[0];
+    int no_cell = 0, n_cand = 0, new_cells = 0;
+    for (int r = threadIdx.x; r < nc; r += NT) {
+        const int2 sc = p.cand[r];
+        const int slot = sc.x, cellv = sc.y;
+        const int y = row_of(p, cellv), x = cellv - y * p.W;
+        uint32_t freem = 0u;
+#pragma unroll
+        for (int dd = 0; dd < 4; ++dd) {
+            const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
+            const bool in = cy >= 0 && cy < p.H && cx >= 0 && cx < p.W;
+            const int c = in ? cy * p.W + cx : cellv;
+            const uint32_t ob = get_bit(O, p, c), rb = get_bit(Rn, p, c);
+            if (in && !ob && !rb) freem |= 1u << dd;
+        }
+        const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+        const int s0 = (int)(d.x & 3u);
+        const uint32_t rot = ((freem >> s0) | (freem << (4 - s0))) & 0xFu;
+        if (!rot) {
+            ++no_cell;
+            continue;
+        }
+        const int dir = (s0 + __ffs(rot) - 1) & 3;
+        const int c = (y + dir_dy(dir)) * p.W + x + dir_dx(dir);
+        uint32_t bit;
+        const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
+        if (!(old & bit)) ++new_cells;
+        atomicMax(p.bkey + c, ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv));
+        p.bslot[cellv] = slot;
+        ++n_cand;
+    }
+    (void)HW;
+    sim_step_record *rec = record_of(p, t, 0);
+    if (no_cell) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_no_cell), (unsigned long long)no_cell);
+    // deferred_claim accumulates the candidates here; the rank subtracts the claimed cells
+    if (n_cand) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_claim), (unsigned long long)n_cand);
+    if (new_cells) atomicAdd(p.n_win, new_cells);
+    __syncthreads();
+}
+
+// Single world, the blocks without the claims: the lazy reset of this step's move claims
+// (each mover's target; the move phase has finished reading them).
+__device__ __forceinline__ void move_claim_reset(const DevParams &p, int64_t t, size_t gtid, size_t gthreads) {
+    const int n = *count_of(p, t, 0);
+    for (size_t k = gtid; k < (size_t)n; k += gthreads) {
+        const int tg = p.mrec[k].z;
+        if (tg >= 0) p.claim[tg] = 0ull;
+    }
+}
 
 // ------------------------------------------------------------------ a5 birth rank
 // Each claimed cell c has exactly one winner: the live parent q adjacent to c that chose c

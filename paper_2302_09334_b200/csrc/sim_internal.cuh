@@ -59,6 +59,8 @@ struct DevParams {
     int32_t *n_alive;            // [2][n_worlds]
     int32_t *n_win;              // [n_worlds] birth-claim winners this step
     int32_t *free_list;          // [n_worlds][S] scratch (first n_place entries used)
+    int2 *cand;                  // [n_worlds][S] single world: this step's eligible parents (slot, cell)
+    int32_t *n_cand;             // [n_worlds] their count
     int32_t *birth_child, *birth_parent, *birth_cell, *n_births;  // by birth rank
     int64_t *res_count;          // [n_worlds] resources at step start
     sim_step_record *log;        // [log_cap][n_worlds]

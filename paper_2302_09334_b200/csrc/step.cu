@@ -177,6 +177,7 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
         const int64_t tw = p.t[w];
         *count_of(p, tw + 1, (int)w) = 0;
         p.n_win[w] = 0;
+        p.n_cand[w] = 0;
         sim_step_record *nxt = record_of(p, tw + 1, (int)w);
         *nxt = sim_step_record{};
         nxt->t = tw + 1;
@@ -1503,13 +1504,15 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
     move_phase(p, gtid, gthreads);
     POST_SYNC(0);
     lap(0);
-    // birth candidates on every thread
-    const uint64_t h0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
-    birth_claim_phase(p, gtid, gthreads);
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)  // summed warp durations of block 0
-        atomicAdd(p.phase_ns + 8, globaltimer_ns() - h0);
-    POST_SYNC(1);
-    lap(1);
+    if (p.n_worlds > 1) {
+        // birth candidates on every thread
+        const uint64_t h0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
+        birth_claim_phase(p, gtid, gthreads);
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)  // summed warp durations of block 0
+            atomicAdd(p.phase_ns + 8, globaltimer_ns() - h0);
+        POST_SYNC(1);
+        lap(1);
+    }
     if (p.n_worlds == 1) {
         // one world: block 0 ranks the births and resolves their winners, publishes the
         // birth lists with a release flag, then places the children and writes the counters
@@ -1518,6 +1521,9 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
         // between the rank and the mutation, and the placement overlaps the mutation.
         unsigned long long *flag = bar + 2;
         if (blockIdx.x == 0) {
+            if (gridDim.x == 1) move_claim_reset(p, T, threadIdx.x, blockDim.x);  // no other block
+            birth_claims_block<POST_THREADS>(p, T);  // the move phase listed the eligible parents
+            lap(1);
             const RankCounts k = rank_counts(p, 0, T);
             rank_publish<POST_THREADS>(p, 0, T, k, scratch, s_free, s_bcell, s_par);
             if (threadIdx.x == 0) {
@@ -1536,6 +1542,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
             const long long c0_ = clock64();
             const uint64_t g0_ = globaltimer_ns();
 #endif
+            move_claim_reset(p, T, btid, bthr);
             regrow_phase(p, T + 1, btid, bthr);
             if (b == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
 #ifdef ECO_BLOCK_CLOCK

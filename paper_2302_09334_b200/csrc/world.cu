@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
         *count_of(p, t, w) = (int32_t)base;
         *count_of(p, t + 1, w) = 0;
         p.n_win[w] = 0;
+        p.n_cand[w] = 0;
         p.n_births[w] = 0;
         p.res_count[w] = (int64_t)res_acc;
     }
