@@ -305,6 +305,33 @@ def test_determinism_and_resume():
     assert sa["t"] == sc["t"] == 150
 
 
+def test_graph_path_equals_instrumented_path_long_run():
+    """The fused graph step (cooperative k_post: flags, block-0 claims and rank, idle-block
+    regrowth) and the instrumented step (one kernel per phase) must agree exactly over a
+    long paper-scale run: an ordering race between the fused phases shows up as a first
+    differing step (one such race first surfaced at step 1134)."""
+    wc = workloads.paper_scale()
+    K = 2000
+    world = sim.World(wc, log_capacity=K + 16)
+    world.step(5)
+    snap = world.get_state()
+    t0 = world.t
+    world.step(K)
+    log_g = world.step_log(t0, K)[:, 0]
+    sg = world.get_state(("alive", "cell", "energy", "h", "weights"))
+    world.set_state(snap)
+    for _ in range(K):
+        world.step_timed()
+    log_t = world.step_log(t0, K)[:, 0]
+    bad = [k for k in range(K) if log_g[k] != log_t[k]]
+    assert not bad, f"first differing step {t0 + bad[0]}"
+    st = world.get_state(("alive", "cell", "energy", "h", "weights"))
+    for f in sg:
+        if f != "t":
+            assert np.array_equal(sg[f], st[f]), f
+    world.destroy()
+
+
 def test_set_state_rejects_bad_occupancy_and_nonfinite():
     wc = workloads.tiny()
     world = sim.World(wc)
