@@ -28,6 +28,7 @@
  */
 #ifndef ECO_SIM_H
 #define ECO_SIM_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -186,6 +187,30 @@ SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
  * per-agent traces after the first 16. */
 #define SIM_NUM_POST_PHASES 10
 SIM_API sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset);
+/* --- agent-sharded mode: one world over n_ranks GPUs (the agent-home
+ * variant of E.2) ------------------------------------------------------------------------
+ * Every rank creates the same world (same config and seed) on its own GPU and calls
+ * sim_shard(h, n_ranks, rank).  Slot s belongs to rank s % n_ranks (children belong to
+ * their parent's rank); only the owner runs an agent's policy and keeps its weights, h, c,
+ * logits and last action current, while every rank runs the integer dynamics (regrowth,
+ * movement, consumption, physiology, death, births) identically.  One step on every rank:
+ *   sim_step_policy(h);                       policy of the owned agents
+ *   exchange: SUM-allreduce over the ranks of the two device buffers sim_exchange returns
+ *     (the move records by slot, int32, 16 B per slot, zero for other ranks' agents; and
+ *     the policy counters, 2 x int64: active inputs, near ties)  — e.g. ncclAllReduce on
+ *     the handle's stream
+ *   sim_step_post(h);                         the dynamics, identical on every rank
+ * The trajectory equals the unsharded one exactly (the sums are of disjoint non-zero
+ * parts).  sim_step and sim_step_timed return SIM_E_STATE on a sharded handle; set_state
+ * resets ownership to s % n_ranks.  Requires n_worlds = 1 and hidden = 32. */
+SIM_API sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank);
+SIM_API sim_status sim_step_policy(sim_handle h);
+SIM_API sim_status sim_step_post(sim_handle h);
+/* Device pointers (owned by the handle, valid until destroy) and sizes of the buffers to
+ * SUM-allreduce between sim_step_policy and sim_step_post: the move records (int32) and
+ * the policy counters (int64). */
+SIM_API sim_status sim_exchange(sim_handle h, void **mrec, size_t *mrec_bytes, void **record, size_t *record_bytes);
+
 /* Synchronise the handle's stream (reports deferred errors). */
 SIM_API sim_status sim_synchronize(sim_handle h);
 /* Number of kernel launches one step performs (for the bench's launch count). */

@@ -122,7 +122,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * (size_t)d.Pd * 4;         // weights
     b += nw * S * 16;                       // move records
     b += nw * S * 4 * 7;                    // alive lists [2], free, birth lists, mutation counters
-    b += nw * S * 8;                        // birth candidates
+    b += nw * S * 8 + S + S * 16;           // birth candidates, slot owners, by-slot move records
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
 }
@@ -360,6 +360,11 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
     CKC(dalloc(h, &p.n_win, nw), "alloc");
     CKC(dalloc(h, &p.free_list, nw * S), "alloc");
+    p.n_ranks = 1;
+    p.rank = 0;
+    CKC(dalloc(h, &p.owner, S ? S : 1), "alloc");
+    CKC(dalloc(h, &p.pol_ctr, 2), "alloc");
+    CKC(dalloc(h, &p.mrec_slot, S ? S : 1), "alloc");
     CKC(dalloc(h, &p.cand, nw * S), "alloc");
     CKC(dalloc(h, &p.n_cand, nw), "alloc");
     CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
@@ -449,6 +454,8 @@ sim_status sim_step(sim_handle h, int64_t n) {
     if (n < 0) return fail(SIM_E_INVALID, "invalid argument: n < 0");
     if ((st = check_nonfinite(h)) != SIM_OK) return st;
     if (n == 0) return SIM_OK;
+    if (h->p.n_ranks > 1)
+        return fail(SIM_E_STATE, "sharded handle: step with sim_step_policy, the exchange, then sim_step_post");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     if (!h->graph_exec) {
         CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -466,10 +473,63 @@ sim_status sim_step(sim_handle h, int64_t n) {
     return SIM_OK;
 }
 
+// --- agent-sharded mode -------------------------------------------------------------
+sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (n_ranks < 1 || n_ranks > 255 || rank < 0 || rank >= n_ranks)
+        return fail(SIM_E_INVALID, "invalid argument: n_ranks (1..255) / rank");
+    if (n_ranks > 1 && (h->d.n_worlds != 1 || h->d.Hd != 32 || !eco::policy_supports_shard()))
+        return fail(SIM_E_INVALID, "sharding needs one world, hidden = 32 and the default policy kernel");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    h->p.n_ranks = n_ranks;
+    h->p.rank = rank;
+    CK(h, eco::launch_set_owner(h->p, h->stream), "owners");
+    if (h->graph_exec) {  // kernel parameters changed: capture again
+        cudaGraphExecDestroy(h->graph_exec);
+        cudaGraphDestroy(h->graph);
+        h->graph_exec = nullptr;
+        h->graph = nullptr;
+    }
+    return sync(h);
+}
+
+sim_status sim_step_policy(sim_handle h) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if ((st = check_nonfinite(h)) != SIM_OK) return st;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, ensure_regrown(h), "regrow");
+    CK(h, eco::launch_policy(h->p, h->lc, h->stream), "policy");
+    return SIM_OK;
+}
+
+sim_status sim_step_post(sim_handle h) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, eco::launch_post(h->p, h->lc, h->bar, h->stream), "post");
+    h->t += 1;
+    return SIM_OK;
+}
+
+sim_status sim_exchange(sim_handle h, void **mrec, size_t *mrec_bytes, void **record, size_t *record_bytes) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!mrec || !mrec_bytes || !record || !record_bytes) return fail(SIM_E_INVALID, "invalid argument: NULL");
+    *mrec = h->p.mrec_slot;
+    *mrec_bytes = (size_t)h->d.S * 16;
+    *record = h->p.pol_ctr;
+    *record_bytes = 2 * sizeof(unsigned long long);
+    return SIM_OK;
+}
+
 sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    if (h->p.n_ranks > 1) return fail(SIM_E_STATE, "sharded handle: sim_step_timed is not available");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     CK(h, ensure_regrown(h), "regrow");
     CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
@@ -637,6 +697,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
+    CK(h, eco::launch_set_owner(p, s), "owners");
     h->regrown_ahead = false;
     return sync(h);
 }

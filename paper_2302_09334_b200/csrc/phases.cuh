@@ -493,6 +493,7 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
     uint32_t bit;
     atomicOr(word_ptr(p.occ + (size_t)w * plane_words(p), p, c, bit), bit);
     p.repr[(size_t)w * p.S + parent] = 0;
+    if (p.n_ranks > 1) p.owner[child] = p.owner[parent];  // sharded: the child's weights stay there
     list_of(p, t + 1, w)[n_surv + r] = child;
 }
 
@@ -744,6 +745,7 @@ __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t 
         mutate_item(p, (int)iu[u], d0[u], dstep[u], j0[u]);
         int child, parent;
         birth((int)bu[u], child, parent, cellc[u]);
+        if (p.n_ranks > 1 && p.owner[child] != p.rank) continue;  // sharded: the owner's weights
         const float *wp = p.weights + ((size_t)w * p.S + parent) * p.Pd + d0[u];
         pa[u] = wp[0];
         pb[u] = dstep[u] ? wp[dstep[u]] : 0.f;

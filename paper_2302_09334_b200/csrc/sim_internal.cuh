@@ -59,6 +59,13 @@ struct DevParams {
     int32_t *n_alive;            // [2][n_worlds]
     int32_t *n_win;              // [n_worlds] birth-claim winners this step
     int32_t *free_list;          // [n_worlds][S] scratch (first n_place entries used)
+    // Agent-sharded mode (one world over n_ranks GPUs, sim_shard): every rank holds the whole
+    // world and runs the integer dynamics identically; the policy of a slot runs only on its
+    // owner (owner[slot] == rank), whose memory alone holds that agent's weights, h and c.
+    int32_t n_ranks, rank;
+    uint8_t *owner;              // [S] owning rank of each slot (children inherit the parent's)
+    unsigned long long *pol_ctr; // [2] sharded: this rank's policy counters (active inputs, near ties)
+    int4 *mrec_slot;             // [S] sharded: move records by SLOT (the list order differs by rank)
     int2 *cand;                  // [n_worlds][S] single world: this step's eligible parents (slot, cell)
     int32_t *n_cand;             // [n_worlds] their count
     int32_t *birth_child, *birth_parent, *birth_cell, *n_births;  // by birth rank
@@ -216,6 +223,8 @@ cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
 cudaError_t post_occupancy(int *blocks_per_sm);
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s);
+cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot] = slot % n_ranks
+bool policy_supports_shard();  // the Hd = 32 policy kernel of this build honours ownership
 
 // state conversion (canonical <-> device)
 cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);

@@ -40,9 +40,15 @@ __device__ __constant__ int kDX[5] = {0, 0, 0, 1, -1};
 
 __device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
 
+template <bool SHARD = false>
 __device__ __forceinline__ void flush_counters(const DevParams &p, int w, unsigned long long nnz,
                                                unsigned long long ties) {
     if (w < 0) return;
+    if (SHARD) {  // sharded: summed over the ranks by the exchange, added in k_post
+        if (nnz) atomicAdd(p.pol_ctr, nnz);
+        if (ties) atomicAdd(p.pol_ctr + 1, ties);
+        return;
+    }
     sim_step_record *rec = record_of(p, p.t[w], w);
     if (nnz) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->obs_nnz), nnz);
     if (ties) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->near_ties), ties);
@@ -98,6 +104,7 @@ __device__ __forceinline__ void obs_mask(const DevParams &p, int w, int64_t t, i
 // stored logits/action, and the move claim of a4: a valid non-stay move posts
 // (MOVE w0 << 32 | ~cell) with atomicMax on claim[target] (R14).  Called by the agent's
 // group leader only.
+template <bool SHARD = false>
 __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i, int slot, size_t gs, int64_t t,
                                                int cellv, const float lg[5], uint64_t m_lo, uint64_t m_hi,
                                                int forced_on, PolicyCounters &ctr, bool &bad) {
@@ -143,12 +150,14 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
             if (!occupied) {
                 const uint4 d = draw4(p.seeds[w], PURPOSE_MOVE, (uint32_t)t, (uint32_t)cellv, 0u);
                 key = ((unsigned long long)d.x << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
-                atomicMax(p.claim + (size_t)w * p.H * p.W + tc, key);
+                if (!SHARD) atomicMax(p.claim + (size_t)w * p.H * p.W + tc, key);  // sharded: in k_post
                 tg = tc;
             }
         }
     }
-    p.mrec[(size_t)w * p.S + i] = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
+    const int4 mr = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
+    if (SHARD) p.mrec_slot[slot] = mr;  // sharded: exchanged by slot, listed in k_post
+    else p.mrec[(size_t)w * p.S + i] = mr;
 }
 
 // housekeeping for the later phases of this step (any policy kernel runs it): the survivor
@@ -177,6 +186,7 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
         const int64_t tw = p.t[w];
         *count_of(p, tw + 1, (int)w) = 0;
         p.n_win[w] = 0;
+        if (p.n_ranks > 1 && w == 0) p.pol_ctr[0] = p.pol_ctr[1] = 0ull;
         p.n_cand[w] = 0;
         sim_step_record *nxt = record_of(p, tw + 1, (int)w);
         *nxt = sim_step_record{};
@@ -1118,6 +1128,9 @@ constexpr int HALF_DEPTH = ECO_HALF_DEPTH;
 constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6
 constexpr int HALF_BPS = HALF_DEPTH <= 6 ? 4 : HALF_DEPTH <= 8 ? 3 : 2;  // blocks per SM the smem allows
 
+// SHARD = false compiles the sharding branches out, so the unsharded kernels keep their code
+// (a local DevParams copy to fold n_ranks costs 3 us in this kernel: measured).
+template <bool SHARD>
 __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
     constexpr unsigned FULL = 0xffffffffu;
@@ -1136,19 +1149,28 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     const int w = in_range ? (int)(v / p.S) : 0;
     const int i = in_range ? (int)(v - (long)w * p.S) : 0;
     const int64_t t = p.t[w];
-    const bool active = in_range && i < *count_of(p, t, w);
+    bool active = in_range && i < *count_of(p, t, w);
     unsigned long long nnz_a = 0ull, tie_a = 0ull;
 #ifdef ECO_POLICY_TRACE
     // diagnostic build: per agent (kernel entry, mask ready, end, nnz) of the last launch
     unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(v & 8191);
     const uint64_t t_entry = globaltimer_ns();
 #endif
+    int slot = 0;
+    if (SHARD) {
+        slot = active ? list_of(p, t, w)[i] : 0;
+        if (active && p.owner[slot] != p.rank) {
+            // another rank's agent: a zero move record, so the ranks' records sum to the whole
+            if (hl == 0) p.mrec_slot[slot] = make_int4(0, 0, 0, 0);
+            active = false;
+        }
+    }
     if (__any_sync(FULL, active)) {  // both halves stay converged for the warp-wide intrinsics
-        int slot = 0, cellv = 0;
+        int cellv = 0;
         size_t gs = 0;
         const float *Wl = p.weights;  // + hl * 4: unit hl of a chunk; unit hl + 16 at + 64 floats
         if (active) {
-            slot = list_of(p, t, w)[i];
+            if (!SHARD) slot = list_of(p, t, w)[i];
             gs = (size_t)w * p.S + slot;
             Wl = p.weights + gs * (size_t)p.Pd + hl * 4;
         }
@@ -1318,7 +1340,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             bool bad = !isfinite(hn0) || !isfinite(cn0) || !isfinite(hn1) || !isfinite(cn1);
             if (hl == 0) {
                 PolicyCounters one;
-                agent_epilogue(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, one, bad);
+                agent_epilogue<SHARD>(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, one, bad);
                 nnz_a = one.nnz;
                 tie_a = one.ties;
             }
@@ -1334,14 +1356,20 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
         s_ties[ag] = tie_a;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        PolicyCounters bc;
-        for (int k = 0; k < HALF_AGENTS; ++k)
-            if (s_w[k] >= 0) {
-                bc.add(p, s_w[k], s_nnz[k], false);
-                bc.ties += s_ties[k];
+    if (threadIdx.x == 0) {  // runs of equal worlds (one world: a single flush per block)
+        int wc = -1;
+        unsigned long long a = 0ull, b = 0ull;
+        for (int k = 0; k < HALF_AGENTS; ++k) {
+            if (s_w[k] < 0) continue;
+            if (s_w[k] != wc) {
+                flush_counters<SHARD>(p, wc, a, b);
+                wc = s_w[k];
+                a = b = 0ull;
             }
-        bc.flush(p);
+            a += s_nnz[k];
+            b += s_ties[k];
+        }
+        flush_counters<SHARD>(p, wc, a, b);
     }
 }
 
@@ -1361,7 +1389,7 @@ cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
         case 32:
             return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_stream, RING_WARPS * 32, RING_SMEM);
 #else
-        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_half, 256, HALF_SMEM);
+        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_half<false>, 256, HALF_SMEM);
 #endif
         default: return cudaErrorInvalidValue;
     }
@@ -1374,7 +1402,9 @@ cudaError_t policy_prepare() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_policy_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, RING_SMEM);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_policy_half, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_policy_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
 }
 
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
@@ -1397,7 +1427,8 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
             const long hk = ((long)p.n_worlds * plane_words(p) + 255) / 256;
             const long hk_cap = (long)lc.sms * 4;
             if (blocks < (hk < hk_cap ? hk : hk_cap)) blocks = hk < hk_cap ? hk : hk_cap;
-            k_policy_half<<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
+            if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
+            else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
             break;
         }
 #else
@@ -1479,7 +1510,10 @@ constexpr int ECO_BLOCK_CLOCK_BASE = 16;
 #define POST_SYNC(k) grid_sync(bar, target)
 #endif
 
-__global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned long long *bar) {
+template <bool SHARD>
+__global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned long long *bar) {
+    DevParams p = p_;
+    if (!SHARD) p.n_ranks = 1;
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     // warp-interleaved global index: consecutive warps of work land on different blocks
@@ -1501,6 +1535,24 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p, unsigned lon
 #ifdef ECO_BLOCK_CLOCK
     uint64_t bt_ = globaltimer_ns();
 #endif
+    if (p.n_ranks > 1) {
+        // sharded: the ranks' policies left their move records (summed over the ranks) but no
+        // claims; post every agent's claim here, then resolve them after a barrier
+        const int n = *count_of(p, T, 0);
+        if (gtid == 0) {  // the ranks' policy counters, summed by the exchange
+            sim_step_record *rec = record_of(p, T, 0);
+            rec->obs_nnz += (int64_t)p.pol_ctr[0];
+            rec->near_ties += (int64_t)p.pol_ctr[1];
+        }
+        for (size_t k = gtid; k < (size_t)n; k += gthreads) {
+            const int4 mr = p.mrec_slot[list_of(p, T, 0)[k]];  // this rank's list order
+            p.mrec[k] = mr;
+            if (mr.z >= 0)
+                atomicMax(p.claim + mr.z, ((unsigned long long)(uint32_t)mr.w << 32) |
+                                              (unsigned long long)(0xFFFFFFFFu - (uint32_t)mr.y));
+        }
+        grid_sync(bar, target);
+    }
     move_phase(p, gtid, gthreads);
     POST_SYNC(0);
     lap(0);
@@ -1634,6 +1686,19 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+bool policy_supports_shard() { return ECO_POLICY_TMA == 0; }  // k_policy_half
+
+__global__ void k_set_owner(DevParams p) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < p.S; k += gridDim.x * blockDim.x)
+        p.owner[k] = (uint8_t)(k % p.n_ranks);
+}
+
+cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s) {
+    if (p.S == 0 || !p.owner) return cudaSuccess;
+    k_set_owner<<<256, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
     k_mutate<<<lc.sms * 8, 256, 0, s>>>(p);
@@ -1641,7 +1706,7 @@ cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 }
 
 cudaError_t post_occupancy(int *blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post, POST_THREADS, 0);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post<true>, POST_THREADS, 0);
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
@@ -1655,7 +1720,8 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_post, p, bar);
+    if (p.n_ranks > 1) return cudaLaunchKernelEx(&cfg, k_post<true>, p, bar);
+    return cudaLaunchKernelEx(&cfg, k_post<false>, p, bar);
 }
 
 }  // namespace eco

@@ -26,7 +26,8 @@ KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate
 
 EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
-            "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns")
+            "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
+            "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange")
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
@@ -113,8 +114,14 @@ def lib():
             L.sim_synchronize.argtypes = [H]
             L.sim_kernels_per_step.restype = ctypes.c_int32
             L.sim_get_phase_ns.argtypes = [H, ctypes.c_void_p, ctypes.c_int32]
+            if hasattr(L, "sim_shard"):  # (an ECO_LIBSIM_OVERRIDE build may predate the sharded mode)
+                L.sim_shard.argtypes = [H, ctypes.c_int32, ctypes.c_int32]
+                L.sim_step_policy.argtypes = [H]
+                L.sim_step_post.argtypes = [H]
+                L.sim_exchange.argtypes = [H, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t),
+                                           ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
             for f in EXPORTED:
-                if f not in ("sim_last_error", "sim_kernels_per_step"):
+                if f not in ("sim_last_error", "sim_kernels_per_step") and hasattr(L, f):
                     getattr(L, f).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -182,6 +189,7 @@ class World:
 
     def __init__(self, wc, device: int = 0, stream=None, log_capacity: int = 0):
         self.wc = wc
+        self.device = device
         self.n_worlds = len(wc.seeds)
         self._cfg, self._seeds = make_config(wc, device, stream, log_capacity)
         self.log_capacity = log_capacity or 4096
@@ -221,6 +229,41 @@ class World:
     def step(self, n: int = 1):
         _check(lib().sim_step(self._h, int(n)))
         self._t += int(n)
+
+    # -- agent-sharded mode (include/sim.h: sim_shard) --------------------------------
+    def shard(self, n_ranks: int, rank: int):
+        """Own slots s with s % n_ranks == rank; step with step_policy / exchange / step_post."""
+        _check(lib().sim_shard(self._h, int(n_ranks), int(rank)))
+
+    def step_policy(self):
+        _check(lib().sim_step_policy(self._h))
+
+    def step_post(self):
+        _check(lib().sim_step_post(self._h))
+        self._t += 1
+
+    def exchange_buffers(self):
+        """(move-record pointer, bytes, record pointer, bytes): the device buffers to
+        SUM-allreduce over the ranks between step_policy and step_post."""
+        mp, mb, rp, rb = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().sim_exchange(self._h, ctypes.byref(mp), ctypes.byref(mb), ctypes.byref(rp), ctypes.byref(rb)))
+        return mp.value, mb.value, rp.value, rb.value
+
+    def exchange_tensors(self):
+        """The exchange buffers as torch CUDA tensors aliasing the library's memory (int32
+        move records, int64 policy counters), for torch.distributed.all_reduce."""
+        import torch
+        mp, mb, rp, rb = self.exchange_buffers()
+        dev = torch.device("cuda", self.device)
+
+        class _View:  # __cuda_array_interface__ over a device pointer owned by the handle
+            def __init__(self, ptr, n, typestr):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+
+        m = torch.as_tensor(_View(mp, mb // 4, "<i4"), device=dev)
+        r = torch.as_tensor(_View(rp, rb // 8, "<i8"), device=dev)
+        return m, r
 
     def step_timed(self) -> dict:
         tm = SimStepTiming()

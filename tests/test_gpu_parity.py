@@ -332,6 +332,62 @@ def test_graph_path_equals_instrumented_path_long_run():
     world.destroy()
 
 
+def _sharded_step(ranks):
+    """One agent-sharded step of all ranks of a world on this GPU: the ranks' policies, the
+    SUM-combine of their exchange buffers (what an NCCL allreduce does across GPUs; here the
+    host sequences it, no kernel waits on another rank's), then every rank's dynamics."""
+    import torch
+    for r in ranks:
+        r.step_policy()
+    for r in ranks:
+        r.synchronize()
+    bufs = [r.exchange_tensors() for r in ranks]
+    m = sum(b[0] for b in bufs)
+    rec = sum(b[1] for b in bufs)
+    for b in bufs:
+        b[0].copy_(m)
+        b[1].copy_(rec)
+    torch.cuda.synchronize()
+    for r in ranks:
+        r.step_post()
+
+
+@pytest.mark.parametrize("n_ranks", [2, 3])
+def test_agent_sharded_world_equals_unsharded(n_ranks):
+    """SURVEY.md §8(e) (agent-home variant): the world stepped as n_ranks ranks, each
+    running the policy of its own slots and the dynamics of the whole world, reproduces the
+    unsharded trajectory exactly: integer state and records bit-exact on every rank, and
+    every live agent's weights, h and c bit-exact on some rank (its owner)."""
+    wc = workloads.paper_scale().replace(slots=2048, n_initial=600)
+    K = 60
+    ref = sim.World(wc)
+    ranks = [sim.World(wc) for _ in range(n_ranks)]
+    for r, w in enumerate(ranks):
+        w.shard(n_ranks, r)
+    with pytest.raises(sim.SimError):
+        ranks[0].step(1)  # a sharded handle steps only through the exchange protocol
+    ref.step(K)
+    for _ in range(K):
+        _sharded_step(ranks)
+    lr = ref.step_log(0, K)
+    assert int(lr["births"].sum()) > 0  # the run exercised reproduction and mutation
+    sr = ref.get_state()
+    ints = ("resources", "alive", "cell", "energy", "age", "repr", "ate")
+    states = [w.get_state() for w in ranks]
+    for w, st in zip(ranks, states):
+        assert np.array_equal(w.step_log(0, K), lr)
+        for f in ints:
+            assert np.array_equal(st[f], sr[f]), f
+    live = np.flatnonzero(sr["alive"][0])
+    for f in ("weights", "h", "c"):
+        ok = np.zeros(len(live), bool)
+        for st in states:
+            ok |= np.all(st[f][0][live] == sr[f][0][live], axis=tuple(range(1, sr[f][0][live].ndim)))
+        assert ok.all(), f"{f}: {int((~ok).sum())} live agents differ on every rank"
+    for w in ranks + [ref]:
+        w.destroy()
+
+
 def test_set_state_rejects_bad_occupancy_and_nonfinite():
     wc = workloads.tiny()
     world = sim.World(wc)
