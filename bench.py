@@ -57,6 +57,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one world over all ranks (agent-sharded, NCCL allreduce of the move records "
+                         "each step; strong scaling) instead of one replica per rank")
     ap.add_argument("--no-flush", action="store_true",
                     help="diagnostic: do not flush L2 between timed steps (the line says so in config.l2)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
@@ -197,14 +200,21 @@ def run_ours(args, rank, world_size, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    wc = workload(args.config, rank, world_size)
+    sharded = args.shard and world_size > 1
+    wc = workload(args.config, 0 if args.shard else rank, world_size)  # --shard: the same world everywhere
+    if sharded:  # state capture and the instrumented replay are per-rank views: skip them
+        args.no_replay = args.no_e2e = args.no_cpu_baseline = True
     K, W = args.steps, args.warmup
     stream = torch.cuda.Stream(device=dev)
     red = Reducer(dist, dev)
     barrier, allmax, allsum = red.barrier, red.max, red.sum
 
     with torch.cuda.stream(stream):
-        world = sim.World(wc, device=local_rank, stream=stream, log_capacity=max(4096, W + K + 8))
+        if sharded:
+            from paper_2302_09334_b200.shard import ShardedWorld
+            world = ShardedWorld(wc, dist, local_rank, stream=stream, log_capacity=max(4096, W + K + 8))
+        else:
+            world = sim.World(wc, device=local_rank, stream=stream, log_capacity=max(4096, W + K + 8))
         flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
         flush_rd = torch.ones(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
@@ -242,7 +252,7 @@ def run_ours(args, rank, world_size, local_rank):
         nnz = int(log["obs_nnz"].sum())
         births = int(log["births"].sum())
         max_ms = allmax(total_ms)
-        all_agents = allsum(agents)
+        all_agents = agents if sharded else allsum(agents)  # sharded: one world, counted once
         value = all_agents / (max_ms / 1e3)
         cells = K * wc.rows * wc.cols * wc.n_worlds
 
@@ -296,7 +306,8 @@ def run_ours(args, rank, world_size, local_rank):
         peak, peak_src = peaks()
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": K, "warmup": W,
-            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{wc.name} (BASELINE.json configs[1])" if args.config == "paper_scale" else wc.name,
                        "grid": f"{wc.rows}x{wc.cols}", "slots": wc.slots, "n_initial": wc.n_initial,
@@ -304,12 +315,14 @@ def run_ours(args, rank, world_size, local_rank):
                        "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + K],
                        "l2": "NOT flushed (diagnostic run)" if args.no_flush
                        else "flushed between timed steps (256 MiB memset + 256 MiB read on the library stream)",
-                       "parallelism": "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
-                       else "single GPU", "global_batch": wc.slots * world_size},
-            "cell_updates_per_s": cells * world_size / (max_ms / 1e3),
+                       "parallelism": (f"agent-sharded: one world over {world_size} GPUs (policy by slot owner, "
+                                       "dynamics on every rank, NCCL SUM-allreduce of the move records per step)")
+                       if sharded else "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
+                       else "single GPU", "global_batch": wc.slots * (1 if sharded else world_size)},
+            "cell_updates_per_s": cells * (1 if sharded else world_size) / (max_ms / 1e3),
             "agents_mean": agents / K,
             "births_mean": births / K,
-            "gpu_launches": 2 * K,
+            "gpu_launches": 2 * K,  # per rank: the policy kernel and the cooperative k_post
             "post_phase_us_per_step": post_phases,
             "clocks": clk,
         }

@@ -65,6 +65,40 @@ def _worker(rank, world_size, port, path):
         dist.destroy_process_group()
 
 
+def _shard_worker(rank, world_size, port, path):
+    """The agent-sharded exchange (paper_2302_09334_b200.shard.combine_) on gloo: each rank
+    holds the move records of its own slots (zero elsewhere) and its policy counters; after
+    the SUM-allreduce every rank holds every slot's record and the world's counters."""
+    import torch
+    import torch.distributed as dist
+    from paper_2302_09334_b200.shard import combine_
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        S = 97
+        rng = np.random.default_rng(5)
+        full = rng.integers(-2**31, 2**31 - 1, size=(S, 4), dtype=np.int64).astype(np.int32)
+        owner = np.arange(S) % world_size
+        mine = np.where((owner == rank)[:, None], full, 0).astype(np.int32)
+        m = torch.from_numpy(mine.reshape(-1).copy())
+        ctr = torch.tensor([10 * (rank + 1), rank], dtype=torch.int64)
+        combine_([m, ctr], dist)
+        if rank == 0:
+            np.save(path, np.concatenate([m.numpy().astype(np.int64), ctr.numpy(), full.reshape(-1).astype(np.int64)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_agent_sharded_exchange_on_gloo():
+    import torch.multiprocessing as mp
+    path = os.path.join(tempfile.mkdtemp(), "exchange.npy")
+    mp.spawn(_shard_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    got = np.load(path)
+    S4 = 97 * 4
+    assert np.array_equal(got[:S4], got[S4 + 2:])  # every slot's record on every rank (wraps exactly)
+    assert list(got[S4:S4 + 2]) == [30, 1]
+
+
 def test_ensemble_shards_partition_the_worlds():
     for n in range(1, 9):
         parts = [workloads.ensemble_shard(n, r) for r in range(n)]
