@@ -698,6 +698,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     CK(h, eco::launch_set_owner(p, s), "owners");
+    CK(h, cudaMemsetAsync(p.pol_ctr, 0, 2 * sizeof(unsigned long long), s), "memset");
     h->regrown_ahead = false;
     return sync(h);
 }

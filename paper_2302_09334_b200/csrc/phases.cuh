@@ -745,7 +745,9 @@ __device__ __forceinline__ void mutate_batch(const DevParams &p, int w, int64_t 
         mutate_item(p, (int)iu[u], d0[u], dstep[u], j0[u]);
         int child, parent;
         birth((int)bu[u], child, parent, cellc[u]);
-        if (p.n_ranks > 1 && p.owner[child] != p.rank) continue;  // sharded: the owner's weights
+        // sharded: mutated on the child's owner = the parent's (placement sets owner[child]
+        // concurrently with this phase, so read the parent's, which is stable)
+        if (p.n_ranks > 1 && p.owner[parent] != p.rank) continue;
         const float *wp = p.weights + ((size_t)w * p.S + parent) * p.Pd + d0[u];
         pa[u] = wp[0];
         pb[u] = dstep[u] ? wp[dstep[u]] : 0.f;

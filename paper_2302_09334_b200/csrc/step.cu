@@ -186,7 +186,6 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
         const int64_t tw = p.t[w];
         *count_of(p, tw + 1, (int)w) = 0;
         p.n_win[w] = 0;
-        if (p.n_ranks > 1 && w == 0) p.pol_ctr[0] = p.pol_ctr[1] = 0ull;
         p.n_cand[w] = 0;
         sim_step_record *nxt = record_of(p, tw + 1, (int)w);
         *nxt = sim_step_record{};
@@ -1539,10 +1538,11 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         // sharded: the ranks' policies left their move records (summed over the ranks) but no
         // claims; post every agent's claim here, then resolve them after a barrier
         const int n = *count_of(p, T, 0);
-        if (gtid == 0) {  // the ranks' policy counters, summed by the exchange
+        if (gtid == 0) {  // the ranks' policy counters, summed by the exchange; then reset
             sim_step_record *rec = record_of(p, T, 0);
             rec->obs_nnz += (int64_t)p.pol_ctr[0];
             rec->near_ties += (int64_t)p.pol_ctr[1];
+            p.pol_ctr[0] = p.pol_ctr[1] = 0ull;
         }
         for (size_t k = gtid; k < (size_t)n; k += gthreads) {
             const int4 mr = p.mrec_slot[list_of(p, T, 0)[k]];  // this rank's list order

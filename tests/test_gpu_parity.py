@@ -359,7 +359,7 @@ def test_agent_sharded_world_equals_unsharded(n_ranks):
     unsharded trajectory exactly: integer state and records bit-exact on every rank, and
     every live agent's weights, h and c bit-exact on some rank (its owner)."""
     wc = workloads.paper_scale().replace(slots=2048, n_initial=600)
-    K = 60
+    K = 150  # births from step ~21, slot reuse (a child in a slot last owned by another rank) later
     ref = sim.World(wc)
     ranks = [sim.World(wc) for _ in range(n_ranks)]
     for r, w in enumerate(ranks):
