@@ -122,7 +122,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * (size_t)d.Pd * 4;         // weights
     b += nw * S * 16;                       // move records
     b += nw * S * 4 * 7;                    // alive lists [2], free, birth lists, mutation counters
-    b += nw * S * 8 + S + S * 16;           // birth candidates, slot owners, by-slot move records
+    b += nw * S * 8 + S + S * 16 + S * 8;   // birth candidates, owners, by-slot move records, own lists
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     return b;
 }
@@ -365,6 +365,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.owner, S ? S : 1), "alloc");
     CKC(dalloc(h, &p.pol_ctr, 2), "alloc");
     CKC(dalloc(h, &p.mrec_slot, S ? S : 1), "alloc");
+    CKC(dalloc(h, &p.own_list, S ? 2 * S : 1), "alloc");
+    CKC(dalloc(h, &p.own_count, 2), "alloc");
     CKC(dalloc(h, &p.cand, nw * S), "alloc");
     CKC(dalloc(h, &p.n_cand, nw), "alloc");
     CKC(dalloc(h, &p.birth_child, nw * S), "alloc");

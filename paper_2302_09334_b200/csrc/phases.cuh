@@ -304,6 +304,14 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             }
             pos0 = __shfl_sync(0xffffffffu, pos0, 0);
             if (survive) list_of(p, t + 1, w)[pos0 + __popc(m & ((1u << lane) - 1u))] = slot;
+            if (p.n_ranks > 1) {  // sharded: this rank's own survivors, the next policy's work
+                const bool mine = survive && p.owner[slot] == p.rank;
+                const unsigned mo = __ballot_sync(0xffffffffu, mine);
+                int o0 = 0;
+                if (lane == 0 && mo) o0 = atomicAdd(p.own_count + ((t0 + 1) & 1), __popc(mo));
+                o0 = __shfl_sync(0xffffffffu, o0, 0);
+                if (mine) p.own_list[((t0 + 1) & 1) * p.S + o0 + __popc(mo & ((1u << lane) - 1u))] = slot;
+            }
         } else {
             sim_step_record *rec = record_of(p, t, w);
             if (ate) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), 1ull);
@@ -388,6 +396,31 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
 }
 
 
+// The candidate cell of the eligible parent on cellv (single world), or -1: the first of
+// the Philox-rotated (N, S, E, W) neighbours that is in-grid, agent-free in O'' and
+// resource-free in R'' (R21).  `key` gets its claim key (BIRTH w1 << 32 | ~cellv).
+__device__ __forceinline__ int birth_target(const DevParams &p, int64_t t, int cellv, unsigned long long &key) {
+    const uint32_t *O = p.occ;
+    const uint32_t *Rn = plane_next(p, t);
+    const int y = row_of(p, cellv), x = cellv - y * p.W;
+    uint32_t freem = 0u;
+#pragma unroll
+    for (int dd = 0; dd < 4; ++dd) {
+        const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
+        const bool in = cy >= 0 && cy < p.H && cx >= 0 && cx < p.W;
+        const int c = in ? cy * p.W + cx : cellv;
+        const uint32_t ob = get_bit(O, p, c), rb = get_bit(Rn, p, c);
+        if (in && !ob && !rb) freem |= 1u << dd;
+    }
+    const uint4 d = draw4(p.seeds[0], PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
+    key = ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
+    const int s0 = (int)(d.x & 3u);
+    const uint32_t rot = ((freem >> s0) | (freem << (4 - s0))) & 0xFu;
+    if (!rot) return -1;
+    const int dir = (s0 + __ffs(rot) - 1) & 3;
+    return (y + dir_dy(dir)) * p.W + x + dir_dx(dir);
+}
+
 // Single world: the claims of the eligible parents the move phase listed, by one block
 // (NT threads): the same decision as birth_claim_phase (first Philox-rotated (N, S, E, W)
 // neighbour that is in-grid, agent-free in O'' and resource-free in R''; slot on the own
@@ -395,48 +428,63 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
 // rank can follow after a block barrier instead of a grid barrier.
 template <int NT>
 __device__ void birth_claims_block(const DevParams &p, int64_t t) {
-    const size_t HW = (size_t)p.H * p.W;
     const int nc = *reinterpret_cast<volatile int32_t *>(p.n_cand);
-    const uint32_t *O = p.occ;
-    const uint32_t *Rn = plane_next(p, t);
-    const uint64_t seed = p.seeds[0];
     int no_cell = 0, n_cand = 0, new_cells = 0;
     for (int r = threadIdx.x; r < nc; r += NT) {
         const int2 sc = p.cand[r];
-        const int slot = sc.x, cellv = sc.y;
-        const int y = row_of(p, cellv), x = cellv - y * p.W;
-        uint32_t freem = 0u;
-#pragma unroll
-        for (int dd = 0; dd < 4; ++dd) {
-            const int cy = y + dir_dy(dd), cx = x + dir_dx(dd);
-            const bool in = cy >= 0 && cy < p.H && cx >= 0 && cx < p.W;
-            const int c = in ? cy * p.W + cx : cellv;
-            const uint32_t ob = get_bit(O, p, c), rb = get_bit(Rn, p, c);
-            if (in && !ob && !rb) freem |= 1u << dd;
-        }
-        const uint4 d = draw4(seed, PURPOSE_BIRTH, (uint32_t)t, (uint32_t)cellv, 0u);
-        const int s0 = (int)(d.x & 3u);
-        const uint32_t rot = ((freem >> s0) | (freem << (4 - s0))) & 0xFu;
-        if (!rot) {
+        unsigned long long key;
+        const int c = birth_target(p, t, sc.y, key);
+        if (c < 0) {
             ++no_cell;
             continue;
         }
-        const int dir = (s0 + __ffs(rot) - 1) & 3;
-        const int c = (y + dir_dy(dir)) * p.W + x + dir_dx(dir);
         uint32_t bit;
         const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
         if (!(old & bit)) ++new_cells;
-        atomicMax(p.bkey + c, ((unsigned long long)d.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv));
-        p.bslot[cellv] = slot;
+        atomicMax(p.bkey + c, key);
+        p.bslot[sc.y] = sc.x;
         ++n_cand;
     }
-    (void)HW;
     sim_step_record *rec = record_of(p, t, 0);
     if (no_cell) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_no_cell), (unsigned long long)no_cell);
     // deferred_claim accumulates the candidates here; the rank subtracts the claimed cells
     if (n_cand) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_claim), (unsigned long long)n_cand);
     if (new_cells) atomicAdd(p.n_win, new_cells);
     __syncthreads();
+}
+
+// Single world with many eligible parents (a large world at its cap): the same claims as
+// birth_claims_block, spread over every thread of the grid (a grid barrier follows).
+__device__ __forceinline__ void birth_claims_grid(const DevParams &p, int64_t t, size_t gtid, size_t gthreads) {
+    const int nc = *reinterpret_cast<volatile int32_t *>(p.n_cand);
+    const unsigned lane = gtid & 31;
+    for (size_t base = gtid - lane; base < (size_t)nc; base += gthreads) {
+        const size_t r = base + lane;
+        int no_cell = 0, cand = 0, new_cell = 0;
+        if (r < (size_t)nc) {
+            const int2 sc = p.cand[r];
+            unsigned long long key;
+            const int c = birth_target(p, t, sc.y, key);
+            if (c < 0) {
+                no_cell = 1;
+            } else {
+                uint32_t bit;
+                const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
+                if (!(old & bit)) new_cell = 1;
+                atomicMax(p.bkey + c, key);
+                p.bslot[sc.y] = sc.x;
+                cand = 1;
+            }
+        }
+        const int a = __reduce_add_sync(0xffffffffu, no_cell), b = __reduce_add_sync(0xffffffffu, cand),
+                  c = __reduce_add_sync(0xffffffffu, new_cell);
+        if (lane == 0) {
+            sim_step_record *rec = record_of(p, t, 0);
+            if (a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_no_cell), (unsigned long long)a);
+            if (b) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_claim), (unsigned long long)b);
+            if (c) atomicAdd(p.n_win, c);
+        }
+    }
 }
 
 // Single world, the blocks without the claims: the lazy reset of this step's move claims
@@ -493,7 +541,10 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
     uint32_t bit;
     atomicOr(word_ptr(p.occ + (size_t)w * plane_words(p), p, c, bit), bit);
     p.repr[(size_t)w * p.S + parent] = 0;
-    if (p.n_ranks > 1) p.owner[child] = p.owner[parent];  // sharded: the child's weights stay there
+    if (p.n_ranks > 1) {  // sharded: the child's weights stay on the parent's rank
+        p.owner[child] = p.owner[parent];
+        if (p.owner[parent] == p.rank) p.own_list[((t + 1) & 1) * p.S + atomicAdd(p.own_count + ((t + 1) & 1), 1)] = child;
+    }
     list_of(p, t + 1, w)[n_surv + r] = child;
 }
 

@@ -66,6 +66,8 @@ struct DevParams {
     uint8_t *owner;              // [S] owning rank of each slot (children inherit the parent's)
     unsigned long long *pol_ctr; // [2] sharded: this rank's policy counters (active inputs, near ties)
     int4 *mrec_slot;             // [S] sharded: move records by SLOT (the list order differs by rank)
+    int32_t *own_list;           // [2][S] sharded: this rank's live slots of step t (by parity)
+    int32_t *own_count;          // [2]
     int2 *cand;                  // [n_worlds][S] single world: this step's eligible parents (slot, cell)
     int32_t *n_cand;             // [n_worlds] their count
     int32_t *birth_child, *birth_parent, *birth_cell, *n_births;  // by birth rank
@@ -223,7 +225,8 @@ cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
 cudaError_t post_occupancy(int *blocks_per_sm);
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s);
-cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot] = slot % n_ranks
+cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot] = slot % n_ranks,
+                                                                  // own list of step t, zero records
 bool policy_supports_shard();  // the Hd = 32 policy kernel of this build honours ownership
 
 // state conversion (canonical <-> device)

@@ -187,6 +187,7 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
         *count_of(p, tw + 1, (int)w) = 0;
         p.n_win[w] = 0;
         p.n_cand[w] = 0;
+        if (p.n_ranks > 1 && w == 0) p.own_count[(tw + 1) & 1] = 0;
         sim_step_record *nxt = record_of(p, tw + 1, (int)w);
         *nxt = sim_step_record{};
         nxt->t = tw + 1;
@@ -1148,7 +1149,8 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     const int w = in_range ? (int)(v / p.S) : 0;
     const int i = in_range ? (int)(v - (long)w * p.S) : 0;
     const int64_t t = p.t[w];
-    bool active = in_range && i < *count_of(p, t, w);
+    // sharded: the contexts walk this rank's own live slots instead of the whole list
+    bool active = in_range && i < (SHARD ? p.own_count[t & 1] : *count_of(p, t, w));
     unsigned long long nnz_a = 0ull, tie_a = 0ull;
 #ifdef ECO_POLICY_TRACE
     // diagnostic build: per agent (kernel entry, mask ready, end, nnz) of the last launch
@@ -1156,14 +1158,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     const uint64_t t_entry = globaltimer_ns();
 #endif
     int slot = 0;
-    if (SHARD) {
-        slot = active ? list_of(p, t, w)[i] : 0;
-        if (active && p.owner[slot] != p.rank) {
-            // another rank's agent: a zero move record, so the ranks' records sum to the whole
-            if (hl == 0) p.mrec_slot[slot] = make_int4(0, 0, 0, 0);
-            active = false;
-        }
-    }
+    if (SHARD) slot = active ? p.own_list[(t & 1) * p.S + i] : 0;
     if (__any_sync(FULL, active)) {  // both halves stay converged for the warp-wide intrinsics
         int cellv = 0;
         size_t gs = 0;
@@ -1480,7 +1475,8 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 #ifndef ECO_POST_THREADS
 #define ECO_POST_THREADS 1024
 #endif
-constexpr int POST_THREADS = ECO_POST_THREADS;  // one block per SM (64 registers per thread at 1024)
+constexpr int POST_THREADS = ECO_POST_THREADS;
+constexpr int CLAIMS_BLOCK_MAX = 4 * POST_THREADS;  // eligible parents block 0 claims by itself  // one block per SM (64 registers per thread at 1024)
 #ifdef ECO_BLOCK_CLOCK
 // diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
 // phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
@@ -1545,8 +1541,10 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             p.pol_ctr[0] = p.pol_ctr[1] = 0ull;
         }
         for (size_t k = gtid; k < (size_t)n; k += gthreads) {
-            const int4 mr = p.mrec_slot[list_of(p, T, 0)[k]];  // this rank's list order
+            const int sl = list_of(p, T, 0)[k];
+            const int4 mr = p.mrec_slot[sl];  // summed over the ranks; listed in this rank's order
             p.mrec[k] = mr;
+            p.mrec_slot[sl] = make_int4(0, 0, 0, 0);  // zero again for the next exchange
             if (mr.z >= 0)
                 atomicMax(p.claim + mr.z, ((unsigned long long)(uint32_t)mr.w << 32) |
                                               (unsigned long long)(0xFFFFFFFFu - (uint32_t)mr.y));
@@ -1572,9 +1570,16 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         // of step T), wait for the flag and mutate the children's weights: no grid barrier
         // between the rank and the mutation, and the placement overlaps the mutation.
         unsigned long long *flag = bar + 2;
+        // many eligible parents (a large world at its cap): claims on every thread and a grid
+        // barrier; otherwise block 0 makes them itself, saving the barrier
+        const bool claims_grid = *reinterpret_cast<volatile int32_t *>(p.n_cand) > CLAIMS_BLOCK_MAX;
+        if (claims_grid) {
+            birth_claims_grid(p, T, gtid, gthreads);
+            grid_sync(bar, target);
+        }
         if (blockIdx.x == 0) {
             if (gridDim.x == 1) move_claim_reset(p, T, threadIdx.x, blockDim.x);  // no other block
-            birth_claims_block<POST_THREADS>(p, T);  // the move phase listed the eligible parents
+            if (!claims_grid) birth_claims_block<POST_THREADS>(p, T);  // the listed eligible parents
             lap(1);
             const RankCounts k = rank_counts(p, 0, T);
             rank_publish<POST_THREADS>(p, 0, T, k, scratch, s_free, s_bcell, s_par);
@@ -1689,13 +1694,31 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
 bool policy_supports_shard() { return ECO_POLICY_TMA == 0; }  // k_policy_half
 
 __global__ void k_set_owner(DevParams p) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < p.S; k += gridDim.x * blockDim.x)
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < p.S; k += gridDim.x * blockDim.x) {
         p.owner[k] = (uint8_t)(k % p.n_ranks);
+        p.mrec_slot[k] = make_int4(0, 0, 0, 0);
+    }
+}
+
+// this rank's own live slots of step t (one block: order is irrelevant to every result)
+__global__ void k_build_own(DevParams p) {
+    const int64_t t = p.t[0];
+    const int n = *count_of(p, t, 0);
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int slot = list_of(p, t, 0)[k];
+        if (p.owner[slot] == p.rank) p.own_list[(t & 1) * p.S + atomicAdd(&cnt, 1)] = slot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.own_count[t & 1] = cnt;
 }
 
 cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s) {
     if (p.S == 0 || !p.owner) return cudaSuccess;
     k_set_owner<<<256, 256, 0, s>>>(p);
+    if (p.n_ranks > 1 && p.n_worlds == 1) k_build_own<<<1, 1024, 0, s>>>(p);
     return cudaGetLastError();
 }
 
