@@ -128,6 +128,20 @@ def test_paper_scale_lockstep_200_steps():
     assert n > 200000
 
 
+def test_large_grid_lockstep():
+    """C3 (configs[3]) parity scope on its 1600x3200 grid: M2 + M3 lock-step for 20 steps
+    with 8,000 agents in 16,384 slots (the full 262,144-slot world would need 17.8 GB of
+    fp32 weights on the oracle's host): large-grid indexing, the claims spread over the
+    grid, births, and the oracle's exact integer state and records every step."""
+    wc = workloads.large_world().replace(slots=16384, n_initial=8000, repr_steps=8, e_repr_gt=10400)
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    flips, n, nulp = lockstep(world, orc, 20, check_weights_every=10)
+    log = world.step_log(0, 20)
+    assert n > 100000 and int(log["births"].sum()) > 0
+    world.destroy()
+
+
 @pytest.mark.parametrize("hidden,r", [(4, 1), (16, 2), (32, 0), (8, 3)])
 def test_other_shapes_lockstep(hidden, r):
     wc = workloads.tiny().replace(rows=30, cols=72, slots=200, n_initial=90, hidden=hidden, obs_radius=r,
