@@ -173,6 +173,17 @@ SIM_API sim_status sim_set_forced_actions(sim_handle h, const uint8_t *act);
 /* Records of steps [first, first+n) for all worlds, out[n][n_worlds]; the steps must be
  * among the last log_capacity steps taken. */
 SIM_API sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_record *out);
+/* The same copy enqueued on the handle's stream without waiting: `out` (pinned host memory,
+ * for a truly asynchronous copy) is valid after the next sim_synchronize or synchronising
+ * call.  Lets a driver read every step's result without a host round trip per step. */
+SIM_API sim_status sim_get_step_log_async(sim_handle h, int64_t first, int64_t n, sim_step_record *out);
+/* Mirror every step's completed record into a caller-owned ring in page-locked, mapped host
+ * memory (`capacity` records per world, a power of two; step t goes to entry
+ * [t % capacity][world]), written by the device as the step completes: a driver reads each
+ * step's result with no copy operation on the stream.  Entries are valid once a later
+ * synchronising call returns.  host = NULL stops mirroring.  The buffer must outlive the
+ * mirroring.  Non-mapped memory -> SIM_E_INVALID. */
+SIM_API sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t capacity);
 SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);

@@ -721,7 +721,8 @@ sim_status sim_set_forced_actions(sim_handle h, const uint8_t *act) {
     return SIM_OK;
 }
 
-sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_record *out) {
+namespace {
+sim_status step_log_copy(sim_handle h, int64_t first, int64_t n, sim_step_record *out, bool wait) {
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (n < 0 || (n > 0 && !out)) return fail(SIM_E_INVALID, "invalid argument: n/out");
@@ -729,14 +730,51 @@ sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_rec
         return fail(SIM_E_INVALID, "invalid argument: steps [%lld, %lld) not in the log (t = %lld, capacity %d)",
                     (long long)first, (long long)(first + n), (long long)h->t, h->d.log_cap);
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
-    if ((st = sync(h)) != SIM_OK) return st;
+    if (wait && (st = sync(h)) != SIM_OK) return st;
     const size_t nw = h->d.n_worlds;
     for (int64_t i = 0; i < n; ++i) {
         const int64_t step = first + i;
         CK(h, cudaMemcpyAsync(out + i * nw, h->p.log + (size_t)(step % h->d.log_cap) * nw, nw * sizeof(sim_step_record),
                               cudaMemcpyDeviceToHost, h->stream), "log");
     }
-    return sync(h);
+    return wait ? sync(h) : SIM_OK;
+}
+}  // namespace
+
+sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_record *out) {
+    return step_log_copy(h, first, n, out, true);
+}
+
+sim_status sim_get_step_log_async(sim_handle h, int64_t first, int64_t n, sim_step_record *out) {
+    return step_log_copy(h, first, n, out, false);
+}
+
+sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t capacity) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    if (!host) {
+        h->p.rec_mirror = nullptr;
+        h->p.mirror_cap = 0;
+    } else {
+        if (capacity < 1 || (capacity & (capacity - 1)) != 0 || capacity > (1 << 30))
+            return fail(SIM_E_INVALID, "invalid argument: capacity (a power of two)");
+        void *dev = nullptr;
+        if (cudaHostGetDevicePointer(&dev, host, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SIM_E_INVALID, "invalid argument: host (not page-locked, mapped memory)");
+        }
+        h->p.rec_mirror = static_cast<sim_step_record *>(dev);
+        h->p.mirror_cap = (int32_t)capacity;
+    }
+    if (h->graph_exec) {  // kernel parameters changed: capture again
+        cudaGraphExecDestroy(h->graph_exec);
+        cudaGraphDestroy(h->graph);
+        h->graph_exec = nullptr;
+        h->graph = nullptr;
+    }
+    return SIM_OK;
 }
 
 sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset) {

@@ -639,6 +639,14 @@ __device__ __forceinline__ void rank_finalize(const DevParams &p, int w, int64_t
     atomicAdd(tot + 4, (unsigned long long)(de + da));
     atomicAdd(tot + 5, (unsigned long long)eaten);
     atomicAdd(tot + 6, (unsigned long long)grown);
+    if (p.rec_mirror) {  // the complete record, straight into the caller's mapped host buffer
+        const volatile int64_t *src = reinterpret_cast<const volatile int64_t *>(rec);
+        volatile int64_t *dst = reinterpret_cast<volatile int64_t *>(
+            p.rec_mirror + (size_t)(t & (p.mirror_cap - 1)) * p.n_worlds + w);
+        constexpr int NF = (int)(sizeof(sim_step_record) / sizeof(int64_t));
+#pragma unroll
+        for (int f = 0; f < NF; ++f) dst[f] = src[f];
+    }
 }
 
 struct RankCounts {

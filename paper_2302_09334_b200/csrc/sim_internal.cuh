@@ -73,6 +73,8 @@ struct DevParams {
     int32_t *birth_child, *birth_parent, *birth_cell, *n_births;  // by birth rank
     int64_t *res_count;          // [n_worlds] resources at step start
     sim_step_record *log;        // [log_cap][n_worlds]
+    sim_step_record *rec_mirror; // optional mapped host ring [mirror_cap][n_worlds] (sim_set_record_mirror)
+    int32_t mirror_cap;          // a power of two
     unsigned long long *totals;  // [7] sim_totals order
     unsigned long long *phase_ns;  // [SIM_NUM_POST_PHASES] k_post phase clock (block 0)
     const uint8_t *forced;       // [n_worlds][S]

@@ -27,7 +27,8 @@ KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate
 EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
-            "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange")
+            "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
+            "sim_set_record_mirror")
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
@@ -109,6 +110,10 @@ def lib():
             L.sim_state_sizes.argtypes = [ctypes.POINTER(SimConfig), ctypes.POINTER(SimStateSizes)]
             L.sim_set_forced_actions.argtypes = [H, ctypes.c_void_p]
             L.sim_get_step_log.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+            if hasattr(L, "sim_get_step_log_async"):
+                L.sim_get_step_log_async.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+            if hasattr(L, "sim_set_record_mirror"):
+                L.sim_set_record_mirror.argtypes = [H, ctypes.c_void_p, ctypes.c_int64]
             L.sim_get_totals.argtypes = [H, ctypes.POINTER(SimTotals)]
             L.sim_step_timed.argtypes = [H, ctypes.POINTER(SimStepTiming)]
             L.sim_synchronize.argtypes = [H]
@@ -327,6 +332,24 @@ class World:
         out = np.zeros((n, self.n_worlds), RECORD_DTYPE)
         _check(lib().sim_get_step_log(self._h, int(first), int(n), _ptr(out)))
         return out
+
+    def step_log_async(self, first: int, n: int, out: np.ndarray):
+        """Enqueue the copy of the records of steps [first, first+n) into `out` (a structured
+        array of RECORD_DTYPE, shape [n, n_worlds], ideally in pinned memory) without waiting;
+        `out` is valid after the next synchronize()."""
+        assert out.dtype == RECORD_DTYPE and out.shape == (n, self.n_worlds) and out.flags.c_contiguous
+        _check(lib().sim_get_step_log_async(self._h, int(first), int(n), _ptr(out)))
+
+    def set_record_mirror(self, buf, capacity: int = 0):
+        """Mirror each step's record into `buf` (RECORD_DTYPE [capacity][n_worlds], page-locked
+        mapped host memory, e.g. a numpy view of a torch pin_memory tensor); None stops."""
+        if buf is None:
+            _check(lib().sim_set_record_mirror(self._h, None, 0))
+            self._mirror = None
+            return
+        assert buf.dtype == RECORD_DTYPE and buf.shape == (capacity, self.n_worlds) and buf.flags.c_contiguous
+        _check(lib().sim_set_record_mirror(self._h, _ptr(buf), int(capacity)))
+        self._mirror = buf  # the device writes into it: keep it alive
 
     def phase_ns(self, reset: bool = False) -> dict:
         """Summed k_post phase durations (ns, block-0 view) since the last reset."""
