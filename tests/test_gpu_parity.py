@@ -402,6 +402,34 @@ def test_agent_sharded_world_equals_unsharded(n_ranks):
         w.destroy()
 
 
+def test_record_mirror_and_async_log_equal_the_log():
+    """sim_set_record_mirror (device-written mapped host ring) and sim_get_step_log_async
+    deliver exactly the records sim_get_step_log returns."""
+    import torch
+    wc = workloads.tiny().replace(rows=40, cols=80, slots=128, n_initial=60, seeds=(4,))
+    world = sim.World(wc)
+    K, cap = 40, 16
+    buf = torch.empty((cap, sim.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True).numpy()
+    ring = buf.view(sim.RECORD_DTYPE).reshape(cap, 1)
+    with pytest.raises(sim.SimError):
+        world.set_record_mirror(ring[:12], 12)  # not a power of two
+    world.set_record_mirror(ring, cap)
+    abuf = torch.empty((K, sim.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True).numpy()
+    alog = abuf.view(sim.RECORD_DTYPE).reshape(K, 1)
+    for k in range(K):
+        world.step(1)
+        world.step_log_async(k, 1, alog[k:k + 1])
+    world.synchronize()
+    log = world.step_log(0, K)
+    assert np.array_equal(alog, log)
+    assert np.array_equal(ring[np.arange(K - cap, K) % cap], log[K - cap:])
+    world.set_record_mirror(None)
+    world.step(1)
+    world.synchronize()
+    assert np.array_equal(ring[np.arange(K - cap, K) % cap], log[K - cap:])  # no longer written
+    world.destroy()
+
+
 def test_set_state_rejects_bad_occupancy_and_nonfinite():
     wc = workloads.tiny()
     world = sim.World(wc)
