@@ -144,6 +144,7 @@ struct sim_ctx {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     bool regrown_ahead = false;
+    bool p_ready = false;  // split policy: the P rows of step t exist
     unsigned long long *bar = nullptr;   // grid-barrier words of k_post
     int64_t t = 0;
     int32_t *nonfinite_host = nullptr;
@@ -202,7 +203,11 @@ constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5};
 cudaError_t launch_phase(sim_ctx *h, int k) {
     switch (k) {
         case 0: return eco::launch_regrow(h->p, 1, h->stream);
-        case 1: return eco::launch_policy(h->p, h->lc, h->stream);
+        case 1: {  // the instrumented policy streams W_hh itself (no P rows)
+            eco::DevParams q = h->p;
+            q.split = 0;
+            return eco::launch_policy(q, h->lc, h->stream);
+        }
         case 2: return eco::launch_move(h->p, h->lc, h->stream);
         case 3: return eco::launch_birth_claim(h->p, h->lc, h->stream);
         case 4: return eco::launch_birth_rank(h->p, h->stream);
@@ -217,12 +222,20 @@ cudaError_t enqueue_step(sim_ctx *h) {
     return eco::launch_post(h->p, h->lc, h->bar, h->stream);
 }
 
-// the regrowth of the current step, needed once after create/set_state
+// the regrowth of the current step, needed once after create/set_state; with the split
+// policy also the P rows of the current step (k_post makes them for every later step)
 cudaError_t ensure_regrown(sim_ctx *h) {
-    if (h->regrown_ahead) return cudaSuccess;
-    cudaError_t e = eco::launch_regrow(h->p, 0, h->stream);
-    if (e == cudaSuccess) h->regrown_ahead = true;
-    return e;
+    if (!h->regrown_ahead) {
+        cudaError_t e = eco::launch_regrow(h->p, 0, h->stream);
+        if (e != cudaSuccess) return e;
+        h->regrown_ahead = true;
+    }
+    if (h->p.split && !h->p_ready) {
+        cudaError_t e = eco::launch_prepare_p(h->p, h->lc, h->stream);
+        if (e != cudaSuccess) return e;
+        h->p_ready = true;
+    }
+    return cudaSuccess;
 }
 
 sim_status sync(sim_ctx *h) {
@@ -373,6 +386,10 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.birth_parent, nw * S), "alloc");
     CKC(dalloc(h, &p.birth_cell, nw * S), "alloc");
     CKC(dalloc(h, &p.n_births, nw), "alloc");
+    // split policy (one world, Hd = 32, the default policy kernel): P rows made by k_post
+    p.split = (nw == 1 && d.Hd == 32 && S > 0 && eco::policy_supports_shard()) ? 1 : 0;
+    CKC(dalloc(h, &p.Pbuf, p.split ? S * (size_t)d.Hd * 4 : 1), "alloc");
+    CKC(dalloc(h, &p.p_children, 1), "alloc");
     CKC(dalloc(h, &p.res_count, nw), "alloc");
     CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");
     CKC(dalloc(h, &p.totals, 8), "alloc");
@@ -394,6 +411,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     // launch configuration: persistent-style grids sized to the 148 SMs
     int bps = 0;
     CKC(eco::policy_prepare(), "kernel attributes");  // before the occupancy query (dynamic smem opt-in)
+    CKC(eco::post_prepare(), "kernel attributes");
     CKC(eco::policy_occupancy(d.Hd, 256, &bps), "occupancy");
     if (bps < 1) bps = 1;
     h->lc.policy_threads = 256;
@@ -414,7 +432,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
         h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    CKC(dalloc(h, &h->bar, 4), "alloc");  // [0] arrivals, [1] next launch's base, [2] births flag
+    CKC(dalloc(h, &h->bar, 6), "alloc");  // [0] arrivals, [1] next base, [2] births flag, [3..4] P counters
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");
@@ -487,6 +505,7 @@ sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
     if ((st = sync(h)) != SIM_OK) return st;
     h->p.n_ranks = n_ranks;
     h->p.rank = rank;
+    if (n_ranks > 1) h->p.split = 0;  // the sharded step streams W_hh in the policy
     CK(h, eco::launch_set_owner(h->p, h->stream), "owners");
     if (h->graph_exec) {  // kernel parameters changed: capture again
         cudaGraphExecDestroy(h->graph_exec);
@@ -541,6 +560,7 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     }
     CK(h, cudaEventSynchronize(h->ev[SIM_NUM_KERNELS]), "event sync");
     h->t += 1;
+    h->p_ready = false;  // the instrumented step made no P rows
     for (int i = 0; i < SIM_NUM_KERNELS; ++i)
         CK(h, cudaEventElapsedTime(&out->kernel_ms[kTimedOrder[i]], h->ev[i], h->ev[i + 1]), "elapsed");
     CK(h, cudaEventElapsedTime(&out->step_ms, h->ev[0], h->ev[SIM_NUM_KERNELS]), "elapsed");
@@ -701,7 +721,9 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     CK(h, eco::launch_set_owner(p, s), "owners");
     CK(h, cudaMemsetAsync(p.pol_ctr, 0, 2 * sizeof(unsigned long long), s), "memset");
+    CK(h, cudaMemsetAsync(h->bar + 3, 0, 2 * sizeof(unsigned long long), s), "memset");  // P counters
     h->regrown_ahead = false;
+    h->p_ready = false;
     return sync(h);
 }
 

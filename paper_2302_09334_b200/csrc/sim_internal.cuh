@@ -68,6 +68,13 @@ struct DevParams {
     int4 *mrec_slot;             // [S] sharded: move records by SLOT (the list order differs by rank)
     int32_t *own_list;           // [2][S] sharded: this rank's live slots of step t (by parity)
     int32_t *own_count;          // [2]
+    // Split policy (one unsharded world, Hd = 32, graph mode): P[slot] = W_hh h + b for the
+    // NEXT step is computed by k_post for the survivors (off the policy's critical path,
+    // beside the latency-bound phases); the policy then streams only P and the active W_ih
+    // columns.  Children (the last *p_children list positions) start from their bias.
+    int32_t split;
+    float *Pbuf;                 // [S][Hd*4] device order [k][4], like b
+    int32_t *p_children;         // list positions at the end of step t's list without a P row
     int2 *cand;                  // [n_worlds][S] single world: this step's eligible parents (slot, cell)
     int32_t *n_cand;             // [n_worlds] their count
     int32_t *birth_child, *birth_parent, *birth_cell, *n_births;  // by birth rank
@@ -230,6 +237,8 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
 cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot] = slot % n_ranks,
                                                                   // own list of step t, zero records
 bool policy_supports_shard();  // the Hd = 32 policy kernel of this build honours ownership
+cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);  // P of step t
+cudaError_t post_prepare();  // kernel attributes of k_post (dynamic shared memory)
 
 // state conversion (canonical <-> device)
 cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);

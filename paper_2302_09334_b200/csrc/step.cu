@@ -1128,9 +1128,90 @@ constexpr int HALF_DEPTH = ECO_HALF_DEPTH;
 constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6
 constexpr int HALF_BPS = HALF_DEPTH <= 6 ? 4 : HALF_DEPTH <= 8 ? 3 : 2;  // blocks per SM the smem allows
 
+// P[slot] = W_hh h + b (Hd = 32) for list positions [0, n) of `list`, one agent per
+// half-warp context (ctx of nctx; both halves of a warp call it together), through the same
+// per-lane cp.async ring as the policy (`ring` = this context's R slots).  The sum is formed
+// in the policy's order (the 32 W_hh rows by FMA, then b), so that a policy starting from P
+// produces exactly the gates of one streaming W_hh itself.
+__device__ __forceinline__ void hh_pass(const DevParams &p, const int32_t *list, int n, int ctx, int nctx,
+                                        float4 *ring) {
+    constexpr int HD = 32, NHH = 32, R = HALF_DEPTH;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    float4 *rg = ring + hl;  // slot s, unit hl: rg[s * 32]; unit hl+16: rg[s * 32 + 16]
+    for (int r0 = 0; r0 < n; r0 += nctx) {
+        const int i = r0 + ctx;
+        const bool active = i < n;
+        if (!__any_sync(FULL, active)) break;
+        const int slot = active ? list[i] : 0;
+        const float *Wl = p.weights + (size_t)slot * p.Pd + hl * 4;
+        const float *Whh = Wl + p.off_hh;
+        auto issue = [&](int s_, const float *src) {
+            if (active) {
+                cp_async16(rg + s_ * 32, src, 0ull);
+                cp_async16(rg + s_ * 32 + 16, src + 64, 0ull);
+            }
+            cp_commit();
+        };
+#pragma unroll
+        for (int q = 0; q < R; ++q) issue(q, Whh + q * HD * 4);
+        const float hk0 = active ? p.h[(size_t)slot * HD + hl] : 0.f;
+        const float hk1 = active ? p.h[(size_t)slot * HD + hl + 16] : 0.f;
+        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+#pragma unroll
+        for (int k = 0; k < NHH; ++k) {
+            cp_wait<R - 1>();
+            const float4 c0 = rg[(k % R) * 32], c1 = rg[(k % R) * 32 + 16];
+            const float hj = __shfl_sync(FULL, k < 16 ? hk0 : hk1, k & 15, 16);
+            acc0.x = fmaf(hj, c0.x, acc0.x);
+            acc0.y = fmaf(hj, c0.y, acc0.y);
+            acc0.z = fmaf(hj, c0.z, acc0.z);
+            acc0.w = fmaf(hj, c0.w, acc0.w);
+            acc1.x = fmaf(hj, c1.x, acc1.x);
+            acc1.y = fmaf(hj, c1.y, acc1.y);
+            acc1.z = fmaf(hj, c1.z, acc1.z);
+            acc1.w = fmaf(hj, c1.w, acc1.w);
+            if (k + R < NHH) issue(k % R, Whh + (k + R) * HD * 4);
+            else if (k + R == NHH) issue(k % R, Wl + p.off_b);
+            else cp_commit();
+        }
+        cp_wait<R - 1>();  // the bias (chunk NHH, slot NHH % R)
+        {
+            const float4 c0 = rg[(NHH % R) * 32], c1 = rg[(NHH % R) * 32 + 16];
+            acc0.x += c0.x;
+            acc0.y += c0.y;
+            acc0.z += c0.z;
+            acc0.w += c0.w;
+            acc1.x += c1.x;
+            acc1.y += c1.y;
+            acc1.z += c1.z;
+            acc1.w += c1.w;
+        }
+        cp_wait<0>();
+        if (active) {
+            float4 *P = reinterpret_cast<float4 *>(p.Pbuf + (size_t)slot * HD * 4);
+            P[hl] = acc0;
+            P[hl + 16] = acc1;
+        }
+        __syncwarp();
+    }
+}
+
+// P of every live agent of step t (after create / set_state / instrumented steps), one
+// half-warp per agent; no children pending afterwards.
+__global__ void __launch_bounds__(256, HALF_BPS) k_prepare_p(DevParams p) {
+    extern __shared__ float4 half_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ag = warp * 2 + (lane >> 4);
+    const int64_t t = p.t[0];
+    hh_pass(p, list_of(p, t, 0), *count_of(p, t, 0), ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
+            half_smem + (ag * HALF_DEPTH) * 32);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.p_children = 0;
+}
+
 // SHARD = false compiles the sharding branches out, so the unsharded kernels keep their code
 // (a local DevParams copy to fold n_ranks costs 3 us in this kernel: measured).
-template <bool SHARD>
+template <bool SHARD, bool SPLIT = false>
 __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
     constexpr unsigned FULL = 0xffffffffu;
@@ -1185,10 +1266,17 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
                 cp_async16(rg + slot_ * 32 + 16, src + 64, 0ull);
             }
         };
-#pragma unroll
-        for (int q = 0; q < R; ++q) {  // prologue: W_hh rows 0..R-1
-            issue(q, Whh + q * HD * 4);
+        // split: the first chunk is P = W_hh h + b (k_post made it), or the bias of a child
+        const bool child = SPLIT && active && i >= *count_of(p, t, w) - *p.p_children;
+        if (SPLIT) {
+            issue(0, child ? Wl + p.off_b : p.Pbuf + (size_t)slot * HD * 4 + hl * 4);
             cp_commit();
+        } else {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {  // prologue: W_hh rows 0..R-1
+                issue(q, Whh + q * HD * 4);
+                cp_commit();
+            }
         }
         float hk0 = 0.f, hk1 = 0.f, ck0 = 0.f, ck1 = 0.f;
         float wo0[5], wo1[5], bo[5];
@@ -1261,13 +1349,49 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             trace[3] = nnz;
         }
 #endif
+        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+        if (SPLIT) {
+            // chunk 0 = P (or b), chunks 1.. = the active columns; R ticks per round from 0
+            const int N1 = 1 + nnz;
+            const int Nw1 = __reduce_max_sync(FULL, active ? N1 : 0);
+#pragma unroll
+            for (int q = 1; q < R; ++q) {
+                if (q < N1) issue(q, Wl + (int)cols[q - 1] * HD * 4);
+                cp_commit();
+            }
+            for (int k0 = 0; k0 < Nw1; k0 += R) {
+#pragma unroll
+                for (int s2 = 0; s2 < R; ++s2) {
+                    const int k = k0 + s2;
+                    cp_wait<R - 1>();
+                    if (k < N1) {
+                        const float4 c0 = rg[s2 * 32], c1 = rg[s2 * 32 + 16];
+                        if (k == 0) {
+                            acc0 = c0;
+                            acc1 = c1;
+                        } else {
+                            acc0.x += c0.x;
+                            acc0.y += c0.y;
+                            acc0.z += c0.z;
+                            acc0.w += c0.w;
+                            acc1.x += c1.x;
+                            acc1.y += c1.y;
+                            acc1.z += c1.z;
+                            acc1.w += c1.w;
+                        }
+                    }
+                    const int kn = k + R;
+                    if (kn < N1) issue(s2, Wl + (int)cols[kn - 1] * HD * 4);
+                    cp_commit();
+                }
+            }
+        } else {
         const int N = Q0 + nnz;
         const int Nw = __reduce_max_sync(FULL, active ? N : 0);  // the warp runs the longer sequence
         auto refill = [&](int kn, int slot_) {
             if (kn < N) issue(slot_, kn < NHH ? Whh + kn * HD * 4 : (kn == QB ? Wl + p.off_b : Wl + (int)cols[kn - Q0] * HD * 4));
             cp_commit();
         };
-        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
 #pragma unroll
         for (int k = 0; k < NHH; ++k) {  // W_hh rows
             cp_wait<R - 1>();
@@ -1313,6 +1437,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
                 refill(k + R, rs);
             }
         }
+        }  // !SPLIT
         cp_wait<0>();
         const float cn0 = sigmoidf_acc(acc0.y) * ck0 + sigmoidf_acc(acc0.x) * tanhf(acc0.z);
         const float hn0 = sigmoidf_acc(acc0.w) * tanhf(cn0);
@@ -1398,6 +1523,10 @@ cudaError_t policy_prepare() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_policy_half<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_prepare_p, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_policy_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
 }
 
@@ -1422,6 +1551,7 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
             const long hk_cap = (long)lc.sms * 4;
             if (blocks < (hk < hk_cap ? hk : hk_cap)) blocks = hk < hk_cap ? hk : hk_cap;
             if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
+            else if (p.split) k_policy_half<false, true><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
             else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
             break;
         }
@@ -1476,7 +1606,8 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 #define ECO_POST_THREADS 1024
 #endif
 constexpr int POST_THREADS = ECO_POST_THREADS;
-constexpr int CLAIMS_BLOCK_MAX = 4 * POST_THREADS;  // eligible parents block 0 claims by itself  // one block per SM (64 registers per thread at 1024)
+constexpr int CLAIMS_BLOCK_MAX = 4 * POST_THREADS;
+constexpr int POST_SMEM = (POST_THREADS / 32) * HALF_DEPTH * 32 * 16;  // split: P rings (96 KB)  // eligible parents block 0 claims by itself  // one block per SM (64 registers per thread at 1024)
 #ifdef ECO_BLOCK_CLOCK
 // diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
 // phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
@@ -1511,6 +1642,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     if (!SHARD) p.n_ranks = 1;
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
+    extern __shared__ float4 post_smem[];  // split: the P rings, POST_THREADS/32 contexts x HALF_DEPTH
     // warp-interleaved global index: consecutive warps of work land on different blocks
     // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
     const size_t gtid = interleaved_gtid();
@@ -1588,52 +1720,52 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
                 asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
             }
             lap(2);
+            if (p.split && gridDim.x > 1) {  // every P block has read the survivor count
+                if (threadIdx.x == 0) {
+                    unsigned long long cur;
+                    do {
+                        asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar + 3 + (T & 1)) : "memory");
+                    } while (cur < gridDim.x - 1);
+                }
+                __syncthreads();
+            }
             rank_place<POST_THREADS>(p, 0, T, k, s_free, s_bcell, s_par);
+            if (threadIdx.x == 0) {
+                *p.p_children = p.split ? k.n_place : 0;  // the new children have no P row
+                bar[3 + ((T + 1) & 1)] = 0ull;            // the next launch's counter
+            }
             if (gridDim.x == 1) mutate_world(p, 0, T, k.n_place, threadIdx.x, blockDim.x);  // no other block
         } else {
             const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
-            const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
-            const size_t bthr = (size_t)nb * blockDim.x;
+            const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            // split policy: the first half of each block's warps make P = W_hh h + b of the next
+            // step's survivors (bandwidth) while the second half regrows and mutates (latency)
+            const int hh_warps = p.split ? POST_THREADS / 64 : 0;
+            if (wid < hh_warps) {
+                const int n_surv = *reinterpret_cast<volatile int32_t *>(count_of(p, T + 1, 0));
+                asm volatile("bar.sync 2, %0;" ::"r"(hh_warps * 32) : "memory");
+                if (threadIdx.x == 0) atomicAdd(bar + 3 + (T & 1), 1ull);  // block 0 may now append births
+                const int ag = wid * 2 + (lane >> 4);
+                hh_pass(p, list_of(p, T + 1, 0), n_surv, ag * (int)nb + (int)b, (int)nb * hh_warps * 2,
+                        post_smem + (ag * HALF_DEPTH) * 32);
+                return;
+            }
+            const int gw = POST_THREADS / 32 - hh_warps;  // the regrowth and mutation warps
+            const size_t btid = ((size_t)(wid - hh_warps) * nb + b) * 32 + lane;
+            const size_t bthr = (size_t)nb * gw * 32;
             const uint64_t r0 = b == 0 ? globaltimer_ns() : 0ull;
-#ifdef ECO_BLOCK_CLOCK
-            const long long c0_ = clock64();
-            const uint64_t g0_ = globaltimer_ns();
-#endif
             move_claim_reset(p, T, btid, bthr);
             regrow_phase(p, T + 1, btid, bthr);
-            if (b == 0 && (threadIdx.x & 31) == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
-#ifdef ECO_BLOCK_CLOCK
-            if (btid < 2600 && (threadIdx.x & 31) == 0) {  // warps with regrowth items: cycles and ns
-                atomicAdd(p.phase_ns + 10, (unsigned long long)(clock64() - c0_));
-                atomicAdd(p.phase_ns + 11, globaltimer_ns() - g0_);
-                atomicAdd(p.phase_ns + 12, 1ull);
-            }
-#endif
-#ifdef ECO_BLOCK_CLOCK
-            __syncthreads();
-            const uint64_t m0_ = globaltimer_ns();
-#endif
-            if (threadIdx.x == 0) {
+            if (b == 0 && lane == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
+            if (threadIdx.x == hh_warps * 32) {
                 unsigned long long cur;
                 do {
                     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(flag) : "memory");
                 } while (cur < target + 1);
             }
-            __syncthreads();
-#ifdef ECO_BLOCK_CLOCK
-            const uint64_t m1_ = globaltimer_ns();
-#endif
+            asm volatile("bar.sync 1, %0;" ::"r"(gw * 32) : "memory");
             const int n_b = *reinterpret_cast<volatile int32_t *>(p.n_births);
             if (n_b > 0) mutate_world(p, 0, T, n_b, btid, bthr);
-#ifdef ECO_BLOCK_CLOCK
-            __syncthreads();
-            if (threadIdx.x == 0) {  // per-block marks of the single-world tail in the k = 2 slots
-                unsigned long long *q_ = p.phase_ns + ECO_BLOCK_CLOCK_BASE + (2 * gridDim.x + blockIdx.x) * 3;
-                q_[0] += m0_ - bt_;
-                q_[1] += m1_ - bt_;
-                q_[2] += globaltimer_ns() - bt_;
-            }
-#endif
         }
     } else {
         // several worlds: one block per world ranks, places and counts them (t += 1); the
@@ -1693,6 +1825,13 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
 
 bool policy_supports_shard() { return ECO_POLICY_TMA == 0; }  // k_policy_half
 
+cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
+    if (!p.split) return cudaSuccess;
+    const unsigned blocks = (unsigned)((p.S + HALF_AGENTS - 1) / HALF_AGENTS);
+    k_prepare_p<<<blocks > 0 ? blocks : 1, 256, HALF_SMEM, s>>>(p);
+    return cudaGetLastError();
+}
+
 __global__ void k_set_owner(DevParams p) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < p.S; k += gridDim.x * blockDim.x) {
         p.owner[k] = (uint8_t)(k % p.n_ranks);
@@ -1729,14 +1868,20 @@ cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 }
 
 cudaError_t post_occupancy(int *blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post<true>, POST_THREADS, 0);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post<true>, POST_THREADS, POST_SMEM);
+}
+
+cudaError_t post_prepare() {
+    cudaError_t e = cudaFuncSetAttribute(k_post<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_post<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lc.post_blocks);
     cfg.blockDim = dim3(POST_THREADS);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = p.split ? POST_SMEM : 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
