@@ -224,6 +224,7 @@ def run_ours(args, rank, world_size, local_rank):
 
         world.step(W)
         world.synchronize()
+        world.phase_ns(reset=True)  # the phase clocks cover the timed steps only
         need_snap = not (args.no_replay and args.no_e2e and args.no_cpu_baseline)
         snap = world.get_state() if need_snap else None
         t0 = world.t

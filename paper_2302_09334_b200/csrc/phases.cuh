@@ -20,8 +20,8 @@ namespace eco {
 // Release/acquire barrier over all blocks of a cooperatively launched grid (co-residency
 // guaranteed by the cooperative launch).  bar[0] counts arrivals monotonically across
 // launches; `target` starts at grid_sync_base() and grows by gridDim per barrier.
-__device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long long &target) {
-    __syncthreads();
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long long &target, int nthr) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     target += gridDim.x;
     if (threadIdx.x == 0) {
         unsigned long long cur;
@@ -29,7 +29,10 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long
         cur += 1;
         while (cur < target) asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+}
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, unsigned long long &target) {
+    grid_sync(bar, target, blockDim.x);
 }
 
 // bar[1] holds the arrival count after the previous launch's last barrier (the launches

@@ -1133,9 +1133,10 @@ constexpr int HALF_BPS = HALF_DEPTH <= 6 ? 4 : HALF_DEPTH <= 8 ? 3 : 2;  // bloc
 // per-lane cp.async ring as the policy (`ring` = this context's R slots).  The sum is formed
 // in the policy's order (the 32 W_hh rows by FMA, then b), so that a policy starting from P
 // produces exactly the gates of one streaming W_hh itself.
+template <int R>
 __device__ __forceinline__ void hh_pass(const DevParams &p, const int32_t *list, int n, int ctx, int nctx,
                                         float4 *ring) {
-    constexpr int HD = 32, NHH = 32, R = HALF_DEPTH;
+    constexpr int HD = 32, NHH = 32;
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, hl = lane & 15;
     float4 *rg = ring + hl;  // slot s, unit hl: rg[s * 32]; unit hl+16: rg[s * 32 + 16]
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_prepare_p(DevParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ag = warp * 2 + (lane >> 4);
     const int64_t t = p.t[0];
-    hh_pass(p, list_of(p, t, 0), *count_of(p, t, 0), ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
+    hh_pass<HALF_DEPTH>(p, list_of(p, t, 0), *count_of(p, t, 0), ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
             half_smem + (ag * HALF_DEPTH) * 32);
     if (blockIdx.x == 0 && threadIdx.x == 0) *p.p_children = 0;
 }
@@ -1606,8 +1607,15 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 #define ECO_POST_THREADS 1024
 #endif
 constexpr int POST_THREADS = ECO_POST_THREADS;
+#ifndef ECO_HH_WARPS
+#define ECO_HH_WARPS 4  // split: the P warps of blocks 1.. (measured: 2..16 warps, depth 6..16)
+#endif
 constexpr int CLAIMS_BLOCK_MAX = 4 * POST_THREADS;
-constexpr int POST_SMEM = (POST_THREADS / 32) * HALF_DEPTH * 32 * 16;  // split: P rings (96 KB)  // eligible parents block 0 claims by itself  // one block per SM (64 registers per thread at 1024)
+#ifndef ECO_HH_DEPTH
+#define ECO_HH_DEPTH 8  // split: 512-B chunks in flight per P context
+#endif
+constexpr int HH_DEPTH = ECO_HH_DEPTH;
+constexpr int POST_SMEM = 2 * ECO_HH_WARPS * HH_DEPTH * 32 * 16;  // split: the P rings
 #ifdef ECO_BLOCK_CLOCK
 // diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
 // phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
@@ -1615,14 +1623,14 @@ constexpr int POST_SMEM = (POST_THREADS / 32) * HALF_DEPTH * 32 * 16;  // split:
 constexpr int ECO_BLOCK_CLOCK_BASE = 16;
 #define POST_SYNC(k)                                                                              \
     do {                                                                                          \
-        __syncthreads();                                                                          \
+        asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");                                  \
         const uint64_t a_ = globaltimer_ns();                                                     \
         uint64_t f_ = a_;                                                                         \
         if (threadIdx.x == 0) {                                                                   \
             asm volatile("fence.acq_rel.gpu;" ::: "memory");                                     \
             f_ = globaltimer_ns();                                                                \
         }                                                                                         \
-        grid_sync(bar, target);                                                                   \
+        grid_sync(bar, target, nthr);                                                             \
         const uint64_t e_ = globaltimer_ns();                                                     \
         if (threadIdx.x == 0) {                                                                   \
             unsigned long long *q_ = p.phase_ns + ECO_BLOCK_CLOCK_BASE + ((k) * gridDim.x + blockIdx.x) * 3; \
@@ -1633,7 +1641,7 @@ constexpr int ECO_BLOCK_CLOCK_BASE = 16;
         bt_ = e_;                                                                                 \
     } while (0)
 #else
-#define POST_SYNC(k) grid_sync(bar, target)
+#define POST_SYNC(k) grid_sync(bar, target, nthr)
 #endif
 
 template <bool SHARD>
@@ -1642,13 +1650,54 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     if (!SHARD) p.n_ranks = 1;
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
-    extern __shared__ float4 post_smem[];  // split: the P rings, POST_THREADS/32 contexts x HALF_DEPTH
-    // warp-interleaved global index: consecutive warps of work land on different blocks
-    // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once
-    const size_t gtid = interleaved_gtid();
-    const size_t gthreads = (size_t)gridDim.x * blockDim.x;
+    extern __shared__ float4 post_smem[];  // split: the P rings, 2 HH_WARPS contexts x HH_DEPTH
     unsigned long long target = grid_sync_base(bar);
     const int64_t T = p.t[0];  // the step this launch completes (all worlds share t)
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // split policy (one world): the last HH_WARPS warps of blocks 1.. make P = W_hh h + b of
+    // every agent alive at the start of step T (the next step's survivors among them) from
+    // the kernel's first cycle, streaming beside the latency-bound dynamics of the other
+    // warps; they take part in no barrier.  The rows of the agents that die are never read
+    // (a child placed in such a slot starts from its bias).
+    constexpr int HH_WARPS = ECO_HH_WARPS, DYN_WARPS = POST_THREADS / 32 - HH_WARPS;
+    const bool hh_split = p.split && p.n_worlds == 1 && gridDim.x > 1;
+#ifdef ECO_END_CLOCK
+    // diagnostic build: per launch, the latest end of the P warps and of the other warps
+    // after block 0's start, summed over the launches in phase_ns[4] and [5]
+    unsigned long long *ec = reinterpret_cast<unsigned long long *>(p.phase_ns) + 10 + 3 * (T & 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long *pe = reinterpret_cast<unsigned long long *>(p.phase_ns) + 10 + 3 * ((T + 1) & 1);
+        if (pe[0]) {
+            p.phase_ns[4] += pe[1] - pe[0];
+            p.phase_ns[5] += pe[2] - pe[0];
+        }
+        pe[0] = pe[1] = pe[2] = 0ull;
+        ec[0] = globaltimer_ns();
+    }
+#define END_CLOCK(k) \
+    if (lane == 0) atomicMax(ec + (k), (unsigned long long)globaltimer_ns())
+#else
+#define END_CLOCK(k)
+#endif
+    if (hh_split && blockIdx.x > 0 && wid >= DYN_WARPS) {
+        const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
+        const int ag = (wid - DYN_WARPS) * 2 + (lane >> 4);
+        hh_pass<HH_DEPTH>(p, list_of(p, T, 0), *count_of(p, T, 0), ag * (int)nb + (int)b, (int)nb * HH_WARPS * 2,
+                          post_smem + (ag * HH_DEPTH) * 32);
+        END_CLOCK(1);
+        return;
+    }
+    // warp-interleaved global index: consecutive warps of work land on different blocks
+    // (SMs), so the per-item dependency chains of every phase run on all 148 SMs at once;
+    // with the split, over the dynamics warps (all of block 0's, DYN_WARPS of the others)
+    size_t gtid = interleaved_gtid(), gthreads = (size_t)gridDim.x * blockDim.x;
+    int nthr = blockDim.x;  // threads of this block in the barriers
+    if (hh_split) {
+        const size_t nb = gridDim.x - 1;
+        gthreads = nb * DYN_WARPS * 32 + blockDim.x;
+        gtid = blockIdx.x == 0 ? nb * DYN_WARPS * 32 + threadIdx.x : ((size_t)wid * nb + blockIdx.x - 1) * 32 + lane;
+        if (blockIdx.x > 0) nthr = DYN_WARPS * 32;
+    }
     // phase clock: block 0 accumulates the time between barriers (as seen by block 0)
     const bool clk = blockIdx.x == 0 && threadIdx.x == 0;
     uint64_t t0 = clk ? globaltimer_ns() : 0ull, t1;
@@ -1707,7 +1756,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         const bool claims_grid = *reinterpret_cast<volatile int32_t *>(p.n_cand) > CLAIMS_BLOCK_MAX;
         if (claims_grid) {
             birth_claims_grid(p, T, gtid, gthreads);
-            grid_sync(bar, target);
+            grid_sync(bar, target, nthr);
         }
         if (blockIdx.x == 0) {
             if (gridDim.x == 1) move_claim_reset(p, T, threadIdx.x, blockDim.x);  // no other block
@@ -1720,44 +1769,19 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
                 asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
             }
             lap(2);
-            if (p.split && gridDim.x > 1) {  // every P block has read the survivor count
-                if (threadIdx.x == 0) {
-                    unsigned long long cur;
-                    do {
-                        asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar + 3 + (T & 1)) : "memory");
-                    } while (cur < gridDim.x - 1);
-                }
-                __syncthreads();
-            }
             rank_place<POST_THREADS>(p, 0, T, k, s_free, s_bcell, s_par);
-            if (threadIdx.x == 0) {
-                *p.p_children = p.split ? k.n_place : 0;  // the new children have no P row
-                bar[3 + ((T + 1) & 1)] = 0ull;            // the next launch's counter
-            }
+            if (threadIdx.x == 0) *p.p_children = p.split ? k.n_place : 0;  // the new children have no P row
             if (gridDim.x == 1) mutate_world(p, 0, T, k.n_place, threadIdx.x, blockDim.x);  // no other block
         } else {
             const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
-            const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            // split policy: the first half of each block's warps make P = W_hh h + b of the next
-            // step's survivors (bandwidth) while the second half regrows and mutates (latency)
-            const int hh_warps = p.split ? POST_THREADS / 64 : 0;
-            if (wid < hh_warps) {
-                const int n_surv = *reinterpret_cast<volatile int32_t *>(count_of(p, T + 1, 0));
-                asm volatile("bar.sync 2, %0;" ::"r"(hh_warps * 32) : "memory");
-                if (threadIdx.x == 0) atomicAdd(bar + 3 + (T & 1), 1ull);  // block 0 may now append births
-                const int ag = wid * 2 + (lane >> 4);
-                hh_pass(p, list_of(p, T + 1, 0), n_surv, ag * (int)nb + (int)b, (int)nb * hh_warps * 2,
-                        post_smem + (ag * HALF_DEPTH) * 32);
-                return;
-            }
-            const int gw = POST_THREADS / 32 - hh_warps;  // the regrowth and mutation warps
-            const size_t btid = ((size_t)(wid - hh_warps) * nb + b) * 32 + lane;
+            const int gw = hh_split ? DYN_WARPS : POST_THREADS / 32;  // the regrowth and mutation warps
+            const size_t btid = ((size_t)wid * nb + b) * 32 + lane;
             const size_t bthr = (size_t)nb * gw * 32;
             const uint64_t r0 = b == 0 ? globaltimer_ns() : 0ull;
             move_claim_reset(p, T, btid, bthr);
             regrow_phase(p, T + 1, btid, bthr);
             if (b == 0 && lane == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
-            if (threadIdx.x == hh_warps * 32) {
+            if (threadIdx.x == 0) {
                 unsigned long long cur;
                 do {
                     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(flag) : "memory");
@@ -1789,6 +1813,10 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
 #ifdef ECO_BLOCK_CLOCK
     __syncthreads();
     if (threadIdx.x == 0) p.phase_ns[ECO_BLOCK_CLOCK_BASE + (3 * gridDim.x + blockIdx.x) * 3] += globaltimer_ns() - bt_;
+#endif
+#ifdef ECO_END_CLOCK
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    if (threadIdx.x == 0) atomicMax(ec + 2, (unsigned long long)globaltimer_ns());
 #endif
     if (clk) {
         lap(3);
