@@ -139,11 +139,14 @@ typedef struct {
     int64_t device_bytes; /* device memory the handle will allocate */
 } sim_state_sizes_t;
 
-/* Per-kernel timing of one instrumented step (milliseconds, CUDA events). */
-#define SIM_NUM_KERNELS 6
+/* Per-kernel timing of one instrumented step (milliseconds, CUDA events).  hh: the P rows
+ * P = W_hh h + b of the next step's agents (the recurrent half of the gate
+ * sum), which graph mode computes inside its cooperative kernel beside the dynamics; 0
+ * when the policy is not split (several worlds, hidden != 32, sharded). */
+#define SIM_NUM_KERNELS 7
 typedef struct {
     float step_ms;                     /* first event to last event of the step */
-    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_rank, mutate */
+    float kernel_ms[SIM_NUM_KERNELS];  /* regrow, policy, move, birth_claim, birth_rank, mutate, hh */
 } sim_step_timing;
 
 /* --- lifecycle ------------------------------------------------------------------- */

@@ -198,21 +198,19 @@ sim_status check_nonfinite(sim_ctx *h) {
 // Instrumented mode: the phases as separate kernels, in graph mode's order, so that every
 // kernel can be bracketed by events.  Index order of sim_step_timing.kernel_ms:
 // 0 regrow (of step t+1, as inside k_post), 1 policy, 2 move, 3 birth_claim, 4 birth_rank,
-// 5 mutate.  Launch order: policy, move, regrow, claim, rank, mutate.
-constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5};
+// 5 mutate, 6 hh (split policy: the next step's P rows, standalone).  Launch order: policy,
+// move, regrow, claim, rank, mutate, hh.
+constexpr int kTimedOrder[SIM_NUM_KERNELS] = {1, 2, 0, 3, 4, 5, 6};
 
 cudaError_t launch_phase(sim_ctx *h, int k) {
     switch (k) {
         case 0: return eco::launch_regrow(h->p, 1, h->stream);
-        case 1: {  // the instrumented policy streams W_hh itself (no P rows)
-            eco::DevParams q = h->p;
-            q.split = 0;
-            return eco::launch_policy(q, h->lc, h->stream);
-        }
+        case 1: return eco::launch_policy(h->p, h->lc, h->stream);  // split: reads the P rows
         case 2: return eco::launch_move(h->p, h->lc, h->stream);
         case 3: return eco::launch_birth_claim(h->p, h->lc, h->stream);
         case 4: return eco::launch_birth_rank(h->p, h->stream);
-        default: return eco::launch_mutate(h->p, h->lc, h->stream);
+        case 5: return eco::launch_mutate(h->p, h->lc, h->stream);
+        default: return eco::launch_prepare_p(h->p, h->lc, h->stream);  // P rows of step t+1 (split only)
     }
 }
 
@@ -371,6 +369,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
     CKC(dalloc(h, &p.mrec, nw * S), "alloc");
     CKC(dalloc(h, &p.alive_list, 2 * nw * S), "alloc");
+    CKC(dalloc(h, &p.list_cell, 2 * nw * S), "alloc");
     CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
     CKC(dalloc(h, &p.n_win, nw), "alloc");
     CKC(dalloc(h, &p.free_list, nw * S), "alloc");
@@ -561,7 +560,9 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     }
     CK(h, cudaEventSynchronize(h->ev[SIM_NUM_KERNELS]), "event sync");
     h->t += 1;
-    h->p_ready = false;  // the instrumented step made no P rows
+    // split: the hh kernel made the P rows of every agent of step t+1 (children included, from
+    // h = 0: exactly b), so p_children is 0 and the next step may run either way
+
     for (int i = 0; i < SIM_NUM_KERNELS; ++i)
         CK(h, cudaEventElapsedTime(&out->kernel_ms[kTimedOrder[i]], h->ev[i], h->ev[i + 1]), "elapsed");
     CK(h, cudaEventElapsedTime(&out->step_ms, h->ev[0], h->ev[SIM_NUM_KERNELS]), "elapsed");
@@ -683,8 +684,25 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
                 seen[c] = 1;
             }
         }
-        if (in->weights && !all_finite(in->weights, nw * S * (size_t)d.P))
+    }
+    // weights up to 2 GiB: one staging copy in flight while the host checks them (the state is
+    // untouched until the check passes); larger: checked first, then staged in 256 MB chunks
+    float *wstage = nullptr;
+    const size_t wcount = nw * S * (size_t)d.P;
+    if (in->weights && S) {
+        if (wcount * 4 <= ((size_t)2 << 30)) {
+            CK(h, cudaMallocAsync(reinterpret_cast<void **>(&wstage), wcount * 4, s), "alloc");
+            const cudaError_t e = cudaMemcpyAsync(wstage, in->weights, wcount * 4, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) cudaFreeAsync(wstage, s);
+            CK(h, e, "weights");
+        }
+        if (!all_finite(in->weights, wcount)) {
+            if (wstage) {
+                cudaFreeAsync(wstage, s);
+                cudaStreamSynchronize(s);
+            }
             return fail(SIM_E_INVALID, "invalid field: weights (non-finite)");
+        }
     }
     if (!in->resources && ((in->t ^ h->t) & 1)) {
         // the current resource plane is selected by step parity: carry it over
@@ -719,7 +737,11 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     if (in->logits && S)
         CK(h, cudaMemcpy2DAsync(p.logits, eco::LOGIT_STRIDE * 4, in->logits, 5 * 4, 5 * 4, nw * S,
                                 cudaMemcpyHostToDevice, s), "logits");
-    if (in->weights && S) {
+    if (wstage) {
+        cudaError_t e = eco::launch_weights_to_device(p, wstage, 0, nw * S, s);
+        cudaFreeAsync(wstage, s);
+        CK(h, e, "weights");
+    } else if (in->weights && S) {
         const size_t total_agents = nw * S;
         const size_t chunk = ((size_t)1 << 26) / (size_t)d.P > 0 ? ((size_t)1 << 26) / (size_t)d.P : 1;
         float *tmp;
@@ -744,7 +766,6 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     CK(h, eco::launch_set_owner(p, s), "owners");
     CK(h, cudaMemsetAsync(p.pol_ctr, 0, 2 * sizeof(unsigned long long), s), "memset");
-    CK(h, cudaMemsetAsync(h->bar + 3, 0, 2 * sizeof(unsigned long long), s), "memset");  // P counters
     h->regrown_ahead = false;
     h->p_ready = false;
     return sync(h);

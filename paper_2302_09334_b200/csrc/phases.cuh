@@ -306,7 +306,11 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 if (m) pos0 = atomicAdd(count_of(p, t0 + 1, w0), __popc(m));
             }
             pos0 = __shfl_sync(0xffffffffu, pos0, 0);
-            if (survive) list_of(p, t + 1, w)[pos0 + __popc(m & ((1u << lane) - 1u))] = slot;
+            if (survive) {
+                const int q = pos0 + __popc(m & ((1u << lane) - 1u));
+                list_of(p, t + 1, w)[q] = slot;
+                list_cell_of(p, t + 1, w)[q] = cand_cell;  // survivors: cand_cell is the cell
+            }
             if (p.n_ranks > 1) {  // sharded: this rank's own survivors, the next policy's work
                 const bool mine = survive && p.owner[slot] == p.rank;
                 const unsigned mo = __ballot_sync(0xffffffffu, mine);
@@ -320,7 +324,11 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             if (ate) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), 1ull);
             if (died_e) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), 1ull);
             if (died_a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), 1ull);
-            if (survive) list_of(p, t + 1, w)[atomicAdd(count_of(p, t + 1, w), 1)] = slot;
+            if (survive) {
+                const int q = atomicAdd(count_of(p, t + 1, w), 1);
+                list_of(p, t + 1, w)[q] = slot;
+                list_cell_of(p, t + 1, w)[q] = cand_cell;
+            }
         }
     }
 }
@@ -429,30 +437,51 @@ __device__ __forceinline__ int birth_target(const DevParams &p, int64_t t, int c
 // neighbour that is in-grid, agent-free in O'' and resource-free in R''; slot on the own
 // cell; atomicMax of the claim key on the candidate cell; the claimed-cell bitmap), so the
 // rank can follow after a block barrier instead of a grid barrier.
+#ifndef ECO_CLAIMS_B
+#define ECO_CLAIMS_B 2  // measured: 1 -> 49.9, 2 -> 49.7, 4 -> 52.8 us per step (code size)
+#endif
 template <int NT>
 __device__ void birth_claims_block(const DevParams &p, int64_t t) {
+    constexpr int B = ECO_CLAIMS_B;  // candidates per thread in flight: their loads overlap
     const int nc = *reinterpret_cast<volatile int32_t *>(p.n_cand);
     int no_cell = 0, n_cand = 0, new_cells = 0;
-    for (int r = threadIdx.x; r < nc; r += NT) {
-        const int2 sc = p.cand[r];
-        unsigned long long key;
-        const int c = birth_target(p, t, sc.y, key);
-        if (c < 0) {
-            ++no_cell;
-            continue;
+    for (int r0 = 0; r0 < nc; r0 += NT * B) {
+        int2 sc[B];
+        int c[B];
+        unsigned long long key[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int r = r0 + u * NT + (int)threadIdx.x;
+            sc[u] = r < nc ? p.cand[r] : make_int2(-1, 0);
         }
-        uint32_t bit;
-        const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
-        if (!(old & bit)) ++new_cells;
-        atomicMax(p.bkey + c, key);
-        p.bslot[sc.y] = sc.x;
-        ++n_cand;
+#pragma unroll
+        for (int u = 0; u < B; ++u) c[u] = sc[u].x >= 0 ? birth_target(p, t, sc[u].y, key[u]) : -2;
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (c[u] == -2) continue;
+            if (c[u] < 0) {
+                ++no_cell;
+                continue;
+            }
+            uint32_t bit;
+            const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, 0), p, c[u], bit), bit);
+            if (!(old & bit)) ++new_cells;
+            atomicMax(p.bkey + c[u], key[u]);
+            p.bslot[sc[u].y] = sc[u].x;
+            ++n_cand;
+        }
     }
-    sim_step_record *rec = record_of(p, t, 0);
-    if (no_cell) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_no_cell), (unsigned long long)no_cell);
-    // deferred_claim accumulates the candidates here; the rank subtracts the claimed cells
-    if (n_cand) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_claim), (unsigned long long)n_cand);
-    if (new_cells) atomicAdd(p.n_win, new_cells);
+    // warp sums first: one atomic per warp and counter, not one per thread
+    no_cell = __reduce_add_sync(0xffffffffu, no_cell);
+    n_cand = __reduce_add_sync(0xffffffffu, n_cand);
+    new_cells = __reduce_add_sync(0xffffffffu, new_cells);
+    if ((threadIdx.x & 31) == 0) {
+        sim_step_record *rec = record_of(p, t, 0);
+        if (no_cell) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_no_cell), (unsigned long long)no_cell);
+        // deferred_claim accumulates the candidates here; the rank subtracts the claimed cells
+        if (n_cand) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_claim), (unsigned long long)n_cand);
+        if (new_cells) atomicAdd(p.n_win, new_cells);
+    }
     __syncthreads();
 }
 
@@ -549,6 +578,7 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
         if (p.owner[parent] == p.rank) p.own_list[((t + 1) & 1) * p.S + atomicAdd(p.own_count + ((t + 1) & 1), 1)] = child;
     }
     list_of(p, t + 1, w)[n_surv + r] = child;
+    list_cell_of(p, t + 1, w)[n_surv + r] = c;
 }
 
 // (1) + (2): free slots and claimed cells of ranks r < n_place into s_free / s_bcell (r <

@@ -56,6 +56,7 @@ struct DevParams {
     float *h, *c, *logits, *weights;
     int4 *mrec;                  // [n_worlds][S] per list position: (slot, cell, target or -1, MOVE w0)
     int32_t *alive_list;         // [2][n_worlds][S]
+    int32_t *list_cell;          // [2][n_worlds][S] the cell of each listed agent (= cell[slot])
     int32_t *n_alive;            // [2][n_worlds]
     int32_t *n_win;              // [n_worlds] birth-claim winners this step
     int32_t *free_list;          // [n_worlds][S] scratch (first n_place entries used)
@@ -199,6 +200,9 @@ __device__ __forceinline__ uint32_t *bbits_of(const DevParams &p, int64_t t, int
 }
 __device__ __forceinline__ int32_t *list_of(const DevParams &p, int64_t t, int w) {
     return p.alive_list + ((size_t)(t & 1) * p.n_worlds + w) * p.S;
+}
+__device__ __forceinline__ int32_t *list_cell_of(const DevParams &p, int64_t t, int w) {
+    return p.list_cell + ((size_t)(t & 1) * p.n_worlds + w) * p.S;
 }
 __device__ __forceinline__ int32_t *count_of(const DevParams &p, int64_t t, int w) {
     return p.n_alive + (size_t)(t & 1) * p.n_worlds + w;

@@ -1210,6 +1210,16 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_prepare_p(DevParams p) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *p.p_children = 0;
 }
 
+#ifdef ECO_TIMELINE
+// diagnostic build: per step t (ring of 1024), the policy's first block start and last block
+// end and k_post's, as globaltimer ns in phase_ns[16 + (t % 1024) * 4 + {0..3}] (starts
+// stored inverted: atomicMax of ~x keeps the earliest); the host zeroes the ring
+__device__ __forceinline__ void timeline_mark(const DevParams &p, int k, unsigned long long v, int64_t t = -1) {
+    if (t < 0) t = p.t[0];
+    atomicMax(p.phase_ns + 16 + (size_t)(t & 1023) * 4 + k, v);
+}
+#endif
+
 // SHARD = false compiles the sharding branches out, so the unsharded kernels keep their code
 // (a local DevParams copy to fold n_ranks costs 3 us in this kernel: measured).
 template <bool SHARD, bool SPLIT = false>
@@ -1224,6 +1234,9 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     const int half = lane >> 4, hl = lane & 15;
     const int ag = warp * 2 + half;                 // agent of this half-warp within the block
     const unsigned hmask = 0xffffu << (16 * half);  // this half's lanes
+#ifdef ECO_TIMELINE
+    if (threadIdx.x == 0) timeline_mark(p, 0, ~globaltimer_ns());
+#endif
     step_housekeeping(p);
     const long total = (long)p.n_worlds * p.S;
     const long v = (long)ag * gridDim.x + blockIdx.x;
@@ -1231,22 +1244,34 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     const int w = in_range ? (int)(v / p.S) : 0;
     const int i = in_range ? (int)(v - (long)w * p.S) : 0;
     const int64_t t = p.t[w];
+    // unsharded: both parities' count, slot and cell of list position i load beside t (one
+    // round trip instead of t -> count -> slot -> cell; entries past a count are stale, unused)
+    int n_list = 0, slot = 0, cell_l = 0, n_ch = 0;
+    if (!SHARD && in_range) {
+        if (SPLIT) n_ch = *p.p_children;
+        const size_t o0 = (size_t)w * p.S + i, o1 = ((size_t)p.n_worlds + w) * p.S + i;
+        const int n0 = p.n_alive[w], n1 = p.n_alive[p.n_worlds + w];
+        const int s0 = p.alive_list[o0], s1 = p.alive_list[o1];
+        const int c0 = p.list_cell[o0], c1 = p.list_cell[o1];
+        const bool odd = (t & 1) != 0;
+        n_list = odd ? n1 : n0;
+        slot = odd ? s1 : s0;
+        cell_l = odd ? c1 : c0;
+    }
     // sharded: the contexts walk this rank's own live slots instead of the whole list
-    bool active = in_range && i < (SHARD ? p.own_count[t & 1] : *count_of(p, t, w));
+    bool active = in_range && i < (SHARD ? p.own_count[t & 1] : n_list);
     unsigned long long nnz_a = 0ull, tie_a = 0ull;
 #ifdef ECO_POLICY_TRACE
     // diagnostic build: per agent (kernel entry, mask ready, end, nnz) of the last launch
     unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(v & 8191);
     const uint64_t t_entry = globaltimer_ns();
 #endif
-    int slot = 0;
     if (SHARD) slot = active ? p.own_list[(t & 1) * p.S + i] : 0;
     if (__any_sync(FULL, active)) {  // both halves stay converged for the warp-wide intrinsics
         int cellv = 0;
         size_t gs = 0;
         const float *Wl = p.weights;  // + hl * 4: unit hl of a chunk; unit hl + 16 at + 64 floats
         if (active) {
-            if (!SHARD) slot = list_of(p, t, w)[i];
             gs = (size_t)w * p.S + slot;
             Wl = p.weights + gs * (size_t)p.Pd + hl * 4;
         }
@@ -1268,7 +1293,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             }
         };
         // split: the first chunk is P = W_hh h + b (k_post made it), or the bias of a child
-        const bool child = SPLIT && active && i >= *count_of(p, t, w) - *p.p_children;
+        const bool child = SPLIT && active && i >= n_list - n_ch;
         if (SPLIT) {
             issue(0, child ? Wl + p.off_b : p.Pbuf + (size_t)slot * HD * 4 + hl * 4);
             cp_commit();
@@ -1286,7 +1311,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             hk1 = p.h[gs * HD + hl + 16];
             ck0 = p.c[gs * HD + hl];
             ck1 = p.c[gs * HD + hl + 16];
-            cellv = p.cell[gs];
+            cellv = SHARD ? p.cell[gs] : cell_l;
         }
         const float *Wo = Wl - hl * 4;
 #pragma unroll
@@ -1490,6 +1515,9 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             b += s_ties[k];
         }
         flush_counters<SHARD>(p, wc, a, b);
+#ifdef ECO_TIMELINE
+        timeline_mark(p, 1, globaltimer_ns());
+#endif
     }
 }
 
@@ -1654,6 +1682,9 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     unsigned long long target = grid_sync_base(bar);
     const int64_t T = p.t[0];  // the step this launch completes (all worlds share t)
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef ECO_TIMELINE
+    if (threadIdx.x == 0) timeline_mark(p, 2, ~globaltimer_ns());
+#endif
     // split policy (one world): the last HH_WARPS warps of blocks 1.. make P = W_hh h + b of
     // every agent alive at the start of step T (the next step's survivors among them) from
     // the kernel's first cycle, streaming beside the latency-bound dynamics of the other
@@ -1685,6 +1716,9 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         hh_pass<HH_DEPTH>(p, list_of(p, T, 0), *count_of(p, T, 0), ag * (int)nb + (int)b, (int)nb * HH_WARPS * 2,
                           post_smem + (ag * HH_DEPTH) * 32);
         END_CLOCK(1);
+#ifdef ECO_TIMELINE
+        if (lane == 0) timeline_mark(p, 3, globaltimer_ns(), T);
+#endif
         return;
     }
     // warp-interleaved global index: consecutive warps of work land on different blocks
@@ -1817,6 +1851,10 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
 #ifdef ECO_END_CLOCK
     asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     if (threadIdx.x == 0) atomicMax(ec + 2, (unsigned long long)globaltimer_ns());
+#endif
+#ifdef ECO_TIMELINE
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+    if (threadIdx.x == 0) timeline_mark(p, 3, globaltimer_ns(), T);
 #endif
     if (clk) {
         lap(3);

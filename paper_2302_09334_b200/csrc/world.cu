@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
         if ((threadIdx.x & 31) == 0 && i < p.S) p.alive_bits[(size_t)w * p.SW + (i >> 5)] = word;
         uint32_t tot;
         const uint32_t ex = block_exclusive_scan<1024>(a, scratch, tot);
-        if (a) list[base + ex] = i;
+        if (a) {
+            list[base + ex] = i;
+            list_cell_of(p, t, w)[base + ex] = p.cell[gs];
+        }
         base += tot;
     }
     if (threadIdx.x == 0) {

@@ -21,8 +21,8 @@ _lib = None
 SIM_OK, SIM_E_INVALID, SIM_E_CUDA, SIM_E_OOM, SIM_E_NCCL, SIM_E_NONFINITE, SIM_E_STATE = 0, -1, -2, -3, -4, -5, -6
 ABI_VERSION = 1
 INT32_MAX = 2**31 - 1
-NUM_KERNELS = 6
-KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate")
+NUM_KERNELS = 7
+KERNEL_NAMES = ("regrow", "policy", "move", "birth_claim", "birth_rank", "mutate", "hh")
 
 EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_destroy", "sim_last_error",
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",

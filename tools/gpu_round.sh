@@ -16,11 +16,11 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(regrow|policy|post|move|birth|mutate)" \
       -s ${NCU_SKIP:-602} -c 60 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
   echo ncu_launch=$? >> $OUT/status.txt
-  # one full capture of the policy launch and of the k_post launch of step W (records known)
+  # one full capture: the graph path's k_post of step W-1, then the instrumented step W's policy and P rows
   W=${PROF_WARMUP:-3000}
   PCMD="python tools/profile_step.py --warmup $W --out $OUT/step_$TAG.json"
   timeout 300 $PCMD > $OUT/plain2_$TAG.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_policy|k_post" -s $((2 * W)) -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_policy_half|k_prepare_p|k_post" -s $((2 * W)) -c 3 \
       -o $OUT/prof_step_$TAG $PCMD > $OUT/ncu_full_$TAG.log 2>&1 && \
   python tools/ncu_summary.py $OUT/prof_step_$TAG.ncu-rep --step $OUT/step_$TAG.json --out $OUT/ncu_summary_$TAG.json > /dev/null 2>&1
   echo ncu_full=$? >> $OUT/status.txt

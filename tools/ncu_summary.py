@@ -59,9 +59,10 @@ if __name__ == "__main__":
         st = json.load(open(a.step))
         summary["step"] = st
         for rec in launches:
-            if "policy" in rec["kernel"]:
+            key = "policy" if "k_policy" in rec["kernel"] else "hh" if "k_prepare_p" in rec["kernel"] else None
+            if key and f"{key}_algorithmic_bytes" in st:
                 traffic = rec.get("dram_read_bytes", 0) + rec.get("dram_write_bytes", 0)
-                alg = st["policy_algorithmic_bytes"]
+                alg = st[f"{key}_algorithmic_bytes"]
                 rec["algorithmic_bytes"] = alg
                 rec["traffic_over_algorithmic"] = traffic / alg
                 rec["algorithmic_GBps"] = alg / rec["duration_ns"]

@@ -1,8 +1,12 @@
-"""Run the paper-scale world W steps through the graph path, then ONE more step whose
-record (agents, active inputs, births) is written to --out as JSON together with the
-algorithmic bytes of its policy launch (bench.policy_bytes).  Meant to run under
-    ncu --set full -k regex:k_policy --launch-skip W --launch-count 1 ...
-so the captured launch is exactly the described step (k_post: --launch-skip W - 1 too)."""
+"""Run the paper-scale world W steps through the graph path, then ONE instrumented step
+(sim_step_timed: the split policy, the phase kernels and k_prepare_p, the P rows of the next
+step) whose record (agents, active inputs, births, population) is written to --out as JSON
+with the algorithmic bytes of its policy and k_prepare_p launches (bench.policy_bytes,
+bench.hh_bytes).  Meant to run under
+    ncu --set full -k regex:"k_policy_half|k_prepare_p|k_post" --launch-skip 2W --launch-count 3
+(launches: one k_prepare_p at start, W x (policy, k_post), then the timed policy and
+k_prepare_p), which captures the graph path's last k_post and the described step's policy
+and P rows."""
 import argparse
 import json
 import os
@@ -22,12 +26,14 @@ world = sim.World(wc, device=0)
 world.step(a.warmup)
 world.synchronize()
 t = world.t
-world.step(1)
+world.step_timed()
 world.synchronize()
 rec = world.step_log(t, 1)[0, 0]
 agents, nnz, births = int(rec["agents_at_start"]), int(rec["obs_nnz"]), int(rec["births"])
 out = {"workload": wc.name, "step": t, "agents": agents, "obs_nnz": nnz, "births": births,
+       "population": int(rec["population"]),
        "policy_algorithmic_bytes": bench.policy_bytes(wc, agents, nnz),
+       "hh_algorithmic_bytes": bench.hh_bytes(wc, int(rec["population"])),
        "step_algorithmic_bytes": bench.step_bytes(wc, agents, nnz, births)}
 json.dump(out, open(a.out, "w"), indent=1)
 print(json.dumps(out))
