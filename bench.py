@@ -196,6 +196,15 @@ def hh_bytes(wc, agents: int) -> int:
     return agents * (4 * (4 * Hd * Hd + 4 * Hd) + 4 * Hd + 4 * 4 * Hd)
 
 
+def post_bytes(wc, agents: int, births: int) -> int:
+    """Algorithmic bytes of the cooperative k_post launch: (split) the P rows of the agents
+    alive at the step's start (hh_bytes), the R and O bit planes read and written (H*W/2 B),
+    the mutation (parent's P weights read, child's written: 8P per birth) and 64 B of
+    per-agent dynamics state (move record, energy/age/repr read and written, list entry)."""
+    hh = hh_bytes(wc, agents) if split_policy(wc) else 0
+    return hh + wc.rows * wc.cols // 2 + births * 8 * wc.n_params + 64 * agents
+
+
 def step_bytes(wc, agents: int, nnz: int, births: int) -> int:
     """Whole-step algorithmic bytes: the policy's and (split) the P rows' bytes + the R and
     O bit planes read and written (H*W/2 B) + 8P per birth (parent read, child written)."""
@@ -286,8 +295,18 @@ def run_ours(args, rank, world_size, local_rank):
                 ssum += tm["step_ms"]
             log2 = world.step_log(t0, K)
             replay_identical = bool(np.array_equal(log2, log))
+            # the graph path's own two kernels, launched directly with events between them
+            world.set_state(snap)
+            gsum = np.zeros(2)
+            for k in range(K):
+                if not args.no_flush:
+                    flush_l2()
+                tg = world.step_graph_timed()
+                gsum += (tg["policy"], tg["post"])
+            log3 = world.step_log(t0, K)
             kern = {"kernel_ms_total": dict(zip(sim.KERNEL_NAMES, ksum.tolist())), "step_ms_total": ssum,
-                    "replay_identical": replay_identical}
+                    "replay_identical": replay_identical and bool(np.array_equal(log3, log)),
+                    "graph_kernel_ms_total": {"policy": gsum[0], "post": gsum[1]}}
 
         # -- e2e through the public API from pinned host buffers
         e2e = None
@@ -355,22 +374,30 @@ def run_ours(args, rank, world_size, local_rank):
         if kern is not None:
             ks = kern["kernel_ms_total"]
             sb = step_bytes(wc, agents, nnz, births)
-            # the two streaming kernels; the roofline line is the one with the larger time
-            cands = {"policy": ("k_policy_half (observe + LSTM gates from P + argmax + move claim)",
-                                policy_bytes(wc, agents, nnz))}
+            # the graph path's two kernels (events around each, same launches as the graph);
+            # the roofline line is the one with the larger time.  The instrumented replay's
+            # standalone P-row kernel (k_prepare_p) is reported beside them.
+            gk = kern["graph_kernel_ms_total"]
+            gstep = gk["policy"] + gk["post"]
+            cands = {
+                "policy": ("k_policy_half (observe + LSTM gates from P + argmax + move claim)",
+                           policy_bytes(wc, agents, nnz), gk["policy"], gstep),
+                "post": ("k_post (move/consume/physiology/death, birth claims + rank + placement, regrowth, "
+                         "mutation; P rows of the next step on 4 warps per block)",
+                         post_bytes(wc, agents, births), gk["post"], gstep)}
             if ks["hh"] > 0:
-                cands["hh"] = ("k_prepare_p (P = W_hh h + b of the next step's agents; inside k_post in graph mode)",
-                               hh_bytes(wc, int(log["population"].sum())))
+                cands["hh"] = ("k_prepare_p (standalone P rows in the instrumented replay; inside k_post in graph mode)",
+                               hh_bytes(wc, int(log["population"].sum())), ks["hh"], kern["step_ms_total"])
             rl = {}
-            for kname, (desc, byt) in cands.items():
-                achieved = byt / (ks[kname] / 1e3) / 1e9
+            for kname, (desc, byt, ms, step_ms_tot) in cands.items():
+                achieved = byt / (ms / 1e3) / 1e9
                 ratio, ratio_src = traffic_ratio(kname)
                 rl[kname] = {
                     "kernel": desc, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": ratio * byt / K if ratio else None,
-                    "traffic_source": ratio_src, "bytes_per_launch": byt / K, "launch_ms": ks[kname] / K,
-                    "peak_source": peak_src, "share_of_step": ks[kname] / kern["step_ms_total"]}
-            dom = max(rl, key=lambda k_: rl[k_]["launch_ms"])
+                    "traffic_source": ratio_src, "bytes_per_launch": byt / K, "launch_ms": ms / K,
+                    "peak_source": peak_src, "share_of_step": ms / step_ms_tot}
+            dom = max(("policy", "post"), key=lambda k_: rl[k_]["launch_ms"])
             result["roofline"] = rl[dom]
             result["kernels_roofline"] = rl
             result["step_roofline"] = {"bytes_per_step": sb / K, "achieved_GBps": sb / (max_ms / 1e3) / 1e9,
@@ -378,6 +405,7 @@ def run_ours(args, rank, world_size, local_rank):
                                        "dense_equiv_GBps": step_bytes(wc, agents, agents * wc.n_inputs, births)
                                        / (max_ms / 1e3) / 1e9}
             result["kernel_ms_per_step"] = {k: v / K for k, v in ks.items()}
+            result["graph_kernel_ms_per_step"] = {k: v / K for k, v in kern["graph_kernel_ms_total"].items()}
             result["replay_identical"] = kern["replay_identical"]
         if e2e is not None:
             result["e2e"] = e2e
@@ -390,7 +418,7 @@ def traffic_ratio(kname="policy"):
     (profiles/*_ncu_summary.json, tools/ncu_summary.py); the roofline's `traffic` is this
     ratio times the bench's algorithmic bytes per launch (the captured launch is one step of
     the same workload, not the bench's own launches)."""
-    tag = {"policy": "k_policy", "hh": "k_prepare_p"}[kname]
+    tag = {"policy": "k_policy", "hh": "k_prepare_p", "post": "k_post"}[kname]
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=os.path.getmtime)
     for f in reversed(files):

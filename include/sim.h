@@ -190,6 +190,11 @@ SIM_API sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, in
 SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
+/* Run ONE step exactly as graph mode does (the policy kernel, then the cooperative k_post
+ * kernel: same kernels, same parameters) launched directly with a CUDA event before,
+ * between and after them; synchronises.  out_ms[0] = policy, out_ms[1] = k_post
+ * (milliseconds).  SIM_E_STATE on a sharded handle. */
+SIM_API sim_status sim_step_graph_timed(sim_handle h, float out_ms[2]);
 /* Graph mode runs everything after the policy kernel as one cooperative kernel whose
  * phases are separated by grid barriers: move | birth candidates | birth rank (beside the
  * regrowth of step t+1 on the blocks without a world) | mutation.

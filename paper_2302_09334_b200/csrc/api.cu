@@ -569,6 +569,25 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
     return check_nonfinite(h);
 }
 
+sim_status sim_step_graph_timed(sim_handle h, float out_ms[2]) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!out_ms) return fail(SIM_E_INVALID, "invalid argument: out_ms (NULL)");
+    if (h->p.n_ranks > 1) return fail(SIM_E_STATE, "sharded handle: sim_step_graph_timed is not available");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    CK(h, ensure_regrown(h), "regrow");
+    CK(h, cudaEventRecord(h->ev[0], h->stream), "event");
+    CK(h, eco::launch_policy(h->p, h->lc, h->stream), "policy");
+    CK(h, cudaEventRecord(h->ev[1], h->stream), "event");
+    CK(h, eco::launch_post(h->p, h->lc, h->bar, h->stream), "post");
+    CK(h, cudaEventRecord(h->ev[2], h->stream), "event");
+    CK(h, cudaEventSynchronize(h->ev[2]), "event sync");
+    h->t += 1;
+    CK(h, cudaEventElapsedTime(&out_ms[0], h->ev[0], h->ev[1]), "elapsed");
+    CK(h, cudaEventElapsedTime(&out_ms[1], h->ev[1], h->ev[2]), "elapsed");
+    return check_nonfinite(h);
+}
+
 sim_status sim_synchronize(sim_handle h) {
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;

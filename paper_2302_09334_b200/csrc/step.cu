@@ -1247,6 +1247,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
     // unsharded: both parities' count, slot and cell of list position i load beside t (one
     // round trip instead of t -> count -> slot -> cell; entries past a count are stale, unused)
     int n_list = 0, slot = 0, cell_l = 0, n_ch = 0;
+    const int forced_on = in_range ? *p.forced_on : 0;  // loaded now, used by the epilogue
     if (!SHARD && in_range) {
         if (SPLIT) n_ch = *p.p_children;
         const size_t o0 = (size_t)w * p.S + i, o1 = ((size_t)p.n_worlds + w) * p.S + i;
@@ -1275,7 +1276,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             gs = (size_t)w * p.S + slot;
             Wl = p.weights + gs * (size_t)p.Pd + hl * 4;
         }
-#if ECO_POLICY_PREFETCH
+#if ECO_POLICY_PREFETCH && ECO_POLICY_PREFETCH != 2
         // the agent's contiguous W_hh | b | W_out | b_out block (17.7 KB at Hd = 32) streams into
         // L2 as one bulk prefetch: DRAM serves it sequentially, the ring then hits L2
         if (active && hl == 0) {
@@ -1379,6 +1380,13 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
         if (SPLIT) {
             // chunk 0 = P (or b), chunks 1.. = the active columns; R ticks per round from 0
             const int N1 = 1 + nnz;
+#if ECO_POLICY_PREFETCH == 2
+            // the columns past the first round: their 128-B lines into L2 now, so the
+            // later rounds hit L2 (lane hl takes lines hl, hl + 16, ... of chunks R..N1-1)
+            if (active)
+                for (int q = hl; q < 4 * (N1 - R); q += 16)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(Wl - hl * 4 + (int)cols[R - 1 + (q >> 2)] * HD * 4 + (q & 3) * 32));
+#endif
             const int Nw1 = __reduce_max_sync(FULL, active ? N1 : 0);
 #pragma unroll
             for (int q = 1; q < R; ++q) {
@@ -1485,7 +1493,7 @@ __global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
             bool bad = !isfinite(hn0) || !isfinite(cn0) || !isfinite(hn1) || !isfinite(cn1);
             if (hl == 0) {
                 PolicyCounters one;
-                agent_epilogue<SHARD>(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, one, bad);
+                agent_epilogue<SHARD>(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, forced_on, one, bad);
                 nnz_a = one.nnz;
                 tie_a = one.ties;
             }
@@ -1638,7 +1646,10 @@ constexpr int POST_THREADS = ECO_POST_THREADS;
 #ifndef ECO_HH_WARPS
 #define ECO_HH_WARPS 4  // split: the P warps of blocks 1.. (measured: 2..16 warps, depth 6..16)
 #endif
-constexpr int CLAIMS_BLOCK_MAX = 4 * POST_THREADS;
+#ifndef ECO_CLAIMS_MAX
+#define ECO_CLAIMS_MAX 1024  // measured: 1024 and 2048 beat 4096 at the population cap
+#endif
+constexpr int CLAIMS_BLOCK_MAX = ECO_CLAIMS_MAX;
 #ifndef ECO_HH_DEPTH
 #define ECO_HH_DEPTH 8  // split: 512-B chunks in flight per P context
 #endif

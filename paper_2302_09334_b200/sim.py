@@ -28,7 +28,7 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
             "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
-            "sim_set_record_mirror")
+            "sim_set_record_mirror", "sim_step_graph_timed")
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
@@ -116,6 +116,8 @@ def lib():
                 L.sim_set_record_mirror.argtypes = [H, ctypes.c_void_p, ctypes.c_int64]
             L.sim_get_totals.argtypes = [H, ctypes.POINTER(SimTotals)]
             L.sim_step_timed.argtypes = [H, ctypes.POINTER(SimStepTiming)]
+            if hasattr(L, "sim_step_graph_timed"):
+                L.sim_step_graph_timed.argtypes = [H, ctypes.c_void_p]
             L.sim_synchronize.argtypes = [H]
             L.sim_kernels_per_step.restype = ctypes.c_int32
             L.sim_get_phase_ns.argtypes = [H, ctypes.c_void_p, ctypes.c_int32]
@@ -275,6 +277,13 @@ class World:
         _check(lib().sim_step_timed(self._h, ctypes.byref(tm)))
         self._t += 1
         return {"step_ms": float(tm.step_ms), **{k: float(tm.kernel_ms[i]) for i, k in enumerate(KERNEL_NAMES)}}
+
+    def step_graph_timed(self) -> dict:
+        """One step through graph mode's two kernels, each bracketed by CUDA events (ms)."""
+        out = (ctypes.c_float * 2)()
+        _check(lib().sim_step_graph_timed(self._h, out))
+        self._t += 1
+        return {"policy": float(out[0]), "post": float(out[1])}
 
     def synchronize(self):
         _check(lib().sim_synchronize(self._h))

@@ -346,6 +346,37 @@ def test_graph_path_equals_instrumented_path_long_run():
     world.destroy()
 
 
+@pytest.mark.gpu
+def test_graph_timed_step_equals_graph_step():
+    """sim_step_graph_timed (the bench's per-kernel timing of the graph path) launches the
+    graph's own two kernels directly: same trajectory and state as sim_step, and interleaving
+    the two modes is seamless (the P rows and children counts carry over)."""
+    wc = workloads.paper_scale()
+    K = 300
+    world = sim.World(wc, log_capacity=K + 16)
+    world.step(5)
+    snap = world.get_state()
+    t0 = world.t
+    world.step(K)
+    log_g = world.step_log(t0, K)[:, 0]
+    sg = world.get_state(("alive", "cell", "energy", "h", "c", "weights"))
+    world.set_state(snap)
+    for k in range(K):
+        if k % 3 == 2:
+            world.step(1)
+        else:
+            ms = world.step_graph_timed()
+            assert ms["policy"] > 0 and ms["post"] > 0
+    log_t = world.step_log(t0, K)[:, 0]
+    bad = [k for k in range(K) if log_g[k] != log_t[k]]
+    assert not bad, f"first differing step {t0 + bad[0]}"
+    st = world.get_state(("alive", "cell", "energy", "h", "c", "weights"))
+    for f in sg:
+        if f != "t":
+            assert np.array_equal(sg[f], st[f]), f
+    world.destroy()
+
+
 def _sharded_step(ranks):
     """One agent-sharded step of all ranks of a world on this GPU: the ranks' policies, the
     SUM-combine of their exchange buffers (what an NCCL allreduce does across GPUs; here the

@@ -1,4 +1,4 @@
-"""Timeline of one k_policy_ring launch (diagnostic build with -DECO_POLICY_TRACE).
+"""Timeline of one k_policy_half launch (graph path) (diagnostic build with -DECO_POLICY_TRACE).
 
 Per live agent the kernel records (start, mask ready, end, nnz) on the global timer; this
 prints the distribution of those times relative to the first agent's start."""
@@ -19,11 +19,21 @@ import workloads  # noqa: E402
 from paper_2302_09334_b200 import sim  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 3000
+flush = "--flush" in sys.argv  # L2 flushed before each traced step, as bench.py
 world = sim.World(workloads.paper_scale(), device=0)
 world.step(W)
 world.synchronize()
+if flush:
+    import torch
+    import bench
+    fb = torch.empty(bench.FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    fr = torch.ones(bench.FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 for rep in range(3):
     world.phase_ns(reset=True)
+    if flush:
+        fb.zero_()
+        fr.sum()
+        torch.cuda.synchronize()
     world.step(1)
     world.synchronize()
     out = np.zeros(16 + 32768, np.int64)

@@ -59,7 +59,8 @@ if __name__ == "__main__":
         st = json.load(open(a.step))
         summary["step"] = st
         for rec in launches:
-            key = "policy" if "k_policy" in rec["kernel"] else "hh" if "k_prepare_p" in rec["kernel"] else None
+            kn = rec["kernel"]
+            key = "policy" if "k_policy" in kn else "hh" if "k_prepare_p" in kn else "post" if "k_post" in kn else None
             if key and f"{key}_algorithmic_bytes" in st:
                 traffic = rec.get("dram_read_bytes", 0) + rec.get("dram_write_bytes", 0)
                 alg = st[f"{key}_algorithmic_bytes"]

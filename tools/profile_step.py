@@ -29,11 +29,14 @@ t = world.t
 world.step_timed()
 world.synchronize()
 rec = world.step_log(t, 1)[0, 0]
+prev = world.step_log(t - 1, 1)[0, 0]  # the step of the captured k_post (the last graph step)
 agents, nnz, births = int(rec["agents_at_start"]), int(rec["obs_nnz"]), int(rec["births"])
 out = {"workload": wc.name, "step": t, "agents": agents, "obs_nnz": nnz, "births": births,
        "population": int(rec["population"]),
        "policy_algorithmic_bytes": bench.policy_bytes(wc, agents, nnz),
        "hh_algorithmic_bytes": bench.hh_bytes(wc, int(rec["population"])),
+       "post_algorithmic_bytes": bench.post_bytes(wc, int(prev["agents_at_start"]), int(prev["births"])),
+       "post_step": t - 1,
        "step_algorithmic_bytes": bench.step_bytes(wc, agents, nnz, births)}
 json.dump(out, open(a.out, "w"), indent=1)
 print(json.dumps(out))
