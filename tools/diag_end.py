@@ -23,6 +23,6 @@ world.step(K)
 e1.record(s)
 world.synchronize()
 ph = {k: v / K / 1e3 for k, v in world.phase_ns().items()}
-print(os.environ.get("ECO_LIBSIM_OVERRIDE"), {"step_us": e0.elapsed_time(e1) / K * 1e3,
+print(os.environ.get("ECO_LIBSIM_OVERRIDE"), {"step_us": e0.elapsed_time(e1) / K * 1e3, "r6": ph["reserved6"], "r7": ph["reserved7"],
       "p_warps_end_us": ph["reserved4"], "dyn_end_us": ph["reserved5"],
       **{k: round(v, 2) for k, v in ph.items() if not k.startswith("reserved")}})
