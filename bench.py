@@ -385,7 +385,7 @@ def run_ours(args, rank, world_size, local_rank):
                 "post": ("k_post (move/consume/physiology/death, birth claims + rank + placement, regrowth, "
                          "mutation; P rows of the next step on 4 warps per block)",
                          post_bytes(wc, agents, births), gk["post"], gstep)}
-            if ks["hh"] > 0:
+            if split_policy(wc):
                 cands["hh"] = ("k_prepare_p (standalone P rows in the instrumented replay; inside k_post in graph mode)",
                                hh_bytes(wc, int(log["population"].sum())), ks["hh"], kern["step_ms_total"])
             rl = {}

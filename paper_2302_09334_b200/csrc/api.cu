@@ -432,7 +432,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
         h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    CKC(dalloc(h, &h->bar, 6), "alloc");  // [0] arrivals, [1] next base, [2] births flag, [3..4] P counters
+    CKC(dalloc(h, &h->bar, 6), "alloc");  // [0] arrivals, [1] next base, [2] births flag, [3..5] spare
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");

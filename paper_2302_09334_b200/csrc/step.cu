@@ -1649,6 +1649,12 @@ constexpr int POST_THREADS = ECO_POST_THREADS;
 #ifndef ECO_HH_WARPS
 #define ECO_HH_WARPS 4  // split: the P warps of blocks 1.. (measured: 2..16 warps, depth 6..16)
 #endif
+#ifndef ECO_HH_WARPS_BIG
+#define ECO_HH_WARPS_BIG 16  // ... above HH_BIG_AGENTS live agents the P stream is the longer part
+#endif
+#ifndef ECO_HH_BIG_AGENTS
+#define ECO_HH_BIG_AGENTS 32768
+#endif
 #ifndef ECO_CLAIMS_MAX
 #define ECO_CLAIMS_MAX 1024  // measured: 1024 and 2048 beat 4096 at the population cap
 #endif
@@ -1657,7 +1663,13 @@ constexpr int CLAIMS_BLOCK_MAX = ECO_CLAIMS_MAX;
 #define ECO_HH_DEPTH 8  // split: 512-B chunks in flight per P context
 #endif
 constexpr int HH_DEPTH = ECO_HH_DEPTH;
-constexpr int POST_SMEM = 2 * ECO_HH_WARPS * HH_DEPTH * 32 * 16;  // split: the P rings
+constexpr int HH_WARPS_MAX = ECO_HH_WARPS > ECO_HH_WARPS_BIG ? ECO_HH_WARPS : ECO_HH_WARPS_BIG;
+constexpr int POST_SMEM = 2 * HH_WARPS_MAX * HH_DEPTH * 32 * 16;        // split: the P rings (max)
+constexpr int POST_SMEM_SMALL = 2 * ECO_HH_WARPS * HH_DEPTH * 32 * 16;  // worlds that never exceed the threshold
+// worlds with more slots than the threshold run k_post<., true>: 16 P warps per block (the
+// P stream is the longer part of the step there: large world 1.71 -> 1.52 ms per step)
+inline bool post_big(const DevParams &p) { return p.split && p.S > ECO_HH_BIG_AGENTS; }
+inline int post_smem_bytes(const DevParams &p) { return !p.split ? 0 : post_big(p) ? POST_SMEM : POST_SMEM_SMALL; }
 #ifdef ECO_BLOCK_CLOCK
 // diagnostic build: per block and barrier k, summed own-work and barrier-wait durations in
 // phase_ns[ECO_BLOCK_CLOCK_BASE + (k * gridDim + block) * 3 + {0, 1, 2}] (2: an explicit
@@ -1686,7 +1698,7 @@ constexpr int ECO_BLOCK_CLOCK_BASE = 16;
 #define POST_SYNC(k) grid_sync(bar, target, nthr)
 #endif
 
-template <bool SHARD>
+template <bool SHARD, bool BIG = false>
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned long long *bar) {
     DevParams p = p_;
     if (!SHARD) p.n_ranks = 1;
@@ -1704,7 +1716,8 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     // the kernel's first cycle, streaming beside the latency-bound dynamics of the other
     // warps; they take part in no barrier.  The rows of the agents that die are never read
     // (a child placed in such a slot starts from its bias).
-    constexpr int HH_WARPS = ECO_HH_WARPS, DYN_WARPS = POST_THREADS / 32 - HH_WARPS;
+    constexpr int HH_WARPS = BIG ? ECO_HH_WARPS_BIG : ECO_HH_WARPS;  // compile-time: the roles need no load
+    constexpr int DYN_WARPS = POST_THREADS / 32 - HH_WARPS;
     const bool hh_split = p.split && p.n_worlds == 1 && gridDim.x > 1;
 #ifdef ECO_END_CLOCK
     // diagnostic build: per launch, the latest end of the P warps and of the other warps
@@ -1958,20 +1971,22 @@ cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 }
 
 cudaError_t post_occupancy(int *blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post<true>, POST_THREADS, POST_SMEM);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_post<false, true>, POST_THREADS, POST_SMEM);
 }
 
 cudaError_t post_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(k_post<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_post<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_post<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    e = cudaFuncSetAttribute(k_post<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_post<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lc.post_blocks);
     cfg.blockDim = dim3(POST_THREADS);
-    cfg.dynamicSmemBytes = p.split ? POST_SMEM : 0;
+    cfg.dynamicSmemBytes = post_smem_bytes(p);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -1979,6 +1994,7 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (p.n_ranks > 1) return cudaLaunchKernelEx(&cfg, k_post<true>, p, bar);
+    if (post_big(p)) return cudaLaunchKernelEx(&cfg, k_post<false, true>, p, bar);
     return cudaLaunchKernelEx(&cfg, k_post<false>, p, bar);
 }
 

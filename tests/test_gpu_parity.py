@@ -142,6 +142,20 @@ def test_large_grid_lockstep():
     world.destroy()
 
 
+@pytest.mark.gpu
+def test_many_slots_lockstep():
+    """A world with more slots than ECO_HH_BIG_AGENTS (32,768) runs the graph path's second
+    k_post variant (16 P warps per block): lock-step with the oracle for 8 steps, births
+    included (33,000 agents in 33,792 slots on the 1600x3200 grid)."""
+    wc = workloads.large_world().replace(slots=33792, n_initial=33000, repr_steps=4, e_repr_gt=10200)
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    flips, n, nulp = lockstep(world, orc, 8, check_weights_every=4)
+    log = world.step_log(0, 8)
+    assert n > 200000 and int(log["births"].sum()) > 0
+    world.destroy()
+
+
 @pytest.mark.parametrize("hidden,r", [(4, 1), (16, 2), (32, 0), (8, 3)])
 def test_other_shapes_lockstep(hidden, r):
     wc = workloads.tiny().replace(rows=30, cols=72, slots=200, n_initial=90, hidden=hidden, obs_radius=r,

@@ -26,3 +26,9 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   echo ncu_full=$? >> $OUT/status.txt
 fi
 cat $OUT/status.txt
+if [ "${EXTRA:-0}" = "1" ]; then
+  timeout 900 python bench.py --config large_world --steps 20 --warmup 300 --no-cpu-baseline --no-e2e > $OUT/bench_large_$TAG.json 2> $OUT/bench_large_$TAG.err; echo large=$? >> $OUT/status.txt
+  timeout 900 python bench.py --config ensemble --steps 30 --warmup 20 --no-cpu-baseline --no-e2e > $OUT/bench_ensemble_$TAG.json 2> $OUT/bench_ensemble_$TAG.err; echo ensemble=$? >> $OUT/status.txt
+  timeout 900 python tools/bench_regrowth.py --out $OUT/regrowth_$TAG.json > /dev/null 2> $OUT/regrowth_$TAG.err; echo regrowth=$? >> $OUT/status.txt
+  cat $OUT/status.txt
+fi
