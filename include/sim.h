@@ -70,7 +70,7 @@ typedef struct {
     double f_value[4];      /* f(class): {0, .01, .05, .1}                               */
     double lat_top, lat_bottom; /* climate lat(0), lat(H-1), linear in y/(H-1)         */
     double spontaneous;     /* constant spontaneous growth probability c                */
-    int32_t slots, n_initial; /* S agent slots (population cap), N0 initial agents       */
+    int32_t slots, n_initial; /* S agent slots (population cap, <= 2^24 - 1), N0 initial agents */
     int32_t obs_radius;     /* r: window (2r+1)^2, 0..3                                   */
     int32_t hidden;         /* LSTM hidden size Hd in {4, 8, 16, 32}                      */
     int32_t n_actions;      /* must be 5 (stay, N, S, E, W)                               */

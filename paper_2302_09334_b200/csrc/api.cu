@@ -54,7 +54,8 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
         if (!prob(cfg->f_value[c])) return fail(SIM_E_INVALID, "invalid field: f_value");
     if (!prob(cfg->lat_top) || !prob(cfg->lat_bottom)) return fail(SIM_E_INVALID, "invalid field: lat");
     if (!prob(cfg->spontaneous)) return fail(SIM_E_INVALID, "invalid field: spontaneous");
-    if (cfg->slots < 0) return fail(SIM_E_INVALID, "invalid field: slots");
+    // (<= 2^24 - 1: k_post carries a step's birth count in 24 bits of its release flag)
+    if (cfg->slots < 0 || cfg->slots > 0xFFFFFF) return fail(SIM_E_INVALID, "invalid field: slots");
     if (cfg->n_initial < 0 || cfg->n_initial > cfg->slots) return fail(SIM_E_INVALID, "invalid field: n_initial");
     if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return fail(SIM_E_INVALID, "invalid field: obs_radius (0..3)");
     if (!(cfg->hidden == 4 || cfg->hidden == 8 || cfg->hidden == 16 || cfg->hidden == 32))

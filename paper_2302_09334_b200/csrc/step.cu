@@ -1826,7 +1826,8 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             const RankCounts k = rank_counts(p, 0, T);
             rank_publish<POST_THREADS>(p, 0, T, k, scratch, s_free, s_bcell, s_par);
             if (threadIdx.x == 0) {
-                const unsigned long long v = target + 1;  // unique per launch (monotonic)
+                // unique per launch (monotonic), with the number of births in the low 24 bits
+                const unsigned long long v = ((target + 1) << 24) | (unsigned long long)k.n_place;
                 asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
             }
             lap(2);
@@ -1848,14 +1849,16 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             // one item of a stale birth entry, no stores)
             if (wid >= 1 && wid <= 4) mutate_world_nl(ma, T, p.seeds[0], 1, lane, (size_t)1 << 30, 1);
 #endif
+            __shared__ int s_nb;
             if (threadIdx.x == 0) {
                 unsigned long long cur;
                 do {
                     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(flag) : "memory");
-                } while (cur < target + 1);
+                } while (cur < ((target + 1) << 24));
+                s_nb = (int)(cur & 0xFFFFFFull);  // the births, carried by the flag itself
             }
             asm volatile("bar.sync 1, %0;" ::"r"(gw * 32) : "memory");
-            const int n_b = *reinterpret_cast<volatile int32_t *>(p.n_births);
+            const int n_b = s_nb;
 #if ECO_MUT_WARM
             if (n_b > 0) mutate_world_nl(ma, T, p.seeds[0], n_b, btid, bthr, 0);
 #else
