@@ -206,10 +206,12 @@ def post_bytes(wc, agents: int, births: int) -> int:
 
 
 def step_bytes(wc, agents: int, nnz: int, births: int) -> int:
-    """Whole-step algorithmic bytes: the policy's and (split) the P rows' bytes + the R and
-    O bit planes read and written (H*W/2 B) + 8P per birth (parent read, child written)."""
-    hh = hh_bytes(wc, agents) if split_policy(wc) else 0
-    return policy_bytes(wc, agents, nnz) + hh + wc.rows * wc.cols // 2 + births * 8 * wc.n_params
+    """Whole-step algorithmic bytes: B_agent per live agent (the unsplit
+    policy's bytes: active W_ih columns, W_hh, b, W_out, b_out, h and c, 32 B of SoA) + the R
+    and O bit planes read and written (H*W/2 B) + 8P per birth (parent read, child written).
+    The split design's extra P-row traffic (written by k_post, read by the policy: ~1.2 KB
+    per agent) is not counted: it is this implementation's cost, not the method's."""
+    return policy_bytes(wc, agents, nnz, split=False) + wc.rows * wc.cols // 2 + births * 8 * wc.n_params
 
 
 # ------------------------------------------------------------------------ our arm

@@ -508,3 +508,37 @@ def test_nonfinite_state_reported():
         world.step(1)
         world.synchronize()
     assert ei.value.status == sim.SIM_E_NONFINITE
+
+
+def test_large_world_full_size_graph_equals_instrumented_and_invariants():
+    """BASELINE configs[3] at its full size (1600x3200, 262,144 slots, 64,000 agents) in the
+    launch configuration bench.py times (the graph path, k_post with 16 P warps per block):
+    two identically created worlds, one stepped through the graph and one through the
+    instrumented phase kernels, agree exactly (records and integer state, h and c), and the
+    properties that hold at any size hold (unique in-range cells of live agents, the
+    population and resource balance of every record, the final resource plane's popcount)."""
+    wc = workloads.large_world()
+    K = 32  # the first births come after T_repr = 20 steps above the energy threshold
+    a, b = sim.World(wc, log_capacity=64), sim.World(wc, log_capacity=64)
+    a.step(K)
+    for _ in range(K):
+        b.step_timed()
+    la, lb = a.step_log(0, K)[:, 0], b.step_log(0, K)[:, 0]
+    assert np.array_equal(la, lb)
+    fields = ("alive", "cell", "energy", "age", "repr", "h", "c", "resources")
+    sa, sb = a.get_state(fields), b.get_state(fields)
+    for f in fields:
+        assert np.array_equal(sa[f], sb[f]), f
+    alive = sa["alive"][0] == 1
+    cells = sa["cell"][0][alive]
+    assert cells.min() >= 0 and cells.max() < wc.rows * wc.cols and np.unique(cells).size == cells.size
+    assert int(alive.sum()) == int(la["population"][-1])
+    for k in range(1, K):
+        assert la["agents_at_start"][k] == la["population"][k - 1]
+        assert la["resources"][k] == la["resources"][k - 1] + la["grown"][k] - la["eaten"][k]
+    assert la["population"][-1] == la["agents_at_start"][-1] - la["deaths_energy"][-1] - la["deaths_age"][-1] \
+        + la["births"][-1]
+    assert int(sa["resources"][0].astype(np.int64).sum()) == int(la["resources"][-1])
+    assert int(la["births"].sum()) > 0
+    a.destroy()
+    b.destroy()
