@@ -1120,13 +1120,24 @@ __global__ void __launch_bounds__(RING_WARPS * 32, STREAM_BPS) k_policy_stream(D
 // h+16 (two float4 gate accumulators) and copies/reads their 2 x 16 B of every 512-B chunk.
 // Ring: HALF_DEPTH chunks per agent (3 KB) in flight; 16 agents per block interleaved over
 // the blocks (agent v = a * gridDim + block).  Column indices are compacted to bytes.
-constexpr int HALF_AGENTS = 16;  // per block (8 warps)
+#ifndef ECO_HALF_FULLGRID
+#define ECO_HALF_FULLGRID 1  // 4 blocks on every SM (592 at 8 warps): 48.0 -> 47.4 us per step
+#endif
+#ifndef ECO_HALF_WARPS
+#define ECO_HALF_WARPS 8
+#endif
+constexpr int HALF_WARPS = ECO_HALF_WARPS;
+constexpr int HALF_THREADS = HALF_WARPS * 32;
+constexpr int HALF_AGENTS = 2 * HALF_WARPS;  // per block (16 at 8 warps)
 #ifndef ECO_HALF_DEPTH
 #define ECO_HALF_DEPTH 6
 #endif
 constexpr int HALF_DEPTH = ECO_HALF_DEPTH;
-constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6
-constexpr int HALF_BPS = HALF_DEPTH <= 6 ? 4 : HALF_DEPTH <= 8 ? 3 : 2;  // blocks per SM the smem allows
+constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6 and 8 warps
+// blocks per SM the smem allows (32 resident warps at depth <= 6)
+constexpr int HALF_BPS = (HALF_DEPTH <= 6 ? 32 : HALF_DEPTH <= 8 ? 24 : 16) / HALF_WARPS > 0
+                             ? (HALF_DEPTH <= 6 ? 32 : HALF_DEPTH <= 8 ? 24 : 16) / HALF_WARPS
+                             : 1;
 
 // P[slot] = W_hh h + b (Hd = 32) for list positions [0, n) of `list`, one agent per
 // half-warp context (ctx of nctx; both halves of a warp call it together), through the same
@@ -1200,7 +1211,7 @@ __device__ __forceinline__ void hh_pass(const DevParams &p, const int32_t *list,
 
 // P of every live agent of step t (after create / set_state / instrumented steps), one
 // half-warp per agent; no children pending afterwards.
-__global__ void __launch_bounds__(256, HALF_BPS) k_prepare_p(DevParams p) {
+__global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p(DevParams p) {
     extern __shared__ float4 half_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ag = warp * 2 + (lane >> 4);
@@ -1223,7 +1234,7 @@ __device__ __forceinline__ void timeline_mark(const DevParams &p, int k, unsigne
 // SHARD = false compiles the sharding branches out, so the unsharded kernels keep their code
 // (a local DevParams copy to fold n_ranks costs 3 us in this kernel: measured).
 template <bool SHARD, bool SPLIT = false>
-__global__ void __launch_bounds__(256, HALF_BPS) k_policy_half(DevParams p) {
+__global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParams p) {
     constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ float4 half_smem[];  // [HALF_AGENTS][R][32 units]
@@ -1545,7 +1556,7 @@ cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
         case 32:
             return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_stream, RING_WARPS * 32, RING_SMEM);
 #else
-        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_half<false>, 256, HALF_SMEM);
+        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_half<false>, HALF_THREADS, HALF_SMEM);
 #endif
         default: return cudaErrorInvalidValue;
     }
@@ -1587,9 +1598,12 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
             const long hk = ((long)p.n_worlds * plane_words(p) + 255) / 256;
             const long hk_cap = (long)lc.sms * 4;
             if (blocks < (hk < hk_cap ? hk : hk_cap)) blocks = hk < hk_cap ? hk : hk_cap;
-            if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
-            else if (p.split) k_policy_half<false, true><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
-            else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), 256, HALF_SMEM, s>>>(p);
+#if ECO_HALF_FULLGRID
+            if (blocks < (long)lc.sms * HALF_BPS) blocks = (long)lc.sms * HALF_BPS;  // every SM the same
+#endif
+            if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
+            else if (p.split) k_policy_half<false, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
+            else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             break;
         }
 #else
@@ -1934,7 +1948,7 @@ bool policy_supports_shard() { return ECO_POLICY_TMA == 0; }  // k_policy_half
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (!p.split) return cudaSuccess;
     const unsigned blocks = (unsigned)((p.S + HALF_AGENTS - 1) / HALF_AGENTS);
-    k_prepare_p<<<blocks > 0 ? blocks : 1, 256, HALF_SMEM, s>>>(p);
+    k_prepare_p<<<blocks > 0 ? blocks : 1, HALF_THREADS, HALF_SMEM, s>>>(p);
     return cudaGetLastError();
 }
 
