@@ -118,6 +118,10 @@ typedef struct {
     int64_t near_ties;         /* live agents with top-1 minus top-2 logit margin < 1e-4  */
     int64_t obs_nnz;           /* sum over live agents of active (= 1) observation inputs:
                                   the W_ih columns the policy kernel must read            */
+    int64_t death_age_sum;     /* sum of the ages (after this step's increment) of the agents
+                                  that died this step: life expectancy over a window is the
+                                  windowed sum / windowed deaths (App. C; SPEC
+                                  metrics.life_expectancy)                                */
 } sim_step_record;
 
 /* Cumulative counters since create (or the last set_state), summed over worlds. */
@@ -188,6 +192,19 @@ SIM_API sim_status sim_get_step_log_async(sim_handle h, int64_t first, int64_t n
  * mirroring.  Non-mapped memory -> SIM_E_INVALID. */
 SIM_API sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t capacity);
 SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
+/* Movement histograms (Appendix C, "17 bins of the distance traveled"; SPEC
+ * metrics.movement_bin): windows of SIM_MOVE_WINDOW steps aligned to multiples of it from
+ * step 0; window k covers steps [50k, 50k+49].  An agent counts in window k iff it is alive
+ * from the start of step 50k to the end of step 50k+49 (its age grows by exactly 50: born or
+ * dead within the window excludes it); its bin is min(16, floor(d / 3)) for d the Manhattan
+ * distance between its cell at the start of step 50k and at the end of step 50k+49.
+ * out[i][w][b] (int32, caller-owned [n][n_worlds][17]) receives window first + i.  Windows
+ * must be complete (50(first+n) <= t) and among the last ceil(log_capacity / 50) windows;
+ * windows that began before the last sim_set_state (with t not a multiple of 50) hold 0.
+ * SIM_E_INVALID otherwise; synchronises. */
+#define SIM_MOVE_WINDOW 50
+#define SIM_MOVE_BINS 17
+SIM_API sim_status sim_get_move_hist(sim_handle h, int64_t first, int64_t n, int32_t *out);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
 /* Run ONE step exactly as graph mode does (the policy kernel, then the cooperative k_post

@@ -13,6 +13,15 @@
 using eco::DevParams;
 
 namespace {
+// movement-histogram windows kept: a power of two covering the step log
+inline int mv_windows(int log_cap) {
+    int c = 1;
+    while (c < log_cap / SIM_MOVE_WINDOW + 2) c <<= 1;
+    return c;
+}
+}  // namespace
+
+namespace {
 
 thread_local std::string g_last_error;
 
@@ -126,6 +135,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * 4 * 7;                    // alive lists [2], free, birth lists, mutation counters
     b += nw * S * 8 + S + S * 16 + S * 8;   // birth candidates, owners, by-slot move records, own lists
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
+    b += nw * S * 8 + nw * (size_t)mv_windows(d.log_cap) * SIM_MOVE_BINS * 4;  // movement metrics
     return b;
 }
 
@@ -371,6 +381,10 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.mrec, nw * S), "alloc");
     CKC(dalloc(h, &p.alive_list, 2 * nw * S), "alloc");
     CKC(dalloc(h, &p.list_cell, 2 * nw * S), "alloc");
+    p.mv_cap = mv_windows(d.log_cap);
+    CKC(dalloc(h, &p.mv_cell, nw * S), "alloc");
+    CKC(dalloc(h, &p.mv_inv, nw * S), "alloc");
+    CKC(dalloc(h, &p.mv_hist, nw * (size_t)p.mv_cap * SIM_MOVE_BINS), "alloc");
     CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
     CKC(dalloc(h, &p.n_win, nw), "alloc");
     CKC(dalloc(h, &p.free_list, nw * S), "alloc");
@@ -433,7 +447,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
         h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    CKC(dalloc(h, &h->bar, 6), "alloc");  // [0] arrivals, [1] next base, [2] births flag, [3..5] spare
+    CKC(dalloc(h, &h->bar, 6), "alloc");  // [0] arrivals, [1] next base, [2] births flag, [3..4] window-end counters, [5] spare
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");
@@ -786,6 +800,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     CK(h, eco::launch_set_owner(p, s), "owners");
     CK(h, cudaMemsetAsync(p.pol_ctr, 0, 2 * sizeof(unsigned long long), s), "memset");
+    CK(h, cudaMemsetAsync(h->bar + 3, 0, 2 * sizeof(unsigned long long), s), "memset");  // window-end counters
     h->regrown_ahead = false;
     h->p_ready = false;
     return sync(h);
@@ -872,6 +887,25 @@ sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset) {
                               cudaMemcpyDeviceToHost, h->stream),
            "phase clock");
     if (reset > 0) CK(h, cudaMemsetAsync(h->p.phase_ns, 0, PHASE_WORDS * 8, h->stream), "phase clock");
+    return sync(h);
+}
+
+sim_status sim_get_move_hist(sim_handle h, int64_t first, int64_t n, int32_t *out) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (n < 0 || (n > 0 && !out)) return fail(SIM_E_INVALID, "invalid argument: n/out");
+    const int64_t done = h->t / SIM_MOVE_WINDOW;  // complete windows
+    if (first < 0 || first + n > done || first < done - h->p.mv_cap)
+        return fail(SIM_E_INVALID, "invalid argument: windows [%lld, %lld) not kept (complete windows %lld, capacity %d)",
+                    (long long)first, (long long)(first + n), (long long)done, h->p.mv_cap);
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    const size_t nw = h->d.n_worlds;
+    for (int64_t i = 0; i < n; ++i)
+        for (size_t w = 0; w < nw; ++w)
+            CK(h, cudaMemcpyAsync(out + (i * nw + w) * SIM_MOVE_BINS,
+                                  h->p.mv_hist + (w * h->p.mv_cap + (size_t)((first + i) & (h->p.mv_cap - 1))) * SIM_MOVE_BINS,
+                                  SIM_MOVE_BINS * 4, cudaMemcpyDeviceToHost, h->stream), "move histogram");
     return sync(h);
 }
 

@@ -222,6 +222,48 @@ __device__ __forceinline__ AgentIter agent_at(const DevParams &p, long v) {
     return a;
 }
 
+// ------------------------------------------------- Appendix C movement metrics (NEXT-3)
+#ifndef ECO_METRICS
+#define ECO_METRICS 3  // bit 0: ages at death, bit 1: movement histograms (diagnostic switch)
+#endif
+// Each slot keeps (cell, inv) from the start of its current 50-step window, inv = age - 50k
+// for window k: an agent alive through window k has the same inv at the start of window k+1,
+// and nothing else does (a newborn's or a reused slot's inv is smaller), so no per-slot flag
+// has to be cleared when agents die or are born.  mv_pass runs at the end of window k (step
+// T = 50k+49, after the children of that step are placed, so every live slot is final):
+// every live slot whose inv is unchanged gets the bin of the Manhattan distance between the
+// two cells, and every live slot (a newborn too, at age 0) starts window k+1.
+constexpr int32_t MV_INVALID = -(1 << 29);
+__device__ __forceinline__ bool mv_window_end(int64_t T) { return (uint32_t)T % SIM_MOVE_WINDOW == SIM_MOVE_WINDOW - 1; }
+
+// Slots [lo, hi) of world w by `nthr` threads of one block (thread index tid; named barrier 1
+// over exactly those threads), counted in a shared histogram, then one global atomic per
+// non-empty bin (a grid-wide per-warp scheme serialises thousands of same-address atomics).
+__device__ __forceinline__ void mv_pass_part(const DevParams &p, int64_t T, int w, int lo, int hi, int tid, int nthr,
+                                             int *s_hist, int bar_id = 1) {
+    const uint32_t k = (uint32_t)T / SIM_MOVE_WINDOW;
+    for (int b = tid; b < SIM_MOVE_BINS; b += nthr) s_hist[b] = 0;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthr) : "memory");
+    for (int i = lo + tid; i < hi; i += nthr) {
+        const size_t gs = (size_t)w * p.S + i;
+        if (!p.alive[gs]) continue;
+        const int c1 = p.cell[gs];
+        const int32_t inv = p.age[gs] - SIM_MOVE_WINDOW * (int32_t)(k + 1);
+        if (p.mv_inv[gs] == inv) {
+            const int c0 = p.mv_cell[gs];
+            const int y0 = row_of(p, c0), y1 = row_of(p, c1);
+            const int d = abs(y1 - y0) + abs((c1 - y1 * p.W) - (c0 - y0 * p.W));
+            atomicAdd(s_hist + min(d / 3, SIM_MOVE_BINS - 1), 1);
+        }
+        p.mv_cell[gs] = c1;
+        p.mv_inv[gs] = inv;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthr) : "memory");
+    int32_t *hist = p.mv_hist + ((size_t)w * p.mv_cap + (size_t)(k & (p.mv_cap - 1))) * SIM_MOVE_BINS;
+    for (int b = tid; b < SIM_MOVE_BINS; b += nthr)
+        if (s_hist[b]) atomicAdd(hist + b, s_hist[b]);
+}
+
 // ----------------------------------------------------------------------- a4 move
 // An agent moves iff it holds the max key on its target (R14); every live agent eats the
 // resource under its final cell; fixed-point energy e += gain*ate - decay,
@@ -251,6 +293,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
         bool ate = false, died_e = false, died_a = false, survive = false, cand = false;
         int cand_cell = 0;
         int slot = 0;
+        int dage = 0;  // metrics: age at death
         if (active) {
             slot = mr.x;
             const size_t gs = (size_t)w * p.S + slot;
@@ -299,6 +342,9 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 p.alive[gs] = 0;
                 atomicAnd(word_ptr(O, p, cellv, bit), ~bit);
                 atomicAnd(p.alive_bits + (size_t)w * p.SW + (slot >> 5), ~(1u << (slot & 31)));
+#if ECO_METRICS & 1
+                dage = ag;
+#endif
             } else {
                 survive = true;
                 cand = p.n_worlds == 1 && p.repr[gs] >= p.repr_steps;
@@ -324,6 +370,14 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             }
             c0 = __shfl_sync(0xffffffffu, c0, 0);
             if (cand) p.cand[c0 + __popc(mc & ((1u << lane) - 1u))] = make_int2(slot, cand_cell);
+            // metrics: the deaths' ages, and at a window end the movement bins (warp sums)
+#if ECO_METRICS & 1
+            if (md | ma) {
+                const int dsum = __reduce_add_sync(0xffffffffu, dage);
+                if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->death_age_sum), (unsigned long long)dsum);
+            }
+#endif
+
             pos0 = __shfl_sync(0xffffffffu, pos0, 0);
             if (survive) {
                 const int q = pos0 + __popc(m & ((1u << lane) - 1u));
@@ -340,6 +394,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             }
         } else {
             sim_step_record *rec = record_of(p, t, w);
+            if (dage) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->death_age_sum), (unsigned long long)dage);
             if (ate) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), 1ull);
             if (died_e) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), 1ull);
             if (died_a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), 1ull);

@@ -75,6 +75,11 @@ struct DevParams {
     // columns.  Children (the last *p_children list positions) start from their bias.
     int32_t split;
     float *Pbuf;                 // [S][Hd*4] device order [k][4], like b
+    // movement-histogram metrics (sim.h: sim_get_move_hist): each slot's cell and age at the
+    // start of the current 50-step window, and the per-window histograms (a ring)
+    int32_t *mv_cell, *mv_inv;   // [n_worlds][S]: cell and age - 50 k at the start of window k
+    int32_t *mv_hist;            // [n_worlds][mv_cap][17]
+    int mv_cap;                  // windows kept (a power of two)
     int32_t *p_children;         // list positions at the end of step t's list without a P row
     int2 *cand;                  // [n_worlds][S] single world: this step's eligible parents (slot, cell)
     int32_t *n_cand;             // [n_worlds] their count

@@ -191,6 +191,10 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
         sim_step_record *nxt = record_of(p, tw + 1, (int)w);
         *nxt = sim_step_record{};
         nxt->t = tw + 1;
+        if (tw % SIM_MOVE_WINDOW == SIM_MOVE_WINDOW - 1) {  // this step ends window tw/50: its bins from 0
+            int32_t *hist = p.mv_hist + ((size_t)w * p.mv_cap + (size_t)((tw / SIM_MOVE_WINDOW) & (p.mv_cap - 1))) * SIM_MOVE_BINS;
+            for (int b = 0; b < SIM_MOVE_BINS; ++b) hist[b] = 0;
+        }
     }
 }
 
@@ -1629,6 +1633,12 @@ __global__ void __launch_bounds__(256) k_move(DevParams p) {
     move_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
+__global__ void __launch_bounds__(256) k_mv_pass(DevParams p) {  // one block per world, after the rank
+    __shared__ int s_mv[SIM_MOVE_BINS];
+    const int64_t T = p.t[blockIdx.x] - 1;  // the rank advanced t
+    if (mv_window_end(T)) mv_pass_part(p, T, blockIdx.x, 0, p.S, threadIdx.x, blockDim.x, s_mv);
+}
+
 __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
     birth_claim_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
@@ -1718,6 +1728,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     if (!SHARD) p.n_ranks = 1;
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
+    __shared__ int s_mv[SIM_MOVE_BINS];  // a window end's movement histogram of this block
     extern __shared__ float4 post_smem[];  // split: the P rings, 2 HH_WARPS contexts x HH_DEPTH
     unsigned long long target = grid_sync_base(bar);
     const int64_t T = p.t[0];  // the step this launch completes (all worlds share t)
@@ -1847,6 +1858,11 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             lap(2);
             rank_place<POST_THREADS>(p, 0, T, k, s_free, s_bcell, s_par);
             if (threadIdx.x == 0) *p.p_children = p.split ? k.n_place : 0;  // the new children have no P row
+#if ECO_METRICS & 2
+            // the end of a movement window: block 0, idle after placing the children, closes it
+            // (every live agent of step T+1 is final here; off the critical path)
+            if (mv_window_end(T)) mv_pass_part(p, T, 0, 0, p.S, threadIdx.x, blockDim.x, s_mv);
+#endif
             if (gridDim.x == 1) mutate_world(p, 0, T, k.n_place, threadIdx.x, blockDim.x);  // no other block
         } else {
             const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
@@ -1892,6 +1908,11 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         }
         POST_SYNC(2);
         lap(2);
+#if ECO_METRICS & 2
+        if (mv_window_end(T))  // movement windows: one block per world, after every placement
+            for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
+                mv_pass_part(p, T, w, 0, p.S, threadIdx.x, blockDim.x, s_mv);
+#endif
         if (p.n_worlds >= (int)gridDim.x) {  // no block was free: the regrowth goes beside the mutation
             const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
             if (gtid >= half) regrow_phase(p, T + 1, gtid - half, gthreads - half);
@@ -1940,6 +1961,9 @@ cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStre
 
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
+#if ECO_METRICS & 2
+    k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);  // the movement histogram at a window end (after placement)
+#endif
     return cudaGetLastError();
 }
 

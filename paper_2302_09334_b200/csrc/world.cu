@@ -157,8 +157,14 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
             list[base + ex] = i;
             list_cell_of(p, t, w)[base + ex] = p.cell[gs];
         }
+        if (i < p.S) {  // movement windows: a run (re)started at a window start measures it
+            p.mv_cell[gs] = a ? p.cell[gs] : 0;
+            p.mv_inv[gs] = (a && t % SIM_MOVE_WINDOW == 0) ? p.age[gs] - (int32_t)t : -(1 << 29);
+        }
         base += tot;
     }
+    for (int k = threadIdx.x; k < p.mv_cap * SIM_MOVE_BINS; k += blockDim.x)
+        p.mv_hist[(size_t)w * p.mv_cap * SIM_MOVE_BINS + k] = 0;
     if (threadIdx.x == 0) {
         *count_of(p, t, w) = (int32_t)base;
         *count_of(p, t + 1, w) = 0;

@@ -28,7 +28,7 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
             "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
-            "sim_set_record_mirror", "sim_step_graph_timed")
+            "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist")
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
@@ -71,7 +71,8 @@ class SimState(ctypes.Structure):
 
 RECORD_FIELDS = ("t", "agents_at_start", "grown", "eaten", "births", "deaths_energy", "deaths_age",
                  "deferred_no_cell", "deferred_claim", "deferred_capacity", "population", "resources",
-                 "near_ties", "obs_nnz")
+                 "near_ties", "obs_nnz", "death_age_sum")
+MOVE_WINDOW, MOVE_BINS = 50, 17  # include/sim.h: SIM_MOVE_WINDOW, SIM_MOVE_BINS
 RECORD_DTYPE = np.dtype([(f, np.int64) for f in RECORD_FIELDS])
 TOTALS_FIELDS = ("steps", "agent_steps", "cell_updates", "births", "deaths", "eaten", "grown")
 
@@ -116,6 +117,8 @@ def lib():
                 L.sim_set_record_mirror.argtypes = [H, ctypes.c_void_p, ctypes.c_int64]
             L.sim_get_totals.argtypes = [H, ctypes.POINTER(SimTotals)]
             L.sim_step_timed.argtypes = [H, ctypes.POINTER(SimStepTiming)]
+            if hasattr(L, "sim_get_move_hist"):
+                L.sim_get_move_hist.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
             if hasattr(L, "sim_step_graph_timed"):
                 L.sim_step_graph_timed.argtypes = [H, ctypes.c_void_p]
             L.sim_synchronize.argtypes = [H]
@@ -365,6 +368,13 @@ class World:
         out = np.zeros(len(POST_PHASES), np.int64)
         _check(lib().sim_get_phase_ns(self._h, _ptr(out), int(reset)))
         return dict(zip(POST_PHASES, out.tolist()))
+
+    def move_hist(self, first: int, n: int) -> np.ndarray:
+        """Movement histograms of windows [first, first+n): int32 [n, n_worlds, 17]
+        (include/sim.h: sim_get_move_hist)."""
+        out = np.zeros((n, self.n_worlds, MOVE_BINS), np.int32)
+        _check(lib().sim_get_move_hist(self._h, int(first), int(n), _ptr(out)))
+        return out
 
     def totals(self) -> dict:
         tt = SimTotals()

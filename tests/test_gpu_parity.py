@@ -542,3 +542,79 @@ def test_large_world_full_size_graph_equals_instrumented_and_invariants():
     assert int(la["births"].sum()) > 0
     a.destroy()
     b.destroy()
+
+
+# ------------------------------------------------- Appendix C metrics
+def _fold_run(world, orc, steps, forced_fn=None):
+    """Step the oracle and the library together (the library forced to the oracle's actions
+    when forced_fn is None) and fold the oracle's states into the Appendix C metrics."""
+    from oracle import metrics
+    fold = metrics.MetricsFold(world.wc.cols)
+    for _ in range(steps):
+        before = {k: orc.st[k].copy() for k in ("alive", "cell", "age")} | {"t": orc.t}
+        if forced_fn is None:
+            r = orc.step(return_actions=True)
+            f = np.full((1, world.wc.slots), 255, np.uint8)
+            f[0] = r["actions"]
+        else:
+            f = forced_fn()
+            r = orc.step(forced=f)
+            f = f[None]
+        assert r["status"] == 0
+        world.set_forced_actions(f)
+        world.step(1)
+        fold.feed(before, {k: orc.st[k] for k in ("alive", "cell", "age")} | {"t": orc.t})
+    world.set_forced_actions(None)
+    return fold
+
+
+def _check_metrics(world, fold, t0, steps):
+    log = world.step_log(t0, steps)[:, 0]
+    for k in range(steps):
+        assert int(log["death_age_sum"][k]) == fold.death_age_sum[t0 + k], f"step {t0 + k}"
+    wins = sorted(fold.hist)
+    got = world.move_hist(wins[0], len(wins))[:, 0]
+    for i, k in enumerate(wins):
+        assert np.array_equal(got[i], fold.hist[k]), (k, got[i], fold.hist[k])
+    return got
+
+
+def test_metrics_scripted_walk():
+    from scenario import E, build_state, forced, small_config
+    wc = small_config(rows=6, cols=60, slots=4)
+    st = build_state(wc, [dict(slot=0, y=2, x=2), dict(slot=1, y=4, x=30), dict(slot=2, y=0, x=50, energy=1000)])
+    world = sim.World(wc)
+    world.set_state(st)
+    orc = oracle.OracleWorld(wc, state=st)
+    fold = _fold_run(world, orc, 50, forced_fn=lambda: forced(wc, {0: E}))
+    got = _check_metrics(world, fold, 0, 50)
+    assert got[0][16] == 1 and got[0][0] == 1 and got[0].sum() == 2
+    assert int(world.step_log(9, 1)[0, 0]["death_age_sum"]) == 10
+
+
+def test_metrics_match_the_oracle_tiny_and_paper_scale():
+    """Movement histograms and ages at death equal the oracle fold: the tiny world over 150
+    steps (three windows), the paper-scale world over 100 steps (two windows, thousands of
+    agents, births and deaths); both forced to the oracle's actions (M2)."""
+    for wc, steps in ((workloads.tiny(), 150), (workloads.paper_scale(), 100)):
+        world = sim.World(wc)
+        orc = oracle.OracleWorld(wc)
+        fold = _fold_run(world, orc, steps)
+        got = _check_metrics(world, fold, 0, steps)
+        assert got.sum() > 0
+        world.destroy()
+
+
+def test_metrics_after_set_state_mid_window():
+    """A run resumed at t = 25 does not measure window 0 (begun before the resume: all 0) and
+    measures window 1 exactly."""
+    wc = workloads.tiny()
+    a = sim.World(wc)
+    a.step(25)
+    snap = a.get_state()
+    world = sim.World(wc)
+    world.set_state(snap)
+    orc = oracle.OracleWorld(wc, state=snap)
+    fold = _fold_run(world, orc, 75)
+    assert world.move_hist(0, 1).sum() == 0
+    assert np.array_equal(world.move_hist(1, 1)[0, 0], fold.hist[1])
