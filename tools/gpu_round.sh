@@ -17,7 +17,7 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
       -s ${NCU_SKIP:-602} -c 60 --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
   echo ncu_launch=$? >> $OUT/status.txt
   # one full capture: the graph path's k_post of step W-1, then the instrumented step W's policy and P rows
-  W=${PROF_WARMUP:-3000}
+  W=${PROF_WARMUP:-3020}  # (step W-1 is not a movement-window end)
   PCMD="python tools/profile_step.py --warmup $W --out $OUT/step_$TAG.json"
   timeout 300 $PCMD > $OUT/plain2_$TAG.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_policy_half|k_prepare_p|k_post" -s $((2 * W)) -c 3 \
