@@ -19,9 +19,10 @@ from paper_2302_09334_b200 import sim  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--warmup", type=int, default=3000)
+ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "large_world"))
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
-wc = workloads.paper_scale()
+wc = workloads.paper_scale() if a.config == "paper_scale" else workloads.large_world()
 world = sim.World(wc, device=0)
 world.step(a.warmup)
 world.synchronize()
