@@ -395,6 +395,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.mrec_slot, S ? S : 1), "alloc");
     CKC(dalloc(h, &p.own_list, S ? 2 * S : 1), "alloc");
     CKC(dalloc(h, &p.own_count, 2), "alloc");
+    CKC(dalloc(h, &p.own_surv, 1), "alloc");
     CKC(dalloc(h, &p.cand, nw * S), "alloc");
     CKC(dalloc(h, &p.n_cand, nw), "alloc");
     CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
@@ -520,7 +521,7 @@ sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
     if ((st = sync(h)) != SIM_OK) return st;
     h->p.n_ranks = n_ranks;
     h->p.rank = rank;
-    if (n_ranks > 1) h->p.split = 0;  // the sharded step streams W_hh in the policy
+    h->p_ready = false;  // every own agent's P row again (a child's too: exactly b)
     CK(h, eco::launch_set_owner(h->p, h->stream), "owners");
     if (h->graph_exec) {  // kernel parameters changed: capture again
         cudaGraphExecDestroy(h->graph_exec);

@@ -69,6 +69,7 @@ struct DevParams {
     int4 *mrec_slot;             // [S] sharded: move records by SLOT (the list order differs by rank)
     int32_t *own_list;           // [2][S] sharded: this rank's live slots of step t (by parity)
     int32_t *own_count;          // [2]
+    int32_t *own_surv;           // sharded + split: own list positions below hold survivors (P rows)
     // Split policy (one unsharded world, Hd = 32, graph mode): P[slot] = W_hh h + b for the
     // NEXT step is computed by k_post for the survivors (off the policy's critical path,
     // beside the latency-bound phases); the policy then streams only P and the active W_ih

@@ -1222,7 +1222,10 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p(DevParams 
     const int64_t t = p.t[0];
     hh_pass<HALF_DEPTH>(p, list_of(p, t, 0), *count_of(p, t, 0), ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
             half_smem + (ag * HALF_DEPTH) * 32);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *p.p_children = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *p.p_children = 0;
+        *p.own_surv = 0x7fffffff;  // sharded: every own agent has its P row
+    }
 }
 
 #ifdef ECO_TIMELINE
@@ -1254,14 +1257,17 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #endif
     step_housekeeping(p);
     const long total = (long)p.n_worlds * p.S;
-    const long v = (long)ag * gridDim.x + blockIdx.x;
+    // one world: contexts interleaved over the blocks (few agents spread over every SM);
+    // sharded: block-major, so this rank's agents (a fraction of the slots) fill whole blocks
+    const long v = SHARD ? (long)blockIdx.x * HALF_AGENTS + ag : (long)ag * gridDim.x + blockIdx.x;
     const bool in_range = v < total;
     const int w = in_range ? (int)(v / p.S) : 0;
     const int i = in_range ? (int)(v - (long)w * p.S) : 0;
     const int64_t t = p.t[w];
     // unsharded: both parities' count, slot and cell of list position i load beside t (one
     // round trip instead of t -> count -> slot -> cell; entries past a count are stale, unused)
-    int n_list = 0, slot = 0, cell_l = 0, n_ch = 0;
+    int n_list = 0, slot = 0, cell_l = 0, n_ch = 0, own_surv = 0;
+    if (SHARD && SPLIT && in_range) own_surv = *p.own_surv;
     const int forced_on = in_range ? *p.forced_on : 0;  // loaded now, used by the epilogue
     if (!SHARD && in_range) {
         if (SPLIT) n_ch = *p.p_children;
@@ -1309,7 +1315,7 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
             }
         };
         // split: the first chunk is P = W_hh h + b (k_post made it), or the bias of a child
-        const bool child = SPLIT && active && i >= n_list - n_ch;
+        const bool child = SPLIT && active && (SHARD ? i >= own_surv : i >= n_list - n_ch);
         if (SPLIT) {
             issue(0, child ? Wl + p.off_b : p.Pbuf + (size_t)slot * HD * 4 + hl * 4);
             cp_commit();
@@ -1577,6 +1583,8 @@ cudaError_t policy_prepare() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_policy_half<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_policy_half<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_prepare_p, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_policy_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
@@ -1605,7 +1613,8 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 #if ECO_HALF_FULLGRID
             if (blocks < (long)lc.sms * HALF_BPS) blocks = (long)lc.sms * HALF_BPS;  // every SM the same
 #endif
-            if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
+            if (p.n_ranks > 1 && p.split) k_policy_half<true, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
+            else if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.split) k_policy_half<false, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             break;
@@ -1765,8 +1774,10 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     if (hh_split && blockIdx.x > 0 && wid >= DYN_WARPS) {
         const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
         const int ag = (wid - DYN_WARPS) * 2 + (lane >> 4);
-        hh_pass<HH_DEPTH>(p, list_of(p, T, 0), *count_of(p, T, 0), ag * (int)nb + (int)b, (int)nb * HH_WARPS * 2,
-                          post_smem + (ag * HH_DEPTH) * 32);
+        // (sharded: this rank's own agents only)
+        const int32_t *hl_ = SHARD ? p.own_list + (size_t)(T & 1) * p.S : list_of(p, T, 0);
+        const int hn_ = SHARD ? p.own_count[T & 1] : *count_of(p, T, 0);
+        hh_pass<HH_DEPTH>(p, hl_, hn_, ag * (int)nb + (int)b, (int)nb * HH_WARPS * 2, post_smem + (ag * HH_DEPTH) * 32);
         END_CLOCK(1);
 #ifdef ECO_TIMELINE
         if (lane == 0) timeline_mark(p, 3, globaltimer_ns(), T);
@@ -1816,11 +1827,15 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
                 atomicMax(p.claim + mr.z, ((unsigned long long)(uint32_t)mr.w << 32) |
                                               (unsigned long long)(0xFFFFFFFFu - (uint32_t)mr.y));
         }
-        grid_sync(bar, target);
+        grid_sync(bar, target, nthr);
     }
     move_phase(p, gtid, gthreads);
     POST_SYNC(0);
     lap(0);
+    // sharded + split: this rank's survivors lead its next list; its children (appended by
+    // the placement) follow and have no P row
+    if (SHARD && p.split && blockIdx.x == 0 && threadIdx.x == 0)
+        *p.own_surv = *reinterpret_cast<volatile int32_t *>(p.own_count + ((T + 1) & 1));
     if (p.n_worlds > 1) {
         // birth candidates on every thread
         const uint64_t h0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
@@ -2020,6 +2035,8 @@ cudaError_t post_prepare() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_post<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_post<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_post<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
 }
 
@@ -2034,7 +2051,7 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (p.n_ranks > 1) return cudaLaunchKernelEx(&cfg, k_post<true>, p, bar);
+    if (p.n_ranks > 1) return cudaLaunchKernelEx(&cfg, post_big(p) ? k_post<true, true> : k_post<true>, p, bar);
     if (post_big(p)) return cudaLaunchKernelEx(&cfg, k_post<false, true>, p, bar);
     return cudaLaunchKernelEx(&cfg, k_post<false>, p, bar);
 }
