@@ -212,13 +212,16 @@ SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
  * between and after them; synchronises.  out_ms[0] = policy, out_ms[1] = k_post
  * (milliseconds).  SIM_E_STATE on a sharded handle. */
 SIM_API sim_status sim_step_graph_timed(sim_handle h, float out_ms[2]);
-/* Graph mode runs everything after the policy kernel as one cooperative kernel whose
- * phases are separated by grid barriers: move | birth candidates | birth rank (beside the
- * regrowth of step t+1 on the blocks without a world) | mutation.
+/* Graph mode runs everything after the policy kernel as one cooperative kernel (k_post).
+ * One world: move | grid barrier | block 0: birth claims, rank (the births flag), placement
+ * and counters, while the other blocks regrow step t+1 and then mutate the children (and
+ * 4 or 16 warps per block make the next step's P rows from the start).  Several worlds:
+ * move | claims | per-world rank beside the regrowth | mutation, separated by barriers.
  * out[i] = summed duration (ns, device global timer, as seen by block 0) over the steps
- * since the last reset; reset > 0 zeroes.  out[0..3]: those four phases; out[4..7]
- * reserved; out[8]: summed durations of block 0's warps working on the birth claims;
- * out[9]: summed durations of the regrowth warps of the first block without a world.
+ * since the last reset; reset > 0 zeroes.  out[0..3]: those four laps of block 0 (move +
+ * barrier, claims, rank until the flag, the rest); out[4..7] reserved (diagnostic builds);
+ * out[8]: summed durations of block 0's warps on the claims (several worlds); out[9]: summed
+ * durations of the regrowth warps of block 1.
  * reset < 0 (diagnostic builds): out receives 16 + 32768 words, the per-block clocks or
  * per-agent traces after the first 16. */
 #define SIM_NUM_POST_PHASES 10
@@ -249,7 +252,7 @@ SIM_API sim_status sim_exchange(sim_handle h, void **mrec, size_t *mrec_bytes, v
 
 /* Synchronise the handle's stream (reports deferred errors). */
 SIM_API sim_status sim_synchronize(sim_handle h);
-/* Number of kernel launches one step performs (for the bench's launch count). */
+/* Number of kernels of an instrumented step (sim_step_timed; a graph step launches two). */
 SIM_API int32_t sim_kernels_per_step(void);
 
 #ifdef __cplusplus
