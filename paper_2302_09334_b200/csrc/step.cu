@@ -1494,6 +1494,9 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
         }
         }  // !SPLIT
         cp_wait<0>();
+#if defined(ECO_POLICY_TRACE) && defined(ECO_POLICY_TRACE_STREAM)
+        if (active && hl == 0) trace[3] = globaltimer_ns();  // the chunks are in: the gates and epilogue follow
+#endif
         const float cn0 = sigmoidf_acc(acc0.y) * ck0 + sigmoidf_acc(acc0.x) * tanhf(acc0.z);
         const float hn0 = sigmoidf_acc(acc0.w) * tanhf(cn0);
         const float cn1 = sigmoidf_acc(acc1.y) * ck1 + sigmoidf_acc(acc1.x) * tanhf(acc1.z);

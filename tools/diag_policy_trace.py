@@ -42,6 +42,11 @@ for rep in range(3):
     live = tr[:, 0] > 0
     t0 = tr[live, 0].min()
     st, mk, en, nnz = (tr[live, 0] - t0) / 1e3, (tr[live, 1] - t0) / 1e3, (tr[live, 2] - t0) / 1e3, tr[live, 3]
+    if "ECO_POLICY_TRACE_STREAM" in extra:  # trace[3] holds the time the chunks were in
+        sd = (tr[live, 3] - t0) / 1e3
+        print(f"  stream done q50 {float(np.median(sd)):6.2f} (after mask {float(np.median(sd - mk)):6.2f}; "
+              f"epilogue to end {float(np.median(en - sd)):6.2f}) us")
+        nnz = np.zeros_like(nnz)
     n = int(live.sum())
     q = lambda a, f: float(np.quantile(a, f))
     print(f"step {world.t}: agents {n}, nnz mean {nnz.mean():.1f} max {nnz.max()}")
