@@ -10,6 +10,8 @@
 //                 counters (block 0), a1 regrowth of step t+1, a5 mutation, t += 1
 // (the first step after create/set_state is preceded by a standalone k_regrow).
 // Instrumented mode (sim_step_timed): the same phases as separate kernels, timed one by one.
+#include <type_traits>
+
 #include "phases.cuh"
 
 // cp.async with an .L2::cache_hint operand raised "illegal instruction" on the B200 pool
@@ -1124,6 +1126,9 @@ __global__ void __launch_bounds__(RING_WARPS * 32, STREAM_BPS) k_policy_stream(D
 // h+16 (two float4 gate accumulators) and copies/reads their 2 x 16 B of every 512-B chunk.
 // Ring: HALF_DEPTH chunks per agent (3 KB) in flight; 16 agents per block interleaved over
 // the blocks (agent v = a * gridDim + block).  Column indices are compacted to bytes.
+#ifndef ECO_POLICY_DEEP
+#define ECO_POLICY_DEEP 1
+#endif
 #ifndef ECO_HALF_FULLGRID
 #define ECO_HALF_FULLGRID 1  // 4 blocks on every SM (592 at 8 warps): 48.0 -> 47.4 us per step
 #endif
@@ -1399,47 +1404,60 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #endif
         float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
         if (SPLIT) {
-            // chunk 0 = P (or b), chunks 1.. = the active columns; R ticks per round from 0
+            // chunk 0 = P (or b), chunks 1.. = the active columns; D ticks per round from 0.
+            // When at most half the contexts hold an agent (one world: exactly the agents of
+            // the first half of every block, ag < HALF_AGENTS/2), an agent also uses the ring
+            // of agent ag + HALF_AGENTS/2, which has none: 2R chunks in flight, so the ~10
+            // columns of a typical agent arrive in one round trip instead of two.
             const int N1 = 1 + nnz;
-#if ECO_POLICY_PREFETCH == 2
-            // the columns past the first round: their 128-B lines into L2 now, so the
-            // later rounds hit L2 (lane hl takes lines hl, hl + 16, ... of chunks R..N1-1)
-            if (active)
-                for (int q = hl; q < 4 * (N1 - R); q += 16)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(Wl - hl * 4 + (int)cols[R - 1 + (q >> 2)] * HD * 4 + (q & 3) * 32));
-#endif
             const int Nw1 = __reduce_max_sync(FULL, active ? N1 : 0);
-#pragma unroll
-            for (int q = 1; q < R; ++q) {
-                if (q < N1) issue(q, Wl + (int)cols[q - 1] * HD * 4);
-                cp_commit();
-            }
-            for (int k0 = 0; k0 < Nw1; k0 += R) {
-#pragma unroll
-                for (int s2 = 0; s2 < R; ++s2) {
-                    const int k = k0 + s2;
-                    cp_wait<R - 1>();
-                    if (k < N1) {
-                        const float4 c0 = rg[s2 * 32], c1 = rg[s2 * 32 + 16];
-                        if (k == 0) {
-                            acc0 = c0;
-                            acc1 = c1;
-                        } else {
-                            acc0.x += c0.x;
-                            acc0.y += c0.y;
-                            acc0.z += c0.z;
-                            acc0.w += c0.w;
-                            acc1.x += c1.x;
-                            acc1.y += c1.y;
-                            acc1.z += c1.z;
-                            acc1.w += c1.w;
-                        }
+            auto stream = [&](auto DC) {
+                constexpr int D = decltype(DC)::value;
+                auto at = [&](int s_) { return rg + (s_ < R ? s_ : s_ + (HALF_AGENTS / 2 - 1) * R) * 32; };
+                auto issue_at = [&](int s_, const float *src) {
+                    if (active) {
+                        cp_async16(at(s_), src, 0ull);
+                        cp_async16(at(s_) + 16, src + 64, 0ull);
                     }
-                    const int kn = k + R;
-                    if (kn < N1) issue(s2, Wl + (int)cols[kn - 1] * HD * 4);
+                };
+#pragma unroll
+                for (int q = 1; q < D; ++q) {
+                    if (q < N1) issue_at(q, Wl + (int)cols[q - 1] * HD * 4);
                     cp_commit();
                 }
-            }
+                for (int k0 = 0; k0 < Nw1; k0 += D) {
+#pragma unroll
+                    for (int s2 = 0; s2 < D; ++s2) {
+                        const int k = k0 + s2;
+                        cp_wait<D - 1>();
+                        if (k < N1) {
+                            const float4 c0 = at(s2)[0], c1 = at(s2)[16];
+                            if (k == 0) {
+                                acc0 = c0;
+                                acc1 = c1;
+                            } else {
+                                acc0.x += c0.x;
+                                acc0.y += c0.y;
+                                acc0.z += c0.z;
+                                acc0.w += c0.w;
+                                acc1.x += c1.x;
+                                acc1.y += c1.y;
+                                acc1.z += c1.z;
+                                acc1.w += c1.w;
+                            }
+                        }
+                        const int kn = k + D;
+                        if (kn < N1) issue_at(s2, Wl + (int)cols[kn - 1] * HD * 4);
+                        cp_commit();
+                    }
+                }
+            };
+#if ECO_POLICY_DEEP
+            if (!SHARD && n_list <= (int)gridDim.x * (HALF_AGENTS / 2)) stream(std::integral_constant<int, 2 * R>{});
+            else stream(std::integral_constant<int, R>{});
+#else
+            stream(std::integral_constant<int, R>{});
+#endif
         } else {
         const int N = Q0 + nnz;
         const int Nw = __reduce_max_sync(FULL, active ? N : 0);  // the warp runs the longer sequence
