@@ -393,7 +393,7 @@ def run_ours(args, rank, world_size, local_rank):
             rl = {}
             for kname, (desc, byt, ms, step_ms_tot) in cands.items():
                 achieved = byt / (ms / 1e3) / 1e9
-                ratio, ratio_src = traffic_ratio(kname)
+                ratio, ratio_src = traffic_ratio(kname, wc.name)
                 rl[kname] = {
                     "kernel": desc, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": ratio * byt / K if ratio else None,
@@ -414,7 +414,7 @@ def run_ours(args, rank, world_size, local_rank):
     return result, snap, wc
 
 
-def traffic_ratio(kname="policy"):
+def traffic_ratio(kname="policy", workload="paper_scale"):
     """DRAM bytes (read + write) over algorithmic bytes of the kernel's launch (policy: the
     k_policy launch; hh: k_prepare_p) in the newest committed ncu --set full summary
     (profiles/*_ncu_summary.json, tools/ncu_summary.py); the roofline's `traffic` is this
@@ -426,6 +426,8 @@ def traffic_ratio(kname="policy"):
     for f in reversed(files):
         try:
             d = json.load(open(f))
+            if d.get("step", {}).get("workload", "paper_scale") != workload:
+                continue  # a capture of another workload
             for rec in d["launches"]:
                 if tag in rec["kernel"] and "traffic_over_algorithmic" in rec:
                     return float(rec["traffic_over_algorithmic"]), os.path.relpath(f, ROOT)

@@ -292,16 +292,20 @@ class World:
         _check(lib().sim_synchronize(self._h))
 
     # -- state ----------------------------------------------------------------------
-    def empty_state(self, fields=STATE_FIELDS) -> dict:
+    def state_shapes(self) -> dict:
+        """field -> (shape, dtype) of the canonical state arrays (leading world axis)."""
         wc, nw = self.wc, self.n_worlds
         S, Hd, P = wc.slots, wc.hidden, wc.n_params
-        shapes = {
+        return {
             "resources": ((nw, wc.rows, wc.cols), np.uint8), "alive": ((nw, S), np.uint8),
             "cell": ((nw, S), np.int32), "energy": ((nw, S), np.int32), "age": ((nw, S), np.int32),
             "repr": ((nw, S), np.int32), "last_action": ((nw, S), np.uint8), "ate": ((nw, S), np.uint8),
             "h": ((nw, S, Hd), np.float32), "c": ((nw, S, Hd), np.float32),
             "weights": ((nw, S, P), np.float32), "logits": ((nw, S, 5), np.float32),
         }
+
+    def empty_state(self, fields=STATE_FIELDS) -> dict:
+        shapes = self.state_shapes()
         return {f: np.zeros(*shapes[f]) for f in fields}
 
     def get_state(self, fields=STATE_FIELDS) -> dict:
@@ -320,11 +324,11 @@ class World:
         Per-field arrays may omit the world axis when n_worlds == 1."""
         st = SimState()
         keep = []
-        ref = self.empty_state([f for f in STATE_FIELDS if f in state])
+        shapes = self.state_shapes()  # (no host allocation: the weights alone are 0.5 GB at paper scale)
         for f in STATE_FIELDS:
             if f not in state:
                 continue
-            a = np.ascontiguousarray(np.asarray(state[f]).reshape(ref[f].shape), dtype=ref[f].dtype)
+            a = np.ascontiguousarray(np.asarray(state[f]).reshape(shapes[f][0]), dtype=shapes[f][1])
             keep.append(a)
             setattr(st, f, _ptr(a))
         st.t = int(state.get("t", self._t))
