@@ -1399,10 +1399,9 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
         float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
         if (SPLIT) {
             // chunk 0 = P (or b), chunks 1.. = the active columns; D ticks per round from 0.
-            // When at most half the contexts hold an agent (one world: exactly the agents of
-            // the first half of every block, ag < HALF_AGENTS/2), an agent also uses the ring
-            // of agent ag + HALF_AGENTS/2, which has none: 2R chunks in flight, so the ~10
-            // columns of a typical agent arrive in one round trip instead of two.
+            // An agent of a block's first half whose partner context (agent ag + HALF_AGENTS/2)
+            // holds no agent this step also uses the partner's ring: 2R chunks in flight, so
+            // the ~10 columns of a typical agent arrive in one round trip instead of two.
             const int N1 = 1 + nnz;
             const int Nw1 = __reduce_max_sync(FULL, active ? N1 : 0);
             auto stream = [&](auto DC) {
@@ -1447,7 +1446,11 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
                 }
             };
 #if ECO_POLICY_DEEP
-            if (!SHARD && n_list <= (int)gridDim.x * (HALF_AGENTS / 2)) stream(std::integral_constant<int, 2 * R>{});
+            // per warp: its agents' partners (agents 2w + HALF_AGENTS/2 and the next, list
+            // positions further on) hold no agent this step, so their rings are free
+            const bool deep = !SHARD && warp < HALF_WARPS / 2 &&
+                              (long)(2 * warp + HALF_AGENTS / 2) * gridDim.x + blockIdx.x >= (long)n_list;
+            if (deep) stream(std::integral_constant<int, 2 * R>{});
             else stream(std::integral_constant<int, R>{});
 #else
             stream(std::integral_constant<int, R>{});
