@@ -19,18 +19,19 @@ from paper_2302_09334_b200 import sim  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--warmup", type=int, default=3000)
-ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "large_world"))
+ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "large_world", "ensemble"))
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
-wc = workloads.paper_scale() if a.config == "paper_scale" else workloads.large_world()
+wc = getattr(workloads, a.config)()
 world = sim.World(wc, device=0)
 world.step(a.warmup)
 world.synchronize()
 t = world.t
 world.step_timed()
 world.synchronize()
-rec = world.step_log(t, 1)[0, 0]
-prev = world.step_log(t - 1, 1)[0, 0]  # the step of the captured k_post (the last graph step)
+lg, lp = world.step_log(t, 1)[0], world.step_log(t - 1, 1)[0]  # every world's record
+rec = {f: int(lg[f].sum()) for f in lg.dtype.names}  # summed over the worlds
+prev = {f: int(lp[f].sum()) for f in lp.dtype.names}  # the step of the captured k_post
 agents, nnz, births = int(rec["agents_at_start"]), int(rec["obs_nnz"]), int(rec["births"])
 out = {"workload": wc.name, "step": t, "agents": agents, "obs_nnz": nnz, "births": births,
        "population": int(rec["population"]),
