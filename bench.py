@@ -13,11 +13,16 @@ Our arm (default):
     library's stream, with L2 flushed between timed steps: a 256 MiB memset (evicts every
     line the step left) followed by a 256 MiB read, so the evicted lines are clean and the
     next step is not charged for writing back the flush buffer's dirty lines;
-  * replays the same K steps from a snapshot through sim_step_timed (events around every
-    kernel) for the per-kernel breakdown and the roofline of the dominant kernel;
+  * replays the same K steps from a snapshot twice, L2 flushed between steps: through
+    sim_step_timed (the phases as separate kernels, events around each) for the per-kernel
+    breakdown, and through sim_step_graph_timed (the graph's own two kernels launched
+    directly, events between them) for `roofline` (the longer of the two, at its
+    algorithmic bytes; `traffic` from the newest profiles/*_ncu_summary.json of the same
+    workload) and `kernels_roofline`; both replays must reproduce the timed run's records;
   * e2e: the same K steps through the public API from pinned HOST buffers: sim_set_state
-    (H2D of the whole state) + per step sim_step + sim_get_step_log (D2H of the step's
-    record), wall clock;
+    (H2D of the whole state), then per step sim_step, each step's record written by the
+    device into a mapped pinned host ring (sim_set_record_mirror: the D2H of the result
+    without a copy operation), wall clock, checked equal to the timed run's records;
   * cpu_baseline: the oracle (oracle/, single thread) on a bounded sample of the same
     workload from the same start state.
 --impl reference: the oracle as the reference arm (no GPU code on that path).
