@@ -20,7 +20,7 @@ Our arm (default):
     algorithmic bytes; `traffic` from the newest profiles/*_ncu_summary.json of the same
     workload) and `kernels_roofline`; both replays must reproduce the timed run's records;
   * e2e: the same K steps through the public API from pinned HOST buffers: sim_set_state
-    (H2D of the whole state), then per step sim_step, each step's record written by the
+    (H2D of the whole state), then sim_step(K) (one call), each step's record written by the
     device into a mapped pinned host ring (sim_set_record_mirror: the D2H of the result
     without a copy operation), wall clock, checked equal to the timed run's records;
   * cpu_baseline: the oracle (oracle/, single thread) on a bounded sample of the same
@@ -341,8 +341,7 @@ def run_ours(args, rank, world_size, local_rank):
             barrier()
             te = time.perf_counter()
             world.set_state(pinned)
-            for k in range(K):
-                world.step(1)
+            world.step(K)  # the user's call: K steps in one sim_step (two-step graphs)
             world.synchronize()
             e_s = time.perf_counter() - te
             world.set_record_mirror(None)

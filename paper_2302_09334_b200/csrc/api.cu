@@ -10,6 +10,10 @@
 
 #include "sim_internal.cuh"
 
+#ifndef ECO_STEP2_PDL
+#define ECO_STEP2_PDL 1
+#endif
+
 using eco::DevParams;
 
 namespace {
@@ -155,6 +159,8 @@ struct sim_ctx {
     // preceded by a standalone regrowth (afterwards each k_post regrows the next step).
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    cudaGraph_t graph2 = nullptr;  // two steps, the second policy a programmatic dependent
+    cudaGraphExec_t graph2_exec = nullptr;
     bool regrown_ahead = false;
     bool p_ready = false;  // split policy: the P rows of step t exist
     unsigned long long *bar = nullptr;   // grid-barrier words of k_post
@@ -226,10 +232,31 @@ cudaError_t launch_phase(sim_ctx *h, int k) {
 }
 
 // graph-mode step: the policy kernel, then the cooperative post-policy kernel
-cudaError_t enqueue_step(sim_ctx *h) {
+cudaError_t enqueue_step(sim_ctx *h, bool pdl = false) {
     cudaError_t e;
-    if ((e = eco::launch_policy(h->p, h->lc, h->stream)) != cudaSuccess) return e;
+    if ((e = eco::launch_policy(h->p, h->lc, h->stream, pdl)) != cudaSuccess) return e;
     return eco::launch_post(h->p, h->lc, h->bar, h->stream);
+}
+
+// capture `steps` (1 or 2) graph steps; in two, the second policy depends programmatically
+// on the first k_post (its launch overlaps k_post's drain)
+cudaError_t capture_steps(sim_ctx *h, int steps, cudaGraph_t *g, cudaGraphExec_t *ge) {
+    cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    for (int i = 0; i < steps && e == cudaSuccess; ++i) e = enqueue_step(h, i > 0);
+    cudaError_t e2 = cudaStreamEndCapture(h->stream, g);
+    if (e != cudaSuccess) return e;
+    if (e2 != cudaSuccess) return e2;
+    return cudaGraphInstantiate(ge, *g, 0);
+}
+
+void drop_graphs(sim_ctx *h) {  // kernel parameters changed: capture again on the next step
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    if (h->graph2_exec) cudaGraphExecDestroy(h->graph2_exec);
+    if (h->graph2) cudaGraphDestroy(h->graph2);
+    h->graph_exec = h->graph2_exec = nullptr;
+    h->graph = h->graph2 = nullptr;
 }
 
 // the regrowth of the current step, needed once after create/set_state; with the split
@@ -256,8 +283,7 @@ sim_status sync(sim_ctx *h) {
 void destroy_all(sim_ctx *h) {
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
-    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-    if (h->graph) cudaGraphDestroy(h->graph);
+    drop_graphs(h);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
     for (void *v : h->allocs) cudaFree(v);
@@ -493,18 +519,18 @@ sim_status sim_step(sim_handle h, int64_t n) {
     if (h->p.n_ranks > 1)
         return fail(SIM_E_STATE, "sharded handle: step with sim_step_policy, the exchange, then sim_step_post");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
-    if (!h->graph_exec) {
-        CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
-        cudaError_t e = enqueue_step(h);
-        cudaGraph_t g = nullptr;
-        cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
-        CK(h, e, "capture step");
-        CK(h, e2, "end capture");
-        h->graph = g;
-        CK(h, cudaGraphInstantiate(&h->graph_exec, g, 0), "graph instantiate");
-    }
+    if (!h->graph_exec) CK(h, capture_steps(h, 1, &h->graph, &h->graph_exec), "capture step");
+#if ECO_STEP2_PDL
+    const bool two = n >= 2 && h->p.split && h->p.n_ranks == 1;  // (the programmatic edge needs the split policy)
+    if (two && !h->graph2_exec) CK(h, capture_steps(h, 2, &h->graph2, &h->graph2_exec), "capture two steps");
+#else
+    const bool two = false;
+#endif
     CK(h, ensure_regrown(h), "regrow");
-    for (int64_t i = 0; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
+    int64_t i = 0;
+    if (two)
+        for (; i + 2 <= n; i += 2) CK(h, cudaGraphLaunch(h->graph2_exec, h->stream), "graph launch");
+    for (; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
     h->t += n;
     return SIM_OK;
 }
@@ -523,12 +549,7 @@ sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
     h->p.rank = rank;
     h->p_ready = false;  // every own agent's P row again (a child's too: exactly b)
     CK(h, eco::launch_set_owner(h->p, h->stream), "owners");
-    if (h->graph_exec) {  // kernel parameters changed: capture again
-        cudaGraphExecDestroy(h->graph_exec);
-        cudaGraphDestroy(h->graph);
-        h->graph_exec = nullptr;
-        h->graph = nullptr;
-    }
+    drop_graphs(h);  // kernel parameters changed: capture again
     return sync(h);
 }
 
@@ -870,12 +891,7 @@ sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t ca
         h->p.rec_mirror = static_cast<sim_step_record *>(dev);
         h->p.mirror_cap = (int32_t)capacity;
     }
-    if (h->graph_exec) {  // kernel parameters changed: capture again
-        cudaGraphExecDestroy(h->graph_exec);
-        cudaGraphDestroy(h->graph);
-        h->graph_exec = nullptr;
-        h->graph = nullptr;
-    }
+    drop_graphs(h);  // kernel parameters changed: capture again
     return SIM_OK;
 }
 

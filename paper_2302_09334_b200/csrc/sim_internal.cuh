@@ -236,7 +236,8 @@ cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
 cudaError_t policy_prepare();  // kernel attributes (dynamic shared memory of k_policy_tma)
-cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
+// pdl: launched as a programmatic dependent of the preceding k_post (two-step graphs)
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl = false);
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);

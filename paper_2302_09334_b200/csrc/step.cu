@@ -1120,6 +1120,9 @@ __global__ void __launch_bounds__(RING_WARPS * 32, STREAM_BPS) k_policy_stream(D
 // h+16 (two float4 gate accumulators) and copies/reads their 2 x 16 B of every 512-B chunk.
 // Ring: HALF_DEPTH chunks per agent (3 KB) in flight; 16 agents per block interleaved over
 // the blocks (agent v = a * gridDim + block).  Column indices are compacted to bytes.
+#ifndef ECO_STEP2_PDL
+#define ECO_STEP2_PDL 1  // sim_step(n >= 2): two-step graphs, the second policy a programmatic dependent
+#endif
 #ifndef ECO_POST_PDL
 #define ECO_POST_PDL 1  // measured: 48.0 -> 47.45 us per step (2, the policy triggering early: 48.65)
 #endif
@@ -1259,6 +1262,11 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #endif
 #if ECO_POST_PDL >= 2
     asm volatile("griddepcontrol.launch_dependents;");  // k_post may be scheduled as blocks drain
+#endif
+#if ECO_STEP2_PDL
+    // the second policy of a two-step graph is a programmatic dependent of k_post: wait for
+    // it (a no-op for an ordinary launch)
+    if (SPLIT && !SHARD) asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
     step_housekeeping(p);
     const long total = (long)p.n_worlds * p.S;
@@ -1614,7 +1622,7 @@ cudaError_t policy_prepare() {
     return cudaFuncSetAttribute(k_policy_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
 }
 
-cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
+cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl) {
     switch (p.Hd) {
         case 4: k_policy_reg<4><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
         case 8: k_policy_reg<8><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
@@ -1639,6 +1647,19 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 #endif
             if (p.n_ranks > 1 && p.split) k_policy_half<true, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
+            else if (p.split && pdl) {  // a programmatic dependent of the previous k_post
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)(blocks > 0 ? blocks : 1));
+                cfg.blockDim = dim3(HALF_THREADS);
+                cfg.dynamicSmemBytes = HALF_SMEM;
+                cfg.stream = s;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                return cudaLaunchKernelEx(&cfg, k_policy_half<false, true>, p);
+            }
             else if (p.split) k_policy_half<false, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             break;
