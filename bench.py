@@ -219,6 +219,18 @@ def step_bytes(wc, agents: int, nnz: int, births: int) -> int:
     return policy_bytes(wc, agents, nnz, split=False) + wc.rows * wc.cols // 2 + births * 8 * wc.n_params
 
 
+def workload_config(wc, args, world_size: int, sharded: bool, t0: int) -> dict:
+    """The `config` object of both arms' JSON lines (the same workload, the same dict)."""
+    return {"workload": f"{wc.name} (BASELINE.json configs[1])" if args.config == "paper_scale" else wc.name,
+            "grid": f"{wc.rows}x{wc.cols}", "slots": wc.slots, "n_initial": wc.n_initial,
+            "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x2", "hidden": wc.hidden,
+            "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + args.steps],
+            "parallelism": (f"agent-sharded: one world over {world_size} GPUs (policy by slot owner, "
+                            "dynamics on every rank, NCCL SUM-allreduce of the move records per step)")
+            if sharded else "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
+            else "single device", "global_batch": wc.slots * (1 if sharded else world_size)}
+
+
 # ------------------------------------------------------------------------ our arm
 def run_ours(args, rank, world_size, local_rank):
     import torch
@@ -320,12 +332,15 @@ def run_ours(args, rank, world_size, local_rank):
         if not args.no_e2e:
             pinned = {}
             h2d = 0
+            n_live = int(snap["alive"].sum())
             for k_, v in snap.items():
                 if isinstance(v, np.ndarray):
                     tt = torch.empty(v.shape, dtype=getattr(torch, str(v.dtype)), pin_memory=True)
                     tt.numpy()[...] = v
                     pinned[k_] = tt.numpy()
-                    h2d += v.nbytes
+                    # the library reads the live slots' weights only (a dead slot's weights are
+                    # unspecified, sim.h), every other field whole
+                    h2d += n_live * wc.n_params * 4 if k_ == "weights" else v.nbytes
                 else:
                     pinned[k_] = v
             rec_bytes = sim.RECORD_DTYPE.itemsize * wc.n_worlds
@@ -334,8 +349,7 @@ def run_ours(args, rank, world_size, local_rank):
             cap = 1 << (K - 1).bit_length()
             rec_pin = torch.empty((cap, rec_bytes), dtype=torch.uint8, pin_memory=True).numpy()
             rec_host = rec_pin.view(sim.RECORD_DTYPE).reshape(cap, wc.n_worlds)
-            world.set_record_mirror(rec_host, cap)
-            world.step(1)  # re-capture the step's graph (its parameters changed) outside the timing
+            world.set_record_mirror(rec_host, cap)  # (re-captures both step graphs at once)
             world.synchronize()
             torch.cuda.synchronize()
             barrier()
@@ -360,16 +374,9 @@ def run_ours(args, rank, world_size, local_rank):
             "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{wc.name} (BASELINE.json configs[1])" if args.config == "paper_scale" else wc.name,
-                       "grid": f"{wc.rows}x{wc.cols}", "slots": wc.slots, "n_initial": wc.n_initial,
-                       "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x2", "hidden": wc.hidden,
-                       "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + K],
-                       "l2": "NOT flushed (diagnostic run)" if args.no_flush
-                       else "flushed between timed steps (256 MiB memset + 256 MiB read on the library stream)",
-                       "parallelism": (f"agent-sharded: one world over {world_size} GPUs (policy by slot owner, "
-                                       "dynamics on every rank, NCCL SUM-allreduce of the move records per step)")
-                       if sharded else "replicas (one independent world per GPU, seed 1+rank)" if world_size > 1
-                       else "single GPU", "global_batch": wc.slots * (1 if sharded else world_size)},
+            "config": workload_config(wc, args, world_size, sharded, t0),
+            "l2": "NOT flushed (diagnostic run)" if args.no_flush
+            else "flushed between timed steps (256 MiB memset + 256 MiB read on the library stream)",
             "cell_updates_per_s": cells * (1 if sharded else world_size) / (max_ms / 1e3),
             "agents_mean": agents / K,
             "births_mean": births / K,
@@ -456,6 +463,24 @@ def oracle_rate(wc, start_state, budget_s, max_steps):
     return agents / el, steps, el, a0, int(w.st["alive"].sum()), w.t
 
 
+def host_cpu() -> dict:
+    """The host CPU the oracle ran on: model name, logical CPUs (nproc) and the CPUs this
+    process may use (the oracle itself is single-threaded: cores = 1)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = None
+    return {"cpu_model": model, "nproc": os.cpu_count(), "cpus_usable": usable}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return None
@@ -471,9 +496,8 @@ def run_reference(args, rank):
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": args.warmup, "ms_per_step": el / max(steps, 1) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{wc.name} (BASELINE.json configs[1])", "grid": f"{wc.rows}x{wc.cols}",
-                   "slots": wc.slots, "n_initial": wc.n_initial, "seed": int(wc.seeds[0])},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "config": workload_config(wc, args, args.gpus, False, args.warmup),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, **host_cpu()},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -498,7 +522,7 @@ def main():
             rate, steps, el, a0, a1, t1 = oracle_rate(wc.replace(seeds=(wc.seeds[0],)), w0, args.cpu_budget_s,
                                                       args.steps)
             res["cpu_baseline"] = {
-                "value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", **host_cpu(),
                 "sample": f"{steps} oracle world steps from the timed region's start state (t={w0['t']}..{t1}, "
                           f"agents {a0}->{a1}), {el:.1f} s on one host core",
             }

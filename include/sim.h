@@ -158,7 +158,11 @@ typedef struct {
  * resources, N0 agents on the N0 smallest (draw, cell) empty cells, N(0, std^2)
  * weights).  n_initial > number of empty cells -> SIM_E_INVALID. */
 SIM_API sim_status sim_create(const sim_config *cfg, sim_handle *out);
-/* Enqueue n >= 0 world steps on the stream (one CUDA graph launch per step). */
+/* Enqueue n >= 0 world steps on the stream, asynchronously: CUDA graphs of [policy, k_post]
+ * (a two-step graph per pair of steps for n >= 2, whose second policy is a programmatic
+ * dependent of the first k_post; a one-step graph for an odd remainder).  The graphs are
+ * captured at the handle's first step and whenever a kernel parameter changes
+ * (sim_set_record_mirror), never by a later sim_step. */
 SIM_API sim_status sim_step(sim_handle h, int64_t n);
 /* Synchronise, convert to the canonical layout and copy into caller buffers. */
 SIM_API sim_status sim_get_state(sim_handle h, sim_state *out);

@@ -1,5 +1,6 @@
 // api.cu — the C ABI of include/sim.h: validation, device allocation, initialisation,
 // the per-step CUDA graph, state import/export and the test/measurement hooks.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -9,10 +10,6 @@
 #include <vector>
 
 #include "sim_internal.cuh"
-
-#ifndef ECO_STEP2_PDL
-#define ECO_STEP2_PDL 1
-#endif
 
 using eco::DevParams;
 
@@ -170,6 +167,16 @@ struct sim_ctx {
     uint8_t *forced_dev = nullptr;
     std::vector<void *> allocs;
     cudaEvent_t ev[SIM_NUM_KERNELS + 1] = {};
+    // set_state staging, persistent (no allocation per call): the live slots' global indices,
+    // the byte plane of the resources, the gathered device-layout rows of the live weights
+    // (grow-only) and, for pageable caller memory only, their compacted canonical rows
+    int32_t *live_dev = nullptr;
+    uint8_t *res_bytes = nullptr;
+    float *wstage = nullptr;
+    size_t wstage_rows = 0;
+    float *wcanon = nullptr;
+    size_t wcanon_rows = 0;
+    int32_t *bad_host = nullptr;  // mapped: a non-finite weight seen by the gather
 };
 
 namespace {
@@ -259,6 +266,24 @@ void drop_graphs(sim_ctx *h) {  // kernel parameters changed: capture again on t
     h->graph = h->graph2 = nullptr;
 }
 
+// both step graphs, captured eagerly (at create and whenever a kernel parameter changes) so
+// that sim_step only launches
+bool two_step_graphs(const sim_ctx *h) {
+#if ECO_STEP2_PDL
+    return h->p.split && h->p.n_ranks == 1;  // (the programmatic edge needs the split policy)
+#else
+    (void)h;
+    return false;
+#endif
+}
+cudaError_t ensure_graphs(sim_ctx *h) {
+    if (h->p.n_ranks > 1) return cudaSuccess;  // sharded handles step without graphs
+    cudaError_t e = cudaSuccess;
+    if (!h->graph_exec) e = capture_steps(h, 1, &h->graph, &h->graph_exec);
+    if (e == cudaSuccess && two_step_graphs(h) && !h->graph2_exec) e = capture_steps(h, 2, &h->graph2, &h->graph2_exec);
+    return e;
+}
+
 // the regrowth of the current step, needed once after create/set_state; with the split
 // policy also the P rows of the current step (k_post makes them for every later step)
 cudaError_t ensure_regrown(sim_ctx *h) {
@@ -287,7 +312,10 @@ void destroy_all(sim_ctx *h) {
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
     for (void *v : h->allocs) cudaFree(v);
+    if (h->wstage) cudaFree(h->wstage);
+    if (h->wcanon) cudaFree(h->wcanon);
     if (h->nonfinite_host) cudaFreeHost(h->nonfinite_host);
+    if (h->bad_host) cudaFreeHost(h->bad_host);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
@@ -356,6 +384,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(cudaHostAlloc(reinterpret_cast<void **>(&h->nonfinite_host), sizeof(int32_t), cudaHostAllocMapped),
         "cudaHostAlloc");
     *h->nonfinite_host = 0;
+    CKC(cudaHostAlloc(reinterpret_cast<void **>(&h->bad_host), sizeof(int32_t), cudaHostAllocMapped), "cudaHostAlloc");
+    *h->bad_host = 0;
 
     DevParams &p = h->p;
     p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
@@ -438,6 +468,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.phase_ns, PHASE_WORDS), "alloc");  // + per-block clocks / traces of diagnostic builds
     CKC(dalloc(h, &h->forced_dev, nw * S), "alloc");
     CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
+    CKC(dalloc(h, &h->live_dev, nw * S), "alloc");
+    CKC(dalloc(h, &h->res_bytes, nw * HW), "alloc");
     p.seeds = seeds_d;
     p.T = T_d;
     p.forced = h->forced_dev;
@@ -498,6 +530,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     }
     CKC(eco::launch_rebuild(p, h->stream), "rebuild");
     CKC(cudaStreamSynchronize(h->stream), "sync");
+    CKC(ensure_graphs(h), "capture step graphs");
 #undef CKC
     *out = h;
     return SIM_OK;
@@ -519,13 +552,8 @@ sim_status sim_step(sim_handle h, int64_t n) {
     if (h->p.n_ranks > 1)
         return fail(SIM_E_STATE, "sharded handle: step with sim_step_policy, the exchange, then sim_step_post");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
-    if (!h->graph_exec) CK(h, capture_steps(h, 1, &h->graph, &h->graph_exec), "capture step");
-#if ECO_STEP2_PDL
-    const bool two = n >= 2 && h->p.split && h->p.n_ranks == 1;  // (the programmatic edge needs the split policy)
-    if (two && !h->graph2_exec) CK(h, capture_steps(h, 2, &h->graph2, &h->graph2_exec), "capture two steps");
-#else
-    const bool two = false;
-#endif
+    CK(h, ensure_graphs(h), "capture step graphs");  // (captured already unless a capture failed)
+    const bool two = n >= 2 && two_step_graphs(h);
     CK(h, ensure_regrown(h), "regrow");
     int64_t i = 0;
     if (two)
@@ -685,30 +713,18 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     return sync(h);
 }
 
-// every float finite (exponent field not all ones), checked on up to 16 host threads: the
-// weights are the bulk of a state (0.5 GB at paper scale) and one core reads ~10 GB/s
-static bool all_finite(const float *x, size_t n) {
-    auto scan = [x](size_t lo, size_t hi) {
-        uint32_t bad = 0;
-        for (size_t k = lo; k < hi; ++k) {
-            uint32_t b;
-            memcpy(&b, x + k, 4);
-            bad |= (uint32_t)((b & 0x7f800000u) == 0x7f800000u);
-        }
-        return bad == 0;
-    };
-    const unsigned hc = std::thread::hardware_concurrency();
-    const size_t nt = n < ((size_t)1 << 22) ? 1 : (hc == 0 ? 1 : hc > 16 ? 16 : hc);
-    if (nt == 1) return scan(0, n);
-    std::vector<std::thread> th;
-    std::vector<char> ok(nt, 0);
-    for (size_t i = 0; i < nt; ++i)
-        th.emplace_back([&, i] { ok[i] = scan(n * i / nt, n * (i + 1) / nt); });
-    for (auto &t : th) t.join();
-    for (char o : ok)
-        if (!o) return false;
-    return true;
+namespace {
+// grow-only device buffer of `rows` rows of `width` floats
+cudaError_t ensure_rows(float **buf, size_t *have, size_t rows, size_t width) {
+    if (rows <= *have) return cudaSuccess;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(buf), rows * width * sizeof(float));
+    if (e == cudaSuccess) *have = rows;
+    return e;
 }
+}  // namespace
 
 sim_status sim_set_state(sim_handle h, const sim_state *in) {
     sim_status st = check_handle(h);
@@ -722,8 +738,10 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
     cudaStream_t s = h->stream;
     // host-side validation on the merged view (device values where a field is NULL)
+    std::vector<uint8_t> live_merged;
     if (S) {
-        std::vector<uint8_t> alive(nw * S);
+        std::vector<uint8_t> &alive = live_merged;
+        alive.resize(nw * S);
         std::vector<int32_t> cell(nw * S);
         if (in->alive) memcpy(alive.data(), in->alive, nw * S);
         else CK(h, cudaMemcpy(alive.data(), p.alive, nw * S, cudaMemcpyDeviceToHost), "download");
@@ -741,24 +759,49 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
             }
         }
     }
-    // weights up to 2 GiB: one staging copy in flight while the host checks them (the state is
-    // untouched until the check passes); larger: checked first, then staged in 256 MB chunks
-    float *wstage = nullptr;
-    const size_t wcount = nw * S * (size_t)d.P;
+    // weights: only the live slots' rows are imported (a dead slot's weights are unspecified,
+    // sim.h), gathered into the device layout in a persistent staging buffer and checked for
+    // non-finite values there; the handle's weights change only after the check passed.
+    // Mapped (page-locked) caller memory is read in place by the gather kernel; pageable
+    // memory is first copied run by run (runs of consecutive live slots) to the device.
+    int n_live = 0;
     if (in->weights && S) {
-        if (wcount * 4 <= ((size_t)2 << 30)) {
-            CK(h, cudaMallocAsync(reinterpret_cast<void **>(&wstage), wcount * 4, s), "alloc");
-            const cudaError_t e = cudaMemcpyAsync(wstage, in->weights, wcount * 4, cudaMemcpyHostToDevice, s);
-            if (e != cudaSuccess) cudaFreeAsync(wstage, s);
-            CK(h, e, "weights");
-        }
-        if (!all_finite(in->weights, wcount)) {
-            if (wstage) {
-                cudaFreeAsync(wstage, s);
-                cudaStreamSynchronize(s);
+        if (nw * S >= ((size_t)1 << 31)) return fail(SIM_E_INVALID, "invalid argument: n_worlds * slots too large");
+        for (size_t g = 0; g < nw * S; ++g) n_live += live_merged[g] ? 1 : 0;
+    }
+    if (n_live > 0) {
+        std::vector<int32_t> live;
+        live.reserve(n_live);
+        for (size_t g = 0; g < nw * S; ++g)
+            if (live_merged[g]) live.push_back((int32_t)g);
+        CK(h, cudaMemcpyAsync(h->live_dev, live.data(), (size_t)n_live * 4, cudaMemcpyHostToDevice, s), "live list");
+        CK(h, ensure_rows(&h->wstage, &h->wstage_rows, (size_t)n_live, (size_t)d.Pd), "alloc staging");
+        const float *src = nullptr;
+        bool by_slot = false;
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, in->weights) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer) {
+            src = static_cast<const float *>(pa.devicePointer);
+            by_slot = true;
+        } else {
+            cudaGetLastError();
+            CK(h, ensure_rows(&h->wcanon, &h->wcanon_rows, (size_t)n_live, (size_t)d.P), "alloc staging");
+            for (int k0 = 0; k0 < n_live;) {
+                int k1 = k0 + 1;
+                while (k1 < n_live && live[k1] == live[k1 - 1] + 1) ++k1;
+                CK(h, cudaMemcpyAsync(h->wcanon + (size_t)k0 * d.P, in->weights + (size_t)live[k0] * d.P,
+                                      (size_t)(k1 - k0) * d.P * 4, cudaMemcpyHostToDevice, s), "weights");
+                k0 = k1;
             }
-            return fail(SIM_E_INVALID, "invalid field: weights (non-finite)");
+            src = h->wcanon;
         }
+        *reinterpret_cast<volatile int32_t *>(h->bad_host) = 0;
+        int32_t *bad_dev = nullptr;
+        CK(h, cudaHostGetDevicePointer(reinterpret_cast<void **>(&bad_dev), h->bad_host, 0), "cudaHostGetDevicePointer");
+        CK(h, eco::launch_weights_gather(p, src, by_slot, h->live_dev, n_live, h->wstage, bad_dev, s), "weights gather");
+        CK(h, cudaStreamSynchronize(s), "sync");
+        if (*reinterpret_cast<volatile int32_t *>(h->bad_host))
+            return fail(SIM_E_INVALID, "invalid field: weights (non-finite in a live slot)");
     }
     if (!in->resources && ((in->t ^ h->t) & 1)) {
         // the current resource plane is selected by step parity: carry it over
@@ -770,12 +813,8 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemcpyAsync(p.t, tv.data(), nw * 8, cudaMemcpyHostToDevice, s), "t");
     h->t = in->t;
     if (in->resources) {
-        uint8_t *tmp;
-        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), nw * HW, s), "alloc");
-        cudaError_t e = cudaMemcpyAsync(tmp, in->resources, nw * HW, cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = eco::launch_pack_resources(p, tmp, s);
-        cudaFreeAsync(tmp, s);
-        CK(h, e, "resources");
+        CK(h, cudaMemcpyAsync(h->res_bytes, in->resources, nw * HW, cudaMemcpyHostToDevice, s), "resources");
+        CK(h, eco::launch_pack_resources(p, h->res_bytes, s), "resources");
     }
     auto put = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
         if (!src || !bytes) return cudaSuccess;
@@ -793,24 +832,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     if (in->logits && S)
         CK(h, cudaMemcpy2DAsync(p.logits, eco::LOGIT_STRIDE * 4, in->logits, 5 * 4, 5 * 4, nw * S,
                                 cudaMemcpyHostToDevice, s), "logits");
-    if (wstage) {
-        cudaError_t e = eco::launch_weights_to_device(p, wstage, 0, nw * S, s);
-        cudaFreeAsync(wstage, s);
-        CK(h, e, "weights");
-    } else if (in->weights && S) {
-        const size_t total_agents = nw * S;
-        const size_t chunk = ((size_t)1 << 26) / (size_t)d.P > 0 ? ((size_t)1 << 26) / (size_t)d.P : 1;
-        float *tmp;
-        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), chunk * d.P * 4, s), "alloc");
-        cudaError_t e = cudaSuccess;
-        for (size_t a0 = 0; a0 < total_agents && e == cudaSuccess; a0 += chunk) {
-            const size_t n = (total_agents - a0) < chunk ? total_agents - a0 : chunk;
-            e = cudaMemcpyAsync(tmp, in->weights + a0 * d.P, n * d.P * 4, cudaMemcpyHostToDevice, s);
-            if (e == cudaSuccess) e = eco::launch_weights_to_device(p, tmp, a0, n, s);
-        }
-        cudaFreeAsync(tmp, s);
-        CK(h, e, "weights");
-    }
+    if (n_live > 0) CK(h, eco::launch_weights_scatter(p, h->wstage, h->live_dev, n_live, s), "weights scatter");
     // scratch and derived structures
     if (S) {
         CK(h, cudaMemsetAsync(p.claim, 0, nw * HW * 8, s), "memset");
@@ -855,10 +877,14 @@ sim_status step_log_copy(sim_handle h, int64_t first, int64_t n, sim_step_record
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     if (wait && (st = sync(h)) != SIM_OK) return st;
     const size_t nw = h->d.n_worlds;
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t step = first + i;
-        CK(h, cudaMemcpyAsync(out + i * nw, h->p.log + (size_t)(step % h->d.log_cap) * nw, nw * sizeof(sim_step_record),
+    // the ring is contiguous by step: [first, first+n) is at most two runs (split at the wrap)
+    int64_t done = 0;
+    while (done < n) {
+        const int64_t slot = (first + done) % h->d.log_cap;
+        const int64_t run = std::min<int64_t>(n - done, h->d.log_cap - slot);
+        CK(h, cudaMemcpyAsync(out + done * nw, h->p.log + (size_t)slot * nw, (size_t)run * nw * sizeof(sim_step_record),
                               cudaMemcpyDeviceToHost, h->stream), "log");
+        done += run;
     }
     return wait ? sync(h) : SIM_OK;
 }
@@ -891,7 +917,8 @@ sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t ca
         h->p.rec_mirror = static_cast<sim_step_record *>(dev);
         h->p.mirror_cap = (int32_t)capacity;
     }
-    drop_graphs(h);  // kernel parameters changed: capture again
+    drop_graphs(h);  // kernel parameters changed: capture again, now (not inside a later sim_step)
+    CK(h, ensure_graphs(h), "capture step graphs");
     return SIM_OK;
 }
 

@@ -21,6 +21,13 @@
 
 #include "../../include/sim.h"
 
+// sim_step(n >= 2) launches two-step graphs in which the second policy is a programmatic
+// dependent of the first k_post (griddepcontrol.wait in the policy).  Defined once here so
+// the host launch (api.cu) and the device wait (step.cu) always agree.
+#ifndef ECO_STEP2_PDL
+#define ECO_STEP2_PDL 1
+#endif
+
 namespace eco {
 
 constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
@@ -227,7 +234,7 @@ struct LaunchCfg {
     int policy_blocks, policy_threads;
     int agent_blocks, agent_threads;
     int post_blocks;  // co-resident blocks of the cooperative k_post
-    int sms;          // multiprocessors (one k_policy_tma CTA each)
+    int sms;          // multiprocessors
 };
 
 cudaError_t launch_init_resources(const DevParams &p, cudaStream_t s);
@@ -235,7 +242,7 @@ size_t init_agents_scratch_bytes(const DevParams &p);
 cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
-cudaError_t policy_prepare();  // kernel attributes (dynamic shared memory of k_policy_tma)
+cudaError_t policy_prepare();  // kernel attributes (dynamic shared memory of k_policy_half)
 // pdl: launched as a programmatic dependent of the preceding k_post (two-step graphs)
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl = false);
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
@@ -256,6 +263,10 @@ cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cuda
 cudaError_t launch_unpack_resources(const DevParams &p, uint8_t *bytes, cudaStream_t s);
 cudaError_t launch_weights_to_device(const DevParams &p, const float *canon, size_t first_agent, size_t n_agents,
                                      cudaStream_t s);
+cudaError_t launch_weights_gather(const DevParams &p, const float *src, bool by_slot, const int32_t *live, int n_live,
+                                  float *stage, int32_t *bad, cudaStream_t s);
+cudaError_t launch_weights_scatter(const DevParams &p, const float *stage, const int32_t *live, int n_live,
+                                   cudaStream_t s);
 cudaError_t launch_weights_to_canon(const DevParams &p, float *canon, size_t first_agent, size_t n_agents,
                                     cudaStream_t s);
 

@@ -14,21 +14,9 @@
 
 #include "phases.cuh"
 
-// cp.async with an .L2::cache_hint operand raised "illegal instruction" on the B200 pool
-// (driver 580.159), so the per-lane column copies use the default L2 policy.
-#ifndef ECO_CPASYNC_HINT
-#define ECO_CPASYNC_HINT 0
-#endif
-#ifndef ECO_SPARSE_BULK
-#define ECO_SPARSE_BULK 0
-#endif
-// Hd = 32 policy kernel: 0 = k_policy_half (one agent per half-warp, per-lane cp.async
-// ring), 1 = the per-warp TMA/cp.async pipeline k_policy_tma (73 us per step at ~5,000
-// agents), 2 = register-streaming k_policy_reg<32> (43 us), 3 = k_policy_ring (one warp per
-// agent, 34 us), 4 = k_policy_stream (persistent warps, ring across agents, 39 us)
-#ifndef ECO_POLICY_TMA
-#define ECO_POLICY_TMA 0
-#endif
+// The Hd = 32 policy kernel is k_policy_half.  Discarded variants (a per-warp TMA/cp.async
+// pipeline, register streaming, one warp per agent with a 12-chunk ring, persistent warps
+// streaming across agents) are recorded with their timings in DESIGN.md §6 and git history.
 // k_policy_half: bulk L2 prefetch of each agent's W_hh|b|W_out block and active columns
 // (1), of the block only (2), none (0: measured fastest, 34 vs 43 us with 1)
 #ifndef ECO_POLICY_PREFETCH
@@ -200,314 +188,17 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
     }
 }
 
-// ============================================================ k_policy_tma (Hd = 32)
-// Per live agent:
-//   z  = sum over ACTIVE inputs j of W_ih^T[j][k][:] + sum_j h_j W_hh^T[j][k][:] + b[k][:]
-//        (x is binary: only the nnz columns with x_j = 1 are read — the algorithmic bytes)
-//   c' = f*c + i*g,  h' = o*tanh(c'),  logits = W_out h' + b_out,  a = argmax   (R12, R28)
-// Lane k of the agent's warp owns hidden unit k and its gate rows (i, f, g, o).
-//
-// Data movement: each warp owns TMA_STAGES shared-memory stages with one mbarrier each and
-// streams a sequence of units through them, keeping up to TMA_STAGES units in flight:
-//   unit 0 of an agent  = the contiguous [W_hh | b | W_out | b_out] block (17,664 B) plus
-//                         its h and c (128 B each): three 1-D TMA bulk copies
-//                         (cp.async.bulk ... complete_tx), expect_tx by lane 0;
-//   units 1.. (<= 32 each) = the agent's active W_ih columns, 512 B each: one cp.async
-//                         (16 B per lane, LDGSTS) warp instruction per column, completion
-//                         counted by cp.async.mbarrier.arrive.noinc of all 32 lanes.
-// Every stage's mbarrier expects 32 arrivals.  Weights stream with an L2 evict-first
-// policy so planes, lists and claims stay L2-resident.  Observation masks are computed
-// 32 agents at a time (one per lane) into a per-warp ring, so no agent waits on its
-// window gather.
-constexpr int TMA_WARPS = 4;
-constexpr int TMA_STAGES = 3;
-constexpr int TMA_STAGE_BYTES = 17920;  // 17,664 (W_hh|b|W_out|b_out|pad) + 128 (h) + 128 (c)
-constexpr int TMA_RING = 64;
-constexpr int TMA_SMEM = TMA_WARPS * TMA_STAGES * TMA_STAGE_BYTES;
-
+// ------------------------------------------------------------- cp.async helpers
 __device__ __forceinline__ uint32_t smem_addr(const void *ptr) {
     return (uint32_t)__cvta_generic_to_shared(ptr);
 }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {  // (the state token is not needed)
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-        : "memory");
-}
+// 16-B global -> shared copy (LDGSTS), default L2 policy (a .L2::cache_hint operand raised
+// "illegal instruction" on the B200 pool, driver 580.159)
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t policy) {
-#if ECO_CPASYNC_HINT
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
-                 "l"(policy)
-                 : "memory");
-#else
     (void)policy;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-#endif
-}
-__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-struct __align__(16) AgentRec {
-    uint64_t lo, hi;   // observation mask
-    int w, i, slot, cell;
-};
-
-// lane-local observation mask (all 2(2r+1) rows by one lane)
-__device__ __forceinline__ void obs_mask_lane(const DevParams &p, int w, int64_t t, int y, int x, uint64_t &m_lo,
-                                              uint64_t &m_hi) {
-    const int wd = 2 * p.r + 1;
-    const uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
-    const uint32_t *O = p.occ + (size_t)w * plane_words(p);
-    uint64_t lo = 0ull, hi = 0ull;
-#pragma unroll 2
-    for (int q = 0; q < 2 * wd; ++q) {
-        const int ch = q / wd, row = q - ch * wd;
-        const int yy = y - p.r + row;
-        if (yy < 0 || yy >= p.H) continue;
-        const uint64_t bits = row_bits((ch ? O : Rn) + (size_t)yy * p.WW, p.WW, x - p.r, wd);
-        const int pos = ch * wd * wd + row * wd;
-        if (pos < 64) {
-            lo |= bits << pos;
-            if (pos + wd > 64) hi |= bits >> (64 - pos);
-        } else {
-            hi |= bits << (pos - 64);
-        }
-    }
-    m_lo = lo;
-    m_hi = hi;
-}
-
-__global__ void __launch_bounds__(TMA_WARPS * 32, 1) k_policy_tma(DevParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[TMA_WARPS][TMA_STAGES];
-    __shared__ AgentRec ring_all[TMA_WARPS][TMA_RING];
-    constexpr unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    step_housekeeping(p);
-    if (lane == 0)
-        for (int s = 0; s < TMA_STAGES; ++s) mbar_init(&bars[wib][s], 32);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    const int forced_on = *p.forced_on;
-    uint64_t policy;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-    uint8_t *stage_base = smem + (size_t)wib * TMA_STAGES * TMA_STAGE_BYTES;
-    AgentRec *ring = ring_all[wib];
-    const uint32_t u0_bytes = (uint32_t)(p.Pd - p.off_hh) * 4u;  // 17,664 at Hd=32, I=98
-
-    // static interleaved assignment over the flattened (world, list position) space
-    const int nwarps = gridDim.x * TMA_WARPS;
-    const long total = (long)p.n_worlds * p.S;
-    long v_next = wib * gridDim.x + blockIdx.x;  // consecutive agents on different SMs
-    int filled = 0;                              // ring entries written (monotonic)
-
-    // fill the ring with the next <= 32 live agents (one per lane); false at the end
-    auto refill = [&]() -> bool {
-        while (v_next < total) {
-            const long v = v_next + (long)lane * nwarps;
-            v_next += 32L * nwarps;
-            AgentRec rec;
-            bool act = false;
-            if (v < total) {
-                rec.w = (int)(v / p.S);
-                rec.i = (int)(v - (long)rec.w * p.S);
-                const int64_t t = p.t[rec.w];
-                if (rec.i < *count_of(p, t, rec.w)) {
-                    act = true;
-                    rec.slot = list_of(p, t, rec.w)[rec.i];
-                    rec.cell = p.cell[(size_t)rec.w * p.S + rec.slot];
-                    const int y = row_of(p, rec.cell);
-                    obs_mask_lane(p, rec.w, t, y, rec.cell - y * p.W, rec.lo, rec.hi);
-                }
-            }
-            const unsigned m = __ballot_sync(FULL, act);
-            if (act) ring[(filled + __popc(m & ((1u << lane) - 1u))) % TMA_RING] = rec;
-            filled += __popc(m);
-            __syncwarp();
-            if (m) return true;
-        }
-        return false;
-    };
-    auto nunits = [](const AgentRec &r) -> int {
-        return 1 + (int)(((unsigned)(__popcll(r.lo) + __popcll(r.hi)) + 31u) / 32u);
-    };
-
-    // issue unit u of agent rec into stage s (all lanes)
-    auto issue = [&](const AgentRec &rec, int u, int s) {
-        uint8_t *dst = stage_base + (size_t)s * TMA_STAGE_BYTES;
-        uint64_t *bar = &bars[wib][s];
-        const size_t gs = (size_t)rec.w * p.S + rec.slot;
-        const float *Wa = p.weights + gs * (size_t)p.Pd;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (u == 0) {
-            if (lane == 0) {
-                mbar_arrive_expect_tx(bar, u0_bytes + 256u);
-                bulk_g2s(dst, Wa + p.off_hh, u0_bytes, bar, policy);
-                bulk_g2s(dst + u0_bytes, p.h + gs * 32, 128u, bar, policy);
-                bulk_g2s(dst + u0_bytes + 128, p.c + gs * 32, 128u, bar, policy);
-            } else {
-                mbar_arrive(bar);
-            }
-        } else {
-            const unsigned r0 = (unsigned)(u - 1) * 32u;
-            uint64_t lo = rec.lo, hi = rec.hi;
-            unsigned rank = 0;
-#if ECO_SPARSE_BULK
-            if (lane == 0)
-                mbar_arrive_expect_tx(bar, min(32u, (unsigned)(__popcll(lo) + __popcll(hi)) - r0) * 512u);
-            __syncwarp();
-#endif
-            while (lo | hi) {  // warp-uniform walk over the active columns in order
-                int col;
-                if (lo) {
-                    col = __ffsll((long long)lo) - 1;
-                    lo &= lo - 1ull;
-                } else {
-                    col = 64 + __ffsll((long long)hi) - 1;
-                    hi &= hi - 1ull;
-                }
-                if (rank >= r0 + 32u) break;
-#if ECO_SPARSE_BULK
-                if (rank >= r0 && lane == 0) bulk_g2s(dst + (size_t)(rank - r0) * 512, Wa + (size_t)col * 128, 512u, bar, policy);
-                ++rank;
-                continue;
-#endif
-                if (rank >= r0) cp_async16(dst + (size_t)(rank - r0) * 512 + lane * 16, Wa + (size_t)col * 128 + lane * 4,
-                                           policy);
-                ++rank;
-            }
-#if ECO_SPARSE_BULK
-            if (lane != 0) mbar_arrive(bar);
-#else
-            cp_async_arrive(bar);
-#endif
-        }
-    };
-
-    PolicyCounters ctr;
-    uint32_t use[TMA_STAGES];
-#pragma unroll
-    for (int s = 0; s < TMA_STAGES; ++s) use[s] = 0u;
-    int pi = 0, ui = 0;  // issue cursor: ring position, unit
-    int pc = 0, uc = 0;  // consume cursor
-    int s_issue = 0, s_cons = 0, in_flight = 0;
-    bool more = true;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float hk = 0.f, ck = 0.f;
-    float wout[5], bout[5];
-
-    while (true) {
-        while (in_flight < TMA_STAGES) {
-            if (pi == filled) {
-                if (!more || !(more = refill())) break;
-            }
-            const AgentRec rec = ring[pi % TMA_RING];
-            issue(rec, ui, s_issue);
-            s_issue = s_issue + 1 == TMA_STAGES ? 0 : s_issue + 1;
-            ++in_flight;
-            if (++ui == nunits(rec)) {
-                ui = 0;
-                ++pi;
-            }
-        }
-        if (in_flight == 0) break;
-        const AgentRec rec = ring[pc % TMA_RING];
-        uint32_t par = 0u;
-#pragma unroll
-        for (int s = 0; s < TMA_STAGES; ++s)
-            if (s == s_cons) par = use[s]++ & 1u;
-        mbar_wait(&bars[wib][s_cons], par);
-        const uint8_t *src = stage_base + (size_t)s_cons * TMA_STAGE_BYTES;
-        if (uc == 0) {
-            const float *tail = reinterpret_cast<const float *>(src);
-            hk = tail[u0_bytes / 4 + lane];
-            ck = tail[u0_bytes / 4 + 32 + lane];
-            const float4 *whh = reinterpret_cast<const float4 *>(src);
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j) {
-                const float hj = __shfl_sync(FULL, hk, j);
-                const float4 v = whh[j * 32 + lane];
-                acc.x = fmaf(hj, v.x, acc.x);
-                acc.y = fmaf(hj, v.y, acc.y);
-                acc.z = fmaf(hj, v.z, acc.z);
-                acc.w = fmaf(hj, v.w, acc.w);
-            }
-            const float4 bb = whh[32 * 32 + lane];
-            acc.x += bb.x;
-            acc.y += bb.y;
-            acc.z += bb.z;
-            acc.w += bb.w;
-#pragma unroll
-            for (int a = 0; a < 5; ++a) {
-                wout[a] = tail[(p.off_out - p.off_hh) + a * 32 + lane];
-                bout[a] = tail[(p.off_bout - p.off_hh) + a];
-            }
-        } else {
-            const unsigned nnz = (unsigned)(__popcll(rec.lo) + __popcll(rec.hi));
-            const unsigned ncols = min(32u, nnz - (unsigned)(uc - 1) * 32u);
-            const float4 *cols = reinterpret_cast<const float4 *>(src);
-            for (unsigned c = 0; c < ncols; ++c) {
-                const float4 v = cols[c * 32 + lane];
-                acc.x += v.x;
-                acc.y += v.y;
-                acc.z += v.z;
-                acc.w += v.w;
-            }
-        }
-        --in_flight;
-        s_cons = s_cons + 1 == TMA_STAGES ? 0 : s_cons + 1;
-        if (++uc == nunits(rec)) {
-            const float ig = sigmoidf_acc(acc.x);
-            const float fg = sigmoidf_acc(acc.y);
-            const float gg = tanhf(acc.z);
-            const float og = sigmoidf_acc(acc.w);
-            const float cn = fg * ck + ig * gg;
-            const float hn = og * tanhf(cn);
-            float lg[5];
-#pragma unroll
-            for (int a = 0; a < 5; ++a) {
-                float s = wout[a] * hn;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-                lg[a] = s + bout[a];
-            }
-            const size_t gs = (size_t)rec.w * p.S + rec.slot;
-            p.h[gs * 32 + lane] = hn;
-            p.c[gs * 32 + lane] = cn;
-            bool bad = !isfinite(hn) || !isfinite(cn);
-            if (lane == 0)
-                agent_epilogue(p, rec.w, rec.i, rec.slot, gs, p.t[rec.w], rec.cell, lg, rec.lo, rec.hi, forced_on, ctr,
-                               bad);
-            if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
-            acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            uc = 0;
-            ++pc;
-        }
-        __syncwarp();
-    }
-    if (lane == 0) ctr.flush(p);
-}
 
 // ============================================================ k_policy_reg (Hd < 32)
 // The same step with register loads; a lane group of HD lanes per agent.
@@ -626,21 +317,8 @@ __global__ void __launch_bounds__(256) k_policy_reg(DevParams p) {
     if (k == 0) ctr.flush(p);
 }
 
-// ============================================================ k_policy_ring (Hd = 32)
-// One warp per live agent (lane k = hidden unit k, gates i,f,g,o in a float4), a block of
-// RING_WARPS independent warps, the grid sized to all slots (inactive warps exit early).
-// The agent's weights are streamed as a sequence of 512-B chunks, one 16-B cp.async per lane
-// (each lane copies exactly the 16 B it later reads: no cross-lane synchronisation), through
-// a per-warp ring of RING_DEPTH chunks kept in flight (one commit group per chunk):
-//   q = 0..31        W_hh^T row q   (acc += h_q * chunk)   - needs only the slot, so these
-//   q = 32           b                                        stream while the observation
-//   q = 33..32+nnz   active W_ih^T columns, ascending (acc += chunk)    mask is gathered
-// The column offsets are compacted once per agent into a per-warp shared list (ballots), and
-// the loops are unrolled so that ring slots and W_hh offsets are compile-time constants.
-constexpr int RING_WARPS = 8;
-constexpr int RING_DEPTH = 12;
-constexpr int RING_COLS = 128;  // >= I = 2(2r+1)^2 for r <= 3 (98)
-constexpr int RING_SMEM = RING_WARPS * RING_DEPTH * 32 * 16;  // 48 KB (dynamic: + lists > 48 KB)
+// ------------------------------------------------------------- cp.async groups
+constexpr int RING_COLS = 128;  // >= I = 2(2r+1)^2 for r <= 3 (98): compacted active-column list
 
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -648,481 +326,14 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(RING_WARPS * 32, 4) k_policy_ring(DevParams p) {
-    constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33;  // chunk q: W_hh row q < 32, b at 32, columns from 33
-    constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ float4 ring_smem[];  // [RING_WARPS][RING_DEPTH][32]
-    __shared__ int s_col[RING_WARPS][RING_COLS];  // float offsets idx * HD * 4 of the active columns
-    __shared__ int s_w[RING_WARPS];
-    __shared__ unsigned long long s_nnz[RING_WARPS], s_ties[RING_WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    step_housekeeping(p);
-    const long total = (long)p.n_worlds * p.S;
-    const long v = (long)blockIdx.x * RING_WARPS + warp;
-    const bool in_range = v < total;
-    const int w = in_range ? (int)(v / p.S) : 0;
-    const int i = in_range ? (int)(v - (long)w * p.S) : 0;
-    const int64_t t = p.t[w];
-    const bool active = in_range && i < *count_of(p, t, w);
-    unsigned long long nnz_w = 0ull, tie_w = 0ull;
-#ifdef ECO_POLICY_TRACE
-    // diagnostic build: per agent (start, mask ready, end, nnz) of the last launch
-    unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(v & 8191);
-    if (lane == 0 && active) trace[0] = globaltimer_ns();
-#endif
-    if (active) {
-        const int slot = list_of(p, t, w)[i];
-        const size_t gs = (size_t)w * p.S + slot;
-        const float *Wl = p.weights + gs * (size_t)p.Pd + lane * 4;  // this lane's 16 B of any chunk
-        const float *Whh = Wl + p.off_hh;
-        float4 *rg = ring_smem + (warp * RING_DEPTH) * 32 + lane;  // ring slot s of this lane: rg[s * 32]
-        int *cols = s_col[warp];
-#pragma unroll
-        for (int q = 0; q < RING_DEPTH; ++q) {  // prologue: W_hh rows 0..RING_DEPTH-1
-            cp_async16(rg + q * 32, Whh + q * HD * 4, 0ull);
-            cp_commit();
-        }
-        const float hk = p.h[gs * HD + lane];
-        const float ck = p.c[gs * HD + lane];
-        float wo[5], bo[5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            wo[a] = __ldg(Wl - lane * 4 + p.off_out + a * HD + lane);
-            bo[a] = __ldg(Wl - lane * 4 + p.off_bout + a);
-        }
-        const int cellv = p.cell[gs];
-        uint64_t m_lo, m_hi;
-        {
-            const int y = row_of(p, cellv), x = cellv - y * p.W;
-            obs_mask(p, w, t, y, x, lane, 32, FULL, m_lo, m_hi);
-        }
-        // compacted list of the active columns (ascending)
-        int nnz = 0;
-#pragma unroll
-        for (int part = 0; part < 4; ++part) {
-            const int bit = part * 32 + lane;
-            const uint64_t word = part < 2 ? m_lo : m_hi;
-            const bool on = ((word >> (bit & 63)) & 1ull) != 0ull;
-            const unsigned bal = __ballot_sync(FULL, on);
-            if (on) cols[nnz + __popc(bal & ((1u << lane) - 1u))] = bit * HD * 4;
-            nnz += __popc(bal);
-        }
-        __syncwarp();
-#ifdef ECO_POLICY_TRACE
-        if (lane == 0) {
-            trace[1] = globaltimer_ns();
-            trace[3] = nnz;
-        }
-#endif
-        const int N = Q0 + nnz;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        // W_hh rows: consume q, refill with chunk q + RING_DEPTH
-#pragma unroll
-        for (int q = 0; q < NHH; ++q) {
-            cp_wait<RING_DEPTH - 1>();
-            const float4 c4 = rg[(q % RING_DEPTH) * 32];
-            const float hj = __shfl_sync(FULL, hk, q);
-            acc.x = fmaf(hj, c4.x, acc.x);
-            acc.y = fmaf(hj, c4.y, acc.y);
-            acc.z = fmaf(hj, c4.z, acc.z);
-            acc.w = fmaf(hj, c4.w, acc.w);
-            const int qn = q + RING_DEPTH;
-            if (qn < NHH) {
-                cp_async16(rg + (q % RING_DEPTH) * 32, Whh + qn * HD * 4, 0ull);
-            } else if (qn == QB) {
-                cp_async16(rg + (q % RING_DEPTH) * 32, Wl + p.off_b, 0ull);
-            } else if (qn - Q0 < nnz) {
-                cp_async16(rg + (q % RING_DEPTH) * 32, Wl + cols[qn - Q0], 0ull);
-            }
-            cp_commit();
-        }
-        {  // q = 32: the bias
-            constexpr int q = QB;
-            cp_wait<RING_DEPTH - 1>();
-            const float4 c4 = rg[(q % RING_DEPTH) * 32];
-            acc.x += c4.x;
-            acc.y += c4.y;
-            acc.z += c4.z;
-            acc.w += c4.w;
-            if (q + RING_DEPTH - Q0 < nnz) cp_async16(rg + (q % RING_DEPTH) * 32, Wl + cols[q + RING_DEPTH - Q0], 0ull);
-            cp_commit();
-        }
-        // active columns q = 33.., RING_DEPTH per round so ring slots stay static
-        for (int q0 = Q0; q0 < N; q0 += RING_DEPTH) {
-#pragma unroll
-            for (int s = 0; s < RING_DEPTH; ++s) {
-                const int q = q0 + s;
-                if (q >= N) break;
-                constexpr int base = Q0 % RING_DEPTH;
-                const int rs = (base + s) % RING_DEPTH;
-                cp_wait<RING_DEPTH - 1>();
-                const float4 c4 = rg[rs * 32];
-                acc.x += c4.x;
-                acc.y += c4.y;
-                acc.z += c4.z;
-                acc.w += c4.w;
-                const int cn = q + RING_DEPTH - Q0;
-                if (cn < nnz) cp_async16(rg + rs * 32, Wl + cols[cn], 0ull);
-                cp_commit();
-            }
-        }
-        cp_wait<0>();
-        const float ig = sigmoidf_acc(acc.x);
-        const float fg = sigmoidf_acc(acc.y);
-        const float gg = tanhf(acc.z);
-        const float og = sigmoidf_acc(acc.w);
-        const float cn = fg * ck + ig * gg;
-        const float hn = og * tanhf(cn);
-        float lg[5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            float s = wo[a] * hn;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-            lg[a] = s + bo[a];
-        }
-        p.h[gs * HD + lane] = hn;
-        p.c[gs * HD + lane] = cn;
-        bool bad = !isfinite(hn) || !isfinite(cn);
-        if (lane == 0) {
-            PolicyCounters one;  // the block flushes the counters below
-            agent_epilogue(p, w, i, slot, gs, t, cellv, lg, m_lo, m_hi, *p.forced_on, one, bad);
-            nnz_w = one.nnz;
-            tie_w = one.ties;
-        }
-        if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
-#ifdef ECO_POLICY_TRACE
-        if (lane == 0) trace[2] = globaltimer_ns();
-#endif
-    }
-    // per-block counters: one atomic per (block, world) run instead of one per agent
-    if (lane == 0) {
-        s_w[warp] = active ? w : -1;
-        s_nnz[warp] = nnz_w;
-        s_ties[warp] = tie_w;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        PolicyCounters ctr;
-        for (int k = 0; k < RING_WARPS; ++k)
-            if (s_w[k] >= 0) {
-                ctr.add(p, s_w[k], s_nnz[k], false);
-                ctr.ties += s_ties[k];
-            }
-        ctr.flush(p);
-    }
-}
-
-// ========================================================== k_policy_stream (Hd = 32)
-// Persistent form of k_policy_ring: a grid of STREAM_BPS blocks per SM, every warp walks the
-// live agents v = g, g + TW, g + 2TW, ... (g = its warp index interleaved over SMs, TW = all
-// warps) and its ring never drains between agents:
-//   * an agent's chunk sequence (32 W_hh rows, b, nnz columns) is padded to a multiple of
-//     RING_DEPTH ticks, so every agent starts on ring slot 0 and all slot indices are
-//     compile-time constants; pad ticks consume nothing and commit empty groups;
-//   * the refills of the current agent's last RING_DEPTH ticks are the next agent's first
-//     W_hh rows;
-//   * the next agent's list slot, cell, h/c and observation rows are gathered in stages at
-//     fixed ticks of the current agent's W_hh phase (0, 4, 10, 18), so its mask and column
-//     list are ready long before its first column chunk is issued.
-constexpr int STREAM_BPS = 3;
-
-// observation rows of one agent: lane q < 2(2r+1) loads the two plane words of its row
-__device__ __forceinline__ void obs_issue(const DevParams &p, int w, int64_t t, int cellv, int lane, uint32_t &wlo,
-                                          uint32_t &whi) {
-    const int wd = 2 * p.r + 1;
-    const int y = row_of(p, cellv), x = cellv - y * p.W;
-    wlo = whi = 0u;
-    if (lane < 2 * wd) {
-        const int ch = lane / wd, row = lane - ch * wd;
-        const int yy = y - p.r + row;
-        if (yy >= 0 && yy < p.H) {
-            const uint32_t *pl = ch ? p.occ + (size_t)w * plane_words(p) : plane_next(p, t) + (size_t)w * plane_words(p);
-            const uint32_t *rw = pl + (size_t)yy * p.WW;
-            const int w0 = (x - p.r) >> 5;
-            if (w0 >= 0 && w0 < p.WW) wlo = __ldg(rw + w0);
-            if (w0 + 1 >= 0 && w0 + 1 < p.WW) whi = __ldg(rw + w0 + 1);
-        }
-    }
-}
-__device__ __forceinline__ void obs_finish(const DevParams &p, int cellv, int lane, uint32_t wlo, uint32_t whi,
-                                           uint64_t &m_lo, uint64_t &m_hi) {
-    const int wd = 2 * p.r + 1;
-    const int y = row_of(p, cellv), x = cellv - y * p.W;
-    (void)y;
-    uint64_t lo = 0ull, hi = 0ull;
-    if (lane < 2 * wd) {
-        const int ch = lane / wd, row = lane - ch * wd;
-        const uint64_t bits = __funnelshift_r(wlo, whi, (x - p.r) & 31) & ((1u << wd) - 1u);
-        const int pos = ch * wd * wd + row * wd;
-        if (pos < 64) {
-            lo = bits << pos;
-            if (pos + wd > 64) hi = bits >> (64 - pos);
-        } else {
-            hi = bits << (pos - 64);
-        }
-    }
-    const uint32_t a0 = __reduce_or_sync(0xffffffffu, (uint32_t)lo), a1 = __reduce_or_sync(0xffffffffu, (uint32_t)(lo >> 32));
-    const uint32_t a2 = __reduce_or_sync(0xffffffffu, (uint32_t)hi), a3 = __reduce_or_sync(0xffffffffu, (uint32_t)(hi >> 32));
-    m_lo = ((uint64_t)a1 << 32) | a0;
-    m_hi = ((uint64_t)a3 << 32) | a2;
-}
-// compacted ascending list of the active columns as float offsets; returns nnz
-__device__ __forceinline__ int obs_columns(uint64_t m_lo, uint64_t m_hi, int lane, int *cols) {
-    int nnz = 0;
-#pragma unroll
-    for (int part = 0; part < 4; ++part) {
-        const int bit = part * 32 + lane;
-        const uint64_t word = part < 2 ? m_lo : m_hi;
-        const bool on = ((word >> (bit & 63)) & 1ull) != 0ull;
-        const unsigned bal = __ballot_sync(0xffffffffu, on);
-        if (on) cols[nnz + __popc(bal & ((1u << lane) - 1u))] = bit * 32 * 4;
-        nnz += __popc(bal);
-    }
-    __syncwarp();
-    return nnz;
-}
-
-__global__ void __launch_bounds__(RING_WARPS * 32, STREAM_BPS) k_policy_stream(DevParams p) {
-    constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = RING_DEPTH;
-    constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ float4 ring_smem[];  // [RING_WARPS][R][32]
-    __shared__ int s_col[RING_WARPS][2][RING_COLS];
-    __shared__ int s_w[RING_WARPS];
-    __shared__ unsigned long long s_nnz[RING_WARPS], s_ties[RING_WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    step_housekeeping(p);
-    const long total = (long)p.n_worlds * p.S;
-    const long TW = (long)gridDim.x * RING_WARPS;
-    float4 *rg = ring_smem + (warp * R) * 32 + lane;  // ring slot s of this lane: rg[s * 32]
-    // world cache of advance(): the first live v' >= v of this warp's residue class
-    int cw = -1, ccount = 0;
-    int64_t ct = 0;
-    auto advance = [&](long v) -> long {
-        while (v < total) {
-            const int w = (int)(v / p.S);
-            if (w != cw) {
-                cw = w;
-                ct = p.t[w];
-                ccount = *count_of(p, ct, w);
-            }
-            if (v - (long)w * p.S < ccount) return v;
-            const long nb = (long)(w + 1) * p.S;  // this residue's first v in world w+1
-            v += ((nb - v + TW - 1) / TW) * TW;
-        }
-        return total;
-    };
-    PolicyCounters ctr;
-    long vA = advance((long)warp * gridDim.x + blockIdx.x);
-    int wA = 0, iA = 0, slotA = 0, cellA = 0, nnzA = 0, buf = 0;
-    int64_t tA = 0;
-    size_t gsA = 0;
-    const float *WlA = nullptr;
-    uint64_t mAlo = 0ull, mAhi = 0ull;
-    float hkA = 0.f, ckA = 0.f;
-    if (vA < total) {  // the first agent: its own gather chain, W_hh streaming meanwhile
-        wA = cw;
-        tA = ct;
-        iA = (int)(vA - (long)wA * p.S);
-        slotA = list_of(p, tA, wA)[iA];
-        gsA = (size_t)wA * p.S + slotA;
-        WlA = p.weights + gsA * (size_t)p.Pd + lane * 4;
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            cp_async16(rg + q * 32, WlA + p.off_hh + q * HD * 4, 0ull);
-            cp_commit();
-        }
-        cellA = p.cell[gsA];
-        hkA = p.h[gsA * HD + lane];
-        ckA = p.c[gsA * HD + lane];
-        uint32_t rlo, rhi;
-        obs_issue(p, wA, tA, cellA, lane, rlo, rhi);
-        obs_finish(p, cellA, lane, rlo, rhi, mAlo, mAhi);
-        nnzA = obs_columns(mAlo, mAhi, lane, s_col[warp][0]);
-    }
-    while (vA < total) {
-#ifdef ECO_POLICY_TRACE
-        unsigned long long *trace = p.phase_ns + 16 + 4 * (size_t)(vA & 8191);
-        if (lane == 0) {
-            trace[0] = globaltimer_ns();
-            trace[1] = trace[0];
-            trace[3] = nnzA;
-        }
-#endif
-        const int NA = Q0 + nnzA, TA = (NA + R - 1) / R * R;
-        const int *colsA = s_col[warp][buf];
-        const float *WhhA = WlA + p.off_hh;
-        float wo[5], bo[5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            wo[a] = __ldg(WlA - lane * 4 + p.off_out + a * HD + lane);
-            bo[a] = __ldg(WlA - lane * 4 + p.off_bout + a);
-        }
-        // next agent (B) state, gathered in stages
-        long vB = total;
-        int wB = 0, slotB = 0, cellB = 0, nnzB = 0;
-        int64_t tB = 0;
-        size_t gsB = 0;
-        const float *WlB = nullptr;
-        uint32_t rlo = 0u, rhi = 0u;
-        uint64_t mBlo = 0ull, mBhi = 0ull;
-        float hkB = 0.f, ckB = 0.f;
-        // refill the slot of tick k with the sequence's chunk kn = k + R: own chunk, a pad
-        // (nothing) or one of B's first W_hh rows
-        auto refill = [&](int kn, int slot) {
-            const float *src = nullptr;
-            if (kn < NA) src = kn < NHH ? WhhA + kn * HD * 4 : (kn == QB ? WlA + p.off_b : WlA + colsA[kn - Q0]);
-            else if (kn >= TA && vB < total) src = WlB + p.off_hh + (kn - TA) * HD * 4;
-            if (src) cp_async16(rg + slot * 32, src, 0ull);
-            cp_commit();
-        };
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < NHH; ++k) {  // W_hh rows
-            if (k == 0) {
-                vB = advance(vA + TW);
-                if (vB < total) {
-                    wB = cw;
-                    tB = ct;
-                    slotB = list_of(p, tB, wB)[vB - (long)wB * p.S];
-                }
-            } else if (k == 4 && vB < total) {
-                gsB = (size_t)wB * p.S + slotB;
-                WlB = p.weights + gsB * (size_t)p.Pd + lane * 4;
-                cellB = p.cell[gsB];
-                hkB = p.h[gsB * HD + lane];
-                ckB = p.c[gsB * HD + lane];
-            } else if (k == 10 && vB < total) {
-                obs_issue(p, wB, tB, cellB, lane, rlo, rhi);
-            } else if (k == 18 && vB < total) {
-                obs_finish(p, cellB, lane, rlo, rhi, mBlo, mBhi);
-                nnzB = obs_columns(mBlo, mBhi, lane, s_col[warp][buf ^ 1]);
-            }
-            cp_wait<R - 1>();
-            const float4 c4 = rg[(k % R) * 32];
-            const float hj = __shfl_sync(FULL, hkA, k);
-            acc.x = fmaf(hj, c4.x, acc.x);
-            acc.y = fmaf(hj, c4.y, acc.y);
-            acc.z = fmaf(hj, c4.z, acc.z);
-            acc.w = fmaf(hj, c4.w, acc.w);
-            if (k + R < NHH) {
-                cp_async16(rg + (k % R) * 32, WhhA + (k + R) * HD * 4, 0ull);
-                cp_commit();
-            } else if (k + R == QB) {
-                cp_async16(rg + (k % R) * 32, WlA + p.off_b, 0ull);
-                cp_commit();
-            } else {
-                refill(k + R, k % R);
-            }
-        }
-        {  // tick 32: the bias
-            constexpr int k = QB;
-            cp_wait<R - 1>();
-            const float4 c4 = rg[(k % R) * 32];
-            acc.x += c4.x;
-            acc.y += c4.y;
-            acc.z += c4.z;
-            acc.w += c4.w;
-            refill(k + R, k % R);
-        }
-#pragma unroll
-        for (int k = Q0; k < 3 * R; ++k) {  // ticks 33..35 (slots 9..11)
-            cp_wait<R - 1>();
-            if (k < NA) {
-                const float4 c4 = rg[(k % R) * 32];
-                acc.x += c4.x;
-                acc.y += c4.y;
-                acc.z += c4.z;
-                acc.w += c4.w;
-            }
-            refill(k + R, k % R);
-        }
-        for (int k0 = 3 * R; k0 < TA; k0 += R) {  // full rounds of R ticks
-#pragma unroll
-            for (int s2 = 0; s2 < R; ++s2) {
-                const int k = k0 + s2;
-                cp_wait<R - 1>();
-                if (k < NA) {
-                    const float4 c4 = rg[s2 * 32];
-                    acc.x += c4.x;
-                    acc.y += c4.y;
-                    acc.z += c4.z;
-                    acc.w += c4.w;
-                }
-                refill(k + R, s2);
-            }
-        }
-#ifdef ECO_POLICY_TRACE
-        if (lane == 0) trace[1] = globaltimer_ns();
-#endif
-        // epilogue of A (B's first R chunks are in flight)
-        const float ig = sigmoidf_acc(acc.x);
-        const float fg = sigmoidf_acc(acc.y);
-        const float gg = tanhf(acc.z);
-        const float og = sigmoidf_acc(acc.w);
-        const float cn = fg * ckA + ig * gg;
-        const float hn = og * tanhf(cn);
-        float lg[5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            float sm = wo[a] * hn;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(FULL, sm, o);
-            lg[a] = sm + bo[a];
-        }
-        p.h[gsA * HD + lane] = hn;
-        p.c[gsA * HD + lane] = cn;
-        bool bad = !isfinite(hn) || !isfinite(cn);
-        if (lane == 0) agent_epilogue(p, wA, iA, slotA, gsA, tA, cellA, lg, mAlo, mAhi, *p.forced_on, ctr, bad);
-        if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
-#ifdef ECO_POLICY_TRACE
-        if (lane == 0) trace[2] = globaltimer_ns();
-#endif
-        // B becomes the current agent
-        vA = vB;
-        wA = wB;
-        tA = tB;
-        iA = (int)(vB - (long)wB * p.S);
-        slotA = slotB;
-        gsA = gsB;
-        WlA = WlB;
-        cellA = cellB;
-        nnzA = nnzB;
-        mAlo = mBlo;
-        mAhi = mBhi;
-        hkA = hkB;
-        ckA = ckB;
-        buf ^= 1;
-    }
-    cp_wait<0>();
-    // per-block counters: one atomic per (block, world) run
-    if (lane == 0) {
-        s_w[warp] = ctr.w;
-        s_nnz[warp] = ctr.nnz;
-        s_ties[warp] = ctr.ties;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        PolicyCounters bc;
-        for (int k = 0; k < RING_WARPS; ++k)
-            if (s_w[k] >= 0) {
-                bc.add(p, s_w[k], s_nnz[k], false);
-                bc.ties += s_ties[k];
-            }
-        bc.flush(p);
-    }
-}
 
 // ============================================================ k_policy_half (Hd = 32)
-// k_policy_ring with one agent per HALF-warp, so that a launch keeps every live agent of the
+// One agent per HALF-warp, so that a launch keeps every live agent of the
 // paper-scale world resident at once (4 blocks x 16 agents per SM = 9,472 >= 8,192 slots):
 // no second wave, the tail is one agent's own latency.  Half-lane h owns hidden units h and
 // h+16 (two float4 gate accumulators) and copies/reads their 2 x 16 B of every 512-B chunk.
 // Ring: HALF_DEPTH chunks per agent (3 KB) in flight; 16 agents per block interleaved over
 // the blocks (agent v = a * gridDim + block).  Column indices are compacted to bytes.
-#ifndef ECO_STEP2_PDL
-#define ECO_STEP2_PDL 1  // sim_step(n >= 2): two-step graphs, the second policy a programmatic dependent
-#endif
 #ifndef ECO_POST_PDL
 #define ECO_POST_PDL 1  // measured: 48.0 -> 47.45 us per step (2, the policy triggering early: 48.65)
 #endif
@@ -1587,31 +798,13 @@ cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
         case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<4>, threads, 0);
         case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<8>, threads, 0);
         case 16: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<16>, threads, 0);
-#if ECO_POLICY_TMA == 1
-        case 32: *blocks_per_sm = 1; return cudaSuccess;
-#elif ECO_POLICY_TMA == 2
-        case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<32>, threads, 0);
-#elif ECO_POLICY_TMA == 3
-        case 32:
-            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_ring, RING_WARPS * 32, RING_SMEM);
-#elif ECO_POLICY_TMA == 4
-        case 32:
-            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_stream, RING_WARPS * 32, RING_SMEM);
-#else
         case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_half<false>, HALF_THREADS, HALF_SMEM);
-#endif
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t policy_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(k_policy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, RING_SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, RING_SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_policy_half<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
@@ -1627,13 +820,6 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
         case 4: k_policy_reg<4><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
         case 8: k_policy_reg<8><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
         case 16: k_policy_reg<16><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
-#if ECO_POLICY_TMA == 1
-        case 32: k_policy_tma<<<lc.sms, TMA_WARPS * 32, TMA_SMEM, s>>>(p); break;
-#elif ECO_POLICY_TMA == 2
-        case 32: k_policy_reg<32><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
-#elif ECO_POLICY_TMA == 4
-        case 32: k_policy_stream<<<lc.policy_blocks, RING_WARPS * 32, RING_SMEM, s>>>(p); break;
-#elif ECO_POLICY_TMA == 0
         case 32: {
             // one half-warp per slot; at least enough blocks for the housekeeping's clear of
             // the claimed-cell bitmap (a large grid with few slots)
@@ -1664,15 +850,6 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
             else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             break;
         }
-#else
-        case 32: {
-            // one warp per slot of every world; blocks past the live agents exit at once
-            const long slots = (long)p.n_worlds * p.S;
-            const unsigned blocks = (unsigned)((slots + RING_WARPS - 1) / RING_WARPS);
-            k_policy_ring<<<blocks > 0 ? blocks : 1, RING_WARPS * 32, RING_SMEM, s>>>(p);
-            break;
-        }
-#endif
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -2030,7 +1207,7 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-bool policy_supports_shard() { return ECO_POLICY_TMA == 0; }  // k_policy_half
+bool policy_supports_shard() { return true; }  // k_policy_half honours ownership
 
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (!p.split) return cudaSuccess;

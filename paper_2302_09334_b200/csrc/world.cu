@@ -243,4 +243,51 @@ cudaError_t launch_weights_to_canon(const DevParams &p, float *canon, size_t fir
     return cudaGetLastError();
 }
 
+// ------------------------------------------- set_state: the live agents' weights only
+// sim_set_state imports the weights of LIVE slots only (a dead slot's fields are unspecified,
+// sim.h): live[k] = w*S + slot for k < n_live.  Gather: canonical row k of the source (row
+// live[k] when by_slot, i.e. the caller's whole [n_worlds*S][P] array read in place from
+// mapped host memory; row k of a compacted device copy otherwise) -> device-layout row k of
+// `stage`, and any non-finite value sets *bad (the handle's weights are not touched yet).
+// Scatter (after the host saw *bad == 0): stage row k -> the weights of live[k].
+__global__ void k_weights_gather(DevParams p, const float *src, int by_slot, const int32_t *live, int n_live,
+                                 float *stage, int32_t *bad) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p.P) return;
+    const int d = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
+    int nonfin = 0;
+    for (int k = blockIdx.y; k < n_live; k += gridDim.y) {
+        const size_t row = by_slot ? (size_t)live[k] : (size_t)k;
+        const float v = src[row * p.P + j];
+        nonfin |= !isfinite(v);
+        stage[(size_t)k * p.Pd + d] = v;
+    }
+    if (nonfin) atomicOr(bad, 1);
+}
+
+__global__ void k_weights_scatter(DevParams p, const float4 *stage, const int32_t *live, int n_live) {
+    const int q4 = p.Pd >> 2;  // float4 per row (Pd is a multiple of 32 floats)
+    for (int k = blockIdx.y; k < n_live; k += gridDim.y) {
+        float4 *dst = reinterpret_cast<float4 *>(p.weights + (size_t)live[k] * p.Pd);
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < q4; q += gridDim.x * blockDim.x)
+            dst[q] = stage[(size_t)k * q4 + q];
+    }
+}
+
+cudaError_t launch_weights_gather(const DevParams &p, const float *src, bool by_slot, const int32_t *live, int n_live,
+                                  float *stage, int32_t *bad, cudaStream_t s) {
+    if (n_live <= 0) return cudaSuccess;
+    dim3 g((unsigned)((p.P + 255) / 256), (unsigned)(n_live < 8192 ? n_live : 8192));
+    k_weights_gather<<<g, 256, 0, s>>>(p, src, by_slot ? 1 : 0, live, n_live, stage, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_weights_scatter(const DevParams &p, const float *stage, const int32_t *live, int n_live,
+                                   cudaStream_t s) {
+    if (n_live <= 0) return cudaSuccess;
+    dim3 g((unsigned)((p.Pd / 4 + 255) / 256), (unsigned)(n_live < 8192 ? n_live : 8192));
+    k_weights_scatter<<<g, 256, 0, s>>>(p, reinterpret_cast<const float4 *>(stage), live, n_live);
+    return cudaGetLastError();
+}
+
 }  // namespace eco

@@ -10,7 +10,9 @@ One step is
 
 where the buffers are the move records by slot (zero for the other ranks' agents) and the
 policy counters.  The allreduce is the step's only collective; everything runs on the
-library's stream (the handle is created on torch's current stream, so NCCL orders with it).
+library's stream: the handle is created on torch's current stream of `device` when no
+stream is given, and the allreduce is issued with that stream current, so NCCL (which
+orders with torch's current stream) runs between sim_step_policy and sim_step_post.
 The trajectory equals the unsharded world's exactly (tests/test_gpu_parity.py).
 """
 from . import sim
@@ -29,6 +31,10 @@ class ShardedWorld:
         self.dist, self.group = dist, group
         self.n_ranks = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        import torch
+        if stream is None:  # the library must share NCCL's stream (torch's current one)
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
         self.world = sim.World(wc, device=device, stream=stream, log_capacity=log_capacity)
         if self.n_ranks > 1:
             self.world.shard(self.n_ranks, self.rank)
@@ -42,10 +48,12 @@ class ShardedWorld:
         if self.n_ranks == 1:
             self.world.step(n)
             return
-        for _ in range(n):
-            self.world.step_policy()
-            combine_(self._bufs, self.dist, self.group)
-            self.world.step_post()
+        import torch
+        with torch.cuda.stream(self.stream):
+            for _ in range(n):
+                self.world.step_policy()
+                combine_(self._bufs, self.dist, self.group)
+                self.world.step_post()
 
     def __getattr__(self, name):  # step_log, get_state, synchronize, destroy, ...
         return getattr(self.world, name)

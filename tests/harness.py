@@ -1,14 +1,15 @@
 """Comparison protocol between the CUDA library and the oracle (SURVEY.md
-§8c C.6): integer state bit-exact, fp32 LSTM state within |g - o| <= 1e-5 max(1, |o|)
-(R27: "1e-5 relative" taken relative to the unit scale of h in (-1, 1), c and logits, since
-fp32 summation of ~130 products leaves an absolute floor of a few 1e-7 near zero), weights
-bit-exact up to counted 1-ulp differences (R29), argmax disagreements only at flagged
-near-ties (margin < 1e-4, R28)."""
+§8c C.6): integer state bit-exact, fp32 LSTM state within |g - o| <= 1e-5 |o| + 2e-6
+(R27: north_star's "1e-5 relative" plus an absolute floor of 2e-6 = about twice the
+largest fp32-vs-fp64 difference measured near zero, 4.8e-7 .. 1e-6: fp32 summation of
+~130 products cannot be relative near 0), weights bit-exact up to counted 1-ulp
+differences (R29), argmax disagreements only at flagged near-ties (margin < 1e-4, R28)."""
 import numpy as np
 
 import oracle
 
-REL, ABS = 1e-5, 1e-5
+REL, ABS = 1e-5, 2e-6
+MAX_ABS_SEEN = {"h": 0.0, "c": 0.0, "logits": 0.0}  # largest |g - o| compared (reported by tests)
 INT_FIELDS = ("cell", "energy", "age", "repr", "ate")
 REC_EXACT = ("grown", "eaten", "births", "deaths_energy", "deaths_age", "deferred_no_cell", "deferred_claim",
              "deferred_capacity", "population", "resources")
@@ -47,6 +48,9 @@ def compare_ints(g: dict, o: dict, where: str = ""):
 
 def compare_floats(g: dict, o: dict, slots, where: str = ""):
     for f in ("h", "c", "logits"):
+        d = np.abs(np.asarray(g[f][slots], np.float64) - o[f][slots])
+        if d.size:
+            MAX_ABS_SEEN[f] = max(MAX_ABS_SEEN[f], float(d.max()))
         ok = close(g[f][slots], o[f][slots])
         assert ok.all(), (f"{where}: {f} out of tolerance at slots "
                           f"{np.asarray(slots)[np.flatnonzero(~ok.all(axis=1))][:5].tolist()}: "

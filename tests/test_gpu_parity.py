@@ -2,15 +2,16 @@
 
 Integer state, step records and slot layout bit-exact; LSTM state within R27; weights
 bit-exact up to counted 1-ulp differences (R29); argmax disagreements only at flagged
-near-ties (R28).  Sizes span several tiles and ragged tails; BASELINE sizes are covered
-by sampled one-step checks in test_gpu_fullsize.py.
+near-ties (R28).  Sizes span several tiles and ragged tails; the BASELINE configs at their
+full sizes (8192x16384 regrowth, the 64-world ensemble, ensemble worlds at 8,192 slots) are
+in test_gpu_fullsize.py.
 """
 import numpy as np
 import pytest
 
 import oracle
 import workloads
-from harness import (compare_floats, compare_ints, compare_record, compare_weights, gpu_world_state, lockstep)
+from harness import (MAX_ABS_SEEN, compare_floats, compare_ints, compare_record, compare_weights, gpu_world_state, lockstep)
 from scenario import E, N, STAY, W, build_state, forced, small_config
 
 pytestmark = pytest.mark.gpu
@@ -124,7 +125,8 @@ def test_paper_scale_lockstep_200_steps():
     world = sim.World(wc)
     orc = oracle.OracleWorld(wc)
     flips, n, nulp = lockstep(world, orc, 200, check_weights_every=100)
-    print(f"paper-scale: {n} agent-steps compared, {flips} near-tie disagreements, {nulp} one-ulp weights")
+    print(f"paper-scale: {n} agent-steps compared, {flips} near-tie disagreements, {nulp} one-ulp weights, "
+          f"max |g-o| {MAX_ABS_SEEN}")
     assert n > 200000
 
 
