@@ -242,7 +242,9 @@ cudaError_t launch_phase(sim_ctx *h, int k) {
 cudaError_t enqueue_step(sim_ctx *h, bool pdl = false) {
     cudaError_t e;
     if ((e = eco::launch_policy(h->p, h->lc, h->stream, pdl)) != cudaSuccess) return e;
-    return eco::launch_post(h->p, h->lc, h->bar, h->stream);
+    if ((e = eco::launch_post(h->p, h->lc, h->bar, h->stream)) != cudaSuccess) return e;
+    if (h->p.regrow_split) return eco::launch_regrow(h->p, 0, h->stream);  // step t+1 (k_post advanced t)
+    return cudaSuccess;
 }
 
 // capture `steps` (1 or 2) graph steps; in two, the second policy depends programmatically
@@ -389,6 +391,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
 
     DevParams &p = h->p;
     p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
+    p.row_lo = 0; p.row_hi = d.H;
+    p.regrow_split = 0;
     p.hd_shift = 0;
     while ((1 << p.hd_shift) < d.Hd) ++p.hd_shift;  // Hd is a power of two (validated)
     p.n_worlds = d.n_worlds; p.r = cfg->obs_radius; p.log_cap = d.log_cap;
@@ -506,7 +510,9 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
         h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    CKC(dalloc(h, &h->bar, 6), "alloc");  // [0] arrivals, [1] next base, [2] births flag, [3..4] window-end counters, [5] spare
+    // [0] arrivals, [1] next base, [2] births flag, [3..4] window-end counters, [5] spare
+    CKC(dalloc(h, &h->bar, 6), "alloc");
+    p.regrow_split = (S == 0 && eco::regrow_tiled(p)) ? 1 : 0;  // agent-free benchmark grids
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");
@@ -645,6 +651,7 @@ sim_status sim_step_graph_timed(sim_handle h, float out_ms[2]) {
     CK(h, eco::launch_policy(h->p, h->lc, h->stream), "policy");
     CK(h, cudaEventRecord(h->ev[1], h->stream), "event");
     CK(h, eco::launch_post(h->p, h->lc, h->bar, h->stream), "post");
+    if (h->p.regrow_split) CK(h, eco::launch_regrow(h->p, 0, h->stream), "regrow");
     CK(h, cudaEventRecord(h->ev[2], h->stream), "event");
     CK(h, cudaEventSynchronize(h->ev[2]), "event sync");
     h->t += 1;

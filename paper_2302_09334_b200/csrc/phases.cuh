@@ -105,30 +105,11 @@ __device__ __forceinline__ uint32_t ge_const(const uint32_t c[5], int m) {
     return gt | eq;
 }
 
-// Regrow groups [g0, g0 + ng) (4 cells each) of word (y, wx) of world w for step `t`:
-// src = plane_cur(t).  Returns the grown bits (the caller ORs the lanes of the word and
-// stores cur | grow into plane_next(t)); `cur` gets the word's current bits.
-__device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int y, int wx, int64_t t, int g0, int ng,
-                                                  uint32_t &cur) {
-    const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
-    // a word whose cells are all full cannot grow: no window, no count, no draw
-    cur = ld_plain(src + (size_t)y * p.WW + wx);
-    {
-        const int nv = p.W - (wx << 5);  // valid cells in the word
-        const uint32_t pad = nv >= 32 ? 0u : ~((1u << nv) - 1u);
-        if ((cur | pad) == 0xFFFFFFFFu) return 0u;
-    }
-    uint32_t win[5][3];
-#pragma unroll
-    for (int dy = -2; dy <= 2; ++dy) {
-        const int yy = y + dy;
-#pragma unroll
-        for (int dw = -1; dw <= 1; ++dw) {
-            const int ww = wx + dw;
-            win[dy + 2][dw + 1] =
-                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
-        }
-    }
+// The grown bits of groups [g0, g0 + ng) (4 cells each) of word (y, wx) of world w for step
+// `t`, given its window win[dy + 2][dw + 1] = word (y + dy, wx + dw) of R_t (0 off-grid) and
+// cur = win[2][1].  Shared by the L2-gather path below and the shared-memory-tiled kernel.
+__device__ __forceinline__ uint32_t regrow_window(const DevParams &p, int w, int y, int wx, int64_t t, int g0, int ng,
+                                                  const uint32_t (&win)[5][3], uint32_t cur) {
     uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
 #pragma unroll
     for (int r = 0; r < 5; ++r) {  // disc row dy = r - 2: offsets dx = -m..m (compact loop)
@@ -169,6 +150,36 @@ __device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int
     return grow;
 }
 
+// a word whose real cells are all full cannot grow: no window, no count, no draw
+__device__ __forceinline__ bool word_full(const DevParams &p, int wx, uint32_t cur) {
+    const int nv = p.W - (wx << 5);  // valid cells in the word
+    const uint32_t pad = nv >= 32 ? 0u : ~((1u << nv) - 1u);
+    return (cur | pad) == 0xFFFFFFFFu;
+}
+
+// Regrow groups [g0, g0 + ng) of word (y, wx) of world w for step `t`, the window gathered
+// from src = plane_cur(t) with coherent loads (inside the cooperative kernel the plane was
+// written earlier in the same launch).  Returns the grown bits (the caller ORs the lanes of
+// the word and stores cur | grow into plane_next(t)); `cur` gets the word's current bits.
+__device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int y, int wx, int64_t t, int g0, int ng,
+                                                  uint32_t &cur) {
+    const uint32_t *src = plane_cur(p, t) + (size_t)w * plane_words(p);
+    cur = ld_plain(src + (size_t)y * p.WW + wx);
+    if (word_full(p, wx, cur)) return 0u;
+    uint32_t win[5][3];
+#pragma unroll
+    for (int dy = -2; dy <= 2; ++dy) {
+        const int yy = y + dy;
+#pragma unroll
+        for (int dw = -1; dw <= 1; ++dw) {
+            const int ww = wx + dw;
+            win[dy + 2][dw + 1] =
+                (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW) ? ld_plain(src + (size_t)yy * p.WW + ww) : 0u;
+        }
+    }
+    return regrow_window(p, w, y, wx, t, g0, ng, win, cur);
+}
+
 // Grid-stride regrowth of every world for step `tstep` (all worlds share t).  A word's 8
 // four-cell groups are split over L = 1..8 consecutive lanes (as many as the threads allow:
 // a small grid gets 8 short chains per word instead of one long one); the lanes of a word
@@ -176,7 +187,8 @@ __device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int
 // record of that step.  Must be called by all 32 lanes of a warp.
 __device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, size_t gtid, size_t gthreads) {
     const int real_words = (p.W + 31) >> 5;
-    const size_t per_world = (size_t)p.H * real_words;
+    const int rows = p.row_hi - p.row_lo;  // the rows this handle owns (all H unless banded)
+    const size_t per_world = (size_t)rows * real_words;
     const size_t total = per_world * p.n_worlds;
     int lsh = 0;  // L = 1 << lsh lanes per word
     while (lsh < 3 && (total << (lsh + 1)) <= gthreads) ++lsh;
@@ -195,6 +207,7 @@ __device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, 
             const uint32_t r = k32 - (uint32_t)w * pw32;
             y = (int)(r / (uint32_t)real_words);
             wx = (int)(r - (uint32_t)y * (uint32_t)real_words);
+            y += p.row_lo;
             grow = regrow_groups(p, w, y, wx, tstep, sub * ng, ng, cur);
         }
         for (int o = 1; o < L; o <<= 1) grow |= __shfl_xor_sync(0xffffffffu, grow, o);

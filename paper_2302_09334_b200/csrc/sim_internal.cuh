@@ -39,6 +39,9 @@ constexpr uint8_t NO_DIR = 0xFF;
 // captured CUDA graph serves every step; the step index lives in device memory).
 struct DevParams {
     int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, r, log_cap;
+    int row_lo, row_hi;  // rows this handle owns: [0, H) unless it is one latitude band (banded mode)
+    int regrow_split;    // 1: k_post leaves the regrowth of step t+1 to k_regrow_tiled, launched after
+                         // it (agent-free worlds of many words: the configs[2] benchmark grids)
     int hd_shift;  // Hd = 1 << hd_shift
     double invW;   // 1 / W (cell -> row without an integer division)
     int repr_steps, max_age;
@@ -242,6 +245,7 @@ size_t init_agents_scratch_bytes(const DevParams &p);
 cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
+bool regrow_tiled(const DevParams &p);  // launch_regrow uses the shared-memory-tiled kernel
 cudaError_t policy_prepare();  // kernel attributes (dynamic shared memory of k_policy_half)
 // pdl: launched as a programmatic dependent of the preceding k_post (two-step graphs)
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl = false);

@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             const size_t bthr = (size_t)nb * gw * 32;
             const uint64_t r0 = b == 0 ? globaltimer_ns() : 0ull;
             move_claim_reset(p, T, btid, bthr);
-            regrow_phase(p, T + 1, btid, bthr);
+            if (!p.regrow_split) regrow_phase(p, T + 1, btid, bthr);
             if (b == 0 && lane == 0) atomicAdd(p.phase_ns + 9, globaltimer_ns() - r0);
 #if ECO_MUT_WARM
             const MutArgs ma = mut_args(p);
@@ -1178,9 +1178,139 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
 }
 
 // --------------------------------------------------------------------------- launchers
+// ------------------------------------------------ a1, large grids: shared-memory tiles
+// PAPER.md:255-267 as regrow_window, for grids of many words (the configs[2] benchmark
+// grids, the first step of a large world): a tile is RG_TH rows x RG_TW words (one word per
+// thread: warp = row, lane = word); its window rows y0-2 .. y0+RG_TH+1 and words wx0-4 ..
+// wx0+RG_TW+3 are staged in shared memory with 128-bit loads (one HBM read per word, the
+// halo re-reads of neighbouring tiles hit L2), so each word's 15-word window costs 15
+// shared-memory reads instead of 15 L2 round trips.  Persistent blocks walk the tiles with
+// the next tile's vector already in flight (one register per thread); output words are
+// coalesced 128-B warp stores; all-full words skip the count and the draws.  The grown
+// count is summed per block and added once per block and world.
+constexpr int RG_TW = 32, RG_TH = 8;              // one 256-thread block per tile
+constexpr int RG_VW = (RG_TW + 8) / 4;            // uint4 per staged row (4-word halo each side)
+constexpr int RG_LOADS = (RG_TH + 4) * RG_VW;     // 120 vectors per tile (threads 0..119)
+static_assert(RG_LOADS <= RG_TH * 32, "one staged vector per thread");
+
+__device__ __forceinline__ uint4 rg_load(const DevParams &p, const uint32_t *src, int y0, int wx0, int k) {
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (k < RG_LOADS) {
+        const int r = k / RG_VW, q = k - r * RG_VW;
+        const int yy = y0 - 2 + r, ww = wx0 - 4 + 4 * q;  // ww, WW multiples of 4: aligned, in-row
+        if (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW)
+            v = __ldg(reinterpret_cast<const uint4 *>(src + (size_t)yy * p.WW + ww));
+    }
+    return v;
+}
+
+__device__ __forceinline__ void rg_flush(const DevParams &p, int64_t tstep, int w, unsigned long long acc,
+                                         unsigned long long *s_red) {
+    acc = __reduce_add_sync(0xffffffffu, (unsigned)acc);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sum = 0;
+        for (int i = 0; i < RG_TH; ++i) sum += s_red[i];
+        if (sum) atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, tstep, w)->grown), sum);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(RG_TH * 32, 4) k_regrow_tiled(DevParams p, int ahead) {
+    __shared__ uint4 s_tile[RG_TH + 4][RG_VW];
+    __shared__ unsigned long long s_red[RG_TH];
+    const int64_t tstep = p.t[0] + ahead;
+    const int real_words = (p.W + 31) >> 5;
+    const int ntx = (real_words + RG_TW - 1) / RG_TW, nty = (p.row_hi - p.row_lo + RG_TH - 1) / RG_TH;
+    const int per_world = ntx * nty;
+    const int ntiles = per_world * p.n_worlds;  // validated: n_worlds * H * words < 2^31
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t pw = plane_words(p);
+    auto coords = [&](int tile, int &w, int &y0, int &wx0) {
+        w = tile / per_world;
+        const int r = tile - w * per_world;
+        const int ty = r / ntx;
+        y0 = p.row_lo + ty * RG_TH;
+        wx0 = (r - ty * ntx) * RG_TW;
+    };
+    unsigned long long acc = 0;
+    int acc_w = -1;
+    int tile = blockIdx.x;
+    uint4 pre = make_uint4(0u, 0u, 0u, 0u);
+    if (tile < ntiles) {
+        int w, y0, wx0;
+        coords(tile, w, y0, wx0);
+        pre = rg_load(p, plane_cur(p, tstep) + (size_t)w * pw, y0, wx0, threadIdx.x);
+    }
+    for (; tile < ntiles; tile += gridDim.x) {
+        int w, y0, wx0;
+        coords(tile, w, y0, wx0);
+        if (w != acc_w) {  // block-uniform
+            if (acc_w >= 0) rg_flush(p, tstep, acc_w, acc, s_red);
+            acc_w = w;
+            acc = 0;
+        }
+        if (threadIdx.x < RG_LOADS) s_tile[threadIdx.x / RG_VW][threadIdx.x % RG_VW] = pre;
+        __syncthreads();
+        {  // the next tile's vector in flight while this one is computed
+            const int nt = tile + gridDim.x;
+            if (nt < ntiles) {
+                int w2, y2, x2;
+                coords(nt, w2, y2, x2);
+                pre = rg_load(p, plane_cur(p, tstep) + (size_t)w2 * pw, y2, x2, threadIdx.x);
+            }
+        }
+        const int y = y0 + warp, wx = wx0 + lane;
+        if (y < p.row_hi && wx < real_words) {
+            const uint32_t *sw = reinterpret_cast<const uint32_t *>(&s_tile[0][0]);
+            constexpr int RS = RG_VW * 4;  // words per staged row
+            const uint32_t cur = sw[(warp + 2) * RS + lane + 4];
+            uint32_t grow = 0u;
+            if (!word_full(p, wx, cur)) {
+                uint32_t win[5][3];
+#pragma unroll
+                for (int r = 0; r < 5; ++r)
+#pragma unroll
+                    for (int dw = 0; dw < 3; ++dw) win[r][dw] = sw[(warp + r) * RS + lane + 3 + dw];
+                grow = regrow_window(p, w, y, wx, tstep, 0, 8, win, cur);
+            }
+            plane_next(p, tstep)[(size_t)w * pw + (size_t)y * p.WW + wx] = cur | grow;
+            acc += (unsigned long long)__popc(grow);
+        }
+        __syncthreads();  // the tile's shared reads are done before the next tile is staged
+    }
+    if (acc_w >= 0) rg_flush(p, tstep, acc_w, acc, s_red);
+}
+
+// words of all worlds from which the tiled kernel is used (the per-word gather path keeps
+// small grids on up to 8 lanes per word, shorter Philox chains)
+constexpr size_t RG_TILED_MIN_WORDS = 65536;
+
+bool regrow_tiled(const DevParams &p) {
+    const int real_words = (p.W + 31) >> 5;
+    return (size_t)(p.row_hi - p.row_lo) * real_words * p.n_worlds >= RG_TILED_MIN_WORDS;
+}
+
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
     const int real_words = (p.W + 31) >> 5;
-    const size_t items = (size_t)p.H * real_words * p.n_worlds;
+    const size_t items = (size_t)(p.row_hi - p.row_lo) * real_words * p.n_worlds;
+    if (regrow_tiled(p)) {
+        static int bps = 0;
+        if (bps == 0) {
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_regrow_tiled, RG_TH * 32, 0);
+            if (e != cudaSuccess || bps < 1) bps = 4;
+        }
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t ntiles =
+            (size_t)p.n_worlds * ((p.row_hi - p.row_lo + RG_TH - 1) / RG_TH) * ((real_words + RG_TW - 1) / RG_TW);
+        size_t blocks = (size_t)sms * bps;
+        if (blocks > ntiles) blocks = ntiles;
+        k_regrow_tiled<<<(unsigned)blocks, RG_TH * 32, 0, s>>>(p, ahead);
+        return cudaGetLastError();
+    }
     size_t blocks = (items + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_regrow<<<(unsigned)blocks, 256, 0, s>>>(p, ahead);

@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
     unsigned long long local = 0ull;
     for (size_t i = threadIdx.x; i < plane_words(p); i += blockDim.x) {
         O[i] = 0u;
-        local += __popc(R[i]);
+        const int y = (int)(i / p.WW);
+        if (y >= p.row_lo && y < p.row_hi) local += __popc(R[i]);  // the rows this handle owns
     }
     atomicAdd(&res_acc, local);
     __syncthreads();
