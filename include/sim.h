@@ -50,7 +50,7 @@ typedef enum {
     SIM_E_INVALID = -1,   /* a config field or argument is invalid; message names it   */
     SIM_E_CUDA = -2,      /* CUDA runtime failure (handle poisoned)                      */
     SIM_E_OOM = -3,       /* device allocation failed                                    */
-    SIM_E_NCCL = -4,      /* reserved for the banded multi-GPU mode                      */
+    SIM_E_NCCL = -4,      /* an NCCL call of the banded multi-GPU mode failed            */
     SIM_E_NONFINITE = -5, /* a non-finite h', c' or logit was produced */
     SIM_E_STATE = -6      /* the handle is poisoned by an earlier failure                */
 } sim_status;
@@ -80,6 +80,24 @@ typedef struct {
                                                 e_max = INT32_MAX means no clip          */
     int32_t repr_steps, max_age;
     void *cuda_stream;      /* borrowed cudaStream_t; NULL -> library-owned stream       */
+    /* Banded mode: ONE world (n_worlds = 1) split into n_bands
+     * latitude bands of rows; band b owns rows [band_rows[b], band_rows[b+1]) and the agents
+     * standing in them, exchanges halo rows, boundary claims, migrating agents (with their
+     * weights and LSTM state) and newborns with bands b-1 and b+1, and reads every band's
+     * birth counts for the global population cap.  The trajectory equals the unbanded
+     * world's keyed by cell (slot layouts differ).  n_bands <= 1: unbanded (the fields below
+     * are ignored).  This handle holds bands [band_first, band_first + band_local) on its
+     * device: all n_bands on one GPU (exchanges are device reads between the bands), or one
+     * band per GPU (one process per GPU; the other bands are attached with
+     * sim_band_export / sim_band_import and the steps synchronise through NCCL,
+     * sim_band_nccl_init). */
+    int32_t n_bands;        /* G, 2..32 (0 or 1: unbanded)                               */
+    int32_t band_first, band_local;
+    const int32_t *band_rows; /* [G+1] ascending row boundaries from 0 to H, each band >= 3
+                                 rows (the halo); NULL -> equal split b*H/G; copied        */
+    int32_t band_slots;     /* agent slots of each band (0 -> slots: a band can then hold
+                               the whole population and never overflows); a band whose
+                               pool overflows poisons the handle with SIM_E_OOM           */
 } sim_config;
 
 /* Canonical state, host buffers owned by the caller, layouts with the world index
@@ -253,6 +271,26 @@ SIM_API sim_status sim_step_post(sim_handle h);
  * SUM-allreduce between sim_step_policy and sim_step_post: the move records (int32) and
  * the policy counters (int64). */
 SIM_API sim_status sim_exchange(sim_handle h, void **mrec, size_t *mrec_bytes, void **record, size_t *record_bytes);
+
+/* --- banded mode over several GPUs (sim_config.n_bands) -----------
+ * One process per GPU, each handle holding one band (band_first = rank, band_local = 1):
+ *   every rank: sim_band_export(h, rank, blob, &bytes)  -> all-gather the blobs (e.g.
+ *     torch.distributed.all_gather_object); sim_band_import(h, b, blob_b, bytes) for every
+ *     other band b (CUDA IPC: the neighbours' planes, claims and outboxes become readable
+ *     over NVLink, and every band's birth counts);
+ *   rank 0: sim_band_nccl_id(id) -> broadcast the 128 bytes; every rank:
+ *     sim_band_nccl_init(h, id, n_bands, rank);
+ * then sim_step(h, n) on every rank: the phases of each step are separated by stream-
+ * ordered NCCL token exchanges with the neighbour bands (and one all-reduce for the global
+ * birth counts), and the exchanges themselves are kernels reading the neighbours' memory.
+ * sim_get_state returns this band's rows and agents (the caller merges the ranks' states by
+ * cell); sim_set_state takes the whole world's state on every rank and keeps its band's
+ * share.  sim_band_export with out = NULL returns the blob size in *bytes.  NCCL is loaded
+ * at run time (libnccl.so.2); its failures return SIM_E_NCCL and poison the handle. */
+SIM_API sim_status sim_band_export(sim_handle h, int32_t band, void *out, size_t *bytes);
+SIM_API sim_status sim_band_import(sim_handle h, int32_t band, const void *blob, size_t bytes);
+SIM_API sim_status sim_band_nccl_id(void *out128);
+SIM_API sim_status sim_band_nccl_init(sim_handle h, const void *id128, int32_t n_ranks, int32_t rank);
 
 /* Synchronise the handle's stream (reports deferred errors). */
 SIM_API sim_status sim_synchronize(sim_handle h);

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsim.so")
-SOURCES = ["api.cu", "world.cu", "step.cu"]
+SOURCES = ["api.cu", "world.cu", "step.cu", "band.cu"]
 HEADERS = ["sim_internal.cuh", "block_scan.cuh", "phases.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

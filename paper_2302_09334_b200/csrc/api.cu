@@ -177,6 +177,18 @@ struct sim_ctx {
     float *wcanon = nullptr;
     size_t wcanon_rows = 0;
     int32_t *bad_host = nullptr;  // mapped: a non-finite weight seen by the gather
+    // banded mode (band.cu): a banded handle drives its local bands,
+    // each a sub-context holding the global grid and its own rows' agents
+    std::vector<sim_ctx *> bands;   // parent: the local bands in band order
+    int G = 1, band_first = 0;
+    std::vector<int32_t> band_rows;  // parent: [G+1] row boundaries
+    bool is_band = false;            // this context is one band
+    eco::BandParams bp{};            // band: its exchange buffers and neighbours
+    int32_t *n_own_dev = nullptr;
+    struct BandNccl *nccl = nullptr; // parent with remote bands: the NCCL barrier
+    int32_t *band_tmp = nullptr;     // parent: device scratch of get_state (a band's live list)
+    float *band_canon = nullptr;     // parent: canonical rows of one band's live weights
+    size_t band_canon_rows = 0;
 };
 
 namespace {
@@ -302,14 +314,20 @@ cudaError_t ensure_regrown(sim_ctx *h) {
     return cudaSuccess;
 }
 
+sim_status band_sync(sim_ctx *h);  // api_band.inc
 sim_status sync(sim_ctx *h) {
+    if (!h->bands.empty()) return band_sync(h);
     CK(h, cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
     return check_nonfinite(h);
 }
 
+void band_nccl_destroy(sim_ctx *h);  // api_band.inc
 void destroy_all(sim_ctx *h) {
     if (!h) return;
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (sim_ctx *b : h->bands) destroy_all(b);  // (they borrow this stream)
+    h->bands.clear();
+    band_nccl_destroy(h);
     drop_graphs(h);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
@@ -347,7 +365,10 @@ sim_status sim_state_sizes(const sim_config *cfg, sim_state_sizes_t *out) {
     return SIM_OK;
 }
 
-sim_status sim_create(const sim_config *cfg, sim_handle *out) {
+}  // extern "C"
+
+namespace {
+sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_handle *out) {
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     *out = nullptr;
     Derived d;
@@ -391,7 +412,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
 
     DevParams &p = h->p;
     p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
-    p.row_lo = 0; p.row_hi = d.H;
+    p.row_lo = band ? band->y0 : 0;
+    p.row_hi = band ? band->y1 : d.H;
     p.regrow_split = 0;
     p.hd_shift = 0;
     while ((1 << p.hd_shift) < d.Hd) ++p.hd_shift;  // Hd is a power of two (validated)
@@ -463,7 +485,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &p.birth_cell, nw * S), "alloc");
     CKC(dalloc(h, &p.n_births, nw), "alloc");
     // split policy (one world, Hd = 32, the default policy kernel): P rows made by k_post
-    p.split = (nw == 1 && d.Hd == 32 && S > 0 && eco::policy_supports_shard()) ? 1 : 0;
+    p.split = (nw == 1 && d.Hd == 32 && S > 0 && !band && eco::policy_supports_shard()) ? 1 : 0;
     CKC(dalloc(h, &p.Pbuf, p.split ? S * (size_t)d.Hd * 4 : 1), "alloc");
     CKC(dalloc(h, &p.p_children, 1), "alloc");
     CKC(dalloc(h, &p.res_count, nw), "alloc");
@@ -474,6 +496,22 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
     CKC(dalloc(h, &h->live_dev, nw * S), "alloc");
     CKC(dalloc(h, &h->res_bytes, nw * HW), "alloc");
+    if (band) {  // one band of a banded world: its outboxes, counts and lists (band.cu)
+        h->is_band = true;
+        eco::BandParams &bp = h->bp;
+        bp = *band;
+        bp.cap = d.W < (int)S ? d.W : (int)S;
+        CKC(dalloc(h, &bp.mig_out, eco::band_box_words(d.W, (int)S, d.Hd, d.Pd, false)), "alloc");
+        CKC(dalloc(h, &bp.nb_out, eco::band_box_words(d.W, (int)S, d.Hd, d.Pd, true)), "alloc");
+        CKC(dalloc(h, &bp.counts, 8), "alloc");
+        CKC(dalloc(h, &bp.plist, S), "alloc");
+        CKC(dalloc(h, &bp.n_plist, 1), "alloc");
+        CKC(dalloc(h, &bp.arr_slot, 2 * (size_t)bp.cap), "alloc");
+        CKC(dalloc(h, &bp.cslot, HW), "alloc");
+        CKC(dalloc(h, &bp.cand_tgt, S), "alloc");
+        CKC(dalloc(h, &bp.flags, 4), "alloc");
+        CKC(dalloc(h, &h->n_own_dev, 1), "alloc");
+    }
     p.seeds = seeds_d;
     p.T = T_d;
     p.forced = h->forced_dev;
@@ -512,7 +550,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     }
     // [0] arrivals, [1] next base, [2] births flag, [3..4] window-end counters, [5] spare
     CKC(dalloc(h, &h->bar, 6), "alloc");
-    p.regrow_split = (S == 0 && eco::regrow_tiled(p)) ? 1 : 0;  // agent-free benchmark grids
+    p.regrow_split = (S == 0 && !band && eco::regrow_tiled(p)) ? 1 : 0;  // agent-free benchmark grids
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");
@@ -520,7 +558,7 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     std::vector<int64_t> res(nw);
     CKC(cudaMemcpyAsync(res.data(), p.res_count, nw * 8, cudaMemcpyDeviceToHost, h->stream), "download");
     CKC(cudaStreamSynchronize(h->stream), "sync");
-    for (size_t w = 0; w < nw; ++w)
+    for (size_t w = 0; w < nw && !band; ++w)  // (banded: the parent checks the whole grid)
         if ((int64_t)HW - res[w] < cfg->n_initial)
             return bail(fail(SIM_E_INVALID, "invalid field: n_initial (%d > %lld empty cells in world %zu)",
                              cfg->n_initial, (long long)((int64_t)HW - res[w]), w));
@@ -528,7 +566,8 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
         const size_t sb = eco::init_agents_scratch_bytes(p);
         void *scratch = nullptr;
         CKC(cudaMalloc(&scratch, sb), "alloc scratch");
-        cudaError_t e = eco::launch_init_agents(p, cfg->n_initial, h->stream, scratch, sb);
+        cudaError_t e = eco::launch_init_agents(p, band ? band->N0 : cfg->n_initial, h->stream, scratch, sb,
+                                                band ? &h->bp : nullptr, h->n_own_dev);
         cudaError_t e2 = cudaStreamSynchronize(h->stream);
         cudaFree(scratch);
         CKC(e, "init agents");
@@ -536,10 +575,21 @@ sim_status sim_create(const sim_config *cfg, sim_handle *out) {
     }
     CKC(eco::launch_rebuild(p, h->stream), "rebuild");
     CKC(cudaStreamSynchronize(h->stream), "sync");
-    CKC(ensure_graphs(h), "capture step graphs");
+    if (!band) CKC(ensure_graphs(h), "capture step graphs");
 #undef CKC
     *out = h;
     return SIM_OK;
+}
+}  // namespace
+
+#include "api_band.inc"
+
+extern "C" {
+
+sim_status sim_create(const sim_config *cfg, sim_handle *out) {
+    if (cfg && cfg->abi_version == SIM_ABI_VERSION && cfg->struct_size == sizeof(sim_config) && cfg->n_bands > 1)
+        return create_banded(cfg, out);
+    return create_one(cfg, nullptr, out);
 }
 
 sim_status sim_destroy(sim_handle h) {
@@ -558,6 +608,7 @@ sim_status sim_step(sim_handle h, int64_t n) {
     if (h->p.n_ranks > 1)
         return fail(SIM_E_STATE, "sharded handle: step with sim_step_policy, the exchange, then sim_step_post");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (!h->bands.empty()) return band_step(h, n);
     CK(h, ensure_graphs(h), "capture step graphs");  // (captured already unless a capture failed)
     const bool two = n >= 2 && two_step_graphs(h);
     CK(h, ensure_regrown(h), "regrow");
@@ -571,6 +622,7 @@ sim_status sim_step(sim_handle h, int64_t n) {
 
 // --- agent-sharded mode -------------------------------------------------------------
 sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (n_ranks < 1 || n_ranks > 255 || rank < 0 || rank >= n_ranks)
@@ -588,6 +640,7 @@ sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
 }
 
 sim_status sim_step_policy(sim_handle h) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if ((st = check_nonfinite(h)) != SIM_OK) return st;
@@ -598,6 +651,7 @@ sim_status sim_step_policy(sim_handle h) {
 }
 
 sim_status sim_step_post(sim_handle h) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
@@ -618,6 +672,7 @@ sim_status sim_exchange(sim_handle h, void **mrec, size_t *mrec_bytes, void **re
 }
 
 sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
@@ -641,6 +696,7 @@ sim_status sim_step_timed(sim_handle h, sim_step_timing *out) {
 }
 
 sim_status sim_step_graph_timed(sim_handle h, float out_ms[2]) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!out_ms) return fail(SIM_E_INVALID, "invalid argument: out_ms (NULL)");
@@ -672,6 +728,7 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (!h->bands.empty()) return band_get_state(h, out);
     if ((st = sync(h)) != SIM_OK) return st;
     const Derived &d = h->d;
     const DevParams &p = h->p;
@@ -720,25 +777,13 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     return sync(h);
 }
 
-namespace {
-// grow-only device buffer of `rows` rows of `width` floats
-cudaError_t ensure_rows(float **buf, size_t *have, size_t rows, size_t width) {
-    if (rows <= *have) return cudaSuccess;
-    if (*buf) cudaFree(*buf);
-    *buf = nullptr;
-    *have = 0;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(buf), rows * width * sizeof(float));
-    if (e == cudaSuccess) *have = rows;
-    return e;
-}
-}  // namespace
-
 sim_status sim_set_state(sim_handle h, const sim_state *in) {
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!in) return fail(SIM_E_INVALID, "invalid argument: in (NULL)");
     if (in->t < 0 || in->t >= ((int64_t)1 << 32)) return fail(SIM_E_INVALID, "invalid field: t");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (!h->bands.empty()) return band_set_state(h, in);
     if ((st = sync(h)) != SIM_OK) return st;
     const Derived &d = h->d;
     DevParams &p = h->p;
@@ -858,6 +903,7 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
 }
 
 sim_status sim_set_forced_actions(sim_handle h, const uint8_t *act) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
@@ -882,6 +928,7 @@ sim_status step_log_copy(sim_handle h, int64_t first, int64_t n, sim_step_record
         return fail(SIM_E_INVALID, "invalid argument: steps [%lld, %lld) not in the log (t = %lld, capacity %d)",
                     (long long)first, (long long)(first + n), (long long)h->t, h->d.log_cap);
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (!h->bands.empty()) return n ? band_step_log(h, first, n, out) : SIM_OK;  // summed over the bands
     if (wait && (st = sync(h)) != SIM_OK) return st;
     const size_t nw = h->d.n_worlds;
     // the ring is contiguous by step: [first, first+n) is at most two runs (split at the wrap)
@@ -906,6 +953,7 @@ sim_status sim_get_step_log_async(sim_handle h, int64_t first, int64_t n, sim_st
 }
 
 sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t capacity) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
@@ -930,6 +978,7 @@ sim_status sim_set_record_mirror(sim_handle h, sim_step_record *host, int64_t ca
 }
 
 sim_status sim_get_phase_ns(sim_handle h, int64_t *out, int32_t reset) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
@@ -945,6 +994,15 @@ sim_status sim_get_move_hist(sim_handle h, int64_t first, int64_t n, int32_t *ou
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (n < 0 || (n > 0 && !out)) return fail(SIM_E_INVALID, "invalid argument: n/out");
+    if (!h->bands.empty()) {  // summed over the local bands
+        std::vector<int32_t> tmp((size_t)n * SIM_MOVE_BINS);
+        memset(out, 0, (size_t)n * SIM_MOVE_BINS * 4);
+        for (sim_ctx *b : h->bands) {
+            if ((st = sim_get_move_hist(b, first, n, tmp.data())) != SIM_OK) return st;
+            for (size_t i = 0; i < tmp.size(); ++i) out[i] += tmp[i];
+        }
+        return SIM_OK;
+    }
     const int64_t done = h->t / SIM_MOVE_WINDOW;  // complete windows
     if (first < 0 || first + n > done || first < done - h->p.mv_cap)
         return fail(SIM_E_INVALID, "invalid argument: windows [%lld, %lld) not kept (complete windows %lld, capacity %d)",
@@ -964,6 +1022,21 @@ sim_status sim_get_totals(sim_handle h, sim_totals *out) {
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
+    if (!h->bands.empty()) {  // summed over the local bands (steps counted once)
+        *out = sim_totals{};
+        for (sim_ctx *b : h->bands) {
+            sim_totals tb;
+            if ((st = sim_get_totals(b, &tb)) != SIM_OK) return st;
+            out->steps = tb.steps;
+            out->agent_steps += tb.agent_steps;
+            out->cell_updates += tb.cell_updates;
+            out->births += tb.births;
+            out->deaths += tb.deaths;
+            out->eaten += tb.eaten;
+            out->grown += tb.grown;
+        }
+        return SIM_OK;
+    }
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     unsigned long long v[8];
     CK(h, cudaMemcpyAsync(v, h->p.totals, sizeof v, cudaMemcpyDeviceToHost, h->stream), "totals");

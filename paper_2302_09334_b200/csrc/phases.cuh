@@ -671,13 +671,15 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
 // (1) + (2): free slots and claimed cells of ranks r < n_place into s_free / s_bcell (r <
 // RANK_SMEM_CAP) or g_free / g_bcell (larger r).  All NT threads; `scratch` holds
 // 2 * (NT/32 + 1) words.
+// (Banded mode: only the claimed cells of bitmap words [bw_lo, bw_hi), the band's own rows.)
 template <int NT>
 __device__ void rank_lists(const DevParams &p, int w, int64_t t, int n_place, uint32_t *scratch, int *s_free,
-                           int *s_bcell, int32_t *g_free, int32_t *g_bcell) {
+                           int *s_bcell, int32_t *g_free, int32_t *g_bcell, size_t bw_lo = 0,
+                           size_t bw_hi = ~(size_t)0) {
     const int tid = threadIdx.x;
     const uint32_t *ab = p.alive_bits + (size_t)w * p.SW;
     const uint32_t *bb = bbits_of(p, t, w);
-    const size_t nbw = (size_t)p.H * p.WW;
+    const size_t nbw = bw_hi < (size_t)p.H * p.WW ? bw_hi : (size_t)p.H * p.WW;
     uint32_t run_f = 0u, run_c = 0u;
     for (size_t j = 0;; ++j) {
         const bool need_f = run_f < (uint32_t)n_place, need_c = run_c < (uint32_t)n_place;  // block-uniform
@@ -690,7 +692,7 @@ __device__ void rank_lists(const DevParams &p, int w, int64_t t, int n_place, ui
             const uint32_t valid = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
             fr = ~ld_plain(ab + fi) & valid;
         }
-        const size_t bi0 = (j * NT + tid) * RANK_K;
+        const size_t bi0 = bw_lo + (j * NT + tid) * RANK_K;
         uint32_t wd[RANK_K];
 #pragma unroll
         for (int u = 0; u < RANK_K; ++u) wd[u] = (need_c && bi0 + u < nbw) ? ld_plain(bb + bi0 + u) : 0u;
@@ -886,13 +888,13 @@ __device__ __forceinline__ void mutate_item(const PP &p, int it, int &d0, int &d
 // (z[j0], z[j0+1]) for (step t, child cell): bit-identical to box_muller()'s (za, zb).
 // Not inlined: one copy of the Philox + log + sincos code serves every call site (the
 // one-shot phases of k_post are bound by instruction fetch, not by call overhead).
-__device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0);
+static __device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0);
 __device__ __forceinline__ void gauss_pair(uint64_t seed, int64_t t, int cellc, int j0, double &za, double &zb) {
     const double2 z = gauss_pair_nl(seed, t, cellc, j0);
     za = z.x;
     zb = z.y;
 }
-__device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0) {
+static __device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0) {
     double za, zb;
     const uint4 d = draw4(seed, PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)(j0 >> 2));
     const bool lo = (j0 & 3) == 0;
@@ -1024,7 +1026,7 @@ __device__ __forceinline__ MutArgs mut_args(const DevParams &p) {
     a.rank = p.rank;
     return a;
 }
-__device__ __noinline__ void mutate_world_nl(MutArgs a, int64_t t, uint64_t seed, int nb, size_t gtid, size_t gthreads,
+static __device__ __noinline__ void mutate_world_nl(MutArgs a, int64_t t, uint64_t seed, int nb, size_t gtid, size_t gthreads,
                                              int dry) {
     mutate_world_impl(a, 0, t, seed, nb, gtid, gthreads, dry != 0);
 }

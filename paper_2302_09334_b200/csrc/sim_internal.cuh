@@ -106,6 +106,30 @@ struct DevParams {
     int32_t *nonfinite;          // host-mapped flag
 };
 
+// Banded mode (band.cu): the buffers of another band that a band's
+// pull kernels read (a band of this process, or peer memory mapped from another GPU).
+struct BandPeer {
+    const uint32_t *plane0, *plane1, *occ, *bbits;
+    const unsigned long long *claim, *bkey;
+    const int32_t *mig, *nb;   // migrant and newborn outboxes ([2 directions][count + records])
+};
+constexpr int BAND_MAX = 32;
+struct BandParams {
+    int b, G, y0, y1;          // band b of G owns rows [y0, y1)
+    int S_global;              // the world's population cap (R22 is global)
+    int N0;                    // the world's initial agents (C.2 is global)
+    int cap;                   // records per outbox direction: min(W, local slots)
+    int32_t *mig_out, *nb_out; // this band's outboxes (pulled by the neighbours)
+    int64_t *counts;           // [2 parities][4]: claimed cells in the own rows, survivors
+    int32_t *plist, *n_plist;  // agents of this step after the move (stayers, then arrivals)
+    int32_t *arr_slot;         // [2 cap] the arrivals' local slots
+    int32_t *cslot;            // [H*W] local slot of a child whose parent is in a neighbour band
+    int2 *cand_tgt;            // [S] per eligible parent: (claimed cell or -1, claim key hi)
+    int32_t *flags;            // [0] bit 0: local slot pool exhausted; [1] arrivals placed
+    BandPeer up, down;         // bands b-1 and b+1 (plane0 == nullptr: none)
+    const int64_t *all_counts[BAND_MAX];  // every band's counts
+};
+
 // ------------------------------------------------------------------ Philox4x32-10
 // Salmon et al. SC'11.  Counter (c0 = sub, c1 = entity, c2 = step, c3 = purpose),
 // key (seed lo, seed hi) — the RNG contract of DESIGN.md §3 (C.1).
@@ -242,7 +266,9 @@ struct LaunchCfg {
 
 cudaError_t launch_init_resources(const DevParams &p, cudaStream_t s);
 size_t init_agents_scratch_bytes(const DevParams &p);
-cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes);
+// band != nullptr: only the initial agents in the band's rows, in local slots 0.. (*n_own)
+cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch, size_t scratch_bytes,
+                               const BandParams *band = nullptr, int32_t *n_own_dev = nullptr);
 cudaError_t launch_rebuild(const DevParams &p, cudaStream_t s);
 cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s);
 bool regrow_tiled(const DevParams &p);  // launch_regrow uses the shared-memory-tiled kernel
@@ -262,6 +288,22 @@ bool policy_supports_shard();  // the Hd = 32 policy kernel of this build honour
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);  // P of step t
 cudaError_t post_prepare();  // kernel attributes of k_post (dynamic shared memory)
 
+// banded mode (band.cu); kinds: halo 0 = X1, 1 = X4a; merge 0 = X2, 1 = X4b
+cudaError_t band_halo(const DevParams &p, const BandParams &bp, int kind, cudaStream_t s);
+cudaError_t band_merge(const DevParams &p, const BandParams &bp, int kind, cudaStream_t s);
+cudaError_t band_move(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
+cudaError_t band_arrive(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
+cudaError_t band_live(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
+cudaError_t band_claims(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
+cudaError_t band_counts(const DevParams &p, const BandParams &bp, cudaStream_t s);
+cudaError_t band_rank(const DevParams &p, const BandParams &bp, cudaStream_t s);
+cudaError_t band_mutate(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
+cudaError_t band_newborns(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
+cudaError_t band_init_agents(const DevParams &p, const BandParams &bp, int n_initial, const unsigned long long *sorted,
+                             int32_t *n_own, cudaStream_t s);
+size_t band_box_words(int W, int S, int Hd, int Pd, bool newborn);
+cudaError_t launch_mv_pass(const DevParams &p, cudaStream_t s);  // movement histograms at a window end
+
 // state conversion (canonical <-> device)
 cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);
 cudaError_t launch_unpack_resources(const DevParams &p, uint8_t *bytes, cudaStream_t s);
@@ -271,6 +313,8 @@ cudaError_t launch_weights_gather(const DevParams &p, const float *src, bool by_
                                   float *stage, int32_t *bad, cudaStream_t s);
 cudaError_t launch_weights_scatter(const DevParams &p, const float *stage, const int32_t *live, int n_live,
                                    cudaStream_t s);
+// device-layout weights of slots list[k] (k < n) -> canonical rows k of `canon`
+cudaError_t launch_weights_to_canon_list(const DevParams &p, const int32_t *list, int n, float *canon, cudaStream_t s);
 cudaError_t launch_weights_to_canon(const DevParams &p, float *canon, size_t first_agent, size_t n_agents,
                                     cudaStream_t s);
 

@@ -1337,6 +1337,13 @@ cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_mv_pass(const DevParams &p, cudaStream_t s) {
+#if ECO_METRICS & 2
+    k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);
+#endif
+    return cudaGetLastError();
+}
+
 bool policy_supports_shard() { return true; }  // k_policy_half honours ownership
 
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {

@@ -93,7 +93,7 @@ size_t init_agents_scratch_bytes(const DevParams &p) {
 }
 
 cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s, void *scratch,
-                               size_t scratch_bytes) {
+                               size_t scratch_bytes, const BandParams *band, int32_t *n_own_dev) {
     if (p.S == 0) return cudaSuccess;
     const int64_t HW = (int64_t)p.H * p.W;
     unsigned long long *keys_in = static_cast<unsigned long long *>(scratch);
@@ -109,11 +109,20 @@ cudaError_t launch_init_agents(const DevParams &p, int n_initial, cudaStream_t s
         if (need > tmp_bytes) return cudaErrorMemoryAllocation;
         e = cub::DeviceRadixSort::SortKeys(tmp, need, keys_in, keys_out, (int)HW, 0, 64, s);
         if (e != cudaSuccess) return e;
-        k_init_agents<<<(p.S + 255) / 256, 256, 0, s>>>(p, w, n_initial, keys_out);
-        if (n_initial > 0) {
+        int n_agents = n_initial;
+        if (band) {  // one band of a banded world: its rows' agents in local slots 0..
+            if ((e = band_init_agents(p, *band, n_initial, keys_out, n_own_dev, s)) != cudaSuccess) return e;
+            int32_t n_own = 0;
+            if ((e = cudaMemcpyAsync(&n_own, n_own_dev, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+            n_agents = n_own < p.S ? n_own : p.S;
+        } else {
+            k_init_agents<<<(p.S + 255) / 256, 256, 0, s>>>(p, w, n_initial, keys_out);
+        }
+        if (n_agents > 0) {
             const int groups = (p.P + 3) >> 2;
-            dim3 g((groups + 127) / 128, n_initial < 4096 ? n_initial : 4096);
-            k_init_weights<<<g, 128, 0, s>>>(p, w, n_initial);
+            dim3 g((groups + 127) / 128, n_agents < 4096 ? n_agents : 4096);
+            k_init_weights<<<g, 128, 0, s>>>(p, w, n_agents);
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -273,6 +282,20 @@ __global__ void k_weights_scatter(DevParams p, const float4 *stage, const int32_
         for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < q4; q += gridDim.x * blockDim.x)
             dst[q] = stage[(size_t)k * q4 + q];
     }
+}
+
+__global__ void k_weights_to_canon_list(DevParams p, const int32_t *list, int n, float *canon) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p.P) return;
+    const int d = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
+    for (int k = blockIdx.y; k < n; k += gridDim.y) canon[(size_t)k * p.P + j] = p.weights[(size_t)list[k] * p.Pd + d];
+}
+
+cudaError_t launch_weights_to_canon_list(const DevParams &p, const int32_t *list, int n, float *canon, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    dim3 g((unsigned)((p.P + 255) / 256), (unsigned)(n < 8192 ? n : 8192));
+    k_weights_to_canon_list<<<g, 256, 0, s>>>(p, list, n, canon);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_weights_gather(const DevParams &p, const float *src, bool by_slot, const int32_t *live, int n_live,

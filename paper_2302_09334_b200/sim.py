@@ -28,7 +28,8 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_validate", "sim_state_sizes", "sim_set_forced_actions", "sim_get_step_log", "sim_get_totals",
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
             "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
-            "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist")
+            "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist",
+            "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init")
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
@@ -60,6 +61,9 @@ class SimConfig(ctypes.Structure):
         ("e_repr_gt", ctypes.c_int32), ("e_death_le", ctypes.c_int32), ("e_max", ctypes.c_int32),
         ("repr_steps", ctypes.c_int32), ("max_age", ctypes.c_int32),
         ("cuda_stream", ctypes.c_void_p),
+        # banded mode (include/sim.h: one world in latitude bands)
+        ("n_bands", ctypes.c_int32), ("band_first", ctypes.c_int32), ("band_local", ctypes.c_int32),
+        ("band_rows", ctypes.POINTER(ctypes.c_int32)), ("band_slots", ctypes.c_int32),
     ]
 
 
@@ -130,6 +134,11 @@ def lib():
                 L.sim_step_post.argtypes = [H]
                 L.sim_exchange.argtypes = [H, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t),
                                            ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
+            if hasattr(L, "sim_band_export"):
+                L.sim_band_export.argtypes = [H, ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]
+                L.sim_band_import.argtypes = [H, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t]
+                L.sim_band_nccl_id.argtypes = [ctypes.c_void_p]
+                L.sim_band_nccl_init.argtypes = [H, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
             for f in EXPORTED:
                 if f not in ("sim_last_error", "sim_kernels_per_step") and hasattr(L, f):
                     getattr(L, f).restype = ctypes.c_int
@@ -150,9 +159,10 @@ def _stream_handle(stream) -> int:
     return int(stream.cuda_stream)  # torch.cuda.Stream
 
 
-def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0):
+def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0, bands=None):
     """SimConfig from a workloads.WorldConfig (or any object with the same fields).
-    Returns (config, seeds array) — keep the array alive while the config is used."""
+    `bands` (banded mode): dict(n_bands=G, band_first=0, band_local=G, band_rows=None,
+    band_slots=0).  Returns (config, keep-alive arrays) — keep them while the config is used."""
     seeds = np.ascontiguousarray(np.array([int(s) & 0xFFFFFFFFFFFFFFFF for s in wc.seeds], dtype=np.uint64))
     c = SimConfig()
     c.abi_version, c.struct_size = ABI_VERSION, ctypes.sizeof(SimConfig)
@@ -171,7 +181,18 @@ def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0):
     c.e_repr_gt, c.e_death_le, c.e_max = wc.e_repr_gt, wc.e_death_le, wc.e_max
     c.repr_steps, c.max_age = wc.repr_steps, wc.max_age
     c.cuda_stream = _stream_handle(stream)
-    return c, seeds
+    keep = [seeds]
+    if bands:
+        G = int(bands["n_bands"])
+        c.n_bands = G
+        c.band_first = int(bands.get("band_first", 0))
+        c.band_local = int(bands.get("band_local", G - c.band_first))
+        c.band_slots = int(bands.get("band_slots", 0))
+        if bands.get("band_rows") is not None:
+            rows = np.ascontiguousarray(np.asarray(bands["band_rows"], np.int32))
+            c.band_rows = rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            keep.append(rows)
+    return c, keep
 
 
 def validate(wc) -> None:
@@ -197,11 +218,14 @@ def _ptr(a: np.ndarray):
 class World:
     """One handle of libsim.so: n_worlds independent worlds batched on one GPU."""
 
-    def __init__(self, wc, device: int = 0, stream=None, log_capacity: int = 0):
+    def __init__(self, wc, device: int = 0, stream=None, log_capacity: int = 0, bands=None):
+        """bands: banded mode (one world in latitude bands, include/sim.h), e.g.
+        dict(n_bands=4) for four bands on this GPU (see paper_2302_09334_b200.banded)."""
         self.wc = wc
         self.device = device
         self.n_worlds = len(wc.seeds)
-        self._cfg, self._seeds = make_config(wc, device, stream, log_capacity)
+        self.bands = dict(bands) if bands else None
+        self._cfg, self._seeds = make_config(wc, device, stream, log_capacity, bands)
         self.log_capacity = log_capacity or 4096
         h = ctypes.c_void_p()
         _check(lib().sim_create(ctypes.byref(self._cfg), ctypes.byref(h)))
