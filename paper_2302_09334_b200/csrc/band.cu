@@ -374,7 +374,7 @@ __global__ void k_band_live(DevParams p, BandParams bp) {
 // --------------------------------------------------------------------- P7 claims
 // Lazy reset of this step's move claims (the own claimants' targets and the four merged
 // boundary rows), the outbox counters of this step (the neighbours pulled them before
-// barrier X4a), then the birth claims of the own eligible parents (birth_target: first free
+// barrier X4a) and the P5 list, then the birth claims of the own eligible parents (birth_target: first free
 // Philox-rotated neighbour in O'' / R'', halo rows included; R21).  Each candidate's target
 // and claim key are kept for P10.
 __global__ void k_band_claims(DevParams p, BandParams bp) {
@@ -396,6 +396,7 @@ __global__ void k_band_claims(DevParams p, BandParams bp) {
         *box_dir(bp.mig_out, 1, bp.cap, ms) = 0;
         *box_dir(bp.nb_out, 0, bp.cap, ns) = 0;
         *box_dir(bp.nb_out, 1, bp.cap, ns) = 0;
+        *bp.n_plist = 0;  // (P5 consumed the list)
     }
     const int nc = *p.n_cand;
     const unsigned lane = threadIdx.x & 31;

@@ -1180,28 +1180,37 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
 // --------------------------------------------------------------------------- launchers
 // ------------------------------------------------ a1, large grids: shared-memory tiles
 // PAPER.md:255-267 as regrow_window, for grids of many words (the configs[2] benchmark
-// grids, the first step of a large world): a tile is RG_TH rows x RG_TW words (one word per
-// thread: warp = row, lane = word); its window rows y0-2 .. y0+RG_TH+1 and words wx0-4 ..
-// wx0+RG_TW+3 are staged in shared memory with 128-bit loads (one HBM read per word, the
-// halo re-reads of neighbouring tiles hit L2), so each word's 15-word window costs 15
-// shared-memory reads instead of 15 L2 round trips.  Persistent blocks walk the tiles with
-// the next tile's vector already in flight (one register per thread); output words are
-// coalesced 128-B warp stores; all-full words skip the count and the draws.  The grown
-// count is summed per block and added once per block and world.
-constexpr int RG_TW = 32, RG_TH = 8;              // one 256-thread block per tile
-constexpr int RG_VW = (RG_TW + 8) / 4;            // uint4 per staged row (4-word halo each side)
-constexpr int RG_LOADS = (RG_TH + 4) * RG_VW;     // 120 vectors per tile (threads 0..119)
-static_assert(RG_LOADS <= RG_TH * 32, "one staged vector per thread");
+// grids, the first step of a large world).  A tile is RG_TH rows x RG_TW words; its window
+// rows y0-2 .. y0+RG_TH+1 and words wx0-4 .. wx0+RG_TW+3 are staged in shared memory by
+// 16-B cp.async copies (zero-filled off the grid) through an RG_STAGES-deep ring, so every
+// block keeps RG_STAGES-1 tiles of loads in flight while it computes one (one HBM read per
+// word; the halo re-reads of neighbouring tiles hit L2).  The work of a tile is balanced
+// over its 256 threads instead of one word per lane (which diverges as soon as one word of
+// a warp needs its count or a draw): (1) the words holding an empty cell are listed, (2)
+// one thread per listed word forms its bit-sliced count and class masks and lists its
+// 4-cell groups holding an empty cell, (3) one thread per listed group draws the Philox
+// block and ORs the grown bits into the word, (4) the words are stored (coalesced), all-
+// full words unchanged.  The grown count is summed per block and added once per world.
+constexpr int RG_TW = 32, RG_TH = 16;            // 512 words (16,384 cells) per tile
+constexpr int RG_THREADS = 256, RG_WPT = RG_TW * RG_TH / RG_THREADS;  // words per thread (2)
+constexpr int RG_VW = (RG_TW + 8) / 4;           // uint4 per staged row (4-word halo each side)
+constexpr int RG_SROWS = RG_TH + 4;
+constexpr int RG_LOADS = RG_SROWS * RG_VW;       // 200 vectors per tile
+constexpr int RG_STAGES = 4;
+constexpr int RG_WORDS = RG_TW * RG_TH;
+static_assert(RG_LOADS <= RG_THREADS, "one staged vector per thread");
 
-__device__ __forceinline__ uint4 rg_load(const DevParams &p, const uint32_t *src, int y0, int wx0, int k) {
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+__device__ __forceinline__ void rg_issue(const DevParams &p, const uint32_t *src, int y0, int wx0, uint4 *stage) {
+    const int k = threadIdx.x;
     if (k < RG_LOADS) {
         const int r = k / RG_VW, q = k - r * RG_VW;
         const int yy = y0 - 2 + r, ww = wx0 - 4 + 4 * q;  // ww, WW multiples of 4: aligned, in-row
-        if (yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW)
-            v = __ldg(reinterpret_cast<const uint4 *>(src + (size_t)yy * p.WW + ww));
+        const bool in = yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW;
+        const uint32_t *g = in ? src + (size_t)yy * p.WW + ww : src;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(stage + k)), "l"(g),
+                     "r"(in ? 16 : 0)
+                     : "memory");
     }
-    return v;
 }
 
 __device__ __forceinline__ void rg_flush(const DevParams &p, int64_t tstep, int w, unsigned long long acc,
@@ -1211,15 +1220,20 @@ __device__ __forceinline__ void rg_flush(const DevParams &p, int64_t tstep, int 
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long sum = 0;
-        for (int i = 0; i < RG_TH; ++i) sum += s_red[i];
+        for (int i = 0; i < RG_THREADS / 32; ++i) sum += s_red[i];
         if (sum) atomicAdd(reinterpret_cast<unsigned long long *>(&record_of(p, tstep, w)->grown), sum);
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(RG_TH * 32, 4) k_regrow_tiled(DevParams p, int ahead) {
-    __shared__ uint4 s_tile[RG_TH + 4][RG_VW];
-    __shared__ unsigned long long s_red[RG_TH];
+__global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int ahead) {
+    __shared__ uint4 s_ring[RG_STAGES][RG_LOADS];
+    __shared__ uint32_t s_ge[3][RG_WORDS];       // class masks of the listed words
+    __shared__ uint32_t s_grow[RG_WORDS];        // grown bits by tile word
+    __shared__ uint16_t s_need[RG_WORDS];        // listed words (tile word index)
+    __shared__ uint16_t s_item[RG_WORDS * 8];    // listed groups (list index << 3 | group)
+    __shared__ int s_nneed, s_nitem;
+    __shared__ unsigned long long s_red[RG_THREADS / 32];
     const int64_t tstep = p.t[0] + ahead;
     const int real_words = (p.W + 31) >> 5;
     const int ntx = (real_words + RG_TW - 1) / RG_TW, nty = (p.row_hi - p.row_lo + RG_TH - 1) / RG_TH;
@@ -1227,6 +1241,7 @@ __global__ void __launch_bounds__(RG_TH * 32, 4) k_regrow_tiled(DevParams p, int
     const int ntiles = per_world * p.n_worlds;  // validated: n_worlds * H * words < 2^31
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t pw = plane_words(p);
+    constexpr int RS = RG_VW * 4;  // words per staged row
     auto coords = [&](int tile, int &w, int &y0, int &wx0) {
         w = tile / per_world;
         const int r = tile - w * per_world;
@@ -1234,16 +1249,22 @@ __global__ void __launch_bounds__(RG_TH * 32, 4) k_regrow_tiled(DevParams p, int
         y0 = p.row_lo + ty * RG_TH;
         wx0 = (r - ty * ntx) * RG_TW;
     };
+    auto issue = [&](int j) {  // the block's j-th tile into stage j % RG_STAGES (an empty group past the end)
+        const int tile = blockIdx.x + j * gridDim.x;
+        if (tile < ntiles) {
+            int w, y0, wx0;
+            coords(tile, w, y0, wx0);
+            rg_issue(p, plane_cur(p, tstep) + (size_t)w * pw, y0, wx0, s_ring[j % RG_STAGES]);
+        }
+        cp_commit();
+    };
+#pragma unroll
+    for (int j = 0; j < RG_STAGES - 1; ++j) issue(j);
     unsigned long long acc = 0;
     int acc_w = -1;
-    int tile = blockIdx.x;
-    uint4 pre = make_uint4(0u, 0u, 0u, 0u);
-    if (tile < ntiles) {
-        int w, y0, wx0;
-        coords(tile, w, y0, wx0);
-        pre = rg_load(p, plane_cur(p, tstep) + (size_t)w * pw, y0, wx0, threadIdx.x);
-    }
-    for (; tile < ntiles; tile += gridDim.x) {
+    for (int j = 0;; ++j) {
+        const int tile = blockIdx.x + j * gridDim.x;
+        if (tile >= ntiles) break;
         int w, y0, wx0;
         coords(tile, w, y0, wx0);
         if (w != acc_w) {  // block-uniform
@@ -1251,35 +1272,110 @@ __global__ void __launch_bounds__(RG_TH * 32, 4) k_regrow_tiled(DevParams p, int
             acc_w = w;
             acc = 0;
         }
-        if (threadIdx.x < RG_LOADS) s_tile[threadIdx.x / RG_VW][threadIdx.x % RG_VW] = pre;
+        cp_wait<RG_STAGES - 2>();
+        if (threadIdx.x == 0) s_nneed = s_nitem = 0;
+        __syncthreads();  // tile j staged for every thread; the previous tile's reads are done
+        issue(j + RG_STAGES - 1);
+        const uint32_t *sw = reinterpret_cast<const uint32_t *>(s_ring[j % RG_STAGES]);
+        // (1) words holding an empty cell
+#pragma unroll
+        for (int u = 0; u < RG_WPT; ++u) {
+            const int tw = threadIdx.x + u * RG_THREADS;
+            const int r = tw / RG_TW, col = tw - r * RG_TW;
+            const int y = y0 + r, wx = wx0 + col;
+            const bool valid = y < p.row_hi && wx < real_words;
+            const uint32_t cur = sw[(r + 2) * RS + col + 4];
+            const bool need = valid && !word_full(p, wx, cur);
+            s_grow[tw] = 0u;
+            const unsigned m = __ballot_sync(0xffffffffu, need);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_nneed, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (need) s_need[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)tw;
+        }
         __syncthreads();
-        {  // the next tile's vector in flight while this one is computed
-            const int nt = tile + gridDim.x;
-            if (nt < ntiles) {
-                int w2, y2, x2;
-                coords(nt, w2, y2, x2);
-                pre = rg_load(p, plane_cur(p, tstep) + (size_t)w2 * pw, y2, x2, threadIdx.x);
+        // (2) counts and class masks of the listed words, and their groups to draw
+        const int nneed = s_nneed;
+        for (int k = threadIdx.x; k < nneed; k += RG_THREADS) {
+            const int tw = s_need[k];
+            const int r = tw / RG_TW, col = tw - r * RG_TW;
+            const int wx = wx0 + col;
+            uint32_t win[5][3];
+#pragma unroll
+            for (int dr = 0; dr < 5; ++dr)
+#pragma unroll
+                for (int dw = 0; dw < 3; ++dw) win[dr][dw] = sw[(r + dr) * RS + col + 3 + dw];
+            const uint32_t cur = win[2][1];
+            uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int dr = 0; dr < 5; ++dr) {
+                const int m = p.row_dx[dr];
+#pragma unroll 1
+                for (int dx = -m; dx <= m; ++dx) {
+                    if (dr == 2 && dx == 0) continue;
+                    uint32_t cy = shifted_word(win[dr][0], win[dr][1], win[dr][2], dx), tt;
+                    tt = c[0] & cy; c[0] ^= cy; cy = tt;
+                    tt = c[1] & cy; c[1] ^= cy; cy = tt;
+                    tt = c[2] & cy; c[2] ^= cy; cy = tt;
+                    tt = c[3] & cy; c[3] ^= cy; cy = tt;
+                    c[4] ^= cy;
+                }
+            }
+            s_ge[0][k] = ge_const(c, p.cls_k1);
+            s_ge[1][k] = ge_const(c, p.cls_k2);
+            s_ge[2][k] = ge_const(c, p.cls_k3);
+            const int nv = p.W - (wx << 5);  // valid cells of the word
+            const uint32_t empty = ~cur & (nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u));
+            uint32_t gm = 0u;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) gm |= ((empty >> (4 * g)) & 0xFu) ? (1u << g) : 0u;
+            int pos = atomicAdd(&s_nitem, __popc(gm));
+            while (gm) {
+                const int g = __ffs(gm) - 1;
+                gm &= gm - 1u;
+                s_item[pos++] = (uint16_t)((k << 3) | g);
             }
         }
-        const int y = y0 + warp, wx = wx0 + lane;
-        if (y < p.row_hi && wx < real_words) {
-            const uint32_t *sw = reinterpret_cast<const uint32_t *>(&s_tile[0][0]);
-            constexpr int RS = RG_VW * 4;  // words per staged row
-            const uint32_t cur = sw[(warp + 2) * RS + lane + 4];
-            uint32_t grow = 0u;
-            if (!word_full(p, wx, cur)) {
-                uint32_t win[5][3];
+        __syncthreads();
+        // (3) one Philox block per listed group (the draw is keyed by the cell: exact)
+        const int nitem = s_nitem;
+        const uint64_t seed = p.seeds[w];
+        for (int i = threadIdx.x; i < nitem; i += RG_THREADS) {
+            const int it = s_item[i];
+            const int k = it >> 3, g = it & 7;
+            const int tw = s_need[k];
+            const int r = tw / RG_TW, col = tw - r * RG_TW;
+            const int y = y0 + r, x0 = ((wx0 + col) << 5) + 4 * g;
+            const uint32_t cur = sw[(r + 2) * RS + col + 4];
+            const uint32_t ge1 = s_ge[0][k], ge2 = s_ge[1][k], ge3 = s_ge[2][k];
+            const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
+            const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)tstep, (uint32_t)(((int64_t)y * p.W + x0) >> 2), 0u);
+            uint32_t bits = 0u;
 #pragma unroll
-                for (int r = 0; r < 5; ++r)
-#pragma unroll
-                    for (int dw = 0; dw < 3; ++dw) win[r][dw] = sw[(warp + r) * RS + lane + 3 + dw];
-                grow = regrow_window(p, w, y, wx, tstep, 0, 8, win, cur);
+            for (int m = 0; m < 4; ++m) {
+                const int bb = 4 * g + m;
+                const uint32_t thr = ((ge3 >> bb) & 1u) ? Trow.w : ((ge2 >> bb) & 1u) ? Trow.z
+                                     : ((ge1 >> bb) & 1u) ? Trow.y : Trow.x;
+                const bool grows = !((cur >> bb) & 1u) && x0 + m < p.W && word_of(d, m) < thr;
+                bits |= grows ? (1u << m) : 0u;
             }
-            plane_next(p, tstep)[(size_t)w * pw + (size_t)y * p.WW + wx] = cur | grow;
-            acc += (unsigned long long)__popc(grow);
+            if (bits) atomicOr(&s_grow[tw], bits << (4 * g));
         }
-        __syncthreads();  // the tile's shared reads are done before the next tile is staged
+        __syncthreads();
+        // (4) the tile's words
+#pragma unroll
+        for (int u = 0; u < RG_WPT; ++u) {
+            const int tw = threadIdx.x + u * RG_THREADS;
+            const int r = tw / RG_TW, col = tw - r * RG_TW;
+            const int y = y0 + r, wx = wx0 + col;
+            if (y < p.row_hi && wx < real_words) {
+                const uint32_t grow = s_grow[tw];
+                plane_next(p, tstep)[(size_t)w * pw + (size_t)y * p.WW + wx] = sw[(r + 2) * RS + col + 4] | grow;
+                acc += (unsigned long long)__popc(grow);
+            }
+        }
     }
+    cp_wait<0>();
     if (acc_w >= 0) rg_flush(p, tstep, acc_w, acc, s_red);
 }
 
@@ -1298,7 +1394,7 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
     if (regrow_tiled(p)) {
         static int bps = 0;
         if (bps == 0) {
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_regrow_tiled, RG_TH * 32, 0);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_regrow_tiled, RG_THREADS, 0);
             if (e != cudaSuccess || bps < 1) bps = 4;
         }
         int dev = 0, sms = 148;
@@ -1308,7 +1404,7 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
             (size_t)p.n_worlds * ((p.row_hi - p.row_lo + RG_TH - 1) / RG_TH) * ((real_words + RG_TW - 1) / RG_TW);
         size_t blocks = (size_t)sms * bps;
         if (blocks > ntiles) blocks = ntiles;
-        k_regrow_tiled<<<(unsigned)blocks, RG_TH * 32, 0, s>>>(p, ahead);
+        k_regrow_tiled<<<(unsigned)blocks, RG_THREADS, 0, s>>>(p, ahead);
         return cudaGetLastError();
     }
     size_t blocks = (items + 255) / 256;
