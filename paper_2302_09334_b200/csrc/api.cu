@@ -522,6 +522,11 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     p.nonfinite = nf_dev;
     std::vector<uint32_t> T;
     threshold_table(cfg, T);
+    p.t_monotone = 1;
+    for (size_t y = 0; y < (size_t)d.H; ++y)
+        for (int c = 1; c < 4; ++c)
+            if (T[y * 4 + c] < T[y * 4 + c - 1]) p.t_monotone = 0;
+    p.disc12 = (p.row_dx[0] == 0 && p.row_dx[1] == 1 && p.row_dx[2] == 2 && p.row_dx[3] == 1 && p.row_dx[4] == 0) ? 1 : 0;
     CKC(cudaMemcpyAsync(T_d, T.data(), T.size() * 4, cudaMemcpyHostToDevice, h->stream), "upload T");
     CKC(cudaMemcpyAsync(seeds_d, h->seeds.data(), nw * 8, cudaMemcpyHostToDevice, h->stream), "upload seeds");
 

@@ -48,6 +48,8 @@ struct DevParams {
     int e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max;
     int cls_k1, cls_k2, cls_k3;  // class thresholds f_class_min_k[1..3]
     int row_dx[5];  // regrowth disc: offsets (dy, dx) with |dx| <= row_dx[dy + 2], centre excluded
+    int disc12;     // 1: the disc is BASELINE's radius-2 disc (row_dx = 0,1,2,1,0: 12 cells)
+    int t_monotone; // 1: T[y][c] is non-decreasing in the class c on every row
     int off_hh, off_b, off_out, off_bout;  // offsets inside one agent's device weights
     double mutation_std, init_weight_std;
     uint32_t init_res_thr;

@@ -1242,31 +1242,50 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t pw = plane_words(p);
     constexpr int RS = RG_VW * 4;  // words per staged row
-    auto coords = [&](int tile, int &w, int &y0, int &wx0) {
-        w = tile / per_world;
-        const int r = tile - w * per_world;
-        const int ty = r / ntx;
-        y0 = p.row_lo + ty * RG_TH;
-        wx0 = (r - ty * ntx) * RG_TW;
+    // tile coordinates walked incrementally (block b visits tiles b, b + gridDim, ...): one
+    // division per block instead of two per tile
+    struct TileAt {
+        int w, ty, tx;
     };
+    auto decompose = [&](int tile) {
+        TileAt a;
+        a.w = tile / per_world;
+        const int r = tile - a.w * per_world;
+        a.ty = r / ntx;
+        a.tx = r - a.ty * ntx;
+        return a;
+    };
+    const TileAt stride = decompose((int)gridDim.x);
+    auto advance = [&](TileAt &a) {
+        a.tx += stride.tx;
+        if (a.tx >= ntx) {
+            a.tx -= ntx;
+            ++a.ty;
+        }
+        a.ty += stride.ty;
+        if (a.ty >= nty) {
+            a.ty -= nty;
+            ++a.w;
+        }
+        a.w += stride.w;
+    };
+    TileAt at_issue = decompose((int)blockIdx.x), at = at_issue;
     auto issue = [&](int j) {  // the block's j-th tile into stage j % RG_STAGES (an empty group past the end)
         const int tile = blockIdx.x + j * gridDim.x;
-        if (tile < ntiles) {
-            int w, y0, wx0;
-            coords(tile, w, y0, wx0);
-            rg_issue(p, plane_cur(p, tstep) + (size_t)w * pw, y0, wx0, s_ring[j % RG_STAGES]);
-        }
+        if (tile < ntiles)
+            rg_issue(p, plane_cur(p, tstep) + (size_t)at_issue.w * pw, p.row_lo + at_issue.ty * RG_TH,
+                     at_issue.tx * RG_TW, s_ring[j % RG_STAGES]);
+        advance(at_issue);
         cp_commit();
     };
 #pragma unroll
     for (int j = 0; j < RG_STAGES - 1; ++j) issue(j);
     unsigned long long acc = 0;
     int acc_w = -1;
-    for (int j = 0;; ++j) {
+    for (int j = 0;; ++j, advance(at)) {
         const int tile = blockIdx.x + j * gridDim.x;
         if (tile >= ntiles) break;
-        int w, y0, wx0;
-        coords(tile, w, y0, wx0);
+        const int w = at.w, y0 = p.row_lo + at.ty * RG_TH, wx0 = at.tx * RG_TW;
         if (w != acc_w) {  // block-uniform
             if (acc_w >= 0) rg_flush(p, tstep, acc_w, acc, s_red);
             acc_w = w;
@@ -1307,18 +1326,31 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
                 for (int dw = 0; dw < 3; ++dw) win[dr][dw] = sw[(r + dr) * RS + col + 3 + dw];
             const uint32_t cur = win[2][1];
             uint32_t c[5] = {0u, 0u, 0u, 0u, 0u};
+            auto add = [&](uint32_t cy) {  // bit-sliced counter += cy
+                uint32_t tt;
+                tt = c[0] & cy; c[0] ^= cy; cy = tt;
+                tt = c[1] & cy; c[1] ^= cy; cy = tt;
+                tt = c[2] & cy; c[2] ^= cy; cy = tt;
+                tt = c[3] & cy; c[3] ^= cy; cy = tt;
+                c[4] ^= cy;
+            };
+            if (p.disc12) {  // BASELINE's 12-cell disc, offsets compile-time (R4)
 #pragma unroll
-            for (int dr = 0; dr < 5; ++dr) {
-                const int m = p.row_dx[dr];
+                for (int dr = 0; dr < 5; ++dr) {
+                    const int m = dr == 2 ? 2 : (dr == 1 || dr == 3) ? 1 : 0;
+#pragma unroll
+                    for (int dx = -m; dx <= m; ++dx)
+                        if (!(dr == 2 && dx == 0)) add(shifted_word(win[dr][0], win[dr][1], win[dr][2], dx));
+                }
+            } else {
+#pragma unroll
+                for (int dr = 0; dr < 5; ++dr) {
+                    const int m = p.row_dx[dr];
 #pragma unroll 1
-                for (int dx = -m; dx <= m; ++dx) {
-                    if (dr == 2 && dx == 0) continue;
-                    uint32_t cy = shifted_word(win[dr][0], win[dr][1], win[dr][2], dx), tt;
-                    tt = c[0] & cy; c[0] ^= cy; cy = tt;
-                    tt = c[1] & cy; c[1] ^= cy; cy = tt;
-                    tt = c[2] & cy; c[2] ^= cy; cy = tt;
-                    tt = c[3] & cy; c[3] ^= cy; cy = tt;
-                    c[4] ^= cy;
+                    for (int dx = -m; dx <= m; ++dx) {
+                        if (dr == 2 && dx == 0) continue;
+                        add(shifted_word(win[dr][0], win[dr][1], win[dr][2], dx));
+                    }
                 }
             }
             s_ge[0][k] = ge_const(c, p.cls_k1);
@@ -1350,14 +1382,31 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
             const uint32_t ge1 = s_ge[0][k], ge2 = s_ge[1][k], ge3 = s_ge[2][k];
             const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
             const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)tstep, (uint32_t)(((int64_t)y * p.W + x0) >> 2), 0u);
+            const int nv = p.W - x0;  // valid cells of the group
+            const uint32_t empty4 = (~cur >> (4 * g)) & (nv >= 4 ? 0xFu : ((1u << nv) - 1u));
             uint32_t bits = 0u;
+            if (p.t_monotone) {
+                // T[y][.] non-decreasing: d < T[class] iff d < T0, or class >= c and d < T[c]
+                // for some c (the largest admissible threshold decides), as 4-cell masks
+                const uint32_t g1 = (ge1 >> (4 * g)) & 0xFu, g2 = (ge2 >> (4 * g)) & 0xFu, g3 = (ge3 >> (4 * g)) & 0xFu;
+                uint32_t m0 = 0u, m1 = 0u, m2 = 0u, m3 = 0u;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int bb = 4 * g + m;
-                const uint32_t thr = ((ge3 >> bb) & 1u) ? Trow.w : ((ge2 >> bb) & 1u) ? Trow.z
-                                     : ((ge1 >> bb) & 1u) ? Trow.y : Trow.x;
-                const bool grows = !((cur >> bb) & 1u) && x0 + m < p.W && word_of(d, m) < thr;
-                bits |= grows ? (1u << m) : 0u;
+                for (int m = 0; m < 4; ++m) {
+                    const uint32_t dm = word_of(d, m);
+                    m0 |= (dm < Trow.x ? 1u : 0u) << m;
+                    m1 |= (dm < Trow.y ? 1u : 0u) << m;
+                    m2 |= (dm < Trow.z ? 1u : 0u) << m;
+                    m3 |= (dm < Trow.w ? 1u : 0u) << m;
+                }
+                bits = empty4 & (m0 | (g1 & m1) | (g2 & m2) | (g3 & m3));
+            } else {
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int bb = 4 * g + m;
+                    const uint32_t thr = ((ge3 >> bb) & 1u) ? Trow.w : ((ge2 >> bb) & 1u) ? Trow.z
+                                         : ((ge1 >> bb) & 1u) ? Trow.y : Trow.x;
+                    bits |= (((empty4 >> m) & 1u) && word_of(d, m) < thr) ? (1u << m) : 0u;
+                }
             }
             if (bits) atomicOr(&s_grow[tw], bits << (4 * g));
         }

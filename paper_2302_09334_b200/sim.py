@@ -29,7 +29,9 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
             "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
             "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist",
-            "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init")
+            "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init", "sim_band_step_timed")
+BAND_PHASES = ("halo_x1", "policy", "merge_x2", "move", "arrive_x3", "live", "halo_x4a", "claims", "merge_x4b",
+               "counts", "rank", "mutate", "newborns_x5", "regrow")  # include/sim.h: SIM_BAND_PHASES
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1
@@ -139,6 +141,7 @@ def lib():
                 L.sim_band_import.argtypes = [H, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t]
                 L.sim_band_nccl_id.argtypes = [ctypes.c_void_p]
                 L.sim_band_nccl_init.argtypes = [H, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+                L.sim_band_step_timed.argtypes = [H, ctypes.c_void_p, ctypes.c_int32]
             for f in EXPORTED:
                 if f not in ("sim_last_error", "sim_kernels_per_step") and hasattr(L, f):
                     getattr(L, f).restype = ctypes.c_int
@@ -304,6 +307,15 @@ class World:
         _check(lib().sim_step_timed(self._h, ctypes.byref(tm)))
         self._t += 1
         return {"step_ms": float(tm.step_ms), **{k: float(tm.kernel_ms[i]) for i, k in enumerate(KERNEL_NAMES)}}
+
+    def band_step_timed(self) -> np.ndarray:
+        """Banded handle: one step with events around every local band's phases (bands one
+        after the other): float [band_local][len(BAND_PHASES)] milliseconds."""
+        nl = int(self.bands.get("band_local", self.bands["n_bands"] - self.bands.get("band_first", 0)))
+        out = np.zeros((nl, len(BAND_PHASES)), np.float32)
+        _check(lib().sim_band_step_timed(self._h, _ptr(out), len(BAND_PHASES)))
+        self._t += 1
+        return out
 
     def step_graph_timed(self) -> dict:
         """One step through graph mode's two kernels, each bracketed by CUDA events (ms)."""

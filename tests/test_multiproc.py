@@ -126,3 +126,64 @@ def test_two_gloo_ranks_reduce_to_the_single_process_result():
     assert np.array_equal(got[:4], want), (got, want)
     assert got[4] == 2.0  # max over ranks, not the sum
     assert got[5] == len(SEEDS)
+
+
+# ------------------------------------------------------------- banded mode (E.2) host logic
+def _band_worker(rank, world_size, port, path):
+    """Each rank holds its band's share of one world (paper_2302_09334_b200.banded.split_state,
+    the layout sim_get_state returns for a band); gathered over gloo, rank 0 merges them."""
+    import torch.distributed as dist
+    from paper_2302_09334_b200 import banded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        wc = workloads.tiny().replace(rows=24, cols=40, slots=300)
+        full = workloads.random_state(wc, seed=11, n_alive=180, t=7)
+        rows = banded.agent_weighted_rows(full["cell"][full["alive"] == 1] // wc.cols, wc.rows, world_size)
+        mine = banded.split_state(full, rows, rank, wc.cols)
+        parts = [None] * world_size
+        dist.all_gather_object(parts, mine)
+        if rank == 0:
+            merged = banded.merge_band_states(parts, rows, wc.cols)
+            np.save(path, np.array([_same_by_cell(full, merged), int(mine["alive"].sum()),
+                                    int(parts[1]["alive"].sum())]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _same_by_cell(a, b) -> int:
+    if a["t"] != b["t"] or not np.array_equal(a["resources"], b["resources"]):
+        return 0
+    la, lb = np.flatnonzero(a["alive"] == 1), np.flatnonzero(b["alive"] == 1)
+    ma, mb = dict(zip(a["cell"][la].tolist(), la)), dict(zip(b["cell"][lb].tolist(), lb))
+    if ma.keys() != mb.keys():
+        return 0
+    for c in ma:
+        for f in ("energy", "age", "repr", "last_action", "ate", "h", "c", "weights", "logits"):
+            if not np.array_equal(a[f][ma[c]], b[f][mb[c]]):
+                return 0
+    return 1
+
+
+def test_banded_states_split_and_merge_on_gloo():
+    import torch.multiprocessing as mp
+    path = os.path.join(tempfile.mkdtemp(), "banded.npy")
+    mp.spawn(_band_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    same, n0, n1 = np.load(path)
+    assert same == 1 and n0 + n1 == 180 and abs(int(n0) - int(n1)) <= 40  # agent-weighted rows
+
+
+def test_band_rows_helpers():
+    from paper_2302_09334_b200 import banded
+    assert banded.equal_band_rows(200, 8) == [0, 25, 50, 75, 100, 125, 150, 175, 200]
+    rng = np.random.default_rng(3)
+    ys = np.minimum((rng.random(50000) ** 0.5 * 1600).astype(int), 1599)  # more agents lower down
+    for G in (2, 4, 8):
+        rows = banded.agent_weighted_rows(ys, 1600, G)
+        assert rows[0] == 0 and rows[-1] == 1600 and all(b - a >= 3 for a, b in zip(rows, rows[1:]))
+        per = np.bincount(banded.band_of_rows(rows, ys), minlength=G)
+        assert per.max() / per.mean() < 1.05  # balanced by agents
+    # degenerate: every agent in one row still leaves every band its halo depth
+    rows = banded.agent_weighted_rows(np.full(100, 7), 40, 8)
+    assert all(b - a >= 3 for a, b in zip(rows, rows[1:])) and rows[-1] == 40
+    assert list(banded.band_of_rows([0, 5, 9, 20], [0, 4, 5, 8, 9, 19])) == [0, 0, 1, 1, 2, 2]
