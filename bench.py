@@ -67,6 +67,8 @@ def parse_args():
                          "each step; strong scaling) instead of one replica per rank")
     ap.add_argument("--no-flush", action="store_true",
                     help="diagnostic: do not flush L2 between timed steps (the line says so in config.l2)")
+    ap.add_argument("--no-l2-persist", action="store_true",
+                    help="ablation: no L2-persisting window on the hot-state arena (ECO_L2_PERSIST=0)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -233,6 +235,8 @@ def workload_config(wc, args, world_size: int, sharded: bool, t0: int) -> dict:
 
 # ------------------------------------------------------------------------ our arm
 def run_ours(args, rank, world_size, local_rank):
+    if args.no_l2_persist:
+        os.environ["ECO_L2_PERSIST"] = "0"
     import torch
     from paper_2302_09334_b200 import sim
 
@@ -375,8 +379,11 @@ def run_ours(args, rank, world_size, local_rank):
             "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": workload_config(wc, args, world_size, sharded, t0),
-            "l2": "NOT flushed (diagnostic run)" if args.no_flush
-            else "flushed between timed steps (256 MiB memset + 256 MiB read on the library stream)",
+            "l2": ("NOT flushed (diagnostic run)" if args.no_flush
+                   else "flushed between timed steps (256 MiB memset + 256 MiB read on the library stream)")
+            + ("" if args.no_l2_persist else "; the step graph's kernels mark the library's hot-state arena "
+               "(counters, planes, lists, SoA, P rows, h, c, claims: everything but the weights, first 32 MiB) "
+               "L2-persisting, so the flush cannot evict it; the weights stream from HBM every step"),
             "cell_updates_per_s": cells * (1 if sharded else world_size) / (max_ms / 1e3),
             "agents_mean": agents / K,
             "births_mean": births / K,

@@ -190,6 +190,8 @@ struct sim_ctx {
     int32_t *band_tmp = nullptr;     // parent: device scratch of get_state (a band's live list)
     float *band_canon = nullptr;     // parent: canonical rows of one band's live weights
     size_t band_canon_rows = 0;
+    char *hot_base = nullptr;        // the arena of everything but the weights (L2-persisting prefix)
+    size_t hot_bytes = 0;
 };
 
 namespace {
@@ -260,6 +262,52 @@ cudaError_t enqueue_step(sim_ctx *h, bool pdl = false) {
     return cudaSuccess;
 }
 
+// The L2 access-policy window of a step graph's kernels: the arena's first bytes (the
+// counters, planes, lists, SoA, P rows, h, c ...; never the weights) persisting, within the
+// device's persisting carve-out (cudaLimitPersistingL2CacheSize, set here once).  Disabled
+// with ECO_L2_PERSIST=0.
+bool l2_persist_enabled() {
+    const char *v = getenv("ECO_L2_PERSIST");
+    return !(v && v[0] == '0');
+}
+cudaError_t set_persistence(sim_ctx *h, cudaGraph_t g) {
+    if (!l2_persist_enabled() || !h->hot_base) return cudaSuccess;
+    int max_win = 0, max_persist = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+    if (max_win <= 0 || max_persist <= 0) return cudaSuccess;
+    size_t want = h->hot_bytes;
+    const size_t budget = (size_t)32 << 20;  // the step's hot state, not the bulk of a large world
+    if (want > budget) want = budget;
+    if (want > (size_t)max_win) want = (size_t)max_win;
+    size_t carve = 0;
+    cudaDeviceGetLimit(&carve, cudaLimitPersistingL2CacheSize);
+    if (carve < want && carve < (size_t)max_persist) {
+        const size_t c = want < (size_t)max_persist ? want : (size_t)max_persist;
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c) == cudaSuccess) carve = c;
+        else cudaGetLastError();
+    }
+    if (carve == 0) return cudaSuccess;
+    cudaKernelNodeAttrValue v{};
+    v.accessPolicyWindow.base_ptr = h->hot_base;
+    v.accessPolicyWindow.num_bytes = want;
+    v.accessPolicyWindow.hitRatio = carve >= want ? 1.0f : (float)carve / (float)want;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    size_t n = 0;
+    cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
+    if (e != cudaSuccess) return e;
+    std::vector<cudaGraphNode_t> nodes(n);
+    if ((e = cudaGraphGetNodes(g, nodes.data(), &n)) != cudaSuccess) return e;
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+        if ((e = cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v)) != cudaSuccess)
+            return e;
+    }
+    return cudaSuccess;
+}
+
 // capture `steps` (1 or 2) graph steps; in two, the second policy depends programmatically
 // on the first k_post (its launch overlaps k_post's drain)
 cudaError_t capture_steps(sim_ctx *h, int steps, cudaGraph_t *g, cudaGraphExec_t *ge) {
@@ -269,6 +317,7 @@ cudaError_t capture_steps(sim_ctx *h, int steps, cudaGraph_t *g, cudaGraphExec_t
     cudaError_t e2 = cudaStreamEndCapture(h->stream, g);
     if (e != cudaSuccess) return e;
     if (e2 != cudaSuccess) return e2;
+    if ((e = set_persistence(h, *g)) != cudaSuccess) return e;
     return cudaGraphInstantiate(ge, *g, 0);
 }
 
@@ -329,6 +378,7 @@ void destroy_all(sim_ctx *h) {
     for (sim_ctx *b : h->bands) destroy_all(b);  // (they borrow this stream)
     h->bands.clear();
     band_nccl_destroy(h);
+    if (h->graph && l2_persist_enabled()) cudaCtxResetPersistingL2Cache();  // release the carve-out's lines
     drop_graphs(h);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
@@ -439,64 +489,86 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     const size_t nw = d.n_worlds, S = d.S, HW = (size_t)d.H * d.W;
     uint64_t *seeds_d;
     uint32_t *T_d;
-    CKC(dalloc(h, &seeds_d, nw), "alloc");
-    CKC(dalloc(h, &p.t, nw), "alloc");
-    CKC(dalloc(h, &p.plane0, nw * d.pw), "alloc");
-    CKC(dalloc(h, &p.plane1, nw * d.pw), "alloc");
-    CKC(dalloc(h, &p.occ, nw * d.pw), "alloc");
-    CKC(dalloc(h, &p.bbits, 2 * nw * d.pw), "alloc");
-    CKC(dalloc(h, &T_d, (size_t)d.H * 4), "alloc");
-    CKC(dalloc(h, &p.claim, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.bkey, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.bslot, S ? nw * HW : 1), "alloc");
-    CKC(dalloc(h, &p.alive_bits, nw * (size_t)d.SW), "alloc");
-    CKC(dalloc(h, &p.alive, nw * S), "alloc");
-    CKC(dalloc(h, &p.last_action, nw * S), "alloc");
-    CKC(dalloc(h, &p.ate, nw * S), "alloc");
-    CKC(dalloc(h, &p.cell, nw * S), "alloc");
-    CKC(dalloc(h, &p.energy, nw * S), "alloc");
-    CKC(dalloc(h, &p.age, nw * S), "alloc");
-    CKC(dalloc(h, &p.repr, nw * S), "alloc");
-    CKC(dalloc(h, &p.h, nw * S * d.Hd), "alloc");
-    CKC(dalloc(h, &p.c, nw * S * d.Hd), "alloc");
-    CKC(dalloc(h, &p.logits, nw * S * eco::LOGIT_STRIDE), "alloc");
-    CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
-    CKC(dalloc(h, &p.mrec, nw * S), "alloc");
-    CKC(dalloc(h, &p.alive_list, 2 * nw * S), "alloc");
-    CKC(dalloc(h, &p.list_cell, 2 * nw * S), "alloc");
     p.mv_cap = mv_windows(d.log_cap);
-    CKC(dalloc(h, &p.mv_cell, nw * S), "alloc");
-    CKC(dalloc(h, &p.mv_inv, nw * S), "alloc");
-    CKC(dalloc(h, &p.mv_hist, nw * (size_t)p.mv_cap * SIM_MOVE_BINS), "alloc");
-    CKC(dalloc(h, &p.n_alive, 2 * nw), "alloc");
-    CKC(dalloc(h, &p.n_win, nw), "alloc");
-    CKC(dalloc(h, &p.free_list, nw * S), "alloc");
     p.n_ranks = 1;
     p.rank = 0;
-    CKC(dalloc(h, &p.owner, S ? S : 1), "alloc");
-    CKC(dalloc(h, &p.pol_ctr, 2), "alloc");
-    CKC(dalloc(h, &p.mrec_slot, S ? S : 1), "alloc");
-    CKC(dalloc(h, &p.own_list, S ? 2 * S : 1), "alloc");
-    CKC(dalloc(h, &p.own_count, 2), "alloc");
-    CKC(dalloc(h, &p.own_surv, 1), "alloc");
-    CKC(dalloc(h, &p.cand, nw * S), "alloc");
-    CKC(dalloc(h, &p.n_cand, nw), "alloc");
-    CKC(dalloc(h, &p.birth_child, nw * S), "alloc");
-    CKC(dalloc(h, &p.birth_parent, nw * S), "alloc");
-    CKC(dalloc(h, &p.birth_cell, nw * S), "alloc");
-    CKC(dalloc(h, &p.n_births, nw), "alloc");
     // split policy (one world, Hd = 32, the default policy kernel): P rows made by k_post
     p.split = (nw == 1 && d.Hd == 32 && S > 0 && !band && eco::policy_supports_shard()) ? 1 : 0;
-    CKC(dalloc(h, &p.Pbuf, p.split ? S * (size_t)d.Hd * 4 : 1), "alloc");
-    CKC(dalloc(h, &p.p_children, 1), "alloc");
-    CKC(dalloc(h, &p.res_count, nw), "alloc");
-    CKC(dalloc(h, &p.log, (size_t)d.log_cap * nw), "alloc");
-    CKC(dalloc(h, &p.totals, 8), "alloc");
-    CKC(dalloc(h, &p.phase_ns, PHASE_WORDS), "alloc");  // + per-block clocks / traces of diagnostic builds
-    CKC(dalloc(h, &h->forced_dev, nw * S), "alloc");
-    CKC(dalloc(h, &h->forced_on_dev, 1), "alloc");
-    CKC(dalloc(h, &h->live_dev, nw * S), "alloc");
-    CKC(dalloc(h, &h->res_bytes, nw * HW), "alloc");
+    // Everything but the weights lives in one arena, ordered by how latency-critical it is:
+    // counters, barrier words, planes, lists and SoA first.  Graph kernels get an L2
+    // access-policy window marking its prefix persisting (set_persistence below), so the
+    // dependent loads of a step's chains hit L2 even when other work evicted the rest.
+    std::vector<std::pair<void **, size_t>> hot;
+    auto H = [&hot](auto **ptr, size_t count) {
+        hot.emplace_back(reinterpret_cast<void **>(ptr), (count ? count : 1) * sizeof(**ptr));
+    };
+    H(&p.t, nw);
+    H(&h->bar, 6);  // [0] arrivals, [1] next base, [2] births flag, [3..4] window-end counters, [5] spare
+    H(&p.n_alive, 2 * nw);
+    H(&p.n_win, nw);
+    H(&p.n_cand, nw);
+    H(&p.n_births, nw);
+    H(&p.res_count, nw);
+    H(&p.totals, 8);
+    H(&p.p_children, 1);
+    H(&p.own_count, 2);
+    H(&p.own_surv, 1);
+    H(&p.pol_ctr, 2);
+    H(&h->forced_on_dev, 1);
+    H(&seeds_d, nw);
+    H(&T_d, (size_t)d.H * 4);
+    H(&p.plane0, nw * d.pw);
+    H(&p.plane1, nw * d.pw);
+    H(&p.occ, nw * d.pw);
+    H(&p.bbits, 2 * nw * d.pw);
+    H(&p.alive_bits, nw * (size_t)d.SW);
+    H(&p.alive, nw * S);
+    H(&p.last_action, nw * S);
+    H(&p.ate, nw * S);
+    H(&p.cell, nw * S);
+    H(&p.energy, nw * S);
+    H(&p.age, nw * S);
+    H(&p.repr, nw * S);
+    H(&p.mrec, nw * S);
+    H(&p.alive_list, 2 * nw * S);
+    H(&p.list_cell, 2 * nw * S);
+    H(&p.cand, nw * S);
+    H(&p.birth_child, nw * S);
+    H(&p.birth_parent, nw * S);
+    H(&p.birth_cell, nw * S);
+    H(&p.free_list, nw * S);
+    H(&p.log, (size_t)d.log_cap * nw);
+    H(&p.mv_cell, nw * S);
+    H(&p.mv_inv, nw * S);
+    H(&p.mv_hist, nw * (size_t)p.mv_cap * SIM_MOVE_BINS);
+    H(&h->forced_dev, nw * S);
+    H(&p.Pbuf, p.split ? S * (size_t)d.Hd * 4 : 1);
+    H(&p.h, nw * S * d.Hd);
+    H(&p.c, nw * S * d.Hd);
+    H(&p.logits, nw * S * eco::LOGIT_STRIDE);
+    H(&p.claim, S ? nw * HW : 1);
+    H(&p.bkey, S ? nw * HW : 1);
+    H(&p.bslot, S ? nw * HW : 1);
+    H(&p.owner, S ? S : 1);
+    H(&p.mrec_slot, S ? S : 1);
+    H(&p.own_list, S ? 2 * S : 1);
+    H(&p.phase_ns, PHASE_WORDS);  // + per-block clocks / traces of diagnostic builds
+    H(&h->live_dev, nw * S);
+    H(&h->res_bytes, nw * HW);
+    {
+        size_t total = 0;
+        for (auto &it : hot) total += (it.second + 255) / 256 * 256;
+        char *arena = nullptr;
+        CKC(dalloc(h, &arena, total), "alloc");
+        size_t off = 0;
+        for (auto &it : hot) {
+            *it.first = arena + off;
+            off += (it.second + 255) / 256 * 256;
+        }
+        h->hot_base = arena;
+        h->hot_bytes = total;
+    }
+    CKC(dalloc(h, &p.weights, nw * S * (size_t)d.Pd), "alloc");
     if (band) {  // one band of a banded world: its outboxes, counts and lists (band.cu)
         h->is_band = true;
         eco::BandParams &bp = h->bp;
@@ -554,8 +626,6 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
         h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    // [0] arrivals, [1] next base, [2] births flag, [3..4] window-end counters, [5] spare
-    CKC(dalloc(h, &h->bar, 6), "alloc");
     p.regrow_split = (S == 0 && !band && eco::regrow_tiled(p)) ? 1 : 0;  // agent-free benchmark grids
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists

@@ -1184,25 +1184,25 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
 // rows y0-2 .. y0+RG_TH+1 and words wx0-4 .. wx0+RG_TW+3 are staged in shared memory by
 // 16-B cp.async copies (zero-filled off the grid) through an RG_STAGES-deep ring, so every
 // block keeps RG_STAGES-1 tiles of loads in flight while it computes one (one HBM read per
-// word; the halo re-reads of neighbouring tiles hit L2).  The work of a tile is balanced
-// over its 256 threads instead of one word per lane (which diverges as soon as one word of
-// a warp needs its count or a draw): (1) the words holding an empty cell are listed, (2)
-// one thread per listed word forms its bit-sliced count and class masks and lists its
-// 4-cell groups holding an empty cell, (3) one thread per listed group draws the Philox
-// block and ORs the grown bits into the word, (4) the words are stored (coalesced), all-
-// full words unchanged.  The grown count is summed per block and added once per world.
-constexpr int RG_TW = 32, RG_TH = 16;            // 512 words (16,384 cells) per tile
-constexpr int RG_THREADS = 256, RG_WPT = RG_TW * RG_TH / RG_THREADS;  // words per thread (2)
+// word; the halo re-reads of neighbouring tiles hit L2).  Each thread owns 4 consecutive
+// words of a row (one 128-bit vector in and out).  The work of a tile is balanced over its
+// 256 threads instead of one word per lane (which diverges as soon as one word of a warp
+// needs its count or a draw): (1) the words holding an empty cell are listed, (2) one
+// thread per listed word forms its bit-sliced count and a 2-bit class per cell and lists
+// its 4-cell groups holding an empty cell, (3) one thread per listed group draws the Philox
+// block and ORs the grown bits into the word, (4) each thread stores its 4 words (all-full
+// words unchanged).  The grown count is summed per block and added once per world.
+constexpr int RG_TW = 32, RG_TH = 32;            // 1024 words (32,768 cells) per tile
+constexpr int RG_THREADS = 256;                  // one 4-word vector per thread
 constexpr int RG_VW = (RG_TW + 8) / 4;           // uint4 per staged row (4-word halo each side)
 constexpr int RG_SROWS = RG_TH + 4;
-constexpr int RG_LOADS = RG_SROWS * RG_VW;       // 200 vectors per tile
-constexpr int RG_STAGES = 4;
+constexpr int RG_LOADS = RG_SROWS * RG_VW;       // 360 vectors per tile
+constexpr int RG_STAGES = 3;
 constexpr int RG_WORDS = RG_TW * RG_TH;
-static_assert(RG_LOADS <= RG_THREADS, "one staged vector per thread");
+static_assert(RG_WORDS == 4 * RG_THREADS, "one 4-word vector per thread");
 
 __device__ __forceinline__ void rg_issue(const DevParams &p, const uint32_t *src, int y0, int wx0, uint4 *stage) {
-    const int k = threadIdx.x;
-    if (k < RG_LOADS) {
+    for (int k = threadIdx.x; k < RG_LOADS; k += RG_THREADS) {
         const int r = k / RG_VW, q = k - r * RG_VW;
         const int yy = y0 - 2 + r, ww = wx0 - 4 + 4 * q;  // ww, WW multiples of 4: aligned, in-row
         const bool in = yy >= 0 && yy < p.H && ww >= 0 && ww < p.WW;
@@ -1226,12 +1226,23 @@ __device__ __forceinline__ void rg_flush(const DevParams &p, int64_t tstep, int 
     __syncthreads();
 }
 
+// 16 bits -> every other bit of 32 (bit i -> bit 2i)
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+    x &= 0xFFFFu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+
 __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int ahead) {
     __shared__ uint4 s_ring[RG_STAGES][RG_LOADS];
-    __shared__ uint32_t s_ge[3][RG_WORDS];       // class masks of the listed words
+    __shared__ uint32_t s_code[2][RG_WORDS];     // listed words: 2-bit class per cell (cells 0-15, 16-31)
     __shared__ uint32_t s_grow[RG_WORDS];        // grown bits by tile word
     __shared__ uint16_t s_need[RG_WORDS];        // listed words (tile word index)
     __shared__ uint16_t s_item[RG_WORDS * 8];    // listed groups (list index << 3 | group)
+    __shared__ uint32_t s_T[RG_TH][4];           // thresholds of the tile's rows
     __shared__ int s_nneed, s_nitem;
     __shared__ unsigned long long s_red[RG_THREADS / 32];
     const int64_t tstep = p.t[0] + ahead;
@@ -1239,7 +1250,7 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
     const int ntx = (real_words + RG_TW - 1) / RG_TW, nty = (p.row_hi - p.row_lo + RG_TH - 1) / RG_TH;
     const int per_world = ntx * nty;
     const int ntiles = per_world * p.n_worlds;  // validated: n_worlds * H * words < 2^31
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const size_t pw = plane_words(p);
     constexpr int RS = RG_VW * 4;  // words per staged row
     // tile coordinates walked incrementally (block b visits tiles b, b + gridDim, ...): one
@@ -1280,6 +1291,8 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
     };
 #pragma unroll
     for (int j = 0; j < RG_STAGES - 1; ++j) issue(j);
+    // this thread's vector: row tr, words tq*4 .. tq*4+3 of the tile
+    const int tr = threadIdx.x >> 3, tq = threadIdx.x & 7;
     unsigned long long acc = 0;
     int acc_w = -1;
     for (int j = 0;; ++j, advance(at)) {
@@ -1293,27 +1306,44 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
         }
         cp_wait<RG_STAGES - 2>();
         if (threadIdx.x == 0) s_nneed = s_nitem = 0;
+        if (threadIdx.x < RG_TH * 4) {
+            const int y = y0 + (threadIdx.x >> 2);
+            s_T[threadIdx.x >> 2][threadIdx.x & 3] = y < p.row_hi ? p.T[(size_t)y * 4 + (threadIdx.x & 3)] : 0u;
+        }
         __syncthreads();  // tile j staged for every thread; the previous tile's reads are done
         issue(j + RG_STAGES - 1);
         const uint32_t *sw = reinterpret_cast<const uint32_t *>(s_ring[j % RG_STAGES]);
-        // (1) words holding an empty cell
+        const int y = y0 + tr, wxv = wx0 + 4 * tq;
+        const bool row_ok = y < p.row_hi;
+        const uint4 cur4 = *reinterpret_cast<const uint4 *>(sw + (tr + 2) * RS + 4 * tq + 4);
+        // (1) words holding an empty cell, listed
+        uint32_t needm = 0u;
+        {
+            const uint32_t cw[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
 #pragma unroll
-        for (int u = 0; u < RG_WPT; ++u) {
-            const int tw = threadIdx.x + u * RG_THREADS;
-            const int r = tw / RG_TW, col = tw - r * RG_TW;
-            const int y = y0 + r, wx = wx0 + col;
-            const bool valid = y < p.row_hi && wx < real_words;
-            const uint32_t cur = sw[(r + 2) * RS + col + 4];
-            const bool need = valid && !word_full(p, wx, cur);
-            s_grow[tw] = 0u;
-            const unsigned m = __ballot_sync(0xffffffffu, need);
+            for (int u = 0; u < 4; ++u)
+                if (row_ok && wxv + u < real_words && !word_full(p, wxv + u, cw[u])) needm |= 1u << u;
+        }
+        *reinterpret_cast<uint4 *>(s_grow + 4 * threadIdx.x) = make_uint4(0u, 0u, 0u, 0u);
+        {
+            const int n = __popc(needm);
+            int incl = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
             int base = 0;
-            if (lane == 0 && m) base = atomicAdd(&s_nneed, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (need) s_need[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)tw;
+            if (lane == 31 && incl) base = atomicAdd(&s_nneed, incl);
+            base = __shfl_sync(0xffffffffu, base, 31) + incl - n;
+            while (needm) {
+                const int u = __ffs(needm) - 1;
+                needm &= needm - 1u;
+                s_need[base++] = (uint16_t)(4 * threadIdx.x + u);
+            }
         }
         __syncthreads();
-        // (2) counts and class masks of the listed words, and their groups to draw
+        // (2) counts and 2-bit classes of the listed words, and their groups to draw
         const int nneed = s_nneed;
         for (int k = threadIdx.x; k < nneed; k += RG_THREADS) {
             const int tw = s_need[k];
@@ -1353,9 +1383,12 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
                     }
                 }
             }
-            s_ge[0][k] = ge_const(c, p.cls_k1);
-            s_ge[1][k] = ge_const(c, p.cls_k2);
-            s_ge[2][k] = ge_const(c, p.cls_k3);
+            // class(k) = [k >= k1] + [k >= k2] + [k >= k3] (nested masks): low bit g1^g2^g3,
+            // high bit g2; interleaved into 2 bits per cell
+            const uint32_t g1 = ge_const(c, p.cls_k1), g2 = ge_const(c, p.cls_k2), g3 = ge_const(c, p.cls_k3);
+            const uint32_t lo = g1 ^ g2 ^ g3, hi = g2;
+            s_code[0][k] = spread16(lo) | (spread16(hi) << 1);
+            s_code[1][k] = spread16(lo >> 16) | (spread16(hi >> 16) << 1);
             const int nv = p.W - (wx << 5);  // valid cells of the word
             const uint32_t empty = ~cur & (nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u));
             uint32_t gm = 0u;
@@ -1376,52 +1409,35 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
             const int it = s_item[i];
             const int k = it >> 3, g = it & 7;
             const int tw = s_need[k];
-            const int r = tw / RG_TW, col = tw - r * RG_TW;
-            const int y = y0 + r, x0 = ((wx0 + col) << 5) + 4 * g;
+            const int r = tw >> 5, col = tw & 31;  // RG_TW = 32
+            const int yy = y0 + r, x0 = ((wx0 + col) << 5) + 4 * g;
             const uint32_t cur = sw[(r + 2) * RS + col + 4];
-            const uint32_t ge1 = s_ge[0][k], ge2 = s_ge[1][k], ge3 = s_ge[2][k];
-            const uint4 Trow = *reinterpret_cast<const uint4 *>(p.T + (size_t)y * 4);
-            const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)tstep, (uint32_t)(((int64_t)y * p.W + x0) >> 2), 0u);
-            const int nv = p.W - x0;  // valid cells of the group
+            const uint32_t code = s_code[g >> 2][k] >> (8 * (g & 3));  // 2 bits per cell of the group
+            const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)tstep, (uint32_t)(((int64_t)yy * p.W + x0) >> 2), 0u);
+            const int nv = p.W - x0;
             const uint32_t empty4 = (~cur >> (4 * g)) & (nv >= 4 ? 0xFu : ((1u << nv) - 1u));
+            const uint32_t *Tr = s_T[r];
             uint32_t bits = 0u;
-            if (p.t_monotone) {
-                // T[y][.] non-decreasing: d < T[class] iff d < T0, or class >= c and d < T[c]
-                // for some c (the largest admissible threshold decides), as 4-cell masks
-                const uint32_t g1 = (ge1 >> (4 * g)) & 0xFu, g2 = (ge2 >> (4 * g)) & 0xFu, g3 = (ge3 >> (4 * g)) & 0xFu;
-                uint32_t m0 = 0u, m1 = 0u, m2 = 0u, m3 = 0u;
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const uint32_t dm = word_of(d, m);
-                    m0 |= (dm < Trow.x ? 1u : 0u) << m;
-                    m1 |= (dm < Trow.y ? 1u : 0u) << m;
-                    m2 |= (dm < Trow.z ? 1u : 0u) << m;
-                    m3 |= (dm < Trow.w ? 1u : 0u) << m;
-                }
-                bits = empty4 & (m0 | (g1 & m1) | (g2 & m2) | (g3 & m3));
-            } else {
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const int bb = 4 * g + m;
-                    const uint32_t thr = ((ge3 >> bb) & 1u) ? Trow.w : ((ge2 >> bb) & 1u) ? Trow.z
-                                         : ((ge1 >> bb) & 1u) ? Trow.y : Trow.x;
-                    bits |= (((empty4 >> m) & 1u) && word_of(d, m) < thr) ? (1u << m) : 0u;
-                }
-            }
+            bits |= (d.x < Tr[code & 3u]) ? 1u : 0u;
+            bits |= (d.y < Tr[(code >> 2) & 3u]) ? 2u : 0u;
+            bits |= (d.z < Tr[(code >> 4) & 3u]) ? 4u : 0u;
+            bits |= (d.w < Tr[(code >> 6) & 3u]) ? 8u : 0u;
+            bits &= empty4;
             if (bits) atomicOr(&s_grow[tw], bits << (4 * g));
         }
         __syncthreads();
-        // (4) the tile's words
-#pragma unroll
-        for (int u = 0; u < RG_WPT; ++u) {
-            const int tw = threadIdx.x + u * RG_THREADS;
-            const int r = tw / RG_TW, col = tw - r * RG_TW;
-            const int y = y0 + r, wx = wx0 + col;
-            if (y < p.row_hi && wx < real_words) {
-                const uint32_t grow = s_grow[tw];
-                plane_next(p, tstep)[(size_t)w * pw + (size_t)y * p.WW + wx] = sw[(r + 2) * RS + col + 4] | grow;
-                acc += (unsigned long long)__popc(grow);
+        // (4) this thread's 4 words (128-bit store when the whole vector is in the row)
+        if (row_ok && wxv < real_words) {
+            const uint4 g4 = *reinterpret_cast<const uint4 *>(s_grow + 4 * threadIdx.x);
+            const uint4 o = make_uint4(cur4.x | g4.x, cur4.y | g4.y, cur4.z | g4.z, cur4.w | g4.w);
+            uint32_t *dst = plane_next(p, tstep) + (size_t)w * pw + (size_t)y * p.WW + wxv;
+            if (wxv + 4 <= real_words) {
+                *reinterpret_cast<uint4 *>(dst) = o;
+            } else {
+                const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+                for (int u = 0; wxv + u < real_words; ++u) dst[u] = ov[u];
             }
+            acc += (unsigned long long)(__popc(g4.x) + __popc(g4.y) + __popc(g4.z) + __popc(g4.w));
         }
     }
     cp_wait<0>();
