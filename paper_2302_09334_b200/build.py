@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsim.so")
 SOURCES = ["api.cu", "world.cu", "step.cu", "band.cu"]
-HEADERS = ["sim_internal.cuh", "block_scan.cuh", "phases.cuh"]
+HEADERS = ["sim_internal.cuh", "block_scan.cuh", "phases.cuh", "api_band.inc"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -29,6 +29,16 @@ def _stale() -> bool:
     deps.append(os.path.join(HERE, "..", "include", "sim.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
+
+
+CHECKED = os.path.join(HERE, "libsim_checked.so")  # diagnostic: device asserts (-DECO_CHECKS=1)
+
+
+def build_checked(force: bool = False) -> str:
+    """The diagnostic variant with device-side bounds asserts (tests/test_gpu_checks.py)."""
+    if not force and os.path.exists(CHECKED) and os.path.getmtime(CHECKED) >= os.path.getmtime(LIB) and not _stale():
+        return CHECKED
+    return build(force=True, defines=("ECO_CHECKS=1",), out=CHECKED)
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:

@@ -170,6 +170,7 @@ __global__ void k_band_move(DevParams p, BandParams bp) {
                     const int dir = ty < bp.y0 ? 0 : 1;
                     int32_t *box = box_dir(bp.mig_out, dir, bp.cap, ms);
                     const int k = atomicAdd(box, 1);
+                    ECO_CHECK(k < bp.cap);
                     int32_t *rec = box + BOX_HDR + (size_t)k * ms;
                     rec[0] = tg;
                     rec[1] = p.energy[slot];
@@ -189,6 +190,7 @@ __global__ void k_band_move(DevParams p, BandParams bp) {
         int q0 = 0;
         if (lane == 0 && m) q0 = atomicAdd(bp.n_plist, __popc(m));
         q0 = __shfl_sync(0xffffffffu, q0, 0);
+        ECO_CHECK(!stay || (q0 + __popc(m & ((1u << lane) - 1u)) < p.S && slot < p.S));
         if (stay) bp.plist[q0 + __popc(m & ((1u << lane) - 1u))] = slot;
     }
 }
@@ -276,6 +278,7 @@ __global__ void k_band_arrive_copy(DevParams p, BandParams bp) {
         const int32_t *rec = k < n_up ? box_dir(bp.up.mig, 1, bp.cap, ms) + BOX_HDR + (size_t)k * ms
                                       : box_dir(bp.down.mig, 0, bp.cap, ms) + BOX_HDR + (size_t)(k - n_up) * ms;
         const int slot = bp.arr_slot[k];
+        ECO_CHECK(slot >= 0 && slot < p.S && k < 2 * bp.cap);
         const float *f = reinterpret_cast<const float *>(rec);
         if (lane == 0) {
             const int cell = rec[0];
@@ -318,6 +321,7 @@ __global__ void k_band_live(DevParams p, BandParams bp) {
         int slot = 0, cellv = 0, dage = 0;
         if (i < n) {
             slot = bp.plist[i];
+            ECO_CHECK(slot >= 0 && slot < p.S && i < p.S);
             cellv = p.cell[slot];
             uint32_t bit;
             uint32_t *rw = word_ptr(Rn, p, cellv, bit);
@@ -513,6 +517,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         const unsigned long long k = p.bkey[c];
         const int q = (int)(0xFFFFFFFFu - (uint32_t)k);  // the winning parent's cell
         const int par = own_row(bp, row_of(p, q)) ? p.bslot[q] : -1;
+        ECO_CHECK(child >= 0 && child < p.S && par < p.S && n_surv + r < p.S);
         p.alive[child] = 1;
         atomicOr(p.alive_bits + (child >> 5), 1u << (child & 31));
         p.cell[child] = c;
@@ -563,6 +568,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
             p.repr[sc.x] = 0;
             int32_t *box = box_dir(bp.nb_out, dir, bp.cap, ns);
             const int kk = atomicAdd(box, 1);
+            ECO_CHECK(kk < bp.cap);
             int32_t *rec = box + BOX_HDR + (size_t)kk * ns;
             rec[0] = tg.x;
             rec[1] = sc.x;
@@ -648,6 +654,7 @@ __global__ void k_band_newborns(DevParams p, BandParams bp) {
         const int32_t *rec = k < n_up ? box_dir(bp.up.nb, 1, bp.cap, ns) + BOX_HDR + (size_t)k * ns
                                       : box_dir(bp.down.nb, 0, bp.cap, ns) + BOX_HDR + (size_t)(k - n_up) * ns;
         const int child = bp.cslot[rec[0]];
+        ECO_CHECK(child >= 0 && child < p.S);
         const float4 *src = reinterpret_cast<const float4 *>(rec + NB_HDR);
         float4 *dst = reinterpret_cast<float4 *>(p.weights + (size_t)child * p.Pd);
         for (int q = lane; q < p.Pd / 4; q += 32) dst[q] = src[q];

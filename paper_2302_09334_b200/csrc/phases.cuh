@@ -309,6 +309,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
         int dage = 0;  // metrics: age at death
         if (active) {
             slot = mr.x;
+            ECO_CHECK(slot >= 0 && slot < p.S && (mr.z < 0 || (int64_t)mr.z < (int64_t)p.H * p.W));
             const size_t gs = (size_t)w * p.S + slot;
             uint32_t *O = p.occ + (size_t)w * plane_words(p);
             uint32_t *Rn = plane_next(p, t) + (size_t)w * plane_words(p);
@@ -382,6 +383,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 if (ma) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), (unsigned long long)__popc(ma));
             }
             c0 = __shfl_sync(0xffffffffu, c0, 0);
+            ECO_CHECK(!cand || c0 + __popc(mc & ((1u << lane) - 1u)) < p.S);
             if (cand) p.cand[c0 + __popc(mc & ((1u << lane) - 1u))] = make_int2(slot, cand_cell);
             // metrics: the deaths' ages, and at a window end the movement bins (warp sums)
 #if ECO_METRICS & 1
@@ -394,6 +396,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             pos0 = __shfl_sync(0xffffffffu, pos0, 0);
             if (survive) {
                 const int q = pos0 + __popc(m & ((1u << lane) - 1u));
+                ECO_CHECK(q < p.S && slot >= 0 && slot < p.S);
                 list_of(p, t + 1, w)[q] = slot;
                 list_cell_of(p, t + 1, w)[q] = cand_cell;  // survivors: cand_cell is the cell
             }
@@ -413,6 +416,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             if (died_a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), 1ull);
             if (survive) {
                 const int q = atomicAdd(count_of(p, t + 1, w), 1);
+                ECO_CHECK(q < p.S);
                 list_of(p, t + 1, w)[q] = slot;
                 list_cell_of(p, t + 1, w)[q] = cand_cell;
             }
@@ -641,6 +645,7 @@ __device__ __forceinline__ int birth_parent_of(const DevParams &p, int w, int64_
 // child state of birth r in slot `child` on cell c; parent's repr reset; birth lists
 __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t, int c, int r, int n_surv, int child,
                                             int parent) {
+    ECO_CHECK(child >= 0 && child < p.S && parent >= 0 && parent < p.S && n_surv + r < p.S);
     const size_t cs = (size_t)w * p.S + child;
     p.alive[cs] = 1;
     atomicOr(p.alive_bits + (size_t)w * p.SW + (child >> 5), 1u << (child & 31));
@@ -928,6 +933,7 @@ __device__ __forceinline__ void mutate_batch(const PP &p, int w, int64_t t, uint
         mutate_item(p, (int)iu[u], d0[u], dstep[u], j0[u]);
         int child, parent;
         birth((int)bu[u], child, parent, cellc[u]);
+        ECO_CHECK(child >= 0 && child < p.S && parent >= 0 && parent < p.S);
         // sharded: mutated on the child's owner = the parent's (placement sets owner[child]
         // concurrently with this phase, so read the parent's, which is stable)
         if (p.n_ranks > 1 && p.owner[parent] != p.rank) continue;

@@ -24,6 +24,19 @@
 // sim_step(n >= 2) launches two-step graphs in which the second policy is a programmatic
 // dependent of the first k_post (griddepcontrol.wait in the policy).  Defined once here so
 // the host launch (api.cu) and the device wait (step.cu) always agree.
+// Diagnostic build (-DECO_CHECKS=1, libsim_checked.so): device asserts on every cell, slot,
+// list position and outbox index the kernels compute (compute-sanitizer is not available
+// on the GPU pool; tests/test_gpu_checks.py runs the checked build).
+#ifndef ECO_CHECKS
+#define ECO_CHECKS 0
+#endif
+#if ECO_CHECKS
+#include <cassert>
+#define ECO_CHECK(cond) assert(cond)
+#else
+#define ECO_CHECK(cond) ((void)0)
+#endif
+
 #ifndef ECO_STEP2_PDL
 #define ECO_STEP2_PDL 1
 #endif
@@ -205,6 +218,7 @@ __host__ __device__ __forceinline__ size_t plane_words(const DevParams &p) { ret
 // row of a cell (cell / W) without an integer division: a double multiply (relative error
 // < 2^-52, so the truncation is at most one below for cells < 2^31) plus one correction
 __device__ __forceinline__ int row_of(const DevParams &p, int cell) {
+    ECO_CHECK(cell >= 0 && (int64_t)cell < (int64_t)p.H * p.W);
     int y = __double2int_rz((double)cell * p.invW);
     y += (cell - y * p.W >= p.W) ? 1 : 0;
     return y;
