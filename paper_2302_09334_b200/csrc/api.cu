@@ -187,6 +187,8 @@ struct sim_ctx {
     eco::BandParams bp{};            // band: its exchange buffers and neighbours
     int32_t *n_own_dev = nullptr;
     struct BandNccl *nccl = nullptr; // parent with remote bands: the NCCL barrier
+    cudaStream_t side = nullptr;     // parent: the split policy's P rows beside the step
+    cudaEvent_t fork_ev[eco::BAND_MAX] = {}, join_ev = nullptr;
     int32_t *band_tmp = nullptr;     // parent: device scratch of get_state (a band's live list)
     float *band_canon = nullptr;     // parent: canonical rows of one band's live weights
     size_t band_canon_rows = 0;
@@ -377,6 +379,13 @@ void destroy_all(sim_ctx *h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (sim_ctx *b : h->bands) destroy_all(b);  // (they borrow this stream)
     h->bands.clear();
+    if (h->side) {
+        cudaStreamSynchronize(h->side);
+        cudaStreamDestroy(h->side);
+    }
+    for (auto &e : h->fork_ev)
+        if (e) cudaEventDestroy(e);
+    if (h->join_ev) cudaEventDestroy(h->join_ev);
     band_nccl_destroy(h);
     if (h->graph && l2_persist_enabled()) cudaCtxResetPersistingL2Cache();  // release the carve-out's lines
     drop_graphs(h);
@@ -493,7 +502,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     p.n_ranks = 1;
     p.rank = 0;
     // split policy (one world, Hd = 32, the default policy kernel): P rows made by k_post
-    p.split = (nw == 1 && d.Hd == 32 && S > 0 && !band && eco::policy_supports_shard()) ? 1 : 0;
+    p.split = (nw == 1 && d.Hd == 32 && S > 0 && eco::policy_supports_shard()) ? 1 : 0;
     // Everything but the weights lives in one arena, ordered by how latency-critical it is:
     // counters, barrier words, planes, lists and SoA first.  Graph kernels get an L2
     // access-policy window marking its prefix persisting (set_persistence below), so the
@@ -581,7 +590,9 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
         CKC(dalloc(h, &bp.n_plist, 1), "alloc");
         CKC(dalloc(h, &bp.arr_slot, 2 * (size_t)bp.cap), "alloc");
         CKC(dalloc(h, &bp.cslot, HW), "alloc");
-        CKC(dalloc(h, &bp.cand_tgt, S), "alloc");
+        CKC(dalloc(h, &bp.hcand, 2 * (size_t)bp.cap), "alloc");
+        CKC(dalloc(h, &bp.n_hcand, 1), "alloc");
+        CKC(dalloc(h, &bp.snap, 2), "alloc");
         CKC(dalloc(h, &bp.flags, 4), "alloc");
         CKC(dalloc(h, &h->n_own_dev, 1), "alloc");
     }

@@ -195,28 +195,41 @@ __global__ void k_band_move(DevParams p, BandParams bp) {
     }
 }
 
-// the departing agents' float state and weights into their outbox records (one warp per
-// record, 16-B vectors)
+// the departing agents' float state and weights into their outbox records: every thread
+// of the grid copies 16-B vectors of any record (a record is ~17 KB at Hd = 32; one warp per
+// record left each warp a chain of dependent 512-B copies: measured 117 us per step)
+__device__ __forceinline__ void copy_agent_vecs(const DevParams &p, size_t q, const float *logits, const float *h,
+                                                const float *c, const float *w, float *lo, float *ho, float *co,
+                                                float *wo) {
+    // vector q of an agent's float state: [0, 2) logits, then h, c (Hd/4 each), then Pd/4 weights
+    const int nh = p.Hd >> 2;
+    if (q < 2) {
+        reinterpret_cast<float4 *>(lo)[q] = reinterpret_cast<const float4 *>(logits)[q];
+    } else if (q < 2 + (size_t)nh) {
+        reinterpret_cast<float4 *>(ho)[q - 2] = reinterpret_cast<const float4 *>(h)[q - 2];
+    } else if (q < 2 + 2 * (size_t)nh) {
+        reinterpret_cast<float4 *>(co)[q - 2 - nh] = reinterpret_cast<const float4 *>(c)[q - 2 - nh];
+    } else {
+        const size_t k = q - 2 - 2 * nh;
+        reinterpret_cast<float4 *>(wo)[k] = reinterpret_cast<const float4 *>(w)[k];
+    }
+}
+
 __global__ void k_band_pack(DevParams p, BandParams bp) {
     const int ms = mig_stride(p.Hd, p.Pd);
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int dir = 0; dir < 2; ++dir) {
-        int32_t *box = box_dir(bp.mig_out, dir, bp.cap, ms);
-        const int n = *reinterpret_cast<volatile int32_t *>(box);
-        for (int k = warp; k < n; k += nwarps) {
-            int32_t *rec = box + BOX_HDR + (size_t)k * ms;
-            const int slot = rec[8];
-            float *f = reinterpret_cast<float *>(rec);
-            if (lane < LOGIT_STRIDE) f[16 + lane] = p.logits[(size_t)slot * LOGIT_STRIDE + lane];
-            for (int j = lane; j < p.Hd; j += 32) {
-                f[MIG_HDR + j] = p.h[(size_t)slot * p.Hd + j];
-                f[MIG_HDR + p.Hd + j] = p.c[(size_t)slot * p.Hd + j];
-            }
-            const float4 *src = reinterpret_cast<const float4 *>(p.weights + (size_t)slot * p.Pd);
-            float4 *dst = reinterpret_cast<float4 *>(f + MIG_HDR + 2 * p.Hd);
-            for (int q = lane; q < p.Pd / 4; q += 32) dst[q] = src[q];
-        }
+    const size_t per = 2 + 2 * (size_t)(p.Hd >> 2) + (size_t)(p.Pd >> 2);  // vectors per agent
+    const int n0 = *box_dir(bp.mig_out, 0, bp.cap, ms), n1 = *box_dir(bp.mig_out, 1, bp.cap, ms);
+    const size_t n = (size_t)(n0 + n1) * per;
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(v / per);
+        const size_t q = v - (size_t)k * per;
+        int32_t *rec = k < n0 ? box_dir(bp.mig_out, 0, bp.cap, ms) + BOX_HDR + (size_t)k * ms
+                              : box_dir(bp.mig_out, 1, bp.cap, ms) + BOX_HDR + (size_t)(k - n0) * ms;
+        const int slot = rec[8];
+        float *f = reinterpret_cast<float *>(rec);
+        copy_agent_vecs(p, q, p.logits + (size_t)slot * LOGIT_STRIDE, p.h + (size_t)slot * p.Hd,
+                        p.c + (size_t)slot * p.Hd, p.weights + (size_t)slot * p.Pd, f + 16, f + MIG_HDR,
+                        f + MIG_HDR + p.Hd, f + MIG_HDR + 2 * p.Hd);
     }
 }
 
@@ -272,35 +285,36 @@ __global__ void k_band_arrive_copy(DevParams p, BandParams bp) {
     const int ms = mig_stride(p.Hd, p.Pd);
     const int n_up = bp.up.plane0 ? *box_dir(bp.up.mig, 1, bp.cap, ms) : 0;
     const int got = bp.flags[1];
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int k = warp; k < got; k += nwarps) {
-        const int32_t *rec = k < n_up ? box_dir(bp.up.mig, 1, bp.cap, ms) + BOX_HDR + (size_t)k * ms
-                                      : box_dir(bp.down.mig, 0, bp.cap, ms) + BOX_HDR + (size_t)(k - n_up) * ms;
+    const size_t per = 2 + 2 * (size_t)(p.Hd >> 2) + (size_t)(p.Pd >> 2);
+    auto rec_of = [&](int k) {
+        return k < n_up ? box_dir(bp.up.mig, 1, bp.cap, ms) + BOX_HDR + (size_t)k * ms
+                        : box_dir(bp.down.mig, 0, bp.cap, ms) + BOX_HDR + (size_t)(k - n_up) * ms;
+    };
+    const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, gthr = (size_t)gridDim.x * blockDim.x;
+    for (size_t k = gtid; k < (size_t)got; k += gthr) {  // scalar state and occupancy
+        const int32_t *rec = rec_of((int)k);
         const int slot = bp.arr_slot[k];
-        ECO_CHECK(slot >= 0 && slot < p.S && k < 2 * bp.cap);
-        const float *f = reinterpret_cast<const float *>(rec);
-        if (lane == 0) {
-            const int cell = rec[0];
-            p.cell[slot] = cell;
-            p.energy[slot] = rec[1];
-            p.age[slot] = rec[2];
-            p.repr[slot] = rec[3];
-            p.last_action[slot] = (uint8_t)rec[4];
-            p.ate[slot] = (uint8_t)rec[5];
-            p.mv_cell[slot] = rec[6];
-            p.mv_inv[slot] = rec[7];
-            uint32_t ob;
-            atomicOr(word_ptr(p.occ, p, cell, ob), ob);
-        }
-        if (lane < LOGIT_STRIDE) p.logits[(size_t)slot * LOGIT_STRIDE + lane] = f[16 + lane];
-        for (int j = lane; j < p.Hd; j += 32) {
-            p.h[(size_t)slot * p.Hd + j] = f[MIG_HDR + j];
-            p.c[(size_t)slot * p.Hd + j] = f[MIG_HDR + p.Hd + j];
-        }
-        const float4 *src = reinterpret_cast<const float4 *>(f + MIG_HDR + 2 * p.Hd);
-        float4 *dst = reinterpret_cast<float4 *>(p.weights + (size_t)slot * p.Pd);
-        for (int q = lane; q < p.Pd / 4; q += 32) dst[q] = src[q];
+        ECO_CHECK(slot >= 0 && slot < p.S && (int)k < 2 * bp.cap);
+        const int cell = rec[0];
+        p.cell[slot] = cell;
+        p.energy[slot] = rec[1];
+        p.age[slot] = rec[2];
+        p.repr[slot] = rec[3];
+        p.last_action[slot] = (uint8_t)rec[4];
+        p.ate[slot] = (uint8_t)rec[5];
+        p.mv_cell[slot] = rec[6];
+        p.mv_inv[slot] = rec[7];
+        uint32_t ob;
+        atomicOr(word_ptr(p.occ, p, cell, ob), ob);
+    }
+    for (size_t v = gtid; v < (size_t)got * per; v += gthr) {  // logits, h, c, weights
+        const int k = (int)(v / per);
+        const size_t q = v - (size_t)k * per;
+        const float *f = reinterpret_cast<const float *>(rec_of(k));
+        const int slot = bp.arr_slot[k];
+        copy_agent_vecs(p, q, f + 16, f + MIG_HDR, f + MIG_HDR + p.Hd, f + MIG_HDR + 2 * p.Hd,
+                        p.logits + (size_t)slot * LOGIT_STRIDE, p.h + (size_t)slot * p.Hd, p.c + (size_t)slot * p.Hd,
+                        p.weights + (size_t)slot * p.Pd);
     }
 }
 
@@ -311,6 +325,7 @@ __global__ void k_band_arrive_copy(DevParams p, BandParams bp) {
 // candidate list; the step's counters.
 __global__ void k_band_live(DevParams p, BandParams bp) {
     const int64_t t = p.t[0];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bp.n_hcand = 0;  // (P7 lists this step's)
     const int n = *bp.n_plist;
     const int lane = threadIdx.x & 31;
     uint32_t *Rn = plane_next(p, t);
@@ -413,13 +428,16 @@ __global__ void k_band_claims(DevParams p, BandParams bp) {
             const int c = birth_target(p, t, sc.y, key);
             if (c < 0) {
                 no_cell = 1;
-                bp.cand_tgt[r] = make_int2(-1, 0);
             } else {
                 uint32_t bit;
                 atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
                 atomicMax(p.bkey + c, key);
                 p.bslot[sc.y] = sc.x;
-                bp.cand_tgt[r] = make_int2(c, (int)(uint32_t)(key >> 32));
+                if (!own_row(bp, row_of(p, c))) {  // a cell of a neighbour's row: P10 decides it here too
+                    const int k = atomicAdd(bp.n_hcand, 1);
+                    ECO_CHECK(k < 2 * bp.cap);
+                    bp.hcand[k] = make_int4(sc.x, sc.y, c, (int)(uint32_t)(key >> 32));
+                }
                 is_cand = 1;
             }
         }
@@ -541,15 +559,13 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         p.birth_parent[r] = par;
         p.birth_cell[r] = c;
     }
-    // local parents of children in a neighbour's boundary row
-    const int nc = *p.n_cand;
+    // local parents of children in a neighbour's boundary row (listed by the claims)
+    const int nc = *bp.n_hcand;
     const uint32_t *bb = bbits_of(p, t, 0);
     for (int k = threadIdx.x; k < nc; k += BAND_NT) {
-        const int2 tg = bp.cand_tgt[k];
-        if (tg.x < 0) continue;
+        const int4 hc = bp.hcand[k];
+        const int2 tg = make_int2(hc.z, hc.w), sc = make_int2(hc.x, hc.y);
         const int ty = row_of(p, tg.x);
-        if (own_row(bp, ty)) continue;
-        const int2 sc = p.cand[k];
         const unsigned long long key =
             ((unsigned long long)(uint32_t)tg.y << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)sc.y);
         if (p.bkey[tg.x] != key) continue;  // lost the claim
@@ -590,6 +606,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         rec->resources = res;
         *count_of(p, t + 1, 0) = n_surv + n_place;
         p.n_births[0] = n_place;
+        *p.p_children = n_place;  // split policy: the children (list end) start from their bias
         unsigned long long *tot = p.totals;
         atomicAdd(tot + 0, 1ull);
         atomicAdd(tot + 1, (unsigned long long)rec->agents_at_start);
@@ -648,16 +665,16 @@ __global__ void k_band_newborns(DevParams p, BandParams bp) {
     const int ns = nb_stride(p.Pd);
     const int n_up = bp.up.plane0 ? *box_dir(bp.up.nb, 1, bp.cap, ns) : 0;
     const int n_dn = bp.down.plane0 ? *box_dir(bp.down.nb, 0, bp.cap, ns) : 0;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int k = warp; k < n_up + n_dn; k += nwarps) {
+    const size_t per = (size_t)(p.Pd >> 2);
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < (size_t)(n_up + n_dn) * per;
+         v += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(v / per);
+        const size_t q = v - (size_t)k * per;
         const int32_t *rec = k < n_up ? box_dir(bp.up.nb, 1, bp.cap, ns) + BOX_HDR + (size_t)k * ns
                                       : box_dir(bp.down.nb, 0, bp.cap, ns) + BOX_HDR + (size_t)(k - n_up) * ns;
         const int child = bp.cslot[rec[0]];
         ECO_CHECK(child >= 0 && child < p.S);
-        const float4 *src = reinterpret_cast<const float4 *>(rec + NB_HDR);
-        float4 *dst = reinterpret_cast<float4 *>(p.weights + (size_t)child * p.Pd);
-        for (int q = lane; q < p.Pd / 4; q += 32) dst[q] = src[q];
+        reinterpret_cast<float4 *>(p.weights + (size_t)child * p.Pd)[q] = reinterpret_cast<const float4 *>(rec + NB_HDR)[q];
     }
 }
 
@@ -703,7 +720,19 @@ __global__ void __launch_bounds__(BAND_NT) k_band_init_agents(DevParams p, BandP
     }
 }
 
+// split policy: the step and the survivors' count after P5 (read by the P-row kernel on the
+// second stream while P10 advances t and appends the children)
+__global__ void k_band_snap(DevParams p, BandParams bp) {
+    const int64_t t = p.t[0];
+    bp.snap[0] = t + 1;
+    bp.snap[1] = *count_of(p, t + 1, 0);
+}
+
 // --------------------------------------------------------------------- launchers
+cudaError_t band_snap(const DevParams &p, const BandParams &bp, cudaStream_t s) {
+    k_band_snap<<<1, 1, 0, s>>>(p, bp);
+    return cudaGetLastError();
+}
 cudaError_t band_halo(const DevParams &p, const BandParams &bp, int kind, cudaStream_t s) {
     k_band_halo<<<32, 256, 0, s>>>(p, bp, kind);
     return cudaGetLastError();

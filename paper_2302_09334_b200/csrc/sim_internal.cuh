@@ -139,7 +139,10 @@ struct BandParams {
     int32_t *plist, *n_plist;  // agents of this step after the move (stayers, then arrivals)
     int32_t *arr_slot;         // [2 cap] the arrivals' local slots
     int32_t *cslot;            // [H*W] local slot of a child whose parent is in a neighbour band
-    int2 *cand_tgt;            // [S] per eligible parent: (claimed cell or -1, claim key hi)
+    int4 *hcand;               // [2 cap] own parents claiming a cell in a neighbour's row:
+                               // (parent slot, parent cell, claimed cell, claim key hi)
+    int32_t *n_hcand;
+    int64_t *snap;             // [2] split policy: (step t, survivors) after P5, for the P rows
     int32_t *flags;            // [0] bit 0: local slot pool exhausted; [1] arrivals placed
     BandPeer up, down;         // bands b-1 and b+1 (plane0 == nullptr: none)
     const int64_t *all_counts[BAND_MAX];  // every band's counts
@@ -302,6 +305,8 @@ cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot
                                                                   // own list of step t, zero records
 bool policy_supports_shard();  // the Hd = 32 policy kernel of this build honours ownership
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);  // P of step t
+cudaError_t launch_prepare_p_snap(const DevParams &p, const int64_t *snap, cudaStream_t s);  // banded
+cudaError_t band_snap(const DevParams &p, const BandParams &bp, cudaStream_t s);
 cudaError_t post_prepare();  // kernel attributes of k_post (dynamic shared memory)
 
 // banded mode (band.cu); kinds: halo 0 = X1, 1 = X4a; merge 0 = X2, 1 = X4b

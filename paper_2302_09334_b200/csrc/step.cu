@@ -444,6 +444,17 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p(DevParams 
     }
 }
 
+// Banded mode: P rows of the survivors of the step in progress (list_of(snap[0])[0, snap[1]),
+// snapshotted right after the band's consumption/physiology/death), on a second stream while
+// the rest of the step runs; the children placed later have none (p_children, set by the rank).
+__global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p_snap(DevParams p, const int64_t *snap) {
+    extern __shared__ float4 half_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ag = warp * 2 + (lane >> 4);
+    hh_pass<HALF_DEPTH>(p, list_of(p, snap[0], 0), (int)snap[1], ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
+                        half_smem + (ag * HALF_DEPTH) * 32);
+}
+
 #ifdef ECO_TIMELINE
 // diagnostic build: per step t (ring of 1024), the policy's first block start and last block
 // end and k_post's, as globaltimer ns in phase_ns[16 + (t % 1024) * 4 + {0..3}] (starts
@@ -811,6 +822,8 @@ cudaError_t policy_prepare() {
     e = cudaFuncSetAttribute(k_policy_half<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_prepare_p, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_prepare_p_snap, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_policy_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
 }
@@ -1506,6 +1519,13 @@ cudaError_t launch_mv_pass(const DevParams &p, cudaStream_t s) {
 }
 
 bool policy_supports_shard() { return true; }  // k_policy_half honours ownership
+
+cudaError_t launch_prepare_p_snap(const DevParams &p, const int64_t *snap, cudaStream_t s) {
+    if (!p.split) return cudaSuccess;
+    const unsigned blocks = (unsigned)((p.S + HALF_AGENTS - 1) / HALF_AGENTS);
+    k_prepare_p_snap<<<blocks > 0 ? blocks : 1, HALF_THREADS, HALF_SMEM, s>>>(p, snap);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (!p.split) return cudaSuccess;
