@@ -293,12 +293,13 @@ SIM_API sim_status sim_band_nccl_id(void *out128);
 SIM_API sim_status sim_band_nccl_init(sim_handle h, const void *id128, int32_t n_ranks, int32_t rank);
 /* One banded step with CUDA events around every local band's phases, run one band after the
  * other (so each time is that band's alone, as on its own GPU); synchronises.  out:
- * [band_local][n_phases] ms, n_phases = SIM_BAND_PHASES in the order halo_x1, policy,
- * merge_x2, move, arrive_x3, live, prep_p, halo_x4a, claims, merge_x4b, counts, rank,
- * mutate, newborns_x5, regrow (prep_p: the next step's recurrent gate sums P = W_hh h + b
- * of the survivors, which sim_step runs on a second stream beside halo_x4a .. regrow; 0
- * unless hidden = 32).  (A banded sim_step on one GPU replays one CUDA graph per step.) */
-#define SIM_BAND_PHASES 15
+ * [band_local][n_phases] ms, n_phases = SIM_BAND_PHASES in the order halo_x1 (with the
+ * previous step's cross-band newborns), policy, merge_x2, move, arrive_x3, live, prep_p,
+ * halo_x4a, claims, merge_x4b, rank, mutate, regrow (prep_p: the next step's recurrent gate
+ * sums P = W_hh h + b of the survivors, which sim_step runs on a second stream beside
+ * halo_x4a .. regrow; 0 unless hidden = 32).  (A banded sim_step on one GPU replays one
+ * CUDA graph per step.) */
+#define SIM_BAND_PHASES 13
 SIM_API sim_status sim_band_step_timed(sim_handle h, float *out, int32_t n_phases);
 
 /* Synchronise the handle's stream (reports deferred errors). */

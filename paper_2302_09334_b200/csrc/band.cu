@@ -22,16 +22,18 @@
 //   X4a R'' = R_{t+1} rows [y0-2, y0), [y1, y1+2) and O'' rows y0-1, y1 from the neighbours
 //   P7  birth candidates and claims of the own eligible parents (R21; halo cells included)
 //   X4b the birth-claim keys and claimed-cell bits of the boundary rows, max/OR-merged
-//   P9  counts: claimed cells in the own rows, survivors; ALL bands' counts are read (the
-//       capacity rule R22 is global: claimed cells are ranked row-major over the whole grid,
-//       i.e. band order then local order, and the first S - A_total are placed)
+//   P9  counts (kept by P5, P7 and X4b): claimed cells in the own rows, survivors; ALL
+//       bands' counts are read (the capacity rule R22 is global: claimed cells are ranked
+//       row-major over the whole grid, i.e. band order then local order, and the first
+//       S - A_total are placed)
 //   P10 rank and placement of the children in the own rows (first free local slots); a
 //       parent whose child's cell lies in a neighbour's row computes the child's global rank
 //       itself (from the merged boundary-row bits and the counts), so both sides take the
 //       same capacity decision; such a parent's mutated child weights go to the neighbour
 //   P11 mutation (children of local parents, and the outgoing newborns' weights)
-//   X5  incoming newborns' weights into the child slots placed in P10
 //   P13 regrowth of step t+1 on the own rows (R_{t+1} rows y0-2 .. y1+1 are present)
+//   X5  incoming newborns' weights into the child slots placed in P10, pulled with the next
+//       step's X1 (before the children's first policy; sim_get_state pulls them too)
 //
 // Exchanges are PULLS: a band's kernel reads its neighbour's buffers (device pointers of
 // another band of this process, or peer memory mapped from another GPU).  Between a
@@ -72,6 +74,7 @@ __device__ __forceinline__ bool own_row(const BandParams &bp, int y) { return y 
 // ------------------------------------------------------------------- X1 / X4a halo
 // kind 0 (X1): R' = plane_next(t) and O rows, 3 each side; kind 1 (X4a): R'' (plane_next(t))
 // 2 rows each side, O'' 1 row each side.  Rows are copied word for word (global rows).
+__global__ void k_band_newborns(DevParams p, BandParams bp);
 __global__ void k_band_halo(DevParams p, BandParams bp, int kind) {
     const int64_t t = p.t[0];
     const int nr = kind == 0 ? 3 : 2, no = kind == 0 ? 3 : 1;
@@ -131,7 +134,12 @@ __global__ void k_band_merge(DevParams p, BandParams bp, int kind) {
             if (y < 0 || y >= p.H) continue;
             const size_t off = (size_t)y * WW + wx;
             const uint32_t v = q.bbits[(size_t)(t & 1) * plane_words(p) + off];
-            if (v) atomicOr(const_cast<uint32_t *>(mine) + off, v);
+            if (v) {
+                const uint32_t old = atomicOr(const_cast<uint32_t *>(mine) + off, v);
+                const int fresh = __popc(v & ~old);  // cells claimed only from the neighbour's side
+                if (fresh && own_row(bp, y))
+                    atomicAdd(reinterpret_cast<unsigned long long *>(bp.counts + (t & 1) * 4), (unsigned long long)fresh);
+            }
         }
     }
 }
@@ -325,7 +333,10 @@ __global__ void k_band_arrive_copy(DevParams p, BandParams bp) {
 // candidate list; the step's counters.
 __global__ void k_band_live(DevParams p, BandParams bp) {
     const int64_t t = p.t[0];
-    if (blockIdx.x == 0 && threadIdx.x == 0) *bp.n_hcand = 0;  // (P7 lists this step's)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *bp.n_hcand = 0;                      // (P7 lists this step's)
+        bp.counts[(t & 1) * 4] = 0;           // own-row claimed cells, counted by P7 and X4b
+    }
     const int n = *bp.n_plist;
     const int lane = threadIdx.x & 31;
     uint32_t *Rn = plane_next(p, t);
@@ -421,7 +432,7 @@ __global__ void k_band_claims(DevParams p, BandParams bp) {
     const unsigned lane = threadIdx.x & 31;
     for (size_t base = gtid - lane; base < (size_t)nc; base += gthr) {
         const size_t r = base + lane;
-        int no_cell = 0, is_cand = 0;
+        int no_cell = 0, is_cand = 0, new_own = 0;
         if (r < (size_t)nc) {
             const int2 sc = p.cand[r];
             unsigned long long key;
@@ -430,10 +441,12 @@ __global__ void k_band_claims(DevParams p, BandParams bp) {
                 no_cell = 1;
             } else {
                 uint32_t bit;
-                atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
+                const uint32_t old = atomicOr(word_ptr(bbits_of(p, t, 0), p, c, bit), bit);
                 atomicMax(p.bkey + c, key);
                 p.bslot[sc.y] = sc.x;
-                if (!own_row(bp, row_of(p, c))) {  // a cell of a neighbour's row: P10 decides it here too
+                const bool own = own_row(bp, row_of(p, c));
+                if (own && !(old & bit)) new_own = 1;  // a distinct claimed cell of the own rows
+                if (!own) {  // a cell of a neighbour's row: P10 decides it here too
                     const int k = atomicAdd(bp.n_hcand, 1);
                     ECO_CHECK(k < 2 * bp.cap);
                     bp.hcand[k] = make_int4(sc.x, sc.y, c, (int)(uint32_t)(key >> 32));
@@ -441,33 +454,14 @@ __global__ void k_band_claims(DevParams p, BandParams bp) {
                 is_cand = 1;
             }
         }
-        const int a = __reduce_add_sync(0xffffffffu, no_cell), b = __reduce_add_sync(0xffffffffu, is_cand);
+        const int a = __reduce_add_sync(0xffffffffu, no_cell), b = __reduce_add_sync(0xffffffffu, is_cand),
+                  n_own = __reduce_add_sync(0xffffffffu, new_own);
         if (lane == 0) {
             sim_step_record *rec = record_of(p, t, 0);
             if (a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_no_cell), (unsigned long long)a);
             if (b) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deferred_claim), (unsigned long long)b);
+            if (n_own) atomicAdd(reinterpret_cast<unsigned long long *>(bp.counts + (t & 1) * 4), (unsigned long long)n_own);
         }
-    }
-}
-
-// ---------------------------------------------------------------------- P9 counts
-// [parity t][0] claimed cells in the own rows, [1] survivors (own agents of step t+1 before
-// the births).  One block.
-__global__ void __launch_bounds__(BAND_NT) k_band_counts(DevParams p, BandParams bp) {
-    __shared__ unsigned long long s_sum;
-    const int64_t t = p.t[0];
-    if (threadIdx.x == 0) s_sum = 0ull;
-    __syncthreads();
-    const uint32_t *bb = bbits_of(p, t, 0);
-    unsigned long long c = 0ull;
-    for (size_t k = (size_t)bp.y0 * p.WW + threadIdx.x; k < (size_t)bp.y1 * p.WW; k += BAND_NT) c += __popc(bb[k]);
-    c = __reduce_add_sync(0xffffffffu, (unsigned)c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_sum, c);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t *cnt = bp.counts + (size_t)(t & 1) * 4;
-        cnt[0] = (int64_t)s_sum;
-        cnt[1] = *count_of(p, t + 1, 0);
     }
 }
 
@@ -494,9 +488,11 @@ __device__ __forceinline__ int row_popc_range(const uint32_t *row, int x0, int x
     return n;
 }
 
+constexpr int BAND_ROW_WORDS = 2048;  // boundary-row prefix counts kept in shared memory (W <= 65,536)
 __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams bp) {
     __shared__ uint32_t scratch[2 * (BAND_NT / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP];
+    __shared__ uint16_t s_pre[2][BAND_ROW_WORDS];  // exclusive prefix popcounts of rows y0-1 and y1
     __shared__ long long s_clt, s_atot;
     const int64_t t = p.t[0];
     const int par_t = (int)(t & 1);
@@ -559,9 +555,28 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         p.birth_parent[r] = par;
         p.birth_cell[r] = c;
     }
-    // local parents of children in a neighbour's boundary row (listed by the claims)
+    // local parents of children in a neighbour's boundary row (listed by the claims); the
+    // claimed cells of those two rows ranked with prefix popcounts (one block scan per row)
     const int nc = *bp.n_hcand;
     const uint32_t *bb = bbits_of(p, t, 0);
+    const bool pre_ok = p.WW <= BAND_ROW_WORDS;
+    if (nc > 0 && pre_ok) {  // (block-uniform)
+        for (int side = 0; side < 2; ++side) {
+            const int y = side == 0 ? bp.y0 - 1 : bp.y1;
+            const bool ex = y >= 0 && y < p.H;
+            uint32_t run = 0u;
+            for (int w0 = 0; w0 < p.WW; w0 += BAND_NT) {
+                const int wx = w0 + (int)threadIdx.x;
+                const uint32_t v = (ex && wx < p.WW) ? (uint32_t)__popc(bb[(size_t)y * p.WW + wx]) : 0u;
+                uint32_t tot;
+                const uint32_t e = run + block_exclusive_scan<BAND_NT>(v, scratch, tot);
+                if (wx < p.WW) s_pre[side][wx] = (uint16_t)e;
+                run += tot;
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
     for (int k = threadIdx.x; k < nc; k += BAND_NT) {
         const int4 hc = bp.hcand[k];
         const int2 tg = make_int2(hc.z, hc.w), sc = make_int2(hc.x, hc.y);
@@ -573,11 +588,16 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         const uint32_t *row = bb + (size_t)ty * p.WW;
         long long g;
         int dir;
+        // claimed cells of the row before tx (prefix of whole words + the partial word)
+        const int wx = tx >> 5;
+        const int before = pre_ok ? (int)s_pre[ty < bp.y0 ? 0 : 1][wx] + __popc(row[wx] & ((1u << (tx & 31)) - 1u))
+                                  : row_popc_range(row, 0, tx);
         if (ty < bp.y0) {  // the up neighbour's last row: its claimed cells at x' >= tx rank after it
-            g = clt - row_popc_range(row, tx, p.W);
+            const int total = pre_ok ? (int)s_pre[0][p.WW - 1] + __popc(row[p.WW - 1]) : row_popc_range(row, 0, p.W);
+            g = clt - (total - before);
             dir = 0;
         } else {  // the down neighbour's first row
-            g = clt + c_own + row_popc_range(row, 0, tx);
+            g = clt + c_own + before;
             dir = 1;
         }
         if (g < cap) {
@@ -720,12 +740,15 @@ __global__ void __launch_bounds__(BAND_NT) k_band_init_agents(DevParams p, BandP
     }
 }
 
-// split policy: the step and the survivors' count after P5 (read by the P-row kernel on the
-// second stream while P10 advances t and appends the children)
+// after P5: the survivors (the band's count for the global cap) and, for the split policy,
+// the step and the survivors' count read by the P-row kernel on the second stream while P10
+// advances t and appends the children
 __global__ void k_band_snap(DevParams p, BandParams bp) {
     const int64_t t = p.t[0];
+    const int n = *count_of(p, t + 1, 0);
     bp.snap[0] = t + 1;
-    bp.snap[1] = *count_of(p, t + 1, 0);
+    bp.snap[1] = n;
+    bp.counts[(t & 1) * 4 + 1] = n;  // survivors, read by every band for the global cap
 }
 
 // --------------------------------------------------------------------- launchers
@@ -759,10 +782,6 @@ cudaError_t band_live(const DevParams &p, const BandParams &bp, int sms, cudaStr
 }
 cudaError_t band_claims(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s) {
     k_band_claims<<<sms * 2, 256, 0, s>>>(p, bp);
-    return cudaGetLastError();
-}
-cudaError_t band_counts(const DevParams &p, const BandParams &bp, cudaStream_t s) {
-    k_band_counts<<<1, BAND_NT, 0, s>>>(p, bp);
     return cudaGetLastError();
 }
 cudaError_t band_rank(const DevParams &p, const BandParams &bp, cudaStream_t s) {

@@ -316,7 +316,6 @@ cudaError_t band_move(const DevParams &p, const BandParams &bp, int sms, cudaStr
 cudaError_t band_arrive(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
 cudaError_t band_live(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
 cudaError_t band_claims(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
-cudaError_t band_counts(const DevParams &p, const BandParams &bp, cudaStream_t s);
 cudaError_t band_rank(const DevParams &p, const BandParams &bp, cudaStream_t s);
 cudaError_t band_mutate(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);
 cudaError_t band_newborns(const DevParams &p, const BandParams &bp, int sms, cudaStream_t s);

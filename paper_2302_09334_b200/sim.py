@@ -31,7 +31,7 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist",
             "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init", "sim_band_step_timed")
 BAND_PHASES = ("halo_x1", "policy", "merge_x2", "move", "arrive_x3", "live", "prep_p", "halo_x4a", "claims",
-               "merge_x4b", "counts", "rank", "mutate", "newborns_x5", "regrow")  # include/sim.h: SIM_BAND_PHASES
+               "merge_x4b", "rank", "mutate", "regrow")  # include/sim.h: SIM_BAND_PHASES
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
                "reserved4", "reserved5", "reserved6", "reserved7",
                "claim.warp_sum_b0", "regrow.warp_sum_b1")  # summed over the warps of block 0 / block 1

@@ -9,7 +9,7 @@
   alone (the bands run one after the other), i.e. what each band's own GPU would spend.
 * Estimate of a G-GPU step: sum over phases of the slowest band's phase time (the P rows of
   the split policy overlap the phases after them, as on the second stream of sim_step), plus the
-  phase barriers (6 neighbour token exchanges and 1 all-reduce per step) at an ASSUMED
+  phase barriers (5 neighbour token exchanges and 1 all-reduce per step) at an ASSUMED
   latency (--nbr-us, --all-us: host-launched NCCL over NVLink, not measured here); the
   exchanges themselves are pull kernels inside the phase times.  E(G) = T(1) / (G T(G)).
 Writes one JSON object (stdout, --out)."""
@@ -91,7 +91,7 @@ def main():
             # the P rows (prep_p) run on a second stream beside the phases after it
             ip = sim.BAND_PHASES.index("prep_p")
             compute = float(slowest[:ip].sum() + max(slowest[ip + 1:].sum(), slowest[ip]))
-            est = compute + (6 * a.nbr_us + a.all_us) / 1e3
+            est = compute + (5 * a.nbr_us + a.all_us) / 1e3  # 5 neighbour barriers, 1 all-reduce per step
             res["bands"].append({
                 "G": G, "rows": kind, "band_rows": rows, "agents_per_band": per_band, "band_slots": slots,
                 "phase_ms_slowest_band": dict(zip(sim.BAND_PHASES, slowest.round(5).tolist())),
