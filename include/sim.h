@@ -227,6 +227,25 @@ SIM_API sim_status sim_get_totals(sim_handle h, sim_totals *out);
 #define SIM_MOVE_WINDOW 50
 #define SIM_MOVE_BINS 17
 SIM_API sim_status sim_get_move_hist(sim_handle h, int64_t first, int64_t n, int32_t *out);
+/* Greediness (§3.3, "Does the density of resources affect agents' greediness?"):
+ * windows of SIM_GREED_WINDOW steps aligned to multiples of it from step 0; T_r counts the
+ * windows in which the agent had at least one resource in its field of view (a 1 in the
+ * resource channel of its observation, R10/R11) and C_r those in which it consumed at least
+ * one resource; G = C_r / T_r.  A window is counted for every agent alive at the start of
+ * its last step (agents born inside a window count its remainder).  T_r, C_r: caller-owned
+ * int32 [n_worlds][S], slot order of sim_get_state (banded: its compaction); meaningful for
+ * live slots; the counts restart at 0 at sim_set_state and for every newborn.  Sharded
+ * handles: valid on the slot's owner only.  Synchronises. */
+#define SIM_GREED_WINDOW 20
+SIM_API sim_status sim_get_greediness(sim_handle h, int32_t *T_r, int32_t *C_r);
+/* Life expectancy (Appendix C: "average of age of agent that died during a large
+ * time window of 500 timesteps"), accumulated on the device: for windows [first, first+n)
+ * of SIM_LIFE_WINDOW steps (aligned to multiples of it), per world the deaths and the summed
+ * ages at death (age after the step's increment); the expectancy is age_sum / deaths.
+ * out[i][w] (int64, caller-owned [n][n_worlds]); windows must be complete and among the
+ * last kept (the step log's span); counts restart at sim_set_state.  Synchronises. */
+#define SIM_LIFE_WINDOW 500
+SIM_API sim_status sim_get_life_windows(sim_handle h, int64_t first, int64_t n, int64_t *deaths, int64_t *age_sum);
 /* Run ONE step without the graph, with CUDA events around every kernel; synchronises. */
 SIM_API sim_status sim_step_timed(sim_handle h, sim_step_timing *out);
 /* Run ONE step exactly as graph mode does (the policy kernel, then the cooperative k_post

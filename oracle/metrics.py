@@ -11,6 +11,12 @@ library (include/sim.h: sim_get_move_hist, sim_step_record.death_age_sum).
   iff it is alive through it ("every agent alive during a time window"; born or dying
   inside it excludes it, SPEC design decision) — read off the state as: alive at the start
   of step 50k and at the end of step 50k+49 with its age grown by exactly 50.
+* Greediness (§3.3 lab set-up: "non-overlapping fixed windows of 20 timesteps",
+  T_r = windows with "at least one resource in its field of view", C_r = windows in which
+  "the agent consumed at least one resource", G = C_r / T_r): windows aligned to multiples
+  of 20 from step 0; the field of view is the agent's observation (its resource channel,
+  after the step's regrowth, R10/R11) at every step of the window it is alive; a window is
+  closed for the agents alive at the start of its last step; a newborn starts from zero.
 * Life expectancy (Appendix C: "average of age of agent that died during a large
   time window of 500 timesteps"; SPEC.md metrics.life_expectancy): per step the sum of the
   ages at death (an agent that dies in step t was alive at its start and its age was
@@ -18,7 +24,7 @@ library (include/sim.h: sim_get_move_hist, sim_step_record.death_age_sum).
 """
 import numpy as np
 
-WINDOW, BINS, LIFE_WINDOW = 50, 17, 500
+WINDOW, BINS, LIFE_WINDOW, GREED_WINDOW = 50, 17, 500, 20
 
 
 def movement_bin(c0: int, c1: int, cols: int) -> int:
@@ -69,3 +75,43 @@ class MetricsFold:
             tot, n = out.get(k, (0, 0))
             out[k] = (tot + s, n + self.deaths[t])
         return {k: (tot / n if n else None) for k, (tot, n) in out.items()}
+
+
+class GreedinessFold:
+    """Feed (state before step t, state after it) for consecutive steps; the oracle's own
+    regrowth and observation functions give the field of view (test infrastructure)."""
+
+    def __init__(self, wc):
+        self.wc = wc
+        S = wc.slots
+        self.T = np.zeros(S, np.int64)
+        self.C = np.zeros(S, np.int64)
+        self.seen = np.zeros(S, bool)
+        self.ate = np.zeros(S, bool)
+
+    def feed(self, before: dict, after: dict):
+        import oracle
+        wc = self.wc
+        t = int(before["t"])
+        a0 = before["alive"] == 1
+        Rp, _ = oracle.regrow(wc, t, before["resources"])  # R' of step t (what the policy sees)
+        O = np.zeros((wc.rows, wc.cols), np.uint8)
+        cells = before["cell"][a0]
+        O.reshape(-1)[cells] = 1
+        wd2 = (2 * wc.obs_radius + 1) ** 2
+        for i in np.flatnonzero(a0):
+            c = int(before["cell"][i])
+            x = oracle.observe(wc, Rp, O, c // wc.cols, c % wc.cols)
+            if x[:wd2].any():
+                self.seen[i] = True
+        # consumption of the agents alive at step start (a newborn in a freed slot has age 0)
+        same = a0 & (after["alive"] == 1) & (after["age"] == before["age"] + 1)
+        self.ate[same & (after["ate"] == 1)] = True
+        if t % GREED_WINDOW == GREED_WINDOW - 1:
+            self.T[a0] += self.seen[a0]
+            self.C[a0] += self.ate[a0]
+            self.seen[:] = False
+            self.ate[:] = False
+        born = (after["alive"] == 1) & (after["age"] == 0)
+        self.T[born] = self.C[born] = 0
+        self.seen[born] = self.ate[born] = False

@@ -21,6 +21,12 @@ inline int mv_windows(int log_cap) {
     while (c < log_cap / SIM_MOVE_WINDOW + 2) c <<= 1;
     return c;
 }
+// life-expectancy windows kept: a power of two covering the step log
+inline int le_windows(int log_cap) {
+    int c = 2;
+    while (c < log_cap / SIM_LIFE_WINDOW + 2) c <<= 1;
+    return c;
+}
 }  // namespace
 
 namespace {
@@ -550,6 +556,12 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     H(&p.mv_cell, nw * S);
     H(&p.mv_inv, nw * S);
     H(&p.mv_hist, nw * (size_t)p.mv_cap * SIM_MOVE_BINS);
+    H(&p.gr_seen, nw * S);
+    H(&p.gr_ate, nw * S);
+    H(&p.gr_T, nw * S);
+    H(&p.gr_C, nw * S);
+    p.le_cap = le_windows(d.log_cap);
+    H(&p.le, nw * (size_t)p.le_cap * 2);
     H(&h->forced_dev, nw * S);
     H(&p.Pbuf, p.split ? S * (size_t)d.Hd * 4 : 1);
     H(&p.h, nw * S * d.Hd);
@@ -980,6 +992,11 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, cudaMemsetAsync(p.bbits, 0, 2 * nw * d.pw * 4, s), "memset");
     CK(h, cudaMemsetAsync(p.log, 0, (size_t)d.log_cap * nw * sizeof(sim_step_record), s), "memset");
     CK(h, cudaMemsetAsync(p.totals, 0, 8 * 8, s), "memset");
+    CK(h, cudaMemsetAsync(p.gr_seen, 0, nw * S, s), "memset");  // greediness counts from here on
+    CK(h, cudaMemsetAsync(p.gr_ate, 0, nw * S, s), "memset");
+    CK(h, cudaMemsetAsync(p.gr_T, 0, nw * S * 4, s), "memset");
+    CK(h, cudaMemsetAsync(p.gr_C, 0, nw * S * 4, s), "memset");
+    CK(h, cudaMemsetAsync(p.le, 0, nw * (size_t)p.le_cap * 16, s), "memset");
     CK(h, eco::launch_rebuild(p, s), "rebuild");
     CK(h, eco::launch_set_owner(p, s), "owners");
     CK(h, cudaMemsetAsync(p.pol_ctr, 0, 2 * sizeof(unsigned long long), s), "memset");
@@ -1103,6 +1120,48 @@ sim_status sim_get_move_hist(sim_handle h, int64_t first, int64_t n, int32_t *ou
                                   h->p.mv_hist + (w * h->p.mv_cap + (size_t)((first + i) & (h->p.mv_cap - 1))) * SIM_MOVE_BINS,
                                   SIM_MOVE_BINS * 4, cudaMemcpyDeviceToHost, h->stream), "move histogram");
     return sync(h);
+}
+
+sim_status sim_get_greediness(sim_handle h, int32_t *T_r, int32_t *C_r) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!T_r || !C_r) return fail(SIM_E_INVALID, "invalid argument: NULL");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if (!h->bands.empty()) return band_get_greediness(h, T_r, C_r);
+    if ((st = sync(h)) != SIM_OK) return st;
+    const size_t n = (size_t)h->d.n_worlds * h->d.S;
+    CK(h, cudaMemcpyAsync(T_r, h->p.gr_T, n * 4, cudaMemcpyDeviceToHost, h->stream), "greediness");
+    CK(h, cudaMemcpyAsync(C_r, h->p.gr_C, n * 4, cudaMemcpyDeviceToHost, h->stream), "greediness");
+    return sync(h);
+}
+
+sim_status sim_get_life_windows(sim_handle h, int64_t first, int64_t n, int64_t *deaths, int64_t *age_sum) {
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (n < 0 || (n > 0 && (!deaths || !age_sum))) return fail(SIM_E_INVALID, "invalid argument: n/out");
+    const int64_t done = h->t / SIM_LIFE_WINDOW;  // complete windows
+    const int cap = h->bands.empty() ? h->p.le_cap : h->bands[0]->p.le_cap;
+    if (first < 0 || first + n > done || first < done - cap)
+        return fail(SIM_E_INVALID, "invalid argument: windows [%lld, %lld) not kept (complete windows %lld, capacity %d)",
+                    (long long)first, (long long)(first + n), (long long)done, cap);
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    const size_t nw = h->d.n_worlds;
+    memset(deaths, 0, (size_t)n * nw * 8);
+    memset(age_sum, 0, (size_t)n * nw * 8);
+    std::vector<sim_ctx *> parts;
+    if (h->bands.empty()) parts.push_back(h);
+    else parts = h->bands;
+    for (sim_ctx *b : parts)
+        for (int64_t i = 0; i < n; ++i)
+            for (size_t w = 0; w < nw; ++w) {
+                unsigned long long v[2];
+                CK(h, cudaMemcpy(v, b->p.le + (w * b->p.le_cap + (size_t)((first + i) & (b->p.le_cap - 1))) * 2, 16,
+                                 cudaMemcpyDeviceToHost), "life windows");
+                deaths[i * nw + w] += (int64_t)v[0];
+                age_sum[i * nw + w] += (int64_t)v[1];
+            }
+    return SIM_OK;
 }
 
 sim_status sim_get_totals(sim_handle h, sim_totals *out) {

@@ -48,7 +48,8 @@ namespace eco {
 
 // ------------------------------------------------------------------ record layouts
 // migrant record (int32 words): [0] cell (the new one), [1] energy, [2] age, [3] repr,
-// [4] last_action, [5] ate, [6] mv_cell, [7] mv_inv, [8] source slot, [16..24) logits,
+// [4] last_action, [5] ate, [6] mv_cell, [7] mv_inv, [8] source slot, [9] greediness T_r,
+// [10] C_r, [11] the window's flags (seen | ate << 1), [16..24) logits,
 // [24, 24+Hd) h, [24+Hd, 24+2Hd) c, [24+2Hd, +Pd) weights in the device layout.
 // newborn record: [0] cell, [1] parent slot, [4, 4+Pd) weights (device layout, mutated).
 // An outbox direction: [0] count, records from word 4.  dir 0 = towards band b-1 (up),
@@ -189,6 +190,9 @@ __global__ void k_band_move(DevParams p, BandParams bp) {
                     rec[6] = p.mv_cell[slot];
                     rec[7] = p.mv_inv[slot];
                     rec[8] = slot;
+                    rec[9] = p.gr_T[slot];
+                    rec[10] = p.gr_C[slot];
+                    rec[11] = p.gr_seen[slot] | (p.gr_ate[slot] << 1);
                     p.alive[slot] = 0;
                     atomicAnd(p.alive_bits + (slot >> 5), ~(1u << (slot & 31)));
                 }
@@ -312,6 +316,10 @@ __global__ void k_band_arrive_copy(DevParams p, BandParams bp) {
         p.ate[slot] = (uint8_t)rec[5];
         p.mv_cell[slot] = rec[6];
         p.mv_inv[slot] = rec[7];
+        p.gr_T[slot] = rec[9];
+        p.gr_C[slot] = rec[10];
+        p.gr_seen[slot] = (uint8_t)(rec[11] & 1);
+        p.gr_ate[slot] = (uint8_t)(rec[11] >> 1);
         uint32_t ob;
         atomicOr(word_ptr(p.occ, p, cell, ob), ob);
     }
@@ -356,6 +364,7 @@ __global__ void k_band_live(DevParams p, BandParams bp) {
                 ate = true;
             }
             p.ate[slot] = ate ? 1 : 0;
+            greed_update(p, slot, t, ate);
             long long e = (long long)p.energy[slot] + (ate ? (long long)p.e_gain : 0ll) - (long long)p.e_decay;
             if (p.e_max != 0x7fffffff && e > p.e_max) e = p.e_max;
             const int en = (int)e, ag = p.age[slot] + 1;
@@ -540,6 +549,10 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         p.repr[child] = 0;
         p.last_action[child] = 0;
         p.ate[child] = 0;
+        p.gr_seen[child] = 0;
+        p.gr_ate[child] = 0;
+        p.gr_T[child] = 0;
+        p.gr_C[child] = 0;
         for (int j = 0; j < p.Hd; ++j) {
             p.h[(size_t)child * p.Hd + j] = 0.f;
             p.c[(size_t)child * p.Hd + j] = 0.f;
@@ -624,6 +637,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         rec->deferred_capacity = c_own - n_place;
         rec->population = n_surv + n_place;
         rec->resources = res;
+        life_window_add(p, 0, t, rec->deaths_energy + rec->deaths_age, rec->death_age_sum);
         *count_of(p, t + 1, 0) = n_surv + n_place;
         p.n_births[0] = n_place;
         *p.p_children = n_place;  // split policy: the children (list end) start from their bias
@@ -713,6 +727,8 @@ __global__ void __launch_bounds__(BAND_NT) k_band_init_agents(DevParams p, BandP
         p.repr[i] = 0;
         p.last_action[i] = 0;
         p.ate[i] = 0;
+        p.gr_seen[i] = p.gr_ate[i] = 0;
+        p.gr_T[i] = p.gr_C[i] = 0;
     }
     __syncthreads();
     uint32_t run = 0u;

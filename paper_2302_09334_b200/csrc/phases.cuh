@@ -343,6 +343,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 ate = true;
             }
             p.ate[gs] = ate ? 1 : 0;
+            greed_update(p, gs, t, ate);
             long long e = (long long)en0 + (ate ? (long long)p.e_gain : 0ll) - (long long)p.e_decay;
             if (p.e_max != 0x7fffffff && e > p.e_max) e = p.e_max;
             const int en = (int)e;
@@ -655,6 +656,10 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
     p.repr[cs] = 0;
     p.last_action[cs] = 0;
     p.ate[cs] = 0;
+    p.gr_seen[cs] = 0;
+    p.gr_ate[cs] = 0;
+    p.gr_T[cs] = 0;
+    p.gr_C[cs] = 0;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);  // Hd in {4, 8, 16, 32}: rows are float4-aligned
     for (int k = 0; k < p.Hd; k += 4) {
         *reinterpret_cast<float4 *>(p.h + cs * p.Hd + k) = z4;
@@ -756,6 +761,7 @@ __device__ __forceinline__ void rank_finalize(const DevParams &p, int w, int64_t
     rec->deferred_capacity = n_win - n_place;
     rec->population = n_surv + n_place;
     rec->resources = res;
+    life_window_add(p, w, t, de + da, rec->death_age_sum);
     *count_of(p, t + 1, w) = n_surv + n_place;
     p.n_births[w] = n_place;
     unsigned long long *tot = p.totals;

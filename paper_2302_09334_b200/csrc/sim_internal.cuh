@@ -106,6 +106,15 @@ struct DevParams {
     int32_t *mv_cell, *mv_inv;   // [n_worlds][S]: cell and age - 50 k at the start of window k
     int32_t *mv_hist;            // [n_worlds][mv_cap][17]
     int mv_cap;                  // windows kept (a power of two)
+    // greediness (§3.3 lab set-up, "non-overlapping fixed windows of 20 timesteps"):
+    // per slot, flags of the current window (a resource was in the field of view / the agent
+    // ate) and the counts T_r, C_r of the closed windows; G = C_r / T_r
+    uint8_t *gr_seen, *gr_ate;   // [n_worlds][S]
+    int32_t *gr_T, *gr_C;        // [n_worlds][S]
+    // life expectancy (Appendix C, 500-step windows): per window, deaths and the
+    // summed ages at death ([n_worlds][le_cap][2], a ring of windows aligned to 500 t)
+    unsigned long long *le;
+    int le_cap;
     int32_t *p_children;         // list positions at the end of step t's list without a P row
     int2 *cand;                  // [n_worlds][S] single world: this step's eligible parents (slot, cell)
     int32_t *n_cand;             // [n_worlds] their count
@@ -269,6 +278,29 @@ __device__ __forceinline__ int32_t *count_of(const DevParams &p, int64_t t, int 
 
 __device__ __forceinline__ sim_step_record *record_of(const DevParams &p, int64_t t, int w) {
     return p.log + (size_t)(t & (p.log_cap - 1)) * p.n_worlds + w;  // log_cap: a power of two
+}
+
+constexpr int GR_WINDOW = 20;   // sim.h SIM_GREED_WINDOW
+constexpr int LE_WINDOW = 500;  // sim.h SIM_LIFE_WINDOW
+__device__ __forceinline__ bool gr_window_end(int64_t t) { return (uint32_t)t % GR_WINDOW == GR_WINDOW - 1; }
+// the greediness bookkeeping of one agent processed in step t (ate: this step's consumption)
+__device__ __forceinline__ void greed_update(const DevParams &p, size_t gs, int64_t t, bool ate) {
+    if (gr_window_end(t)) {
+        const int seen = p.gr_seen[gs], a = ate ? 1 : p.gr_ate[gs];
+        p.gr_T[gs] += seen;
+        p.gr_C[gs] += a;
+        p.gr_seen[gs] = 0;
+        p.gr_ate[gs] = 0;
+    } else if (ate) {
+        p.gr_ate[gs] = 1;
+    }
+}
+// the step's deaths into its 500-step window (one thread per world, after the step's counts)
+__device__ __forceinline__ void life_window_add(const DevParams &p, int w, int64_t t, int64_t deaths, int64_t age_sum) {
+    if (!deaths) return;
+    unsigned long long *e = p.le + ((size_t)w * p.le_cap + (size_t)((t / LE_WINDOW) & (p.le_cap - 1))) * 2;
+    atomicAdd(e, (unsigned long long)deaths);
+    atomicAdd(e + 1, (unsigned long long)age_sum);
 }
 
 // N, S, E, W (R13 order for moves is stay, N, S, E, W; births use N, S, E, W = 0..3)

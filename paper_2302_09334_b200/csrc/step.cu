@@ -115,6 +115,10 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
         p.logits[gs * LOGIT_STRIDE + a] = lg[a];
     }
     ctr.add(p, w, nnz, (double)bestv - second < 1e-4);
+    {  // greediness: a resource in the field of view (the window's resource channel, R10/R11)
+        const int wd2 = (2 * p.r + 1) * (2 * p.r + 1);  // <= 49
+        if (m_lo & ((1ull << wd2) - 1ull)) p.gr_seen[gs] = 1;
+    }
     int act = best;
     if (forced_on) {
         const uint8_t f = p.forced[gs];

@@ -54,6 +54,8 @@ __global__ void k_init_agents(DevParams p, int w, int n_initial, const unsigned 
     p.repr[gs] = 0;
     p.last_action[gs] = 0;
     p.ate[gs] = 0;
+    p.gr_seen[gs] = p.gr_ate[gs] = 0;
+    p.gr_T[gs] = p.gr_C[gs] = 0;
 }
 
 // initial weights w_j = (float)(std * z_j), z from INIT_W keyed by the initial cell

@@ -29,7 +29,9 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_step_timed", "sim_synchronize", "sim_kernels_per_step", "sim_get_phase_ns",
             "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
             "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist",
-            "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init", "sim_band_step_timed")
+            "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init", "sim_band_step_timed",
+            "sim_get_greediness", "sim_get_life_windows")
+GREED_WINDOW, LIFE_WINDOW = 20, 500  # include/sim.h: SIM_GREED_WINDOW, SIM_LIFE_WINDOW
 BAND_PHASES = ("halo_x1", "policy", "merge_x2", "move", "arrive_x3", "live", "prep_p", "halo_x4a", "claims",
                "merge_x4b", "rank", "mutate", "regrow")  # include/sim.h: SIM_BAND_PHASES
 POST_PHASES = ("move", "birth_claim", "birth_rank+regrow_next", "mutate",
@@ -142,6 +144,9 @@ def lib():
                 L.sim_band_nccl_id.argtypes = [ctypes.c_void_p]
                 L.sim_band_nccl_init.argtypes = [H, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
                 L.sim_band_step_timed.argtypes = [H, ctypes.c_void_p, ctypes.c_int32]
+            if hasattr(L, "sim_get_greediness"):
+                L.sim_get_greediness.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p]
+                L.sim_get_life_windows.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
             for f in EXPORTED:
                 if f not in ("sim_last_error", "sim_kernels_per_step") and hasattr(L, f):
                     getattr(L, f).restype = ctypes.c_int
@@ -415,6 +420,20 @@ class World:
         out = np.zeros((n, self.n_worlds, MOVE_BINS), np.int32)
         _check(lib().sim_get_move_hist(self._h, int(first), int(n), _ptr(out)))
         return out
+
+    def greediness(self):
+        """(T_r, C_r) int32 [n_worlds][S] (include/sim.h sim_get_greediness); G = C_r / T_r."""
+        T = np.zeros((self.n_worlds, self.wc.slots), np.int32)
+        C = np.zeros((self.n_worlds, self.wc.slots), np.int32)
+        _check(lib().sim_get_greediness(self._h, _ptr(T), _ptr(C)))
+        return T, C
+
+    def life_windows(self, first: int, n: int):
+        """(deaths, age_sum) int64 [n][n_worlds] of 500-step windows [first, first+n)."""
+        d = np.zeros((n, self.n_worlds), np.int64)
+        a = np.zeros((n, self.n_worlds), np.int64)
+        _check(lib().sim_get_life_windows(self._h, int(first), int(n), _ptr(d), _ptr(a)))
+        return d, a
 
     def totals(self) -> dict:
         tt = SimTotals()

@@ -620,3 +620,65 @@ def test_metrics_after_set_state_mid_window():
     fold = _fold_run(world, orc, 75)
     assert world.move_hist(0, 1).sum() == 0
     assert np.array_equal(world.move_hist(1, 1)[0, 0], fold.hist[1])
+
+
+# ------------------------------------------------- greediness and life expectancy (NEXT-3)
+def test_greediness_counts_equal_oracle_fold():
+    """T_r and C_r of every live agent after 200 tiny steps (10 windows; the GPU forced to
+    the oracle's actions, M2) equal the oracle fold (oracle/metrics.py GreedinessFold)."""
+    from oracle import metrics
+    wc = workloads.tiny().replace(repr_steps=6, e_repr_gt=10300)  # births reuse slots
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    fold = metrics.GreedinessFold(wc)
+    births = 0
+    for t in range(200):
+        before = orc.state()
+        orec = orc.step(return_actions=True)
+        fold.feed(before, orc.state())
+        births += orec["births"]
+        f = np.full((1, wc.slots), 255, np.uint8)
+        f[0] = orec["actions"]
+        world.set_forced_actions(f)
+        world.step(1)
+    world.set_forced_actions(None)
+    g = gpu_state(world, weights=False)
+    compare_ints(g, orc.state(), "greediness run end")
+    T, C = world.greediness()
+    live = orc.st["alive"] == 1
+    assert births > 0 and int(fold.T[live].sum()) > 0 and int(fold.C[live].sum()) > 0
+    assert np.array_equal(T[0][live], fold.T[live]) and np.array_equal(C[0][live], fold.C[live])
+    world.destroy()
+
+
+def test_banded_greediness_equals_unbanded_by_cell():
+    wc = workloads.paper_scale()
+    ref = sim.World(wc)
+    ban = sim.World(wc, bands=dict(n_bands=4))
+    ref.step(120)
+    ban.step(120)
+    out = []
+    for w in (ref, ban):
+        st = w.get_state(("alive", "cell"))
+        T, C = w.greediness()
+        live = np.flatnonzero(st["alive"][0])
+        out.append(dict(zip(st["cell"][0][live].tolist(), zip(T[0][live].tolist(), C[0][live].tolist()))))
+    assert out[0] == out[1] and sum(v[0] for v in out[0].values()) > 0
+    ref.destroy()
+    ban.destroy()
+
+
+def test_life_windows_equal_the_records():
+    """The device's 500-step windows of deaths and ages at death equal the sums of the step
+    records (which are pinned against the oracle) over each window."""
+    wc = workloads.paper_scale()
+    world = sim.World(wc, log_capacity=2048)
+    world.step(1100)
+    d, a = world.life_windows(0, 2)
+    log = world.step_log(0, 1000)[:, 0]
+    for k in range(2):
+        rk = log[500 * k:500 * (k + 1)]
+        assert d[k, 0] == int(rk["deaths_energy"].sum() + rk["deaths_age"].sum())
+        assert a[k, 0] == int(rk["death_age_sum"].sum())
+    assert d[1, 0] > 0
+    world.destroy()

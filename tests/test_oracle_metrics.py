@@ -59,3 +59,25 @@ def test_scripted_walk_histogram_and_death_age():
     assert sum(fold.deaths.values()) == 1
     assert ow.st["cell"][0] == 2 * wc.cols + 52
     assert fold.life_expectancy_windows()[0] == 10
+
+
+# ------------------------------------------------------------------- greediness (NEXT-3)
+def test_greediness_fold_scripted():
+    """Regrowth off.  A stays 2 cells west of a resource (in its 5x5 field of view, never
+    eats) for 40 steps: T_r = 2, C_r = 0.  B walks east onto a resource in step 5 (window 0)
+    and then stays on the bare cell with nothing in view: T_r = 1 (window 0 only), C_r = 1.
+    D has nothing in view at all: T_r = C_r = 0."""
+    wc = small_config(rows=12, cols=60, slots=4).replace(obs_radius=2)
+    st = build_state(wc, [dict(slot=0, y=2, x=5), dict(slot=1, y=8, x=20), dict(slot=2, y=8, x=50)])
+    st["resources"][2, 7] = 1         # A's: 2 east, never reached
+    st["resources"][8, 25] = 1        # B's: 5 east of B
+    w = oracle.OracleWorld(wc, state=st)
+    fold = metrics.GreedinessFold(wc)
+    for t in range(40):
+        acts = {1: E} if t < 5 else {}
+        before = w.state()
+        w.step(forced=forced(wc, acts))
+        fold.feed(before, w.state())
+    assert (fold.T[0], fold.C[0]) == (2, 0)
+    assert (fold.T[1], fold.C[1]) == (1, 1)
+    assert (fold.T[2], fold.C[2]) == (0, 0)
