@@ -56,6 +56,7 @@ class Config(ctypes.Structure):
         ("e_init", ctypes.c_int32), ("e_decay", ctypes.c_int32), ("e_gain", ctypes.c_int32),
         ("e_repr_gt", ctypes.c_int32), ("e_death_le", ctypes.c_int32), ("e_max", ctypes.c_int32),
         ("repr_steps", ctypes.c_int32), ("max_age", ctypes.c_int32),
+        ("climate_alpha", ctypes.c_double), ("death_steps", ctypes.c_int32), ("lethal_walls", ctypes.c_int32),
     ]
 
 
@@ -66,12 +67,12 @@ class State(ctypes.Structure):
         ("energy", ctypes.c_void_p), ("age", ctypes.c_void_p), ("repr", ctypes.c_void_p),
         ("last_action", ctypes.c_void_p), ("ate", ctypes.c_void_p),
         ("h", ctypes.c_void_p), ("c", ctypes.c_void_p), ("weights", ctypes.c_void_p),
-        ("logits", ctypes.c_void_p),
+        ("logits", ctypes.c_void_p), ("low", ctypes.c_void_p),
     ]
 
 
 RECORD_FIELDS = ("t", "grown", "eaten", "births", "deaths_energy", "deaths_age", "deferred_no_cell",
-                 "deferred_claim", "deferred_capacity", "population", "resources", "near_ties")
+                 "deferred_claim", "deferred_capacity", "population", "resources", "near_ties", "deaths_wall")
 
 
 class Record(ctypes.Structure):
@@ -143,6 +144,9 @@ def make_config(wc, world: int = 0) -> Config:
     c.e_init, c.e_decay, c.e_gain = wc.e_init, wc.e_decay, wc.e_gain
     c.e_repr_gt, c.e_death_le, c.e_max = wc.e_repr_gt, wc.e_death_le, wc.e_max
     c.repr_steps, c.max_age = wc.repr_steps, wc.max_age
+    c.climate_alpha = float(getattr(wc, "climate_alpha", 0.0))
+    c.death_steps = int(getattr(wc, "death_steps", 0))
+    c.lethal_walls = int(getattr(wc, "lethal_walls", 0))
     return c
 
 
@@ -256,7 +260,7 @@ class OracleWorld:
         s = self._cst
         s.t = int(self.st["t"])
         for f in ("resources", "alive", "cell", "energy", "age", "repr", "last_action", "ate", "h", "c",
-                  "weights", "logits"):
+                  "weights", "logits", "low"):
             setattr(s, f, _ptr(self.st[f]))
         return ctypes.byref(s)
 

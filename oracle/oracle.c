@@ -117,17 +117,23 @@ int orc_validate(const orc_config *cfg, char *msg, int msg_len) {
     if (!(cfg->mutation_std >= 0.0)) return bad(msg, msg_len, "mutation_std");
     if (cfg->repr_steps < 1) return bad(msg, msg_len, "repr_steps");
     if (cfg->max_age < 0) return bad(msg, msg_len, "max_age");
+    if (!(cfg->climate_alpha >= 0.0)) return bad(msg, msg_len, "climate_alpha");
+    if (cfg->death_steps < 0) return bad(msg, msg_len, "death_steps");
+    if (cfg->lethal_walls != 0 && cfg->lethal_walls != 1) return bad(msg, msg_len, "lethal_walls");
     return ORC_OK;
 }
 
 /* ------------------------------------------------------------ regrowth (C.3.1) */
-/* lat(y) = lat_top + (lat_bottom-lat_top)*(y/(H-1)), division first (R3);
+/* lat(y) = lat_top + (lat_bottom-lat_top)*(y/(H-1)), division first (R3); with
+ * climate_alpha > 0 the paper's climate c(x) = (alpha^x + 1)/(alpha + 1) at x = y/(H-1)
+ * (x = 1 at the bottom row, R1);
  * p = lat*f[c] + spont ("p = p_I * c(x) + c");
  * T = min(floor(p*2^32), 2^32-1) (R8). */
 void orc_thresholds(const orc_config *cfg, uint32_t *T) {
     for (int32_t y = 0; y < cfg->rows; ++y) {
         double frac = (double)y / (double)(cfg->rows - 1);
         double lat = cfg->lat_top + (cfg->lat_bottom - cfg->lat_top) * frac;
+        if (cfg->climate_alpha > 0.0) lat = (pow(cfg->climate_alpha, frac) + 1.0) / (cfg->climate_alpha + 1.0);
         for (int c = 0; c < 4; ++c) {
             double p = lat * cfg->f_value[c] + cfg->spontaneous;
             double s = floor(p * 4294967296.0);
@@ -312,6 +318,7 @@ int orc_init(const orc_config *cfg, orc_state *st) {
         st->energy[i] = is_init ? cfg->e_init : 0;
         st->age[i] = 0;
         st->repr[i] = 0;
+        if (st->low) st->low[i] = 0;
         st->last_action[i] = 0;
         st->ate[i] = 0;
         for (int32_t k = 0; k < Hd; ++k) {
@@ -387,7 +394,10 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
         if (!st->alive[i] || action[i] == 0) continue;
         int32_t y = st->cell[i] / W, xx = st->cell[i] % W;
         int32_t ty = y + DY[action[i]], tx = xx + DX[action[i]];
-        if (ty < 0 || ty >= H || tx < 0 || tx >= W) continue;
+        if (ty < 0 || ty >= H || tx < 0 || tx >= W) {
+            if (cfg->lethal_walls) target[i] = -2; /* walks into the wall: dies */
+            continue;
+        }
         int32_t tc = ty * W + tx;
         if (O[tc]) continue;
         uint32_t w4[4];
@@ -398,6 +408,14 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
     }
     for (int32_t i = 0; i < S; ++i)
         if (target[i] >= 0 && claim[target[i]] == key[i]) st->cell[i] = target[i];
+    /* wall deaths: before consumption, so such an agent neither eats nor ages; its age at
+     * death counts the step (age + 1, as every death) */
+    for (int32_t i = 0; i < S; ++i)
+        if (st->alive[i] && target[i] == -2) {
+            st->alive[i] = 0;
+            st->ate[i] = 0;
+            rec->deaths_wall++;
+        }
 
     /* 5. CONSUME ("if the agent consumes a resource") */
     for (int32_t i = 0; i < S; ++i) {
@@ -420,12 +438,17 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
         st->energy[i] = (int32_t)e;
         st->age[i] += 1;
         st->repr[i] = (st->energy[i] > cfg->e_repr_gt) ? st->repr[i] + 1 : 0;
+        if (st->low) st->low[i] = (st->energy[i] <= cfg->e_death_le) ? st->low[i] + 1 : 0;
     }
 
     /* 7. DEATH (immediate form, R18) */
     for (int32_t i = 0; i < S; ++i) {
         if (!st->alive[i]) continue;
-        if (st->energy[i] <= cfg->e_death_le) {
+        /* immediate form (R18), or the paper's timer: T_death consecutive steps at or below
+         * the threshold */
+        const int starved = cfg->death_steps > 0 ? (st->low && st->low[i] >= cfg->death_steps)
+                                                 : (st->energy[i] <= cfg->e_death_le);
+        if (starved) {
             st->alive[i] = 0;
             rec->deaths_energy++;
         } else if (st->age[i] > cfg->max_age) {
@@ -504,6 +527,7 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
             st->energy[ch] = cfg->e_init;
             st->age[ch] = 0;
             st->repr[ch] = 0;
+            if (st->low) st->low[ch] = 0;
             st->last_action[ch] = 0;
             st->ate[ch] = 0;
             for (int32_t k = 0; k < Hd; ++k) {

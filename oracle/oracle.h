@@ -55,6 +55,12 @@ typedef struct {
     double init_weight_std, mutation_std;
     int32_t e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max; /* milli-units */
     int32_t repr_steps, max_age;
+    /* the paper's own world (App. B.4), off by default:            */
+    double climate_alpha;         /* > 0: c(x) = (alpha^x + 1)/(alpha + 1), x = y/(H-1),  */
+                                  /* replaces the linear lat               */
+    int32_t death_steps;          /* > 0: die after this many consecutive steps with      */
+                                  /* energy <= e_death_le (T_death)          */
+    int32_t lethal_walls;         /* 1: a move off the grid kills the agent */
 } orc_config;
 
 /* Canonical state; all buffers are owned by the caller. */
@@ -72,6 +78,7 @@ typedef struct {
     float *c;             /* [S][Hd]                                             */
     float *weights;       /* [S][P] canonical: W_ih[4Hd][I], W_hh[4Hd][Hd], b[4Hd], W_out[5][Hd], b_out[5] */
     float *logits;        /* [S][5]                                              */
+    int32_t *low;         /* [S] consecutive steps with energy <= e_death_le (death timer) */
 } orc_state;
 
 typedef struct {
@@ -81,6 +88,7 @@ typedef struct {
     int64_t deferred_no_cell, deferred_claim, deferred_capacity;
     int64_t population, resources; /* after the step */
     int64_t near_ties;              /* live agents with top1-top2 logit margin < 1e-4 */
+    int64_t deaths_wall;            /* agents killed by a move off the grid (lethal walls) */
 } orc_record;
 
 int32_t orc_param_count(const orc_config *cfg);

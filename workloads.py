@@ -46,6 +46,10 @@ class WorldConfig:
     e_max: int = INT32_MAX                   # no clip
     repr_steps: int = 20                     # ... for 20 consecutive steps
     max_age: int = 1000
+    # the paper's own world (App. B.4); BASELINE's world leaves them off
+    climate_alpha: float = 0.0               # > 0: exponential climate (alpha^x + 1)/(alpha + 1)
+    death_steps: int = 0                     # > 0: the death timer T_death (else immediate death)
+    lethal_walls: int = 0                    # 1: moving off the grid kills
     steps: int = 100                         # run length named by the config
     name: str = ""
 
@@ -77,6 +81,28 @@ def paper_scale() -> WorldConfig:
     """BASELINE.json configs[1]: 200x400, seed 1, rho 0.1, 8192 slots / 1000 agents, 7x7x2 obs, Hd 32, 10,000 steps."""
     return WorldConfig(rows=200, cols=400, seeds=(1,), init_resource_p=0.10, slots=8192, n_initial=1000,
                        obs_radius=3, hidden=32, steps=10000, name="paper_scale")
+
+
+def paper_world() -> WorldConfig:
+    """The paper's own natural environment (App. B.4; SURVEY.md §8(f)
+    NEXT-1), on this build's mechanics: 400x200 read as H = 200 rows x W = 400 (R2); 1000
+    slots, 330 initial agents; "16 0000" resources read as 16,000 = Bernoulli(0.2) of the
+    80,000 cells; regrowth p = p_I c(x) + c with p_I = 0.002 * 1[I >= 1] over the 4 direct
+    neighbours (the disc of r^2 = 1; class 1 iff k >= 1, SPEC's indicator reading of
+    1_{I=1}), c(x) = (200^x + 1)/201 with x = 1 at the bottom row, c = 5e-5; E0 = E_max = 3,
+    decay 0.025, +1 per resource (milli-units: 3000, 25, 1000, clip 3000); reproduction after
+    T_repr = 140 steps above E_min = 0; death after T_death = 200 steps below 0 (energy <= -1
+    milli-unit) or at age > 650; sigma = 0.02; lethal walls; an LSTM of hidden size 4.
+    Deviations kept from this build's mechanics: exclusive occupancy with the
+    child on an adjacent cell (the paper: the parent's cell), a 7x7x2 window (the paper:
+    15x15 with walls) and the LSTM + linear head with argmax (the paper: a CNN-LSTM with
+    softmax sampling, NEXT-2)."""
+    return WorldConfig(rows=200, cols=400, seeds=(1,), init_resource_p=0.2, regrow_r2=1,
+                       f_class_min_k=(0, 1, 5, 5), f_value=(0.0, 0.002, 0.0, 0.0), spontaneous=5e-5,
+                       climate_alpha=200.0, slots=1000, n_initial=330, obs_radius=3, hidden=4,
+                       mutation_std=0.02, e_init=3000, e_decay=25, e_gain=1000, e_repr_gt=0, e_death_le=-1,
+                       e_max=3000, repr_steps=140, death_steps=200, max_age=650, lethal_walls=1,
+                       steps=1_000_000, name="paper_world")
 
 
 def regrowth_micro(rows: int = 200, cols: int = 400) -> WorldConfig:
@@ -136,6 +162,7 @@ def empty_state(cfg: WorldConfig) -> dict:
         "c": np.zeros((S, Hd), np.float32),
         "weights": np.zeros((S, P), np.float32),
         "logits": np.zeros((S, A), np.float32),
+        "low": np.zeros(S, np.int32),
     }
 
 
