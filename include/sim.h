@@ -98,6 +98,14 @@ typedef struct {
     int32_t band_slots;     /* agent slots of each band (0 -> slots: a band can then hold
                                the whole population and never overflows); a band whose
                                pool overflows poisons the handle with SIM_E_OOM           */
+    /* The paper's own world (App. B.4), all off
+     * (0) for BASELINE's world: */
+    double climate_alpha;   /* > 0: climate c(x) = (alpha^x + 1)/(alpha + 1) at x = y/(H-1)
+                                replaces the linear lat_top..lat_bottom      */
+    int32_t death_steps;    /* > 0: an agent dies after this many consecutive steps with
+                               energy <= e_death_le (T_death), else at once  */
+    int32_t lethal_walls;   /* 1: a move off the grid kills the agent,
+                               0: it is blocked (R15)                                      */
 } sim_config;
 
 /* Canonical state, host buffers owned by the caller, layouts with the world index
@@ -120,6 +128,8 @@ typedef struct {
     float *c;              /* [n_worlds][S][Hd]                                            */
     float *weights;        /* [n_worlds][S][P]                                             */
     float *logits;         /* [n_worlds][S][5] of the last step                            */
+    int32_t *low;          /* [n_worlds][S] consecutive steps with energy <= e_death_le (the
+                              death timer of death_steps > 0)                               */
 } sim_state;
 
 /* Per world, per step counters (integer, exact). */
@@ -140,6 +150,7 @@ typedef struct {
                                   that died this step: life expectancy over a window is the
                                   windowed sum / windowed deaths (App. C; SPEC
                                   metrics.life_expectancy)                                */
+    int64_t deaths_wall;       /* agents killed by a move off the grid (lethal_walls)      */
 } sim_step_record;
 
 /* Cumulative counters since create (or the last set_state), summed over worlds. */

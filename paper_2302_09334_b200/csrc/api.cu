@@ -85,6 +85,10 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
     if (cfg->repr_steps < 1) return fail(SIM_E_INVALID, "invalid field: repr_steps");
     if (cfg->max_age < 0) return fail(SIM_E_INVALID, "invalid field: max_age");
     if (cfg->log_capacity < 0 || cfg->log_capacity == 1) return fail(SIM_E_INVALID, "invalid field: log_capacity");
+    if (!(cfg->climate_alpha >= 0.0) || !std::isfinite(cfg->climate_alpha))
+        return fail(SIM_E_INVALID, "invalid field: climate_alpha");
+    if (cfg->death_steps < 0) return fail(SIM_E_INVALID, "invalid field: death_steps");
+    if (cfg->lethal_walls != 0 && cfg->lethal_walls != 1) return fail(SIM_E_INVALID, "invalid field: lethal_walls (0 or 1)");
     if (d) {
         d->H = cfg->rows;
         d->W = cfg->cols;
@@ -113,12 +117,15 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
 }
 
 // Bernoulli thresholds T[y][c] = min(floor((lat(y) f_c + c_spont) 2^32), 2^32-1) with the
-// linear climate lat(y) = lat_top + (lat_bottom - lat_top) * (y / (H-1)) (R3, R8).
+// linear climate lat(y) = lat_top + (lat_bottom - lat_top) * (y / (H-1)) (R3, R8), or the
+// paper's exponential climate when climate_alpha > 0.
 void threshold_table(const sim_config *cfg, std::vector<uint32_t> &T) {
     T.assign((size_t)cfg->rows * 4, 0u);
     for (int y = 0; y < cfg->rows; ++y) {
         const double frac = (double)y / (double)(cfg->rows - 1);
-        const double lat = cfg->lat_top + (cfg->lat_bottom - cfg->lat_top) * frac;
+        double lat = cfg->lat_top + (cfg->lat_bottom - cfg->lat_top) * frac;
+        // the paper's climate c(x) = (alpha^x + 1)/(alpha + 1), x = 1 at the bottom row (R1)
+        if (cfg->climate_alpha > 0.0) lat = (std::pow(cfg->climate_alpha, frac) + 1.0) / (cfg->climate_alpha + 1.0);
         for (int c = 0; c < 4; ++c) {
             const double pr = lat * cfg->f_value[c] + cfg->spontaneous;
             const double s = std::floor(pr * 4294967296.0);
@@ -488,6 +495,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     p.repr_steps = cfg->repr_steps; p.max_age = cfg->max_age;
     p.e_init = cfg->e_init; p.e_decay = cfg->e_decay; p.e_gain = cfg->e_gain;
     p.e_repr_gt = cfg->e_repr_gt; p.e_death_le = cfg->e_death_le; p.e_max = cfg->e_max;
+    p.death_steps = cfg->death_steps; p.lethal_walls = cfg->lethal_walls;
     p.cls_k1 = cfg->f_class_min_k[1]; p.cls_k2 = cfg->f_class_min_k[2]; p.cls_k3 = cfg->f_class_min_k[3];
     for (int dy = -2; dy <= 2; ++dy) {  // the disc dy^2 + dx^2 <= r2 row by row (r2 <= 8: |dx| <= 2)
         int m = -1;
@@ -544,6 +552,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     H(&p.energy, nw * S);
     H(&p.age, nw * S);
     H(&p.repr, nw * S);
+    H(&p.low, nw * S);
     H(&p.mrec, nw * S);
     H(&p.alive_list, 2 * nw * S);
     H(&p.list_cell, 2 * nw * S);
@@ -851,6 +860,7 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     CK(h, get(out->energy, p.energy, nw * S * 4), "energy");
     CK(h, get(out->age, p.age, nw * S * 4), "age");
     CK(h, get(out->repr, p.repr, nw * S * 4), "repr");
+    CK(h, get(out->low, p.low, nw * S * 4), "low");
     CK(h, get(out->last_action, p.last_action, nw * S), "last_action");
     CK(h, get(out->ate, p.ate, nw * S), "ate");
     CK(h, get(out->h, p.h, nw * S * d.Hd * 4), "h");
@@ -976,6 +986,8 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, put(p.energy, in->energy, nw * S * 4), "energy");
     CK(h, put(p.age, in->age, nw * S * 4), "age");
     CK(h, put(p.repr, in->repr, nw * S * 4), "repr");
+    if (in->low) CK(h, put(p.low, in->low, nw * S * 4), "low");
+    else CK(h, cudaMemsetAsync(p.low, 0, nw * S * 4, s), "memset");  // (a state without the timer: 0)
     CK(h, put(p.last_action, in->last_action, nw * S), "last_action");
     CK(h, put(p.ate, in->ate, nw * S), "ate");
     CK(h, put(p.h, in->h, nw * S * d.Hd * 4), "h");

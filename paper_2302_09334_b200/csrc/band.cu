@@ -49,7 +49,7 @@ namespace eco {
 // ------------------------------------------------------------------ record layouts
 // migrant record (int32 words): [0] cell (the new one), [1] energy, [2] age, [3] repr,
 // [4] last_action, [5] ate, [6] mv_cell, [7] mv_inv, [8] source slot, [9] greediness T_r,
-// [10] C_r, [11] the window's flags (seen | ate << 1), [16..24) logits,
+// [10] C_r, [11] the window's flags (seen | ate << 1), [12] the death timer, [16..24) logits,
 // [24, 24+Hd) h, [24+Hd, 24+2Hd) c, [24+2Hd, +Pd) weights in the device layout.
 // newborn record: [0] cell, [1] parent slot, [4, 4+Pd) weights (device layout, mutated).
 // An outbox direction: [0] count, records from word 4.  dir 0 = towards band b-1 (up),
@@ -167,7 +167,20 @@ __global__ void k_band_move(DevParams p, BandParams bp) {
             const unsigned long long key =
                 ((unsigned long long)(uint32_t)mr.w << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
             stay = true;
-            if (tg >= 0 && p.claim[tg] == key) {
+            if (tg == WALL_TARGET) {  // walked into a lethal wall: dies before eating
+                stay = false;
+                uint32_t ob;
+                p.alive[slot] = 0;
+                p.ate[slot] = 0;
+                greed_update(p, slot, t, false);
+                atomicAnd(word_ptr(p.occ, p, cellv, ob), ~ob);
+                atomicAnd(p.alive_bits + (slot >> 5), ~(1u << (slot & 31)));
+                sim_step_record *rec = record_of(p, t, 0);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_wall), 1ull);
+#if ECO_METRICS & 1
+                atomicAdd(reinterpret_cast<unsigned long long *>(&rec->death_age_sum), (unsigned long long)(p.age[slot] + 1));
+#endif
+            } else if (tg >= 0 && p.claim[tg] == key) {
                 uint32_t ob;
                 atomicAnd(word_ptr(p.occ, p, cellv, ob), ~ob);
                 const int ty = row_of(p, tg);
@@ -193,6 +206,7 @@ __global__ void k_band_move(DevParams p, BandParams bp) {
                     rec[9] = p.gr_T[slot];
                     rec[10] = p.gr_C[slot];
                     rec[11] = p.gr_seen[slot] | (p.gr_ate[slot] << 1);
+                    rec[12] = p.low[slot];
                     p.alive[slot] = 0;
                     atomicAnd(p.alive_bits + (slot >> 5), ~(1u << (slot & 31)));
                 }
@@ -320,6 +334,7 @@ __global__ void k_band_arrive_copy(DevParams p, BandParams bp) {
         p.gr_C[slot] = rec[10];
         p.gr_seen[slot] = (uint8_t)(rec[11] & 1);
         p.gr_ate[slot] = (uint8_t)(rec[11] >> 1);
+        p.low[slot] = rec[12];
         uint32_t ob;
         atomicOr(word_ptr(p.occ, p, cell, ob), ob);
     }
@@ -372,7 +387,7 @@ __global__ void k_band_live(DevParams p, BandParams bp) {
             p.age[slot] = ag;
             const int rp = en > p.e_repr_gt ? p.repr[slot] + 1 : 0;
             p.repr[slot] = rp;
-            if (en <= p.e_death_le) died_e = true;
+            if (starves(p, slot, en)) died_e = true;
             else if (ag > p.max_age) died_a = true;
             if (died_e || died_a) {
                 p.alive[slot] = 0;
@@ -553,6 +568,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         p.gr_ate[child] = 0;
         p.gr_T[child] = 0;
         p.gr_C[child] = 0;
+        p.low[child] = 0;
         for (int j = 0; j < p.Hd; ++j) {
             p.h[(size_t)child * p.Hd + j] = 0.f;
             p.c[(size_t)child * p.Hd + j] = 0.f;
@@ -637,7 +653,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         rec->deferred_capacity = c_own - n_place;
         rec->population = n_surv + n_place;
         rec->resources = res;
-        life_window_add(p, 0, t, rec->deaths_energy + rec->deaths_age, rec->death_age_sum);
+        life_window_add(p, 0, t, rec->deaths_energy + rec->deaths_age + rec->deaths_wall, rec->death_age_sum);
         *count_of(p, t + 1, 0) = n_surv + n_place;
         p.n_births[0] = n_place;
         *p.p_children = n_place;  // split policy: the children (list end) start from their bias
@@ -646,7 +662,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_rank(DevParams p, BandParams b
         atomicAdd(tot + 1, (unsigned long long)rec->agents_at_start);
         atomicAdd(tot + 2, (unsigned long long)((size_t)(bp.y1 - bp.y0) * p.W));
         atomicAdd(tot + 3, (unsigned long long)n_place);
-        atomicAdd(tot + 4, (unsigned long long)(rec->deaths_energy + rec->deaths_age));
+        atomicAdd(tot + 4, (unsigned long long)(rec->deaths_energy + rec->deaths_age + rec->deaths_wall));
         atomicAdd(tot + 5, (unsigned long long)eaten);
         atomicAdd(tot + 6, (unsigned long long)grown);
         p.t[0] = t + 1;
@@ -729,6 +745,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band_init_agents(DevParams p, BandP
         p.ate[i] = 0;
         p.gr_seen[i] = p.gr_ate[i] = 0;
         p.gr_T[i] = p.gr_C[i] = 0;
+        p.low[i] = 0;
     }
     __syncthreads();
     uint32_t run = 0u;

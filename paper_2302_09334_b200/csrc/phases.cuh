@@ -303,11 +303,24 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             n_list = (t & 1) ? n1 : n0;
         }
         const bool active = it.in_range && it.i < n_list;
-        bool ate = false, died_e = false, died_a = false, survive = false, cand = false;
+        bool ate = false, died_e = false, died_a = false, died_w = false, survive = false, cand = false;
         int cand_cell = 0;
         int slot = 0;
         int dage = 0;  // metrics: age at death
-        if (active) {
+        if (active && mr.z == WALL_TARGET) {  // walked into a lethal wall: dies before eating
+            slot = mr.x;
+            const size_t gs = (size_t)w * p.S + slot;
+            uint32_t bit;
+            p.alive[gs] = 0;
+            p.ate[gs] = 0;
+            greed_update(p, gs, t, false);
+            atomicAnd(word_ptr(p.occ + (size_t)w * plane_words(p), p, mr.y, bit), ~bit);
+            atomicAnd(p.alive_bits + (size_t)w * p.SW + (slot >> 5), ~(1u << (slot & 31)));
+            died_w = true;
+#if ECO_METRICS & 1
+            dage = p.age[gs] + 1;
+#endif
+        } else if (active) {
             slot = mr.x;
             ECO_CHECK(slot >= 0 && slot < p.S && (mr.z < 0 || (int64_t)mr.z < (int64_t)p.H * p.W));
             const size_t gs = (size_t)w * p.S + slot;
@@ -322,7 +335,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             int en0 = p.energy[gs], ag0 = p.age[gs], rp0 = p.repr[gs];
             uint32_t bit, bit_t = 0u;
             uint32_t *rw = word_ptr(Rn, p, cellv, bit), *rw_t = nullptr;
-            const unsigned long long ck = tg >= 0 ? p.claim[(size_t)w * HW + tg] : 0ull;
+            const unsigned long long ck = tg >= 0 ? p.claim[(size_t)w * HW + tg] : 0ull;  // (tg -2: never here)
             uint32_t r_c = ld_plain(rw), r_t = 0u;
             if (tg >= 0) {
                 rw_t = word_ptr(Rn, p, tg, bit_t);
@@ -351,7 +364,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             p.energy[gs] = en;
             p.age[gs] = ag;
             p.repr[gs] = en > p.e_repr_gt ? rp0 + 1 : 0;
-            if (en <= p.e_death_le) died_e = true;
+            if (starves(p, gs, en)) died_e = true;
             else if (ag > p.max_age) died_a = true;
             if (died_e || died_a) {
                 p.alive[gs] = 0;
@@ -371,7 +384,8 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             const int64_t t0 = __shfl_sync(0xffffffffu, t, 0);  // lane 0 is in range here
             sim_step_record *rec = record_of(p, t0, w0);
             const unsigned me = __ballot_sync(0xffffffffu, ate), md = __ballot_sync(0xffffffffu, died_e),
-                           ma = __ballot_sync(0xffffffffu, died_a), m = __ballot_sync(0xffffffffu, survive);
+                           ma = __ballot_sync(0xffffffffu, died_a), m = __ballot_sync(0xffffffffu, survive),
+                           mw = __ballot_sync(0xffffffffu, died_w);
             // eligible parents (R19) for the single-world claims in k_post; both list appends'
             // atomics are in flight together
             const unsigned mc = p.n_worlds == 1 ? __ballot_sync(0xffffffffu, cand) : 0u;
@@ -382,13 +396,14 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
                 if (me) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), (unsigned long long)__popc(me));
                 if (md) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), (unsigned long long)__popc(md));
                 if (ma) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), (unsigned long long)__popc(ma));
+                if (mw) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_wall), (unsigned long long)__popc(mw));
             }
             c0 = __shfl_sync(0xffffffffu, c0, 0);
             ECO_CHECK(!cand || c0 + __popc(mc & ((1u << lane) - 1u)) < p.S);
             if (cand) p.cand[c0 + __popc(mc & ((1u << lane) - 1u))] = make_int2(slot, cand_cell);
             // metrics: the deaths' ages, and at a window end the movement bins (warp sums)
 #if ECO_METRICS & 1
-            if (md | ma) {
+            if (md | ma | mw) {
                 const int dsum = __reduce_add_sync(0xffffffffu, dage);
                 if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->death_age_sum), (unsigned long long)dsum);
             }
@@ -415,6 +430,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             if (ate) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->eaten), 1ull);
             if (died_e) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_energy), 1ull);
             if (died_a) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_age), 1ull);
+            if (died_w) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->deaths_wall), 1ull);
             if (survive) {
                 const int q = atomicAdd(count_of(p, t + 1, w), 1);
                 ECO_CHECK(q < p.S);
@@ -449,7 +465,7 @@ __device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gti
             const int slot = mr.x;
             const size_t gs = (size_t)w * p.S + slot;
             const int tg = mr.z;
-            if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;
+            if (tg >= 0) p.claim[(size_t)w * HW + tg] = 0ull;  // (-1 no move, -2 lethal wall)
             if (p.alive[gs]) {
                 const int cellv = p.cell[gs];
                 uint8_t dir = NO_DIR;
@@ -660,6 +676,7 @@ __device__ __forceinline__ void place_child(const DevParams &p, int w, int64_t t
     p.gr_ate[cs] = 0;
     p.gr_T[cs] = 0;
     p.gr_C[cs] = 0;
+    p.low[cs] = 0;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);  // Hd in {4, 8, 16, 32}: rows are float4-aligned
     for (int k = 0; k < p.Hd; k += 4) {
         *reinterpret_cast<float4 *>(p.h + cs * p.Hd + k) = z4;
@@ -750,8 +767,8 @@ __device__ void rank_lists(const DevParams &p, int w, int64_t t, int n_place, ui
 __device__ __forceinline__ void rank_finalize(const DevParams &p, int w, int64_t t, int n_start, int n_surv,
                                               int n_win, int n_place) {
     volatile sim_step_record *rec = record_of(p, t, w);
-    const int64_t de = rec->deaths_energy, da = rec->deaths_age, grown = rec->grown, eaten = rec->eaten,
-                  dc = rec->deferred_claim;
+    const int64_t de = rec->deaths_energy, da = rec->deaths_age + rec->deaths_wall, grown = rec->grown,
+                  eaten = rec->eaten, dc = rec->deferred_claim;
     const int64_t res = p.res_count[w] + grown - eaten;
     p.res_count[w] = res;
     rec->t = t;
@@ -761,7 +778,7 @@ __device__ __forceinline__ void rank_finalize(const DevParams &p, int w, int64_t
     rec->deferred_capacity = n_win - n_place;
     rec->population = n_surv + n_place;
     rec->resources = res;
-    life_window_add(p, w, t, de + da, rec->death_age_sum);
+    life_window_add(p, w, t, de + da, rec->death_age_sum);  // (da includes the wall deaths)
     *count_of(p, t + 1, w) = n_surv + n_place;
     p.n_births[w] = n_place;
     unsigned long long *tot = p.totals;

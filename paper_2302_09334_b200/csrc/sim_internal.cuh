@@ -59,6 +59,8 @@ struct DevParams {
     double invW;   // 1 / W (cell -> row without an integer division)
     int repr_steps, max_age;
     int e_init, e_decay, e_gain, e_repr_gt, e_death_le, e_max;
+    int death_steps;   // > 0: the death timer T_death, else immediate death
+    int lethal_walls;  // 1: a move off the grid kills; the policy marks target -2
     int cls_k1, cls_k2, cls_k3;  // class thresholds f_class_min_k[1..3]
     int row_dx[5];  // regrowth disc: offsets (dy, dx) with |dx| <= row_dx[dy + 2], centre excluded
     int disc12;     // 1: the disc is BASELINE's radius-2 disc (row_dx = 0,1,2,1,0: 12 cells)
@@ -78,6 +80,7 @@ struct DevParams {
     uint8_t *alive, *last_action, *ate;
     uint32_t *alive_bits;        // [n_worlds][SW]
     int32_t *cell, *energy, *age, *repr;
+    int32_t *low;                // [n_worlds][S] consecutive steps with energy <= e_death_le
     float *h, *c, *logits, *weights;
     int4 *mrec;                  // [n_worlds][S] per list position: (slot, cell, target or -1, MOVE w0)
     int32_t *alive_list;         // [2][n_worlds][S]
@@ -295,6 +298,17 @@ __device__ __forceinline__ void greed_update(const DevParams &p, size_t gs, int6
         p.gr_ate[gs] = 1;
     }
 }
+// energy <= e_death_le: immediately (BASELINE, R18) or after death_steps consecutive steps
+// (the paper's timer); `low` is the agent's counter (updated here)
+__device__ __forceinline__ bool starves(const DevParams &p, size_t gs, int en) {
+    const bool below = en <= p.e_death_le;
+    if (p.death_steps <= 0) return below;
+    const int32_t l = below ? p.low[gs] + 1 : 0;
+    p.low[gs] = l;
+    return l >= p.death_steps;
+}
+constexpr int WALL_TARGET = -2;  // move record target of an agent walking into a lethal wall
+
 // the step's deaths into its 500-step window (one thread per world, after the step's counts)
 __device__ __forceinline__ void life_window_add(const DevParams &p, int w, int64_t t, int64_t deaths, int64_t age_sum) {
     if (!deaths) return;

@@ -130,6 +130,7 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
     if (act != 0) {
         const int y = row_of(p, cellv), x = cellv - y * p.W;
         const int ty = y + kDY[act], tx = x + kDX[act];
+        if (p.lethal_walls && !(ty >= 0 && ty < p.H && tx >= 0 && tx < p.W)) tg = WALL_TARGET;
         if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
             const int tc = ty * p.W + tx;
             // O_t of the target: the agent channel of the window already holds it (r >= 1)

@@ -68,18 +68,20 @@ class SimConfig(ctypes.Structure):
         # banded mode (include/sim.h: one world in latitude bands)
         ("n_bands", ctypes.c_int32), ("band_first", ctypes.c_int32), ("band_local", ctypes.c_int32),
         ("band_rows", ctypes.POINTER(ctypes.c_int32)), ("band_slots", ctypes.c_int32),
+        # the paper's own world (include/sim.h)
+        ("climate_alpha", ctypes.c_double), ("death_steps", ctypes.c_int32), ("lethal_walls", ctypes.c_int32),
     ]
 
 
 class SimState(ctypes.Structure):
     _fields_ = [("t", ctypes.c_int64)] + [(f, ctypes.c_void_p) for f in (
         "resources", "alive", "cell", "energy", "age", "repr", "last_action", "ate", "h", "c", "weights",
-        "logits")]
+        "logits", "low")]
 
 
 RECORD_FIELDS = ("t", "agents_at_start", "grown", "eaten", "births", "deaths_energy", "deaths_age",
                  "deferred_no_cell", "deferred_claim", "deferred_capacity", "population", "resources",
-                 "near_ties", "obs_nnz", "death_age_sum")
+                 "near_ties", "obs_nnz", "death_age_sum", "deaths_wall")
 MOVE_WINDOW, MOVE_BINS = 50, 17  # include/sim.h: SIM_MOVE_WINDOW, SIM_MOVE_BINS
 RECORD_DTYPE = np.dtype([(f, np.int64) for f in RECORD_FIELDS])
 TOTALS_FIELDS = ("steps", "agent_steps", "cell_updates", "births", "deaths", "eaten", "grown")
@@ -189,6 +191,9 @@ def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0, bands=N
     c.e_repr_gt, c.e_death_le, c.e_max = wc.e_repr_gt, wc.e_death_le, wc.e_max
     c.repr_steps, c.max_age = wc.repr_steps, wc.max_age
     c.cuda_stream = _stream_handle(stream)
+    c.climate_alpha = float(getattr(wc, "climate_alpha", 0.0))
+    c.death_steps = int(getattr(wc, "death_steps", 0))
+    c.lethal_walls = int(getattr(wc, "lethal_walls", 0))
     keep = [seeds]
     if bands:
         G = int(bands["n_bands"])
@@ -216,7 +221,7 @@ def state_sizes(wc) -> dict:
 
 
 STATE_FIELDS = ("resources", "alive", "cell", "energy", "age", "repr", "last_action", "ate", "h", "c",
-                "weights", "logits")
+                "weights", "logits", "low")
 
 
 def _ptr(a: np.ndarray):
@@ -343,6 +348,7 @@ class World:
             "repr": ((nw, S), np.int32), "last_action": ((nw, S), np.uint8), "ate": ((nw, S), np.uint8),
             "h": ((nw, S, Hd), np.float32), "c": ((nw, S, Hd), np.float32),
             "weights": ((nw, S, P), np.float32), "logits": ((nw, S, 5), np.float32),
+            "low": ((nw, S), np.int32),
         }
 
     def empty_state(self, fields=STATE_FIELDS) -> dict:

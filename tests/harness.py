@@ -10,9 +10,9 @@ import oracle
 
 REL, ABS = 1e-5, 2e-6
 MAX_ABS_SEEN = {"h": 0.0, "c": 0.0, "logits": 0.0}  # largest |g - o| compared (reported by tests)
-INT_FIELDS = ("cell", "energy", "age", "repr", "ate")
+INT_FIELDS = ("cell", "energy", "age", "repr", "ate", "low")
 REC_EXACT = ("grown", "eaten", "births", "deaths_energy", "deaths_age", "deferred_no_cell", "deferred_claim",
-             "deferred_capacity", "population", "resources")
+             "deferred_capacity", "population", "resources", "deaths_wall")
 
 
 def gpu_world_state(gs: dict, w: int = 0) -> dict:

@@ -32,9 +32,9 @@ def gpu_state(world, w=0, weights=True):
 
 
 # ----------------------------------------------------------------------------- init
-@pytest.mark.parametrize("cfg", ["tiny", "paper", "odd"])
+@pytest.mark.parametrize("cfg", ["tiny", "paper", "odd", "paper_world"])
 def test_init_matches_oracle(cfg):
-    wc = {"tiny": workloads.tiny(), "paper": workloads.paper_scale(),
+    wc = {"tiny": workloads.tiny(), "paper": workloads.paper_scale(), "paper_world": workloads.paper_world(),
           "odd": workloads.tiny().replace(rows=37, cols=68, slots=100, n_initial=77, seeds=(12345678901,),
                                           hidden=16, obs_radius=3)}[cfg]
     with sim.World(wc) as world:
@@ -682,3 +682,41 @@ def test_life_windows_equal_the_records():
         assert a[k, 0] == int(rk["death_age_sum"].sum())
     assert d[1, 0] > 0
     world.destroy()
+
+
+# ---------------------------------------------- the paper's own world (NEXT-1, App. B.4)
+def test_paper_world_lockstep_400_steps():
+    """workloads.paper_world (exponential climate, 4-neighbour indicator regrowth, clipped
+    energy, death timer, lethal walls, Hd = 4) in M2 + M3 lock-step with the oracle for 400
+    steps: births from ~140 on, timer starvation from ~319, wall deaths."""
+    wc = workloads.paper_world()
+    world = sim.World(wc)
+    orc = oracle.OracleWorld(wc)
+    flips, n, nulp = lockstep(world, orc, 400, check_weights_every=200)
+    log = world.step_log(0, 400)[:, 0]
+    print(f"paper world: {n} agent-steps, births {int(log['births'].sum())}, timer deaths "
+          f"{int(log['deaths_energy'].sum())}, wall deaths {int(log['deaths_wall'].sum())}")
+    assert int(log["births"].sum()) > 0 and int(log["deaths_wall"].sum()) > 0
+    world.destroy()
+
+
+def test_paper_world_banded_equals_unbanded():
+    wc = workloads.paper_world()
+    ref = sim.World(wc)
+    ban = sim.World(wc, bands=dict(n_bands=4))
+    ref.step(400)
+    ban.step(400)
+    a, b = ref.get_state(), ban.get_state()
+    for st in (a, b):
+        live = np.flatnonzero(st["alive"][0])
+        st["_by_cell"] = {int(st["cell"][0][i]): i for i in live}
+    assert np.array_equal(a["resources"], b["resources"]) and a["_by_cell"].keys() == b["_by_cell"].keys()
+    for c, i in a["_by_cell"].items():
+        j = b["_by_cell"][c]
+        for f in ("energy", "age", "repr", "low", "h", "c", "weights"):
+            assert np.array_equal(a[f][0][i], b[f][0][j]), (c, f)
+    la, lb = ref.step_log(0, 400)[:, 0], ban.step_log(0, 400)[:, 0]
+    for f in sim.RECORD_FIELDS:
+        assert np.array_equal(la[f], lb[f]), f
+    ref.destroy()
+    ban.destroy()
