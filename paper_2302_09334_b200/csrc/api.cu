@@ -737,6 +737,8 @@ sim_status sim_shard(sim_handle h, int32_t n_ranks, int32_t rank) {
         return fail(SIM_E_INVALID, "invalid argument: n_ranks (1..255) / rank");
     if (n_ranks > 1 && (h->d.n_worlds != 1 || h->d.Hd != 32 || !eco::policy_supports_shard()))
         return fail(SIM_E_INVALID, "sharding needs one world, hidden = 32 and the default policy kernel");
+    if (n_ranks > 1 && eco::paper_rules(h->p))
+        return fail(SIM_E_INVALID, "sharding does not support the paper world's death timer / lethal walls");
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     if ((st = sync(h)) != SIM_OK) return st;
     h->p.n_ranks = n_ranks;

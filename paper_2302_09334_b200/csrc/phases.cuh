@@ -284,6 +284,10 @@ __device__ __forceinline__ void mv_pass_part(const DevParams &p, int64_t T, int 
 // or age > max_age (cause age) (R18).  O is updated in place with bit atomics; distinct
 // agents touch distinct bits.  Survivors are appended to the step-(t+1) list (order is
 // irrelevant to every result).  Must be called by all 32 lanes of a warp.
+// PAPER: the paper world's death timer and lethal walls (death_steps > 0 or lethal_walls),
+// compiled into separate kernels so BASELINE's move phase keeps its code (measured: the
+// runtime checks cost 6 us per capped paper-scale step).
+template <bool PAPER = false>
 __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
@@ -307,7 +311,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
         int cand_cell = 0;
         int slot = 0;
         int dage = 0;  // metrics: age at death
-        if (active && mr.z == WALL_TARGET) {  // walked into a lethal wall: dies before eating
+        if (PAPER && active && mr.z == WALL_TARGET) {  // walked into a lethal wall: dies before eating
             slot = mr.x;
             const size_t gs = (size_t)w * p.S + slot;
             uint32_t bit;
@@ -364,7 +368,7 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
             p.energy[gs] = en;
             p.age[gs] = ag;
             p.repr[gs] = en > p.e_repr_gt ? rp0 + 1 : 0;
-            if (starves(p, gs, en)) died_e = true;
+            if (PAPER ? starves(p, gs, en) : en <= p.e_death_le) died_e = true;
             else if (ag > p.max_age) died_a = true;
             if (died_e || died_a) {
                 p.alive[gs] = 0;

@@ -286,18 +286,30 @@ __device__ __forceinline__ sim_step_record *record_of(const DevParams &p, int64_
 constexpr int GR_WINDOW = 20;   // sim.h SIM_GREED_WINDOW
 constexpr int LE_WINDOW = 500;  // sim.h SIM_LIFE_WINDOW
 __device__ __forceinline__ bool gr_window_end(int64_t t) { return (uint32_t)t % GR_WINDOW == GR_WINDOW - 1; }
-// the greediness bookkeeping of one agent processed in step t (ate: this step's consumption)
+// the greediness flag of one agent that ate in step t (the window's counts are closed after
+// the window's last step by greed_pass_part, off the move phase's critical path)
+#ifndef ECO_GREED
+#define ECO_GREED 1  // diagnostic switch (0: no greediness bookkeeping)
+#endif
 __device__ __forceinline__ void greed_update(const DevParams &p, size_t gs, int64_t t, bool ate) {
-    if (gr_window_end(t)) {
-        const int seen = p.gr_seen[gs], a = ate ? 1 : p.gr_ate[gs];
-        p.gr_T[gs] += seen;
-        p.gr_C[gs] += a;
+    (void)t;
+#if ECO_GREED
+    if (ate) p.gr_ate[gs] = 1;
+#endif
+}
+// Close greediness window T / 20 for world w's slots [lo, hi) (after the step's placement):
+// every live agent adds its flags (a newborn of step T has none) and starts the next window.
+__device__ __forceinline__ void greed_pass_part(const DevParams &p, int w, int lo, int hi, int tid, int nthr) {
+    for (int i = lo + tid; i < hi; i += nthr) {
+        const size_t gs = (size_t)w * p.S + i;
+        if (!p.alive[gs]) continue;
+        p.gr_T[gs] += p.gr_seen[gs];
+        p.gr_C[gs] += p.gr_ate[gs];
         p.gr_seen[gs] = 0;
         p.gr_ate[gs] = 0;
-    } else if (ate) {
-        p.gr_ate[gs] = 1;
     }
 }
+
 // energy <= e_death_le: immediately (BASELINE, R18) or after death_steps consecutive steps
 // (the paper's timer); `low` is the agent's counter (updated here)
 __device__ __forceinline__ bool starves(const DevParams &p, size_t gs, int en) {
@@ -308,6 +320,7 @@ __device__ __forceinline__ bool starves(const DevParams &p, size_t gs, int en) {
     return l >= p.death_steps;
 }
 constexpr int WALL_TARGET = -2;  // move record target of an agent walking into a lethal wall
+__host__ __device__ __forceinline__ bool paper_rules(const DevParams &p) { return p.death_steps > 0 || p.lethal_walls; }
 
 // the step's deaths into its 500-step window (one thread per world, after the step's counts)
 __device__ __forceinline__ void life_window_add(const DevParams &p, int w, int64_t t, int64_t deaths, int64_t age_sum) {

@@ -115,10 +115,12 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
         p.logits[gs * LOGIT_STRIDE + a] = lg[a];
     }
     ctr.add(p, w, nnz, (double)bestv - second < 1e-4);
+#if ECO_GREED
     {  // greediness: a resource in the field of view (the window's resource channel, R10/R11)
         const int wd2 = (2 * p.r + 1) * (2 * p.r + 1);  // <= 49
         if (m_lo & ((1ull << wd2) - 1ull)) p.gr_seen[gs] = 1;
     }
+#endif
     int act = best;
     if (forced_on) {
         const uint8_t f = p.forced[gs];
@@ -878,14 +880,18 @@ __global__ void __launch_bounds__(256) k_regrow(DevParams p, int ahead) {
     regrow_phase(p, p.t[0] + ahead, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
+template <bool PAPER>
 __global__ void __launch_bounds__(256) k_move(DevParams p) {
-    move_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
+    move_phase<PAPER>(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
 }
 
 __global__ void __launch_bounds__(256) k_mv_pass(DevParams p) {  // one block per world, after the rank
     __shared__ int s_mv[SIM_MOVE_BINS];
     const int64_t T = p.t[blockIdx.x] - 1;  // the rank advanced t
+#if ECO_METRICS & 2
     if (mv_window_end(T)) mv_pass_part(p, T, blockIdx.x, 0, p.S, threadIdx.x, blockDim.x, s_mv);
+#endif
+    if (gr_window_end(T)) greed_pass_part(p, blockIdx.x, 0, p.S, threadIdx.x, blockDim.x);
 }
 
 __global__ void __launch_bounds__(256) k_birth_claim(DevParams p) {
@@ -971,7 +977,7 @@ constexpr int ECO_BLOCK_CLOCK_BASE = 16;
 #define POST_SYNC(k) grid_sync(bar, target, nthr)
 #endif
 
-template <bool SHARD, bool BIG = false>
+template <bool SHARD, bool BIG = false, bool PAPER = false>
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned long long *bar) {
     DevParams p = p_;
     if (!SHARD) p.n_ranks = 1;
@@ -1072,7 +1078,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         }
         grid_sync(bar, target, nthr);
     }
-    move_phase(p, gtid, gthreads);
+    move_phase<PAPER>(p, gtid, gthreads);
     POST_SYNC(0);
     lap(0);
     // sharded + split: this rank's survivors lead its next list; its children (appended by
@@ -1121,6 +1127,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             // (every live agent of step T+1 is final here; off the critical path)
             if (mv_window_end(T)) mv_pass_part(p, T, 0, 0, p.S, threadIdx.x, blockDim.x, s_mv);
 #endif
+            if (gr_window_end(T)) greed_pass_part(p, 0, 0, p.S, threadIdx.x, blockDim.x);  // greediness windows
             if (gridDim.x == 1) mutate_world(p, 0, T, k.n_place, threadIdx.x, blockDim.x);  // no other block
         } else {
             const unsigned nb = gridDim.x - 1, b = blockIdx.x - 1;
@@ -1171,6 +1178,9 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
                 mv_pass_part(p, T, w, 0, p.S, threadIdx.x, blockDim.x, s_mv);
 #endif
+        if (gr_window_end(T))  // greediness windows
+            for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
+                greed_pass_part(p, w, 0, p.S, threadIdx.x, blockDim.x);
         if (p.n_worlds >= (int)gridDim.x) {  // no block was free: the regrowth goes beside the mutation
             const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
             if (gtid >= half) regrow_phase(p, T + 1, gtid - half, gthreads - half);
@@ -1498,7 +1508,8 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
 
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
-    k_move<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
+    if (paper_rules(p)) k_move<true><<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
+    else k_move<false><<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -1510,16 +1521,12 @@ cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStre
 
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
-#if ECO_METRICS & 2
-    k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);  // the movement histogram at a window end (after placement)
-#endif
+    k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);  // movement / greediness windows ending here (after placement)
     return cudaGetLastError();
 }
 
 cudaError_t launch_mv_pass(const DevParams &p, cudaStream_t s) {
-#if ECO_METRICS & 2
-    k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);
-#endif
+    k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);  // movement / greediness windows ending here
     return cudaGetLastError();
 }
 
@@ -1585,6 +1592,10 @@ cudaError_t post_prepare() {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_post<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_post<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_post<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_post<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
 }
 
@@ -1606,7 +1617,10 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = 2;
 #endif
+    if (p.n_ranks > 1 && paper_rules(p)) return cudaErrorInvalidValue;  // (sim_shard refuses the paper rules)
     if (p.n_ranks > 1) return cudaLaunchKernelEx(&cfg, post_big(p) ? k_post<true, true> : k_post<true>, p, bar);
+    if (paper_rules(p))
+        return cudaLaunchKernelEx(&cfg, post_big(p) ? k_post<false, true, true> : k_post<false, false, true>, p, bar);
     if (post_big(p)) return cudaLaunchKernelEx(&cfg, k_post<false, true>, p, bar);
     return cudaLaunchKernelEx(&cfg, k_post<false>, p, bar);
 }
