@@ -23,7 +23,7 @@ _lock = threading.Lock()
 _lib = None
 
 OK, E_INVALID, E_NONFINITE = 0, -1, -5
-P_INIT_RES, P_INIT_PLACE, P_INIT_W, P_REGROW, P_MOVE, P_BIRTH, P_MUTATE = 1, 2, 3, 4, 5, 6, 7
+P_INIT_RES, P_INIT_PLACE, P_INIT_W, P_REGROW, P_MOVE, P_BIRTH, P_MUTATE, P_ACTION = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 def build(force: bool = False) -> str:
@@ -57,6 +57,7 @@ class Config(ctypes.Structure):
         ("e_repr_gt", ctypes.c_int32), ("e_death_le", ctypes.c_int32), ("e_max", ctypes.c_int32),
         ("repr_steps", ctypes.c_int32), ("max_age", ctypes.c_int32),
         ("climate_alpha", ctypes.c_double), ("death_steps", ctypes.c_int32), ("lethal_walls", ctypes.c_int32),
+        ("network", ctypes.c_int32),
     ]
 
 
@@ -116,6 +117,18 @@ def lib():
             L.orc_policy.argtypes = [cp, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)]
+            L.orc_observe_paper.argtypes = [cp, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_void_p]
+            L.orc_conv3x3_s2_same.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]
+            L.orc_avgpool2_s1.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_void_p]
+            L.orc_policy_cnn.argtypes = [cp, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p]
+            L.orc_sample_action.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
+            L.orc_sample_action.restype = ctypes.c_int32
             L.orc_init.argtypes = [cp, ctypes.POINTER(State)]
             L.orc_step.argtypes = [cp, ctypes.POINTER(State), ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Record)]
             _lib = L
@@ -147,6 +160,7 @@ def make_config(wc, world: int = 0) -> Config:
     c.climate_alpha = float(getattr(wc, "climate_alpha", 0.0))
     c.death_steps = int(getattr(wc, "death_steps", 0))
     c.lethal_walls = int(getattr(wc, "lethal_walls", 0))
+    c.network = int(getattr(wc, "network", 0))
     return c
 
 
@@ -236,6 +250,59 @@ def policy(wc, w: np.ndarray, x: np.ndarray, h: np.ndarray, c: np.ndarray):
     rc = lib().orc_policy(ctypes.byref(make_config(wc)), _ptr(w), _ptr(x), _ptr(h), _ptr(c), _ptr(ho),
                           _ptr(co), _ptr(lg), ctypes.byref(a), ctypes.byref(m))
     return ho, co, lg[:wc.n_actions].copy(), int(a.value), float(m.value), int(rc)
+
+
+# ------------------------------------------- network 1: the paper's CNN-LSTM (NEXT-2)
+def observe_paper(wc, R: np.ndarray, O: np.ndarray, y: int, x: int) -> np.ndarray:
+    """The 15x15x3 window (HWC: resources, agents, walls) around (y, x)."""
+    R = np.ascontiguousarray(R, np.uint8)
+    O = np.ascontiguousarray(O, np.uint8)
+    out = np.zeros((15, 15, 3), np.float64)
+    lib().orc_observe_paper(ctypes.byref(make_config(wc)), _ptr(R), _ptr(O), y, x, _ptr(out))
+    return out
+
+
+def conv3x3_s2_same(x: np.ndarray, w: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """x [H][W][cin] fp64, w [cout][3][3][cin] fp32, b [cout] fp32 -> [ceil(H/2)][ceil(W/2)][cout]."""
+    x = np.ascontiguousarray(x, np.float64)
+    w = np.ascontiguousarray(w, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    H, W, cin = x.shape
+    cout = w.shape[0]
+    out = np.zeros(((H + 1) // 2, (W + 1) // 2, cout), np.float64)
+    lib().orc_conv3x3_s2_same(_ptr(x), H, W, cin, _ptr(w), _ptr(b), cout, _ptr(out))
+    return out
+
+
+def avgpool2_s1(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float64)
+    H, W, C = x.shape
+    out = np.zeros((H - 1, W - 1, C), np.float64)
+    lib().orc_avgpool2_s1(_ptr(x), H, W, C, _ptr(out))
+    return out
+
+
+def policy_cnn(wc, w: np.ndarray, obs: np.ndarray, last_action: int, ate: int, h: np.ndarray, c: np.ndarray):
+    """One agent's CNN-LSTM forward; returns (h', c', logits, embedding[78], status)."""
+    w = np.ascontiguousarray(w, np.float32)
+    obs = np.ascontiguousarray(obs, np.float64)
+    h = np.ascontiguousarray(h, np.float32)
+    c = np.ascontiguousarray(c, np.float32)
+    ho, co = np.zeros(4, np.float32), np.zeros(4, np.float32)
+    lg = np.zeros(5, np.float32)
+    emb = np.zeros(78, np.float64)
+    rc = lib().orc_policy_cnn(ctypes.byref(make_config(wc)), _ptr(w), _ptr(obs), last_action, ate, _ptr(h), _ptr(c),
+                              _ptr(ho), _ptr(co), _ptr(lg), _ptr(emb))
+    return ho, co, lg, emb, int(rc)
+
+
+def sample_action(seed: int, step: int, cell: int, logits: np.ndarray):
+    """softmax(50 logits) sampled with the (ACTION, step, cell) draw: (action, probs, margin)."""
+    lg = np.ascontiguousarray(logits, np.float32)
+    probs = np.zeros(5, np.float64)
+    m = ctypes.c_double()
+    a = lib().orc_sample_action(int(seed) & 0xFFFFFFFFFFFFFFFF, step, cell, _ptr(lg), _ptr(probs), ctypes.byref(m))
+    return int(a), probs, float(m.value)
 
 
 # ------------------------------------------------------------------ world

@@ -79,12 +79,24 @@ void orc_gauss(uint64_t seed, uint32_t purpose, uint32_t step, uint32_t entity, 
 
 /* ------------------------------------------------------------- sizes/validation */
 int32_t orc_input_count(const orc_config *cfg) {
+    if (cfg->network == 1) return ORC_CNN_WO * ORC_CNN_WO * ORC_CNN_CH; /* 15x15x3 */
     int32_t w = 2 * cfg->obs_radius + 1;
     return 2 * w * w;
 }
 
-/* P = 4Hd*I + 4Hd*Hd + 4Hd + 5Hd + 5 (canonical order) */
+/* network 0: P = 4Hd*I + 4Hd*Hd + 4Hd + 5Hd + 5 (canonical order).
+ * network 1, counted layer by layer from the architecture:
+ *   conv1 3x3x3 -> 4 (+4 biases), conv2 3x3x4 -> 8 (+8), LSTM 78 -> 4 (4 gates over
+ *   78 + 4 inputs, +16 biases), dense 82 -> 8 (+8), dense 8 -> 5 (+5)          */
 int32_t orc_param_count(const orc_config *cfg) {
+    if (cfg->network == 1) {
+        const int32_t c1 = 3 * 3 * ORC_CNN_CH * 4 + 4, c2 = 3 * 3 * 4 * 8 + 8;
+        const int32_t G = 4 * ORC_CNN_HD;
+        const int32_t lstm = G * (ORC_CNN_EMB + ORC_CNN_HD) + G;
+        const int32_t dense = (ORC_CNN_EMB + ORC_CNN_HD) * ORC_CNN_DENSE + ORC_CNN_DENSE;
+        const int32_t out = ORC_CNN_DENSE * cfg->n_actions + cfg->n_actions;
+        return c1 + c2 + lstm + dense + out;
+    }
     int32_t I = orc_input_count(cfg), Hd = cfg->hidden, A = cfg->n_actions;
     return 4 * Hd * I + 4 * Hd * Hd + 4 * Hd + A * Hd + A;
 }
@@ -110,8 +122,14 @@ int orc_validate(const orc_config *cfg, char *msg, int msg_len) {
     if (!prob_ok(cfg->spontaneous)) return bad(msg, msg_len, "spontaneous");
     if (cfg->slots < 0) return bad(msg, msg_len, "slots");
     if (cfg->n_initial < 0 || cfg->n_initial > cfg->slots) return bad(msg, msg_len, "n_initial");
-    if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return bad(msg, msg_len, "obs_radius");
-    if (cfg->hidden < 1 || cfg->hidden > 32) return bad(msg, msg_len, "hidden");
+    if (cfg->network != 0 && cfg->network != 1) return bad(msg, msg_len, "network");
+    if (cfg->network == 1) { /* the paper's architecture fixes the window and the LSTM */
+        if (cfg->obs_radius != (ORC_CNN_WO - 1) / 2) return bad(msg, msg_len, "obs_radius");
+        if (cfg->hidden != ORC_CNN_HD) return bad(msg, msg_len, "hidden");
+    } else {
+        if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return bad(msg, msg_len, "obs_radius");
+        if (cfg->hidden < 1 || cfg->hidden > 32) return bad(msg, msg_len, "hidden");
+    }
     if (cfg->n_actions != 5) return bad(msg, msg_len, "n_actions");
     if (!(cfg->init_weight_std >= 0.0)) return bad(msg, msg_len, "init_weight_std");
     if (!(cfg->mutation_std >= 0.0)) return bad(msg, msg_len, "mutation_std");
@@ -258,6 +276,140 @@ int orc_policy(const orc_config *cfg, const float *w, const double *x, const flo
     return nonfinite ? ORC_E_NONFINITE : ORC_OK;
 }
 
+/* ------------------------------------- network 1: the paper's CNN-LSTM (NEXT-2) */
+/* "An agent observes pixel values ... within its visual range (a square of size
+ * [w_o, w_o] centered around the agent)"; "The pixel values contain information about the
+ * resources, other agents (including their number) and walls"; w_o = 15
+ * (PAPER.md:317).  Three channels (R33): resources after regrowth, agents at step start
+ * incl. self (0/1 under exclusive occupancy), walls = every cell off the grid. */
+void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O, int32_t y,
+                       int32_t x, double *xout) {
+    const int32_t r = (ORC_CNN_WO - 1) / 2, H = cfg->rows, W = cfg->cols;
+    for (int32_t row = 0; row < ORC_CNN_WO; ++row)
+        for (int32_t col = 0; col < ORC_CNN_WO; ++col) {
+            int32_t yy = y - r + row, xx = x - r + col;
+            int on = yy >= 0 && yy < H && xx >= 0 && xx < W;
+            double *px = xout + ((size_t)row * ORC_CNN_WO + col) * ORC_CNN_CH;
+            px[0] = on && R[yy * W + xx] ? 1.0 : 0.0;
+            px[1] = on && O[yy * W + xx] ? 1.0 : 0.0;
+            px[2] = on ? 0.0 : 1.0;
+        }
+}
+
+/* "First CNN has a kernel size (3,3), stride 2": SAME zero padding (R34),
+ * out = ceil(n/2) with total padding 2(out-1) + 3 - n, its floor half before. */
+void orc_conv3x3_s2_same(const double *in, int32_t H, int32_t W, int32_t cin, const float *w,
+                         const float *b, int32_t cout, double *out) {
+    const int32_t OH = (H + 1) / 2, OW = (W + 1) / 2;
+    const int32_t pad_y = (2 * (OH - 1) + 3 - H) / 2, pad_x = (2 * (OW - 1) + 3 - W) / 2;
+    for (int32_t oy = 0; oy < OH; ++oy)
+        for (int32_t ox = 0; ox < OW; ++ox)
+            for (int32_t f = 0; f < cout; ++f) {
+                double s = (double)b[f];
+                for (int32_t ky = 0; ky < 3; ++ky)
+                    for (int32_t kx = 0; kx < 3; ++kx) {
+                        int32_t iy = 2 * oy + ky - pad_y, ix = 2 * ox + kx - pad_x;
+                        if (iy < 0 || iy >= H || ix < 0 || ix >= W) continue; /* zero pad */
+                        for (int32_t ch = 0; ch < cin; ++ch)
+                            s += (double)w[((f * 3 + ky) * 3 + kx) * cin + ch] *
+                                 in[((size_t)iy * W + ix) * cin + ch];
+                    }
+                out[((size_t)oy * OW + ox) * cout + f] = s;
+            }
+}
+
+/* "average pooling of size (2,2) and stride 1", VALID (R34) */
+void orc_avgpool2_s1(const double *in, int32_t H, int32_t W, int32_t C, double *out) {
+    for (int32_t y = 0; y + 1 < H; ++y)
+        for (int32_t x = 0; x + 1 < W; ++x)
+            for (int32_t ch = 0; ch < C; ++ch) {
+                double s = in[((size_t)y * W + x) * C + ch] + in[((size_t)y * W + x + 1) * C + ch] +
+                           in[((size_t)(y + 1) * W + x) * C + ch] +
+                           in[((size_t)(y + 1) * W + x + 1) * C + ch];
+                out[((size_t)y * (W - 1) + x) * C + ch] = s / 4.0;
+            }
+}
+
+/* CNN -> flatten (72) ++ previous action (one-hot 5) ++ ate (1) = e (78);
+ * LSTM(4) on e; [e, h'] (82) -> dense 8 tanh -> dense 5 = logits.  No activation after
+ * the convolutions (R35); the LSTM gates as network 0 (i,f,g,o, one bias, R12). */
+int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int32_t last_action,
+                   int32_t ate, const float *h, const float *c, float *h_out, float *c_out,
+                   float *logits_out, double *emb_out) {
+    const int32_t E = ORC_CNN_EMB, Hd = ORC_CNN_HD, G = 4 * Hd, D = ORC_CNN_DENSE, A = cfg->n_actions;
+    const float *c1w = w, *c1b = c1w + 3 * 3 * ORC_CNN_CH * 4;
+    const float *c2w = c1b + 4, *c2b = c2w + 3 * 3 * 4 * 8;
+    const float *W_ih = c2b + 8, *W_hh = W_ih + G * E, *bl = W_hh + G * Hd;
+    const float *W_d = bl + G, *b_d = W_d + D * (E + Hd);
+    const float *W_o = b_d + D, *b_o = W_o + A * D;
+    double a1[8 * 8 * 4], p1[7 * 7 * 4], a2[4 * 4 * 8], e[ORC_CNN_EMB + ORC_CNN_HD], z[16], d[8];
+    orc_conv3x3_s2_same(obs, ORC_CNN_WO, ORC_CNN_WO, ORC_CNN_CH, c1w, c1b, 4, a1); /* 8x8x4 */
+    orc_avgpool2_s1(a1, 8, 8, 4, p1);                                              /* 7x7x4 */
+    orc_conv3x3_s2_same(p1, 7, 7, 4, c2w, c2b, 8, a2);                             /* 4x4x8 */
+    orc_avgpool2_s1(a2, 4, 4, 8, e);                                               /* 3x3x8 = 72 */
+    for (int32_t a = 0; a < 5; ++a) e[72 + a] = (a == last_action) ? 1.0 : 0.0;
+    e[77] = ate ? 1.0 : 0.0;
+    for (int32_t r = 0; r < G; ++r) {
+        double s = 0.0;
+        for (int32_t j = 0; j < E; ++j) s += (double)W_ih[r * E + j] * e[j];
+        for (int32_t j = 0; j < Hd; ++j) s += (double)W_hh[r * Hd + j] * (double)h[j];
+        z[r] = s + (double)bl[r];
+    }
+    int nonfinite = 0;
+    for (int32_t k = 0; k < Hd; ++k) {
+        double ig = sigmoid(z[k]), fg = sigmoid(z[Hd + k]), gg = tanh(z[2 * Hd + k]);
+        double og = sigmoid(z[3 * Hd + k]);
+        double cn = fg * (double)c[k] + ig * gg;
+        c_out[k] = (float)cn;
+        h_out[k] = (float)(og * tanh(cn));
+        if (!isfinite(c_out[k]) || !isfinite(h_out[k])) nonfinite = 1;
+    }
+    /* "we concatenate the embedding with the output of the LSTM" */
+    for (int32_t k = 0; k < Hd; ++k) e[E + k] = (double)h_out[k];
+    for (int32_t r = 0; r < D; ++r) {
+        double s = 0.0;
+        for (int32_t j = 0; j < E + Hd; ++j) s += (double)W_d[r * (E + Hd) + j] * e[j];
+        d[r] = tanh(s + (double)b_d[r]);
+    }
+    for (int32_t a = 0; a < A; ++a) {
+        double s = 0.0;
+        for (int32_t k = 0; k < D; ++k) s += (double)W_o[a * D + k] * d[k];
+        logits_out[a] = (float)(s + (double)b_o[a]);
+        if (!isfinite(logits_out[a])) nonfinite = 1;
+    }
+    if (emb_out) memcpy(emb_out, e, sizeof(double) * (size_t)E);
+    return nonfinite ? ORC_E_NONFINITE : ORC_OK;
+}
+
+/* "a last denser layer of size 5 ... with softmax to get the action probability from which
+ * the action will be sampled.  The softmax we use has a low temperature (1/50)"
+ * (PAPER.md:348): P_a = exp(50 l_a) / sum_b exp(50 l_b) from the fp32 logits; inverse-CDF
+ * sampling with one Philox word keyed by the agent's cell (R32). */
+int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const float *logits,
+                          double *probs_out, double *margin) {
+    double m = -INFINITY, p[5], S = 0.0;
+    for (int a = 0; a < 5; ++a)
+        if (ORC_CNN_TEMP_INV * (double)logits[a] > m) m = ORC_CNN_TEMP_INV * (double)logits[a];
+    for (int a = 0; a < 5; ++a) {
+        p[a] = exp(ORC_CNN_TEMP_INV * (double)logits[a] - m);
+        S += p[a];
+    }
+    for (int a = 0; a < 5; ++a) p[a] /= S;
+    uint32_t w4[4];
+    orc_draw4(seed, ORC_P_ACTION, step, cell, 0u, w4);
+    const double u = (double)w4[0] * 2.3283064365386963e-10; /* [0, 1) */
+    int32_t act = 4;
+    double cum = 0.0, mg = INFINITY;
+    for (int a = 0; a < 4; ++a) {
+        cum += p[a];
+        if (fabs(u - cum) < mg) mg = fabs(u - cum);
+        if (act == 4 && u < cum) act = a;
+    }
+    if (probs_out) memcpy(probs_out, p, sizeof(p));
+    *margin = mg;
+    return act;
+}
+
 /* ------------------------------------------------------------ init (C.2) ------ */
 typedef struct {
     uint32_t draw;
@@ -370,12 +522,20 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
     for (int32_t i = 0; i < S; ++i) {
         if (!st->alive[i]) continue;
         int32_t y = st->cell[i] / W, xx = st->cell[i] % W;
-        orc_observe(cfg, Rn, O, y, xx, x);
         float hn[32], cn[32], lg[8];
         int32_t a;
         double margin;
-        int rc = orc_policy(cfg, st->weights + (size_t)i * P, x, st->h + (size_t)i * Hd,
+        int rc;
+        if (cfg->network == 1) { /* the paper's CNN-LSTM, sampled */
+            orc_observe_paper(cfg, Rn, O, y, xx, x);
+            rc = orc_policy_cnn(cfg, st->weights + (size_t)i * P, x, st->last_action[i], st->ate[i],
+                                st->h + (size_t)i * Hd, st->c + (size_t)i * Hd, hn, cn, lg, NULL);
+            a = orc_sample_action(cfg->seed, t, (uint32_t)st->cell[i], lg, NULL, &margin);
+        } else {
+            orc_observe(cfg, Rn, O, y, xx, x);
+            rc = orc_policy(cfg, st->weights + (size_t)i * P, x, st->h + (size_t)i * Hd,
                             st->c + (size_t)i * Hd, hn, cn, lg, &a, &margin);
+        }
         if (rc != ORC_OK) status = rc;
         if (margin < 1e-4) rec->near_ties++;
         memcpy(st->h + (size_t)i * Hd, hn, sizeof(float) * (size_t)Hd);

@@ -40,6 +40,15 @@ extern "C" {
 #define ORC_P_MOVE 5u
 #define ORC_P_BIRTH 6u
 #define ORC_P_MUTATE 7u
+#define ORC_P_ACTION 8u  /* the sampled action of network 1 ("sampled") */
+
+/* network 1, the paper's CNN-LSTM: sizes */
+#define ORC_CNN_WO 15   /* field of view w_o = 15                        */
+#define ORC_CNN_CH 3    /* resources, agents, walls (SPEC's 2445 count)   */
+#define ORC_CNN_EMB 78  /* 3*3*8 CNN features + one-hot previous action (5) + ate (1)   */
+#define ORC_CNN_HD 4    /* LSTM hidden size                              */
+#define ORC_CNN_DENSE 8 /* dense layer with tanh                         */
+#define ORC_CNN_TEMP_INV 50.0 /* softmax temperature 1/50: softmax(50 * logits)         */
 
 typedef struct {
     int32_t rows, cols;           /* H (latitude axis, row 0 = top), W            */
@@ -61,6 +70,10 @@ typedef struct {
     int32_t death_steps;          /* > 0: die after this many consecutive steps with      */
                                   /* energy <= e_death_le (T_death)          */
     int32_t lethal_walls;         /* 1: a move off the grid kills the agent */
+    /* the agents' network: 0 = LSTM + linear head with argmax on a
+     * (2r+1)^2 x 2 window (BASELINE); 1 = the paper's CNN-LSTM on a 15x15x3 window with
+     * softmax(50 logits) sampling (obs_radius 7, hidden 4)            */
+    int32_t network;
 } orc_config;
 
 /* Canonical state; all buffers are owned by the caller. */
@@ -76,7 +89,11 @@ typedef struct {
     uint8_t *ate;         /* [S]                                                 */
     float *h;             /* [S][Hd]                                             */
     float *c;             /* [S][Hd]                                             */
-    float *weights;       /* [S][P] canonical: W_ih[4Hd][I], W_hh[4Hd][Hd], b[4Hd], W_out[5][Hd], b_out[5] */
+    float *weights;       /* [S][P] canonical: W_ih[4Hd][I], W_hh[4Hd][Hd], b[4Hd], W_out[5][Hd], b_out[5];
+                             network 1 (P = 2445): conv1_w[4][3][3][3] ([out][ky][kx][in]),
+                             conv1_b[4], conv2_w[8][3][3][4], conv2_b[8], W_ih[16][78],
+                             W_hh[16][4], b[16] (gates i,f,g,o), W_d[8][82], b_d[8],
+                             W_out[5][8], b_out[5]                                   */
     float *logits;        /* [S][5]                                              */
     int32_t *low;         /* [S] consecutive steps with energy <= e_death_le (death timer) */
 } orc_state;
@@ -87,7 +104,8 @@ typedef struct {
     int64_t deaths_energy, deaths_age;
     int64_t deferred_no_cell, deferred_claim, deferred_capacity;
     int64_t population, resources; /* after the step */
-    int64_t near_ties;              /* live agents with top1-top2 logit margin < 1e-4 */
+    int64_t near_ties;              /* live agents with top1-top2 logit margin < 1e-4 (network 1:
+                                       the sampling margin < 1e-4, R32) */
     int64_t deaths_wall;            /* agents killed by a move off the grid (lethal walls) */
 } orc_record;
 
@@ -123,6 +141,29 @@ void orc_observe(const orc_config *cfg, const uint8_t *R, const uint8_t *O, int3
 int orc_policy(const orc_config *cfg, const float *w, const double *x, const float *h,
                const float *c, float *h_out, float *c_out, float *logits_out, int32_t *action,
                double *margin);
+
+/* ---- network 1: the paper's CNN-LSTM, evaluated in fp64 ---- */
+/* 15x15x3 window, HWC (x[(row*15 + col)*3 + ch]), rows from the top: ch 0 resources
+ * after regrowth, ch 1 agents at step start incl. self, ch 2 walls = 1 off the grid */
+void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O, int32_t y,
+                       int32_t x, double *xout);
+/* 3x3 convolution, stride 2, SAME zero padding (out = ceil(n/2), pad 1 before), HWC in,
+ * w[cout][3][3][cin], b[cout]; out[(oy*OW + ox)*cout + f] */
+void orc_conv3x3_s2_same(const double *in, int32_t H, int32_t W, int32_t cin, const float *w,
+                         const float *b, int32_t cout, double *out);
+/* 2x2 average pool, stride 1, VALID: (H-1)x(W-1)xC, HWC */
+void orc_avgpool2_s1(const double *in, int32_t H, int32_t W, int32_t C, double *out);
+/* the forward of one agent: the 78-float embedding e, the LSTM (h', c', fp32 stored), the
+ * tanh dense layer and the 5 logits (fp32).  emb_out may be NULL. Returns ORC_OK or
+ * ORC_E_NONFINITE. */
+int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int32_t last_action,
+                   int32_t ate, const float *h, const float *c, float *h_out, float *c_out,
+                   float *logits_out, double *emb_out);
+/* softmax(50 * logits) sampled with u = draw(ACTION, step, cell)[0] * 2^-32: the least a
+ * with u < P_0 + ... + P_a (4 if none); *margin = min over the 4 inner boundaries of
+ * |u - (P_0 + ... + P_k)| (a near-tie below 1e-4, R32); probs_out (may be NULL) [5] */
+int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const float *logits,
+                          double *probs_out, double *margin);
 
 /* initial world (C.2) */
 int orc_init(const orc_config *cfg, orc_state *st);

@@ -50,6 +50,7 @@ class WorldConfig:
     climate_alpha: float = 0.0               # > 0: exponential climate (alpha^x + 1)/(alpha + 1)
     death_steps: int = 0                     # > 0: the death timer T_death (else immediate death)
     lethal_walls: int = 0                    # 1: moving off the grid kills
+    network: int = 0                         # 1: the paper's CNN-LSTM, sampled (NEXT-2; r 7, Hd 4)
     steps: int = 100                         # run length named by the config
     name: str = ""
 
@@ -59,11 +60,15 @@ class WorldConfig:
 
     @property
     def n_inputs(self) -> int:
+        if self.network == 1:
+            return 15 * 15 * 3
         w = 2 * self.obs_radius + 1
         return 2 * w * w
 
     @property
     def n_params(self) -> int:
+        if self.network == 1:  # the paper's count
+            return 2445
         I, Hd, A = self.n_inputs, self.hidden, self.n_actions
         return 4 * Hd * I + 4 * Hd * Hd + 4 * Hd + A * Hd + A
 
@@ -103,6 +108,15 @@ def paper_world() -> WorldConfig:
                        mutation_std=0.02, e_init=3000, e_decay=25, e_gain=1000, e_repr_gt=0, e_death_le=-1,
                        e_max=3000, repr_steps=140, death_steps=200, max_age=650, lethal_walls=1,
                        steps=1_000_000, name="paper_world")
+
+
+def paper_world_cnn() -> WorldConfig:
+    """The paper's own world with the paper's own agents (SURVEY.md §8(f) NEXT-1 + NEXT-2):
+    paper_world() with the CNN-LSTM of PAPER.md:346-350 -- a 15x15x3 window (resources,
+    agents, walls), conv 3x3/2 (4) -> avgpool 2/1 -> conv 3x3/2 (8) -> avgpool 2/1 -> 72,
+    ++ previous action (5) ++ ate (1) -> LSTM(4) -> [78 ++ 4] -> dense 8 tanh -> dense 5 ->
+    softmax(50 logits), sampled; 2445 parameters per agent."""
+    return paper_world().replace(network=1, obs_radius=7, hidden=4, name="paper_world_cnn")
 
 
 def regrowth_micro(rows: int = 200, cols: int = 400) -> WorldConfig:
