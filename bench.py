@@ -411,7 +411,7 @@ def run_ours(args, rank, world_size, local_rank):
             rl = {}
             for kname, (desc, byt, ms, step_ms_tot) in cands.items():
                 achieved = byt / (ms / 1e3) / 1e9
-                ratio, ratio_src = traffic_ratio(kname, wc.name)
+                ratio, ratio_src = traffic_ratio(kname, wc.name, agents / K)
                 rl[kname] = {
                     "kernel": desc, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": ratio * byt / K if ratio else None,
@@ -432,26 +432,35 @@ def run_ours(args, rank, world_size, local_rank):
     return result, snap, wc
 
 
-def traffic_ratio(kname="policy", workload="paper_scale"):
+def traffic_ratio(kname="policy", workload="paper_scale", agents=None):
     """DRAM bytes (read + write) over algorithmic bytes of the kernel's launch (policy: the
-    k_policy launch; hh: k_prepare_p) in the newest committed ncu --set full summary
-    (profiles/*_ncu_summary.json, tools/ncu_summary.py); the roofline's `traffic` is this
-    ratio times the bench's algorithmic bytes per launch (the captured launch is one step of
-    the same workload, not the bench's own launches)."""
+    k_policy launch; hh: k_prepare_p) in a committed ncu --set full summary
+    (profiles/<generation>_*_ncu_summary.json, tools/ncu_summary.py): of the newest
+    generation (the name's prefix, e.g. r2a) that captured this workload, the capture whose
+    live-agent count is closest to the bench's mean; the roofline's `traffic` is this ratio
+    times the bench's algorithmic bytes per launch (the captured launch is one step of the
+    same workload, not the bench's own launches)."""
     tag = {"policy": "k_policy", "hh": "k_prepare_p", "post": "k_post"}[kname]
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=os.path.getmtime)
-    for f in reversed(files):
+    found = []
+    for f in glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")):
         try:
             d = json.load(open(f))
-            if d.get("step", {}).get("workload", "paper_scale") != workload:
+            st = d.get("step", {})
+            if st.get("workload", "paper_scale") != workload:
                 continue  # a capture of another workload
             for rec in d["launches"]:
                 if tag in rec["kernel"] and "traffic_over_algorithmic" in rec:
-                    return float(rec["traffic_over_algorithmic"]), os.path.relpath(f, ROOT)
+                    gen = os.path.basename(f).split("_")[0]
+                    dist = abs(st.get("agents", 0) - agents) if agents is not None else 0
+                    found.append((gen, -dist, float(rec["traffic_over_algorithmic"]), os.path.relpath(f, ROOT)))
+                    break
         except Exception:
             continue
-    return None, None
+    if not found:
+        return None, None
+    best = max(found)
+    return best[2], best[3]
 
 
 # -------------------------------------------------------------- oracle (CPU) legs
