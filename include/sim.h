@@ -71,8 +71,8 @@ typedef struct {
     double lat_top, lat_bottom; /* climate lat(0), lat(H-1), linear in y/(H-1)         */
     double spontaneous;     /* constant spontaneous growth probability c                */
     int32_t slots, n_initial; /* S agent slots (population cap, <= 2^24 - 1), N0 initial agents */
-    int32_t obs_radius;     /* r: window (2r+1)^2, 0..3                                   */
-    int32_t hidden;         /* LSTM hidden size Hd in {4, 8, 16, 32}                      */
+    int32_t obs_radius;     /* r: window (2r+1)^2, 0..3 (network 1: 7)                    */
+    int32_t hidden;         /* LSTM hidden size Hd in {4, 8, 16, 32} (network 1: 4)       */
     int32_t n_actions;      /* must be 5 (stay, N, S, E, W)                               */
     int32_t log_capacity;   /* step records kept per world (ring, rounded up to a power of 2); 0 -> 4096 */
     double init_weight_std, mutation_std; /* standard deviations (R23)                   */
@@ -106,6 +106,16 @@ typedef struct {
                                energy <= e_death_le (T_death), else at once  */
     int32_t lethal_walls;   /* 1: a move off the grid kills the agent,
                                0: it is blocked (R15)                                      */
+    /* The agents' network:
+     *   0  an LSTM of `hidden` units on the (2r+1)^2 x 2 window + a linear head, argmax
+     *      (BASELINE.json);
+     *   1  the paper's CNN-LSTM: a 15x15x3 window (resources, agents,
+     *      walls = off the grid), conv 3x3/2 SAME (4) -> avgpool 2/1 -> conv 3x3/2 SAME (8)
+     *      -> avgpool 2/1 -> 72 ++ one-hot previous action (5) ++ ate (1) = 78 -> LSTM(4) ->
+     *      [78 ++ h'] -> dense 8 tanh -> dense 5 -> softmax(50 logits), the action SAMPLED by
+     *      inverse CDF with the Philox word (ACTION = 8, t, cell) (R32-R36);
+     *      requires obs_radius = 7, hidden = 4 and n_bands <= 1; 2445 parameters.        */
+    int32_t network;
 } sim_config;
 
 /* Canonical state, host buffers owned by the caller, layouts with the world index
@@ -113,7 +123,10 @@ typedef struct {
  * keeps the device value.  Dead slots: only `alive` is meaningful.
  *   weights: per slot P floats in canonical order W_ih[4Hd][I] (gate blocks i,f,g,o,
  *   row-major), W_hh[4Hd][Hd], b[4Hd], W_out[5][Hd], b_out[5];
- *   P = 4Hd*I + 4Hd*Hd + 4Hd + 5Hd + 5 with I = 2(2r+1)^2. */
+ *   P = 4Hd*I + 4Hd*Hd + 4Hd + 5Hd + 5 with I = 2(2r+1)^2.
+ *   network 1 (P = 2445): conv1_w[4][3][3][3] ([out][ky][kx][in]), conv1_b[4],
+ *   conv2_w[8][3][3][4], conv2_b[8], W_ih[16][78], W_hh[16][4], b[16] (gates i,f,g,o),
+ *   W_d[8][82], b_d[8], W_out[5][8], b_out[5]. */
 typedef struct {
     int64_t t;             /* steps taken; all worlds share t                              */
     uint8_t *resources;    /* [n_worlds][H][W] 0/1                                         */
@@ -210,6 +223,11 @@ SIM_API sim_status sim_state_sizes(const sim_config *cfg, sim_state_sizes_t *out
 /* act: [n_worlds][S], 255 = use the policy; NULL clears.  The policy still runs (h, c,
  * logits update); only the move uses the forced action.  Applies to every later step. */
 SIM_API sim_status sim_set_forced_actions(sim_handle h, const uint8_t *act);
+/* Test hook: out[n_worlds][S] receives, for the most recent step taken while forced
+ * actions were set, each slot's OWN policy decision (network 0: the argmax; network 1:
+ * the sampled action) before the forced action replaced it.  Meaningful only for slots
+ * alive at that step's start.  Synchronises.  Not available on banded handles. */
+SIM_API sim_status sim_get_policy_actions(sim_handle h, uint8_t *out);
 /* Records of steps [first, first+n) for all worlds, out[n][n_worlds]; the steps must be
  * among the last log_capacity steps taken. */
 SIM_API sim_status sim_get_step_log(sim_handle h, int64_t first, int64_t n, sim_step_record *out);

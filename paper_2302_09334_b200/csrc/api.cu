@@ -47,6 +47,7 @@ sim_status fail(sim_status st, const char *fmt, ...) {
 struct Derived {
     int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, log_cap;
     int off_hh, off_b, off_out, off_bout;
+    int net;    // 0: LSTM + linear head (argmax); 1: the paper's CNN-LSTM (sampled)
     size_t pw;  // words per plane per world
 };
 
@@ -74,9 +75,17 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
     // (<= 2^24 - 1: k_post carries a step's birth count in 24 bits of its release flag)
     if (cfg->slots < 0 || cfg->slots > 0xFFFFFF) return fail(SIM_E_INVALID, "invalid field: slots");
     if (cfg->n_initial < 0 || cfg->n_initial > cfg->slots) return fail(SIM_E_INVALID, "invalid field: n_initial");
-    if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return fail(SIM_E_INVALID, "invalid field: obs_radius (0..3)");
-    if (!(cfg->hidden == 4 || cfg->hidden == 8 || cfg->hidden == 16 || cfg->hidden == 32))
-        return fail(SIM_E_INVALID, "invalid field: hidden (4, 8, 16 or 32)");
+    if (cfg->network != 0 && cfg->network != 1) return fail(SIM_E_INVALID, "invalid field: network (0 or 1)");
+    if (cfg->network == 1) {  // the paper's architecture fixes the window and the LSTM
+        if (cfg->obs_radius != 7) return fail(SIM_E_INVALID, "invalid field: obs_radius (network 1: 7, a 15x15 window)");
+        if (cfg->hidden != 4) return fail(SIM_E_INVALID, "invalid field: hidden (network 1: 4)");
+        if (cfg->n_bands > 1)
+            return fail(SIM_E_INVALID, "invalid field: n_bands (network 1's 7-row window exceeds the bands' halo)");
+    } else {
+        if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return fail(SIM_E_INVALID, "invalid field: obs_radius (0..3)");
+        if (!(cfg->hidden == 4 || cfg->hidden == 8 || cfg->hidden == 16 || cfg->hidden == 32))
+            return fail(SIM_E_INVALID, "invalid field: hidden (4, 8, 16 or 32)");
+    }
     if (cfg->n_actions != 5) return fail(SIM_E_INVALID, "invalid field: n_actions (must be 5)");
     if (!(cfg->init_weight_std >= 0.0) || !std::isfinite(cfg->init_weight_std))
         return fail(SIM_E_INVALID, "invalid field: init_weight_std");
@@ -104,6 +113,13 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
         d->off_out = d->off_b + d->Hd * 4;
         d->off_bout = d->off_out + 5 * d->Hd;
         d->Pd = (d->off_bout + 5 + 31) / 32 * 32;
+        d->net = cfg->network;
+        if (d->net == 1) {  // canonical order on the device too (sim.h), rows padded to 32 floats
+            d->I = 15 * 15 * 3;
+            d->P = 2445;
+            d->Pd = 2464;
+            d->off_hh = d->off_b = d->off_out = d->off_bout = 0;  // (network 0's layout only)
+        }
         d->n_worlds = cfg->n_worlds;
         {  // the ring holds at least log_capacity steps: rounded up to a power of two (a mask)
             const int want = cfg->log_capacity ? cfg->log_capacity : 4096;
@@ -485,6 +501,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
 
     DevParams &p = h->p;
     p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
+    p.net = d.net;
     p.row_lo = band ? band->y0 : 0;
     p.row_hi = band ? band->y1 : d.H;
     p.regrow_split = 0;
@@ -572,6 +589,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     p.le_cap = le_windows(d.log_cap);
     H(&p.le, nw * (size_t)p.le_cap * 2);
     H(&h->forced_dev, nw * S);
+    H(&p.own_act, nw * S);
     H(&p.Pbuf, p.split ? S * (size_t)d.Hd * 4 : 1);
     H(&p.h, nw * S * d.Hd);
     H(&p.c, nw * S * d.Hd);
@@ -638,9 +656,8 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     int bps = 0;
     CKC(eco::policy_prepare(), "kernel attributes");  // before the occupancy query (dynamic smem opt-in)
     CKC(eco::post_prepare(), "kernel attributes");
-    CKC(eco::policy_occupancy(d.Hd, 256, &bps), "occupancy");
+    CKC(eco::policy_occupancy(d.Hd, d.net, &bps, &h->lc.policy_threads), "occupancy");
     if (bps < 1) bps = 1;
-    h->lc.policy_threads = 256;
     h->lc.policy_blocks = prop.multiProcessorCount * bps;
     h->lc.sms = prop.multiProcessorCount;
     h->lc.agent_threads = 256;
@@ -1133,6 +1150,18 @@ sim_status sim_get_move_hist(sim_handle h, int64_t first, int64_t n, int32_t *ou
             CK(h, cudaMemcpyAsync(out + (i * nw + w) * SIM_MOVE_BINS,
                                   h->p.mv_hist + (w * h->p.mv_cap + (size_t)((first + i) & (h->p.mv_cap - 1))) * SIM_MOVE_BINS,
                                   SIM_MOVE_BINS * 4, cudaMemcpyDeviceToHost, h->stream), "move histogram");
+    return sync(h);
+}
+
+sim_status sim_get_policy_actions(sim_handle h, uint8_t *out) {
+    if (h && !h->bands.empty()) return fail(SIM_E_STATE, "not available on a banded handle");
+    sim_status st = check_handle(h);
+    if (st != SIM_OK) return st;
+    if (!out) return fail(SIM_E_INVALID, "invalid argument: NULL");
+    CK(h, cudaSetDevice(h->device), "cudaSetDevice");
+    if ((st = sync(h)) != SIM_OK) return st;
+    const size_t n = (size_t)h->d.n_worlds * h->d.S;
+    if (n) CK(h, cudaMemcpyAsync(out, h->p.own_act, n, cudaMemcpyDeviceToHost, h->stream), "policy actions");
     return sync(h);
 }
 

@@ -882,8 +882,10 @@ __device__ void birth_rank_world(const DevParams &p, int w, uint32_t *scratch, i
 // phase advanced t, so the birth step is p.t[w] - 1.
 
 // pair items per child: (I + Hd)/2 column pairs x HD4 rows, 2Hd bias pairs, ceil((5Hd+5)/2)
+// (network 1: its device row is the canonical row, so pair it = weights 2it, 2it + 1)
 template <typename PP>
 __device__ __forceinline__ int mutate_items_per_child(const PP &p) {
+    if (p.net == 1) return (p.P + 1) >> 1;
     return ((p.I + p.Hd) >> 1) * (p.Hd * 4) + 2 * p.Hd + (5 * p.Hd + 6) / 2;
 }
 
@@ -891,6 +893,11 @@ __device__ __forceinline__ int mutate_items_per_child(const PP &p) {
 // the pair is a singleton: the last b_out entry), canonical index j0 (even)
 template <typename PP>
 __device__ __forceinline__ void mutate_item(const PP &p, int it, int &d0, int &dstep, int &j0) {
+    if (p.net == 1) {
+        d0 = j0 = 2 * it;
+        dstep = 2 * it + 1 < p.P ? 1 : 0;
+        return;
+    }
     const int Hd = p.Hd, G = 4 * Hd, HD4 = Hd * 4;
     const int nA = ((p.I + Hd) >> 1) * HD4;
     if (it < nA) {
@@ -1039,6 +1046,7 @@ struct MutArgs {
     const uint8_t *owner;
     double mutation_std;
     int S, Pd, I, Hd, hd_shift, off_b, off_out, n_ranks, rank;
+    int net, P;
 };
 __device__ __forceinline__ MutArgs mut_args(const DevParams &p) {
     MutArgs a;
@@ -1050,6 +1058,8 @@ __device__ __forceinline__ MutArgs mut_args(const DevParams &p) {
     a.mutation_std = p.mutation_std;
     a.S = p.S;
     a.Pd = p.Pd;
+    a.net = p.net;
+    a.P = p.P;
     a.I = p.I;
     a.Hd = p.Hd;
     a.hd_shift = p.hd_shift;

@@ -44,7 +44,8 @@
 namespace eco {
 
 constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
-                   PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7;
+                   PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7,
+                   PURPOSE_ACTION = 8;  // the sampled action of network 1 (R32)
 constexpr int LOGIT_STRIDE = 8;
 constexpr uint8_t NO_DIR = 0xFF;
 
@@ -52,6 +53,7 @@ constexpr uint8_t NO_DIR = 0xFF;
 // captured CUDA graph serves every step; the step index lives in device memory).
 struct DevParams {
     int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, r, log_cap;
+    int net;             // 0: LSTM + linear head, argmax; 1: the paper's CNN-LSTM, sampled (NEXT-2)
     int row_lo, row_hi;  // rows this handle owns: [0, H) unless it is one latitude band (banded mode)
     int regrow_split;    // 1: k_post leaves the regrowth of step t+1 to k_regrow_tiled, launched after
                          // it (agent-free worlds of many words: the configs[2] benchmark grids)
@@ -129,6 +131,7 @@ struct DevParams {
     unsigned long long *totals;  // [7] sim_totals order
     unsigned long long *phase_ns;  // [SIM_NUM_POST_PHASES] k_post phase clock (block 0)
     const uint8_t *forced;       // [n_worlds][S]
+    uint8_t *own_act;            // [n_worlds][S] test hook: the policy's own action while forcing is on
     const int32_t *forced_on;    // device flag
     int32_t *nonfinite;          // host-mapped flag
 };
@@ -201,7 +204,13 @@ __device__ __forceinline__ void box_muller(uint32_t wa, uint32_t wb, double &za,
     zb = __dmul_rn(rad, sin(th));
 }
 
-// canonical weight index j -> device index (see the layout note above)
+// canonical weight index j -> device index (see the layout note above); network 1 keeps
+// the canonical order (its device row is the canonical row padded to Pd)
+__device__ __forceinline__ int canon_to_dev(int j, int I, int Hd, int off_hh, int off_b, int off_out,
+                                            int off_bout);
+__device__ __forceinline__ int canon_to_dev(const DevParams &p, int j) {
+    return p.net == 1 ? j : canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
+}
 __device__ __forceinline__ int canon_to_dev(int j, int I, int Hd, int off_hh, int off_b, int off_out,
                                             int off_bout) {
     const int G = 4 * Hd;
@@ -357,7 +366,7 @@ cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s)
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s);
 cudaError_t launch_mutate(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);
-cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm);
+cudaError_t policy_occupancy(int hidden, int net, int *blocks_per_sm, int *threads);
 cudaError_t post_occupancy(int *blocks_per_sm);
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s);
 cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot] = slot % n_ranks,

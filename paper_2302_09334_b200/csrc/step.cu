@@ -89,6 +89,42 @@ __device__ __forceinline__ void obs_mask(const DevParams &p, int w, int64_t t, i
     m_hi = ((uint64_t)a3 << 32) | a2;
 }
 
+// The action (the policy's, or the forced one of the test hook), last_action, and the move
+// claim of a4: a valid non-stay move posts (MOVE w0 << 32 | ~cell) with atomicMax on
+// claim[target] (R14); a move off the grid is blocked (R15) or marks the lethal wall.
+// occ_in_window(act) answers "is the target in O_t" from the policy's own window (r >= 1).
+template <bool SHARD = false, typename OccFn>
+__device__ __forceinline__ void agent_commit(const DevParams &p, int w, int i, int slot, size_t gs, int64_t t,
+                                             int cellv, int act, int forced_on, OccFn occ_in_window) {
+    if (forced_on) {
+        p.own_act[gs] = (uint8_t)act;  // test hook (sim_get_policy_actions)
+        const uint8_t f = p.forced[gs];
+        if (f != 255) act = f;
+    }
+    p.last_action[gs] = (uint8_t)act;
+    int tg = -1;
+    unsigned long long key = 0ull;
+    if (act != 0) {
+        const int y = row_of(p, cellv), x = cellv - y * p.W;
+        const int ty = y + kDY[act], tx = x + kDX[act];
+        if (p.lethal_walls && !(ty >= 0 && ty < p.H && tx >= 0 && tx < p.W)) tg = WALL_TARGET;
+        if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
+            const int tc = ty * p.W + tx;
+            const bool occupied = p.r >= 1 ? occ_in_window(act)
+                                           : get_bit(p.occ + (size_t)w * plane_words(p), p, tc) != 0u;
+            if (!occupied) {
+                const uint4 d = draw4(p.seeds[w], PURPOSE_MOVE, (uint32_t)t, (uint32_t)cellv, 0u);
+                key = ((unsigned long long)d.x << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
+                if (!SHARD) atomicMax(p.claim + (size_t)w * p.H * p.W + tc, key);  // sharded: in k_post
+                tg = tc;
+            }
+        }
+    }
+    const int4 mr = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
+    if (SHARD) p.mrec_slot[slot] = mr;  // sharded: exchanged by slot, listed in k_post
+    else p.mrec[(size_t)w * p.S + i] = mr;
+}
+
 // ------------------------------------------------------------ agent epilogue (a3, a4)
 // argmax (lowest index on exact ties), near-tie flag (margin < 1e-4, R28), forced action,
 // stored logits/action, and the move claim of a4: a valid non-stay move posts
@@ -121,40 +157,12 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
         if (m_lo & ((1ull << wd2) - 1ull)) p.gr_seen[gs] = 1;
     }
 #endif
-    int act = best;
-    if (forced_on) {
-        const uint8_t f = p.forced[gs];
-        if (f != 255) act = f;
-    }
-    p.last_action[gs] = (uint8_t)act;
-    int tg = -1;
-    unsigned long long key = 0ull;
-    if (act != 0) {
-        const int y = row_of(p, cellv), x = cellv - y * p.W;
-        const int ty = y + kDY[act], tx = x + kDX[act];
-        if (p.lethal_walls && !(ty >= 0 && ty < p.H && tx >= 0 && tx < p.W)) tg = WALL_TARGET;
-        if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
-            const int tc = ty * p.W + tx;
-            // O_t of the target: the agent channel of the window already holds it (r >= 1)
-            bool occupied;
-            if (p.r >= 1) {
-                const int wd = 2 * p.r + 1;
-                const int bi = wd * wd + (p.r + kDY[act]) * wd + (p.r + kDX[act]);
-                occupied = ((bi < 64 ? (m_lo >> bi) : (m_hi >> (bi - 64))) & 1ull) != 0ull;
-            } else {
-                occupied = get_bit(p.occ + (size_t)w * plane_words(p), p, tc) != 0u;
-            }
-            if (!occupied) {
-                const uint4 d = draw4(p.seeds[w], PURPOSE_MOVE, (uint32_t)t, (uint32_t)cellv, 0u);
-                key = ((unsigned long long)d.x << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)cellv);
-                if (!SHARD) atomicMax(p.claim + (size_t)w * p.H * p.W + tc, key);  // sharded: in k_post
-                tg = tc;
-            }
-        }
-    }
-    const int4 mr = make_int4(slot, cellv, tg, (int)(uint32_t)(key >> 32));
-    if (SHARD) p.mrec_slot[slot] = mr;  // sharded: exchanged by slot, listed in k_post
-    else p.mrec[(size_t)w * p.S + i] = mr;
+    agent_commit<SHARD>(p, w, i, slot, gs, t, cellv, best, forced_on, [&](int act) {
+        // O_t of the target: the agent channel of the window already holds it (r >= 1)
+        const int wd = 2 * p.r + 1;
+        const int bi = wd * wd + (p.r + kDY[act]) * wd + (p.r + kDX[act]);
+        return ((bi < 64 ? (m_lo >> bi) : (m_hi >> (bi - 64))) & 1ull) != 0ull;
+    });
 }
 
 // housekeeping for the later phases of this step (any policy kernel runs it): the survivor
@@ -811,7 +819,12 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
     }
 }
 
-cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
+#include "policy_cnn.cuh"
+
+cudaError_t policy_occupancy(int hidden, int net, int *blocks_per_sm, int *threads_out) {
+    const int threads = net == 1 ? CNN_THREADS : 256;
+    *threads_out = threads;
+    if (net == 1) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_cnn, CNN_THREADS, CNN_SMEM);
     switch (hidden) {
         case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<4>, threads, 0);
         case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<8>, threads, 0);
@@ -823,6 +836,8 @@ cudaError_t policy_occupancy(int hidden, int threads, int *blocks_per_sm) {
 
 cudaError_t policy_prepare() {
     cudaError_t e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_policy_cnn, cudaFuncAttributeMaxDynamicSharedMemorySize, CNN_SMEM);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_policy_half<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
     if (e != cudaSuccess) return e;
@@ -836,6 +851,10 @@ cudaError_t policy_prepare() {
 }
 
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl) {
+    if (p.net == 1) {
+        k_policy_cnn<<<lc.policy_blocks, CNN_THREADS, CNN_SMEM, s>>>(p);
+        return cudaGetLastError();
+    }
     switch (p.Hd) {
         case 4: k_policy_reg<4><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;
         case 8: k_policy_reg<8><<<lc.policy_blocks, lc.policy_threads, 0, s>>>(p); break;

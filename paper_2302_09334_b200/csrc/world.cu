@@ -74,7 +74,7 @@ __global__ void k_init_weights(DevParams p, int w, int n_initial) {
         for (int m = 0; m < 4; ++m) {
             const int j = 4 * q + m;
             if (j >= p.P) break;
-            wd[canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout)] =
+            wd[canon_to_dev(p, j)] =
                 __double2float_rn(__dmul_rn(p.init_weight_std, z[m]));
         }
     }
@@ -230,7 +230,7 @@ __global__ void k_weights_to_device(DevParams p, const float *canon, size_t firs
     if (idx >= n * (size_t)p.P) return;
     const size_t a = idx / p.P;
     const int j = (int)(idx - a * p.P);
-    p.weights[(first + a) * p.Pd + canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout)] = canon[idx];
+    p.weights[(first + a) * p.Pd + canon_to_dev(p, j)] = canon[idx];
 }
 
 __global__ void k_weights_to_canon(DevParams p, float *canon, size_t first, size_t n) {
@@ -238,7 +238,7 @@ __global__ void k_weights_to_canon(DevParams p, float *canon, size_t first, size
     if (idx >= n * (size_t)p.P) return;
     const size_t a = idx / p.P;
     const int j = (int)(idx - a * p.P);
-    canon[idx] = p.weights[(first + a) * p.Pd + canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout)];
+    canon[idx] = p.weights[(first + a) * p.Pd + canon_to_dev(p, j)];
 }
 
 cudaError_t launch_weights_to_device(const DevParams &p, const float *canon, size_t first, size_t n, cudaStream_t s) {
@@ -266,7 +266,7 @@ __global__ void k_weights_gather(DevParams p, const float *src, int by_slot, con
                                  float *stage, int32_t *bad) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= p.P) return;
-    const int d = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
+    const int d = canon_to_dev(p, j);
     int nonfin = 0;
     for (int k = blockIdx.y; k < n_live; k += gridDim.y) {
         const size_t row = by_slot ? (size_t)live[k] : (size_t)k;
@@ -289,7 +289,7 @@ __global__ void k_weights_scatter(DevParams p, const float4 *stage, const int32_
 __global__ void k_weights_to_canon_list(DevParams p, const int32_t *list, int n, float *canon) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= p.P) return;
-    const int d = canon_to_dev(j, p.I, p.Hd, p.off_hh, p.off_b, p.off_out, p.off_bout);
+    const int d = canon_to_dev(p, j);
     for (int k = blockIdx.y; k < n; k += gridDim.y) canon[(size_t)k * p.P + j] = p.weights[(size_t)list[k] * p.Pd + d];
 }
 

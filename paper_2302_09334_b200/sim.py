@@ -30,7 +30,7 @@ EXPORTED = ("sim_create", "sim_step", "sim_get_state", "sim_set_state", "sim_des
             "sim_shard", "sim_step_policy", "sim_step_post", "sim_exchange", "sim_get_step_log_async",
             "sim_set_record_mirror", "sim_step_graph_timed", "sim_get_move_hist",
             "sim_band_export", "sim_band_import", "sim_band_nccl_id", "sim_band_nccl_init", "sim_band_step_timed",
-            "sim_get_greediness", "sim_get_life_windows")
+            "sim_get_greediness", "sim_get_life_windows", "sim_get_policy_actions")
 GREED_WINDOW, LIFE_WINDOW = 20, 500  # include/sim.h: SIM_GREED_WINDOW, SIM_LIFE_WINDOW
 BAND_PHASES = ("halo_x1", "policy", "merge_x2", "move", "arrive_x3", "live", "prep_p", "halo_x4a", "claims",
                "merge_x4b", "rank", "mutate", "regrow")  # include/sim.h: SIM_BAND_PHASES
@@ -70,6 +70,7 @@ class SimConfig(ctypes.Structure):
         ("band_rows", ctypes.POINTER(ctypes.c_int32)), ("band_slots", ctypes.c_int32),
         # the paper's own world (include/sim.h)
         ("climate_alpha", ctypes.c_double), ("death_steps", ctypes.c_int32), ("lethal_walls", ctypes.c_int32),
+        ("network", ctypes.c_int32),
     ]
 
 
@@ -120,6 +121,7 @@ def lib():
             L.sim_validate.argtypes = [ctypes.POINTER(SimConfig)]
             L.sim_state_sizes.argtypes = [ctypes.POINTER(SimConfig), ctypes.POINTER(SimStateSizes)]
             L.sim_set_forced_actions.argtypes = [H, ctypes.c_void_p]
+            L.sim_get_policy_actions.argtypes = [H, ctypes.c_void_p]
             L.sim_get_step_log.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
             if hasattr(L, "sim_get_step_log_async"):
                 L.sim_get_step_log_async.argtypes = [H, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
@@ -194,6 +196,7 @@ def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0, bands=N
     c.climate_alpha = float(getattr(wc, "climate_alpha", 0.0))
     c.death_steps = int(getattr(wc, "death_steps", 0))
     c.lethal_walls = int(getattr(wc, "lethal_walls", 0))
+    c.network = int(getattr(wc, "network", 0))
     keep = [seeds]
     if bands:
         G = int(bands["n_bands"])
@@ -208,8 +211,8 @@ def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0, bands=N
     return c, keep
 
 
-def validate(wc) -> None:
-    c, _seeds = make_config(wc)
+def validate(wc, bands=None) -> None:
+    c, _seeds = make_config(wc, bands=bands)
     _check(lib().sim_validate(ctypes.byref(c)))
 
 
@@ -389,6 +392,12 @@ class World:
             return
         a = np.ascontiguousarray(np.asarray(actions, dtype=np.uint8).reshape(self.n_worlds, self.wc.slots))
         _check(lib().sim_set_forced_actions(self._h, _ptr(a)))
+
+    def policy_actions(self) -> np.ndarray:
+        """[n_worlds][S]: the policy's own action of each slot in the last forced step."""
+        out = np.full((self.n_worlds, self.wc.slots), 255, np.uint8)
+        _check(lib().sim_get_policy_actions(self._h, _ptr(out)))
+        return out
 
     def step_log(self, first: int, n: int) -> np.ndarray:
         """Records of steps [first, first+n): structured array of shape [n, n_worlds]."""

@@ -128,3 +128,57 @@ def lockstep(world, orc: "oracle.OracleWorld", steps: int, check_weights_every: 
             n_ulp += compare_weights(gw, o["weights"], o["alive"] == 1, where=where)
     world.set_forced_actions(None)
     return flips, n_cmp, n_ulp
+
+
+def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights_every: int = 0, w: int = 0):
+    """The M2 + M3 protocol for network 1, whose actions are SAMPLED (R32):
+    every step the oracle takes the GPU's h, c, samples its own actions, the GPU is forced
+    to them; integer state and records bit-exact, floats within R27; and the GPU's OWN
+    sampled action of every agent alive at the step's start (sim_get_policy_actions) equals
+    the oracle's except where either side's sampling margin |u - CDF| is below 1e-4.
+    Returns (near_tie_disagreements, n_compared_agent_steps, one_ulp_weights)."""
+    from paper_2302_09334_b200.sim import STATE_FIELDS
+    fields = tuple(f for f in STATE_FIELDS if f != "weights")
+    seed = int(world.wc.seeds[w])
+    nw = world.n_worlds
+    flips = n_cmp = n_ulp = 0
+    for step in range(steps):
+        g0 = gpu_world_state(world.get_state(("h", "c", "alive")), w)
+        live0 = g0["alive"] == 1
+        orc.st["h"][live0] = g0["h"][live0]
+        orc.st["c"][live0] = g0["c"][live0]
+        alive_start = orc.st["alive"].copy() == 1
+        cells_start = orc.st["cell"].copy()
+        t = orc.t
+        orec = orc.step(return_actions=True)
+        assert orec["status"] == 0
+        acts = orec["actions"]
+        forced = np.full((nw, world.wc.slots), 255, np.uint8)
+        forced[w] = acts
+        world.set_forced_actions(forced)
+        world.step(1)
+        g = gpu_world_state(world.get_state(fields), w)
+        o = orc.st
+        where = f"step {orec['t']}"
+        compare_ints(g, {**o, "t": orc.t}, where)
+        compare_record(world.step_log(orec["t"], 1)[0, w], orec, where)
+        keep = alive_start & (o["alive"] == 1) & (o["age"] > 0)
+        slots = np.flatnonzero(keep)
+        if slots.size:
+            compare_floats(g, o, slots, where)
+        own = world.policy_actions()[w]
+        start = np.flatnonzero(alive_start)
+        dis = start[own[start] != acts[start]]
+        for i in dis:
+            if o["alive"][i] == 1 and o["age"][i] == 0:
+                continue  # died and its slot was reused by a newborn: the step's logits are gone
+            _, _, mo = oracle.sample_action(seed, t, int(cells_start[i]), o["logits"][i])
+            _, _, mg = oracle.sample_action(seed, t, int(cells_start[i]), g["logits"][i])
+            assert min(mo, mg) < 1e-4, f"{where}: unflagged sampling disagreement at slot {i} (margins {mo}, {mg})"
+        flips += int(dis.size)
+        n_cmp += int(start.size)
+        if check_weights_every and (step + 1) % check_weights_every == 0:
+            gw = world.get_state(("weights",))["weights"][w]
+            n_ulp += compare_weights(gw, o["weights"], o["alive"] == 1, where=where)
+    world.set_forced_actions(None)
+    return flips, n_cmp, n_ulp

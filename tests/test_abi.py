@@ -88,3 +88,19 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 for needle in ("import oracle", "from oracle", "liboracle", "orc_"):
                     assert needle not in src, f"{f} references the oracle ({needle})"
+
+
+def test_network1_validation_and_sizes():
+    """Network 1 (the paper's CNN-LSTM): 2445 parameters per slot, the
+    architecture fixes the window (r = 7) and the LSTM (4), banded mode is refused."""
+    wc = workloads.paper_world_cnn()
+    sim.validate(wc)
+    sz = sim.state_sizes(wc)
+    assert sz["params"] == 2445 and sz["hidden"] == 4
+    for kw, field in [(dict(obs_radius=3), "obs_radius"), (dict(hidden=8), "hidden"), (dict(network=2), "network")]:
+        with pytest.raises(sim.SimError) as ei:
+            sim.validate(wc.replace(**kw))
+        assert ei.value.status == sim.SIM_E_INVALID and field in str(ei.value)
+    with pytest.raises(sim.SimError) as ei:
+        sim.validate(wc, bands=dict(n_bands=2))
+    assert ei.value.status == sim.SIM_E_INVALID and "n_bands" in str(ei.value)
