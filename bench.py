@@ -56,7 +56,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "tiny", "large_world", "ensemble"))
+    ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "tiny", "large_world", "ensemble", "paper_world",
+                                                                   "paper_world_cnn"))
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -84,6 +85,9 @@ def workload(name: str, rank: int, world_size: int = 1) -> workloads.WorldConfig
         return workloads.tiny().replace(seeds=(rank,))
     if name == "large_world":
         return workloads.large_world().replace(seeds=(3 + rank,))
+    if name in ("paper_world", "paper_world_cnn"):  # the paper's own world (NEXT-1), its own agents (NEXT-2)
+        wc = getattr(workloads, name)()
+        return wc.replace(seeds=(wc.seeds[0] + rank,))
     return workloads.ensemble().replace(seeds=tuple(workloads.ensemble_shard(world_size, rank)))
 
 
@@ -191,6 +195,10 @@ def policy_bytes(wc, agents: int, nnz: int, split: bool = None) -> int:
     columns of active inputs, W_out, b_out, h and c read+written, 32 B of SoA fields and
     claims per agent, and either W_hh and b (unsplit) or the agent's P row (split)."""
     Hd = wc.hidden
+    if getattr(wc, "network", 0) == 1:
+        # the paper's CNN-LSTM (k_policy_cnn): every agent reads its whole parameter row
+        # (2445 floats), h and c read and written, 32 B of SoA fields and the claim
+        return agents * (4 * wc.n_params + 16 * Hd + 32)
     split = split_policy(wc) if split is None else split
     rec = 4 * 4 * Hd if split else 4 * (4 * Hd * Hd + 4 * Hd)
     per_agent_fixed = rec + 4 * (5 * Hd + 5) + 16 * Hd + 32
@@ -225,7 +233,10 @@ def workload_config(wc, args, world_size: int, sharded: bool, t0: int) -> dict:
     """The `config` object of both arms' JSON lines (the same workload, the same dict)."""
     return {"workload": f"{wc.name} (BASELINE.json configs[1])" if args.config == "paper_scale" else wc.name,
             "grid": f"{wc.rows}x{wc.cols}", "slots": wc.slots, "n_initial": wc.n_initial,
-            "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x2", "hidden": wc.hidden,
+            "obs": f"{2 * wc.obs_radius + 1}x{2 * wc.obs_radius + 1}x{3 if getattr(wc, 'network', 0) else 2}",
+            "hidden": wc.hidden,
+            "network": "paper CNN-LSTM, sampled (PAPER.md:346-350)" if getattr(wc, "network", 0)
+            else "LSTM + linear head, argmax",
             "seed": int(wc.seeds[0]), "n_worlds": wc.n_worlds, "timed_steps": [t0, t0 + args.steps],
             "parallelism": (f"agent-sharded: one world over {world_size} GPUs (policy by slot owner, "
                             "dynamics on every rank, NCCL SUM-allreduce of the move records per step)")
@@ -400,7 +411,10 @@ def run_ours(args, rank, world_size, local_rank):
             gk = kern["graph_kernel_ms_total"]
             gstep = gk["policy"] + gk["post"]
             cands = {
-                "policy": ("k_policy_half (observe + LSTM gates from P + argmax + move claim)",
+                "policy": (("k_policy_cnn (15x15x3 window + the paper's CNN-LSTM + softmax sampling + move claim)"
+                            if getattr(wc, "network", 0) else
+                            "k_policy_half (observe + LSTM gates from P + argmax + move claim)" if wc.hidden == 32 else
+                            f"k_policy_reg<{wc.hidden}> (observe + LSTM + argmax + move claim)"),
                            policy_bytes(wc, agents, nnz), gk["policy"], gstep),
                 "post": ("k_post (move/consume/physiology/death, birth claims + rank + placement, regrowth, "
                          "mutation; P rows of the next step on 4 warps per block)",

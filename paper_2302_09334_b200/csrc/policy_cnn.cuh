@@ -29,21 +29,34 @@ constexpr int CNN_WO = 15, CNN_R = 7;
 constexpr int CN_C1W = 0, CN_C1B = 108, CN_C2W = 112, CN_C2B = 400, CN_WIH = 408, CN_WHH = 1656, CN_B = 1720,
               CN_WD = 1736, CN_BD = 2392, CN_WO = 2400, CN_BO = 2440, CN_P = 2445;
 static_assert(CN_BO + 5 == CN_P && CN_P <= CNN_PD && CNN_PD % 32 == 0, "network-1 layout");
-// per-warp shared memory (floats): weights, conv1 out (8x8x4), pool1 (7x7x4), conv2 out
-// (4x4x8), e ++ h' (78 + 4, padded), window rows (R rows 0..14, O rows 16..30)
-constexpr int CS_W = 0, CS_A1 = CNN_PD, CS_P1 = CS_A1 + 256, CS_A2 = CS_P1 + 196, CS_E = CS_A2 + 128,
-              CS_ROWS = CS_E + 96, CS_TOTAL = CS_ROWS + 32;
-static_assert(CS_TOTAL % 4 == 0, "16-B aligned warp slices");
-constexpr int CNN_SMEM = CNN_WARPS * CS_TOTAL * 4;
+// per-warp shared memory: the weights (floats), then fp64 tiles: conv1 out (8x8x4), pool1
+// (7x7x4), conv2 out (4x4x8), e ++ h' (78 + 4, padded); window rows (R rows 0..14, O rows
+// 16..30) as words
+constexpr int CS_W_BYTES = CNN_PD * 4;
+constexpr int CS_A1 = 0, CS_P1 = CS_A1 + 256, CS_A2 = CS_P1 + 196, CS_E = CS_A2 + 128, CS_D_END = CS_E + 84;  // doubles
+constexpr int CS_ROWS_BYTES = 32 * 4;
+constexpr int CS_TOTAL_BYTES = CS_W_BYTES + CS_D_END * 8 + CS_ROWS_BYTES;
+static_assert(CS_W_BYTES % 16 == 0 && CS_TOTAL_BYTES % 16 == 0, "16-B aligned warp slices");
+constexpr int CNN_SMEM = CNN_WARPS * CS_TOTAL_BYTES;
 
+__device__ __forceinline__ double sigmoid_d(double z) { return 1.0 / (1.0 + exp(-z)); }
+
+// Arithmetic: every sum, pool, gate and activation in fp64 from the fp32 weights and
+// inputs (the oracle's precision; B200's FP64 units make this ~4k fp64 FMAs per agent
+// cheap beside the weight stream), h', c' and the logits rounded to fp32 once for storage,
+// the softmax and sampling in fp64 from the fp32 logits.  Only the summation order differs
+// from the oracle's, so the stored values agree to about one fp32 rounding even for
+// weights far larger than the paper's.
 __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
-    extern __shared__ __align__(16) float cnn_smem[];
+    extern __shared__ __align__(16) unsigned char cnn_smem_raw[];
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    float *sw = cnn_smem + wib * CS_TOTAL;
-    float *a1 = sw + CS_A1, *p1 = sw + CS_P1, *a2 = sw + CS_A2, *e = sw + CS_E;
-    uint32_t *rows = reinterpret_cast<uint32_t *>(sw + CS_ROWS);
+    unsigned char *base = cnn_smem_raw + (size_t)wib * CS_TOTAL_BYTES;
+    float *sw = reinterpret_cast<float *>(base);
+    double *sd = reinterpret_cast<double *>(base + CS_W_BYTES);
+    double *a1 = sd + CS_A1, *p1 = sd + CS_P1, *a2 = sd + CS_A2, *e = sd + CS_E;
+    uint32_t *rows = reinterpret_cast<uint32_t *>(base + CS_W_BYTES + CS_D_END * 8);
     step_housekeeping(p);
     PolicyCounters ctr;
     const long total = (long)p.n_worlds * p.S;
@@ -82,9 +95,9 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
             const int pos = lane + 32 * half, oy = pos >> 3, ox = pos & 7;
-            float acc[4];
+            double acc[4];
 #pragma unroll
-            for (int f = 0; f < 4; ++f) acc[f] = sw[CN_C1B + f];
+            for (int f = 0; f < 4; ++f) acc[f] = (double)sw[CN_C1B + f];
 #pragma unroll
             for (int ky = 0; ky < 3; ++ky) {
                 const int iy = 2 * oy + ky - 1;
@@ -97,31 +110,32 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
                     if (ix < 0 || ix >= CNN_WO) continue;
                     const bool r = (rb >> ix) & 1u, o = (ob >> ix) & 1u;
                     const bool wall = !(row_on && (x - CNN_R + ix) >= 0 && (x - CNN_R + ix) < p.W);
-                    const float *wk = sw + CN_C1W + (ky * 3 + kx) * 3;  // + f * 27
+                    const float *wk = sw + CN_C1W + (ky * 3 + kx) * 3;  // + f * 27 + channel
 #pragma unroll
                     for (int f = 0; f < 4; ++f) {
-                        if (r) acc[f] += wk[f * 27 + 0];
-                        if (o) acc[f] += wk[f * 27 + 1];
-                        if (wall) acc[f] += wk[f * 27 + 2];
+                        if (r) acc[f] += (double)wk[f * 27 + 0];
+                        if (o) acc[f] += (double)wk[f * 27 + 1];
+                        if (wall) acc[f] += (double)wk[f * 27 + 2];
                     }
                 }
             }
-            *reinterpret_cast<float4 *>(a1 + pos * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) a1[pos * 4 + f] = acc[f];
         }
         __syncwarp();
         // (4) pool1 -> 7x7x4 (196 values)
         for (int idx = lane; idx < 196; idx += 32) {
             const int py = idx / 28, rem = idx - py * 28, px = rem >> 2, f = rem & 3;
-            const float *b0 = a1 + (py * 8 + px) * 4 + f;
-            p1[idx] = (((b0[0] + b0[4]) + b0[32]) + b0[36]) * 0.25f;
+            const double *b0 = a1 + (py * 8 + px) * 4 + f;
+            p1[idx] = (((b0[0] + b0[4]) + b0[32]) + b0[36]) / 4.0;
         }
         __syncwarp();
         // (5) conv2: lane -> output position lane >> 1 (4x4), features 4 (lane & 1) .. + 3
         {
             const int q = lane >> 1, oy = q >> 2, ox = q & 3, g0 = (lane & 1) * 4;
-            float acc[4];
+            double acc[4];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) acc[g] = sw[CN_C2B + g0 + g];
+            for (int g = 0; g < 4; ++g) acc[g] = (double)sw[CN_C2B + g0 + g];
 #pragma unroll
             for (int ky = 0; ky < 3; ++ky) {
                 const int iy = 2 * oy + ky - 1;
@@ -130,83 +144,86 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
                 for (int kx = 0; kx < 3; ++kx) {
                     const int ix = 2 * ox + kx - 1;
                     if (ix < 0 || ix >= 7) continue;
-                    const float4 in = *reinterpret_cast<const float4 *>(p1 + (iy * 7 + ix) * 4);
+                    const double *in = p1 + (iy * 7 + ix) * 4;
+                    const double i0 = in[0], i1 = in[1], i2 = in[2], i3 = in[3];
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         const float4 wk = *reinterpret_cast<const float4 *>(
                             sw + CN_C2W + ((g0 + g) * 9 + ky * 3 + kx) * 4);
-                        acc[g] = fmaf(wk.x, in.x, acc[g]);
-                        acc[g] = fmaf(wk.y, in.y, acc[g]);
-                        acc[g] = fmaf(wk.z, in.z, acc[g]);
-                        acc[g] = fmaf(wk.w, in.w, acc[g]);
+                        acc[g] = fma((double)wk.x, i0, acc[g]);
+                        acc[g] = fma((double)wk.y, i1, acc[g]);
+                        acc[g] = fma((double)wk.z, i2, acc[g]);
+                        acc[g] = fma((double)wk.w, i3, acc[g]);
                     }
                 }
             }
-            *reinterpret_cast<float4 *>(a2 + q * 8 + g0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) a2[q * 8 + g0 + g] = acc[g];
         }
         __syncwarp();
         // (6) pool2 -> e[0..72); e[72..77) one-hot previous action, e[77] ate
         for (int idx = lane; idx < 72; idx += 32) {
             const int py = idx / 24, rem = idx - py * 24, px = rem >> 3, g = rem & 7;
-            const float *b0 = a2 + (py * 4 + px) * 8 + g;
-            e[idx] = (((b0[0] + b0[8]) + b0[32]) + b0[40]) * 0.25f;
+            const double *b0 = a2 + (py * 4 + px) * 8 + g;
+            e[idx] = (((b0[0] + b0[8]) + b0[32]) + b0[40]) / 4.0;
         }
-        if (lane < 5) e[72 + lane] = lane == last ? 1.f : 0.f;
-        if (lane == 5) e[77] = ate ? 1.f : 0.f;
+        if (lane < 5) e[72 + lane] = lane == last ? 1.0 : 0.0;
+        if (lane == 5) e[77] = ate ? 1.0 : 0.0;
         __syncwarp();
         // (7) LSTM gate rows: lane -> row lane >> 1; the even lane sums e[0..41), the odd
         // lane e[41..78) and W_hh h
-        float z;
+        double z;
         {
-            float hb[4];
+            double hb[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) hb[k] = __shfl_sync(FULL, hold, k);
+            for (int k = 0; k < 4; ++k) hb[k] = (double)__shfl_sync(FULL, hold, k);
             const int r = lane >> 1;
             const bool odd = lane & 1;
             const float *wr = sw + CN_WIH + r * 78;
-            float s = 0.f;
+            double s = 0.0;
             const int jb = odd ? 41 : 0, je = odd ? 78 : 41;
-            for (int j = jb; j < je; ++j) s = fmaf(wr[j], e[j], s);
+            for (int j = jb; j < je; ++j) s = fma((double)wr[j], e[j], s);
             if (odd) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s = fmaf(sw[CN_WHH + r * 4 + k], hb[k], s);
+                for (int k = 0; k < 4; ++k) s = fma((double)sw[CN_WHH + r * 4 + k], hb[k], s);
             }
             s += __shfl_xor_sync(FULL, s, 1);
-            z = s + sw[CN_B + r];
+            z = s + (double)sw[CN_B + r];
         }
         // unit k = lane & 3 on every lane: i = row k, f = 4 + k, g = 8 + k, o = 12 + k
         const int k = lane & 3;
-        const float zi = __shfl_sync(FULL, z, 2 * k), zf = __shfl_sync(FULL, z, 2 * (4 + k));
-        const float zg = __shfl_sync(FULL, z, 2 * (8 + k)), zo = __shfl_sync(FULL, z, 2 * (12 + k));
-        const float ck = __shfl_sync(FULL, cold, k);
-        const float cn = sigmoidf_acc(zf) * ck + sigmoidf_acc(zi) * tanhf(zg);
-        const float hn = sigmoidf_acc(zo) * tanhf(cn);
+        const double zi = __shfl_sync(FULL, z, 2 * k), zf = __shfl_sync(FULL, z, 2 * (4 + k));
+        const double zg = __shfl_sync(FULL, z, 2 * (8 + k)), zo = __shfl_sync(FULL, z, 2 * (12 + k));
+        const double ck = (double)__shfl_sync(FULL, cold, k);
+        const double cnd = sigmoid_d(zf) * ck + sigmoid_d(zi) * tanh(zg);
+        const float cn = (float)cnd;
+        const float hn = (float)(sigmoid_d(zo) * tanh(cnd));
         if (lane < 4) {
             p.h[gs * 4 + lane] = hn;
             p.c[gs * 4 + lane] = cn;
-            e[78 + lane] = hn;  // "we concatenate the embedding with the output of the LSTM"
+            e[78 + lane] = (double)hn;  // "we concatenate the embedding with the output of the LSTM"
         }
         bool bad = !isfinite(hn) || !isfinite(cn);
         __syncwarp();
         // (8) dense 82 -> 8 with tanh: lane -> row lane >> 2, inputs [21 (lane & 3), + 21)
-        float dv;
+        double dv;
         {
             const int r = lane >> 2, j0 = (lane & 3) * 21, j1 = j0 + 21 < 82 ? j0 + 21 : 82;
             const float *wr = sw + CN_WD + r * 82;
-            float s = 0.f;
-            for (int j = j0; j < j1; ++j) s = fmaf(wr[j], e[j], s);
+            double s = 0.0;
+            for (int j = j0; j < j1; ++j) s = fma((double)wr[j], e[j], s);
             s += __shfl_xor_sync(FULL, s, 1);
             s += __shfl_xor_sync(FULL, s, 2);
-            dv = tanhf(s + sw[CN_BD + r]);
+            dv = tanh(s + (double)sw[CN_BD + r]);
         }
         // (9) dense 8 -> 5 logits: lane a < 5
-        float lgv = 0.f;
+        double lgd = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-            const float dk = __shfl_sync(FULL, dv, 4 * kk);
-            if (lane < 5) lgv = fmaf(sw[CN_WO + lane * 8 + kk], dk, lgv);
+            const double dk = __shfl_sync(FULL, dv, 4 * kk);
+            if (lane < 5) lgd = fma((double)sw[CN_WO + lane * 8 + kk], dk, lgd);
         }
-        if (lane < 5) lgv += sw[CN_BO + lane];
+        const float lgv = lane < 5 ? (float)(lgd + (double)sw[CN_BO + lane]) : 0.f;
         float lg[5];
 #pragma unroll
         for (int a = 0; a < 5; ++a) lg[a] = __shfl_sync(FULL, lgv, a);

@@ -130,12 +130,18 @@ def lockstep(world, orc: "oracle.OracleWorld", steps: int, check_weights_every: 
     return flips, n_cmp, n_ulp
 
 
-def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights_every: int = 0, w: int = 0):
+MAX_ULP_SEEN = {"h": 0, "c": 0, "logits": 0}
+
+
+def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights_every: int = 0, w: int = 0,
+                     max_ulp: int = 1):
     """The M2 + M3 protocol for network 1, whose actions are SAMPLED (R32):
     every step the oracle takes the GPU's h, c, samples its own actions, the GPU is forced
     to them; integer state and records bit-exact, floats within R27; and the GPU's OWN
     sampled action of every agent alive at the step's start (sim_get_policy_actions) equals
     the oracle's except where either side's sampling margin |u - CDF| is below 1e-4.
+    k_policy_cnn evaluates the network in fp64 like the oracle (only the summation order
+    differs), so beyond R27 its stored h', c' and logits must be within `max_ulp` fp32 ulps.
     Returns (near_tie_disagreements, n_compared_agent_steps, one_ulp_weights)."""
     from paper_2302_09334_b200.sim import STATE_FIELDS
     fields = tuple(f for f in STATE_FIELDS if f != "weights")
@@ -166,6 +172,10 @@ def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights
         slots = np.flatnonzero(keep)
         if slots.size:
             compare_floats(g, o, slots, where)
+            for f in ("h", "c", "logits"):
+                u = ulp_diff(g[f][slots], o[f][slots])
+                MAX_ULP_SEEN[f] = max(MAX_ULP_SEEN[f], int(u.max()))
+                assert u.max() <= max_ulp, f"{where}: {f} differs by {int(u.max())} ulp (fp64 evaluation on both sides)"
         own = world.policy_actions()[w]
         start = np.flatnonzero(alive_start)
         dis = start[own[start] != acts[start]]

@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 import workloads
-from harness import MAX_ABS_SEEN, compare_floats, compare_ints, compare_weights, gpu_world_state, lockstep_sampled
+from harness import MAX_ABS_SEEN, MAX_ULP_SEEN, compare_floats, compare_ints, compare_weights, gpu_world_state, lockstep_sampled
 
 pytestmark = pytest.mark.gpu
 
@@ -62,7 +62,7 @@ def test_cnn_one_step_random_states(seed, wstd, density):
     assert n == 220
     births = int(world.step_log(st["t"], 1)[0, 0]["births"])
     print(f"one step: {n} agents, {births} births, {flips} flagged flips, {nulp} 1-ulp weights, "
-          f"max |d| {MAX_ABS_SEEN}")
+          f"max |d| {MAX_ABS_SEEN}, max ulp {MAX_ULP_SEEN}")
     assert births > 0
     world.destroy()
 
@@ -76,7 +76,7 @@ def test_cnn_lockstep_small_world_300_steps():
     flips, n, nulp = lockstep_sampled(world, orc, 300, check_weights_every=50)
     log = world.step_log(0, 300)[:, 0]
     print(f"cnn small world: {n} agent-steps, births {int(log['births'].sum())}, wall deaths "
-          f"{int(log['deaths_wall'].sum())}, {flips} flagged flips, {nulp} 1-ulp weights")
+          f"{int(log['deaths_wall'].sum())}, {flips} flagged flips, {nulp} 1-ulp weights, max ulp {MAX_ULP_SEEN}")
     assert int(log["births"].sum()) > 0 and int(log["deaths_wall"].sum()) > 0
     world.destroy()
 

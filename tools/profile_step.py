@@ -19,7 +19,8 @@ from paper_2302_09334_b200 import sim  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--warmup", type=int, default=3000)
-ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "large_world", "ensemble"))
+ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "large_world", "ensemble", "paper_world",
+                                                                 "paper_world_cnn"))
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 wc = getattr(workloads, a.config)()
