@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
         const int64_t t = p.t[w];
         if (i >= *count_of(p, t, w)) continue;
         const int slot = list_of(p, t, w)[i];
+        ECO_CHECK(slot >= 0 && slot < p.S);
         const size_t gs = (size_t)w * p.S + slot;
         // (1) the agent's parameters -> shared memory (616 x 16 B), in flight during (2)
         const float *Wg = p.weights + gs * (size_t)CNN_PD;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
         cp_commit();
         // (2) the window: lane l < 15 fetches R' row l, lane 16 + l fetches O_t row l
         const int cellv = p.cell[gs];
+        ECO_CHECK(cellv >= 0 && cellv < p.H * p.W);
         const int y = row_of(p, cellv), x = cellv - y * p.W;
         {
             const int rr = lane & 15;
