@@ -958,12 +958,16 @@ constexpr int POST_THREADS = ECO_POST_THREADS;
 #endif
 constexpr int CLAIMS_BLOCK_MAX = ECO_CLAIMS_MAX;
 #ifndef ECO_HH_DEPTH
-#define ECO_HH_DEPTH 8  // split: 512-B chunks in flight per P context
+#define ECO_HH_DEPTH 8  // split: 512-B chunks in flight per P context (<= 33: W_hh rows + b)
 #endif
-constexpr int HH_DEPTH = ECO_HH_DEPTH;
-constexpr int HH_WARPS_MAX = ECO_HH_WARPS > ECO_HH_WARPS_BIG ? ECO_HH_WARPS : ECO_HH_WARPS_BIG;
-constexpr int POST_SMEM = 2 * HH_WARPS_MAX * HH_DEPTH * 32 * 16;        // split: the P rings (max)
-constexpr int POST_SMEM_SMALL = 2 * ECO_HH_WARPS * HH_DEPTH * 32 * 16;  // worlds that never exceed the threshold
+#ifndef ECO_HH_DEPTH_BIG
+#define ECO_HH_DEPTH_BIG 8  // ... in the many-slot variant
+#endif
+constexpr int HH_DEPTH = ECO_HH_DEPTH, HH_DEPTH_BIG = ECO_HH_DEPTH_BIG;
+static_assert(HH_DEPTH <= 33 && HH_DEPTH_BIG <= 33, "a P context streams 33 chunks");
+constexpr int HH_RING_SMALL = 2 * ECO_HH_WARPS * HH_DEPTH * 32 * 16, HH_RING_BIG = 2 * ECO_HH_WARPS_BIG * HH_DEPTH_BIG * 32 * 16;
+constexpr int POST_SMEM = HH_RING_SMALL > HH_RING_BIG ? HH_RING_SMALL : HH_RING_BIG;  // split: the P rings (max)
+constexpr int POST_SMEM_SMALL = HH_RING_SMALL;  // worlds that never exceed the threshold
 // worlds with more slots than the threshold run k_post<., true>: 16 P warps per block (the
 // P stream is the longer part of the step there: large world 1.71 -> 1.52 ms per step)
 inline bool post_big(const DevParams &p) { return p.split && p.S > ECO_HH_BIG_AGENTS; }
@@ -1045,7 +1049,8 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         // (sharded: this rank's own agents only)
         const int32_t *hl_ = SHARD ? p.own_list + (size_t)(T & 1) * p.S : list_of(p, T, 0);
         const int hn_ = SHARD ? p.own_count[T & 1] : *count_of(p, T, 0);
-        hh_pass<HH_DEPTH>(p, hl_, hn_, ag * (int)nb + (int)b, (int)nb * HH_WARPS * 2, post_smem + (ag * HH_DEPTH) * 32);
+        constexpr int DEPTH = BIG ? HH_DEPTH_BIG : HH_DEPTH;
+        hh_pass<DEPTH>(p, hl_, hn_, ag * (int)nb + (int)b, (int)nb * HH_WARPS * 2, post_smem + (ag * DEPTH) * 32);
         END_CLOCK(1);
 #ifdef ECO_TIMELINE
         if (lane == 0) timeline_mark(p, 3, globaltimer_ns(), T);
