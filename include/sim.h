@@ -113,7 +113,7 @@ typedef struct {
      *      walls = off the grid), conv 3x3/2 SAME (4) -> avgpool 2/1 -> conv 3x3/2 SAME (8)
      *      -> avgpool 2/1 -> 72 ++ one-hot previous action (5) ++ ate (1) = 78 -> LSTM(4) ->
      *      [78 ++ h'] -> dense 8 tanh -> dense 5 -> softmax(50 logits), the action SAMPLED by
-     *      inverse CDF with the Philox word (ACTION = 8, t, cell) (R32-R36);
+     *      inverse CDF with the Philox word (ACTION = 8, t, cell) (R38-R42);
      *      requires obs_radius = 7, hidden = 4 and n_bands <= 1; 2445 parameters.        */
     int32_t network;
 } sim_config;

@@ -280,7 +280,7 @@ int orc_policy(const orc_config *cfg, const float *w, const double *x, const flo
 /* "An agent observes pixel values ... within its visual range (a square of size
  * [w_o, w_o] centered around the agent)"; "The pixel values contain information about the
  * resources, other agents (including their number) and walls"; w_o = 15
- * (PAPER.md:317).  Three channels (R33): resources after regrowth, agents at step start
+ * (PAPER.md:317).  Three channels (R39): resources after regrowth, agents at step start
  * incl. self (0/1 under exclusive occupancy), walls = every cell off the grid. */
 void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O, int32_t y,
                        int32_t x, double *xout) {
@@ -296,7 +296,7 @@ void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O
         }
 }
 
-/* "First CNN has a kernel size (3,3), stride 2": SAME zero padding (R34),
+/* "First CNN has a kernel size (3,3), stride 2": SAME zero padding (R40),
  * out = ceil(n/2) with total padding 2(out-1) + 3 - n, its floor half before. */
 void orc_conv3x3_s2_same(const double *in, int32_t H, int32_t W, int32_t cin, const float *w,
                          const float *b, int32_t cout, double *out) {
@@ -318,7 +318,7 @@ void orc_conv3x3_s2_same(const double *in, int32_t H, int32_t W, int32_t cin, co
             }
 }
 
-/* "average pooling of size (2,2) and stride 1", VALID (R34) */
+/* "average pooling of size (2,2) and stride 1", VALID (R40) */
 void orc_avgpool2_s1(const double *in, int32_t H, int32_t W, int32_t C, double *out) {
     for (int32_t y = 0; y + 1 < H; ++y)
         for (int32_t x = 0; x + 1 < W; ++x)
@@ -332,7 +332,7 @@ void orc_avgpool2_s1(const double *in, int32_t H, int32_t W, int32_t C, double *
 
 /* CNN -> flatten (72) ++ previous action (one-hot 5) ++ ate (1) = e (78);
  * LSTM(4) on e; [e, h'] (82) -> dense 8 tanh -> dense 5 = logits.  No activation after
- * the convolutions (R35); the LSTM gates as network 0 (i,f,g,o, one bias, R12). */
+ * the convolutions (R41); the LSTM gates as network 0 (i,f,g,o, one bias, R12). */
 int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int32_t last_action,
                    int32_t ate, const float *h, const float *c, float *h_out, float *c_out,
                    float *logits_out, double *emb_out) {
@@ -384,7 +384,7 @@ int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int
 /* "a last denser layer of size 5 ... with softmax to get the action probability from which
  * the action will be sampled.  The softmax we use has a low temperature (1/50)"
  * (PAPER.md:348): P_a = exp(50 l_a) / sum_b exp(50 l_b) from the fp32 logits; inverse-CDF
- * sampling with one Philox word keyed by the agent's cell (R32). */
+ * sampling with one Philox word keyed by the agent's cell (R38). */
 int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const float *logits,
                           double *probs_out, double *margin) {
     double m = -INFINITY, p[5], S = 0.0;

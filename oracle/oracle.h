@@ -105,7 +105,7 @@ typedef struct {
     int64_t deferred_no_cell, deferred_claim, deferred_capacity;
     int64_t population, resources; /* after the step */
     int64_t near_ties;              /* live agents with top1-top2 logit margin < 1e-4 (network 1:
-                                       the sampling margin < 1e-4, R32) */
+                                       the sampling margin < 1e-4, R38) */
     int64_t deaths_wall;            /* agents killed by a move off the grid (lethal walls) */
 } orc_record;
 
@@ -161,7 +161,7 @@ int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int
                    float *logits_out, double *emb_out);
 /* softmax(50 * logits) sampled with u = draw(ACTION, step, cell)[0] * 2^-32: the least a
  * with u < P_0 + ... + P_a (4 if none); *margin = min over the 4 inner boundaries of
- * |u - (P_0 + ... + P_k)| (a near-tie below 1e-4, R32); probs_out (may be NULL) [5] */
+ * |u - (P_0 + ... + P_k)| (a near-tie below 1e-4, R38); probs_out (may be NULL) [5] */
 int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const float *logits,
                           double *probs_out, double *margin);
 

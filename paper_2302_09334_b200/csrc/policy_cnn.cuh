@@ -4,14 +4,14 @@
 //
 //   window   15x15x3: resources R' after regrowth, agents O_t (incl.
 //            self), walls = off the grid; HWC
-//   conv1    3x3, stride 2, SAME (pad 1): 15x15x3 -> 8x8x4      (no activation, R35)
+//   conv1    3x3, stride 2, SAME (pad 1): 15x15x3 -> 8x8x4      (no activation, R41)
 //   pool1    2x2 average, stride 1, VALID: -> 7x7x4
 //   conv2    3x3, stride 2, SAME (pad 1): -> 4x4x8
 //   pool2    -> 3x3x8 = 72; e = [72, one-hot previous action (5), ate (1)] = 78
 //   LSTM(4)  z = W_ih e + W_hh h + b, gates (i, f, g, o)
 //   dense    [e, h'] (82) -> 8, tanh; dense 8 -> 5 logits
 //   action   softmax(50 logits) sampled by inverse CDF with u = draw(ACTION, t, cell).x 2^-32
-//            (R32), in fp64 from the fp32 logits; near-tie when |u - CDF| < 1e-4
+//            (R38), in fp64 from the fp32 logits; near-tie when |u - CDF| < 1e-4
 //
 // One WARP per agent (2,445 parameters, 13.5 k multiply-adds: a per-agent network is a
 // batched GEMV-like chain of tiny layers with different weights per agent, no dense
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
         const unsigned seen = __reduce_or_sync(FULL, rbits);
         bad = __any_sync(FULL, bad);
         if (lane == 0) {
-            // (10) softmax(50 logits) sampled by inverse CDF (fp64 from the fp32 logits, R32)
+            // (10) softmax(50 logits) sampled by inverse CDF (fp64 from the fp32 logits, R38)
             double zmax = -INFINITY;
 #pragma unroll
             for (int a = 0; a < 5; ++a) {

@@ -45,7 +45,7 @@ namespace eco {
 
 constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
                    PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7,
-                   PURPOSE_ACTION = 8;  // the sampled action of network 1 (R32)
+                   PURPOSE_ACTION = 8;  // the sampled action of network 1 (R38)
 constexpr int LOGIT_STRIDE = 8;
 constexpr uint8_t NO_DIR = 0xFF;
 

@@ -135,7 +135,7 @@ MAX_ULP_SEEN = {"h": 0, "c": 0, "logits": 0}
 
 def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights_every: int = 0, w: int = 0,
                      max_ulp: int = 1):
-    """The M2 + M3 protocol for network 1, whose actions are SAMPLED (R32):
+    """The M2 + M3 protocol for network 1, whose actions are SAMPLED (R38):
     every step the oracle takes the GPU's h, c, samples its own actions, the GPU is forced
     to them; integer state and records bit-exact, floats within R27; and the GPU's OWN
     sampled action of every agent alive at the step's start (sim_get_policy_actions) equals

@@ -3,7 +3,7 @@ SURVEY.md §8(f) NEXT-2; k_policy_cnn) against the oracle, through the C ABI.
 
 Integer state, step records and slot layout bit-exact; h', c', logits within R27; weights
 bit-exact up to counted 1-ulp differences (R29); the kernel's own sampled actions
-(sim_get_policy_actions) equal the oracle's except at flagged sampling near-ties (R32).
+(sim_get_policy_actions) equal the oracle's except at flagged sampling near-ties (R38).
 """
 import numpy as np
 import pytest

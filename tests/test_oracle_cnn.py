@@ -1,5 +1,5 @@
 """Pins of the oracle's network 1, the paper's CNN-LSTM with softmax sampling
-(App. B.5; R32-R36).
+(App. B.5; R38-R42).
 
 What fixes it from outside the oracle:
   * the paper's parameter count, 2445, and SPEC's per-layer audit
