@@ -23,7 +23,7 @@ _lock = threading.Lock()
 _lib = None
 
 OK, E_INVALID, E_NONFINITE = 0, -1, -5
-P_INIT_RES, P_INIT_PLACE, P_INIT_W, P_REGROW, P_MOVE, P_BIRTH, P_MUTATE, P_ACTION = 1, 2, 3, 4, 5, 6, 7, 8
+P_INIT_RES, P_INIT_PLACE, P_INIT_W, P_REGROW, P_MOVE, P_BIRTH, P_MUTATE, P_ACTION, P_CONSUME = range(1, 10)
 
 
 def build(force: bool = False) -> str:
@@ -57,7 +57,7 @@ class Config(ctypes.Structure):
         ("e_repr_gt", ctypes.c_int32), ("e_death_le", ctypes.c_int32), ("e_max", ctypes.c_int32),
         ("repr_steps", ctypes.c_int32), ("max_age", ctypes.c_int32),
         ("climate_alpha", ctypes.c_double), ("death_steps", ctypes.c_int32), ("lethal_walls", ctypes.c_int32),
-        ("network", ctypes.c_int32),
+        ("network", ctypes.c_int32), ("colocate", ctypes.c_int32),
     ]
 
 
@@ -161,6 +161,7 @@ def make_config(wc, world: int = 0) -> Config:
     c.death_steps = int(getattr(wc, "death_steps", 0))
     c.lethal_walls = int(getattr(wc, "lethal_walls", 0))
     c.network = int(getattr(wc, "network", 0))
+    c.colocate = int(getattr(wc, "colocate", 0))
     return c
 
 
@@ -254,9 +255,9 @@ def policy(wc, w: np.ndarray, x: np.ndarray, h: np.ndarray, c: np.ndarray):
 
 # ------------------------------------------- network 1: the paper's CNN-LSTM (NEXT-2)
 def observe_paper(wc, R: np.ndarray, O: np.ndarray, y: int, x: int) -> np.ndarray:
-    """The 15x15x3 window (HWC: resources, agents, walls) around (y, x)."""
+    """The 15x15x3 window (HWC: resources, agents, walls) around (y, x); O: agents per cell."""
     R = np.ascontiguousarray(R, np.uint8)
-    O = np.ascontiguousarray(O, np.uint8)
+    O = np.ascontiguousarray(O, np.int32)
     out = np.zeros((15, 15, 3), np.float64)
     lib().orc_observe_paper(ctypes.byref(make_config(wc)), _ptr(R), _ptr(O), y, x, _ptr(out))
     return out

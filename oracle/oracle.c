@@ -123,6 +123,8 @@ int orc_validate(const orc_config *cfg, char *msg, int msg_len) {
     if (cfg->slots < 0) return bad(msg, msg_len, "slots");
     if (cfg->n_initial < 0 || cfg->n_initial > cfg->slots) return bad(msg, msg_len, "n_initial");
     if (cfg->network != 0 && cfg->network != 1) return bad(msg, msg_len, "network");
+    if (cfg->colocate != 0 && cfg->colocate != 1) return bad(msg, msg_len, "colocate");
+    if (cfg->colocate && cfg->network != 1) return bad(msg, msg_len, "colocate"); /* (network 1 only) */
     if (cfg->network == 1) { /* the paper's architecture fixes the window and the LSTM */
         if (cfg->obs_radius != (ORC_CNN_WO - 1) / 2) return bad(msg, msg_len, "obs_radius");
         if (cfg->hidden != ORC_CNN_HD) return bad(msg, msg_len, "hidden");
@@ -282,7 +284,7 @@ int orc_policy(const orc_config *cfg, const float *w, const double *x, const flo
  * resources, other agents (including their number) and walls"; w_o = 15
  * (PAPER.md:317).  Three channels (R39): resources after regrowth, agents at step start
  * incl. self (0/1 under exclusive occupancy), walls = every cell off the grid. */
-void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O, int32_t y,
+void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const int32_t *N, int32_t y,
                        int32_t x, double *xout) {
     const int32_t r = (ORC_CNN_WO - 1) / 2, H = cfg->rows, W = cfg->cols;
     for (int32_t row = 0; row < ORC_CNN_WO; ++row)
@@ -291,7 +293,7 @@ void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O
             int on = yy >= 0 && yy < H && xx >= 0 && xx < W;
             double *px = xout + ((size_t)row * ORC_CNN_WO + col) * ORC_CNN_CH;
             px[0] = on && R[yy * W + xx] ? 1.0 : 0.0;
-            px[1] = on && O[yy * W + xx] ? 1.0 : 0.0;
+            px[1] = on ? (double)N[yy * W + xx] : 0.0; /* "(including their number)" */
             px[2] = on ? 0.0 : 1.0;
         }
 }
@@ -385,7 +387,7 @@ int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int
  * the action will be sampled.  The softmax we use has a low temperature (1/50)"
  * (PAPER.md:348): P_a = exp(50 l_a) / sum_b exp(50 l_b) from the fp32 logits; inverse-CDF
  * sampling with one Philox word keyed by the agent's cell (R38). */
-int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const float *logits,
+int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t entity, const float *logits,
                           double *probs_out, double *margin) {
     double m = -INFINITY, p[5], S = 0.0;
     for (int a = 0; a < 5; ++a)
@@ -396,7 +398,7 @@ int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const flo
     }
     for (int a = 0; a < 5; ++a) p[a] /= S;
     uint32_t w4[4];
-    orc_draw4(seed, ORC_P_ACTION, step, cell, 0u, w4);
+    orc_draw4(seed, ORC_P_ACTION, step, entity, 0u, w4);
     const double u = (double)w4[0] * 2.3283064365386963e-10; /* [0, 1) */
     int32_t act = 4;
     double cum = 0.0, mg = INFINITY;
@@ -514,9 +516,13 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
     /* 1. REGROW */
     rec->grown = orc_regrow(cfg, st->t, st->resources, Rn);
 
-    /* O_t: cells holding a live agent at step start */
+    /* O_t: cells holding a live agent at step start; N_t: the number of agents per cell */
+    int32_t *N = (int32_t *)calloc((size_t)HW, sizeof(int32_t));
     for (int32_t i = 0; i < S; ++i)
-        if (st->alive[i]) O[st->cell[i]] = 1;
+        if (st->alive[i]) {
+            O[st->cell[i]] = 1;
+            N[st->cell[i]] += 1;
+        }
 
     /* 2-3. OBSERVE + POLICY */
     for (int32_t i = 0; i < S; ++i) {
@@ -527,10 +533,12 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
         double margin;
         int rc;
         if (cfg->network == 1) { /* the paper's CNN-LSTM, sampled */
-            orc_observe_paper(cfg, Rn, O, y, xx, x);
+            orc_observe_paper(cfg, Rn, N, y, xx, x);
             rc = orc_policy_cnn(cfg, st->weights + (size_t)i * P, x, st->last_action[i], st->ate[i],
                                 st->h + (size_t)i * Hd, st->c + (size_t)i * Hd, hn, cn, lg, NULL);
-            a = orc_sample_action(cfg->seed, t, (uint32_t)st->cell[i], lg, NULL, &margin);
+            /* keyed by the cell (unique under exclusive occupancy, R9) or by the slot (R47) */
+            a = orc_sample_action(cfg->seed, t, cfg->colocate ? (uint32_t)i : (uint32_t)st->cell[i], lg, NULL,
+                                  &margin);
         } else {
             orc_observe(cfg, Rn, O, y, xx, x);
             rc = orc_policy(cfg, st->weights + (size_t)i * P, x, st->h + (size_t)i * Hd,
@@ -559,6 +567,10 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
             continue;
         }
         int32_t tc = ty * W + tx;
+        if (cfg->colocate) { /* no collision exclusion (R43): every in-grid move succeeds */
+            target[i] = tc;
+            continue;
+        }
         if (O[tc]) continue;
         uint32_t w4[4];
         orc_draw4(cfg->seed, ORC_P_MOVE, t, (uint32_t)st->cell[i], 0u, w4);
@@ -567,7 +579,7 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
         if (key[i] > claim[tc]) claim[tc] = key[i];
     }
     for (int32_t i = 0; i < S; ++i)
-        if (target[i] >= 0 && claim[target[i]] == key[i]) st->cell[i] = target[i];
+        if (target[i] >= 0 && (cfg->colocate || claim[target[i]] == key[i])) st->cell[i] = target[i];
     /* wall deaths: before consumption, so such an agent neither eats nor ages; its age at
      * death counts the step (age + 1, as every death) */
     for (int32_t i = 0; i < S; ++i)
@@ -577,17 +589,43 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
             rec->deaths_wall++;
         }
 
-    /* 5. CONSUME ("if the agent consumes a resource") */
-    for (int32_t i = 0; i < S; ++i) {
-        if (!st->alive[i]) continue;
-        int32_t p = st->cell[i];
-        if (Rn[p]) {
-            Rn[p] = 0;
-            st->ate[i] = 1;
-            rec->eaten++;
-        } else {
-            st->ate[i] = 0;
+    /* 5. CONSUME ("if the agent consumes a resource").  Co-location (R45): the
+     * agents standing on a resource cell hold a lottery, the largest (CONSUME draw of the
+     * slot, -slot) key eats ("exactly one ... consumes"). */
+    if (cfg->colocate) {
+        uint64_t *ckey = (uint64_t *)calloc((size_t)HW, sizeof(uint64_t));
+        for (int32_t i = 0; i < S; ++i) {
+            key[i] = 0;
+            if (!st->alive[i] || !Rn[st->cell[i]]) continue;
+            uint32_t w4[4];
+            orc_draw4(cfg->seed, ORC_P_CONSUME, t, (uint32_t)i, 0u, w4);
+            key[i] = ((uint64_t)w4[0] << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)i);
+            if (key[i] > ckey[st->cell[i]]) ckey[st->cell[i]] = key[i];
         }
+        for (int32_t i = 0; i < S; ++i) {
+            if (!st->alive[i]) continue;
+            int32_t p = st->cell[i];
+            st->ate[i] = (key[i] != 0 && ckey[p] == key[i]) ? 1 : 0;
+        }
+        for (int32_t i = 0; i < S; ++i)
+            if (st->alive[i] && st->ate[i]) {
+                Rn[st->cell[i]] = 0;
+                rec->eaten++;
+            }
+        free(ckey);
+    } else {
+        for (int32_t i = 0; i < S; ++i) {
+            if (!st->alive[i]) continue;
+            int32_t p = st->cell[i];
+            if (Rn[p]) {
+                Rn[p] = 0;
+                st->ate[i] = 1;
+                rec->eaten++;
+            } else {
+                st->ate[i] = 0;
+            }
+        }
+
     }
 
     /* 6. PHYSIOLOGY (linear decrease, +1 per resource; R16, R17, R19) */
@@ -620,7 +658,50 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
         if (st->alive[i]) On[st->cell[i]] = 1; /* O'' */
 
     /* 8. REPRODUCE (R19-R22) */
-    {
+    if (cfg->colocate) {
+        /* co-location (R46): "the off-spring appears on the same cell as its parent"
+         * (PAPER.md:297); the eligible parents in ascending slot order take the free slots
+         * (alive == 0 after phase 7) in ascending order, the rest are deferred (capacity) */
+        int32_t *freelist = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
+        int32_t *elig = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
+        int32_t n_free = 0, n_el = 0;
+        for (int32_t i = 0; i < S; ++i) {
+            if (!st->alive[i]) freelist[n_free++] = i;
+            else if (st->repr[i] >= cfg->repr_steps) elig[n_el++] = i;
+        }
+        double *z = (double *)malloc(sizeof(double) * (size_t)P);
+        for (int32_t r = 0; r < n_el; ++r) {
+            int32_t par = elig[r];
+            if (r >= n_free) {
+                rec->deferred_capacity++;
+                continue;
+            }
+            int32_t ch = freelist[r], cc = st->cell[par];
+            st->alive[ch] = 1;
+            st->cell[ch] = cc;
+            st->energy[ch] = cfg->e_init;
+            st->age[ch] = 0;
+            st->repr[ch] = 0;
+            if (st->low) st->low[ch] = 0;
+            st->last_action[ch] = 0;
+            st->ate[ch] = 0;
+            for (int32_t k = 0; k < Hd; ++k) {
+                st->h[(size_t)ch * Hd + k] = 0.0f;
+                st->c[(size_t)ch * Hd + k] = 0.0f;
+            }
+            for (int32_t a = 0; a < A; ++a) st->logits[(size_t)ch * A + a] = 0.0f;
+            /* the noise keyed by the child's slot (R47: co-located children share a cell) */
+            orc_gauss(cfg->seed, ORC_P_MUTATE, t, (uint32_t)ch, P, z);
+            const float *wp = st->weights + (size_t)par * P;
+            float *wc = st->weights + (size_t)ch * P;
+            for (int32_t j = 0; j < P; ++j) wc[j] = wp[j] + (float)(cfg->mutation_std * z[j]);
+            st->repr[par] = 0;
+            rec->births++;
+        }
+        free(z);
+        free(elig);
+        free(freelist);
+    } else {
         static const int32_t BDY[4] = {-1, 1, 0, 0}; /* N, S, E, W */
         static const int32_t BDX[4] = {0, 0, 1, -1};
         int32_t *cand = (int32_t *)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
@@ -719,6 +800,7 @@ int orc_step(const orc_config *cfg, orc_state *st, const uint8_t *forced, uint8_
     for (int64_t c = 0; c < HW; ++c) rec->resources += st->resources[c];
     st->t += 1;
 
+    free(N);
     free(x);
     free(key);
     free(target);

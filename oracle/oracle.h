@@ -41,6 +41,7 @@ extern "C" {
 #define ORC_P_BIRTH 6u
 #define ORC_P_MUTATE 7u
 #define ORC_P_ACTION 8u  /* the sampled action of network 1 ("sampled") */
+#define ORC_P_CONSUME 9u /* co-location: the lottery among agents sharing a resource cell */
 
 /* network 1, the paper's CNN-LSTM: sizes */
 #define ORC_CNN_WO 15   /* field of view w_o = 15                        */
@@ -74,6 +75,11 @@ typedef struct {
      * (2r+1)^2 x 2 window (BASELINE); 1 = the paper's CNN-LSTM on a 15x15x3 window with
      * softmax(50 logits) sampling (obs_radius 7, hidden 4)            */
     int32_t network;
+    /* co-location (the paper's own reproduction; R43-R47), requires
+     * network 1: any number of agents per cell, moves never conflict, one agent per resource
+     * cell eats (a lottery), the offspring appears on its parent's cell; the
+     * agent channel counts agents; ACTION, CONSUME and MUTATE draws are keyed by slot     */
+    int32_t colocate;
 } orc_config;
 
 /* Canonical state; all buffers are owned by the caller. */
@@ -144,8 +150,9 @@ int orc_policy(const orc_config *cfg, const float *w, const double *x, const flo
 
 /* ---- network 1: the paper's CNN-LSTM, evaluated in fp64 ---- */
 /* 15x15x3 window, HWC (x[(row*15 + col)*3 + ch]), rows from the top: ch 0 resources
- * after regrowth, ch 1 agents at step start incl. self, ch 2 walls = 1 off the grid */
-void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const uint8_t *O, int32_t y,
+ * after regrowth, ch 1 the number of agents at step start incl. self (N: agents per cell),
+ * ch 2 walls = 1 off the grid */
+void orc_observe_paper(const orc_config *cfg, const uint8_t *R, const int32_t *N, int32_t y,
                        int32_t x, double *xout);
 /* 3x3 convolution, stride 2, SAME zero padding (out = ceil(n/2), pad 1 before), HWC in,
  * w[cout][3][3][cin], b[cout]; out[(oy*OW + ox)*cout + f] */
@@ -159,10 +166,11 @@ void orc_avgpool2_s1(const double *in, int32_t H, int32_t W, int32_t C, double *
 int orc_policy_cnn(const orc_config *cfg, const float *w, const double *obs, int32_t last_action,
                    int32_t ate, const float *h, const float *c, float *h_out, float *c_out,
                    float *logits_out, double *emb_out);
-/* softmax(50 * logits) sampled with u = draw(ACTION, step, cell)[0] * 2^-32: the least a
+/* softmax(50 * logits) sampled with u = draw(ACTION, step, entity)[0] * 2^-32 (entity = the
+ * agent's step-start cell, or its slot under co-location): the least a
  * with u < P_0 + ... + P_a (4 if none); *margin = min over the 4 inner boundaries of
  * |u - (P_0 + ... + P_k)| (a near-tie below 1e-4, R38); probs_out (may be NULL) [5] */
-int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t cell, const float *logits,
+int32_t orc_sample_action(uint64_t seed, uint32_t step, uint32_t entity, const float *logits,
                           double *probs_out, double *margin);
 
 /* initial world (C.2) */

@@ -51,6 +51,7 @@ class WorldConfig:
     death_steps: int = 0                     # > 0: the death timer T_death (else immediate death)
     lethal_walls: int = 0                    # 1: moving off the grid kills
     network: int = 0                         # 1: the paper's CNN-LSTM, sampled (NEXT-2; r 7, Hd 4)
+    colocate: int = 0                        # 1: co-location, offspring on the parent's cell (network 1)
     steps: int = 100                         # run length named by the config
     name: str = ""
 
@@ -117,6 +118,15 @@ def paper_world_cnn() -> WorldConfig:
     ++ previous action (5) ++ ate (1) -> LSTM(4) -> [78 ++ 4] -> dense 8 tanh -> dense 5 ->
     softmax(50 logits), sampled; 2445 parameters per agent."""
     return paper_world().replace(network=1, obs_radius=7, hidden=4, name="paper_world_cnn")
+
+
+def paper_world_coloc() -> WorldConfig:
+    """The paper's world, agents and reproduction (SURVEY.md §8(f) NEXT-1 complete, with
+    NEXT-2): paper_world_cnn() with co-location -- any number of agents per cell (the
+    agent channel counts them, "including their number"), no collision
+    exclusion, one agent per resource cell eats (a lottery), the offspring
+    appears on its parent's cell."""
+    return paper_world_cnn().replace(colocate=1, name="paper_world_coloc")
 
 
 def regrowth_micro(rows: int = 200, cols: int = 400) -> WorldConfig:
