@@ -116,6 +116,14 @@ typedef struct {
      *      inverse CDF with the Philox word (ACTION = 8, t, cell) (R38-R42);
      *      requires obs_radius = 7, hidden = 4 and n_bands <= 1; 2445 parameters.        */
     int32_t network;
+    /* Co-location (the paper's own reproduction; R43-R47;
+     * requires network 1): any number of agents per cell -- moves never conflict, the agent
+     * channel counts agents, the agents on a resource cell hold a lottery (the largest
+     * (CONSUME = 9 draw of the slot, -slot) key eats), the eligible parents in slot order
+     * take the free slots in order and "the off-spring appears on the same cell as its
+     * parent"; ACTION and MUTATE draws are keyed by slot.  0: exclusive
+     * occupancy (R14, R21).                                                             */
+    int32_t colocate;
 } sim_config;
 
 /* Canonical state, host buffers owned by the caller, layouts with the world index

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsim.so")
 SOURCES = ["api.cu", "world.cu", "step.cu", "band.cu"]
-HEADERS = ["sim_internal.cuh", "block_scan.cuh", "phases.cuh", "api_band.inc", "policy_cnn.cuh"]
+HEADERS = ["sim_internal.cuh", "block_scan.cuh", "phases.cuh", "api_band.inc", "policy_cnn.cuh", "coloc.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

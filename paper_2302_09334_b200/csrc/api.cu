@@ -48,6 +48,7 @@ struct Derived {
     int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, log_cap;
     int off_hh, off_b, off_out, off_bout;
     int net;    // 0: LSTM + linear head (argmax); 1: the paper's CNN-LSTM (sampled)
+    int coloc;  // 1: co-location (any number of agents per cell; network 1)
     size_t pw;  // words per plane per world
 };
 
@@ -81,6 +82,10 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
         if (cfg->hidden != 4) return fail(SIM_E_INVALID, "invalid field: hidden (network 1: 4)");
         if (cfg->n_bands > 1)
             return fail(SIM_E_INVALID, "invalid field: n_bands (network 1's 7-row window exceeds the bands' halo)");
+    }
+    if (cfg->colocate != 0 && cfg->colocate != 1) return fail(SIM_E_INVALID, "invalid field: colocate (0 or 1)");
+    if (cfg->colocate && cfg->network != 1) return fail(SIM_E_INVALID, "invalid field: colocate (needs network 1)");
+    if (cfg->network == 1) {
     } else {
         if (cfg->obs_radius < 0 || cfg->obs_radius > 3) return fail(SIM_E_INVALID, "invalid field: obs_radius (0..3)");
         if (!(cfg->hidden == 4 || cfg->hidden == 8 || cfg->hidden == 16 || cfg->hidden == 32))
@@ -114,6 +119,7 @@ sim_status validate_cfg(const sim_config *cfg, Derived *d) {
         d->off_bout = d->off_out + 5 * d->Hd;
         d->Pd = (d->off_bout + 5 + 31) / 32 * 32;
         d->net = cfg->network;
+        d->coloc = cfg->colocate;
         if (d->net == 1) {  // canonical order on the device too (sim.h), rows padded to 32 floats
             d->I = 15 * 15 * 3;
             d->P = 2445;
@@ -167,6 +173,7 @@ size_t device_bytes(const Derived &d) {
     b += nw * S * 8 + S + S * 16 + S * 8;   // birth candidates, owners, by-slot move records, own lists
     b += (size_t)d.log_cap * nw * sizeof(sim_step_record);
     b += nw * S * 8 + nw * (size_t)mv_windows(d.log_cap) * SIM_MOVE_BINS * 4;  // movement metrics
+    if (d.coloc) b += nw * HW * 4 + nw * ((S + 31) / 32) * 4;                    // agents per cell, eligible bits
     return b;
 }
 
@@ -502,6 +509,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     DevParams &p = h->p;
     p.H = d.H; p.W = d.W; p.WW = d.WW; p.S = d.S; p.SW = d.SW; p.Hd = d.Hd; p.I = d.I; p.P = d.P; p.Pd = d.Pd;
     p.net = d.net;
+    p.coloc = d.coloc;
     p.row_lo = band ? band->y0 : 0;
     p.row_hi = band ? band->y1 : d.H;
     p.regrow_split = 0;
@@ -600,6 +608,8 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     H(&p.owner, S ? S : 1);
     H(&p.mrec_slot, S ? S : 1);
     H(&p.own_list, S ? 2 * S : 1);
+    H(&p.ncount, d.coloc ? nw * HW : 1);              // co-location: agents per cell
+    H(&p.elig_bits, d.coloc ? nw * (size_t)d.SW : 1);  // co-location: eligible parents by slot
     H(&p.phase_ns, PHASE_WORDS);  // + per-block clocks / traces of diagnostic builds
     H(&h->live_dev, nw * S);
     H(&h->res_bytes, nw * HW);
@@ -934,7 +944,8 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
                 if (!alive[w * S + i]) continue;
                 const int32_t c = cell[w * S + i];
                 if (c < 0 || (size_t)c >= HW) return fail(SIM_E_INVALID, "invalid field: cell (out of range, world %zu slot %zu)", w, i);
-                if (seen[c]) return fail(SIM_E_INVALID, "invalid field: cell (two agents on cell %d, world %zu)", c, w);
+                if (seen[c] && !d.coloc)
+                    return fail(SIM_E_INVALID, "invalid field: cell (two agents on cell %d, world %zu)", c, w);
                 seen[c] = 1;
             }
         }

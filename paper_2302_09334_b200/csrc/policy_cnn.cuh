@@ -35,7 +35,8 @@ static_assert(CN_BO + 5 == CN_P && CN_P <= CNN_PD && CNN_PD % 32 == 0, "network-
 constexpr int CS_W_BYTES = CNN_PD * 4;
 constexpr int CS_A1 = 0, CS_P1 = CS_A1 + 256, CS_A2 = CS_P1 + 196, CS_E = CS_A2 + 128, CS_D_END = CS_E + 84;  // doubles
 constexpr int CS_ROWS_BYTES = 32 * 4;
-constexpr int CS_TOTAL_BYTES = CS_W_BYTES + CS_D_END * 8 + CS_ROWS_BYTES;
+constexpr int CS_CNT_BYTES = 228 * 4;  // the agent channel: agents per window cell (15 x 15)
+constexpr int CS_TOTAL_BYTES = CS_W_BYTES + CS_D_END * 8 + CS_ROWS_BYTES + CS_CNT_BYTES;
 static_assert(CS_W_BYTES % 16 == 0 && CS_TOTAL_BYTES % 16 == 0, "16-B aligned warp slices");
 constexpr int CNN_SMEM = CNN_WARPS * CS_TOTAL_BYTES;
 
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
     double *sd = reinterpret_cast<double *>(base + CS_W_BYTES);
     double *a1 = sd + CS_A1, *p1 = sd + CS_P1, *a2 = sd + CS_A2, *e = sd + CS_E;
     uint32_t *rows = reinterpret_cast<uint32_t *>(base + CS_W_BYTES + CS_D_END * 8);
+    int32_t *cnt = reinterpret_cast<int32_t *>(base + CS_W_BYTES + CS_D_END * 8 + CS_ROWS_BYTES);
     step_housekeeping(p);
     PolicyCounters ctr;
     const long total = (long)p.n_worlds * p.S;
@@ -91,6 +93,22 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
         const float hold = lane < 4 ? p.h[gs * 4 + lane] : 0.f;
         const float cold = lane < 4 ? p.c[gs * 4 + lane] : 0.f;
         const int last = p.last_action[gs], ate = p.ate[gs];
+        __syncwarp();
+        // the agent channel (R39, R44): agents per window cell -- the O bits (0/1) under
+        // exclusive occupancy, the per-cell counts under co-location
+        int occupied = 0;
+        for (int idx = lane; idx < CNN_WO * CNN_WO; idx += 32) {
+            const int row = idx / CNN_WO, col = idx - row * CNN_WO;
+            const int yy = y - CNN_R + row, xx = x - CNN_R + col;
+            int n = 0;
+            if (p.coloc) {
+                if (yy >= 0 && yy < p.H && xx >= 0 && xx < p.W) n = p.ncount[(size_t)w * p.H * p.W + (size_t)yy * p.W + xx];
+            } else {
+                n = (int)((rows[16 + row] >> col) & 1u);
+            }
+            cnt[idx] = n;
+            occupied += n > 0;
+        }
         cp_wait<0>();
         __syncwarp();
         // (3) conv1: positions lane and lane + 32 of the 8x8 output, 4 features each
@@ -104,19 +122,20 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
             for (int ky = 0; ky < 3; ++ky) {
                 const int iy = 2 * oy + ky - 1;
                 if (iy < 0 || iy >= CNN_WO) continue;  // conv zero padding
-                const uint32_t rb = rows[iy], ob = rows[16 + iy];
+                const uint32_t rb = rows[iy];
                 const bool row_on = (y - CNN_R + iy) >= 0 && (y - CNN_R + iy) < p.H;
 #pragma unroll
                 for (int kx = 0; kx < 3; ++kx) {
                     const int ix = 2 * ox + kx - 1;
                     if (ix < 0 || ix >= CNN_WO) continue;
-                    const bool r = (rb >> ix) & 1u, o = (ob >> ix) & 1u;
+                    const bool r = (rb >> ix) & 1u;
+                    const int o = cnt[iy * CNN_WO + ix];
                     const bool wall = !(row_on && (x - CNN_R + ix) >= 0 && (x - CNN_R + ix) < p.W);
                     const float *wk = sw + CN_C1W + (ky * 3 + kx) * 3;  // + f * 27 + channel
 #pragma unroll
                     for (int f = 0; f < 4; ++f) {
                         if (r) acc[f] += (double)wk[f * 27 + 0];
-                        if (o) acc[f] += (double)wk[f * 27 + 1];
+                        if (o) acc[f] = fma((double)o, (double)wk[f * 27 + 1], acc[f]);  // o * w exact
                         if (wall) acc[f] += (double)wk[f * 27 + 2];
                     }
                 }
@@ -230,8 +249,8 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
 #pragma unroll
         for (int a = 0; a < 5; ++a) lg[a] = __shfl_sync(FULL, lgv, a);
         // window counters: active inputs (R and O bits), a resource in view (greediness)
-        const uint32_t rbits = lane < CNN_WO ? rows[lane] : 0u, obits = lane >= 16 && lane < 16 + CNN_WO ? rows[lane] : 0u;
-        const unsigned nnz = __reduce_add_sync(FULL, (unsigned)(__popc(rbits) + __popc(obits)));
+        const uint32_t rbits = lane < CNN_WO ? rows[lane] : 0u;
+        const unsigned nnz = __reduce_add_sync(FULL, (unsigned)(__popc(rbits) + occupied));
         const unsigned seen = __reduce_or_sync(FULL, rbits);
         bad = __any_sync(FULL, bad);
         if (lane == 0) {
@@ -249,7 +268,8 @@ __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
                 pr[a] = exp(50.0 * (double)lg[a] - zmax);
                 S += pr[a];
             }
-            const uint4 d = draw4(p.seeds[w], PURPOSE_ACTION, (uint32_t)t, (uint32_t)cellv, 0u);
+            // keyed by the cell (unique under exclusive occupancy, R9), by the slot under co-location (R47)
+            const uint4 d = draw4(p.seeds[w], PURPOSE_ACTION, (uint32_t)t, (uint32_t)(p.coloc ? slot : cellv), 0u);
             const double u = (double)d.x * 2.3283064365386963e-10;
             int act = 4;
             double cum = 0.0, margin = INFINITY;

@@ -45,7 +45,8 @@ namespace eco {
 
 constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
                    PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7,
-                   PURPOSE_ACTION = 8;  // the sampled action of network 1 (R38)
+                   PURPOSE_ACTION = 8,   // the sampled action of network 1 (R38)
+                   PURPOSE_CONSUME = 9;  // co-location: the lottery on a resource cell (R45)
 constexpr int LOGIT_STRIDE = 8;
 constexpr uint8_t NO_DIR = 0xFF;
 
@@ -54,6 +55,7 @@ constexpr uint8_t NO_DIR = 0xFF;
 struct DevParams {
     int H, W, WW, S, SW, Hd, I, P, Pd, n_worlds, r, log_cap;
     int net;             // 0: LSTM + linear head, argmax; 1: the paper's CNN-LSTM, sampled (NEXT-2)
+    int coloc;           // 1: co-location (NEXT-1, R43-R47): ncount / elig_bits below, no claims
     int row_lo, row_hi;  // rows this handle owns: [0, H) unless it is one latitude band (banded mode)
     int regrow_split;    // 1: k_post leaves the regrowth of step t+1 to k_regrow_tiled, launched after
                          // it (agent-free worlds of many words: the configs[2] benchmark grids)
@@ -132,6 +134,8 @@ struct DevParams {
     unsigned long long *phase_ns;  // [SIM_NUM_POST_PHASES] k_post phase clock (block 0)
     const uint8_t *forced;       // [n_worlds][S]
     uint8_t *own_act;            // [n_worlds][S] test hook: the policy's own action while forcing is on
+    int32_t *ncount;             // co-location: [n_worlds][H*W] agents per cell
+    uint32_t *elig_bits;         // co-location: [n_worlds][SW] eligible parents of the step (by slot)
     const int32_t *forced_on;    // device flag
     int32_t *nonfinite;          // host-mapped flag
 };

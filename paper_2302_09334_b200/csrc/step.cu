@@ -108,7 +108,9 @@ __device__ __forceinline__ void agent_commit(const DevParams &p, int w, int i, i
         const int y = row_of(p, cellv), x = cellv - y * p.W;
         const int ty = y + kDY[act], tx = x + kDX[act];
         if (p.lethal_walls && !(ty >= 0 && ty < p.H && tx >= 0 && tx < p.W)) tg = WALL_TARGET;
-        if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
+        if (p.coloc) {  // co-location (R43): an in-grid move always succeeds, no claim
+            if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) tg = ty * p.W + tx;
+        } else if (ty >= 0 && ty < p.H && tx >= 0 && tx < p.W) {
             const int tc = ty * p.W + tx;
             const bool occupied = p.r >= 1 ? occ_in_window(act)
                                            : get_bit(p.occ + (size_t)w * plane_words(p), p, tc) != 0u;
@@ -1530,21 +1532,29 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+#include "coloc.cuh"
+
 cudaError_t launch_move(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
     if (p.S == 0) return cudaSuccess;
+    if (p.coloc) {  // co-location: the move (and lottery keys), then consumption .. death
+        k_co_move<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
+        k_co_live<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     if (paper_rules(p)) k_move<true><<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
     else k_move<false><<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStream_t s) {
-    if (p.S == 0) return cudaSuccess;
+    if (p.S == 0 || p.coloc) return cudaSuccess;  // (co-location: no birth claims)
     k_birth_claim<<<lc.agent_blocks, lc.agent_threads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
-    k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
+    if (p.coloc) k_co_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
+    else k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
     k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);  // movement / greediness windows ending here (after placement)
     return cudaGetLastError();
 }
@@ -1624,6 +1634,13 @@ cudaError_t post_prepare() {
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
+    if (p.coloc) {  // co-location (coloc.cuh): phase kernels, then the regrowth of step t+1
+        cudaError_t e;
+        if ((e = launch_move(p, lc, s)) != cudaSuccess) return e;
+        if ((e = launch_birth_rank(p, s)) != cudaSuccess) return e;
+        if ((e = launch_mutate(p, lc, s)) != cudaSuccess) return e;
+        return launch_regrow(p, 0, s);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lc.post_blocks);
     cfg.blockDim = dim3(POST_THREADS);

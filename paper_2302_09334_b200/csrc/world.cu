@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
         const int y = (int)(i / p.WW);
         if (y >= p.row_lo && y < p.row_hi) local += __popc(R[i]);  // the rows this handle owns
     }
+    if (p.coloc)  // co-location: agents per cell, counted below
+        for (size_t i = threadIdx.x; i < (size_t)p.H * p.W; i += blockDim.x) p.ncount[(size_t)w * p.H * p.W + i] = 0;
     atomicAdd(&res_acc, local);
     __syncthreads();
     uint32_t base = 0u;
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(1024) k_rebuild(DevParams p) {
             uint32_t bit;
             uint32_t *wp = word_ptr(O, p, p.cell[gs], bit);
             atomicOr(wp, bit);
+            if (p.coloc) atomicAdd(p.ncount + (size_t)w * p.H * p.W + p.cell[gs], 1);
         }
         const uint32_t word = __ballot_sync(0xffffffffu, a != 0u);
         if ((threadIdx.x & 31) == 0 && i < p.S) p.alive_bits[(size_t)w * p.SW + (i >> 5)] = word;

@@ -70,7 +70,7 @@ class SimConfig(ctypes.Structure):
         ("band_rows", ctypes.POINTER(ctypes.c_int32)), ("band_slots", ctypes.c_int32),
         # the paper's own world (include/sim.h)
         ("climate_alpha", ctypes.c_double), ("death_steps", ctypes.c_int32), ("lethal_walls", ctypes.c_int32),
-        ("network", ctypes.c_int32),
+        ("network", ctypes.c_int32), ("colocate", ctypes.c_int32),
     ]
 
 
@@ -197,6 +197,7 @@ def make_config(wc, device: int = 0, stream=None, log_capacity: int = 0, bands=N
     c.death_steps = int(getattr(wc, "death_steps", 0))
     c.lethal_walls = int(getattr(wc, "lethal_walls", 0))
     c.network = int(getattr(wc, "network", 0))
+    c.colocate = int(getattr(wc, "colocate", 0))
     keep = [seeds]
     if bands:
         G = int(bands["n_bands"])

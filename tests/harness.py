@@ -182,8 +182,9 @@ def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights
         for i in dis:
             if o["alive"][i] == 1 and o["age"][i] == 0:
                 continue  # died and its slot was reused by a newborn: the step's logits are gone
-            _, _, mo = oracle.sample_action(seed, t, int(cells_start[i]), o["logits"][i])
-            _, _, mg = oracle.sample_action(seed, t, int(cells_start[i]), g["logits"][i])
+            ent = int(i) if getattr(world.wc, "colocate", 0) else int(cells_start[i])  # R47 / R38
+            _, _, mo = oracle.sample_action(seed, t, ent, o["logits"][i])
+            _, _, mg = oracle.sample_action(seed, t, ent, g["logits"][i])
             assert min(mo, mg) < 1e-4, f"{where}: unflagged sampling disagreement at slot {i} (margins {mo}, {mg})"
         flips += int(dis.size)
         n_cmp += int(start.size)

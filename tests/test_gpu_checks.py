@@ -34,6 +34,8 @@ cases = {
     "batch": (workloads.tiny().replace(seeds=(1, 2, 3), repr_steps=5, e_repr_gt=10200), None),
     "cnn": (workloads.paper_world_cnn().replace(rows=40, cols=60, slots=200, n_initial=120, repr_steps=20,
                                                  seeds=(11,)), None),
+    "coloc": (workloads.paper_world_coloc().replace(rows=40, cols=60, slots=300, n_initial=150, repr_steps=20,
+                                                    seeds=(12,)), None),
     "banded": (workloads.tiny().replace(rows=40, cols=96, slots=600, n_initial=400, hidden=32, obs_radius=3,
                                         repr_steps=6, e_repr_gt=10300, seeds=(4,)), dict(n_bands=4)),
 }
