@@ -57,7 +57,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "tiny", "large_world", "ensemble", "paper_world",
-                                                                   "paper_world_cnn"))
+                                                                   "paper_world_cnn", "paper_world_coloc"))
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -85,7 +85,7 @@ def workload(name: str, rank: int, world_size: int = 1) -> workloads.WorldConfig
         return workloads.tiny().replace(seeds=(rank,))
     if name == "large_world":
         return workloads.large_world().replace(seeds=(3 + rank,))
-    if name in ("paper_world", "paper_world_cnn"):  # the paper's own world (NEXT-1), its own agents (NEXT-2)
+    if name in ("paper_world", "paper_world_cnn", "paper_world_coloc"):  # the paper's world, agents, reproduction
         wc = getattr(workloads, name)()
         return wc.replace(seeds=(wc.seeds[0] + rank,))
     return workloads.ensemble().replace(seeds=tuple(workloads.ensemble_shard(world_size, rank)))

@@ -20,7 +20,7 @@ from paper_2302_09334_b200 import sim  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--warmup", type=int, default=3000)
 ap.add_argument("--config", default="paper_scale", choices=("paper_scale", "large_world", "ensemble", "paper_world",
-                                                                 "paper_world_cnn"))
+                                                                 "paper_world_cnn", "paper_world_coloc"))
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 wc = getattr(workloads, a.config)()
