@@ -16,7 +16,8 @@
 //               bitmaps), each child on its parent's cell, the lottery words reset, the
 //               step's counters, t += 1; the birth lists carry the child SLOT as the
 //               mutation's Philox entity (R47: co-located children share a cell)
-// then k_mutate, k_mv_pass (metrics windows) and k_regrow of step t+1.
+//               (and the metrics windows ending here)
+// then k_mutate and k_regrow of step t+1.
 
 __global__ void __launch_bounds__(256) k_co_move(DevParams p) {
     const long total = (long)p.n_worlds * p.S;
@@ -159,9 +160,13 @@ __device__ void co_rank_lists(const DevParams &p, int w, int n_place, uint32_t *
     __syncthreads();
 }
 
+// One block per world: rank, placement, counters, t += 1, then the world's movement /
+// greediness windows ending here.  (The regrowth of step t+1 is a separate launch: a
+// block regrowing beside this one could start after t advanced.)
 __global__ void __launch_bounds__(RANK_THREADS) k_co_rank(DevParams p) {
     __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
+    __shared__ int s_mv[SIM_MOVE_BINS];
     const size_t HW = (size_t)p.H * p.W;
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) {
         const int64_t t = p.t[w];
@@ -193,5 +198,9 @@ __global__ void __launch_bounds__(RANK_THREADS) k_co_rank(DevParams p) {
             p.t[w] = t + 1;
         }
         __syncthreads();
+#if ECO_METRICS & 2
+        if (mv_window_end(t)) mv_pass_part(p, t, w, 0, p.S, threadIdx.x, blockDim.x, s_mv);
+#endif
+        if (gr_window_end(t)) greed_pass_part(p, w, 0, p.S, threadIdx.x, blockDim.x);
     }
 }

@@ -1553,8 +1553,11 @@ cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStre
 }
 
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
-    if (p.coloc) k_co_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
-    else k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
+    if (p.coloc) {  // (the regrowth of step t+1 is graph mode's: launch_post)
+        k_co_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
     k_mv_pass<<<p.n_worlds, 256, 0, s>>>(p);  // movement / greediness windows ending here (after placement)
     return cudaGetLastError();
 }
@@ -1634,7 +1637,7 @@ cudaError_t post_prepare() {
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
-    if (p.coloc) {  // co-location (coloc.cuh): phase kernels, then the regrowth of step t+1
+    if (p.coloc) {  // co-location (coloc.cuh): move, live, rank (+ metrics windows), mutation, regrowth of t+1
         cudaError_t e;
         if ((e = launch_move(p, lc, s)) != cudaSuccess) return e;
         if ((e = launch_birth_rank(p, s)) != cudaSuccess) return e;
