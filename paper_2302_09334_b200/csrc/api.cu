@@ -184,6 +184,7 @@ struct sim_ctx {
     sim_config cfg{};
     std::vector<uint64_t> seeds;
     int device = 0;
+    bool band_no_graph = false;  // banded, remote bands: the step could not be captured (api_band.inc)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     DevParams p{};

@@ -10,8 +10,13 @@
 * Estimate of a G-GPU step: sum over phases of the slowest band's phase time (the P rows of
   the split policy overlap the phases after them, as on the second stream of sim_step), plus the
   phase barriers (5 neighbour token exchanges and 1 all-reduce per step) at an ASSUMED
-  latency (--nbr-us, --all-us: host-launched NCCL over NVLink, not measured here); the
-  exchanges themselves are pull kernels inside the phase times.  E(G) = T(1) / (G T(G)).
+  latency (--nbr-us, --all-us: NCCL over NVLink, not measured here); the exchanges
+  themselves are pull kernels inside the phase times.  E(G) = T(1) / (G T(G)).
+* Graph estimate (the per-GPU step captured as one CUDA graph, NCCL barriers inside, as
+  api_band.inc does): the banded world's one-GPU graph step (all G bands one after the
+  other, T_graph) / G, times the slowest band's share of the event-timed band totals, plus
+  the same assumed barriers.  The event-timed phases above include every launch's own
+  latency; inside a graph consecutive kernels start ~1 us apart.
 Writes one JSON object (stdout, --out)."""
 import argparse
 import json
@@ -66,7 +71,8 @@ def main():
         torch.cuda.synchronize()
         t1 = ev[0].elapsed_time(ev[1]) / a.steps
         st = w1.get_state(("alive", "cell"))
-        log1 = w1.step_log(a.warmup, a.steps)[:, 0]
+        w1.step(a.steps)  # the window the banded phase timing replays
+        log1 = w1.step_log(a.warmup, 2 * a.steps)[:, 0]
         w1.destroy()
     cells = st["cell"][0][st["alive"][0] == 1]
     hist = np.bincount(cells // wc.cols, minlength=wc.rows)
@@ -80,24 +86,39 @@ def main():
             with torch.cuda.stream(stream):
                 wb = sim.World(wc, stream=stream, bands=dict(n_bands=G, band_rows=rows, band_slots=min(slots, wc.slots)))
                 wb.step(a.warmup)
+                # graph mode: the G bands' whole steps as one CUDA graph per step, bands one
+                # after the other (what a graph-captured per-GPU step spends, summed over bands)
+                ev[0].record(stream)
+                wb.step(a.steps)
+                ev[1].record(stream)
+                torch.cuda.synchronize()
+                tg = ev[0].elapsed_time(ev[1]) / a.steps
                 ph = np.zeros((G, len(sim.BAND_PHASES)))
                 for _ in range(a.steps):
                     ph += wb.band_step_timed()
                 ph /= a.steps
-                lb = wb.step_log(a.warmup, a.steps)[:, 0]
+                lb = wb.step_log(a.warmup, 2 * a.steps)[:, 0]
                 wb.destroy()
             assert np.array_equal(lb, log1), "banded records differ from the unbanded world"
             slowest = ph.max(axis=0)
             # the P rows (prep_p) run on a second stream beside the phases after it
             ip = sim.BAND_PHASES.index("prep_p")
             compute = float(slowest[:ip].sum() + max(slowest[ip + 1:].sum(), slowest[ip]))
-            est = compute + (5 * a.nbr_us + a.all_us) / 1e3  # 5 neighbour barriers, 1 all-reduce per step
+            barriers = (5 * a.nbr_us + a.all_us) / 1e3  # 5 neighbour barriers, 1 all-reduce per step
+            est = compute + barriers
+            # graph estimate: the mean band step inside the one-GPU graph (T_graph / G), scaled by
+            # the slowest band's share of the event-timed band totals (the imbalance)
+            tot = ph.sum(axis=1)
+            est_g = tg / G * float(tot.max() / tot.mean()) + barriers
             res["bands"].append({
                 "G": G, "rows": kind, "band_rows": rows, "agents_per_band": per_band, "band_slots": slots,
                 "phase_ms_slowest_band": dict(zip(sim.BAND_PHASES, slowest.round(5).tolist())),
                 "band_total_ms": ph.sum(axis=1).round(5).tolist(),
                 "est_step_ms_compute": compute, "est_step_ms": est,
                 "est_efficiency": t1 / (G * est), "est_efficiency_compute_only": t1 / (G * compute),
+                "graph_step_ms_all_bands": tg, "est_graph_step_ms": est_g,
+                "est_graph_efficiency": t1 / (G * est_g),
+                "est_graph_efficiency_compute_only": t1 / (G * (est_g - barriers)),
                 "records_equal_unbanded": True})
             print(json.dumps(res["bands"][-1]), file=sys.stderr, flush=True)
     txt = json.dumps(res, indent=1)
