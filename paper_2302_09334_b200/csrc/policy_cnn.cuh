@@ -49,7 +49,7 @@ __device__ __forceinline__ double sigmoid_d(double z) { return 1.0 / (1.0 + exp(
 // from the oracle's, so the stored values agree to about one fp32 rounding even for
 // weights far larger than the paper's.
 __global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
-    extern __shared__ __align__(16) unsigned char cnn_smem_raw[];
+    extern __shared__ __align__(1024) unsigned char cnn_smem_raw[];
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;

@@ -25,6 +25,17 @@
 
 namespace eco {
 
+#ifdef ECO_CODE_PAD
+// diagnostic: an unused kernel of ECO_CODE_PAD straight-line instructions, shifting the
+// module's code layout (tools/gpu_abv.sh layout experiments)
+__global__ void k_code_pad(float *out, float a, float b) {
+    float x = a;
+#pragma unroll
+    for (int i = 0; i < ECO_CODE_PAD; ++i) x = fmaf(x, a, b + (float)i);
+    out[threadIdx.x] = x;
+}
+#endif
+
 __device__ __constant__ int kDY[5] = {0, -1, 1, 0, 0};  // stay, N, S, E, W (R13)
 __device__ __constant__ int kDX[5] = {0, 0, 0, 1, -1};
 
@@ -449,7 +460,7 @@ __device__ __forceinline__ void hh_pass(const DevParams &p, const int32_t *list,
 // P of every live agent of step t (after create / set_state / instrumented steps), one
 // half-warp per agent; no children pending afterwards.
 __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p(DevParams p) {
-    extern __shared__ float4 half_smem[];
+    extern __shared__ __align__(1024) float4 half_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ag = warp * 2 + (lane >> 4);
     const int64_t t = p.t[0];
@@ -465,7 +476,7 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p(DevParams 
 // snapshotted right after the band's consumption/physiology/death), on a second stream while
 // the rest of the step runs; the children placed later have none (p_children, set by the rank).
 __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p_snap(DevParams p, const int64_t *snap) {
-    extern __shared__ float4 half_smem[];
+    extern __shared__ __align__(1024) float4 half_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ag = warp * 2 + (lane >> 4);
     hh_pass<HALF_DEPTH>(p, list_of(p, snap[0], 0), (int)snap[1], ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
@@ -488,7 +499,7 @@ template <bool SHARD, bool SPLIT = false>
 __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParams p) {
     constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
     constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ float4 half_smem[];  // [HALF_AGENTS][R][32 units]
+    extern __shared__ __align__(1024) float4 half_smem[];  // [HALF_AGENTS][R][32 units]
     __shared__ uint8_t s_col[HALF_AGENTS][RING_COLS];
     __shared__ int s_w[HALF_AGENTS];
     __shared__ unsigned long long s_nnz[HALF_AGENTS], s_ties[HALF_AGENTS];
@@ -1009,7 +1020,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_bcell[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     __shared__ int s_mv[SIM_MOVE_BINS];  // a window end's movement histogram of this block
-    extern __shared__ float4 post_smem[];  // split: the P rings, 2 HH_WARPS contexts x HH_DEPTH
+    extern __shared__ __align__(1024) float4 post_smem[];  // split: the P rings, 2 HH_WARPS contexts x HH_DEPTH
 #if ECO_POST_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the policy grid has completed
 #endif
