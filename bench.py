@@ -71,6 +71,9 @@ def parse_args():
     ap.add_argument("--no-l2-persist", action="store_true",
                     help="ablation: no L2-persisting window on the hot-state arena (ECO_L2_PERSIST=0)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--cpu-baseline-suite", default=None, metavar="OUT",
+                    help="run the oracle's CPU baseline of BASELINE.md section 3 on every config, write OUT, exit")
+    ap.add_argument("--quick", action="store_true", help="(with --cpu-baseline-suite) fewer steps")
     return ap.parse_args()
 
 
@@ -397,6 +400,13 @@ def run_ours(args, rank, world_size, local_rank):
                "L2-persisting, so the flush cannot evict it; the weights stream from HBM every step"),
             "cell_updates_per_s": cells * (1 if sharded else world_size) / (max_ms / 1e3),
             "agents_mean": agents / K,
+            # the paper's own timing is of its own world with its own network (1e6
+            # steps in ~20 min on an unnamed GPU with JAX, ~833 world steps/s): context for the
+            # paper-world configs, not vs_baseline (BASELINE.json publishes no number)
+            **({"vs_paper": {"world_steps_per_s": 1e3 / (max_ms / K), "paper_world_steps_per_s": 833.0,
+                             "ratio": 1e3 / (max_ms / K) / 833.0,
+                             "note": "PAPER.md:340, unnamed GPU, JAX; context only"}}
+               if args.config in ("paper_world_cnn", "paper_world_coloc") else {}),
             "births_mean": births / K,
             "gpu_launches": 2 * K,  # per rank: the policy kernel and the cooperative k_post
             "post_phase_us_per_step": post_phases,
@@ -478,6 +488,99 @@ def traffic_ratio(kname="policy", workload="paper_scale", agents=None):
 
 
 # -------------------------------------------------------------- oracle (CPU) legs
+
+# ----------------------------------------------------- the CPU baseline suite
+# `bench.py --cpu-baseline-suite OUT`: the oracle (oracle/, single-threaded C99) on the host CPU
+# of the GPU box per config, reported like the GPU numbers (agent-steps/s, cell-updates/s,
+# wall time; CPU model, 1 core per process, nproc): tiny all 100 steps; paper-scale the
+# first 200; regrowth 1000 steps at 200x400, 100 at 2048x4096, 10 at 8192x16384; the large
+# world extrapolated (its canonical state would hold 17.8 GB of weights); the ensemble as one
+# world and as one world per host core in separate processes; the paper's own world with
+# the paper's network and reproduction beside the paper's ~833 world steps/s.
+def _suite_host() -> dict:
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "cpus_usable": len(os.sched_getaffinity(0))}
+
+
+def _suite_world(wc, steps, world=0):
+    t0 = time.perf_counter()
+    import oracle
+    w = oracle.OracleWorld(wc, world)
+    t_init = time.perf_counter() - t0
+    agents = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        agents += int(w.st["alive"].sum())
+        r = w.step()
+        assert r["status"] == 0
+    el = time.perf_counter() - t0
+    return {"steps": steps, "wall_s": el, "init_s": t_init, "agent_steps": agents,
+            "agent_steps_per_s": agents / el, "cell_updates_per_s": wc.rows * wc.cols * steps / el,
+            "world_steps_per_s": steps / el, "mean_agents": agents / steps}
+
+
+def _suite_regrow(rows, cols, steps):
+    import oracle
+    wc = workloads.regrowth_micro(rows, cols)
+    R = oracle.OracleWorld(wc).st["resources"].copy()
+    t0 = time.perf_counter()
+    for t in range(steps):
+        R, _ = oracle.regrow(wc, t, R)
+    el = time.perf_counter() - t0
+    return {"grid": f"{rows}x{cols}", "steps": steps, "wall_s": el, "us_per_step": el / steps * 1e6,
+            "cell_updates_per_s": rows * cols * steps / el}
+
+
+def _suite_ens_worker(args):
+    seed, steps = args
+    wc = workloads.ensemble(seeds=(seed,))
+    return _suite_world(wc, steps)
+
+
+def cpu_baseline_suite(out: str, q: bool = False) -> dict:
+    import multiprocessing as mp
+    res = {"kind": "oracle", "cores_per_process": 1, **_suite_host(), "configs": {}}
+    res["configs"]["tiny"] = _suite_world(workloads.tiny(), 20 if q else 100)
+    res["configs"]["paper_scale"] = _suite_world(workloads.paper_scale(), 20 if q else 200)
+    res["configs"]["regrowth_micro"] = [_suite_regrow(200, 400, 100 if q else 1000),
+                                        _suite_regrow(2048, 4096, 5 if q else 100),
+                                        _suite_regrow(8192, 16384, 1 if q else 10)]
+    ps = res["configs"]["paper_scale"]
+    per_agent = ps["wall_s"] / ps["agent_steps"]  # (the LSTM dominates: the cell cost is folded in)
+    lw = workloads.large_world()
+    res["configs"]["large_world"] = {
+        "run": False, "why": "the oracle's canonical state would hold 17.8 GB of fp32 weights",
+        "extrapolated_s_per_step_at_cap": per_agent * lw.slots,
+        "extrapolated_agent_steps_per_s": 1.0 / per_agent}
+    steps = 20 if q else 200
+    one = _suite_world(workloads.ensemble(seeds=(100,)), steps)
+    ncores = min(res["cpus_usable"], 32)  # (each process holds a 555 MB world)
+    seeds = [100 + (k % 64) for k in range(ncores)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(ncores) as pool:
+        outs = pool.map(_suite_ens_worker, [(s, steps) for s in seeds])
+    el = time.perf_counter() - t0
+    agg = sum(o["agent_steps"] for o in outs)
+    res["configs"]["ensemble"] = {
+        "one_world": one, "one_core_64_worlds_in_sequence_agent_steps_per_s": one["agent_steps_per_s"],
+        "per_core_processes": {"processes": ncores, "worlds": len(seeds), "steps_each": steps, "wall_s": el,
+                               "agent_steps_per_s": agg / el,
+                               "note": "one world per host core, all cores busy (memory bandwidth shared)"}}
+    pw = _suite_world(workloads.paper_world_coloc(), 40 if q else 200)
+    pw["paper_world_steps_per_s_reported"] = 833.0
+    pw["paper_note"] = "PAPER.md:340: 1e6 steps in ~20 min on 'a single GPU' with JAX (model not stated)"
+    res["configs"]["paper_world_coloc"] = pw
+    open(out, "w").write(json.dumps(res, indent=1))
+    return res
+
+
 def oracle_rate(wc, start_state, budget_s, max_steps):
     import oracle
     w = oracle.OracleWorld(wc, state=start_state)
@@ -534,6 +637,10 @@ def run_reference(args, rank):
 
 def main():
     args = parse_args()
+    if args.cpu_baseline_suite:
+        res = cpu_baseline_suite(args.cpu_baseline_suite, args.quick)
+        print(json.dumps(res))
+        return
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
