@@ -25,16 +25,6 @@
 
 namespace eco {
 
-#ifdef ECO_CODE_PAD
-// diagnostic: an unused kernel of ECO_CODE_PAD straight-line instructions, shifting the
-// module's code layout (tools/gpu_abv.sh layout experiments)
-__global__ void k_code_pad(float *out, float a, float b) {
-    float x = a;
-#pragma unroll
-    for (int i = 0; i < ECO_CODE_PAD; ++i) x = fmaf(x, a, b + (float)i);
-    out[threadIdx.x] = x;
-}
-#endif
 
 __device__ __constant__ int kDY[5] = {0, -1, 1, 0, 0};  // stay, N, S, E, W (R13)
 __device__ __constant__ int kDX[5] = {0, 0, 0, 1, -1};

@@ -1,14 +1,11 @@
 #!/bin/bash
-# 10,000-step A/B (the bench's default run) of build variants and the L2-persist switch
 OUT=gpurun_out
 : > $OUT/ab10k.txt
 for rep in 1 2; do
-for v in base nopersist nogreed; do
-  L=build_var/libsim_$v.so; EXTRA=""
-  if [ $v = nopersist ]; then L=build_var/libsim_base.so; EXTRA="--no-l2-persist"; fi
-  ECO_LIBSIM_OVERRIDE=$L timeout 300 python bench.py --steps 10000 --warmup 5 --no-cpu-baseline --no-e2e --no-replay $EXTRA > $OUT/ab10k_${v}_$rep.json 2>> $OUT/ab10k.err
+for v in "$@"; do
+  ECO_LIBSIM_OVERRIDE=build_var/libsim_$v.so timeout 300 python bench.py --steps 10000 --warmup 5 --no-cpu-baseline --no-e2e --no-replay > $OUT/ab10k_${v}_$rep.json 2>> $OUT/ab10k.err
   python -c "
 import json; d=json.loads(open('$OUT/ab10k_${v}_$rep.json').read().strip().splitlines()[-1])
-print('$v', $rep, round(d['ms_per_step']*1e3,2), d.get('agents_mean'), d.get('post_phase_us_per_step'))" >> $OUT/ab10k.txt 2>&1
+print('$v', $rep, round(d['ms_per_step']*1e3,2), d.get('post_phase_us_per_step'))" >> $OUT/ab10k.txt 2>&1
 done; done
 cat $OUT/ab10k.txt
