@@ -19,10 +19,10 @@
 //               (and the metrics windows ending here)
 // then k_mutate and k_regrow of step t+1.
 
-__global__ void __launch_bounds__(256) k_co_move(DevParams p) {
+__device__ __forceinline__ void co_move_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
-    for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += (long)gridDim.x * blockDim.x) {
+    for (long v = (long)gtid; v < total; v += (long)gthreads) {
         const AgentIter it = agent_at(p, v);
         const int w = it.w;
         const int64_t t = p.t[w];
@@ -64,10 +64,10 @@ __global__ void __launch_bounds__(256) k_co_move(DevParams p) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_co_live(DevParams p) {
+__device__ __forceinline__ void co_live_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
-    for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += (long)gridDim.x * blockDim.x) {
+    for (long v = (long)gtid; v < total; v += (long)gthreads) {
         const AgentIter it = agent_at(p, v);
         const int w = it.w;
         const int64_t t = p.t[w];
@@ -160,47 +160,87 @@ __device__ void co_rank_lists(const DevParams &p, int w, int n_place, uint32_t *
     __syncthreads();
 }
 
-// One block per world: rank, placement, counters, t += 1, then the world's movement /
-// greediness windows ending here.  (The regrowth of step t+1 is a separate launch: a
-// block regrowing beside this one could start after t advanced.)
+// World w's rank, placement, counters, t += 1, then its movement / greediness windows ending
+// here; all RANK_THREADS threads of one block.
+__device__ __forceinline__ void co_rank_world(const DevParams &p, int w, uint32_t *scratch, int *s_free, int *s_par,
+                                              int *s_mv) {
+    const size_t HW = (size_t)p.H * p.W;
+    const int64_t t = p.t[w];
+    const RankCounts k = rank_counts(p, w, t);  // n_win = eligible parents (k_co_live)
+    const size_t ws = (size_t)w * p.S;
+    int32_t *g_free = p.free_list + ws, *g_par = p.birth_parent + ws;
+    if (k.n_place > 0) co_rank_lists<RANK_THREADS>(p, w, k.n_place, scratch, s_free, s_par, g_free, g_par);
+    for (int r = threadIdx.x; r < k.n_place; r += RANK_THREADS) {
+        const bool sm = r < RANK_SMEM_CAP;
+        const int child = sm ? s_free[r] : *reinterpret_cast<volatile int32_t *>(g_free + r);
+        const int par = sm ? s_par[r] : *reinterpret_cast<volatile int32_t *>(g_par + r);
+        const int c = p.cell[ws + par];  // R46: the parent's cell
+        place_child(p, w, t, c, r, k.n_surv, child, par);
+        atomicAdd(p.ncount + (size_t)w * HW + c, 1);
+        p.birth_child[ws + r] = child;
+        p.birth_parent[ws + r] = par;
+        p.birth_cell[ws + r] = child;  // the mutation's Philox entity: the child's slot (R47)
+    }
+    // the lottery words of this step's cells, and the eligible bitmap, back to zero
+    for (int i = threadIdx.x; i < k.n_start; i += RANK_THREADS) {
+        const int4 mr = p.mrec[ws + i];
+        if (mr.z != WALL_TARGET) p.claim[(size_t)w * HW + mr.w] = 0ull;
+    }
+    for (int j = threadIdx.x; j < p.SW; j += RANK_THREADS) p.elig_bits[(size_t)w * p.SW + j] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.n_births[w] = k.n_place;
+        rank_finalize(p, w, t, k.n_start, k.n_surv, k.n_win, k.n_place);
+        p.t[w] = t + 1;
+    }
+    __syncthreads();
+#if ECO_METRICS & 2
+    if (mv_window_end(t)) mv_pass_part(p, t, w, 0, p.S, threadIdx.x, blockDim.x, s_mv);
+#endif
+    if (gr_window_end(t)) greed_pass_part(p, w, 0, p.S, threadIdx.x, blockDim.x);
+}
+
+// One block per world.  (The regrowth of step t+1 is a separate launch in the instrumented
+// path: a block regrowing beside this one could start after t advanced; k_post_co reads t
+// first and keeps every block resident.)
 __global__ void __launch_bounds__(RANK_THREADS) k_co_rank(DevParams p) {
     __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     __shared__ int s_mv[SIM_MOVE_BINS];
-    const size_t HW = (size_t)p.H * p.W;
-    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) {
-        const int64_t t = p.t[w];
-        const RankCounts k = rank_counts(p, w, t);  // n_win = eligible parents (k_co_live)
-        const size_t ws = (size_t)w * p.S;
-        int32_t *g_free = p.free_list + ws, *g_par = p.birth_parent + ws;
-        if (k.n_place > 0) co_rank_lists<RANK_THREADS>(p, w, k.n_place, scratch, s_free, s_par, g_free, g_par);
-        for (int r = threadIdx.x; r < k.n_place; r += RANK_THREADS) {
-            const bool sm = r < RANK_SMEM_CAP;
-            const int child = sm ? s_free[r] : *reinterpret_cast<volatile int32_t *>(g_free + r);
-            const int par = sm ? s_par[r] : *reinterpret_cast<volatile int32_t *>(g_par + r);
-            const int c = p.cell[ws + par];  // R46: the parent's cell
-            place_child(p, w, t, c, r, k.n_surv, child, par);
-            atomicAdd(p.ncount + (size_t)w * HW + c, 1);
-            p.birth_child[ws + r] = child;
-            p.birth_parent[ws + r] = par;
-            p.birth_cell[ws + r] = child;  // the mutation's Philox entity: the child's slot (R47)
-        }
-        // the lottery words of this step's cells, and the eligible bitmap, back to zero
-        for (int i = threadIdx.x; i < k.n_start; i += RANK_THREADS) {
-            const int4 mr = p.mrec[ws + i];
-            if (mr.z != WALL_TARGET) p.claim[(size_t)w * HW + mr.w] = 0ull;
-        }
-        for (int j = threadIdx.x; j < p.SW; j += RANK_THREADS) p.elig_bits[(size_t)w * p.SW + j] = 0u;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            p.n_births[w] = k.n_place;
-            rank_finalize(p, w, t, k.n_start, k.n_surv, k.n_win, k.n_place);
-            p.t[w] = t + 1;
-        }
-        __syncthreads();
-#if ECO_METRICS & 2
-        if (mv_window_end(t)) mv_pass_part(p, t, w, 0, p.S, threadIdx.x, blockDim.x, s_mv);
-#endif
-        if (gr_window_end(t)) greed_pass_part(p, w, 0, p.S, threadIdx.x, blockDim.x);
+    for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) co_rank_world(p, w, scratch, s_free, s_par, s_mv);
+}
+
+__global__ void __launch_bounds__(256) k_co_move(DevParams p) {
+    co_move_phase(p, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+}
+__global__ void __launch_bounds__(256) k_co_live(DevParams p) {
+    co_live_phase(p, (size_t)blockIdx.x * blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x);
+}
+
+// Graph mode: the whole post-policy step in one cooperative launch (one block per SM), the
+// phases separated by grid barriers instead of kernel boundaries: move | live | rank (one
+// block per world) beside the regrowth of step t+1 (the other blocks; t read before any
+// block advances it) | mutation.
+__global__ void __launch_bounds__(RANK_THREADS) k_post_co(DevParams p, unsigned long long *bar) {
+    __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
+    __shared__ int s_free[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
+    __shared__ int s_mv[SIM_MOVE_BINS];
+    unsigned long long target = grid_sync_base(bar);
+    const int64_t T = p.t[0];  // (all worlds share t)
+    const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, gthreads = (size_t)gridDim.x * blockDim.x;
+    co_move_phase(p, gtid, gthreads);
+    grid_sync(bar, target);
+    co_live_phase(p, gtid, gthreads);
+    grid_sync(bar, target);
+    const bool spare = (int)gridDim.x > p.n_worlds;  // blocks left over for the regrowth
+    if ((int)blockIdx.x < p.n_worlds) {
+        for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) co_rank_world(p, w, scratch, s_free, s_par, s_mv);
+    } else {
+        const size_t b = blockIdx.x - p.n_worlds, nb = gridDim.x - p.n_worlds;
+        regrow_phase(p, T + 1, b * blockDim.x + threadIdx.x, nb * blockDim.x);
     }
+    grid_sync(bar, target);
+    mutate_phase(p, gtid, gthreads);
+    if (!spare) regrow_phase(p, T + 1, gtid, gthreads);
+    if (blockIdx.x == 0 && threadIdx.x == 0) grid_sync_done(bar, target);
 }

@@ -1646,12 +1646,18 @@ cudaError_t post_prepare() {
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {
-    if (p.coloc) {  // co-location (coloc.cuh): move, live, rank (+ metrics windows), mutation, regrowth of t+1
-        cudaError_t e;
-        if ((e = launch_move(p, lc, s)) != cudaSuccess) return e;
-        if ((e = launch_birth_rank(p, s)) != cudaSuccess) return e;
-        if ((e = launch_mutate(p, lc, s)) != cudaSuccess) return e;
-        return launch_regrow(p, 0, s);
+    if (p.coloc) {  // co-location (coloc.cuh): one cooperative launch, the phases split by grid barriers
+        if (p.S == 0) return launch_regrow(p, 0, s);
+        cudaLaunchConfig_t cc = {};
+        cc.gridDim = dim3(lc.post_blocks);
+        cc.blockDim = dim3(RANK_THREADS);
+        cc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cc.attrs = at;
+        cc.numAttrs = 1;
+        return cudaLaunchKernelEx(&cc, k_post_co, p, bar);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lc.post_blocks);
