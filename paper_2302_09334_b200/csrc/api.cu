@@ -971,7 +971,13 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
         const float *src = nullptr;
         bool by_slot = false;
         cudaPointerAttributes pa{};
-        if (cudaPointerGetAttributes(&pa, in->weights) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        // page-locked caller memory: read in place by the gather kernel (zero-copy), unless the
+        // live rows form few long runs, which DMA copies move faster (ECO_SETSTATE_ZC=1/0 forces)
+        int runs = 1;
+        for (int k = 1; k < n_live; ++k) runs += live[k] != live[k - 1] + 1;
+        static const char *zc_env = getenv("ECO_SETSTATE_ZC");
+        const bool zc_pref = zc_env ? zc_env[0] == '1' : runs > 64;
+        if (zc_pref && cudaPointerGetAttributes(&pa, in->weights) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
             pa.devicePointer) {
             src = static_cast<const float *>(pa.devicePointer);
             by_slot = true;

@@ -494,6 +494,42 @@ def test_set_state_rejects_bad_occupancy_and_nonfinite():
         world.set_state(st3)
 
 
+@pytest.mark.parametrize("scatter", [False, True])
+def test_set_state_from_pinned_memory(scatter):
+    """sim_set_state from page-locked host buffers: the live rows' weights arrive by DMA runs
+    (few runs) or are gathered in place from mapped memory (more than 64 runs); both paths
+    give the same device state, and a non-finite weight in a live slot is refused either way."""
+    import torch
+    wc = workloads.paper_scale().replace(rows=60, cols=80, slots=600, n_initial=300)
+    st = workloads.random_state(wc, 7, n_alive=300)
+    if not scatter:  # live slots 0..299: one run
+        order = np.argsort(-st["alive"], kind="stable")
+        for k, v in list(st.items()):
+            if isinstance(v, np.ndarray) and v.shape[:1] == (wc.slots,):
+                st[k] = v[order].copy()
+    live = np.flatnonzero(st["alive"])
+    runs = 1 + int((np.diff(live) != 1).sum())
+    assert (runs > 64) == scatter
+    pinned = {}
+    for k, v in st.items():
+        if isinstance(v, np.ndarray):
+            tt = torch.empty((1,) + v.shape, dtype=getattr(torch, str(v.dtype)), pin_memory=True)
+            tt.numpy()[...] = v
+            pinned[k] = tt.numpy()
+        else:
+            pinned[k] = v
+    world = sim.World(wc)
+    world.set_state(pinned)
+    g = gpu_world_state(world.get_state())
+    for f in ("alive", "cell", "energy", "h", "c"):
+        assert np.array_equal(g[f][live], st[f][live]), f
+    assert np.array_equal(g["weights"][live], st["weights"][live])
+    pinned["weights"][0, live[5], 17] = np.inf
+    with pytest.raises(sim.SimError):
+        world.set_state(pinned)
+    world.destroy()
+
+
 def test_nonfinite_state_reported():
     wc = workloads.tiny()
     world = sim.World(wc)
