@@ -1264,7 +1264,20 @@ constexpr int RG_STAGES = 3;
 constexpr int RG_WORDS = RG_TW * RG_TH;
 static_assert(RG_WORDS == 4 * RG_THREADS, "one 4-word vector per thread");
 
+// the tile's window (RG_LOADS vectors) and, after it, the thresholds of its RG_TH rows (one
+// 16-B vector per row, zero past the handle's rows): staged together, so a tile waits on
+// no dependent global load
+constexpr int RG_STAGE_VECS = RG_LOADS + RG_TH;
+constexpr int RG_DYN_SMEM = RG_STAGES * RG_STAGE_VECS * 16;
 __device__ __forceinline__ void rg_issue(const DevParams &p, const uint32_t *src, int y0, int wx0, uint4 *stage) {
+    for (int k = threadIdx.x; k < RG_TH; k += RG_THREADS) {
+        const int y = y0 + k;
+        const bool in = y < p.row_hi;
+        const uint32_t *g = in ? p.T + (size_t)y * 4 : p.T;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(stage + RG_LOADS + k)), "l"(g),
+                     "r"(in ? 16 : 0)
+                     : "memory");
+    }
     for (int k = threadIdx.x; k < RG_LOADS; k += RG_THREADS) {
         const int r = k / RG_VW, q = k - r * RG_VW;
         const int yy = y0 - 2 + r, ww = wx0 - 4 + 4 * q;  // ww, WW multiples of 4: aligned, in-row
@@ -1300,12 +1313,12 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
 }
 
 __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int ahead) {
-    __shared__ uint4 s_ring[RG_STAGES][RG_LOADS];
+    extern __shared__ __align__(1024) uint4 rg_dyn[];  // the stage ring [RG_STAGES][RG_STAGE_VECS]
+    uint4 (*s_ring)[RG_STAGE_VECS] = reinterpret_cast<uint4 (*)[RG_STAGE_VECS]>(rg_dyn);
     __shared__ uint32_t s_code[2][RG_WORDS];     // listed words: 2-bit class per cell (cells 0-15, 16-31)
     __shared__ uint32_t s_grow[RG_WORDS];        // grown bits by tile word
     __shared__ uint16_t s_need[RG_WORDS];        // listed words (tile word index)
     __shared__ uint16_t s_item[RG_WORDS * 8];    // listed groups (list index << 3 | group)
-    __shared__ uint32_t s_T[RG_TH][4];           // thresholds of the tile's rows
     __shared__ int s_nneed, s_nitem;
     __shared__ unsigned long long s_red[RG_THREADS / 32];
     const int64_t tstep = p.t[0] + ahead;
@@ -1369,13 +1382,10 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
         }
         cp_wait<RG_STAGES - 2>();
         if (threadIdx.x == 0) s_nneed = s_nitem = 0;
-        if (threadIdx.x < RG_TH * 4) {
-            const int y = y0 + (threadIdx.x >> 2);
-            s_T[threadIdx.x >> 2][threadIdx.x & 3] = y < p.row_hi ? p.T[(size_t)y * 4 + (threadIdx.x & 3)] : 0u;
-        }
         __syncthreads();  // tile j staged for every thread; the previous tile's reads are done
         issue(j + RG_STAGES - 1);
         const uint32_t *sw = reinterpret_cast<const uint32_t *>(s_ring[j % RG_STAGES]);
+        const uint32_t *sT = reinterpret_cast<const uint32_t *>(s_ring[j % RG_STAGES] + RG_LOADS);  // [RG_TH][4]
         const int y = y0 + tr, wxv = wx0 + 4 * tq;
         const bool row_ok = y < p.row_hi;
         const uint4 cur4 = *reinterpret_cast<const uint4 *>(sw + (tr + 2) * RS + 4 * tq + 4);
@@ -1406,8 +1416,10 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
             }
         }
         __syncthreads();
-        // (2) counts and 2-bit classes of the listed words, and their groups to draw
+        // (2) counts and 2-bit classes of the listed words, and their groups to draw (a tile
+        // whose words are all full -- the saturated grid -- skips (2) and (3): block-uniform)
         const int nneed = s_nneed;
+        if (nneed > 0) {
         for (int k = threadIdx.x; k < nneed; k += RG_THREADS) {
             const int tw = s_need[k];
             const int r = tw / RG_TW, col = tw - r * RG_TW;
@@ -1479,7 +1491,7 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
             const uint4 d = draw4(seed, PURPOSE_REGROW, (uint32_t)tstep, (uint32_t)(((int64_t)yy * p.W + x0) >> 2), 0u);
             const int nv = p.W - x0;
             const uint32_t empty4 = (~cur >> (4 * g)) & (nv >= 4 ? 0xFu : ((1u << nv) - 1u));
-            const uint32_t *Tr = s_T[r];
+            const uint32_t *Tr = sT + 4 * r;
             uint32_t bits = 0u;
             bits |= (d.x < Tr[code & 3u]) ? 1u : 0u;
             bits |= (d.y < Tr[(code >> 2) & 3u]) ? 2u : 0u;
@@ -1489,6 +1501,7 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
             if (bits) atomicOr(&s_grow[tw], bits << (4 * g));
         }
         __syncthreads();
+        }  // nneed > 0
         // (4) this thread's 4 words (128-bit store when the whole vector is in the row)
         if (row_ok && wxv < real_words) {
             const uint4 g4 = *reinterpret_cast<const uint4 *>(s_grow + 4 * threadIdx.x);
@@ -1522,7 +1535,8 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
     if (regrow_tiled(p)) {
         static int bps = 0;
         if (bps == 0) {
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_regrow_tiled, RG_THREADS, 0);
+            cudaFuncSetAttribute(k_regrow_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, RG_DYN_SMEM);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_regrow_tiled, RG_THREADS, RG_DYN_SMEM);
             if (e != cudaSuccess || bps < 1) bps = 4;
         }
         int dev = 0, sms = 148;
@@ -1532,7 +1546,7 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
             (size_t)p.n_worlds * ((p.row_hi - p.row_lo + RG_TH - 1) / RG_TH) * ((real_words + RG_TW - 1) / RG_TW);
         size_t blocks = (size_t)sms * bps;
         if (blocks > ntiles) blocks = ntiles;
-        k_regrow_tiled<<<(unsigned)blocks, RG_THREADS, 0, s>>>(p, ahead);
+        k_regrow_tiled<<<(unsigned)blocks, RG_THREADS, RG_DYN_SMEM, s>>>(p, ahead);
         return cudaGetLastError();
     }
     size_t blocks = (items + 255) / 256;
