@@ -1,7 +1,7 @@
 // coloc.cuh — the co-location step (readings R43-R47): the paper's
 // own reproduction, "the off-spring appears on the same cell as its parent",
 // with any number of agents per cell (the agent channel counts them).
-// Included by step.cu inside namespace eco.  Used with network 1 (k_policy_cnn), which
+// Included by step.cu inside namespace eco.  Used with network 1 (k_policy_cnn_blk), which
 // reads the per-cell counts `ncount` for its agent channel and posts no move claims.
 //
 //   k_co_move   a4: every in-grid move succeeds (no collision exclusion, R43); a lethal wall

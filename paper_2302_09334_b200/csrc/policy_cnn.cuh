@@ -1,4 +1,4 @@
-// policy_cnn.cuh — k_policy_cnn: steps a2 + a3 (+ the claim half of a4) for network 1,
+// policy_cnn.cuh — k_policy_cnn_blk: steps a2 + a3 (+ the claim half of a4) for network 1,
 // the paper's own agent network (App. B.5).
 // Included by step.cu inside namespace eco (it uses the step's epilogue helpers).
 //
@@ -13,23 +13,21 @@
 //   action   softmax(50 logits) sampled by inverse CDF with u = draw(ACTION, t, cell).x 2^-32
 //            (R38), in fp64 from the fp32 logits; near-tie when |u - CDF| < 1e-4
 //
-// One WARP per agent (2,445 parameters, 13.5 k multiply-adds: a per-agent network is a
+// One block per agent (2,445 parameters, 13.5 k multiply-adds: a per-agent network is a
 // batched GEMV-like chain of tiny layers with different weights per agent, no dense
 // contraction for the tensor cores).  The agent's whole parameter row (Pd = 2,464 floats,
-// 9.9 KB, canonical order = device order) is staged into the warp's shared memory with
+// 9.9 KB, canonical order = device order) is staged into the block's shared memory with
 // 16-B cp.async while the window's rows are fetched from the bit planes; every layer then
-// reads its weights from shared memory (broadcast or conflict-free strides) and its inputs
-// from the previous layer's shared-memory tile.  Inputs of conv1 are 0/1 bits, so conv1 is
-// a masked sum of weights.
-constexpr int CNN_WARPS = 4;                 // warps (agents in flight) per block
-constexpr int CNN_THREADS = CNN_WARPS * 32;
+// reads its weights from shared memory and its inputs from the previous layer's
+// shared-memory tile.  The resource and wall inputs of conv1 are 0/1, so conv1 adds weights
+// where they are set.
 constexpr int CNN_PD = 2464;                 // device row: 2445 parameters padded to 32 floats
 constexpr int CNN_WO = 15, CNN_R = 7;
 // canonical / device offsets of network 1 (sim.h)
 constexpr int CN_C1W = 0, CN_C1B = 108, CN_C2W = 112, CN_C2B = 400, CN_WIH = 408, CN_WHH = 1656, CN_B = 1720,
               CN_WD = 1736, CN_BD = 2392, CN_WO = 2400, CN_BO = 2440, CN_P = 2445;
 static_assert(CN_BO + 5 == CN_P && CN_P <= CNN_PD && CNN_PD % 32 == 0, "network-1 layout");
-// per-warp shared memory: the weights (floats), then fp64 tiles: conv1 out (8x8x4), pool1
+// the agent's shared memory: the weights (floats), then fp64 tiles: conv1 out (8x8x4), pool1
 // (7x7x4), conv2 out (4x4x8), e ++ h' (78 + 4, padded); window rows (R rows 0..14, O rows
 // 16..30) as words
 constexpr int CS_W_BYTES = CNN_PD * 4;
@@ -37,8 +35,7 @@ constexpr int CS_A1 = 0, CS_P1 = CS_A1 + 256, CS_A2 = CS_P1 + 196, CS_E = CS_A2 
 constexpr int CS_ROWS_BYTES = 32 * 4;
 constexpr int CS_CNT_BYTES = 228 * 4;  // the agent channel: agents per window cell (15 x 15)
 constexpr int CS_TOTAL_BYTES = CS_W_BYTES + CS_D_END * 8 + CS_ROWS_BYTES + CS_CNT_BYTES;
-static_assert(CS_W_BYTES % 16 == 0 && CS_TOTAL_BYTES % 16 == 0, "16-B aligned warp slices");
-constexpr int CNN_SMEM = CNN_WARPS * CS_TOTAL_BYTES;
+static_assert(CS_W_BYTES % 16 == 0 && CS_TOTAL_BYTES % 16 == 0, "16-B aligned slices");
 
 __device__ __forceinline__ double sigmoid_d(double z) { return 1.0 / (1.0 + exp(-z)); }
 
@@ -48,257 +45,12 @@ __device__ __forceinline__ double sigmoid_d(double z) { return 1.0 / (1.0 + exp(
 // the softmax and sampling in fp64 from the fp32 logits.  Only the summation order differs
 // from the oracle's, so the stored values agree to about one fp32 rounding even for
 // weights far larger than the paper's.
-__global__ void __launch_bounds__(CNN_THREADS) k_policy_cnn(DevParams p) {
-    extern __shared__ __align__(1024) unsigned char cnn_smem_raw[];
-    constexpr unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    unsigned char *base = cnn_smem_raw + (size_t)wib * CS_TOTAL_BYTES;
-    float *sw = reinterpret_cast<float *>(base);
-    double *sd = reinterpret_cast<double *>(base + CS_W_BYTES);
-    double *a1 = sd + CS_A1, *p1 = sd + CS_P1, *a2 = sd + CS_A2, *e = sd + CS_E;
-    uint32_t *rows = reinterpret_cast<uint32_t *>(base + CS_W_BYTES + CS_D_END * 8);
-    int32_t *cnt = reinterpret_cast<int32_t *>(base + CS_W_BYTES + CS_D_END * 8 + CS_ROWS_BYTES);
-    step_housekeeping(p);
-    PolicyCounters ctr;
-    const long total = (long)p.n_worlds * p.S;
-    const long nwarps = (long)gridDim.x * CNN_WARPS;
-    for (long v = (long)wib * gridDim.x + blockIdx.x; v < total; v += nwarps) {  // warp-uniform
-        const int w = (int)(v / p.S);
-        const int i = (int)(v - (long)w * p.S);
-        const int64_t t = p.t[w];
-        if (i >= *count_of(p, t, w)) continue;
-        const int slot = list_of(p, t, w)[i];
-        ECO_CHECK(slot >= 0 && slot < p.S);
-        const size_t gs = (size_t)w * p.S + slot;
-        // (1) the agent's parameters -> shared memory (616 x 16 B), in flight during (2)
-        const float *Wg = p.weights + gs * (size_t)CNN_PD;
-        for (int q = lane; q < CNN_PD / 4; q += 32) cp_async16(sw + 4 * q, Wg + 4 * q, 0);
-        cp_commit();
-        // (2) the window: lane l < 15 fetches R' row l, lane 16 + l fetches O_t row l
-        const int cellv = p.cell[gs];
-        ECO_CHECK(cellv >= 0 && cellv < p.H * p.W);
-        const int y = row_of(p, cellv), x = cellv - y * p.W;
-        {
-            const int rr = lane & 15;
-            uint32_t bits = 0u;
-            const int yy = y - CNN_R + rr;
-            if (rr < CNN_WO && yy >= 0 && yy < p.H) {
-                const uint32_t *pl = lane < 16 ? plane_next(p, t) + (size_t)w * plane_words(p)
-                                               : p.occ + (size_t)w * plane_words(p);
-                bits = row_bits(pl + (size_t)yy * p.WW, p.WW, x - CNN_R, CNN_WO);
-            }
-            rows[lane] = bits;
-        }
-        const float hold = lane < 4 ? p.h[gs * 4 + lane] : 0.f;
-        const float cold = lane < 4 ? p.c[gs * 4 + lane] : 0.f;
-        const int last = p.last_action[gs], ate = p.ate[gs];
-        __syncwarp();
-        // the agent channel (R39, R44): agents per window cell -- the O bits (0/1) under
-        // exclusive occupancy, the per-cell counts under co-location
-        int occupied = 0;
-        for (int idx = lane; idx < CNN_WO * CNN_WO; idx += 32) {
-            const int row = idx / CNN_WO, col = idx - row * CNN_WO;
-            const int yy = y - CNN_R + row, xx = x - CNN_R + col;
-            int n = 0;
-            if (p.coloc) {
-                if (yy >= 0 && yy < p.H && xx >= 0 && xx < p.W) n = p.ncount[(size_t)w * p.H * p.W + (size_t)yy * p.W + xx];
-            } else {
-                n = (int)((rows[16 + row] >> col) & 1u);
-            }
-            cnt[idx] = n;
-            occupied += n > 0;
-        }
-        cp_wait<0>();
-        __syncwarp();
-        // (3) conv1: positions lane and lane + 32 of the 8x8 output, 4 features each
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int pos = lane + 32 * half, oy = pos >> 3, ox = pos & 7;
-            double acc[4];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) acc[f] = (double)sw[CN_C1B + f];
-#pragma unroll
-            for (int ky = 0; ky < 3; ++ky) {
-                const int iy = 2 * oy + ky - 1;
-                if (iy < 0 || iy >= CNN_WO) continue;  // conv zero padding
-                const uint32_t rb = rows[iy];
-                const bool row_on = (y - CNN_R + iy) >= 0 && (y - CNN_R + iy) < p.H;
-#pragma unroll
-                for (int kx = 0; kx < 3; ++kx) {
-                    const int ix = 2 * ox + kx - 1;
-                    if (ix < 0 || ix >= CNN_WO) continue;
-                    const bool r = (rb >> ix) & 1u;
-                    const int o = cnt[iy * CNN_WO + ix];
-                    const bool wall = !(row_on && (x - CNN_R + ix) >= 0 && (x - CNN_R + ix) < p.W);
-                    const float *wk = sw + CN_C1W + (ky * 3 + kx) * 3;  // + f * 27 + channel
-#pragma unroll
-                    for (int f = 0; f < 4; ++f) {
-                        if (r) acc[f] += (double)wk[f * 27 + 0];
-                        if (o) acc[f] = fma((double)o, (double)wk[f * 27 + 1], acc[f]);  // o * w exact
-                        if (wall) acc[f] += (double)wk[f * 27 + 2];
-                    }
-                }
-            }
-#pragma unroll
-            for (int f = 0; f < 4; ++f) a1[pos * 4 + f] = acc[f];
-        }
-        __syncwarp();
-        // (4) pool1 -> 7x7x4 (196 values)
-        for (int idx = lane; idx < 196; idx += 32) {
-            const int py = idx / 28, rem = idx - py * 28, px = rem >> 2, f = rem & 3;
-            const double *b0 = a1 + (py * 8 + px) * 4 + f;
-            p1[idx] = (((b0[0] + b0[4]) + b0[32]) + b0[36]) / 4.0;
-        }
-        __syncwarp();
-        // (5) conv2: lane -> output position lane >> 1 (4x4), features 4 (lane & 1) .. + 3
-        {
-            const int q = lane >> 1, oy = q >> 2, ox = q & 3, g0 = (lane & 1) * 4;
-            double acc[4];
-#pragma unroll
-            for (int g = 0; g < 4; ++g) acc[g] = (double)sw[CN_C2B + g0 + g];
-#pragma unroll
-            for (int ky = 0; ky < 3; ++ky) {
-                const int iy = 2 * oy + ky - 1;
-                if (iy < 0 || iy >= 7) continue;
-#pragma unroll
-                for (int kx = 0; kx < 3; ++kx) {
-                    const int ix = 2 * ox + kx - 1;
-                    if (ix < 0 || ix >= 7) continue;
-                    const double *in = p1 + (iy * 7 + ix) * 4;
-                    const double i0 = in[0], i1 = in[1], i2 = in[2], i3 = in[3];
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const float4 wk = *reinterpret_cast<const float4 *>(
-                            sw + CN_C2W + ((g0 + g) * 9 + ky * 3 + kx) * 4);
-                        acc[g] = fma((double)wk.x, i0, acc[g]);
-                        acc[g] = fma((double)wk.y, i1, acc[g]);
-                        acc[g] = fma((double)wk.z, i2, acc[g]);
-                        acc[g] = fma((double)wk.w, i3, acc[g]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < 4; ++g) a2[q * 8 + g0 + g] = acc[g];
-        }
-        __syncwarp();
-        // (6) pool2 -> e[0..72); e[72..77) one-hot previous action, e[77] ate
-        for (int idx = lane; idx < 72; idx += 32) {
-            const int py = idx / 24, rem = idx - py * 24, px = rem >> 3, g = rem & 7;
-            const double *b0 = a2 + (py * 4 + px) * 8 + g;
-            e[idx] = (((b0[0] + b0[8]) + b0[32]) + b0[40]) / 4.0;
-        }
-        if (lane < 5) e[72 + lane] = lane == last ? 1.0 : 0.0;
-        if (lane == 5) e[77] = ate ? 1.0 : 0.0;
-        __syncwarp();
-        // (7) LSTM gate rows: lane -> row lane >> 1; the even lane sums e[0..41), the odd
-        // lane e[41..78) and W_hh h
-        double z;
-        {
-            double hb[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) hb[k] = (double)__shfl_sync(FULL, hold, k);
-            const int r = lane >> 1;
-            const bool odd = lane & 1;
-            const float *wr = sw + CN_WIH + r * 78;
-            double s = 0.0;
-            const int jb = odd ? 41 : 0, je = odd ? 78 : 41;
-            for (int j = jb; j < je; ++j) s = fma((double)wr[j], e[j], s);
-            if (odd) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) s = fma((double)sw[CN_WHH + r * 4 + k], hb[k], s);
-            }
-            s += __shfl_xor_sync(FULL, s, 1);
-            z = s + (double)sw[CN_B + r];
-        }
-        // unit k = lane & 3 on every lane: i = row k, f = 4 + k, g = 8 + k, o = 12 + k
-        const int k = lane & 3;
-        const double zi = __shfl_sync(FULL, z, 2 * k), zf = __shfl_sync(FULL, z, 2 * (4 + k));
-        const double zg = __shfl_sync(FULL, z, 2 * (8 + k)), zo = __shfl_sync(FULL, z, 2 * (12 + k));
-        const double ck = (double)__shfl_sync(FULL, cold, k);
-        const double cnd = sigmoid_d(zf) * ck + sigmoid_d(zi) * tanh(zg);
-        const float cn = (float)cnd;
-        const float hn = (float)(sigmoid_d(zo) * tanh(cnd));
-        if (lane < 4) {
-            p.h[gs * 4 + lane] = hn;
-            p.c[gs * 4 + lane] = cn;
-            e[78 + lane] = (double)hn;  // "we concatenate the embedding with the output of the LSTM"
-        }
-        bool bad = !isfinite(hn) || !isfinite(cn);
-        __syncwarp();
-        // (8) dense 82 -> 8 with tanh: lane -> row lane >> 2, inputs [21 (lane & 3), + 21)
-        double dv;
-        {
-            const int r = lane >> 2, j0 = (lane & 3) * 21, j1 = j0 + 21 < 82 ? j0 + 21 : 82;
-            const float *wr = sw + CN_WD + r * 82;
-            double s = 0.0;
-            for (int j = j0; j < j1; ++j) s = fma((double)wr[j], e[j], s);
-            s += __shfl_xor_sync(FULL, s, 1);
-            s += __shfl_xor_sync(FULL, s, 2);
-            dv = tanh(s + (double)sw[CN_BD + r]);
-        }
-        // (9) dense 8 -> 5 logits: lane a < 5
-        double lgd = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            const double dk = __shfl_sync(FULL, dv, 4 * kk);
-            if (lane < 5) lgd = fma((double)sw[CN_WO + lane * 8 + kk], dk, lgd);
-        }
-        const float lgv = lane < 5 ? (float)(lgd + (double)sw[CN_BO + lane]) : 0.f;
-        float lg[5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) lg[a] = __shfl_sync(FULL, lgv, a);
-        // window counters: active inputs (R and O bits), a resource in view (greediness)
-        const uint32_t rbits = lane < CNN_WO ? rows[lane] : 0u;
-        const unsigned nnz = __reduce_add_sync(FULL, (unsigned)(__popc(rbits) + occupied));
-        const unsigned seen = __reduce_or_sync(FULL, rbits);
-        bad = __any_sync(FULL, bad);
-        if (lane == 0) {
-            // (10) softmax(50 logits) sampled by inverse CDF (fp64 from the fp32 logits, R38)
-            double zmax = -INFINITY;
-#pragma unroll
-            for (int a = 0; a < 5; ++a) {
-                bad = bad || !isfinite(lg[a]);
-                p.logits[gs * LOGIT_STRIDE + a] = lg[a];
-                zmax = fmax(zmax, 50.0 * (double)lg[a]);
-            }
-            double pr[5], S = 0.0;
-#pragma unroll
-            for (int a = 0; a < 5; ++a) {
-                pr[a] = exp(50.0 * (double)lg[a] - zmax);
-                S += pr[a];
-            }
-            // keyed by the cell (unique under exclusive occupancy, R9), by the slot under co-location (R47)
-            const uint4 d = draw4(p.seeds[w], PURPOSE_ACTION, (uint32_t)t, (uint32_t)(p.coloc ? slot : cellv), 0u);
-            const double u = (double)d.x * 2.3283064365386963e-10;
-            int act = 4;
-            double cum = 0.0, margin = INFINITY;
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                cum += pr[a] / S;
-                margin = fmin(margin, fabs(u - cum));
-                if (act == 4 && u < cum) act = a;
-            }
-            ctr.add(p, w, nnz, margin < 1e-4);
-#if ECO_GREED
-            if (seen) p.gr_seen[gs] = 1;
-#endif
-            agent_commit<false>(p, w, i, slot, gs, t, cellv, act, *p.forced_on, [&](int a) {
-                return ((rows[16 + CNN_R + kDY[a]] >> (CNN_R + kDX[a])) & 1u) != 0u;
-            });
-            if (bad) *reinterpret_cast<volatile int32_t *>(p.nonfinite) = 1;
-        }
-        __syncwarp();  // the slices are rewritten by the warp's next agent
-    }
-    if (lane == 0) ctr.flush(p);
-}
-
-
 // ---------------------------------------------------------------------------------------
-// k_policy_cnn_blk: the same computation with one BLOCK of CNN_BLK_THREADS per agent.  At the
-// paper world's populations (a few hundred agents, far fewer than the GPU's warp slots) the
-// per-agent chain of dependent fp64 operations is the step's critical path, so every layer
-// is spread over 4 warps: conv1 2 outputs per thread, conv2 1 output (36 FMAs) per thread,
+// k_policy_cnn_blk: one BLOCK of CNN_BLK_THREADS per agent.  At the paper world's populations
+// (a few hundred agents, far fewer than the GPU's warp slots) the per-agent chain of
+// dependent fp64 operations is the step's critical path, so every layer is spread over 4
+// warps (one warp per agent -- the first version, in git history -- took 19.5 instead of
+// 16.5 us per launch): conv1 2 outputs per thread, conv2 1 output (36 FMAs) per thread,
 // the LSTM's 16 rows over 8 threads each, dense 8 over 16 threads each, the 5 exponentials of
 // the softmax on 5 threads.  Sums are split into fixed contiguous parts reduced in a fixed
 // order (fp64; the stored h', c', logits stay within an fp32 rounding of the oracle's).

@@ -824,15 +824,11 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 
 #include "policy_cnn.cuh"
 
-#ifndef ECO_CNN_BLOCK
-#define ECO_CNN_BLOCK 1  // network 1: one block per agent (k_policy_cnn_blk); 0: one warp per agent
-#endif
 cudaError_t policy_occupancy(int hidden, int net, int *blocks_per_sm, int *threads_out) {
-    const int threads = net == 1 ? (ECO_CNN_BLOCK ? CNN_BLK_THREADS : CNN_THREADS) : 256;
+    const int threads = net == 1 ? CNN_BLK_THREADS : 256;
     *threads_out = threads;
     if (net == 1)
-        return ECO_CNN_BLOCK ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_cnn_blk, CNN_BLK_THREADS, CNN_BLK_SMEM)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_cnn, CNN_THREADS, CNN_SMEM);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_cnn_blk, CNN_BLK_THREADS, CNN_BLK_SMEM);
     switch (hidden) {
         case 4: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<4>, threads, 0);
         case 8: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_policy_reg<8>, threads, 0);
@@ -844,8 +840,6 @@ cudaError_t policy_occupancy(int hidden, int net, int *blocks_per_sm, int *threa
 
 cudaError_t policy_prepare() {
     cudaError_t e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_cnn, cudaFuncAttributeMaxDynamicSharedMemorySize, CNN_SMEM);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_policy_cnn_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, CNN_BLK_SMEM);
     if (e != cudaSuccess) return e;
@@ -862,8 +856,7 @@ cudaError_t policy_prepare() {
 
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl) {
     if (p.net == 1) {
-        if (ECO_CNN_BLOCK) k_policy_cnn_blk<<<lc.policy_blocks, CNN_BLK_THREADS, CNN_BLK_SMEM, s>>>(p);
-        else k_policy_cnn<<<lc.policy_blocks, CNN_THREADS, CNN_SMEM, s>>>(p);
+        k_policy_cnn_blk<<<lc.policy_blocks, CNN_BLK_THREADS, CNN_BLK_SMEM, s>>>(p);
         return cudaGetLastError();
     }
     switch (p.Hd) {
