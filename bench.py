@@ -199,7 +199,7 @@ def policy_bytes(wc, agents: int, nnz: int, split: bool = None) -> int:
     claims per agent, and either W_hh and b (unsplit) or the agent's P row (split)."""
     Hd = wc.hidden
     if getattr(wc, "network", 0) == 1:
-        # the paper's CNN-LSTM (k_policy_cnn): every agent reads its whole parameter row
+        # the paper's CNN-LSTM (k_policy_cnn_blk): every agent reads its whole parameter row
         # (2445 floats), h and c read and written, 32 B of SoA fields and the claim
         return agents * (4 * wc.n_params + 16 * Hd + 32)
     split = split_policy(wc) if split is None else split
@@ -421,7 +421,7 @@ def run_ours(args, rank, world_size, local_rank):
             gk = kern["graph_kernel_ms_total"]
             gstep = gk["policy"] + gk["post"]
             cands = {
-                "policy": (("k_policy_cnn (15x15x3 window + the paper's CNN-LSTM + softmax sampling + move claim)"
+                "policy": (("k_policy_cnn_blk (15x15x3 window + the paper's CNN-LSTM + softmax sampling + move claim)"
                             if getattr(wc, "network", 0) else
                             "k_policy_half (observe + LSTM gates from P + argmax + move claim)" if wc.hidden == 32 else
                             f"k_policy_reg<{wc.hidden}> (observe + LSTM + argmax + move claim)"),

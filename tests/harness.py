@@ -140,7 +140,7 @@ def lockstep_sampled(world, orc: "oracle.OracleWorld", steps: int, check_weights
     to them; integer state and records bit-exact, floats within R27; and the GPU's OWN
     sampled action of every agent alive at the step's start (sim_get_policy_actions) equals
     the oracle's except where either side's sampling margin |u - CDF| is below 1e-4.
-    k_policy_cnn evaluates the network in fp64 like the oracle (only the summation order
+    k_policy_cnn_blk evaluates the network in fp64 like the oracle (only the summation order
     differs), so beyond R27 its stored h', c' and logits must be within `max_ulp` fp32 ulps.
     Returns (near_tie_disagreements, n_compared_agent_steps, one_ulp_weights)."""
     from paper_2302_09334_b200.sim import STATE_FIELDS

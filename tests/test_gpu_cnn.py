@@ -1,5 +1,5 @@
 """GPU parity of network 1, the paper's CNN-LSTM with softmax sampling (
-SURVEY.md §8(f) NEXT-2; k_policy_cnn) against the oracle, through the C ABI.
+SURVEY.md §8(f) NEXT-2; k_policy_cnn_blk) against the oracle, through the C ABI.
 
 Integer state, step records and slot layout bit-exact; h', c', logits within R27; weights
 bit-exact up to counted 1-ulp differences (R29); the kernel's own sampled actions

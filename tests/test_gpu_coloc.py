@@ -1,6 +1,6 @@
 """GPU parity of co-location (the paper's reproduction on the
 parent's cell; any number of agents per cell; R43-R47) with the
-paper's network (k_policy_cnn + coloc.cuh) against the oracle, through the C ABI: integer
+paper's network (k_policy_cnn_blk + coloc.cuh) against the oracle, through the C ABI: integer
 state, records and slot layout bit-exact, h', c', logits within 1 ulp, the kernel's own
 sampled actions equal to the oracle's except at flagged near-ties."""
 import numpy as np
