@@ -70,3 +70,24 @@ def test_lab_batch_on_gpu():
     p = lab.pressure_experiment(base, genomes, cfg, densities=("high",))
     assert int(p["high"]["arms"]["off"]["births"].sum()) == 0
     assert p["high"]["mean_on"] >= 0 and p["high"]["mean_off"] >= 0
+
+
+@pytest.mark.gpu
+def test_lab_with_the_papers_agents():
+    """The paper's pipeline end to end on the device: a natural run of the paper's world with
+    its own network and same-cell reproduction (paper_world_coloc), genomes sampled from it,
+    the greediness experiment over the three densities (each agent classified by ANOVA +
+    Tukey, §3.3.1) and the peer-pressure arms (§3.3.2) -- with the 2,445-parameter
+    CNN-LSTM genomes, sampled actions and co-location."""
+    from paper_2302_09334_b200 import sim
+    base = workloads.paper_world_coloc()
+    nat = sim.World(base)
+    nat.step(300)
+    genomes = lab.sample_genomes(nat.get_state(), 3, seed=2)
+    nat.destroy()
+    assert genomes.shape == (3, 2445)
+    cfg = lab.LabConfig(trial_steps=200, trials=3)
+    res = lab.greediness_experiment(base, genomes, cfg)
+    assert len(res["agents"]) == 3 and all("class" in a for a in res["agents"])
+    p = lab.pressure_experiment(base, genomes, cfg, densities=("high",))
+    assert int(p["high"]["arms"]["off"]["births"].sum()) == 0
