@@ -119,6 +119,29 @@ class Reducer:
     def sum(self, v: float) -> float:
         return self._all(v, None if self.dist is None else self.dist.ReduceOp.SUM)
 
+    def sum_array(self, a: np.ndarray) -> np.ndarray:
+        """Element-wise int64 SUM over ranks (NCCL on the device / gloo on the CPU)."""
+        if self.dist is None:
+            return np.asarray(a, np.int64).copy()
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return t.cpu().numpy()
+
+
+def ensemble_end_stats(seeds_all, seeds_mine, last_records, red: Reducer) -> dict:
+    """SURVEY.md §8(e) E.1 / north_star (ii): the only cross-GPU traffic of the ensemble, its
+    end-of-run statistics -- each world's population and resource total after the run, placed
+    in the row of its seed (zero rows elsewhere) and SUM-reduced over the ranks."""
+    idx = {s: k for k, s in enumerate(seeds_all)}
+    tab = np.zeros((len(seeds_all), 2), np.int64)
+    for s, rec in zip(seeds_mine, last_records):
+        tab[idx[s]] = (int(rec["population"]), int(rec["resources"]))
+    tab = red.sum_array(tab)
+    return {"worlds": len(seeds_all), "population_total": int(tab[:, 0].sum()),
+            "resources_total": int(tab[:, 1].sum()), "population_min_max": [int(tab[:, 0].min()), int(tab[:, 0].max())],
+            "extinct_worlds": int((tab[:, 0] == 0).sum()), "per_world": tab.tolist()}
+
 
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -314,6 +337,8 @@ def run_ours(args, rank, world_size, local_rank):
         nnz = int(log["obs_nnz"].sum())
         births = int(log["births"].sum())
         max_ms = allmax(total_ms)
+        ens_stats = (ensemble_end_stats(workloads.ensemble().seeds, wc.seeds, log[-1], red)
+                     if args.config == "ensemble" else None)
         all_agents = agents if sharded else allsum(agents)  # sharded: one world, counted once
         value = all_agents / (max_ms / 1e3)
         cells = K * wc.rows * wc.cols * wc.n_worlds
@@ -400,6 +425,8 @@ def run_ours(args, rank, world_size, local_rank):
                "L2-persisting, so the flush cannot evict it; the weights stream from HBM every step"),
             "cell_updates_per_s": cells * (1 if sharded else world_size) / (max_ms / 1e3),
             "agents_mean": agents / K,
+            **({"ensemble_end_stats": {k_: v_ for k_, v_ in ens_stats.items() if k_ != "per_world"}}
+               if ens_stats else {}),
             # the paper's own timing is of its own world with its own network (1e6
             # steps in ~20 min on an unnamed GPU with JAX, ~833 world steps/s): context for the
             # paper-world configs, not vs_baseline (BASELINE.json publishes no number)

@@ -187,3 +187,30 @@ def test_band_rows_helpers():
     rows = banded.agent_weighted_rows(np.full(100, 7), 40, 8)
     assert all(b - a >= 3 for a, b in zip(rows, rows[1:])) and rows[-1] == 40
     assert list(banded.band_of_rows([0, 5, 9, 20], [0, 4, 5, 8, 9, 19])) == [0, 0, 1, 1, 2, 2]
+
+
+def _ens_stats_worker(rank, world_size, port, path):
+    """bench.ensemble_end_stats on gloo: each rank fills the rows of its own worlds' seeds
+    with their (population, resources); the SUM-reduction leaves every world's row on every
+    rank."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        seeds = workloads.ensemble().seeds
+        mine = workloads.ensemble_shard(world_size, rank)
+        recs = [{"population": 1000 + s, "resources": 7 * s} for s in mine]
+        st = bench.ensemble_end_stats(seeds, mine, recs, bench.Reducer(dist, "cpu"))
+        if rank == 0:
+            np.save(path, np.array([st["population_total"], st["resources_total"], st["worlds"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ensemble_end_stats_reduce_over_two_gloo_ranks():
+    import torch.multiprocessing as mp
+    path = os.path.join(tempfile.mkdtemp(), "ens.npy")
+    mp.spawn(_ens_stats_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    got = np.load(path)
+    seeds = workloads.ensemble().seeds
+    assert list(got) == [sum(1000 + s for s in seeds), sum(7 * s for s in seeds), 64]
