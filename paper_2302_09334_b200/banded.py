@@ -91,6 +91,31 @@ def merge_band_states(states: list, band_rows, cols: int) -> dict:
     return out
 
 
+def rebalanced(world, min_rows: int = 3, band_slots: int = 0):
+    """Agent-weighted rebalancing of a banded world whose bands are all on this GPU (SURVEY.md
+    §8(e) E.2 "rebalance by agent count"): the state is read out (sim_get_state merges the
+    bands keyed by cell), a new banded handle is created with row boundaries giving every
+    band about 1/G of the live agents (agent_weighted_rows) and the state is written in
+    (sim_set_state splits it); the old handle is destroyed.  The trajectory continues
+    exactly as the unbanded world's (cells, not slots, key every draw, R9).  The new handle's
+    step log starts at the rebalancing step and the movement windows in progress are not
+    measured (as after any sim_set_state).  Returns the new sim.World."""
+    if not world.bands:
+        raise ValueError("rebalanced() needs a banded world")
+    G = int(world.bands["n_bands"])
+    st = world.get_state()
+    live = st["alive"][0] == 1
+    rows = agent_weighted_rows(st["cell"][0][live] // world.wc.cols, world.wc.rows, G, min_rows)
+    bands = dict(world.bands, band_rows=rows)
+    if band_slots:
+        bands["band_slots"] = band_slots
+    new = sim.World(world.wc, device=world.device, stream=world.stream, log_capacity=world.log_capacity,
+                    bands=bands)
+    world.destroy()
+    new.set_state(st)
+    return new
+
+
 class BandedWorld:
     """This rank's band of one world split over the ranks of `dist` (one band per GPU)."""
 

@@ -240,6 +240,7 @@ class World:
         dict(n_bands=4) for four bands on this GPU (see paper_2302_09334_b200.banded)."""
         self.wc = wc
         self.device = device
+        self.stream = stream
         self.n_worlds = len(wc.seeds)
         self.bands = dict(bands) if bands else None
         self._cfg, self._seeds = make_config(wc, device, stream, log_capacity, bands)

@@ -124,3 +124,29 @@ def test_banded_invalid_rows():
     with pytest.raises(sim.SimError) as ei:
         sim.World(wc, bands=dict(n_bands=2, band_rows=[0, 2, 200]))
     assert ei.value.status == sim.SIM_E_INVALID
+
+
+def test_banded_rebalance_continues_the_unbanded_trajectory():
+    """banded.rebalanced(): equal rows for 80 steps, then agent-weighted rows (the population
+    gathers at the rich bottom rows), 80 more steps -- keyed by cell equal to the unbanded
+    world at every checkpoint, the records of the second half equal."""
+    from paper_2302_09334_b200 import banded
+    wc = workloads.paper_scale()
+    ref = sim.World(wc)
+    ban = sim.World(wc, bands=dict(n_bands=4))
+    ref.step(80)
+    ban.step(80)
+    compare_by_cell(ref.get_state(), ban.get_state(), "t=80")
+    ban = banded.rebalanced(ban)
+    rows = ban.bands["band_rows"]
+    assert rows != banded.equal_band_rows(wc.rows, 4)
+    compare_by_cell(ref.get_state(), ban.get_state(), "rebalanced t=80")
+    for k in range(4):
+        ref.step(20)
+        ban.step(20)
+        compare_by_cell(ref.get_state(), ban.get_state(), f"t={100 + 20 * k}")
+    lr, lb = ref.step_log(80, 80)[:, 0], ban.step_log(80, 80)[:, 0]
+    for f in sim.RECORD_FIELDS:
+        assert np.array_equal(lr[f], lb[f]), f
+    ref.destroy()
+    ban.destroy()
