@@ -29,7 +29,7 @@ def main():
     import torch
     wc = getattr(workloads, a.config)()
     s = torch.cuda.Stream()
-    world = sim.World(wc, stream=s, log_capacity=a.chunk)
+    world = sim.World(wc, stream=s, log_capacity=2 * a.chunk)
     pop, res, births, deaths, walls = [], [], [], [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dev_ms = 0.0
