@@ -112,3 +112,31 @@ def test_coloc_batch_equals_single_worlds_and_instrumented_path():
             assert np.array_equal(np.asarray(a[f])[0], np.asarray(b[f])[k]), (s, f)
         one.destroy()
     batch.destroy()
+
+
+@pytest.mark.parametrize("cfg", ["paper_world_cnn", "paper_world_coloc"])
+def test_network1_determinism_resume_and_instrumented_path(cfg):
+    """The paper's network, exclusive and co-located: two runs are bitwise equal; a run
+    resumed by sim_set_state from its own state at t = 70 equals the uninterrupted run at
+    t = 140 (every field, weights included); the instrumented path (one kernel per phase)
+    equals the graph path."""
+    wc = small() if cfg == "paper_world_coloc" else workloads.paper_world_cnn().replace(
+        rows=40, cols=60, slots=300, n_initial=150, repr_steps=20, seeds=(17,))
+    a, b = sim.World(wc), sim.World(wc)
+    a.step(70)
+    mid = a.get_state()
+    a.step(70)
+    for _ in range(70):
+        b.step_timed()
+    b.step(70)
+    sa, sb = a.get_state(), b.get_state()
+    for f in sim.STATE_FIELDS:
+        assert np.array_equal(np.asarray(sa[f]), np.asarray(sb[f])), f
+    c = sim.World(wc)
+    c.set_state(mid)
+    c.step(70)
+    sc = c.get_state()
+    for f in sim.STATE_FIELDS:
+        assert np.array_equal(np.asarray(sa[f]), np.asarray(sc[f])), ("resume", f)
+    for w in (a, b, c):
+        w.destroy()
