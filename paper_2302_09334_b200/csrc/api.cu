@@ -12,6 +12,22 @@
 
 #include "sim_internal.cuh"
 
+// Tracing: NVTX ranges around the ABI's calls and the banded step's phases,
+// visible in nsys / ncu timelines; free when no tool is attached (ECO_NVTX=0 compiles them out).
+#ifndef ECO_NVTX
+#define ECO_NVTX 1
+#endif
+#if ECO_NVTX
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define ECO_TRACE(name) NvtxRange eco_trace_range_(name)
+#else
+#define ECO_TRACE(name) ((void)0)
+#endif
+
 using eco::DevParams;
 
 namespace {
@@ -723,6 +739,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
 extern "C" {
 
 sim_status sim_create(const sim_config *cfg, sim_handle *out) {
+    ECO_TRACE("sim_create");
     if (cfg && cfg->abi_version == SIM_ABI_VERSION && cfg->struct_size == sizeof(sim_config) && cfg->n_bands > 1)
         return create_banded(cfg, out);
     return create_one(cfg, nullptr, out);
@@ -736,6 +753,7 @@ sim_status sim_destroy(sim_handle h) {
 }
 
 sim_status sim_step(sim_handle h, int64_t n) {
+    ECO_TRACE("sim_step");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (n < 0) return fail(SIM_E_INVALID, "invalid argument: n < 0");
@@ -862,6 +880,7 @@ sim_status sim_synchronize(sim_handle h) {
 }
 
 sim_status sim_get_state(sim_handle h, sim_state *out) {
+    ECO_TRACE("sim_get_state");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!out) return fail(SIM_E_INVALID, "invalid argument: out (NULL)");
@@ -917,6 +936,7 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
 }
 
 sim_status sim_set_state(sim_handle h, const sim_state *in) {
+    ECO_TRACE("sim_set_state");
     sim_status st = check_handle(h);
     if (st != SIM_OK) return st;
     if (!in) return fail(SIM_E_INVALID, "invalid argument: in (NULL)");
