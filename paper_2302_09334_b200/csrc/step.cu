@@ -942,7 +942,11 @@ __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
 // writes in the barrier's release fence; the regrowth's plane writes (measured: +3..6 us of
 // fence when they preceded a barrier) go last, where only the kernel's end waits for them.
 #ifndef ECO_POST_THREADS
-#define ECO_POST_THREADS 1024
+// 24 warps per block (4 P warps + 20 dynamics warps at paper scale): fewer idle warps in every
+// block barrier of the latency-bound phases.  Measured (round 2): 1024 -> 768 threads: the
+// driver's t = 5..25 33.2 -> 31.7 us, 10,000 steps 48.4 -> 46.7 us, large world 1.522 ->
+// 1.514 ms; 512 / 640 / 896 no better overall
+#define ECO_POST_THREADS 768
 #endif
 constexpr int POST_THREADS = ECO_POST_THREADS;
 #ifndef ECO_MUT_WARM
