@@ -19,6 +19,11 @@
 //               (and the metrics windows ending here)
 // then k_mutate and k_regrow of step t+1.
 
+#ifndef ECO_CO_THREADS
+#define ECO_CO_THREADS 1024  // threads per block of k_co_rank and k_post_co
+#endif
+constexpr int CO_THREADS = ECO_CO_THREADS;
+
 __device__ __forceinline__ void co_move_phase(const DevParams &p, size_t gtid, size_t gthreads) {
     const long total = (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
@@ -161,7 +166,7 @@ __device__ void co_rank_lists(const DevParams &p, int w, int n_place, uint32_t *
 }
 
 // World w's rank, placement, counters, t += 1, then its movement / greediness windows ending
-// here; all RANK_THREADS threads of one block.
+// here; all CO_THREADS threads of one block.
 __device__ __forceinline__ void co_rank_world(const DevParams &p, int w, uint32_t *scratch, int *s_free, int *s_par,
                                               int *s_mv) {
     const size_t HW = (size_t)p.H * p.W;
@@ -169,8 +174,8 @@ __device__ __forceinline__ void co_rank_world(const DevParams &p, int w, uint32_
     const RankCounts k = rank_counts(p, w, t);  // n_win = eligible parents (k_co_live)
     const size_t ws = (size_t)w * p.S;
     int32_t *g_free = p.free_list + ws, *g_par = p.birth_parent + ws;
-    if (k.n_place > 0) co_rank_lists<RANK_THREADS>(p, w, k.n_place, scratch, s_free, s_par, g_free, g_par);
-    for (int r = threadIdx.x; r < k.n_place; r += RANK_THREADS) {
+    if (k.n_place > 0) co_rank_lists<CO_THREADS>(p, w, k.n_place, scratch, s_free, s_par, g_free, g_par);
+    for (int r = threadIdx.x; r < k.n_place; r += CO_THREADS) {
         const bool sm = r < RANK_SMEM_CAP;
         const int child = sm ? s_free[r] : *reinterpret_cast<volatile int32_t *>(g_free + r);
         const int par = sm ? s_par[r] : *reinterpret_cast<volatile int32_t *>(g_par + r);
@@ -182,11 +187,11 @@ __device__ __forceinline__ void co_rank_world(const DevParams &p, int w, uint32_
         p.birth_cell[ws + r] = child;  // the mutation's Philox entity: the child's slot (R47)
     }
     // the lottery words of this step's cells, and the eligible bitmap, back to zero
-    for (int i = threadIdx.x; i < k.n_start; i += RANK_THREADS) {
+    for (int i = threadIdx.x; i < k.n_start; i += CO_THREADS) {
         const int4 mr = p.mrec[ws + i];
         if (mr.z != WALL_TARGET) p.claim[(size_t)w * HW + mr.w] = 0ull;
     }
-    for (int j = threadIdx.x; j < p.SW; j += RANK_THREADS) p.elig_bits[(size_t)w * p.SW + j] = 0u;
+    for (int j = threadIdx.x; j < p.SW; j += CO_THREADS) p.elig_bits[(size_t)w * p.SW + j] = 0u;
     __syncthreads();
     if (threadIdx.x == 0) {
         p.n_births[w] = k.n_place;
@@ -203,8 +208,8 @@ __device__ __forceinline__ void co_rank_world(const DevParams &p, int w, uint32_
 // One block per world.  (The regrowth of step t+1 is a separate launch in the instrumented
 // path: a block regrowing beside this one could start after t advanced; k_post_co reads t
 // first and keeps every block resident.)
-__global__ void __launch_bounds__(RANK_THREADS) k_co_rank(DevParams p) {
-    __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
+__global__ void __launch_bounds__(CO_THREADS) k_co_rank(DevParams p) {
+    __shared__ uint32_t scratch[2 * (CO_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     __shared__ int s_mv[SIM_MOVE_BINS];
     for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x) co_rank_world(p, w, scratch, s_free, s_par, s_mv);
@@ -221,8 +226,8 @@ __global__ void __launch_bounds__(256) k_co_live(DevParams p) {
 // phases separated by grid barriers instead of kernel boundaries: move | live | rank (one
 // block per world) beside the regrowth of step t+1 (the other blocks; t read before any
 // block advances it) | mutation.
-__global__ void __launch_bounds__(RANK_THREADS) k_post_co(DevParams p, unsigned long long *bar) {
-    __shared__ uint32_t scratch[2 * (RANK_THREADS / 32 + 1)];
+__global__ void __launch_bounds__(CO_THREADS) k_post_co(DevParams p, unsigned long long *bar) {
+    __shared__ uint32_t scratch[2 * (CO_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     __shared__ int s_mv[SIM_MOVE_BINS];
     unsigned long long target = grid_sync_base(bar);

@@ -1574,7 +1574,7 @@ cudaError_t launch_birth_claim(const DevParams &p, const LaunchCfg &lc, cudaStre
 
 cudaError_t launch_birth_rank(const DevParams &p, cudaStream_t s) {
     if (p.coloc) {  // (the regrowth of step t+1 is graph mode's: launch_post)
-        k_co_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
+        k_co_rank<<<p.n_worlds, CO_THREADS, 0, s>>>(p);
         return cudaGetLastError();
     }
     k_birth_rank<<<p.n_worlds, RANK_THREADS, 0, s>>>(p);
@@ -1661,7 +1661,7 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
         if (p.S == 0) return launch_regrow(p, 0, s);
         cudaLaunchConfig_t cc = {};
         cc.gridDim = dim3(lc.post_blocks);
-        cc.blockDim = dim3(RANK_THREADS);
+        cc.blockDim = dim3(CO_THREADS);
         cc.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeCooperative;
