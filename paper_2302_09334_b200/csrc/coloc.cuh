@@ -20,7 +20,7 @@
 // then k_mutate and k_regrow of step t+1.
 
 #ifndef ECO_CO_THREADS
-#define ECO_CO_THREADS 1024  // threads per block of k_co_rank and k_post_co
+#define ECO_CO_THREADS 384  // threads per block of k_co_rank and k_post_co (measured: 1024 34.4, 768 32.6, 512 31.0, 384 30.8, 256 32.7 us per step)
 #endif
 constexpr int CO_THREADS = ECO_CO_THREADS;
 
