@@ -263,7 +263,10 @@ __global__ void k_band_pack(DevParams p, BandParams bp) {
 // One block: the neighbours' migrants towards this band take the first free local slots in
 // ascending order (alive bitmap scan); slots, alive flags and the P5 list are written here,
 // the records are copied by k_band_arrive_copy.
-constexpr int BAND_NT = 1024;
+#ifndef ECO_BAND_NT
+#define ECO_BAND_NT 1024  // threads of the one-block band kernels (arrivals, rank)
+#endif
+constexpr int BAND_NT = ECO_BAND_NT;
 __global__ void __launch_bounds__(BAND_NT) k_band_arrive(DevParams p, BandParams bp) {
     __shared__ uint32_t scratch[2 * (BAND_NT / 32 + 1)];
     const int ms = mig_stride(p.Hd, p.Pd);
