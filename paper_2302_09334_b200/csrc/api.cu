@@ -231,6 +231,8 @@ struct sim_ctx {
     float *wcanon = nullptr;
     size_t wcanon_rows = 0;
     int32_t *bad_host = nullptr;  // mapped: a non-finite weight seen by the gather
+    float *lstage = nullptr;  // set_state: the caller's [n][5] logits before the restride
+    size_t lstage_n = 0;
     // banded mode (band.cu): a banded handle drives its local bands,
     // each a sub-context holding the global grid and its own rows' agents
     std::vector<sim_ctx *> bands;   // parent: the local bands in band order
@@ -447,6 +449,7 @@ void destroy_all(sim_ctx *h) {
     for (void *v : h->allocs) cudaFree(v);
     if (h->wstage) cudaFree(h->wstage);
     if (h->wcanon) cudaFree(h->wcanon);
+    if (h->lstage) cudaFree(h->lstage);
     if (h->nonfinite_host) cudaFreeHost(h->nonfinite_host);
     if (h->bad_host) cudaFreeHost(h->bad_host);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -914,9 +917,14 @@ sim_status sim_get_state(sim_handle h, sim_state *out) {
     CK(h, get(out->ate, p.ate, nw * S), "ate");
     CK(h, get(out->h, p.h, nw * S * d.Hd * 4), "h");
     CK(h, get(out->c, p.c, nw * S * d.Hd * 4), "c");
-    if (out->logits && S)
-        CK(h, cudaMemcpy2DAsync(out->logits, 5 * 4, p.logits, eco::LOGIT_STRIDE * 4, 5 * 4, nw * S,
-                                cudaMemcpyDeviceToHost, s), "logits");
+    if (out->logits && S) {
+        float *tmp;
+        CK(h, cudaMallocAsync(reinterpret_cast<void **>(&tmp), nw * S * 5 * 4, s), "alloc");
+        cudaError_t e = eco::launch_logits_restride(tmp, 5, p.logits, eco::LOGIT_STRIDE, nw * S, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out->logits, tmp, nw * S * 5 * 4, cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(tmp, s);
+        CK(h, e, "logits");
+    }
     if (out->weights && S) {
         const size_t total_agents = nw * S;
         const size_t chunk = ((size_t)1 << 26) / (size_t)d.P > 0 ? ((size_t)1 << 26) / (size_t)d.P : 1;
@@ -1049,9 +1057,11 @@ sim_status sim_set_state(sim_handle h, const sim_state *in) {
     CK(h, put(p.ate, in->ate, nw * S), "ate");
     CK(h, put(p.h, in->h, nw * S * d.Hd * 4), "h");
     CK(h, put(p.c, in->c, nw * S * d.Hd * 4), "c");
-    if (in->logits && S)
-        CK(h, cudaMemcpy2DAsync(p.logits, eco::LOGIT_STRIDE * 4, in->logits, 5 * 4, 5 * 4, nw * S,
-                                cudaMemcpyHostToDevice, s), "logits");
+    if (in->logits && S) {
+        CK(h, ensure_rows(&h->lstage, &h->lstage_n, nw * S, 5), "alloc staging");
+        CK(h, cudaMemcpyAsync(h->lstage, in->logits, nw * S * 5 * 4, cudaMemcpyHostToDevice, s), "logits");
+        CK(h, eco::launch_logits_restride(p.logits, eco::LOGIT_STRIDE, h->lstage, 5, nw * S, s), "logits");
+    }
     if (n_live > 0) CK(h, eco::launch_weights_scatter(p, h->wstage, h->live_dev, n_live, s), "weights scatter");
     // scratch and derived structures
     if (S) {

@@ -41,7 +41,22 @@
 #define ECO_STEP2_PDL 1
 #endif
 
+// The step kernels' preferred shared-memory carveout (percent of the unified L1/shared
+// array; -1 = the driver's choice).  One value for every kernel of a step, so consecutive
+// kernels never make an SM drain and reconfigure between them.
+#ifndef ECO_CARVEOUT
+#define ECO_CARVEOUT -1
+#endif
+
 namespace eco {
+
+// dynamic shared memory limit and the common carveout (ECO_CARVEOUT) of a kernel
+template <class K>
+inline cudaError_t set_dyn_smem(K k, int bytes) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess || ECO_CARVEOUT < 0) return e;
+    return cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, ECO_CARVEOUT);
+}
 
 constexpr uint32_t PURPOSE_INIT_RES = 1, PURPOSE_INIT_PLACE = 2, PURPOSE_INIT_W = 3, PURPOSE_REGROW = 4,
                    PURPOSE_MOVE = 5, PURPOSE_BIRTH = 6, PURPOSE_MUTATE = 7,
@@ -399,6 +414,8 @@ cudaError_t launch_mv_pass(const DevParams &p, cudaStream_t s);  // movement his
 // state conversion (canonical <-> device)
 cudaError_t launch_pack_resources(const DevParams &p, const uint8_t *bytes, cudaStream_t s);
 cudaError_t launch_unpack_resources(const DevParams &p, uint8_t *bytes, cudaStream_t s);
+cudaError_t launch_logits_restride(float *dst, int dst_stride, const float *src, int src_stride, size_t n,
+                                   cudaStream_t s);
 cudaError_t launch_weights_to_device(const DevParams &p, const float *canon, size_t first_agent, size_t n_agents,
                                      cudaStream_t s);
 cudaError_t launch_weights_gather(const DevParams &p, const float *src, bool by_slot, const int32_t *live, int n_live,

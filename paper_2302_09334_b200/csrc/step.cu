@@ -839,19 +839,19 @@ cudaError_t policy_occupancy(int hidden, int net, int *blocks_per_sm, int *threa
 }
 
 cudaError_t policy_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(k_policy_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    cudaError_t e = set_dyn_smem(k_policy_half<true>, HALF_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_cnn_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, CNN_BLK_SMEM);
+    e = set_dyn_smem(k_policy_cnn_blk, CNN_BLK_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_half<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    e = set_dyn_smem(k_policy_half<false, true>, HALF_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_policy_half<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    e = set_dyn_smem(k_policy_half<true, true>, HALF_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_prepare_p, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    e = set_dyn_smem(k_prepare_p, HALF_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_prepare_p_snap, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    e = set_dyn_smem(k_prepare_p_snap, HALF_SMEM);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_policy_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, HALF_SMEM);
+    return set_dyn_smem(k_policy_half<false>, HALF_SMEM);
 }
 
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl) {
@@ -1532,7 +1532,7 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
     if (regrow_tiled(p)) {
         static int bps = 0;
         if (bps == 0) {
-            cudaFuncSetAttribute(k_regrow_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, RG_DYN_SMEM);
+            set_dyn_smem(k_regrow_tiled, RG_DYN_SMEM);
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_regrow_tiled, RG_THREADS, RG_DYN_SMEM);
             if (e != cudaSuccess || bps < 1) bps = 4;
         }
@@ -1643,17 +1643,19 @@ cudaError_t post_occupancy(int *blocks_per_sm) {
 }
 
 cudaError_t post_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(k_post<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
+    cudaError_t e = set_dyn_smem(k_post_co, 0);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_post<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    e = set_dyn_smem(k_post<true>, POST_SMEM_SMALL);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_post<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    e = set_dyn_smem(k_post<false, true>, POST_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_post<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
+    e = set_dyn_smem(k_post<true, true>, POST_SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_post<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM);
+    e = set_dyn_smem(k_post<false, false, true>, POST_SMEM_SMALL);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_post<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, POST_SMEM_SMALL);
+    e = set_dyn_smem(k_post<false, true, true>, POST_SMEM);
+    if (e != cudaSuccess) return e;
+    return set_dyn_smem(k_post<false>, POST_SMEM_SMALL);
 }
 
 cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long long *bar, cudaStream_t s) {

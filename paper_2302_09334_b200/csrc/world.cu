@@ -227,6 +227,23 @@ cudaError_t launch_unpack_resources(const DevParams &p, uint8_t *bytes, cudaStre
     return cudaGetLastError();
 }
 
+// logits: canonical [n][5] <-> device [n][LOGIT_STRIDE] (one contiguous copy and this kernel
+// instead of a pitched copy of 20-byte rows, which moves a few bytes per DMA row)
+__global__ void k_logits_restride(float *dst, int dst_stride, const float *src, int src_stride, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * 5) return;
+    const size_t a = i / 5;
+    const int k = (int)(i - a * 5);
+    dst[a * dst_stride + k] = src[a * src_stride + k];
+}
+
+cudaError_t launch_logits_restride(float *dst, int dst_stride, const float *src, int src_stride, size_t n,
+                                   cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_logits_restride<<<(unsigned)((n * 5 + 255) / 256), 256, 0, s>>>(dst, dst_stride, src, src_stride, n);
+    return cudaGetLastError();
+}
+
 // --------------------------------------------------- weights canonical <-> device
 __global__ void k_weights_to_device(DevParams p, const float *canon, size_t first, size_t n) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
