@@ -690,6 +690,15 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
     if (bps < 1) bps = 1;
     h->lc.policy_blocks = prop.multiProcessorCount * bps;
     h->lc.sms = prop.multiProcessorCount;
+    {
+        // interleaved contexts spread few agents over every SM when all blocks are resident at
+        // once; with more blocks than one wave they leave every block partly empty (a band of
+        // the large world: 5.6 waves of 62 %-full blocks instead of 3.5 full ones)
+        static const char *bm_env = getenv("ECO_POL_BMAJOR");
+        const long half_blocks = ((long)S + 15) / 16;
+        p.pol_bmajor = (nw == 1 && d.Hd == 32 && d.net == 0 && half_blocks > (long)h->lc.policy_blocks) ? 1 : 0;
+        if (bm_env) p.pol_bmajor = bm_env[0] == '1' && nw == 1 ? 1 : 0;
+    }
     h->lc.agent_threads = 256;
     {
         const long need = ((long)nw * S + 255) / 256;

@@ -122,6 +122,9 @@ struct DevParams {
     // beside the latency-bound phases); the policy then streams only P and the active W_ih
     // columns.  Children (the last *p_children list positions) start from their bias.
     int32_t split;
+    // Hd = 32, one world whose slots need more than one wave of policy blocks (a large world, a
+    // band): contexts block-major (full blocks, then empty ones) instead of interleaved
+    int32_t pol_bmajor;
     float *Pbuf;                 // [S][Hd*4] device order [k][4], like b
     // movement-histogram metrics (sim.h: sim_get_move_hist): each slot's cell and age at the
     // start of the current 50-step window, and the per-window histograms (a ring)

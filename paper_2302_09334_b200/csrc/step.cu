@@ -512,7 +512,8 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
     const long total = (long)p.n_worlds * p.S;
     // one world: contexts interleaved over the blocks (few agents spread over every SM);
     // sharded: block-major, so this rank's agents (a fraction of the slots) fill whole blocks
-    const long v = SHARD ? (long)blockIdx.x * HALF_AGENTS + ag : (long)ag * gridDim.x + blockIdx.x;
+    // (more blocks than one wave: block-major too, p.pol_bmajor)
+    const long v = (SHARD || p.pol_bmajor) ? (long)blockIdx.x * HALF_AGENTS + ag : (long)ag * gridDim.x + blockIdx.x;
     const bool in_range = v < total;
     const int w = in_range ? (int)(v / p.S) : 0;
     const int i = in_range ? (int)(v - (long)w * p.S) : 0;
@@ -702,8 +703,9 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #if ECO_POLICY_DEEP
             // per warp: its agents' partners (agents 2w + HALF_AGENTS/2 and the next, list
             // positions further on) hold no agent this step, so their rings are free
-            const bool deep = !SHARD && warp < HALF_WARPS / 2 &&
-                              (long)(2 * warp + HALF_AGENTS / 2) * gridDim.x + blockIdx.x >= (long)n_list;
+            const long pv = p.pol_bmajor ? (long)blockIdx.x * HALF_AGENTS + 2 * warp + HALF_AGENTS / 2
+                                         : (long)(2 * warp + HALF_AGENTS / 2) * gridDim.x + blockIdx.x;
+            const bool deep = !SHARD && warp < HALF_WARPS / 2 && pv >= (long)n_list;
             if (deep) stream(std::integral_constant<int, 2 * R>{});
             else stream(std::integral_constant<int, R>{});
 #else
