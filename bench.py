@@ -23,6 +23,9 @@ Our arm (default):
     (H2D of the whole state), then sim_step(K) (one call), each step's record written by the
     device into a mapped pinned host ring (sim_set_record_mirror: the D2H of the result
     without a copy operation), wall clock, checked equal to the timed run's records;
+  * whole_run_sample (when K covers only the first steps of the config's 10,000-step run,
+    as the driver's --steps 20 does): 20 more single steps spread evenly over the rest of the
+    run, timed the same way, the steps between them advanced untimed;
   * cpu_baseline: the oracle (oracle/, single thread) on a bounded sample of the same
     workload from the same start state.
 --impl reference: the oracle as the reference arm (no GPU code on that path).
@@ -48,6 +51,7 @@ import workloads  # noqa: E402
 METRIC = "agent-steps/s (paper-scale world step)"
 UNIT = "agent-steps/s"
 FLUSH_BYTES = 256 << 20
+RUN_SAMPLES = 20  # whole_run_sample: single steps timed over the rest of the run
 
 
 def parse_args():
@@ -63,6 +67,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--no-run-sample", action="store_true",
+                    help="skip whole_run_sample (steps sampled over the rest of the config's run)")
     ap.add_argument("--shard", action="store_true",
                     help="one world over all ranks (agent-sharded, NCCL allreduce of the move records "
                          "each step; strong scaling) instead of one replica per rank")
@@ -410,6 +416,31 @@ def run_ours(args, rank, world_size, local_rank):
             e_s = allmax(e_s)
             e2e = {"value": all_agents / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
                    "d2h_bytes_per_step": rec_bytes, "seconds": e_s}
+        # -- the rest of the config's run, sampled: when K covers only the run's first steps (the
+        # driver's --steps 20 times t = 5..25, ~1,000 agents in 8,192 slots), M more single
+        # steps spread evenly over the remaining steps of the run are timed the same way (L2
+        # flush, events around one sim_step(1)), the steps between them advanced untimed
+        run_sample = None
+        if (not sharded and not args.no_run_sample and args.config == "paper_scale" and world.t == t0 + K
+                and wc.steps - world.t >= 40 * RUN_SAMPLES):
+            stride = (wc.steps - world.t) // RUN_SAMPLES
+            s_ms, s_t, s_agents, s_bytes = [], [], 0, 0
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for i in range(RUN_SAMPLES):
+                world.step(stride - 1)
+                flush_l2()
+                ea.record(stream)
+                world.step(1)
+                eb.record(stream)
+                world.synchronize()
+                r = world.step_log(world.t - 1, 1)
+                s_t.append(int(world.t - 1))
+                s_ms.append(ea.elapsed_time(eb))
+                s_agents += int(r["agents_at_start"].sum())
+                s_bytes += step_bytes(wc, int(r["agents_at_start"].sum()), int(r["obs_nnz"].sum()),
+                                      int(r["births"].sum()))
+            run_sample = {"t": s_t, "step_ms": s_ms, "agents": s_agents, "bytes": s_bytes,
+                          "max_ms": allmax(float(sum(s_ms))), "all_agents": allsum(s_agents)}
         world.destroy()
 
     result = None
@@ -483,6 +514,19 @@ def run_ours(args, rank, world_size, local_rank):
             result["replay_identical"] = kern["replay_identical"]
         if e2e is not None:
             result["e2e"] = e2e
+        if run_sample is not None:
+            rs = run_sample
+            result["whole_run_sample"] = {
+                "what": f"{RUN_SAMPLES} single steps spread evenly over the rest of the config's {wc.steps}-step run "
+                        "(each after an L2 flush, events around one sim_step(1); the steps between advanced "
+                        "untimed): the run's regimes beside the timed region's first steps",
+                "t": rs["t"], "ms_per_step": rs["max_ms"] / RUN_SAMPLES,
+                "value": rs["all_agents"] / (rs["max_ms"] / 1e3), "unit": UNIT,
+                "agents_mean": rs["agents"] / RUN_SAMPLES,
+                "step_roofline": {"bytes_per_step": rs["bytes"] / RUN_SAMPLES,
+                                  "achieved_GBps": rs["bytes"] / (sum(rs["step_ms"]) / 1e3) / 1e9,
+                                  "frac": rs["bytes"] / (sum(rs["step_ms"]) / 1e3) / 1e9 / peak},
+                "step_us": [round(v * 1e3, 2) for v in rs["step_ms"]]}
     return result, snap, wc
 
 

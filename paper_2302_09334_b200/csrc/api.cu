@@ -698,6 +698,11 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
         const long half_blocks = ((long)S + 15) / 16;
         p.pol_bmajor = (nw == 1 && d.Hd == 32 && d.net == 0 && half_blocks > (long)h->lc.policy_blocks) ? 1 : 0;
         if (bm_env) p.pol_bmajor = bm_env[0] == '1' && nw == 1 ? 1 : 0;
+        // several worlds whose slot pools need more than one wave of blocks: compacted tiles
+        static const char *pc_env = getenv("ECO_POL_COMPACT");
+        p.pol_compact = (nw > 1 && nw <= (size_t)eco::policy_compact_worlds() && d.Hd == 32 && d.net == 0 &&
+                         (long)nw * half_blocks > (long)h->lc.policy_blocks) ? 1 : 0;
+        if (pc_env && pc_env[0] == '0') p.pol_compact = 0;
     }
     h->lc.agent_threads = 256;
     {

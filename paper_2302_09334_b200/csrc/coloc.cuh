@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_post_co(DevParams p, unsigned lo
         regrow_phase(p, T + 1, b * blockDim.x + threadIdx.x, nb * blockDim.x);
     }
     grid_sync(bar, target);
-    mutate_phase(p, gtid, gthreads);
+    mutate_phase(p, gtid, gthreads, s_free, RANK_SMEM_CAP);  // (the rank's lists are consumed: s_free is free)
     if (!spare) regrow_phase(p, T + 1, gtid, gthreads);
     if (blockIdx.x == 0 && threadIdx.x == 0) grid_sync_done(bar, target);
 }

@@ -185,11 +185,20 @@ __device__ __forceinline__ uint32_t regrow_groups(const DevParams &p, int w, int
 // a small grid gets 8 short chains per word instead of one long one); the lanes of a word
 // OR their grown bits and the first stores the word.  One atomic per warp on the world's
 // record of that step.  Must be called by all 32 lanes of a warp.
-__device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, size_t gtid, size_t gthreads) {
+// (k_lo, k_hi: the words [k_lo, min(k_hi, all)) of the world-major word sequence only — two
+// groups of blocks sharing one regrowth.)
+__device__ __forceinline__ size_t regrow_words(const DevParams &p) {
+    return (size_t)(p.row_hi - p.row_lo) * ((p.W + 31) >> 5) * p.n_worlds;
+}
+__device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, size_t gtid, size_t gthreads,
+                                             size_t k_lo = 0, size_t k_hi = ~(size_t)0) {
     const int real_words = (p.W + 31) >> 5;
     const int rows = p.row_hi - p.row_lo;  // the rows this handle owns (all H unless banded)
     const size_t per_world = (size_t)rows * real_words;
-    const size_t total = per_world * p.n_worlds;
+    const size_t all = per_world * p.n_worlds;
+    if (k_hi > all) k_hi = all;
+    if (k_lo >= k_hi) return;
+    const size_t total = k_hi - k_lo;
     int lsh = 0;  // L = 1 << lsh lanes per word
     while (lsh < 3 && (total << (lsh + 1)) <= gthreads) ++lsh;
     const int L = 1 << lsh, ng = 8 >> lsh;
@@ -197,7 +206,7 @@ __device__ __forceinline__ void regrow_phase(const DevParams &p, int64_t tstep, 
     const unsigned lane = gtid & 31;
     for (size_t base = gtid - lane; base < items; base += gthreads) {
         const size_t it = base + lane;
-        const size_t k = it >> lsh;
+        const size_t k = k_lo + (it >> lsh);
         const int sub = (int)(it & (L - 1));
         int w = 0, y = 0, wx = 0;
         uint32_t grow = 0u, cur = 0u;
@@ -933,7 +942,7 @@ __device__ __forceinline__ void gauss_pair(uint64_t seed, int64_t t, int cellc, 
     za = z.x;
     zb = z.y;
 }
-static __device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0) {
+__device__ __forceinline__ double2 gauss_pair_body(uint64_t seed, int64_t t, int cellc, int j0) {
     double za, zb;
     const uint4 d = draw4(seed, PURPOSE_MUTATE, (uint32_t)t, (uint32_t)cellc, (uint32_t)(j0 >> 2));
     const bool lo = (j0 & 3) == 0;
@@ -949,12 +958,15 @@ static __device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, i
     zb = __dmul_rn(rad, sn);
     return make_double2(za, zb);
 }
+static __device__ __noinline__ double2 gauss_pair_nl(uint64_t seed, int64_t t, int cellc, int j0) {
+    return gauss_pair_body(seed, t, cellc, j0);
+}
 
 // U independent items per thread: all loads, then all Philox/log/sincos chains, then all
 // stores (stores last, so no child store can alias an input the compiler must re-order).
 // Item u is pair `iu[u]` of birth `bu[u]` (skipped unless ok[u]); birth(b, child, parent,
 // cell) gives birth b's slots and cell.
-template <int U, typename PP, typename Birth>
+template <int U, bool INL = false, typename PP, typename Birth>  // INL: the Gaussian pairs inlined (U chains interleave)
 __device__ __forceinline__ void mutate_batch(const PP &p, int w, int64_t t, uint64_t seed, const uint32_t *bu,
                                              const uint32_t *iu, const bool *ok, Birth birth, bool dry = false) {
     float pa[U], pb[U];
@@ -979,7 +991,15 @@ __device__ __forceinline__ void mutate_batch(const PP &p, int w, int64_t t, uint
     double za[U], zb[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (dst[u]) gauss_pair(seed, t, cellc[u], j0[u], za[u], zb[u]);
+        if (dst[u]) {
+            if (INL) {
+                const double2 z = gauss_pair_body(seed, t, cellc[u], j0[u]);
+                za[u] = z.x;
+                zb[u] = z.y;
+            } else {
+                gauss_pair(seed, t, cellc[u], j0[u], za[u], zb[u]);
+            }
+        }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (!dst[u] || dry) continue;
@@ -994,30 +1014,47 @@ __device__ __forceinline__ void mutate_batch(const PP &p, int w, int64_t t, uint
 // the nb children of world w born at step t, from the global birth lists.  Items k = gtid,
 // gtid + gthreads, ... of nb * Q pairs; (birth, pair) = divmod(k, Q) is advanced
 // incrementally (one division per thread).
-template <typename PP>
-__device__ __forceinline__ void mutate_world_impl(const PP &p, int w, int64_t t, uint64_t seed, int nb, size_t gtid,
-                                                  size_t gthreads, bool dry) {
-    constexpr int U = ECO_MUTATE_U;  // independent items in flight per thread
+// U: independent items in flight per thread; INL: inlined Gaussian pairs and 32-bit index
+// divisions where the operands fit (the several-world path; the one-world path keeps its
+// compact code: it is bound by instruction fetch)
+template <int U = ECO_MUTATE_U, bool INL = false, typename PP>
+__device__ __forceinline__ size_t mutate_world_impl(const PP &p, int w, int64_t t, uint64_t seed, int nb, size_t gtid,
+                                                    size_t gthreads, bool dry) {
     const uint32_t Q = (uint32_t)mutate_items_per_child(p);
     const size_t n = (size_t)nb * Q;
-    if (gtid >= n) return;
+    if (gtid >= n) return gtid;
     const size_t ws = (size_t)w * p.S;
     auto birth = [&](int b, int &child, int &parent, int &cell) {
         child = p.birth_child[ws + b];
         parent = p.birth_parent[ws + b];
         cell = p.birth_cell[ws + b];
     };
-    const uint32_t sb = (uint32_t)(gthreads / Q), si = (uint32_t)(gthreads % Q);
-    auto adv = [&](uint32_t &b, uint32_t &i) {
-        i += si;
-        b += sb;
-        if (i >= Q) {
-            i -= Q;
-            ++b;
+    // (INL) 32-bit divisions where the operands allow: a 64-bit one is ~100 instructions
+    uint32_t sb, si, b, it;
+    if (INL && gthreads <= 0xFFFFFFFFull) {
+        sb = (uint32_t)gthreads / Q;
+        si = (uint32_t)gthreads - sb * Q;
+    } else {
+        sb = (uint32_t)(gthreads / Q);
+        si = (uint32_t)(gthreads % Q);
+    }
+    if (INL && gtid <= 0xFFFFFFFFull) {
+        b = (uint32_t)gtid / Q;
+        it = (uint32_t)gtid - b * Q;
+    } else {
+        b = (uint32_t)(gtid / Q);
+        it = (uint32_t)(gtid % Q);
+    }
+    auto adv = [&](uint32_t &b_, uint32_t &i_) {
+        i_ += si;
+        b_ += sb;
+        if (i_ >= Q) {
+            i_ -= Q;
+            ++b_;
         }
     };
-    uint32_t b = (uint32_t)(gtid / Q), it = (uint32_t)(gtid % Q);
-    for (size_t k = gtid; k < n; k += U * gthreads) {
+    size_t k = gtid;
+    for (; k < n; k += U * gthreads) {
         uint32_t bu[U], iu[U];
         bool ok[U];
 #pragma unroll
@@ -1027,8 +1064,14 @@ __device__ __forceinline__ void mutate_world_impl(const PP &p, int w, int64_t t,
             ok[u] = k + u * gthreads < n;
             adv(b, it);
         }
-        mutate_batch<U>(p, w, t, seed, bu, iu, ok, birth, dry);
+        mutate_batch<U, INL>(p, w, t, seed, bu, iu, ok, birth, dry);
     }
+    // the first index >= n of this thread's stride (gtid + m * gthreads): the last batch may
+    // have ended on skipped items
+#pragma unroll
+    for (int u = 1; u < U; ++u)
+        if (k > gtid && k - gthreads >= n) k -= gthreads;
+    return k;
 }
 __device__ __forceinline__ void mutate_world(const DevParams &p, int w, int64_t t, int nb, size_t gtid,
                                              size_t gthreads) {
@@ -1074,11 +1117,127 @@ static __device__ __noinline__ void mutate_world_nl(MutArgs a, int64_t t, uint64
     mutate_world_impl(a, 0, t, seed, nb, gtid, gthreads, dry != 0);
 }
 
-// all worlds, after the rank advanced t
-__device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads) {
-    for (int w = 0; w < p.n_worlds; ++w) {
-        const int nb = *reinterpret_cast<volatile int32_t *>(p.n_births + w);
-        if (nb > 0) mutate_world(p, w, p.t[w] - 1, nb, gtid, gthreads);
+// all worlds, after the rank advanced t.  Several worlds: their pair items form ONE
+// world-major sequence strided over the grid's threads (thread gtid takes items gtid, gtid +
+// gthreads, ... of the concatenation), so every thread has work whatever a single world's
+// births are; the worlds' birth counts are read 32 at a time, one per lane.  (One pass per
+// world — a world's ~10 children are 43,000 items for 113,664 threads, 64 dependent passes —
+// took 157 of the 64-world ensemble's 664 us per step.)  Whole warps call this together.
+#ifndef ECO_MUTATE_INL_MULTI
+#define ECO_MUTATE_INL_MULTI 1  // the Gaussian pair inlined in the several-world path (throughput, not fetch, bound)
+#endif
+#ifndef ECO_MUTATE_U_MULTI
+#define ECO_MUTATE_U_MULTI 1  // measured (64-world ensemble, mutation phase): 1 -> 80.3, 2 -> 82.9, 3 -> 85.3, 4 -> 104 us
+#endif
+// Several worlds, their children prefixed over the worlds in the block's shared array s_cum
+// [n_worlds + 1] (made here by warp 0; every thread of the block calls this): thread gtid
+// takes pair items gtid, gtid + gthreads, ... of the world-major sequence of all children, U
+// of them at a time — independent chains (loads, Philox, log, sincos, stores) of different
+// children, usually of different worlds, interleaved by the compiler.
+template <int U>
+__device__ __forceinline__ void mutate_multi(const DevParams &p, size_t gtid, size_t gthreads, int *s_cum) {
+    const int lane = (int)(threadIdx.x & 31u);
+    if (threadIdx.x < 32) {
+        int run = 0;
+        for (int w0 = 0; w0 < p.n_worlds; w0 += 32) {
+            const int wl = w0 + lane;
+            const int nb = wl < p.n_worlds ? *reinterpret_cast<volatile int32_t *>(p.n_births + wl) : 0;
+            int inc = nb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int up = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += up;
+            }
+            if (wl < p.n_worlds) s_cum[wl] = run + inc - nb;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) s_cum[p.n_worlds] = run;
+    }
+    __syncthreads();
+    const uint32_t Q = (uint32_t)mutate_items_per_child(p);
+    const uint32_t C = (uint32_t)s_cum[p.n_worlds];
+    const size_t n = (size_t)C * Q;
+    if (gtid >= n) return;
+    // (child, pair) of this thread's next item; gtid < n <= 2^31 * Q, gthreads < 2^32
+    uint32_t c = (uint32_t)(gtid / Q), it = (uint32_t)(gtid - (size_t)c * Q);
+    const uint32_t sb = (uint32_t)gthreads / Q, si = (uint32_t)gthreads - sb * Q;
+    int w = 0;  // the world of child c (children are world-major: w only grows)
+    for (size_t k = gtid; k < n; k += U * gthreads) {
+        float pa[U], pb[U];
+        int cellc[U], dstep[U], j0[U];
+        int64_t tb[U];
+        uint64_t seed[U];
+        float *dst[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            dst[u] = nullptr;
+            if (k + u * gthreads < n) {
+                while (c >= (uint32_t)s_cum[w + 1]) ++w;
+                const size_t bi = (size_t)w * p.S + (c - (uint32_t)s_cum[w]);
+                const int child = p.birth_child[bi], parent = p.birth_parent[bi];
+                cellc[u] = p.birth_cell[bi];
+                tb[u] = p.t[w] - 1;
+                seed[u] = p.seeds[w];
+                ECO_CHECK(child >= 0 && child < p.S && parent >= 0 && parent < p.S);
+                int d0;
+                mutate_item(p, (int)it, d0, dstep[u], j0[u]);
+                const float *wp = p.weights + ((size_t)w * p.S + parent) * p.Pd + d0;
+                pa[u] = wp[0];
+                pb[u] = dstep[u] ? wp[dstep[u]] : 0.f;
+                dst[u] = p.weights + ((size_t)w * p.S + child) * p.Pd + d0;
+            }
+            it += si;
+            c += sb;
+            if (it >= Q) {
+                it -= Q;
+                ++c;
+            }
+        }
+        double2 z[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (dst[u]) z[u] = gauss_pair_body(seed[u], tb[u], cellc[u], j0[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!dst[u]) continue;
+            dst[u][0] = __fadd_rn(pa[u], __double2float_rn(__dmul_rn(p.mutation_std, z[u].x)));
+            if (dstep[u]) dst[u][dstep[u]] = __fadd_rn(pb[u], __double2float_rn(__dmul_rn(p.mutation_std, z[u].y)));
+        }
+    }
+}
+
+// `s_cum`: a shared array of the block with room for n_worlds + 1 ints (s_cum_cap entries),
+// or nullptr; with it (and every thread of the block calling) several worlds take the
+// interleaved path above.
+__device__ __forceinline__ void mutate_phase(const DevParams &p, size_t gtid, size_t gthreads, int *s_cum = nullptr,
+                                             int s_cum_cap = 0) {
+    if (p.n_worlds == 1) {
+        const int nb = *reinterpret_cast<volatile int32_t *>(p.n_births);
+        if (nb > 0) mutate_world(p, 0, p.t[0] - 1, nb, gtid, gthreads);
+        return;
+    }
+    if (s_cum && p.n_worlds < s_cum_cap && ECO_MUTATE_U_MULTI > 0) {
+        mutate_multi<(ECO_MUTATE_U_MULTI > 0 ? ECO_MUTATE_U_MULTI : 1)>(p, gtid, gthreads, s_cum);
+        return;
+    }
+    const uint32_t Q = (uint32_t)mutate_items_per_child(p);
+    const int lane = (int)(threadIdx.x & 31u);
+    size_t g = gtid, base = 0;  // this thread's next item and the current world's first, in the concatenation
+    for (int w0 = 0; w0 < p.n_worlds; w0 += 32) {
+        const int wl = w0 + lane;
+        const int nbl = wl < p.n_worlds ? *reinterpret_cast<volatile int32_t *>(p.n_births + wl) : 0;
+        const int wn = p.n_worlds - w0 < 32 ? p.n_worlds - w0 : 32;
+        for (int j = 0; j < wn; ++j) {
+            const int nb = __shfl_sync(0xffffffffu, nbl, j);
+            const size_t n = (size_t)nb * Q;
+            if (g < base + n) {
+                const int w = w0 + j;
+                const size_t r0 = g - base;
+                g = base + mutate_world_impl<1, ECO_MUTATE_INL_MULTI != 0>(p, w, p.t[w] - 1, p.seeds[w], nb,
+                                                                                            r0, gthreads, false);
+            }
+            base += n;
+        }
     }
 }
 

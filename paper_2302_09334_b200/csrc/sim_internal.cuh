@@ -125,6 +125,10 @@ struct DevParams {
     // Hd = 32, one world whose slots need more than one wave of policy blocks (a large world, a
     // band): contexts block-major (full blocks, then empty ones) instead of interleaved
     int32_t pol_bmajor;
+    // Hd = 32, several worlds (unsplit policy): the policy's blocks loop over the 16-agent
+    // tiles of the worlds' LIVE list positions only (a per-block prefix over the worlds' counts)
+    // instead of one block per 16 slots (the 64-world ensemble: 28,000 of 32,768 blocks empty)
+    int32_t pol_compact;
     float *Pbuf;                 // [S][Hd*4] device order [k][4], like b
     // movement-histogram metrics (sim.h: sim_get_move_hist): each slot's cell and age at the
     // start of the current 50-step window, and the per-window histograms (a ring)
@@ -394,6 +398,7 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
 cudaError_t launch_set_owner(const DevParams &p, cudaStream_t s);  // owner[slot] = slot % n_ranks,
                                                                   // own list of step t, zero records
 bool policy_supports_shard();  // the Hd = 32 policy kernel of this build honours ownership
+int policy_compact_worlds();  // most worlds the compacted policy mapping (pol_compact) supports
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);  // P of step t
 cudaError_t launch_prepare_p_snap(const DevParams &p, const int64_t *snap, cudaStream_t s);  // banded
 cudaError_t band_snap(const DevParams &p, const BandParams &bp, cudaStream_t s);

@@ -371,6 +371,10 @@ constexpr int HALF_AGENTS = 2 * HALF_WARPS;  // per block (16 at 8 warps)
 #define ECO_HALF_DEPTH 6
 #endif
 constexpr int HALF_DEPTH = ECO_HALF_DEPTH;
+#ifndef ECO_POL_COMPACT_WAVES
+#define ECO_POL_COMPACT_WAVES 4  // the compacted policy's grid, in waves of resident blocks
+#endif
+constexpr int POLICY_COMPACT_WORLDS = 512;  // worlds whose tile prefix fits the block's shared array
 constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6 and 8 warps
 // blocks per SM the smem allows (32 resident warps at depth <= 6)
 constexpr int HALF_BPS = (HALF_DEPTH <= 6 ? 32 : HALF_DEPTH <= 8 ? 24 : 16) / HALF_WARPS > 0
@@ -382,13 +386,100 @@ constexpr int HALF_BPS = (HALF_DEPTH <= 6 ? 32 : HALF_DEPTH <= 8 ? 24 : 16) / HA
 // per-lane cp.async ring as the policy (`ring` = this context's R slots).  The sum is formed
 // in the policy's order (the 32 W_hh rows by FMA, then b), so that a policy starting from P
 // produces exactly the gates of one streaming W_hh itself.
+// The ring runs on ACROSS a context's agents (ECO_HH_PIPE, default): an agent's 33 chunks
+// are followed at once by the first chunks of the context's next agent (its slot read one
+// agent ahead, its h while the current agent's last R chunks land), so R chunks stay in
+// flight from the first agent's first chunk to the last agent's last — no drain, no
+// dependent list -> slot -> row round trip between agents.  (Before: each agent drained the
+// ring and began with that round trip, ~6.5 round trips per agent instead of 33 / R.)
+#ifndef ECO_HH_PIPE
+#define ECO_HH_PIPE 1
+#endif
 template <int R>
 __device__ __forceinline__ void hh_pass(const DevParams &p, const int32_t *list, int n, int ctx, int nctx,
                                         float4 *ring) {
-    constexpr int HD = 32, NHH = 32;
+    constexpr int HD = 32, NHH = 32, NCH = NHH + 1;  // an agent's chunks: the 32 W_hh rows, then b
+    static_assert(R >= 1 && R <= NCH, "ring depth");
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, hl = lane & 15;
     float4 *rg = ring + hl;  // slot s, unit hl: rg[s * 32]; unit hl+16: rg[s * 32 + 16]
+#if ECO_HH_PIPE
+    int i = ctx;
+    bool active = i < n;
+    if (!__any_sync(FULL, active)) return;
+    auto issue = [&](int s_, const float *src, bool on) {
+        if (on) {
+            cp_async16(rg + s_ * 32, src, 0ull);
+            cp_async16(rg + s_ * 32 + 16, src + 64, 0ull);
+        }
+        cp_commit();
+    };
+    // chunk q of the row at Wl: W_hh row q, or b
+    auto chunk = [&](const float *Wl, int q) { return q < NHH ? Wl + p.off_hh + q * HD * 4 : Wl + p.off_b; };
+    int slot = active ? list[i] : 0;
+    bool nact = i + nctx < n;
+    int nslot = nact ? list[i + nctx] : 0;
+    const float *Wl = p.weights + (size_t)slot * p.Pd + hl * 4;
+#pragma unroll
+    for (int q = 0; q < R; ++q) issue(q, chunk(Wl, q), active);
+    float hk0 = active ? p.h[(size_t)slot * HD + hl] : 0.f;
+    float hk1 = active ? p.h[(size_t)slot * HD + hl + 16] : 0.f;
+    int s = 0;  // the ring slot of the current agent's next chunk
+    for (;;) {
+        const float *Wn = p.weights + (size_t)nslot * p.Pd + hl * 4;
+        float hn0 = 0.f, hn1 = 0.f;
+        float4 acc0 = make_float4(0.f, 0.f, 0.f, 0.f), acc1 = acc0;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            cp_wait<R - 1>();
+            const float4 c0 = rg[s * 32], c1 = rg[s * 32 + 16];
+            if (k < NHH) {
+                const float hj = __shfl_sync(FULL, k < 16 ? hk0 : hk1, k & 15, 16);
+                acc0.x = fmaf(hj, c0.x, acc0.x);
+                acc0.y = fmaf(hj, c0.y, acc0.y);
+                acc0.z = fmaf(hj, c0.z, acc0.z);
+                acc0.w = fmaf(hj, c0.w, acc0.w);
+                acc1.x = fmaf(hj, c1.x, acc1.x);
+                acc1.y = fmaf(hj, c1.y, acc1.y);
+                acc1.z = fmaf(hj, c1.z, acc1.z);
+                acc1.w = fmaf(hj, c1.w, acc1.w);
+            } else {  // the bias
+                acc0.x += c0.x;
+                acc0.y += c0.y;
+                acc0.z += c0.z;
+                acc0.w += c0.w;
+                acc1.x += c1.x;
+                acc1.y += c1.y;
+                acc1.z += c1.z;
+                acc1.w += c1.w;
+            }
+            // refill the slot just read: this agent's chunk k + R, else the next agent's first ones
+            if (k + R < NCH) issue(s, chunk(Wl, k + R), active);
+            else issue(s, chunk(Wn, k + R - NCH), nact);
+            if (k == NCH - R && nact) {  // the next agent's h, landing beside its first chunks
+                hn0 = p.h[(size_t)nslot * HD + hl];
+                hn1 = p.h[(size_t)nslot * HD + hl + 16];
+            }
+            s = s + 1 == R ? 0 : s + 1;
+        }
+        if (active) {
+            float4 *P = reinterpret_cast<float4 *>(p.Pbuf + (size_t)slot * HD * 4);
+            P[hl] = acc0;
+            P[hl + 16] = acc1;
+        }
+        i += nctx;
+        active = nact;
+        slot = nslot;
+        Wl = Wn;
+        hk0 = hn0;
+        hk1 = hn1;
+        if (!__any_sync(FULL, active)) break;
+        nact = i + nctx < n;
+        nslot = nact ? list[i + nctx] : 0;  // needed NCH - R chunks from here
+    }
+    cp_wait<0>();
+    __syncwarp();
+#else
     for (int r0 = 0; r0 < n; r0 += nctx) {
         const int i = r0 + ctx;
         const bool active = i < n;
@@ -445,6 +536,7 @@ __device__ __forceinline__ void hh_pass(const DevParams &p, const int32_t *list,
         }
         __syncwarp();
     }
+#endif
 }
 
 // P of every live agent of step t (after create / set_state / instrumented steps), one
@@ -510,10 +602,51 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #endif
     step_housekeeping(p);
     const long total = (long)p.n_worlds * p.S;
+    // several worlds (p.pol_compact; the unsplit, unsharded kernel only): the block loops over
+    // the tiles of HALF_AGENTS consecutive LIVE list positions of the worlds — tile0[w] = the
+    // tiles of the worlds before w, from the worlds' counts, made by warp 0 — so no block is
+    // launched for the empty tail of a world's slot pool (all worlds share t)
+    constexpr bool CAN_COMPACT = !SHARD && !SPLIT;
+    __shared__ int s_tile0[CAN_COMPACT ? POLICY_COMPACT_WORLDS + 1 : 1];
+    const bool compact = CAN_COMPACT && p.pol_compact;
+    int n_tiles = 1;
+    if (compact) {
+        if (warp == 0) {
+            const int par = (int)(p.t[0] & 1);
+            int run = 0;
+            for (int w0 = 0; w0 < p.n_worlds; w0 += 32) {
+                const int wl = w0 + lane;
+                const int cnt = wl < p.n_worlds ? p.n_alive[par * p.n_worlds + wl] : 0;
+                const int tl = (cnt + HALF_AGENTS - 1) / HALF_AGENTS;
+                int inc = tl;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int up = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += up;
+                }
+                if (wl < p.n_worlds) s_tile0[wl] = run + inc - tl;
+                run += __shfl_sync(FULL, inc, 31);
+            }
+            if (lane == 0) s_tile0[p.n_worlds] = run;
+        }
+        __syncthreads();
+        n_tiles = s_tile0[p.n_worlds];
+    }
+    for (int tile = compact ? (int)blockIdx.x : 0; tile < n_tiles; tile += compact ? (int)gridDim.x : 1) {
     // one world: contexts interleaved over the blocks (few agents spread over every SM);
     // sharded: block-major, so this rank's agents (a fraction of the slots) fill whole blocks
     // (more blocks than one wave: block-major too, p.pol_bmajor)
-    const long v = (SHARD || p.pol_bmajor) ? (long)blockIdx.x * HALF_AGENTS + ag : (long)ag * gridDim.x + blockIdx.x;
+    long v = (SHARD || p.pol_bmajor) ? (long)blockIdx.x * HALF_AGENTS + ag : (long)ag * gridDim.x + blockIdx.x;
+    if (compact) {
+        int lo = 0, hi = p.n_worlds;  // s_tile0[lo] <= tile < s_tile0[hi]: the last such lo owns the tile
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_tile0[mid] <= tile) lo = mid;
+            else hi = mid;
+        }
+        const int ii = (tile - s_tile0[lo]) * HALF_AGENTS + ag;
+        v = ii < p.S ? (long)lo * p.S + ii : total;
+    }
     const bool in_range = v < total;
     const int w = in_range ? (int)(v / p.S) : 0;
     const int i = in_range ? (int)(v - (long)w * p.S) : 0;
@@ -822,6 +955,8 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
         timeline_mark(p, 1, globaltimer_ns());
 #endif
     }
+    if (compact) __syncthreads();  // the next tile's contexts rewrite s_w, s_nnz, s_ties
+    }  // tiles
 }
 
 #include "policy_cnn.cuh"
@@ -839,6 +974,8 @@ cudaError_t policy_occupancy(int hidden, int net, int *blocks_per_sm, int *threa
         default: return cudaErrorInvalidValue;
     }
 }
+
+int policy_compact_worlds() { return POLICY_COMPACT_WORLDS; }
 
 cudaError_t policy_prepare() {
     cudaError_t e = set_dyn_smem(k_policy_half<true>, HALF_SMEM);
@@ -876,6 +1013,9 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
 #if ECO_HALF_FULLGRID
             if (blocks < (long)lc.sms * HALF_BPS) blocks = (long)lc.sms * HALF_BPS;  // every SM the same
 #endif
+            // compacted tiles: resident blocks loop over the live tiles
+            if (p.pol_compact && blocks > (long)lc.sms * HALF_BPS * ECO_POL_COMPACT_WAVES)
+                blocks = (long)lc.sms * HALF_BPS * ECO_POL_COMPACT_WAVES;
             if (p.n_ranks > 1 && p.split) k_policy_half<true, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.split && pdl) {  // a programmatic dependent of the previous k_post
@@ -932,7 +1072,8 @@ __global__ void __launch_bounds__(RANK_THREADS) k_birth_rank(DevParams p) {
 }
 
 __global__ void __launch_bounds__(256) k_mutate(DevParams p) {
-    mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x);
+    __shared__ int s_cum[RANK_SMEM_CAP];  // several worlds: the children prefixed over the worlds
+    mutate_phase(p, interleaved_gtid(), (size_t)gridDim.x * blockDim.x, s_cum, RANK_SMEM_CAP);
 }
 
 // ------------------------------------------------------------------------ k_post
@@ -962,6 +1103,9 @@ constexpr int POST_THREADS = ECO_POST_THREADS;
 #endif
 #ifndef ECO_HH_BIG_AGENTS
 #define ECO_HH_BIG_AGENTS 32768
+#endif
+#ifndef ECO_RANK_SHARE
+#define ECO_RANK_SHARE 4  // several worlds: a ranking block's share of the regrowth, in eighths of a free block's (64-world ensemble, rank + regrowth: 0 -> 35.4, 4 -> 26.2, 6 -> 30.1, 8 -> 30.7 us)
 #endif
 #ifndef ECO_CLAIMS_MAX
 #define ECO_CLAIMS_MAX 1024  // measured: 1024 and 2048 beat 4096 at the population cap
@@ -1197,13 +1341,24 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     } else {
         // several worlds: one block per world ranks, places and counts them (t += 1); the
         // blocks without a world regrow step T+1; a barrier; then the mutation
+        // (the blocks without a world take the first share of the regrowth's words, the ranking
+        // blocks the rest once their world is ranked: a ranking block counts as ECO_RANK_SHARE
+        // / 8 of a free one)
+        const size_t rg_all = regrow_words(p);
+        const size_t nfree = (int)gridDim.x > p.n_worlds ? gridDim.x - p.n_worlds : 0;
+        const size_t rg_split = nfree ? rg_all * (8 * nfree) / (8 * nfree + (size_t)ECO_RANK_SHARE * p.n_worlds) : 0;
         if ((int)blockIdx.x < p.n_worlds) {
             for (int w = blockIdx.x; w < p.n_worlds; w += gridDim.x)
                 birth_rank_world<POST_THREADS>(p, w, scratch, s_free, s_bcell, s_par);
+            if (nfree && rg_split < rg_all) {
+                const unsigned nb = p.n_worlds, b = blockIdx.x;
+                const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
+                regrow_phase(p, T + 1, btid, (size_t)nb * blockDim.x, rg_split, rg_all);
+            }
         } else {
             const unsigned nb = gridDim.x - p.n_worlds, b = blockIdx.x - p.n_worlds;
             const size_t btid = ((size_t)(threadIdx.x >> 5) * nb + b) * 32 + (threadIdx.x & 31);
-            regrow_phase(p, T + 1, btid, (size_t)nb * blockDim.x);
+            regrow_phase(p, T + 1, btid, (size_t)nb * blockDim.x, 0, rg_split);
         }
         POST_SYNC(2);
         lap(2);
@@ -1219,7 +1374,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
             const size_t half = gthreads / 2;  // a multiple of 32: halves are whole warps
             if (gtid >= half) regrow_phase(p, T + 1, gtid - half, gthreads - half);
         }
-        mutate_phase(p, gtid, gthreads);
+        mutate_phase(p, gtid, gthreads, s_free, RANK_SMEM_CAP);  // (the rank's lists are consumed: s_free is free)
     }
 #ifdef ECO_BLOCK_CLOCK
     __syncthreads();
