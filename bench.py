@@ -730,8 +730,10 @@ def main():
     if rank == 0:
         if not args.no_cpu_baseline and world_size == 1 and snap is not None:
             w0 = {k: (v[0] if isinstance(v, np.ndarray) else v) for k, v in snap.items()}
+            # (a rate: as many oracle steps from the start state as fit the budget, whatever K is —
+            # the driver's K = 20 alone would be 0.3 s of CPU work)
             rate, steps, el, a0, a1, t1 = oracle_rate(wc.replace(seeds=(wc.seeds[0],)), w0, args.cpu_budget_s,
-                                                      args.steps)
+                                                      max(args.steps, 100000))
             res["cpu_baseline"] = {
                 "value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", **host_cpu(),
                 "sample": f"{steps} oracle world steps from the timed region's start state (t={w0['t']}..{t1}, "

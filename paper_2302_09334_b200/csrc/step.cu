@@ -371,9 +371,14 @@ constexpr int HALF_AGENTS = 2 * HALF_WARPS;  // per block (16 at 8 warps)
 #define ECO_HALF_DEPTH 6
 #endif
 constexpr int HALF_DEPTH = ECO_HALF_DEPTH;
+#ifndef ECO_POL_COMPACT_TILE
+#define ECO_POL_COMPACT_TILE 2  // live list positions per tile of the compacted policy (2: one warp's; 16: one block's)
+#endif
 #ifndef ECO_POL_COMPACT_WAVES
 #define ECO_POL_COMPACT_WAVES 4  // the compacted policy's grid, in waves of resident blocks
 #endif
+constexpr int CPT_TILE = ECO_POL_COMPACT_TILE;
+static_assert(CPT_TILE >= 2 && CPT_TILE % 2 == 0 && HALF_AGENTS % CPT_TILE == 0, "whole warps per tile");
 constexpr int POLICY_COMPACT_WORLDS = 512;  // worlds whose tile prefix fits the block's shared array
 constexpr int HALF_SMEM = HALF_AGENTS * HALF_DEPTH * 32 * 16;  // 48 KB at depth 6 and 8 warps
 // blocks per SM the smem allows (32 resident warps at depth <= 6)
@@ -577,8 +582,9 @@ __device__ __forceinline__ void timeline_mark(const DevParams &p, int k, unsigne
 
 // SHARD = false compiles the sharding branches out, so the unsharded kernels keep their code
 // (a local DevParams copy to fold n_ranks costs 3 us in this kernel: measured).
-template <bool SHARD, bool SPLIT = false>
+template <bool SHARD, bool SPLIT = false, bool COMPACT = false>
 __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParams p) {
+    static_assert(!(SHARD && COMPACT), "the compacted mapping is for unsharded handles");
     constexpr int HD = 32, NHH = 32, QB = 32, Q0 = 33, R = HALF_DEPTH;
     constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(1024) float4 half_smem[];  // [HALF_AGENTS][R][32 units]
@@ -602,22 +608,22 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #endif
     step_housekeeping(p);
     const long total = (long)p.n_worlds * p.S;
-    // several worlds (p.pol_compact; the unsplit, unsharded kernel only): the block loops over
-    // the tiles of HALF_AGENTS consecutive LIVE list positions of the worlds — tile0[w] = the
-    // tiles of the worlds before w, from the worlds' counts, made by warp 0 — so no block is
-    // launched for the empty tail of a world's slot pool (all worlds share t)
-    constexpr bool CAN_COMPACT = !SHARD && !SPLIT;
-    __shared__ int s_tile0[CAN_COMPACT ? POLICY_COMPACT_WORLDS + 1 : 1];
-    const bool compact = CAN_COMPACT && p.pol_compact;
+    // COMPACT (p.pol_compact: more slots than one wave of blocks holds — several worlds, a
+    // large world, a band; unsharded handles): every warp loops over tiles of CPT_TILE consecutive
+    // LIVE list positions of the worlds — s_tile0[w] = the tiles of the worlds before w, from
+    // the worlds' counts, made by warp 0 — so no block is launched for the empty tail of a
+    // world's slot pool, and a warp goes on to its next tile without waiting for the block's
+    // other agents (all worlds share t).  The compiled-out variant keeps the one-tile code.
+    __shared__ int s_tile0[COMPACT ? POLICY_COMPACT_WORLDS + 1 : 1];
     int n_tiles = 1;
-    if (compact) {
+    if (COMPACT) {
         if (warp == 0) {
             const int par = (int)(p.t[0] & 1);
             int run = 0;
             for (int w0 = 0; w0 < p.n_worlds; w0 += 32) {
                 const int wl = w0 + lane;
                 const int cnt = wl < p.n_worlds ? p.n_alive[par * p.n_worlds + wl] : 0;
-                const int tl = (cnt + HALF_AGENTS - 1) / HALF_AGENTS;
+                const int tl = (cnt + CPT_TILE - 1) / CPT_TILE;
                 int inc = tl;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -632,19 +638,24 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
         __syncthreads();
         n_tiles = s_tile0[p.n_worlds];
     }
-    for (int tile = compact ? (int)blockIdx.x : 0; tile < n_tiles; tile += compact ? (int)gridDim.x : 1) {
+    // (COMPACT) this context's counters of its current world, flushed when the world changes
+    unsigned long long acc_nnz = 0ull, acc_ties = 0ull;
+    int acc_w = -1;
+    constexpr int CPT_PER_BLOCK = HALF_AGENTS / CPT_TILE;  // tiles a block works on at a time
+    for (int tile = COMPACT ? (int)blockIdx.x * CPT_PER_BLOCK + ag / CPT_TILE : 0; tile < n_tiles;
+         tile += COMPACT ? (int)gridDim.x * CPT_PER_BLOCK : 1) {
     // one world: contexts interleaved over the blocks (few agents spread over every SM);
     // sharded: block-major, so this rank's agents (a fraction of the slots) fill whole blocks
     // (more blocks than one wave: block-major too, p.pol_bmajor)
     long v = (SHARD || p.pol_bmajor) ? (long)blockIdx.x * HALF_AGENTS + ag : (long)ag * gridDim.x + blockIdx.x;
-    if (compact) {
+    if (COMPACT) {
         int lo = 0, hi = p.n_worlds;  // s_tile0[lo] <= tile < s_tile0[hi]: the last such lo owns the tile
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (s_tile0[mid] <= tile) lo = mid;
             else hi = mid;
         }
-        const int ii = (tile - s_tile0[lo]) * HALF_AGENTS + ag;
+        const int ii = (tile - s_tile0[lo]) * CPT_TILE + ag % CPT_TILE;
         v = ii < p.S ? (long)lo * p.S + ii : total;
     }
     const bool in_range = v < total;
@@ -838,7 +849,8 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
             // positions further on) hold no agent this step, so their rings are free
             const long pv = p.pol_bmajor ? (long)blockIdx.x * HALF_AGENTS + 2 * warp + HALF_AGENTS / 2
                                          : (long)(2 * warp + HALF_AGENTS / 2) * gridDim.x + blockIdx.x;
-            const bool deep = !SHARD && warp < HALF_WARPS / 2 && pv >= (long)n_list;
+            // (COMPACT: the partner warp works on its own tiles)
+            const bool deep = !SHARD && !COMPACT && warp < HALF_WARPS / 2 && pv >= (long)n_list;
             if (deep) stream(std::integral_constant<int, 2 * R>{});
             else stream(std::integral_constant<int, R>{});
 #else
@@ -931,10 +943,27 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
 #endif
         }
     }
+    if (COMPACT) {
+        if (hl == 0 && active) {
+            if (w != acc_w) {
+                if (acc_w >= 0) flush_counters<SHARD>(p, acc_w, acc_nnz, acc_ties);
+                acc_w = w;
+                acc_nnz = acc_ties = 0ull;
+            }
+            acc_nnz += nnz_a;
+            acc_ties += tie_a;
+        }
+        __syncwarp();  // the warp's next tile rewrites its s_col rows
+        continue;
+    }
+    acc_w = active ? w : -1;
+    acc_nnz = nnz_a;
+    acc_ties = tie_a;
+    }  // tiles
     if (hl == 0) {
-        s_w[ag] = active ? w : -1;
-        s_nnz[ag] = nnz_a;
-        s_ties[ag] = tie_a;
+        s_w[ag] = acc_w;
+        s_nnz[ag] = acc_nnz;
+        s_ties[ag] = acc_ties;
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // runs of equal worlds (one world: a single flush per block)
@@ -955,8 +984,6 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_policy_half(DevParam
         timeline_mark(p, 1, globaltimer_ns());
 #endif
     }
-    if (compact) __syncthreads();  // the next tile's contexts rewrite s_w, s_nnz, s_ties
-    }  // tiles
 }
 
 #include "policy_cnn.cuh"
@@ -986,6 +1013,10 @@ cudaError_t policy_prepare() {
     if (e != cudaSuccess) return e;
     e = set_dyn_smem(k_policy_half<true, true>, HALF_SMEM);
     if (e != cudaSuccess) return e;
+    e = set_dyn_smem(k_policy_half<false, true, true>, HALF_SMEM);
+    if (e != cudaSuccess) return e;
+    e = set_dyn_smem(k_policy_half<false, false, true>, HALF_SMEM);
+    if (e != cudaSuccess) return e;
     e = set_dyn_smem(k_prepare_p, HALF_SMEM);
     if (e != cudaSuccess) return e;
     e = set_dyn_smem(k_prepare_p_snap, HALF_SMEM);
@@ -1014,8 +1045,9 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
             if (blocks < (long)lc.sms * HALF_BPS) blocks = (long)lc.sms * HALF_BPS;  // every SM the same
 #endif
             // compacted tiles: resident blocks loop over the live tiles
-            if (p.pol_compact && blocks > (long)lc.sms * HALF_BPS * ECO_POL_COMPACT_WAVES)
+            if (p.pol_compact && p.n_ranks == 1 && blocks > (long)lc.sms * HALF_BPS * ECO_POL_COMPACT_WAVES)
                 blocks = (long)lc.sms * HALF_BPS * ECO_POL_COMPACT_WAVES;
+            const bool cpt = p.pol_compact && p.n_ranks == 1;
             if (p.n_ranks > 1 && p.split) k_policy_half<true, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.n_ranks > 1) k_policy_half<true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.split && pdl) {  // a programmatic dependent of the previous k_post
@@ -1029,9 +1061,12 @@ cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t 
                 attr[0].val.programmaticStreamSerializationAllowed = 1;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                return cudaLaunchKernelEx(&cfg, k_policy_half<false, true>, p);
+                return cpt ? cudaLaunchKernelEx(&cfg, k_policy_half<false, true, true>, p)
+                           : cudaLaunchKernelEx(&cfg, k_policy_half<false, true>, p);
             }
+            else if (p.split && cpt) k_policy_half<false, true, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else if (p.split) k_policy_half<false, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
+            else if (cpt) k_policy_half<false, false, true><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             else k_policy_half<false><<<(unsigned)(blocks > 0 ? blocks : 1), HALF_THREADS, HALF_SMEM, s>>>(p);
             break;
         }

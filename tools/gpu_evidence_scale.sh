@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu --set full of one step of the large world at its cap and of the 64-world ensemble
-TAG=${1:-r2x}
+TAG=${1:-r2z}
 OUT=gpurun_out
 mkdir -p $OUT
 : > $OUT/status_scale_$TAG.txt

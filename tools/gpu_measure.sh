@@ -2,7 +2,7 @@
 # Measurement job: smoke, the whole -m gpu suite, the bench at the driver's settings
 # and at its defaults, the ncu launch list, one --set full capture of a paper-scale step at
 # A ~ 1000 (t ~ 10) and at t ~ 3000, the regrowth micro and its two captures.
-TAG=${1:-r2x}
+TAG=${1:-r2z}
 OUT=gpurun_out
 mkdir -p $OUT
 : > $OUT/status_$TAG.txt
