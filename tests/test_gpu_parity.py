@@ -289,6 +289,47 @@ def test_ensemble_batch_equals_single_worlds_and_oracle():
         w1.destroy()
 
 
+def test_batched_uneven_worlds_equal_single_worlds():
+    """40 worlds of very different populations in one handle (the several-world policy walks
+    compacted tiles of the worlds' live list positions, the mutation one sequence over all
+    worlds' children, the ranking blocks share the regrowth): empty worlds, 1, 2, 15..17
+    agents (a tile boundary), a full slot table, worlds past the first 32 (the count chunks)
+    -- every world bit-identical to the same state stepped alone, and to the oracle after
+    one step."""
+    n_w = 40
+    wc1 = workloads.paper_scale().replace(rows=40, cols=80, slots=512, n_initial=100, seeds=(200,))
+    counts = [0, 1, 2, 15, 16, 17, 511, 512, 0, 33] + [int(c) for c in np.random.default_rng(5).integers(0, 513, n_w - 10)]
+    states = [workloads.random_state(wc1, 300 + w, n_alive=counts[w], density=0.3, t=77) for w in range(n_w)]
+    wcb = wc1.replace(seeds=tuple(range(200, 200 + n_w)))
+    stack = {k: (np.stack([st[k] for st in states]) if isinstance(v, np.ndarray) else v) for k, v in states[0].items()}
+    batched = sim.World(wcb)
+    batched.set_state(stack)
+    batched.step(1)
+    g1 = batched.get_state()
+    for w in (0, 1, 5, 7, 33):  # against the oracle after one step
+        orc = oracle.OracleWorld(wc1.replace(seeds=(200 + w,)), state=states[w])
+        orec = orc.step()
+        compare_ints(gpu_world_state(g1, w), orc.state(), f"uneven batch world {w}")
+        compare_record(batched.step_log(77, 1)[0, w], orec, f"uneven batch world {w}")
+    batched.step(5)
+    gb = batched.get_state()
+    births = batched.step_log(77, 6)["births"].sum(axis=0)
+    assert (births > 0).sum() >= 20, births  # the mutation ran in many worlds at once
+    for w in range(n_w):
+        single = sim.World(wc1.replace(seeds=(200 + w,)))
+        single.set_state(states[w])
+        single.step(6)
+        gs = single.get_state()
+        live = gs["alive"][0] == 1
+        for k in sim.STATE_FIELDS:
+            if k == "weights":  # (a dead slot's weights are unspecified, sim.h)
+                assert np.array_equal(gb[k][w][live], gs[k][0][live]), (w, counts[w], k)
+            else:
+                assert np.array_equal(gb[k][w], gs[k][0]), (w, counts[w], k)
+        single.destroy()
+    batched.destroy()
+
+
 # --------------------------------------------------------------------- edge cases
 def test_edge_empty_and_degenerate_worlds():
     # no agents at all, agents but zero initial, single-row-pair grid, W not a multiple of 32
