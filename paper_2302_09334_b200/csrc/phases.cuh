@@ -244,6 +244,45 @@ __device__ __forceinline__ AgentIter agent_at(const DevParams &p, long v) {
     return a;
 }
 
+// Several worlds: the LIVE list positions of step t of all worlds as one world-major sequence
+// (a world holds ~1,100 agents in 8,192 slots: a thread striding over every slot of every
+// world runs 4-5 dependent iterations, most of them on empty positions).  live_prefix makes
+// cum[w] = the live positions of the worlds before w (cum[n_worlds] = all) in the block's
+// shared array (warp 0; every thread of the block calls it; ends with a block barrier).
+__device__ __forceinline__ void live_prefix(const DevParams &p, int64_t t, int *cum) {
+    if (threadIdx.x < 32) {
+        const int lane = (int)threadIdx.x, par = (int)(t & 1);
+        int run = 0;
+        for (int w0 = 0; w0 < p.n_worlds; w0 += 32) {
+            const int wl = w0 + lane;
+            const int cnt = wl < p.n_worlds ? p.n_alive[par * p.n_worlds + wl] : 0;
+            int inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int up = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += up;
+            }
+            if (wl < p.n_worlds) cum[wl] = run + inc - cnt;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) cum[p.n_worlds] = run;
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ AgentIter agent_at_live(const DevParams &p, const int *cum, long g) {
+    AgentIter a;
+    a.in_range = g < (long)cum[p.n_worlds];
+    int lo = 0, hi = p.n_worlds;  // cum[lo] <= g < cum[hi]: the last such lo
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if ((long)cum[mid] <= g) lo = mid;
+        else hi = mid;
+    }
+    a.w = a.in_range ? lo : 0;
+    a.i = a.in_range ? (int)(g - cum[lo]) : 0;
+    return a;
+}
+
 // ------------------------------------------------- Appendix C movement metrics (NEXT-3)
 #ifndef ECO_METRICS
 #define ECO_METRICS 3  // bit 0: ages at death, bit 1: movement histograms (diagnostic switch)
@@ -296,13 +335,15 @@ __device__ __forceinline__ void mv_pass_part(const DevParams &p, int64_t T, int 
 // PAPER: the paper world's death timer and lethal walls (death_steps > 0 or lethal_walls),
 // compiled into separate kernels so BASELINE's move phase keeps its code (measured: the
 // runtime checks cost 6 us per capped paper-scale step).
+// live_cum: live_prefix's array (several worlds: only live list positions are visited), or null.
 template <bool PAPER = false>
-__device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size_t gthreads) {
-    const long total = (long)p.n_worlds * p.S;
+__device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size_t gthreads,
+                                           const int *live_cum = nullptr) {
+    const long total = live_cum ? (long)live_cum[p.n_worlds] : (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
     const unsigned lane = gtid & 31;
     for (long base = (long)(gtid - lane); base < total; base += (long)gthreads) {
-        const AgentIter it = agent_at(p, base + lane);
+        const AgentIter it = live_cum ? agent_at_live(p, live_cum, base + lane) : agent_at(p, base + lane);
         const int w = it.w;
         // t, both parities' counts and the move record of list position i load together
         // (entries past the count are stale and unused)
@@ -463,12 +504,13 @@ __device__ __forceinline__ void move_phase(const DevParams &p, size_t gtid, size
 // the candidate cell by atomicMax (the max is the winner) and marks the cell in the step's
 // claimed-cell bitmap.  Distinct claimed cells are counted per world; deferred-claim losers
 // are (candidates - claimed cells).  Must be called by all 32 lanes.
-__device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads) {
-    const long total = (long)p.n_worlds * p.S;
+__device__ __forceinline__ void birth_claim_phase(const DevParams &p, size_t gtid, size_t gthreads,
+                                                  const int *live_cum = nullptr) {
+    const long total = live_cum ? (long)live_cum[p.n_worlds] : (long)p.n_worlds * p.S;
     const size_t HW = (size_t)p.H * p.W;
     const unsigned lane = gtid & 31;
     for (long base = (long)(gtid - lane); base < total; base += (long)gthreads) {
-        const AgentIter it = agent_at(p, base + lane);
+        const AgentIter it = live_cum ? agent_at_live(p, live_cum, base + lane) : agent_at(p, base + lane);
         const int w = it.w;
         const int64_t t = p.t[w];
         unsigned long long no_cell = 0, cand = 0;

@@ -1189,8 +1189,13 @@ constexpr int ECO_BLOCK_CLOCK_BASE = 16;
 #define POST_SYNC(k) grid_sync(bar, target, nthr)
 #endif
 
-template <bool SHARD, bool BIG = false, bool PAPER = false>
+// MULTI: several worlds in the handle (the launcher's choice: p.n_worlds > 1), compiled as its
+// own variant so that the one-world kernels carry none of its code (the one-shot phases are
+// sensitive to code size and layout: as runtime branches the several-world paths cost the
+// paper-scale step 0.8 us, measured)
+template <bool SHARD, bool BIG = false, bool PAPER = false, bool MULTI = false>
 __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned long long *bar) {
+    static_assert(!(MULTI && (SHARD || BIG)), "several worlds: unsharded, no split policy");
     DevParams p = p_;
     if (!SHARD) p.n_ranks = 1;
     __shared__ uint32_t scratch[2 * (POST_THREADS / 32 + 1)];
@@ -1213,7 +1218,7 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
     // (a child placed in such a slot starts from its bias).
     constexpr int HH_WARPS = BIG ? ECO_HH_WARPS_BIG : ECO_HH_WARPS;  // compile-time: the roles need no load
     constexpr int DYN_WARPS = POST_THREADS / 32 - HH_WARPS;
-    const bool hh_split = p.split && p.n_worlds == 1 && gridDim.x > 1;
+    const bool hh_split = !MULTI && p.split && p.n_worlds == 1 && gridDim.x > 1;
 #ifdef ECO_END_CLOCK
     // diagnostic build: per launch, the latest end of the P warps and of the other warps
     // after block 0's start, summed over the launches in phase_ns[4] and [5]
@@ -1291,23 +1296,29 @@ __global__ void __launch_bounds__(POST_THREADS) k_post(DevParams p_, unsigned lo
         }
         grid_sync(bar, target, nthr);
     }
-    move_phase<PAPER>(p, gtid, gthreads);
+    // several worlds: the move and claim phases visit the worlds' live list positions only
+    const int *live_cum = nullptr;
+    if (MULTI && p.n_worlds < RANK_SMEM_CAP) {
+        live_prefix(p, T, s_free);  // (s_free: free until the rank)
+        live_cum = s_free;
+    }
+    move_phase<PAPER>(p, gtid, gthreads, live_cum);
     POST_SYNC(0);
     lap(0);
     // sharded + split: this rank's survivors lead its next list; its children (appended by
     // the placement) follow and have no P row
     if (SHARD && p.split && blockIdx.x == 0 && threadIdx.x == 0)
         *p.own_surv = *reinterpret_cast<volatile int32_t *>(p.own_count + ((T + 1) & 1));
-    if (p.n_worlds > 1) {
+    if (MULTI) {
         // birth candidates on every thread
         const uint64_t h0 = blockIdx.x == 0 ? globaltimer_ns() : 0ull;
-        birth_claim_phase(p, gtid, gthreads);
+        birth_claim_phase(p, gtid, gthreads, live_cum);
         if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)  // summed warp durations of block 0
             atomicAdd(p.phase_ns + 8, globaltimer_ns() - h0);
         POST_SYNC(1);
         lap(1);
     }
-    if (p.n_worlds == 1) {
+    if (!MULTI) {
         // one world: block 0 ranks the births and resolves their winners, publishes the
         // birth lists with a release flag, then places the children and writes the counters
         // (t += 1).  The other blocks regrow the grid of step T+1 meanwhile (it needs only R''
@@ -1845,6 +1856,10 @@ cudaError_t post_prepare() {
     if (e != cudaSuccess) return e;
     e = set_dyn_smem(k_post<false, false, true>, POST_SMEM_SMALL);
     if (e != cudaSuccess) return e;
+    e = set_dyn_smem(k_post<false, false, false, true>, POST_SMEM_SMALL);
+    if (e != cudaSuccess) return e;
+    e = set_dyn_smem(k_post<false, false, true, true>, POST_SMEM_SMALL);
+    if (e != cudaSuccess) return e;
     e = set_dyn_smem(k_post<false, true, true>, POST_SMEM);
     if (e != cudaSuccess) return e;
     return set_dyn_smem(k_post<false>, POST_SMEM_SMALL);
@@ -1883,6 +1898,8 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
 #endif
     if (p.n_ranks > 1 && paper_rules(p)) return cudaErrorInvalidValue;  // (sim_shard refuses the paper rules)
     if (p.n_ranks > 1) return cudaLaunchKernelEx(&cfg, post_big(p) ? k_post<true, true> : k_post<true>, p, bar);
+    if (p.n_worlds > 1)  // (post_big needs the split policy, i.e. one world)
+        return cudaLaunchKernelEx(&cfg, paper_rules(p) ? k_post<false, false, true, true> : k_post<false, false, false, true>, p, bar);
     if (paper_rules(p))
         return cudaLaunchKernelEx(&cfg, post_big(p) ? k_post<false, true, true> : k_post<false, false, true>, p, bar);
     if (post_big(p)) return cudaLaunchKernelEx(&cfg, k_post<false, true>, p, bar);

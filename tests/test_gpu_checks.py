@@ -4,7 +4,8 @@ libsim_checked.so (-DECO_CHECKS=1), whose kernels assert every cell, slot, list 
 and outbox index they compute.  A fresh process runs it over 50 steps of: the tiny world
 and a 64x64 world through the graph path and through the instrumented path (every phase
 a separate kernel), the paper-scale network on a small grid (split policy, k_post with P
-warps), a 3-world batch, the paper's CNN-LSTM world (network 1) and a 4-band banded world; any failed assert aborts the process.
+warps), a 3-world batch, a 20-world Hd = 32 batch (the compacted policy tiles, the single mutation
+sequence), the paper's CNN-LSTM world (network 1) and a 4-band banded world; any failed assert aborts the process.
 The same runs with the product build must give the same step records (the checks change
 no result)."""
 import json
@@ -32,6 +33,8 @@ cases = {
     "hd32": (workloads.tiny().replace(rows=40, cols=96, slots=600, n_initial=400, hidden=32, obs_radius=3,
                                       repr_steps=6, e_repr_gt=10300, seeds=(4,)), None),
     "batch": (workloads.tiny().replace(seeds=(1, 2, 3), repr_steps=5, e_repr_gt=10200), None),
+    "batch_hd32": (workloads.tiny().replace(rows=40, cols=96, slots=600, n_initial=400, hidden=32, obs_radius=3,
+                                            repr_steps=6, e_repr_gt=10300, seeds=tuple(range(40, 60))), None),
     "cnn": (workloads.paper_world_cnn().replace(rows=40, cols=60, slots=200, n_initial=120, repr_steps=20,
                                                  seeds=(11,)), None),
     "coloc": (workloads.paper_world_coloc().replace(rows=40, cols=60, slots=300, n_initial=150, repr_steps=20,
