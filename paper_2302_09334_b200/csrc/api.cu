@@ -243,7 +243,7 @@ struct sim_ctx {
     int32_t *n_own_dev = nullptr;
     struct BandNccl *nccl = nullptr; // parent with remote bands: the NCCL barrier
     cudaStream_t side = nullptr;     // parent: the split policy's P rows beside the step
-    cudaEvent_t fork_ev[eco::BAND_MAX] = {}, join_ev = nullptr;
+    cudaEvent_t fork_ev[eco::BAND_MAX] = {}, fork2_ev[eco::BAND_MAX] = {}, join_ev = nullptr;
     int32_t *band_tmp = nullptr;     // parent: device scratch of get_state (a band's live list)
     float *band_canon = nullptr;     // parent: canonical rows of one band's live weights
     size_t band_canon_rows = 0;
@@ -439,6 +439,8 @@ void destroy_all(sim_ctx *h) {
         cudaStreamDestroy(h->side);
     }
     for (auto &e : h->fork_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : h->fork2_ev)
         if (e) cudaEventDestroy(e);
     if (h->join_ev) cudaEventDestroy(h->join_ev);
     band_nccl_destroy(h);
@@ -661,7 +663,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
         CKC(dalloc(h, &bp.cslot, HW), "alloc");
         CKC(dalloc(h, &bp.hcand, 2 * (size_t)bp.cap), "alloc");
         CKC(dalloc(h, &bp.n_hcand, 1), "alloc");
-        CKC(dalloc(h, &bp.snap, 2), "alloc");
+        CKC(dalloc(h, &bp.snap, 4), "alloc");
         CKC(dalloc(h, &bp.flags, 4), "alloc");
         CKC(dalloc(h, &h->n_own_dev, 1), "alloc");
     }

@@ -787,9 +787,21 @@ __global__ void k_band_snap(DevParams p, BandParams bp) {
     bp.counts[(t & 1) * 4 + 1] = n;  // survivors, read by every band for the global cap
 }
 
+// split policy, right after the policy: the step and its list's count, read by the P-row
+// kernel that runs on the second stream from here to the step's end (P10 advances t meanwhile)
+__global__ void k_band_snap0(DevParams p, BandParams bp) {
+    const int64_t t = p.t[0];
+    bp.snap[2] = t;
+    bp.snap[3] = *count_of(p, t, 0);
+}
+
 // --------------------------------------------------------------------- launchers
 cudaError_t band_snap(const DevParams &p, const BandParams &bp, cudaStream_t s) {
     k_band_snap<<<1, 1, 0, s>>>(p, bp);
+    return cudaGetLastError();
+}
+cudaError_t band_snap0(const DevParams &p, const BandParams &bp, cudaStream_t s) {
+    k_band_snap0<<<1, 1, 0, s>>>(p, bp);
     return cudaGetLastError();
 }
 cudaError_t band_halo(const DevParams &p, const BandParams &bp, int kind, cudaStream_t s) {

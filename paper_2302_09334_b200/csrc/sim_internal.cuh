@@ -183,7 +183,8 @@ struct BandParams {
     int4 *hcand;               // [2 cap] own parents claiming a cell in a neighbour's row:
                                // (parent slot, parent cell, claimed cell, claim key hi)
     int32_t *n_hcand;
-    int64_t *snap;             // [2] split policy: (step t, survivors) after P5, for the P rows
+    int64_t *snap;             // [4] (step t + 1, survivors) after P5 (the global cap's input); split policy: [2..3] =
+                               // (step t, its list's count) after the policy, for the P rows on the second stream
     int32_t *flags;            // [0] bit 0: local slot pool exhausted; [1] arrivals placed
     BandPeer up, down;         // bands b-1 and b+1 (plane0 == nullptr: none)
     const int64_t *all_counts[BAND_MAX];  // every band's counts
@@ -402,6 +403,8 @@ int policy_compact_worlds();  // most worlds the compacted policy mapping (pol_c
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);  // P of step t
 cudaError_t launch_prepare_p_snap(const DevParams &p, const int64_t *snap, cudaStream_t s);  // banded
 cudaError_t band_snap(const DevParams &p, const BandParams &bp, cudaStream_t s);
+cudaError_t band_snap0(const DevParams &p, const BandParams &bp, cudaStream_t s);
+cudaError_t launch_prepare_p_list(const DevParams &p, const int32_t *list, const int32_t *n, int sms, cudaStream_t s);  // banded
 cudaError_t post_prepare();  // kernel attributes of k_post (dynamic shared memory)
 
 // banded mode (band.cu); kinds: halo 0 = X1, 1 = X4a; merge 0 = X2, 1 = X4b

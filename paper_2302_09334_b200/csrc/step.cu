@@ -559,8 +559,8 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p(DevParams 
     }
 }
 
-// Banded mode: P rows of the survivors of the step in progress (list_of(snap[0])[0, snap[1]),
-// snapshotted right after the band's consumption/physiology/death), on a second stream while
+// Banded mode: P rows of list_of(snap[0])[0, snap[1]) — the agents of the step in progress,
+// snapshotted right after the band's policy (band_snap0) — on a second stream while
 // the rest of the step runs; the children placed later have none (p_children, set by the rank).
 __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p_snap(DevParams p, const int64_t *snap) {
     extern __shared__ __align__(1024) float4 half_smem[];
@@ -568,6 +568,15 @@ __global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p_snap(DevPa
     const int ag = warp * 2 + (lane >> 4);
     hh_pass<HALF_DEPTH>(p, list_of(p, snap[0], 0), (int)snap[1], ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS,
                         half_smem + (ag * HALF_DEPTH) * 32);
+}
+
+// Banded mode: P rows of the slots list[0, *n) (the step's arrivals from the neighbour bands)
+__global__ void __launch_bounds__(HALF_THREADS, HALF_BPS) k_prepare_p_list(DevParams p, const int32_t *list,
+                                                                           const int32_t *n) {
+    extern __shared__ __align__(1024) float4 half_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ag = warp * 2 + (lane >> 4);
+    hh_pass<HALF_DEPTH>(p, list, *n, ag * gridDim.x + blockIdx.x, gridDim.x * HALF_AGENTS, half_smem + (ag * HALF_DEPTH) * 32);
 }
 
 #ifdef ECO_TIMELINE
@@ -1020,6 +1029,8 @@ cudaError_t policy_prepare() {
     e = set_dyn_smem(k_prepare_p, HALF_SMEM);
     if (e != cudaSuccess) return e;
     e = set_dyn_smem(k_prepare_p_snap, HALF_SMEM);
+    if (e != cudaSuccess) return e;
+    e = set_dyn_smem(k_prepare_p_list, HALF_SMEM);
     if (e != cudaSuccess) return e;
     return set_dyn_smem(k_policy_half<false>, HALF_SMEM);
 }
@@ -1796,6 +1807,12 @@ cudaError_t launch_prepare_p_snap(const DevParams &p, const int64_t *snap, cudaS
     if (!p.split) return cudaSuccess;
     const unsigned blocks = (unsigned)((p.S + HALF_AGENTS - 1) / HALF_AGENTS);
     k_prepare_p_snap<<<blocks > 0 ? blocks : 1, HALF_THREADS, HALF_SMEM, s>>>(p, snap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepare_p_list(const DevParams &p, const int32_t *list, const int32_t *n, int sms, cudaStream_t s) {
+    if (!p.split) return cudaSuccess;
+    k_prepare_p_list<<<sms > 0 ? sms : 1, HALF_THREADS, HALF_SMEM, s>>>(p, list, n);
     return cudaGetLastError();
 }
 

@@ -101,9 +101,11 @@ def main():
                 wb.destroy()
             assert np.array_equal(lb, log1), "banded records differ from the unbanded world"
             slowest = ph.max(axis=0)
-            # the P rows (prep_p) run on a second stream beside the phases after it
-            ip = sim.BAND_PHASES.index("prep_p")
-            compute = float(slowest[:ip].sum() + max(slowest[ip + 1:].sum(), slowest[ip]))
+            # the P rows (prep_p) run on a second stream from the end of the band's policy on,
+            # beside every later phase
+            ip, ipol = sim.BAND_PHASES.index("prep_p"), sim.BAND_PHASES.index("policy")
+            rest = float(slowest[ipol + 1:].sum() - slowest[ip])
+            compute = float(slowest[:ipol + 1].sum() + max(rest, slowest[ip]))
             barriers = (5 * a.nbr_us + a.all_us) / 1e3  # 5 neighbour barriers, 1 all-reduce per step
             est = compute + barriers
             # graph estimate: the mean band step inside the one-GPU graph (T_graph / G), scaled by
