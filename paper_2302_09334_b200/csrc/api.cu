@@ -313,6 +313,10 @@ cudaError_t launch_phase(sim_ctx *h, int k) {
 // graph-mode step: the policy kernel, then the cooperative post-policy kernel
 cudaError_t enqueue_step(sim_ctx *h, bool pdl = false) {
     cudaError_t e;
+    if (h->p.S == 0 && h->p.regrow_split && !h->p.coloc) {  // an agent-free world: bookkeeping, then the regrowth of t+1
+        if ((e = eco::launch_advance_empty(h->p, h->stream)) != cudaSuccess) return e;
+        return eco::launch_regrow(h->p, 0, h->stream);
+    }
     if ((e = eco::launch_policy(h->p, h->lc, h->stream, pdl)) != cudaSuccess) return e;
     if ((e = eco::launch_post(h->p, h->lc, h->bar, h->stream)) != cudaSuccess) return e;
     if (h->p.regrow_split) return eco::launch_regrow(h->p, 0, h->stream);  // step t+1 (k_post advanced t)
@@ -725,7 +729,7 @@ sim_status create_one(const sim_config *cfg, const eco::BandParams *band, sim_ha
         if (pbs < 1) return bail(fail(SIM_E_CUDA, "k_post cannot be resident"));
         h->lc.post_blocks = prop.multiProcessorCount;  // one block per SM
     }
-    p.regrow_split = (S == 0 && !band && eco::regrow_tiled(p)) ? 1 : 0;  // agent-free benchmark grids
+    p.regrow_split = (S == 0 && !band) ? 1 : 0;  // agent-free benchmark grids: the regrowth as its own launch
 
     // K0: resources, check N0 <= empty cells, agents + weights, occupancy/lists
     CKC(eco::launch_init_resources(p, h->stream), "init resources");

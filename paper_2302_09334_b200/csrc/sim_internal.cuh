@@ -403,6 +403,7 @@ int policy_compact_worlds();  // most worlds the compacted policy mapping (pol_c
 cudaError_t launch_prepare_p(const DevParams &p, const LaunchCfg &lc, cudaStream_t s);  // P of step t
 cudaError_t launch_prepare_p_snap(const DevParams &p, const int64_t *snap, cudaStream_t s);  // banded
 cudaError_t band_snap(const DevParams &p, const BandParams &bp, cudaStream_t s);
+cudaError_t launch_advance_empty(const DevParams &p, cudaStream_t s);  // an agent-free world's step bookkeeping
 cudaError_t band_snap0(const DevParams &p, const BandParams &bp, cudaStream_t s);
 cudaError_t launch_prepare_p_list(const DevParams &p, const int32_t *list, const int32_t *n, int sms, cudaStream_t s);  // banded
 cudaError_t post_prepare();  // kernel attributes of k_post (dynamic shared memory)

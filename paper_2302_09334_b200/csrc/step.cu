@@ -172,6 +172,21 @@ __device__ __forceinline__ void agent_epilogue(const DevParams &p, int w, int i,
 // list of step t+1, the winner counters and the record of step t+1 (whose regrowth runs
 // early, inside this step's k_post) start at 0; the claimed-cell bitmap of parity t+1
 // (used by step t-1) is cleared for step t+1.
+// (one thread per world: the counters and the record of step t+1)
+__device__ __forceinline__ void housekeeping_world(const DevParams &p, int w) {
+    const int64_t tw = p.t[w];
+    *count_of(p, tw + 1, w) = 0;
+    p.n_win[w] = 0;
+    p.n_cand[w] = 0;
+    if (p.n_ranks > 1 && w == 0) p.own_count[(tw + 1) & 1] = 0;
+    sim_step_record *nxt = record_of(p, tw + 1, w);
+    *nxt = sim_step_record{};
+    nxt->t = tw + 1;
+    if (tw % SIM_MOVE_WINDOW == SIM_MOVE_WINDOW - 1) {  // this step ends window tw/50: its bins from 0
+        int32_t *hist = p.mv_hist + ((size_t)w * p.mv_cap + (size_t)((tw / SIM_MOVE_WINDOW) & (p.mv_cap - 1))) * SIM_MOVE_BINS;
+        for (int b = 0; b < SIM_MOVE_BINS; ++b) hist[b] = 0;
+    }
+}
 __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
     const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t gthreads = (size_t)gridDim.x * blockDim.x;
@@ -190,20 +205,7 @@ __device__ __forceinline__ void step_housekeeping(const DevParams &p) {
             }
         }
     }
-    for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) {
-        const int64_t tw = p.t[w];
-        *count_of(p, tw + 1, (int)w) = 0;
-        p.n_win[w] = 0;
-        p.n_cand[w] = 0;
-        if (p.n_ranks > 1 && w == 0) p.own_count[(tw + 1) & 1] = 0;
-        sim_step_record *nxt = record_of(p, tw + 1, (int)w);
-        *nxt = sim_step_record{};
-        nxt->t = tw + 1;
-        if (tw % SIM_MOVE_WINDOW == SIM_MOVE_WINDOW - 1) {  // this step ends window tw/50: its bins from 0
-            int32_t *hist = p.mv_hist + ((size_t)w * p.mv_cap + (size_t)((tw / SIM_MOVE_WINDOW) & (p.mv_cap - 1))) * SIM_MOVE_BINS;
-            for (int b = 0; b < SIM_MOVE_BINS; ++b) hist[b] = 0;
-        }
-    }
+    for (size_t w = gtid; w < (size_t)p.n_worlds; w += gthreads) housekeeping_world(p, (int)w);
 }
 
 // ------------------------------------------------------------- cp.async helpers
@@ -1472,6 +1474,9 @@ constexpr int RG_VW = (RG_TW + 8) / 4;           // uint4 per staged row (4-word
 constexpr int RG_SROWS = RG_TH + 4;
 constexpr int RG_LOADS = RG_SROWS * RG_VW;       // 360 vectors per tile
 constexpr int RG_STAGES = 3;
+#ifndef ECO_RG_BPS
+#define ECO_RG_BPS 4  // resident blocks per SM the tiled regrowth is compiled for (registers per thread)
+#endif
 constexpr int RG_WORDS = RG_TW * RG_TH;
 static_assert(RG_WORDS == 4 * RG_THREADS, "one 4-word vector per thread");
 
@@ -1523,7 +1528,7 @@ __device__ __forceinline__ uint32_t spread16(uint32_t x) {
     return x;
 }
 
-__global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int ahead) {
+__global__ void __launch_bounds__(RG_THREADS, ECO_RG_BPS) k_regrow_tiled(DevParams p, int ahead) {
     extern __shared__ __align__(1024) uint4 rg_dyn[];  // the stage ring [RG_STAGES][RG_STAGE_VECS]
     uint4 (*s_ring)[RG_STAGE_VECS] = reinterpret_cast<uint4 (*)[RG_STAGE_VECS]>(rg_dyn);
     __shared__ uint32_t s_code[2][RG_WORDS];     // listed words: 2-bit class per cell (cells 0-15, 16-31)
@@ -1734,6 +1739,24 @@ __global__ void __launch_bounds__(RG_THREADS, 4) k_regrow_tiled(DevParams p, int
 // words of all worlds from which the tiled kernel is used (the per-word gather path keeps
 // small grids on up to 8 lanes per word, shorter Philox chains)
 constexpr size_t RG_TILED_MIN_WORDS = 65536;
+
+// An agent-free world (no slots: the configs[2] regrowth grids): a step is the regrowth kernel
+// and this bookkeeping — the record and counters of step t+1 from zero, step t's record
+// (resources += grown, as the rank's last thread writes it), t += 1 — one thread per world;
+// no policy launch and no k_post (which would sweep a 16.8 MB claimed-cell bitmap and run
+// five empty phases: 47 of the 94 us per step at 8192x16384).
+__global__ void __launch_bounds__(256) k_advance_empty(DevParams p) {
+    for (int w = threadIdx.x; w < p.n_worlds; w += blockDim.x) {
+        const int64_t t = p.t[w];
+        housekeeping_world(p, w);
+        rank_finalize(p, w, t, 0, 0, 0, 0);
+        p.t[w] = t + 1;
+    }
+}
+cudaError_t launch_advance_empty(const DevParams &p, cudaStream_t s) {
+    k_advance_empty<<<1, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 bool regrow_tiled(const DevParams &p) {
     const int real_words = (p.W + 31) >> 5;
