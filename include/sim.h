@@ -212,7 +212,9 @@ SIM_API sim_status sim_create(const sim_config *cfg, sim_handle *out);
  * (a two-step graph per pair of steps for n >= 2, whose second policy is a programmatic
  * dependent of the first k_post; a one-step graph for an odd remainder).  The graphs are
  * captured at the handle's first step and whenever a kernel parameter changes
- * (sim_set_record_mirror), never by a later sim_step. */
+ * (sim_set_record_mirror), never by a later sim_step.  A world without agent slots
+ * (slots = 0: the regrowth grids of BASELINE configs[2]) steps with a one-block bookkeeping
+ * kernel and the regrowth kernel instead (same records, no policy and no k_post launch). */
 SIM_API sim_status sim_step(sim_handle h, int64_t n);
 /* Synchronise, convert to the canonical layout and copy into caller buffers. */
 SIM_API sim_status sim_get_state(sim_handle h, sim_state *out);
