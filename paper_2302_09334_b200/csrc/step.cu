@@ -1473,7 +1473,10 @@ constexpr int RG_THREADS = 256;                  // one 4-word vector per thread
 constexpr int RG_VW = (RG_TW + 8) / 4;           // uint4 per staged row (4-word halo each side)
 constexpr int RG_SROWS = RG_TH + 4;
 constexpr int RG_LOADS = RG_SROWS * RG_VW;       // 360 vectors per tile
-constexpr int RG_STAGES = 3;
+#ifndef ECO_RG_STAGES
+#define ECO_RG_STAGES 3
+#endif
+constexpr int RG_STAGES = ECO_RG_STAGES;
 #ifndef ECO_RG_BPS
 #define ECO_RG_BPS 4  // resident blocks per SM the tiled regrowth is compiled for (registers per thread)
 #endif
@@ -1485,7 +1488,38 @@ static_assert(RG_WORDS == 4 * RG_THREADS, "one 4-word vector per thread");
 // no dependent global load
 constexpr int RG_STAGE_VECS = RG_LOADS + RG_TH;
 constexpr int RG_DYN_SMEM = RG_STAGES * RG_STAGE_VECS * 16;
-__device__ __forceinline__ void rg_issue(const DevParams &p, const uint32_t *src, int y0, int wx0, uint4 *stage) {
+// (ro: this thread's one or two window vectors as word offsets from the tile's origin, made
+// once per launch — a tile whose window lies inside the grid needs no bounds test and no
+// index arithmetic per vector: the staging was 40 % of the full-grid kernel's instructions)
+struct RgOff {
+    int off0, off1;
+    bool has1;
+};
+__device__ __forceinline__ RgOff rg_offsets(const DevParams &p) {
+    RgOff o;
+    const int k0 = threadIdx.x, k1 = threadIdx.x + RG_THREADS;
+    static_assert(RG_LOADS > RG_THREADS && RG_LOADS <= 2 * RG_THREADS, "one or two window vectors per thread");
+    o.off0 = (k0 / RG_VW - 2) * p.WW + 4 * (k0 % RG_VW) - 4;
+    o.has1 = k1 < RG_LOADS;
+    o.off1 = (k1 / RG_VW - 2) * p.WW + 4 * (k1 % RG_VW) - 4;
+    return o;
+}
+__device__ __forceinline__ void rg_issue(const DevParams &p, const uint32_t *src, int y0, int wx0, uint4 *stage,
+                                         const RgOff &ro) {
+    if (y0 >= 2 && y0 + RG_TH + 2 <= p.H && y0 + RG_TH <= p.row_hi && wx0 >= 4 && wx0 + RG_TW + 4 <= p.WW) {
+        if (threadIdx.x < RG_TH)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(stage + RG_LOADS + threadIdx.x)),
+                         "l"(p.T + (size_t)(y0 + (int)threadIdx.x) * 4)
+                         : "memory");
+        const uint32_t *base = src + (size_t)y0 * p.WW + wx0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(stage + threadIdx.x)), "l"(base + ro.off0)
+                     : "memory");
+        if (ro.has1)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(stage + threadIdx.x + RG_THREADS)),
+                         "l"(base + ro.off1)
+                         : "memory");
+        return;
+    }
     for (int k = threadIdx.x; k < RG_TH; k += RG_THREADS) {
         const int y = y0 + k;
         const bool in = y < p.row_hi;
@@ -1573,11 +1607,12 @@ __global__ void __launch_bounds__(RG_THREADS, ECO_RG_BPS) k_regrow_tiled(DevPara
         a.w += stride.w;
     };
     TileAt at_issue = decompose((int)blockIdx.x), at = at_issue;
+    const RgOff ro = rg_offsets(p);
     auto issue = [&](int j) {  // the block's j-th tile into stage j % RG_STAGES (an empty group past the end)
         const int tile = blockIdx.x + j * gridDim.x;
         if (tile < ntiles)
             rg_issue(p, plane_cur(p, tstep) + (size_t)at_issue.w * pw, p.row_lo + at_issue.ty * RG_TH,
-                     at_issue.tx * RG_TW, s_ring[j % RG_STAGES]);
+                     at_issue.tx * RG_TW, s_ring[j % RG_STAGES], ro);
         advance(at_issue);
         cp_commit();
     };
