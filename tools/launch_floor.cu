@@ -1,7 +1,8 @@
 // The event-timed floor of one step's launches after an L2 flush, by launch method:
 // (a) a CUDA graph of {plain kernel, cooperative kernel with a programmatic edge} — what
 // sim_step(1) launches — against (b) the same two kernels launched directly on the stream,
-// (c) one cooperative kernel alone (graph and direct), (d) two events with nothing between.
+// (c) one cooperative kernel alone (graph and direct), (d) two events with nothing between,
+// (e) the graphs of (a) and (c) without the cooperative attribute on the 148 x 768 kernel.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o /tmp/launch_floor tools/launch_floor.cu
 #include <algorithm>
 #include <cstdio>
@@ -33,6 +34,7 @@ __global__ void k_flush(const float4 *src, float *out, size_t n) {
     if (acc == 123.456f) out[0] = acc;
 }
 
+static bool g_no_coop = false;  // the second kernel without the cooperative attribute (same grid)
 static cudaError_t launch_pair(cudaStream_t s, int *x, bool coop_only) {
     cudaError_t e = cudaSuccess;
     if (!coop_only) {
@@ -52,6 +54,10 @@ static cudaError_t launch_pair(cudaStream_t s, int *x, bool coop_only) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = coop_only ? 1 : 2;
+    if (g_no_coop) {  // only the programmatic edge (or no attribute at all)
+        at[0] = at[1];
+        cfg.numAttrs = coop_only ? 0 : 1;
+    }
     return cudaLaunchKernelEx(&cfg, k_b, x);
 }
 
@@ -72,18 +78,21 @@ int main() {
         CK(cudaEventCreate(&e0[i]));
         CK(cudaEventCreate(&e1[i]));
     }
-    cudaGraph_t g[2];
-    cudaGraphExec_t ge[2];
-    for (int c = 0; c < 2; ++c) {
+    cudaGraph_t g[4];
+    cudaGraphExec_t ge[4];
+    for (int c = 0; c < 4; ++c) {
+        g_no_coop = c >= 2;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        CK(launch_pair(s, x, c == 1));
+        CK(launch_pair(s, x, (c & 1) == 1));
         CK(cudaStreamEndCapture(s, &g[c]));
         CK(cudaGraphInstantiate(&ge[c], g[c], 0));
         CK(cudaGraphUpload(ge[c], s));
     }
-    const char *names[] = {"graph {plain, coop+PDL}", "direct {plain, coop+PDL}", "graph {coop}", "direct {coop}", "nothing"};
+    g_no_coop = false;
+    const char *names[] = {"graph {plain, coop+PDL}", "direct {plain, coop+PDL}", "graph {coop}", "direct {coop}", "nothing",
+                           "graph {plain, big+PDL}", "graph {big}"};
     for (int flush = 1; flush >= 0; --flush)
-        for (int m = 0; m < 5; ++m) {
+        for (int m = 0; m < 7; ++m) {
             for (int i = 0; i < K; ++i) {
                 if (flush) {
                     CK(cudaMemsetAsync(fb, i & 1, FL, s));
@@ -94,6 +103,8 @@ int main() {
                 if (m == 1) CK(launch_pair(s, x, false));
                 if (m == 2) CK(cudaGraphLaunch(ge[1], s));
                 if (m == 3) CK(launch_pair(s, x, true));
+                if (m == 5) CK(cudaGraphLaunch(ge[2], s));
+                if (m == 6) CK(cudaGraphLaunch(ge[3], s));
                 CK(cudaEventRecord(e1[i], s));
             }
             CK(cudaStreamSynchronize(s));
