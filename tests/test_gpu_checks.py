@@ -74,3 +74,36 @@ def test_checked_build_runs_clean_and_changes_nothing():
     a = json.loads(rc.stdout.strip().splitlines()[-1])
     b = json.loads(ref.stdout.strip().splitlines()[-1])
     assert a == b
+
+
+COMPACT_SCRIPT = r'''
+import hashlib, json, sys
+sys.path.insert(0, ROOT)
+import numpy as np
+import workloads
+from paper_2302_09334_b200 import sim
+wc = workloads.paper_scale().replace(rows=120, cols=200, slots=16384, n_initial=3000, seeds=(21,))
+w = sim.World(wc)
+w.step(40)
+st = w.get_state()
+live = st["alive"][0] == 1
+h = hashlib.sha256()
+for k in sim.STATE_FIELDS:
+    a = st[k][0][live] if k in ("weights", "h", "c") else st[k][0]
+    h.update(np.ascontiguousarray(a).tobytes())
+print(json.dumps({"digest": h.hexdigest(), "records": w.step_log(0, 40).tolist()}))
+w.destroy()
+'''
+
+
+def test_compacted_policy_forced_on_one_world_changes_nothing():
+    """ECO_POL_COMPACT=1 compacts the policy's tiles for ONE world whose slots need more than a
+    wave of blocks (default: several worlds only): same state and records as the default."""
+    code = COMPACT_SCRIPT.replace("ROOT", repr(ROOT))
+    outs = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           env=dict(os.environ, ECO_POL_COMPACT=v), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1] and len(outs[0]["records"]) == 40

@@ -87,6 +87,36 @@ def test_regrowth_other_radii(r2):
     assert np.array_equal(world.get_state(("resources",))["resources"][0], R)
 
 
+def test_regrowth_only_several_worlds_and_resume():
+    """Agent-free worlds step with the regrowth kernel and the one-block bookkeeping kernel
+    (k_advance_empty): three worlds in one handle against the oracle's regrowth world by
+    world (grids, grown and resource counts of every record), and a resume from get_state."""
+    seeds = (2, 3, 4)
+    wc = workloads.regrowth_micro(70, 132).replace(seeds=seeds)
+    world = sim.World(wc)
+    Rs = [oracle.OracleWorld(wc.replace(seeds=(s_,))).st["resources"].copy() for s_ in seeds]
+    for t in range(25):
+        world.step(1)
+        rec = world.step_log(t, 1)[0]
+        for wi, s_ in enumerate(seeds):
+            Rs[wi], grown = oracle.regrow(wc.replace(seeds=(s_,)), t, Rs[wi])
+            assert rec[wi]["t"] == t and rec[wi]["grown"] == grown and rec[wi]["resources"] == int(Rs[wi].sum()), (t, s_)
+            assert rec[wi]["population"] == 0 and rec[wi]["births"] == 0
+    g = world.get_state(("resources",))["resources"]
+    for wi in range(3):
+        assert np.array_equal(g[wi], Rs[wi]), wi
+    snap = world.get_state()
+    other = sim.World(wc)
+    other.set_state(snap)
+    other.step(10)
+    world.step(10)
+    assert np.array_equal(other.get_state(("resources",))["resources"], world.get_state(("resources",))["resources"])
+    assert np.array_equal(other.step_log(25, 10), world.step_log(25, 10))
+    assert world.totals()["steps"] == 35
+    world.destroy()
+    other.destroy()
+
+
 # --------------------------------------------------------------- full trajectories
 def test_tiny_free_running_100_steps_bit_exact():
     """M1: the tiny config's 100 steps, free running on both sides."""
