@@ -22,7 +22,9 @@ Our arm (default):
   * e2e: the same K steps through the public API from pinned HOST buffers: sim_set_state
     (H2D of the whole state), then sim_step(K) (one call), each step's record written by the
     device into a mapped pinned host ring (sim_set_record_mirror: the D2H of the result
-    without a copy operation), wall clock, checked equal to the timed run's records;
+    without a copy operation), wall clock, checked equal to the timed run's records; the
+    sim_step(K) call alone is also bracketed by CUDA events (`one_call`: SURVEY.md D.4's
+    procedure, no per-step event pair or L2 flush);
   * whole_run_sample (when K covers only the first steps of the config's 10,000-step run,
     as the driver's --steps 20 does): 20 more single steps spread evenly over the rest of the
     run, timed the same way, the steps between them advanced untimed;
@@ -405,17 +407,21 @@ def run_ours(args, rank, world_size, local_rank):
             world.synchronize()
             torch.cuda.synchronize()
             barrier()
+            ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             te = time.perf_counter()
             world.set_state(pinned)
-            world.step(K)  # the user's call: K steps in one sim_step (two-step graphs)
+            ev_a.record(stream)
+            world.step(K)  # the user's call: K steps in one sim_step (eight-step graphs)
+            ev_b.record(stream)
             world.synchronize()
             e_s = time.perf_counter() - te
+            call_ms = allmax(ev_a.elapsed_time(ev_b))  # the one sim_step(K) call alone, on the device
             world.set_record_mirror(None)
             got = rec_host[(np.arange(t0, t0 + K) & (cap - 1))]
             assert np.array_equal(got, log), "e2e records differ from the timed run"
             e_s = allmax(e_s)
             e2e = {"value": all_agents / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
-                   "d2h_bytes_per_step": rec_bytes, "seconds": e_s}
+                   "d2h_bytes_per_step": rec_bytes, "seconds": e_s, "step_call_device_ms": call_ms}
         # -- the rest of the config's run, sampled: when K covers only the run's first steps (the
         # driver's --steps 20 times t = 5..25, ~1,000 agents in 8,192 slots), M more single
         # steps spread evenly over the remaining steps of the run are timed the same way (L2
@@ -514,6 +520,17 @@ def run_ours(args, rank, world_size, local_rank):
             result["replay_identical"] = kern["replay_identical"]
         if e2e is not None:
             result["e2e"] = e2e
+            # SURVEY.md §8(d) D.4's procedure beside the per-step one: the K steps as ONE sim_step(K)
+            # call bracketed by CUDA events (no event pair, graph-launch gap or L2 flush per step;
+            # the records still mirrored to the host), and D.3c's run-level fraction of it
+            cms = e2e["step_call_device_ms"]
+            sb_run = step_bytes(wc, agents, nnz, births)
+            result["one_call"] = {
+                "what": "the same K steps as one sim_step(K) call, CUDA events around the call (SURVEY.md D.4); "
+                        "L2 not flushed between its steps",
+                "ms_per_step": cms / K, "value": all_agents / (cms / 1e3), "unit": UNIT,
+                "step_roofline": {"bytes_per_step": sb_run / K, "achieved_GBps": sb_run / (cms / 1e3) / 1e9,
+                                  "frac": sb_run / (cms / 1e3) / 1e9 / peak}}
         if run_sample is not None:
             rs = run_sample
             result["whole_run_sample"] = {

@@ -209,8 +209,8 @@ typedef struct {
  * weights).  n_initial > number of empty cells -> SIM_E_INVALID. */
 SIM_API sim_status sim_create(const sim_config *cfg, sim_handle *out);
 /* Enqueue n >= 0 world steps on the stream, asynchronously: CUDA graphs of [policy, k_post]
- * (a two-step graph per pair of steps for n >= 2, whose second policy is a programmatic
- * dependent of the first k_post; a one-step graph for an odd remainder).  The graphs are
+ * (an eight-step graph per eight steps for n >= 8, each later policy a programmatic
+ * dependent of the k_post before it; one-step graphs for the remainder).  The graphs are
  * captured at the handle's first step and whenever a kernel parameter changes
  * (sim_set_record_mirror), never by a later sim_step.  A world without agent slots
  * (slots = 0: the regrowth grids of BASELINE configs[2]) steps with a one-block bookkeeping

@@ -210,7 +210,7 @@ struct sim_ctx {
     // preceded by a standalone regrowth (afterwards each k_post regrows the next step).
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
-    cudaGraph_t graph2 = nullptr;  // two steps, the second policy a programmatic dependent
+    cudaGraph_t graph2 = nullptr;  // ECO_GRAPH_STEPS steps, every policy after the first a programmatic dependent
     cudaGraphExec_t graph2_exec = nullptr;
     bool regrown_ahead = false;
     bool p_ready = false;  // split policy: the P rows of step t exist
@@ -405,7 +405,7 @@ cudaError_t ensure_graphs(sim_ctx *h) {
     if (h->p.n_ranks > 1) return cudaSuccess;  // sharded handles step without graphs
     cudaError_t e = cudaSuccess;
     if (!h->graph_exec) e = capture_steps(h, 1, &h->graph, &h->graph_exec);
-    if (e == cudaSuccess && two_step_graphs(h) && !h->graph2_exec) e = capture_steps(h, 2, &h->graph2, &h->graph2_exec);
+    if (e == cudaSuccess && two_step_graphs(h) && !h->graph2_exec) e = capture_steps(h, ECO_GRAPH_STEPS, &h->graph2, &h->graph2_exec);
     return e;
 }
 
@@ -791,11 +791,11 @@ sim_status sim_step(sim_handle h, int64_t n) {
     CK(h, cudaSetDevice(h->device), "cudaSetDevice");
     if (!h->bands.empty()) return band_step(h, n);
     CK(h, ensure_graphs(h), "capture step graphs");  // (captured already unless a capture failed)
-    const bool two = n >= 2 && two_step_graphs(h);
+    const bool two = n >= ECO_GRAPH_STEPS && two_step_graphs(h);
     CK(h, ensure_regrown(h), "regrow");
     int64_t i = 0;
     if (two)
-        for (; i + 2 <= n; i += 2) CK(h, cudaGraphLaunch(h->graph2_exec, h->stream), "graph launch");
+        for (; i + ECO_GRAPH_STEPS <= n; i += ECO_GRAPH_STEPS) CK(h, cudaGraphLaunch(h->graph2_exec, h->stream), "graph launch");
     for (; i < n; ++i) CK(h, cudaGraphLaunch(h->graph_exec, h->stream), "graph launch");
     h->t += n;
     return SIM_OK;
