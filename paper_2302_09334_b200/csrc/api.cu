@@ -395,7 +395,9 @@ void drop_graphs(sim_ctx *h) {  // kernel parameters changed: capture again on t
 // that sim_step only launches
 bool two_step_graphs(const sim_ctx *h) {
 #if ECO_STEP2_PDL
-    return h->p.split && h->p.n_ranks == 1;  // (the programmatic edge needs the split policy)
+    // (any unsharded handle; the programmatic edge between steps needs the split policy and is
+    // only made there, launch_policy)
+    return ECO_GRAPH_ALL ? h->p.n_ranks == 1 : (h->p.split && h->p.n_ranks == 1);
 #else
     (void)h;
     return false;

@@ -40,6 +40,9 @@
 #ifndef ECO_GRAPH_STEPS
 #define ECO_GRAPH_STEPS 8  // (measured, sim_step(10000) at paper scale: 2 -> 41.16, 4 -> 40.25, 8 -> 39.79, 16 -> 39.60 us per step) steps per graph of sim_step(n >= this): every policy after the first a programmatic dependent
 #endif
+#ifndef ECO_GRAPH_ALL
+#define ECO_GRAPH_ALL 1  // multi-step graphs for every unsharded handle (0: the split policy's only)
+#endif
 #ifndef ECO_STEP2_PDL
 #define ECO_STEP2_PDL 1
 #endif
