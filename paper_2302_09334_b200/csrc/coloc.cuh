@@ -230,6 +230,9 @@ __global__ void __launch_bounds__(CO_THREADS) k_post_co(DevParams p, unsigned lo
     __shared__ uint32_t scratch[2 * (CO_THREADS / 32 + 1)];
     __shared__ int s_free[RANK_SMEM_CAP], s_par[RANK_SMEM_CAP];
     __shared__ int s_mv[SIM_MOVE_BINS];
+#if ECO_POST_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the policy grid has completed (programmatic dependent)
+#endif
     unsigned long long target = grid_sync_base(bar);
     const int64_t T = p.t[0];  // (all worlds share t)
     const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, gthreads = (size_t)gridDim.x * blockDim.x;

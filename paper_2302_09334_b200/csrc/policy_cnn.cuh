@@ -57,6 +57,11 @@ __device__ __forceinline__ double sigmoid_d(double z) { return 1.0 / (1.0 + exp(
 constexpr int CNN_BLK_THREADS = 128;
 
 __global__ void __launch_bounds__(CNN_BLK_THREADS) k_policy_cnn_blk(DevParams p) {
+#if ECO_STEP2_PDL
+    // inside a multi-step graph the policy is a programmatic dependent of the previous step's
+    // post-policy kernel: wait for it (a no-op for an ordinary launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     extern __shared__ __align__(1024) unsigned char cnn_smem_raw[];
     __shared__ double s_z[16], s_d[8], s_ex[5];
     __shared__ unsigned s_nnz, s_seen;

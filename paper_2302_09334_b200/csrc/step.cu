@@ -1039,6 +1039,21 @@ cudaError_t policy_prepare() {
 
 cudaError_t launch_policy(const DevParams &p, const LaunchCfg &lc, cudaStream_t s, bool pdl) {
     if (p.net == 1) {
+#if ECO_STEP2_PDL
+        if (pdl && p.n_ranks == 1) {  // a programmatic dependent of the previous step's post-policy kernel
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(lc.policy_blocks);
+            cfg.blockDim = dim3(CNN_BLK_THREADS);
+            cfg.dynamicSmemBytes = CNN_BLK_SMEM;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, k_policy_cnn_blk, p);
+        }
+#endif
         k_policy_cnn_blk<<<lc.policy_blocks, CNN_BLK_THREADS, CNN_BLK_SMEM, s>>>(p);
         return cudaGetLastError();
     }
@@ -1965,11 +1980,16 @@ cudaError_t launch_post(const DevParams &p, const LaunchCfg &lc, unsigned long l
         cc.gridDim = dim3(lc.post_blocks);
         cc.blockDim = dim3(CO_THREADS);
         cc.stream = s;
-        cudaLaunchAttribute at[1];
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
         cc.attrs = at;
         cc.numAttrs = 1;
+#if ECO_POST_PDL
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // scheduled while the policy drains
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cc.numAttrs = 2;
+#endif
         return cudaLaunchKernelEx(&cc, k_post_co, p, bar);
     }
     cudaLaunchConfig_t cfg = {};
