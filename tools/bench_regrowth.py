@@ -54,6 +54,17 @@ def run_grid(H, W, steps, flush, flush_rd, stream):
             flush_rd.sum()
             kern_ms[k] = world.step_timed()["regrow"]
         log2 = world.step_log(0, steps)[:, 0]
+        # the config's run as ONE sim_step(steps) call bracketed by CUDA events (no event pair or
+        # L2 flush per step: the grid's two planes exceed the L2 from 2048x4096 up anyway)
+        world.set_state(snap)
+        world.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        world.step(steps)
+        eb.record(stream)
+        world.synchronize()
+        call_ms = ea.elapsed_time(eb)
+        log3 = world.step_log(0, steps)[:, 0]
         world.destroy()
     cells = H * W
     peak, peak_src = bench.peaks()
@@ -69,7 +80,11 @@ def run_grid(H, W, steps, flush, flush_rd, stream):
 
     return {"grid": f"{H}x{W}", "cells": cells, "steps": steps,
             "growth": part(0, min(200, steps)), "saturated": part(min(200, steps), steps), "all": part(0, steps),
-            "final_resources": int(log["resources"][-1]), "replay_identical": bool(np.array_equal(log, log2)),
+            "one_call": {"what": f"sim_step({steps}) as one call, CUDA events around it", "ms": call_ms,
+                         "step_us": call_ms / steps * 1e3, "cell_updates_per_s": steps * cells / (call_ms / 1e3),
+                         "plane_GBps": steps * cells / 4 / (call_ms / 1e3) / 1e9},
+            "final_resources": int(log["resources"][-1]),
+            "replay_identical": bool(np.array_equal(log, log2) and np.array_equal(log, log3)),
             "peak_GBps": peak, "peak_source": peak_src}
 
 
