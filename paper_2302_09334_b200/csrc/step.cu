@@ -1581,6 +1581,9 @@ __global__ void __launch_bounds__(RG_THREADS, ECO_RG_BPS) k_regrow_tiled(DevPara
     extern __shared__ __align__(1024) uint4 rg_dyn[];  // the stage ring [RG_STAGES][RG_STAGE_VECS]
     uint4 (*s_ring)[RG_STAGE_VECS] = reinterpret_cast<uint4 (*)[RG_STAGE_VECS]>(rg_dyn);
     __shared__ uint32_t s_code[2][RG_WORDS];     // listed words: 2-bit class per cell (cells 0-15, 16-31)
+#if ECO_STEP2_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // (a programmatic dependent in the agent-free step's graphs)
+#endif
     __shared__ uint32_t s_grow[RG_WORDS];        // grown bits by tile word
     __shared__ uint16_t s_need[RG_WORDS];        // listed words (tile word index)
     __shared__ uint16_t s_item[RG_WORDS * 8];    // listed groups (list index << 3 | group)
@@ -1814,6 +1817,9 @@ constexpr size_t RG_TILED_MIN_WORDS = 65536;
 // no policy launch and no k_post (which would sweep a 16.8 MB claimed-cell bitmap and run
 // five empty phases: 47 of the 94 us per step at 8192x16384).
 __global__ void __launch_bounds__(256) k_advance_empty(DevParams p) {
+#if ECO_STEP2_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous regrowth's counts are complete
+#endif
     for (int w = threadIdx.x; w < p.n_worlds; w += blockDim.x) {
         const int64_t t = p.t[w];
         housekeeping_world(p, w);
@@ -1822,8 +1828,21 @@ __global__ void __launch_bounds__(256) k_advance_empty(DevParams p) {
     }
 }
 cudaError_t launch_advance_empty(const DevParams &p, cudaStream_t s) {
+#if ECO_STEP2_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_advance_empty, p);
+#else
     k_advance_empty<<<1, 256, 0, s>>>(p);
     return cudaGetLastError();
+#endif
 }
 
 bool regrow_tiled(const DevParams &p) {
@@ -1848,6 +1867,21 @@ cudaError_t launch_regrow(const DevParams &p, int ahead, cudaStream_t s) {
             (size_t)p.n_worlds * ((p.row_hi - p.row_lo + RG_TH - 1) / RG_TH) * ((real_words + RG_TW - 1) / RG_TW);
         size_t blocks = (size_t)sms * bps;
         if (blocks > ntiles) blocks = ntiles;
+#if ECO_STEP2_PDL
+        if (p.S == 0 && p.regrow_split) {  // the agent-free step: a programmatic dependent of k_advance_empty
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)blocks);
+            cfg.blockDim = dim3(RG_THREADS);
+            cfg.dynamicSmemBytes = RG_DYN_SMEM;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, k_regrow_tiled, p, ahead);
+        }
+#endif
         k_regrow_tiled<<<(unsigned)blocks, RG_THREADS, RG_DYN_SMEM, s>>>(p, ahead);
         return cudaGetLastError();
     }
