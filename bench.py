@@ -479,6 +479,12 @@ def run_ours(args, rank, world_size, local_rank):
             "post_phase_us_per_step": post_phases,
             "clocks": clk,
         }
+        if not sharded and wc.slots > 0:  # (from the records alone: no replay needed)
+            sb = step_bytes(wc, agents, nnz, births)
+            result["step_roofline"] = {"bytes_per_step": sb / K, "achieved_GBps": sb / (max_ms / 1e3) / 1e9,
+                                       "frac": sb / (max_ms / 1e3) / 1e9 / peak,
+                                       "dense_equiv_GBps": step_bytes(wc, agents, agents * wc.n_inputs, births)
+                                       / (max_ms / 1e3) / 1e9}
         if kern is not None:
             ks = kern["kernel_ms_total"]
             sb = step_bytes(wc, agents, nnz, births)
@@ -511,10 +517,6 @@ def run_ours(args, rank, world_size, local_rank):
             dom = max(("policy", "post"), key=lambda k_: rl[k_]["launch_ms"])
             result["roofline"] = rl[dom]
             result["kernels_roofline"] = rl
-            result["step_roofline"] = {"bytes_per_step": sb / K, "achieved_GBps": sb / (max_ms / 1e3) / 1e9,
-                                       "frac": sb / (max_ms / 1e3) / 1e9 / peak,
-                                       "dense_equiv_GBps": step_bytes(wc, agents, agents * wc.n_inputs, births)
-                                       / (max_ms / 1e3) / 1e9}
             result["kernel_ms_per_step"] = {k: v / K for k, v in ks.items()}
             result["graph_kernel_ms_per_step"] = {k: v / K for k, v in kern["graph_kernel_ms_total"].items()}
             result["replay_identical"] = kern["replay_identical"]
